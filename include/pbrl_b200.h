@@ -1,0 +1,183 @@
+/* pbrl_b200 — C ABI of the B200-native population update path.
+ *
+ * Drop-in boundary for the reference's proj/core population-trainer API (namespace pbrl,
+ * a header-only C++20 template library with no FFI of its own).  Each entry point below names
+ * the reference interface it replaces.  A C++ facade with the reference's names and exception
+ * types sits on top of this ABI in include/pbrl_b200.hpp; the Python host mirror is
+ * paper_2206_08888_b200/pbrl.py.  See INTEGRATION.md for the bindings.
+ *
+ * Conventions
+ *  - Every function returns an int status: PBRL_OK or a negative code that maps 1:1 onto the
+ *    reference exception classes in errors.hpp:9-48 (ShapeError, ConfigError, UsageError,
+ *    NotReadyError, ResourceError, DataStarvationError) plus CUDA / NCCL failures.
+ *    pbrl_last_error() returns the thread-local message of the last failure.
+ *  - Host pointers are caller-owned and only read/written during the call.  Device pointers
+ *    (the *_device variants) must be valid on the population's device.
+ *  - Calls on one handle must be serialised (the reference learner-thread contract,
+ *    pipeline_run.hpp:330-355); distinct handles are independent.
+ *  - Arrays of per-member values are indexed by LOCAL member (0 .. n-1); a shard created with
+ *    member_offset = o keys its RNG streams by global id o + i (algos.hpp:210).
+ */
+#ifndef PBRL_B200_H
+#define PBRL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (errors.hpp:9-48) */
+#define PBRL_OK 0
+#define PBRL_E_SHAPE (-1)       /* ShapeError */
+#define PBRL_E_CONFIG (-2)      /* ConfigError */
+#define PBRL_E_USAGE (-3)       /* UsageError */
+#define PBRL_E_NOT_READY (-4)   /* NotReadyError */
+#define PBRL_E_RESOURCE (-5)    /* ResourceError */
+#define PBRL_E_STARVATION (-6)  /* DataStarvationError */
+#define PBRL_E_CUDA (-7)
+#define PBRL_E_NCCL (-8)
+
+#define PBRL_ALGO_TD3 0
+#define PBRL_ALGO_SAC 1
+
+/* arithmetic of the dense contractions; everything else is fp32 in every mode */
+#define PBRL_PREC_FFMA32 0 /* CUDA-core fp32, reference k-order, no FMA: bit-exact check mode */
+#define PBRL_PREC_BF16 1   /* tcgen05 kind::f16, bf16 operands, fp32 accumulate in TMEM */
+#define PBRL_PREC_TF32 2   /* tcgen05 kind::tf32, fp32 operands rounded to tf32 */
+
+/* network ids (Td3State / SacState members, algos.hpp:166-169, :475-477) */
+#define PBRL_NET_POLICY 0
+#define PBRL_NET_POLICY_TARGET 1 /* TD3 only */
+#define PBRL_NET_CRITIC1 2
+#define PBRL_NET_CRITIC2 3
+#define PBRL_NET_CRITIC1_TARGET 4
+#define PBRL_NET_CRITIC2_TARGET 5
+
+#define PBRL_REPLAY_PER_AGENT 0 /* BufferMode::kPerAgent (replay.hpp:175) */
+#define PBRL_REPLAY_SHARED 1    /* BufferMode::kShared */
+
+typedef struct pbrl_pop pbrl_pop;
+
+/* Population descriptor: the arguments of make_td3_state / make_sac_state
+ * (algos.hpp:181-184, :490-493) plus device placement and sharding. */
+typedef struct {
+  int algo;                 /* PBRL_ALGO_* */
+  uint64_t n;               /* local members on this device */
+  uint64_t obs_dim, act_dim;
+  uint32_t n_hidden;
+  const uint64_t* hidden;   /* hidden widths */
+  double action_bound;
+  uint64_t seed;            /* make_*_state seed */
+  int precision;            /* PBRL_PREC_* */
+  int device;               /* CUDA ordinal */
+  uint64_t member_offset;   /* global id of local member 0 (0 unless sharded) */
+  uint64_t n_global;        /* population size across shards (0 = n) */
+} pbrl_pop_desc;
+
+/* One population batch (TransitionBatch, algos.hpp:14-24): s [n][B][obs], a [n][B][act],
+ * r [n][B], s2 [n][B][obs], done [n][B]. */
+typedef struct {
+  const float* s;
+  const float* a;
+  const float* r;
+  const float* s2;
+  const float* done;
+} pbrl_batch;
+
+/* ---- lifecycle: make_td3_state / make_sac_state (algos.hpp:181-212, :490-521) */
+int pbrl_pop_create(const pbrl_pop_desc* desc, pbrl_pop** out);
+int pbrl_pop_destroy(pbrl_pop* pop);
+int pbrl_last_error(char* buf, size_t len);
+int pbrl_version(int* major, int* minor);
+
+/* ---- hyperparameters: Td3Hyper / SacHyper per-member vectors (algos.hpp:32-156).
+ * TD3 fields: critic_lr policy_lr policy_delay_ratio explore_std target_std target_clip gamma tau
+ * SAC fields: policy_lr critic_lr alpha_lr target_entropy reward_scale gamma tau
+ * pbrl_set_hyper validates like Td3Hyper::validate (algos.hpp:81-108) -> PBRL_E_CONFIG. */
+int pbrl_set_hyper(pbrl_pop* pop, const char* field, const double* per_member);
+int pbrl_get_hyper(pbrl_pop* pop, const char* field, double* per_member);
+
+/* ---- parameters in flatten_member layout (net_pop.hpp:162-202) */
+int pbrl_param_count(pbrl_pop* pop, int net, uint64_t* count);
+int pbrl_get_member(pbrl_pop* pop, int net, uint64_t member, float* flat);
+int pbrl_set_member(pbrl_pop* pop, int net, uint64_t member, const float* flat);
+/* copy_member (net_pop.hpp:192-202) for one network, on device */
+int pbrl_copy_member(pbrl_pop* pop, int net, uint64_t src, uint64_t dst);
+/* Adam moments of one member in flatten order + its step count (pop_tensor.hpp:299-323);
+ * net = PBRL_NET_POLICY / CRITIC1 / CRITIC2 */
+int pbrl_get_adam(pbrl_pop* pop, int net, uint64_t member, float* m, float* v, int64_t* t);
+/* TD3: delay_acc + steps (algos.hpp:170-171).  SAC: delay_acc unused (may be NULL). */
+int pbrl_get_counters(pbrl_pop* pop, double* delay_acc, uint64_t* steps);
+/* SAC temperature state: log_alpha, its Adam m, v, t (algos.hpp:478-479) */
+int pbrl_get_alpha(pbrl_pop* pop, float* log_alpha, float* m, float* v, int64_t* t);
+
+/* ---- update: td3_update_step / sac_update_step (algos.hpp:351-422, :781-837) chained k
+ * times as in update_k_steps (algos.hpp:953-983).  batches: k host batches of B rows;
+ * policy_mask (TD3 only, may be NULL): [n] bytes, policy_member_mask of td3_update_step. */
+int pbrl_update_batches(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k, uint64_t batch_rows,
+                        const uint8_t* policy_mask);
+/* Same with device-resident batches (pointers valid on the population's device). */
+int pbrl_update_batches_device(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k,
+                               uint64_t batch_rows, const uint8_t* policy_mask);
+/* update_k_steps fed by the device replay: per step i, sample_batch(..., draw_id = first+i)
+ * (replay.hpp:181-204) then one update.  *ready = 0 (and nothing runs) when a source buffer
+ * holds fewer than max(min_size, 1) transitions (sample_batch's nullopt). */
+int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t sample_seed, uint64_t first_draw_id,
+                  uint64_t batch_rows, uint64_t min_size, int* ready);
+/* Per-member losses of the LAST step: critic1 / critic2 MSE (mse_loss_grads, algos.hpp:288-314)
+ * and the policy loss (td3_policy_loss_grads :318-338 / sac_policy_loss_grads :643-735);
+ * each [n] (TD3 policy entries are 0 for members that did not fire). */
+int pbrl_last_losses(pbrl_pop* pop, double* critic1, double* critic2, double* policy);
+
+/* ---- replay: ReplayBuffer (replay.hpp:28-173) held in HBM, one ring per member (per-agent) or
+ * one shared ring.  Insert is the batched equivalent of push (:56-69). */
+int pbrl_replay_create(pbrl_pop* pop, uint64_t capacity, int mode);
+int pbrl_replay_insert(pbrl_pop* pop, const float* s, const float* a, const float* r,
+                       const float* s2, const float* done, const uint32_t* member, uint64_t count);
+int pbrl_replay_size(pbrl_pop* pop, uint64_t buffer, uint64_t* size);
+/* sample_batch (replay.hpp:181-204) into host arrays shaped like pbrl_batch; *ready as above */
+int pbrl_sample_batch(pbrl_pop* pop, uint64_t sample_seed, uint64_t draw_id, uint64_t batch_rows,
+                      uint64_t min_size, float* s, float* a, float* r, float* s2, float* done,
+                      int* ready);
+
+/* ---- PBT exploit/explore (evolve.hpp:112-213).
+ * pbrl_pbt_plan: ranks fitness (mean of each member's return ring, evolve.hpp:104-122) and draws
+ * donors on device; fitness is [n_total] means over the WHOLE population (all shards).
+ * rng_key/rng_next = the RngSequence (rng.hpp:74-95); *rng_next advances by the plan size.
+ * replaced/donors receive global ids; *count = ceil(trunc * n_total) (0 when n_total < 4). */
+int pbrl_pbt_plan(pbrl_pop* pop, const double* fitness, uint64_t n_total, double trunc,
+                  uint64_t rng_key, uint64_t* rng_next, uint64_t* replaced, uint64_t* donors,
+                  uint32_t* count);
+/* Applies a plan to the local shard: copy every network of donor -> replaced (both local),
+ * reset the replaced member's optimiser state (and TD3 delay_acc).  Pairs whose donor or
+ * receiver is not local are skipped (the caller moves them with pbrl_export/import_member). */
+int pbrl_pbt_apply(pbrl_pop* pop, const uint64_t* replaced, const uint64_t* donors, uint32_t count);
+/* Full pbt_evolve_trainer for a single-shard population: plan + apply + hyper re-draw
+ * (Td3Prior / SacPrior, evolve.hpp:31-73); returns the plan and updates the hypers. */
+int pbrl_pbt_evolve(pbrl_pop* pop, const double* fitness, uint64_t rng_key, uint64_t* rng_next,
+                    uint64_t* replaced, uint64_t* donors, uint32_t* count);
+/* Member state blob for cross-device exploit copies: every network of one local member,
+ * concatenated in net-id order (plus log_alpha for SAC).  dev_buf is a device pointer. */
+int pbrl_member_blob_size(pbrl_pop* pop, uint64_t* floats);
+int pbrl_export_member(pbrl_pop* pop, uint64_t member, float* dev_buf);
+int pbrl_import_member(pbrl_pop* pop, uint64_t member, const float* dev_buf);
+
+/* ---- synthetic inputs: make_synthetic_batches (bench.hpp:69-93) generated on the device.
+ * out: count device batches; each field is a device pointer to [count][n][b][dim] floats laid out
+ * contiguously (out->s holds all count batches).  pop may be NULL (current device). */
+int pbrl_synthetic_batches_device(pbrl_pop* pop, uint64_t count, uint64_t n, uint64_t b,
+                                  uint64_t obs_dim, uint64_t act_dim, uint64_t seed,
+                                  const pbrl_batch* out);
+
+/* ---- observability */
+int pbrl_launch_count(pbrl_pop* pop, uint64_t* launches); /* kernels launched (cf. kernel_invocations, pop_tensor.hpp:21-28) */
+int pbrl_synchronize(pbrl_pop* pop);
+/* Bytes of fp32 state this population keeps in HBM (params, targets, moments, replay). */
+int pbrl_device_bytes(pbrl_pop* pop, uint64_t* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

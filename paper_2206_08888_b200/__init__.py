@@ -1,0 +1,15 @@
+"""B200-native population-vectorized off-policy update path (TD3 / SAC + replay + PBT).
+
+The compute lives in libpbrl_b200.so (hand-written sm_100a CUDA behind the C ABI in
+include/pbrl_b200.h); this package is the host mirror of the reference pbrl API.
+"""
+from .errors import (ConfigError, CudaError, DataStarvationError, NcclError, NotReadyError,
+                     PbrlError, ResourceError, ShapeError, UsageError)
+from .pbrl import (NETS, PBTState, RngSequence, RngStream, SacHyper, SacPrior, SacState, Td3Hyper,
+                   Td3Prior, Td3State, Transition, TransitionBatch, DeviceReplay, EvolvePlan,
+                   HyperRange, make_sac_state, make_synthetic_batches, make_td3_state, mix64,
+                   pbt_apply_returns_reset, pbt_evolve_trainer, pbt_plan, pbt_rank,
+                   sac_update_step, sample_batch, td3_update_step, update_k_steps,
+                   update_k_from_replay)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

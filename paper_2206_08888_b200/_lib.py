@@ -1,0 +1,104 @@
+"""ctypes binding of the C ABI in include/pbrl_b200.h (libpbrl_b200.so, built in-tree).
+
+There is no fallback: if the CUDA library is missing or fails to load, importing the
+population API raises.  This is the binding a reference-side maintainer would add (see
+INTEGRATION.md); the rest of the package only uses the symbols declared here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import raise_for
+
+LIB_PATH = Path(__file__).resolve().parent / "libpbrl_b200.so"
+
+u64 = C.c_uint64
+u32 = C.c_uint32
+i64 = C.c_int64
+dbl = C.c_double
+f32p = C.POINTER(C.c_float)
+f64p = C.POINTER(C.c_double)
+u64p = C.POINTER(C.c_uint64)
+u32p = C.POINTER(C.c_uint32)
+u8p = C.POINTER(C.c_uint8)
+i64p = C.POINTER(C.c_int64)
+intp = C.POINTER(C.c_int)
+vp = C.c_void_p
+
+
+class PopDesc(C.Structure):
+    _fields_ = [("algo", C.c_int), ("n", u64), ("obs_dim", u64), ("act_dim", u64),
+                ("n_hidden", u32), ("hidden", u64p), ("action_bound", dbl), ("seed", u64),
+                ("precision", C.c_int), ("device", C.c_int), ("member_offset", u64),
+                ("n_global", u64)]
+
+
+class Batch(C.Structure):
+    _fields_ = [("s", vp), ("a", vp), ("r", vp), ("s2", vp), ("done", vp)]
+
+
+# name -> (restype, argtypes); every function returns an int status
+SIGNATURES = {
+    "pbrl_pop_create": [C.POINTER(PopDesc), C.POINTER(vp)],
+    "pbrl_pop_destroy": [vp],
+    "pbrl_last_error": [C.c_char_p, C.c_size_t],
+    "pbrl_version": [intp, intp],
+    "pbrl_set_hyper": [vp, C.c_char_p, f64p],
+    "pbrl_get_hyper": [vp, C.c_char_p, f64p],
+    "pbrl_param_count": [vp, C.c_int, u64p],
+    "pbrl_get_member": [vp, C.c_int, u64, f32p],
+    "pbrl_set_member": [vp, C.c_int, u64, f32p],
+    "pbrl_copy_member": [vp, C.c_int, u64, u64],
+    "pbrl_get_adam": [vp, C.c_int, u64, f32p, f32p, i64p],
+    "pbrl_get_counters": [vp, f64p, u64p],
+    "pbrl_get_alpha": [vp, f32p, f32p, f32p, i64p],
+    "pbrl_update_batches": [vp, C.POINTER(Batch), u32, u64, u8p],
+    "pbrl_update_batches_device": [vp, C.POINTER(Batch), u32, u64, u8p],
+    "pbrl_update_k": [vp, u32, u64, u64, u64, u64, intp],
+    "pbrl_last_losses": [vp, f64p, f64p, f64p],
+    "pbrl_replay_create": [vp, u64, C.c_int],
+    "pbrl_replay_insert": [vp, f32p, f32p, f32p, f32p, f32p, u32p, u64],
+    "pbrl_replay_size": [vp, u64, u64p],
+    "pbrl_sample_batch": [vp, u64, u64, u64, u64, f32p, f32p, f32p, f32p, f32p, intp],
+    "pbrl_pbt_plan": [vp, f64p, u64, dbl, u64, u64p, u64p, u64p, u32p],
+    "pbrl_pbt_apply": [vp, u64p, u64p, u32],
+    "pbrl_pbt_evolve": [vp, f64p, u64, u64p, u64p, u64p, u32p],
+    "pbrl_member_blob_size": [vp, u64p],
+    "pbrl_export_member": [vp, u64, vp],
+    "pbrl_import_member": [vp, u64, vp],
+    "pbrl_launch_count": [vp, u64p],
+    "pbrl_synchronize": [vp],
+    "pbrl_device_bytes": [vp, u64p],
+    "pbrl_synthetic_batches_device": [vp, u64, u64, u64, u64, u64, u64, C.POINTER(Batch)],
+}
+
+_lib = None
+
+
+def lib():
+    """Load libpbrl_b200.so once; raises if the CUDA extension is absent (no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() or "
+                              f"`make -C paper_2206_08888_b200`")
+        L = C.CDLL(str(LIB_PATH))
+        for name, args in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = C.c_int
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    buf = C.create_string_buffer(4096)
+    lib().pbrl_last_error(buf, len(buf))
+    return buf.value.decode(errors="replace")
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        raise_for(rc, f"{name}: {last_error()}")

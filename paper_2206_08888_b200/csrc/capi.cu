@@ -1,0 +1,628 @@
+// extern "C" boundary (include/pbrl_b200.h): error mapping, member access, replay, PBT.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+
+#include "pop_impl.cuh"
+
+namespace pbrl {
+
+std::atomic<uint64_t> g_launches{0};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PBRL_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_last_error = e.what();
+    return PBRL_E_RESOURCE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PBRL_E_USAGE;
+  }
+}
+
+Pop* P(pbrl_pop* h) {
+  if (!h) PBRL_THROW(PBRL_E_USAGE, "null population handle");
+  Pop* p = reinterpret_cast<Pop*>(h);
+  CUDA_CHECK(cudaSetDevice(p->device));
+  return p;
+}
+
+void check_member(const Pop* p, uint64_t m, const char* what) {
+  if (m >= static_cast<uint64_t>(p->n)) PBRL_THROW(PBRL_E_USAGE, std::string(what) + ": index out of range");
+}
+
+// RngSequence (rng.hpp:74-95) on the host, used for the PBT hyper re-draws so they match the
+// reference's glibc exp/log bit for bit.
+struct Seq {
+  uint64_t key, next;
+  double uniform(double lo, double hi) {
+    const double u = static_cast<double>(rng_bits(key, next++) >> 11) * 0x1.0p-53;
+    return lo + (hi - lo) * u;
+  }
+  double log_uniform(double lo, double hi) { return std::exp(uniform(std::log(lo), std::log(hi))); }
+};
+
+// Td3Prior / SacPrior::sample_member (evolve.hpp:31-73): the sampled fields, then the untuned
+// fields reset to their defaults (set_member copies the whole one-member hyper).
+void prior_sample(Pop* p, Seq& rng, uint64_t m) {
+  auto& h = p->hyper;
+  if (p->algo == PBRL_ALGO_TD3) {
+    h[0][m] = rng.log_uniform(3e-5, 3e-3);
+    h[1][m] = rng.log_uniform(3e-5, 3e-3);
+    h[2][m] = rng.uniform(0.2, 1.0);
+    h[3][m] = rng.uniform(0.0, 1.0);
+    h[4][m] = rng.uniform(0.0, 1.0);
+    h[6][m] = rng.uniform(0.9, 1.0);
+    h[5][m] = 0.5;
+    h[7][m] = 0.005;
+  } else {
+    h[0][m] = rng.log_uniform(3e-5, 3e-3);
+    h[1][m] = rng.log_uniform(3e-5, 3e-3);
+    h[2][m] = rng.log_uniform(3e-5, 3e-3);
+    h[3][m] = rng.uniform(0.2, 2.0) * -1.0;  // SacPrior::default_target_entropy = -1
+    h[4][m] = rng.uniform(0.1, 10.0);
+    h[5][m] = rng.uniform(0.9, 1.0);
+    h[6][m] = 0.005;
+  }
+}
+}  // namespace
+
+float* Pop::net_row(int net, uint64_t member) {
+  switch (net) {
+    case PBRL_NET_POLICY: return pol_p.p + member * pol.stride;
+    case PBRL_NET_POLICY_TARGET:
+      if (algo != PBRL_ALGO_TD3) PBRL_THROW(PBRL_E_USAGE, "SAC has no policy target");
+      return pol_t.p + member * pol.stride;
+    case PBRL_NET_CRITIC1: return cri_p.p + member * cri.stride;
+    case PBRL_NET_CRITIC2: return cri_p.p + (n + member) * cri.stride;
+    case PBRL_NET_CRITIC1_TARGET: return cri_t.p + member * cri.stride;
+    case PBRL_NET_CRITIC2_TARGET: return cri_t.p + (n + member) * cri.stride;
+    default: PBRL_THROW(PBRL_E_USAGE, "unknown network id");
+  }
+}
+
+const NetShape& Pop::net_shape(int net) const {
+  return (net == PBRL_NET_POLICY || net == PBRL_NET_POLICY_TARGET) ? pol : cri;
+}
+
+}  // namespace pbrl
+
+using namespace pbrl;
+
+extern "C" {
+
+int pbrl_version(int* major, int* minor) {
+  if (major) *major = 0;
+  if (minor) *minor = 1;
+  return PBRL_OK;
+}
+
+int pbrl_last_error(char* buf, size_t len) {
+  if (!buf || len == 0) return PBRL_E_USAGE;
+  std::strncpy(buf, g_last_error.c_str(), len - 1);
+  buf[len - 1] = '\0';
+  return PBRL_OK;
+}
+
+int pbrl_pop_create(const pbrl_pop_desc* desc, pbrl_pop** out) {
+  return guarded([&] {
+    if (!desc || !out) PBRL_THROW(PBRL_E_USAGE, "null argument");
+    *out = reinterpret_cast<pbrl_pop*>(new Pop(*desc));
+  });
+}
+
+int pbrl_pop_destroy(pbrl_pop* pop) {
+  return guarded([&] {
+    Pop* p = reinterpret_cast<Pop*>(pop);
+    if (!p) return;
+    cudaSetDevice(p->device);
+    delete p->replay;
+    delete p;
+  });
+}
+
+int pbrl_set_hyper(pbrl_pop* pop, const char* field, const double* v) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    const int f = p->field_index(field ? field : "");
+    if (f < 0) PBRL_THROW(PBRL_E_CONFIG, std::string("unknown hyperparameter ") + (field ? field : ""));
+    auto saved = p->hyper[f];
+    p->hyper[f].assign(v, v + p->n);
+    try {
+      p->validate_hyper();
+    } catch (...) {
+      p->hyper[f] = saved;
+      throw;
+    }
+    p->upload_hyper();
+  });
+}
+
+int pbrl_get_hyper(pbrl_pop* pop, const char* field, double* v) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    const int f = p->field_index(field ? field : "");
+    if (f < 0) PBRL_THROW(PBRL_E_CONFIG, std::string("unknown hyperparameter ") + (field ? field : ""));
+    std::memcpy(v, p->hyper[f].data(), sizeof(double) * p->n);
+  });
+}
+
+int pbrl_param_count(pbrl_pop* pop, int net, uint64_t* count) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    p->net_row(net, 0);
+    *count = p->net_shape(net).P;
+  });
+}
+
+int pbrl_get_member(pbrl_pop* pop, int net, uint64_t member, float* flat) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    check_member(p, member, "flatten_member");
+    const float* src = p->net_row(net, member);
+    CUDA_CHECK(cudaMemcpyAsync(flat, src, p->net_shape(net).P * 4, cudaMemcpyDeviceToHost,
+                               p->stream));
+    p->sync();
+  });
+}
+
+int pbrl_set_member(pbrl_pop* pop, int net, uint64_t member, const float* flat) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    check_member(p, member, "unflatten_member");
+    float* dst = p->net_row(net, member);
+    CUDA_CHECK(cudaMemcpyAsync(dst, flat, p->net_shape(net).P * 4, cudaMemcpyHostToDevice,
+                               p->stream));
+    p->sync();
+  });
+}
+
+int pbrl_copy_member(pbrl_pop* pop, int net, uint64_t src, uint64_t dst) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    if (src >= static_cast<uint64_t>(p->n) || dst >= static_cast<uint64_t>(p->n))
+      PBRL_THROW(PBRL_E_USAGE, "copy_member: index out of range");
+    if (src == dst) return;
+    CUDA_CHECK(cudaMemcpyAsync(p->net_row(net, dst), p->net_row(net, src),
+                               p->net_shape(net).P * 4, cudaMemcpyDeviceToDevice, p->stream));
+    p->sync();
+  });
+}
+
+int pbrl_get_adam(pbrl_pop* pop, int net, uint64_t member, float* m, float* v, int64_t* t) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    check_member(p, member, "get_adam");
+    const float *pm, *pv;
+    const int64_t* pt;
+    size_t P_;
+    if (net == PBRL_NET_POLICY) {
+      pm = p->pol_m.p + member * p->pol.stride;
+      pv = p->pol_v.p + member * p->pol.stride;
+      pt = p->t_pol.p + member;
+      P_ = p->pol.P;
+    } else if (net == PBRL_NET_CRITIC1 || net == PBRL_NET_CRITIC2) {
+      const uint64_t row = (net == PBRL_NET_CRITIC1 ? 0 : p->n) + member;
+      pm = p->cri_m.p + row * p->cri.stride;
+      pv = p->cri_v.p + row * p->cri.stride;
+      pt = p->t_cri.p + row;
+      P_ = p->cri.P;
+    } else {
+      PBRL_THROW(PBRL_E_USAGE, "get_adam: network has no optimiser state");
+    }
+    if (m) CUDA_CHECK(cudaMemcpyAsync(m, pm, P_ * 4, cudaMemcpyDeviceToHost, p->stream));
+    if (v) CUDA_CHECK(cudaMemcpyAsync(v, pv, P_ * 4, cudaMemcpyDeviceToHost, p->stream));
+    if (t) CUDA_CHECK(cudaMemcpyAsync(t, pt, 8, cudaMemcpyDeviceToHost, p->stream));
+    p->sync();
+  });
+}
+
+int pbrl_get_counters(pbrl_pop* pop, double* delay_acc, uint64_t* steps) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    if (delay_acc)
+      CUDA_CHECK(cudaMemcpyAsync(delay_acc, p->delay_acc.p, 8 * p->n, cudaMemcpyDeviceToHost,
+                                 p->stream));
+    if (steps)
+      CUDA_CHECK(cudaMemcpyAsync(steps, p->steps.p, 8 * p->n, cudaMemcpyDeviceToHost, p->stream));
+    p->sync();
+  });
+}
+
+int pbrl_get_alpha(pbrl_pop* pop, float* log_alpha, float* m, float* v, int64_t* t) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    if (p->algo != PBRL_ALGO_SAC) PBRL_THROW(PBRL_E_USAGE, "temperature state is SAC-only");
+    const size_t n = p->n;
+    if (log_alpha)
+      CUDA_CHECK(cudaMemcpyAsync(log_alpha, p->log_alpha.p, 4 * n, cudaMemcpyDeviceToHost, p->stream));
+    if (m) CUDA_CHECK(cudaMemcpyAsync(m, p->alpha_m.p, 4 * n, cudaMemcpyDeviceToHost, p->stream));
+    if (v) CUDA_CHECK(cudaMemcpyAsync(v, p->alpha_v.p, 4 * n, cudaMemcpyDeviceToHost, p->stream));
+    if (t) CUDA_CHECK(cudaMemcpyAsync(t, p->t_alpha.p, 8 * n, cudaMemcpyDeviceToHost, p->stream));
+    p->sync();
+  });
+}
+
+int pbrl_update_batches(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k, uint64_t rows,
+                        const uint8_t* policy_mask) {
+  return guarded([&] { P(pop)->update_batches(batches, k, rows, policy_mask, false); });
+}
+
+int pbrl_update_batches_device(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k,
+                               uint64_t rows, const uint8_t* policy_mask) {
+  return guarded([&] { P(pop)->update_batches(batches, k, rows, policy_mask, true); });
+}
+
+int pbrl_last_losses(pbrl_pop* pop, double* c1, double* c2, double* pl) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    const size_t n = p->n;
+    if (c1) CUDA_CHECK(cudaMemcpyAsync(c1, p->losses.p, 8 * n, cudaMemcpyDeviceToHost, p->stream));
+    if (c2) CUDA_CHECK(cudaMemcpyAsync(c2, p->losses.p + n, 8 * n, cudaMemcpyDeviceToHost, p->stream));
+    if (pl) CUDA_CHECK(cudaMemcpyAsync(pl, p->losses.p + 2 * n, 8 * n, cudaMemcpyDeviceToHost, p->stream));
+    p->sync();
+  });
+}
+
+// ---------------------------------------------------------------- replay
+int pbrl_replay_create(pbrl_pop* pop, uint64_t capacity, int mode) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    if (capacity < 1) PBRL_THROW(PBRL_E_CONFIG, "ReplayBuffer: capacity must be >= 1");
+    if (mode != PBRL_REPLAY_PER_AGENT && mode != PBRL_REPLAY_SHARED)
+      PBRL_THROW(PBRL_E_CONFIG, "unknown buffer mode");
+    auto* r = new Replay();
+    r->mode = mode;
+    r->cap = capacity;
+    r->nbuf = mode == PBRL_REPLAY_PER_AGENT ? p->n : 1;
+    r->rw = (2 * p->ds + p->da + 2 + 3) / 4 * 4;
+    try {
+      r->ring.alloc(static_cast<size_t>(r->nbuf) * capacity * r->rw);
+      r->sizes.alloc(r->nbuf);
+      r->sizes.zero(p->stream);
+      r->ring.zero(p->stream);
+    } catch (...) {
+      delete r;
+      throw;
+    }
+    r->inserts.assign(r->nbuf, 0);
+    delete p->replay;
+    p->replay = r;
+    p->sync();
+  });
+}
+
+int pbrl_replay_insert(pbrl_pop* pop, const float* s, const float* a, const float* r_,
+                       const float* s2, const float* d, const uint32_t* member, uint64_t count) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    Replay* r = p->replay;
+    if (!r) PBRL_THROW(PBRL_E_USAGE, "replay buffer not created");
+    if (count == 0) return;
+    const int ds = p->ds, da = p->da, rw = r->rw;
+    // ReplayBuffer::push order (replay.hpp:56-69): slot = inserts % cap, later pushes win
+    std::vector<uint64_t> dst(count);
+    for (uint64_t i = 0; i < count; ++i) {
+      const uint64_t buf = r->mode == PBRL_REPLAY_PER_AGENT ? member[i] : 0;
+      if (buf >= static_cast<uint64_t>(r->nbuf))
+        PBRL_THROW(PBRL_E_USAGE, "replay insert: member id out of range");
+      dst[i] = buf * r->cap + (r->inserts[buf] % r->cap);
+      r->inserts[buf]++;
+    }
+    std::unordered_map<uint64_t, uint64_t> last;
+    last.reserve(count * 2);
+    for (uint64_t i = 0; i < count; ++i) last[dst[i]] = i;
+    std::vector<float> rows;
+    std::vector<uint64_t> rdst;
+    rows.reserve(last.size() * rw);
+    for (uint64_t i = 0; i < count; ++i) {
+      if (last[dst[i]] != i) continue;
+      const size_t o = rows.size();
+      rows.resize(o + rw, 0.0f);
+      std::memcpy(&rows[o], s + i * ds, 4 * ds);
+      std::memcpy(&rows[o + ds], a + i * da, 4 * da);
+      std::memcpy(&rows[o + ds + da], s2 + i * ds, 4 * ds);
+      rows[o + 2 * ds + da] = r_[i];
+      rows[o + 2 * ds + da + 1] = d[i];
+      rdst.push_back(dst[i]);
+    }
+    r->stage_rows.alloc(rows.size());
+    r->stage_dst.alloc(rdst.size());
+    r->stage_rows.upload(rows.data(), rows.size(), p->stream);
+    r->stage_dst.upload(rdst.data(), rdst.size(), p->stream);
+    launch_replay_scatter(r->stage_rows.p, r->stage_dst.p, rdst.size(), rw, r->ring.p, p->stream);
+    p->count_launch(1);
+    std::vector<uint64_t> sz(r->nbuf);
+    for (int b = 0; b < r->nbuf; ++b) sz[b] = std::min<uint64_t>(r->inserts[b], r->cap);
+    r->sizes.upload(sz.data(), r->nbuf, p->stream);
+    p->sync();
+  });
+}
+
+int pbrl_replay_size(pbrl_pop* pop, uint64_t buffer, uint64_t* size) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    Replay* r = p->replay;
+    if (!r) PBRL_THROW(PBRL_E_USAGE, "replay buffer not created");
+    if (buffer >= static_cast<uint64_t>(r->nbuf)) PBRL_THROW(PBRL_E_USAGE, "buffer index out of range");
+    *size = std::min<uint64_t>(r->inserts[buffer], r->cap);
+  });
+}
+
+namespace {
+bool replay_ready(Pop* p, uint64_t min_size) {
+  Replay* r = p->replay;
+  if (!r) PBRL_THROW(PBRL_E_USAGE, "replay buffer not created");
+  const uint64_t need = std::max<uint64_t>(min_size, 1);
+  for (int b = 0; b < r->nbuf; ++b)
+    if (std::min<uint64_t>(r->inserts[b], r->cap) < need) return false;
+  return true;
+}
+
+void gather(Pop* p, int B, uint64_t seed, uint64_t draw_id) {
+  Replay* r = p->replay;
+  launch_replay_gather(p->n, B, p->ds, p->da, r->rw, r->ring.p, r->cap,
+                       r->mode == PBRL_REPLAY_SHARED, r->sizes.p, p->streams.p, seed, draw_id,
+                       p->S.in_sa.p, p->S.in_s2a.p, p->S.sa_pi.p, p->S.r.p, p->S.d.p, p->stream);
+  p->count_launch(1);
+}
+}  // namespace
+
+int pbrl_sample_batch(pbrl_pop* pop, uint64_t seed, uint64_t draw_id, uint64_t rows,
+                      uint64_t min_size, float* s, float* a, float* r_, float* s2, float* d,
+                      int* ready) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    *ready = 0;
+    if (!replay_ready(p, min_size)) return;
+    const int B = static_cast<int>(rows);
+    p->ensure_scratch(B);
+    gather(p, B, seed, draw_id);
+    const size_t nb = static_cast<size_t>(p->n) * B;
+    const int dsa = p->ds + p->da;
+    std::vector<float> sa(nb * dsa), s2a(nb * dsa);
+    CUDA_CHECK(cudaMemcpyAsync(sa.data(), p->S.in_sa.p, 4 * nb * dsa, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_CHECK(cudaMemcpyAsync(s2a.data(), p->S.in_s2a.p, 4 * nb * dsa, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_CHECK(cudaMemcpyAsync(r_, p->S.r.p, 4 * nb, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_CHECK(cudaMemcpyAsync(d, p->S.d.p, 4 * nb, cudaMemcpyDeviceToHost, p->stream));
+    p->sync();
+    for (size_t i = 0; i < nb; ++i) {
+      std::memcpy(s + i * p->ds, &sa[i * dsa], 4 * p->ds);
+      std::memcpy(a + i * p->da, &sa[i * dsa + p->ds], 4 * p->da);
+      std::memcpy(s2 + i * p->ds, &s2a[i * dsa], 4 * p->ds);
+    }
+    *ready = 1;
+  });
+}
+
+int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t seed, uint64_t first_draw_id,
+                  uint64_t rows, uint64_t min_size, int* ready) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    *ready = 0;
+    if (k < 1) PBRL_THROW(PBRL_E_CONFIG, "update_k_steps: k must be >= 1");
+    if (!replay_ready(p, min_size)) return;
+    p->validate_hyper();
+    const int B = static_cast<int>(rows);
+    p->ensure_scratch(B);
+    p->ensure_corr(p->t_bound + k + 4);
+    for (uint32_t i = 0; i < k; ++i) {
+      gather(p, B, seed, first_draw_id + i);
+      p->step(B, nullptr);
+    }
+    CUDA_CHECK(cudaGetLastError());
+    *ready = 1;
+  });
+}
+
+// ---------------------------------------------------------------- PBT
+int pbrl_pbt_plan(pbrl_pop* pop, const double* fitness, uint64_t n_total, double trunc,
+                  uint64_t rng_key, uint64_t* rng_next, uint64_t* replaced, uint64_t* donors,
+                  uint32_t* count) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    *count = 0;
+    if (n_total < 4) return;  // pbt_plan: populations smaller than 4 are left alone
+    const int cut = static_cast<int>(std::ceil(trunc * static_cast<double>(n_total)));
+    p->pbt_fit.alloc(n_total);
+    p->pbt_order.alloc(n_total);
+    p->pbt_rep.alloc(n_total);
+    p->pbt_don.alloc(n_total);
+    p->pbt_fit.upload(fitness, n_total, p->stream);
+    launch_pbt_plan(static_cast<int>(n_total), p->pbt_fit.p, cut, rng_key, *rng_next,
+                    p->pbt_order.p, p->pbt_rep.p, p->pbt_don.p, p->stream);
+    p->count_launch(1);
+    CUDA_CHECK(cudaMemcpyAsync(replaced, p->pbt_rep.p, 8 * cut, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_CHECK(cudaMemcpyAsync(donors, p->pbt_don.p, 8 * cut, cudaMemcpyDeviceToHost, p->stream));
+    p->sync();
+    *rng_next += static_cast<uint64_t>(cut);
+    *count = static_cast<uint32_t>(cut);
+  });
+}
+
+int pbrl_pbt_apply(pbrl_pop* pop, const uint64_t* replaced, const uint64_t* donors,
+                   uint32_t count) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    const uint64_t lo = p->member_offset, hi = lo + p->n;
+    std::vector<uint64_t> src, dst, reset;
+    for (uint32_t i = 0; i < count; ++i) {
+      const bool dl = replaced[i] >= lo && replaced[i] < hi;
+      const bool sl = donors[i] >= lo && donors[i] < hi;
+      if (dl) reset.push_back(replaced[i] - lo);
+      if (dl && sl) {
+        dst.push_back(replaced[i] - lo);
+        src.push_back(donors[i] - lo);
+      }
+    }
+    // pairs are applied in plan order (evolve.hpp:174-187); donors and receivers are disjoint
+    // strata, so one grouped copy per arena is equivalent to the sequential loop.
+    const int np = static_cast<int>(src.size());
+    if (np) {
+      p->pbt_src.alloc(np);
+      p->pbt_dst.alloc(np);
+      p->pbt_src.upload(src.data(), np, p->stream);
+      p->pbt_dst.upload(dst.data(), np, p->stream);
+      launch_member_copy(p->pol_p.p, p->pol.stride, p->pol.P, p->pbt_src.p, p->pbt_dst.p, np, p->stream);
+      if (p->algo == PBRL_ALGO_TD3)
+        launch_member_copy(p->pol_t.p, p->pol.stride, p->pol.P, p->pbt_src.p, p->pbt_dst.p, np, p->stream);
+      for (float* arena : {p->cri_p.p, p->cri_t.p}) {
+        for (int c = 0; c < 2; ++c) {
+          launch_member_copy(arena + static_cast<size_t>(c) * p->n * p->cri.stride, p->cri.stride,
+                             p->cri.P, p->pbt_src.p, p->pbt_dst.p, np, p->stream);
+        }
+      }
+      if (p->algo == PBRL_ALGO_SAC) {
+        for (int i = 0; i < np; ++i)
+          CUDA_CHECK(cudaMemcpyAsync(p->log_alpha.p + dst[i], p->log_alpha.p + src[i], 4,
+                                     cudaMemcpyDeviceToDevice, p->stream));
+      }
+      p->count_launch(p->algo == PBRL_ALGO_TD3 ? 6 : 5);
+    }
+    // MlpAdam::reset_member (optim.hpp:32-35), delay_acc = 0 (evolve.hpp:185)
+    const int nr = static_cast<int>(reset.size());
+    if (nr) {
+      p->pbt_dst.alloc(std::max(np, nr));
+      p->pbt_dst.upload(reset.data(), nr, p->stream);
+      launch_member_zero(p->pol_m.p, p->pol.stride, p->pbt_dst.p, nr, p->stream);
+      launch_member_zero(p->pol_v.p, p->pol.stride, p->pbt_dst.p, nr, p->stream);
+      for (float* arena : {p->cri_m.p, p->cri_v.p}) {
+        for (int c = 0; c < 2; ++c)
+          launch_member_zero(arena + static_cast<size_t>(c) * p->n * p->cri.stride, p->cri.stride,
+                             p->pbt_dst.p, nr, p->stream);
+      }
+      p->count_launch(6);
+      for (uint64_t m : reset) {
+        const int64_t zero = 0;
+        const double dz = 0.0;
+        const float fz = 0.0f;
+        CUDA_CHECK(cudaMemcpyAsync(p->t_pol.p + m, &zero, 8, cudaMemcpyHostToDevice, p->stream));
+        CUDA_CHECK(cudaMemcpyAsync(p->t_cri.p + m, &zero, 8, cudaMemcpyHostToDevice, p->stream));
+        CUDA_CHECK(cudaMemcpyAsync(p->t_cri.p + p->n + m, &zero, 8, cudaMemcpyHostToDevice, p->stream));
+        if (p->algo == PBRL_ALGO_TD3) {
+          CUDA_CHECK(cudaMemcpyAsync(p->delay_acc.p + m, &dz, 8, cudaMemcpyHostToDevice, p->stream));
+        } else {
+          CUDA_CHECK(cudaMemcpyAsync(p->t_alpha.p + m, &zero, 8, cudaMemcpyHostToDevice, p->stream));
+          CUDA_CHECK(cudaMemcpyAsync(p->alpha_m.p + m, &fz, 4, cudaMemcpyHostToDevice, p->stream));
+          CUDA_CHECK(cudaMemcpyAsync(p->alpha_v.p + m, &fz, 4, cudaMemcpyHostToDevice, p->stream));
+        }
+        p->sync();
+      }
+    }
+    p->sync();
+  });
+}
+
+int pbrl_pbt_evolve(pbrl_pop* pop, const double* fitness, uint64_t rng_key, uint64_t* rng_next,
+                    uint64_t* replaced, uint64_t* donors, uint32_t* count) {
+  if (pop && (reinterpret_cast<Pop*>(pop)->member_offset != 0 ||
+              reinterpret_cast<Pop*>(pop)->n_global != static_cast<uint64_t>(reinterpret_cast<Pop*>(pop)->n))) {
+    g_last_error = "pbt_evolve: single-shard populations only (use plan/apply + export/import)";
+    return PBRL_E_USAGE;
+  }
+  int rc = pbrl_pbt_plan(pop, fitness, reinterpret_cast<Pop*>(pop)->n, 0.3, rng_key, rng_next,
+                         replaced, donors, count);
+  if (rc != PBRL_OK || *count == 0) return rc;
+  rc = pbrl_pbt_apply(pop, replaced, donors, *count);
+  if (rc != PBRL_OK) return rc;
+  return guarded([&] {
+    Pop* p = P(pop);
+    Seq rng{rng_key, *rng_next};
+    for (uint32_t i = 0; i < *count; ++i) prior_sample(p, rng, replaced[i] - p->member_offset);
+    *rng_next = rng.next;
+    p->upload_hyper();
+  });
+}
+
+int pbrl_member_blob_size(pbrl_pop* pop, uint64_t* floats) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    *floats = (p->algo == PBRL_ALGO_TD3) ? 2 * p->pol.P + 4 * p->cri.P : p->pol.P + 4 * p->cri.P + 1;
+  });
+}
+
+int pbrl_export_member(pbrl_pop* pop, uint64_t member, float* buf) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    check_member(p, member, "export_member");
+    size_t at = 0;
+    for (int net = 0; net < 6; ++net) {
+      if (net == PBRL_NET_POLICY_TARGET && p->algo != PBRL_ALGO_TD3) continue;
+      const size_t cnt = p->net_shape(net).P;
+      CUDA_CHECK(cudaMemcpyAsync(buf + at, p->net_row(net, member), cnt * 4,
+                                 cudaMemcpyDeviceToDevice, p->stream));
+      at += cnt;
+    }
+    if (p->algo == PBRL_ALGO_SAC)
+      CUDA_CHECK(cudaMemcpyAsync(buf + at, p->log_alpha.p + member, 4, cudaMemcpyDeviceToDevice, p->stream));
+    p->sync();
+  });
+}
+
+int pbrl_import_member(pbrl_pop* pop, uint64_t member, const float* buf) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    check_member(p, member, "import_member");
+    size_t at = 0;
+    for (int net = 0; net < 6; ++net) {
+      if (net == PBRL_NET_POLICY_TARGET && p->algo != PBRL_ALGO_TD3) continue;
+      const size_t cnt = p->net_shape(net).P;
+      CUDA_CHECK(cudaMemcpyAsync(p->net_row(net, member), buf + at, cnt * 4,
+                                 cudaMemcpyDeviceToDevice, p->stream));
+      at += cnt;
+    }
+    if (p->algo == PBRL_ALGO_SAC)
+      CUDA_CHECK(cudaMemcpyAsync(p->log_alpha.p + member, buf + at, 4, cudaMemcpyDeviceToDevice, p->stream));
+    p->sync();
+  });
+}
+
+int pbrl_synthetic_batches_device(pbrl_pop* pop, uint64_t count, uint64_t n, uint64_t b,
+                                  uint64_t ds, uint64_t da, uint64_t seed, const pbrl_batch* out) {
+  return guarded([&] {
+    cudaStream_t st = nullptr;
+    if (pop) st = P(pop)->stream;
+    if (!out) PBRL_THROW(PBRL_E_USAGE, "null output batch");
+    launch_synth(count, n, b, ds, da, seed, const_cast<float*>(out->s), const_cast<float*>(out->a),
+                 const_cast<float*>(out->r), const_cast<float*>(out->s2),
+                 const_cast<float*>(out->done), st);
+    g_launches.fetch_add(count);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int pbrl_launch_count(pbrl_pop* pop, uint64_t* launches) {
+  (void)pop;
+  *launches = g_launches.load();
+  return PBRL_OK;
+}
+
+int pbrl_synchronize(pbrl_pop* pop) {
+  return guarded([&] { P(pop)->sync(); });
+}
+
+int pbrl_device_bytes(pbrl_pop* pop, uint64_t* bytes) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    uint64_t b = 0;
+    for (auto* d : {&p->pol_p, &p->pol_t, &p->pol_m, &p->pol_v, &p->pol_g, &p->cri_p, &p->cri_t,
+                    &p->cri_m, &p->cri_v, &p->cri_g})
+      b += d->count * 4;
+    if (p->replay) b += p->replay->ring.count * 4;
+    *bytes = b;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,716 @@
+// CUDA-core kernels of the population update: the FFMA32 check-mode grouped GEMM with fused
+// epilogues, and every elementwise / reduction step of TD3 and SAC.  All kernels are grouped
+// over population members (grid.z or grid.y = member or member x critic), so the number of
+// launches per update step does not depend on the population size (test_bench.cpp:40-53).
+#include "pop.cuh"
+
+namespace pbrl {
+
+// ================================================================== grouped SIMT GEMM
+// Reference order: every output accumulates its products in ascending k in fp32 without FMA
+// (pop_tensor.hpp:155-166 forward, :194-206 backward), so results are bit-identical to the CPU.
+template <int BM, int BN, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    k_gemm_simt(const GemmArgs g) {
+  constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY, BK = 16;
+  const int grp = blockIdx.z;
+  const int mem = grp % g.n_members;
+  if (g.active && !g.active[mem]) return;
+  const int i0 = blockIdx.y * BM, j0 = blockIdx.x * BN;
+  __shared__ float As[BK][BM + 1];
+  __shared__ float Bs[BK][BN + 1];
+  const float* A = g.A.p + (g.A.by_member ? mem : grp) * g.A.gs;
+  const float* B = g.B.p + (g.B.by_member ? mem : grp) * g.B.gs;
+  const int tid = threadIdx.x;
+  const int ty = tid / TX, tx = tid % TX;
+  float acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = g.acc_init;
+
+  for (int k0 = 0; k0 < g.K; k0 += BK) {
+    for (int e = tid; e < BK * BM; e += NT) {
+      int kk, ii;
+      if (g.A.cs == 1) { kk = e % BK; ii = e / BK; } else { ii = e % BM; kk = e / BM; }
+      const int gi = i0 + ii, gk = k0 + kk;
+      float v = 0.0f;
+      if (gi < g.M && gk < g.K) {
+        v = (g.a_ones_row && gi == g.M - 1) ? 1.0f : A[gi * g.A.rs + gk * g.A.cs];
+      }
+      As[kk][ii] = v;
+    }
+    for (int e = tid; e < BK * BN; e += NT) {
+      int kk, jj;
+      if (g.B.cs == 1) { jj = e % BN; kk = e / BN; } else { kk = e % BK; jj = e / BK; }
+      const int gj = j0 + jj, gk = k0 + kk;
+      Bs[kk][jj] = (gj < g.N && gk < g.K) ? B[gk * g.B.rs + gj * g.B.cs] : 0.0f;
+    }
+    __syncthreads();
+    const int kmax = min(BK, g.K - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      float a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty + i * TY];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx + j * TX];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = acc[i][j] + a[i] * b[j];
+    }
+    __syncthreads();
+  }
+
+  float* C = g.C + (g.c_by_member ? mem : grp) * g.c_gs;
+  const float* bias = g.bias.p ? g.bias.p + (g.bias.by_member ? mem : grp) * g.bias.gs : nullptr;
+  const float* aux = g.aux.p ? g.aux.p + (g.aux.by_member ? mem : grp) * g.aux.gs : nullptr;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int gi = i0 + ty + i * TY;
+    if (gi >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int gj = j0 + tx + j * TX;
+      if (gj >= g.N) continue;
+      float v = acc[i][j];
+      switch (g.epi) {
+        case EPI_BIAS: v = v + bias[gj]; break;
+        case EPI_BIAS_RELU: {
+          const float z = v + bias[gj];
+          v = z > 0.0f ? z : 0.0f;
+          break;
+        }
+        case EPI_BIAS_TANH:
+        case EPI_BIAS_TANH_NOISE: {
+          const float t = libm_tanhf(v + bias[gj]);
+          if (g.C2) g.C2[grp * g.c2_gs + gi * g.c2_rs + gj] = t;
+          v = (g.scale != 1.0f) ? t * g.scale : t;
+          if (g.epi == EPI_BIAS_TANH_NOISE) {
+            // algos.hpp:252-262: eps = clamp((T)normal * sd, +-clip); a = clamp(a + eps, +-bound)
+            const uint64_t e = static_cast<uint64_t>(gi) * g.N + gj;
+            float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
+                        g.noise_sd[mem];
+            eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+            v = clampf_ref(v + eps, -g.bound, g.bound);
+          }
+          break;
+        }
+        case EPI_RELU_MASK:
+          if (!(aux[gi * g.aux.rs + gj * g.aux.cs] > 0.0f)) v = 0.0f;
+          break;
+        case EPI_TANH_GRAD: {
+          if (g.scale != 1.0f) v = v * g.scale;
+          const float t = aux[gi * g.aux.rs + gj * g.aux.cs];
+          v = v * (1.0f - t * t);
+          break;
+        }
+        default: break;
+      }
+      C[gi * g.c_rs + gj] = v;
+    }
+  }
+}
+
+void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
+  if (g.M <= 0 || g.N <= 0 || g.groups <= 0) return;
+  if (g.N <= 16) {
+    constexpr int BM = 128, BN = 16, TM = 4, TN = 2;
+    dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.groups);
+    k_gemm_simt<BM, BN, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, s>>>(g);
+  } else {
+    constexpr int BM = 64, BN = 64, TM = 4, TN = 4;
+    dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.groups);
+    k_gemm_simt<BM, BN, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, s>>>(g);
+  }
+}
+
+// ================================================================== TD3 step bookkeeping
+// Delayed-policy fire mask (algos.hpp:379-393), Adam step counters, target-noise stream keys
+// (algos.hpp:253) and steps += 1 (:421).  One thread per member.
+__global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
+                                 const uint8_t* mask, int* fire, int64_t* t_pol, int64_t* t_c1,
+                                 int64_t* t_c2, uint64_t* steps, const uint64_t* streams,
+                                 uint64_t seed, uint64_t* noise_key) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  int f = 0;
+  double acc = delay_acc[m] + ratio[m];
+  if (acc >= 1.0 - 1e-12) {
+    acc -= 1.0;
+    f = 1;
+  }
+  delay_acc[m] = acc;
+  if (mask && !mask[m]) f = 0;
+  fire[m] = f;
+  t_c1[m] += 1;
+  t_c2[m] += 1;
+  if (f) t_pol[m] += 1;
+  noise_key[m] = stream_key(seed, streams[m], kTargetNoise, steps[m]);
+  steps[m] += 1;
+}
+
+void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const uint8_t* mask,
+                           int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
+                           uint64_t* steps, const uint64_t* streams, uint64_t seed,
+                           uint64_t* noise_key, cudaStream_t s) {
+  k_td3_step_begin<<<(n + 127) / 128, 128, 0, s>>>(n, delay_acc, ratio, mask, fire, t_pol, t_c1,
+                                                   t_c2, steps, streams, seed, noise_key);
+}
+
+// concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts
+__global__ void k_pack_batch(int n, int B, int ds, int da, const float* s, const float* a,
+                             const float* r, const float* s2, const float* d, float* in_sa,
+                             float* in_s2a, float* sa_pi, float* r_out, float* d_out) {
+  const int dsa = ds + da;
+  const long long rows = static_cast<long long>(n) * B;
+  const long long total = rows * dsa;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long row = e / dsa;
+    const int c = static_cast<int>(e % dsa);
+    if (c < ds) {
+      const float sv = s[row * ds + c];
+      in_sa[e] = sv;
+      sa_pi[e] = sv;
+      in_s2a[e] = s2[row * ds + c];
+    } else {
+      in_sa[e] = a[row * da + (c - ds)];
+    }
+    if (c == 0) {
+      r_out[row] = r[row];
+      d_out[row] = d[row];
+    }
+  }
+}
+
+void launch_pack_batch(int n, int B, int ds, int da, const float* s, const float* a,
+                       const float* r, const float* s2, const float* d, float* in_sa,
+                       float* in_s2a, float* sa_pi, float* r_out, float* d_out, cudaStream_t st) {
+  const long long total = static_cast<long long>(n) * B * (ds + da);
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  k_pack_batch<<<blocks, 256, 0, st>>>(n, B, ds, da, s, a, r, s2, d, in_sa, in_s2a, sa_pi, r_out,
+                                       d_out);
+}
+
+// y = r + gamma*(1-done)*min(Q1', Q2')   (algos.hpp:268-281)
+__global__ void k_td_target(int n, int B, const float* r, const float* d, const float* q2n,
+                            const float* gamma, float* y) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * B) return;
+  const int m = e / B;
+  const float qmin = minf_ref(q2n[e], q2n[n * B + e]);
+  y[e] = r[e] + gamma[m] * (1.0f - d[e]) * qmin;
+}
+
+void launch_td_target(int n, int B, const float* r, const float* d, const float* q2n,
+                      const float* gamma, float* y, cudaStream_t s) {
+  k_td_target<<<(n * B + 255) / 256, 256, 0, s>>>(n, B, r, d, q2n, gamma, y);
+}
+
+// mse_loss_grads (algos.hpp:288-314): dq = (2/B)(q - y); loss = sum (double) d^2 / B in row order
+__global__ void k_mse(int n, int B, const float* q, const float* y, float* dq, double* loss) {
+  const int grp = blockIdx.x;
+  const int m = grp % n;
+  const float scale = 2.0f / static_cast<float>(B);
+  const float* qg = q + static_cast<long long>(grp) * B;
+  const float* yg = y + static_cast<long long>(m) * B;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    dq[static_cast<long long>(grp) * B + b] = scale * (qg[b] - yg[b]);
+  }
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int b = 0; b < B; ++b) {
+      const float dl = qg[b] - yg[b];
+      acc += static_cast<double>(dl) * static_cast<double>(dl);
+    }
+    loss[grp] = acc / static_cast<double>(B);
+  }
+}
+
+void launch_mse(int groups, int n, int B, const float* q, const float* y, float* dq, double* loss,
+                cudaStream_t s) {
+  k_mse<<<groups, 256, 0, s>>>(n, B, q, y, dq, loss);
+}
+
+// td3_policy_loss_grads (algos.hpp:318-338): loss = -sum q / B; cotangent -1/B everywhere
+__global__ void k_td3_policy_loss(int n, int B, const float* q, const int* fire, double* loss,
+                                  float* gq) {
+  const int m = blockIdx.x;
+  const float gv = -1.0f / static_cast<float>(B);
+  for (int b = threadIdx.x; b < B; b += blockDim.x) gq[static_cast<long long>(m) * B + b] = gv;
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    if (fire[m]) {
+      for (int b = 0; b < B; ++b) acc -= static_cast<double>(q[static_cast<long long>(m) * B + b]);
+      acc /= static_cast<double>(B);
+    }
+    loss[m] = acc;
+  }
+}
+
+void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, double* loss,
+                            float* gq, cudaStream_t s) {
+  k_td3_policy_loss<<<n, 256, 0, s>>>(n, B, q, fire, loss, gq);
+}
+
+// ================================================================== fused Adam + Polyak
+// adam_step_inplace (pop_tensor.hpp:328-366) with the bias corrections looked up from
+// host-computed tables (corr[t] = (float)(1 - pow(beta, t)) in double, exactly :347-350), and
+// the target update tgt = (T)tau*on + (T)(1-tau)*tgt (:422-426) fused on the fresh parameter.
+__global__ void k_adam(int n, size_t P, size_t stride, float* __restrict__ p,
+                       float* __restrict__ mo, float* __restrict__ vo,
+                       const float* __restrict__ g, const int64_t* t, const float* corr1,
+                       const float* corr2, const float* lr, const int* active,
+                       float* __restrict__ tgt, const float* tau_a, const float* tau_b,
+                       const int* polyak_gate) {
+  const int grp = blockIdx.y;
+  const int m = grp % n;
+  if (active && !active[m]) return;
+  const long long base = static_cast<long long>(grp) * stride;
+  const float b1 = static_cast<float>(0.9);
+  const float b2 = static_cast<float>(0.999);
+  const float c1 = corr1[t[grp]];
+  const float c2 = corr2[t[grp]];
+  const float step = lr[m];
+  const float epsv = static_cast<float>(1e-8);
+  const bool do_polyak = tgt && (!polyak_gate || polyak_gate[m]);
+  const float ta = do_polyak ? tau_a[m] : 0.0f;
+  const float tb = do_polyak ? tau_b[m] : 0.0f;
+  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < P;
+       k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const long long e = base + static_cast<long long>(k);
+    const float gk = g[e];
+    const float mk = b1 * mo[e] + (1.0f - b1) * gk;
+    const float vk = b2 * vo[e] + (1.0f - b2) * gk * gk;
+    mo[e] = mk;
+    vo[e] = vk;
+    const float mhat = mk / c1;
+    const float vhat = vk / c2;
+    const float pk = p[e] - step * mhat / (sqrtf(vhat) + epsv);
+    p[e] = pk;
+    if (do_polyak) tgt[e] = ta * pk + tb * tgt[e];
+  }
+}
+
+void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m, float* v,
+                 const float* g, const int64_t* t, const float* corr1, const float* corr2,
+                 const float* lr, const int* active, float* tgt, const float* tau_a,
+                 const float* tau_b, const int* polyak_gate, cudaStream_t s) {
+  const int threads = 256;
+  int bx = static_cast<int>((P + threads * 4 - 1) / (threads * 4));
+  bx = bx < 1 ? 1 : bx;
+  dim3 grid(bx, groups);
+  k_adam<<<grid, threads, 0, s>>>(n, P, stride, p, m, v, g, t, corr1, corr2, lr, active, tgt,
+                                  tau_a, tau_b, polyak_gate);
+}
+
+__global__ void k_fill(float* p, size_t count, float v) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+void launch_fill(float* p, size_t count, float v, cudaStream_t s) {
+  const int blocks = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 8));
+  k_fill<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(p, count, v);
+}
+
+// ================================================================== SAC
+__global__ void k_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
+                                 int64_t* t_alpha, uint64_t* steps, const uint64_t* streams,
+                                 uint64_t seed, uint64_t* key_eps, uint64_t* key_eps_t) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  t_pol[m] += 1;
+  t_c1[m] += 1;
+  t_c2[m] += 1;
+  t_alpha[m] += 1;
+  key_eps[m] = stream_key(seed, streams[m], kSacEps, steps[m]);
+  key_eps_t[m] = stream_key(seed, streams[m], kSacEpsTarget, steps[m]);
+  steps[m] += 1;
+}
+
+void launch_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2, int64_t* t_alpha,
+                           uint64_t* steps, const uint64_t* streams, uint64_t seed,
+                           uint64_t* key_eps, uint64_t* key_eps_t, cudaStream_t s) {
+  k_sac_step_begin<<<(n + 127) / 128, 128, 0, s>>>(n, t_pol, t_c1, t_c2, t_alpha, steps, streams,
+                                                   seed, key_eps, key_eps_t);
+}
+
+// glibc-compatible float transcendentals for SAC: exp/log1p evaluated in double and rounded
+// (glibc's expf is within 0.502 ulp; log1pf is the fdlibm algorithm) -- agreement is
+// near-bitwise, and SAC parity is stated with a tolerance.
+__device__ __forceinline__ float sac_expf(float x) {
+  return static_cast<float>(exp(static_cast<double>(x)));
+}
+__device__ __forceinline__ float sac_log1pf(float x) {
+  return static_cast<float>(log1p(static_cast<double>(x)));
+}
+
+// log_one_minus_tanh_sq (algos.hpp:523-529)
+__device__ __forceinline__ float l1mts(float x) {
+  const float z = -2.0f * x;
+  const float sp = maxf_ref(z, 0.0f) + sac_log1pf(sac_expf(-fabsf(z)));
+  return static_cast<float>(1.3862943611198906) - 2.0f * x - 2.0f * sp;
+}
+
+// split_policy_head + draw_eps + tanh_gaussian_logprob + tanh squash (algos.hpp:534-629)
+__global__ void k_sac_head(int n, int B, int ds, int da, const float* head, const uint64_t* key,
+                           float bound, float log_bound, float* sa, float* x, float* th,
+                           float* ls_out, uint8_t* clamped, float* eps_out, float* logp) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // (m, b)
+  if (e >= n * B) return;
+  const int m = e / B, b = e % B;
+  const float hl2pi = static_cast<float>(0.9189385332046727);
+  const float* h = head + static_cast<long long>(e) * 2 * da;
+  float acc = 0.0f;
+  for (int j = 0; j < da; ++j) {
+    const long long k = static_cast<long long>(e) * da + j;
+    const float mu = h[j];
+    float ls = h[da + j];
+    uint8_t c = 0;
+    if (ls < static_cast<float>(-20.0)) { ls = static_cast<float>(-20.0); c = 1; }
+    else if (ls > static_cast<float>(2.0)) { ls = static_cast<float>(2.0); c = 1; }
+    const float ep = static_cast<float>(
+        rng_normal_pair(key[m], 2 * (static_cast<uint64_t>(b) * da + j)));
+    const float sig = sac_expf(ls);
+    const float xv = mu + sig * ep;
+    acc += -0.5f * ep * ep - ls - hl2pi;
+    acc -= l1mts(xv);
+    acc -= log_bound;
+    const float t = libm_tanhf(xv);
+    if (x) x[k] = xv;
+    if (th) th[k] = t;
+    if (ls_out) ls_out[k] = ls;
+    if (clamped) clamped[k] = c;
+    if (eps_out) eps_out[k] = ep;
+    sa[static_cast<long long>(e) * (ds + da) + ds + j] = t * bound;
+  }
+  logp[e] = acc;
+}
+
+void launch_sac_head(int n, int B, int ds, int da, const float* head, const uint64_t* key,
+                     float bound, float* sa, float* x, float* th, float* ls, uint8_t* clamped,
+                     float* eps, float* logp, cudaStream_t s) {
+  extern float host_logf(float);
+  k_sac_head<<<(n * B + 127) / 128, 128, 0, s>>>(n, B, ds, da, head, key, bound, host_logf(bound),
+                                                 sa, x, th, ls, clamped, eps, logp);
+}
+
+// y = rs*r + gamma*(1-d)*(min(Q1',Q2') - alpha*logp')  (algos.hpp:759-774)
+__global__ void k_sac_y(int n, int B, const float* r, const float* d, const float* q2n,
+                        const float* logp2, const float* log_alpha, const float* gamma,
+                        const float* rscale, float* y) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * B) return;
+  const int m = e / B;
+  const float alpha = sac_expf(log_alpha[m]);
+  const float qmin = minf_ref(q2n[e], q2n[n * B + e]);
+  y[e] = rscale[m] * r[e] + gamma[m] * (1.0f - d[e]) * (qmin - alpha * logp2[e]);
+}
+
+void launch_sac_y(int n, int B, const float* r, const float* d, const float* q2n,
+                  const float* logp2, const float* log_alpha, const float* gamma,
+                  const float* rscale, float* y, cudaStream_t s) {
+  k_sac_y<<<(n * B + 255) / 256, 256, 0, s>>>(n, B, r, d, q2n, logp2, log_alpha, gamma, rscale,
+                                              y);
+}
+
+// policy-loss cotangents (algos.hpp:665-692): -1/B routed to the smaller critic, logp weight
+// alpha/B, loss accumulated per member in row order (double).
+__global__ void k_sac_policy_top(int n, int B, const float* q2n, const float* logp,
+                                 const float* log_alpha, double* loss, float* gq2n, float* lw) {
+  const int m = blockIdx.x;
+  const float am = static_cast<float>(exp(static_cast<double>(log_alpha[m])));
+  const float inv_rows = 1.0f / static_cast<float>(B);
+  const long long o = static_cast<long long>(m) * B;
+  const long long o2 = static_cast<long long>(n) * B + o;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const float q1 = q2n[o + b], q2 = q2n[o2 + b];
+    lw[o + b] = am * inv_rows;
+    gq2n[o + b] = (q1 <= q2) ? -inv_rows : 0.0f;
+    gq2n[o2 + b] = (q1 <= q2) ? 0.0f : -inv_rows;
+  }
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int b = 0; b < B; ++b) {
+      const float qmin = minf_ref(q2n[o + b], q2n[o2 + b]);
+      acc += static_cast<double>(am * logp[o + b] - qmin) / static_cast<double>(B);
+    }
+    loss[m] = acc;
+  }
+}
+
+void launch_sac_policy_top(int n, int B, const float* q2n, const float* logp,
+                           const float* log_alpha, double* loss, float* gq2n, float* lw,
+                           cudaStream_t s) {
+  k_sac_policy_top<<<n, 256, 0, s>>>(n, B, q2n, logp, log_alpha, loss, gq2n, lw);
+}
+
+// tanh_gaussian_logprob_backward + the action path (algos.hpp:571-595, :705-724) -> head grad
+__global__ void k_sac_head_grad(int n, int B, int da, const float* ga2n, const float* lw,
+                                const float* x, const float* th, const float* ls,
+                                const uint8_t* clamped, const float* eps, float bound,
+                                float* gh) {
+  const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;  // (m,b,j)
+  const long long total = static_cast<long long>(n) * B * da;
+  if (e >= total) return;
+  const long long row = e / da;
+  const int j = static_cast<int>(e % da);
+  const float w = lw[row];
+  const float dlogp_dx = 2.0f * libm_tanhf(x[e]);
+  const float el = sac_expf(ls[e]);
+  float gmu = w * dlogp_dx;
+  float gls = w * (dlogp_dx * el * eps[e] - 1.0f);
+  const float ga = ga2n[e] + ga2n[total + e];
+  const float t = th[e];
+  const float dadx = bound * (1.0f - t * t);
+  const float gx = ga * dadx;
+  gmu += gx;
+  gls += gx * el * eps[e];
+  if (clamped[e]) gls = 0.0f;
+  gh[row * 2 * da + j] = gmu;
+  gh[row * 2 * da + da + j] = gls;
+}
+
+void launch_sac_head_grad(int n, int B, int da, const float* ga2n, const float* lw,
+                          const float* x, const float* th, const float* ls,
+                          const uint8_t* clamped, const float* eps, float bound, float* gh,
+                          cudaStream_t s) {
+  const long long total = static_cast<long long>(n) * B * da;
+  k_sac_head_grad<<<static_cast<int>((total + 255) / 256), 256, 0, s>>>(
+      n, B, da, ga2n, lw, x, th, ls, clamped, eps, bound, gh);
+}
+
+// temperature step (algos.hpp:814-825): g = -alpha * mean_b(logp + target_entropy) in double,
+// then a one-parameter Adam on log_alpha.
+__global__ void k_sac_alpha(int n, int B, const float* logp, const double* te,
+                            float* log_alpha, float* am, float* av, const int64_t* t,
+                            const float* corr1, const float* corr2, const float* lr) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const double alpha = exp(static_cast<double>(log_alpha[m]));
+  double mt = 0.0;
+  for (int b = 0; b < B; ++b) mt += static_cast<double>(logp[static_cast<long long>(m) * B + b]) + te[m];
+  mt /= static_cast<double>(B);
+  const float g = static_cast<float>(-alpha * mt);
+  const float b1 = static_cast<float>(0.9), b2 = static_cast<float>(0.999);
+  const float mk = b1 * am[m] + (1.0f - b1) * g;
+  const float vk = b2 * av[m] + (1.0f - b2) * g * g;
+  am[m] = mk;
+  av[m] = vk;
+  const float mhat = mk / corr1[t[m]];
+  const float vhat = vk / corr2[t[m]];
+  log_alpha[m] = log_alpha[m] - lr[m] * mhat / (sqrtf(vhat) + static_cast<float>(1e-8));
+}
+
+void launch_sac_alpha(int n, int B, const float* logp, const float* log_alpha_in,
+                      const double* target_entropy, float* log_alpha, float* am, float* av,
+                      const int64_t* t, const float* corr1, const float* corr2, const float* lr,
+                      cudaStream_t s) {
+  (void)log_alpha_in;
+  k_sac_alpha<<<(n + 127) / 128, 128, 0, s>>>(n, B, logp, target_entropy, log_alpha, am, av, t,
+                                              corr1, corr2, lr);
+}
+
+// ================================================================== replay
+// ReplayBuffer rows live in HBM as [buffer][cap][rw] floats: s | a | s2 | r | done | pad.
+__global__ void k_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t count,
+                                 int rw, float* ring) {
+  const long long total = static_cast<long long>(count) * rw;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = e / rw;
+    const int c = static_cast<int>(e % rw);
+    ring[dst_row[i] * rw + c] = rows[e];
+  }
+}
+
+void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t count, int rw,
+                           float* ring, cudaStream_t s) {
+  const long long total = static_cast<long long>(count) * rw;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  k_replay_scatter<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(rows, dst_row, count, rw, ring);
+}
+
+// sample_batch (replay.hpp:181-204): slot = bits(key, b) % size with key =
+// RngStream::of(seed, streams[m], kSample, draw_id); one warp gathers one row (coalesced 4 B
+// lanes over the row) straight into the critic-input layouts.
+__global__ void k_replay_gather(int n, int B, int ds, int da, int rw, const float* ring,
+                                uint64_t cap, int shared, const uint64_t* sizes,
+                                const uint64_t* streams, uint64_t seed, uint64_t draw_id,
+                                float* in_sa, float* in_s2a, float* sa_pi, float* r_out,
+                                float* d_out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= n * B) return;
+  const int m = warp / B, b = warp % B;
+  const int buf = shared ? 0 : m;
+  const uint64_t key = stream_key(seed, streams[m], kSample, draw_id);
+  const uint64_t slot = rng_bits(key, static_cast<uint64_t>(b)) % sizes[buf];
+  const float* row = ring + (static_cast<uint64_t>(buf) * cap + slot) * rw;
+  const int dsa = ds + da;
+  const long long o = static_cast<long long>(warp) * dsa;
+  for (int c = lane; c < 2 * ds + da + 2; c += 32) {
+    const float v = row[c];
+    if (c < ds) {
+      in_sa[o + c] = v;
+      if (sa_pi) sa_pi[o + c] = v;
+    } else if (c < dsa) {
+      in_sa[o + c] = v;
+    } else if (c < dsa + ds) {
+      in_s2a[o + (c - dsa)] = v;
+    } else if (c == dsa + ds) {
+      r_out[warp] = v;
+    } else {
+      d_out[warp] = v;
+    }
+  }
+}
+
+void launch_replay_gather(int n, int B, int ds, int da, int rw, const float* ring,
+                          uint64_t cap, int shared, const uint64_t* sizes,
+                          const uint64_t* streams, uint64_t seed, uint64_t draw_id,
+                          float* in_sa, float* in_s2a, float* sa_pi, float* r_out, float* d_out,
+                          cudaStream_t s) {
+  const long long warps = static_cast<long long>(n) * B;
+  const int blocks = static_cast<int>((warps * 32 + 255) / 256);
+  k_replay_gather<<<blocks, 256, 0, s>>>(n, B, ds, da, rw, ring, cap, shared, sizes, streams,
+                                         seed, draw_id, in_sa, in_s2a, sa_pi, r_out, d_out);
+}
+
+// ================================================================== PBT
+// pbt_rank (evolve.hpp:112-122) as a stable rank: position of i = #{j : f_j > f_i} +
+// #{j < i : f_j == f_i}; then pbt_plan (:133-145): replaced[i] = order[n-1-i],
+// donors[i] = order[bits(key, next + i) % cut].  One block.
+__global__ void k_pbt_plan(int n, const double* fitness, int cut, uint64_t key, uint64_t next,
+                           uint64_t* order, uint64_t* replaced, uint64_t* donors) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double fi = fitness[i];
+    int pos = 0;
+    for (int j = 0; j < n; ++j) {
+      const double fj = fitness[j];
+      pos += (fj > fi) || (j < i && !(fj > fi) && !(fi > fj));
+    }
+    order[pos] = static_cast<uint64_t>(i);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < cut; i += blockDim.x) {
+    replaced[i] = order[n - 1 - i];
+    donors[i] = order[rng_bits(key, next + static_cast<uint64_t>(i)) % static_cast<uint64_t>(cut)];
+  }
+}
+
+void launch_pbt_plan(int n, const double* fitness, int cut, uint64_t key, uint64_t next,
+                     uint64_t* order, uint64_t* replaced, uint64_t* donors, cudaStream_t s) {
+  k_pbt_plan<<<1, 256, 0, s>>>(n, fitness, cut, key, next, order, replaced, donors);
+}
+
+// copy_member (net_pop.hpp:192-202) for many (src, dst) pairs of one arena
+__global__ void k_member_copy(float* arena, size_t stride, size_t P, const uint64_t* src,
+                              const uint64_t* dst) {
+  const int pr = blockIdx.y;
+  const uint64_t s = src[pr], d = dst[pr];
+  if (s == d) return;
+  const float* a = arena + s * stride;
+  float* b = arena + d * stride;
+  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < P;
+       k += static_cast<size_t>(gridDim.x) * blockDim.x)
+    b[k] = a[k];
+}
+
+void launch_member_copy(float* arena, size_t stride, size_t P, const uint64_t* src,
+                        const uint64_t* dst, int pairs, cudaStream_t s) {
+  if (pairs <= 0) return;
+  dim3 grid(static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((P + 1023) / 1024, 64))),
+            pairs);
+  k_member_copy<<<grid, 256, 0, s>>>(arena, stride, P, src, dst);
+}
+
+__global__ void k_member_zero(float* arena, size_t stride, const uint64_t* dst) {
+  float* b = arena + dst[blockIdx.y] * stride;
+  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < stride;
+       k += static_cast<size_t>(gridDim.x) * blockDim.x)
+    b[k] = 0.0f;
+}
+
+void launch_member_zero(float* arena, size_t stride, const uint64_t* dst, int pairs,
+                        cudaStream_t s) {
+  if (pairs <= 0) return;
+  dim3 grid(static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((stride + 1023) / 1024, 64))),
+            pairs);
+  k_member_zero<<<grid, 256, 0, s>>>(arena, stride, dst);
+}
+
+// ================================================================== init
+// init_pop_mlp (net_pop.hpp:69-100): w = (T)(lo + (hi-lo)*u) in double per (member, layer)
+// stream; exact on the device (IEEE double ops, no contraction).
+__global__ void k_init_layer(float* arena, size_t stride, size_t woff, size_t boff, int fi,
+                             int fo, uint64_t member_offset, uint64_t seed, int layer) {
+  const int m = blockIdx.y;
+  const uint64_t gm = member_offset + static_cast<uint64_t>(m);
+  const double wb = sqrt(1.0 / static_cast<double>(fi));
+  const double bb = 1.0 / sqrt(static_cast<double>(fi));
+  const uint64_t ws = stream_key(seed, gm, kInitWeight, static_cast<uint64_t>(layer));
+  const uint64_t bs = stream_key(seed, gm, kInitBias, static_cast<uint64_t>(layer));
+  float* w = arena + static_cast<size_t>(m) * stride + woff;
+  float* bv = arena + static_cast<size_t>(m) * stride + boff;
+  const size_t nw = static_cast<size_t>(fi) * fo;
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < nw + fo;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    if (e < nw) {
+      w[e] = static_cast<float>(-wb + (wb - (-wb)) * rng_uniform(ws, e));
+    } else {
+      const size_t k = e - nw;
+      bv[k] = static_cast<float>(-bb + (bb - (-bb)) * rng_uniform(bs, k));
+    }
+  }
+}
+
+void launch_init_net(const NetShape& sh, float* arena, int n, uint64_t member_offset,
+                     uint64_t seed, cudaStream_t s) {
+  for (int l = 0; l < sh.depth; ++l) {
+    const size_t cnt = static_cast<size_t>(sh.dims[l]) * sh.dims[l + 1] + sh.dims[l + 1];
+    dim3 grid(static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((cnt + 255) / 256, 64))),
+              n);
+    k_init_layer<<<grid, 256, 0, s>>>(arena, sh.stride, sh.woff[l], sh.boff[l], sh.dims[l],
+                                      sh.dims[l + 1], member_offset, seed, l);
+  }
+}
+
+// make_synthetic_batches (bench.hpp:69-93): per batch i, s/a/r/s2 ~ U[-1,1) from
+// RngStream::of(seed, i, kGeneric, 1..4) and done = U < 0.02 from step 5; element e counters.
+__global__ void k_synth(uint64_t n_elems_s, uint64_t n_elems_a, uint64_t n_elems_r, uint64_t seed,
+                        uint64_t batch, float* s, float* a, float* r, float* s2, float* d) {
+  const uint64_t ks = stream_key(seed, batch, kGeneric, 1), ka = stream_key(seed, batch, kGeneric, 2),
+                 kr = stream_key(seed, batch, kGeneric, 3), k2 = stream_key(seed, batch, kGeneric, 4),
+                 kd = stream_key(seed, batch, kGeneric, 5);
+  const uint64_t total = 2 * n_elems_s + n_elems_a + 2 * n_elems_r;
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t k = e;
+    if (k < n_elems_s) { s[k] = static_cast<float>(-1.0 + (1.0 - (-1.0)) * rng_uniform(ks, k)); continue; }
+    k -= n_elems_s;
+    if (k < n_elems_a) { a[k] = static_cast<float>(-1.0 + (1.0 - (-1.0)) * rng_uniform(ka, k)); continue; }
+    k -= n_elems_a;
+    if (k < n_elems_r) { r[k] = static_cast<float>(-1.0 + (1.0 - (-1.0)) * rng_uniform(kr, k)); continue; }
+    k -= n_elems_r;
+    if (k < n_elems_s) { s2[k] = static_cast<float>(-1.0 + (1.0 - (-1.0)) * rng_uniform(k2, k)); continue; }
+    k -= n_elems_s;
+    d[k] = rng_uniform(kd, k) < 0.02 ? 1.0f : 0.0f;
+  }
+}
+
+void launch_synth(uint64_t count, uint64_t n, uint64_t b, uint64_t ds, uint64_t da, uint64_t seed,
+                  float* s, float* a, float* r, float* s2, float* d, cudaStream_t st) {
+  const uint64_t es = n * b * ds, ea = n * b * da, er = n * b;
+  for (uint64_t i = 0; i < count; ++i) {
+    const uint64_t total = 2 * es + ea + 2 * er;
+    const int blocks = static_cast<int>(std::min<uint64_t>((total + 255) / 256, 148 * 16));
+    k_synth<<<blocks, 256, 0, st>>>(es, ea, er, seed, i, s + i * es, a + i * ea, r + i * er,
+                                    s2 + i * es, d + i * er);
+  }
+}
+
+}  // namespace pbrl

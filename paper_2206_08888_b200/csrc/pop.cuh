@@ -1,0 +1,163 @@
+// Internal declarations of the B200 population-update library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pbrl_b200.h"
+#include "common.cuh"
+
+namespace pbrl {
+
+constexpr int kMaxLayers = 8;
+enum Act { ACT_NONE = 0, ACT_RELU = 1, ACT_TANH = 2 };
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PBRL_THROW(code, msg) throw ::pbrl::Error((code), (msg))
+#define CUDA_CHECK(x)                                                                       \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::pbrl::Error(PBRL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+// A population of identically shaped MLPs (PopMLPParams, net_pop.hpp:17-43).  On device every
+// member occupies `stride` floats (P rounded up to 64 so member rows are 256 B aligned); the
+// first P floats are the member in flatten_member order: W0 [in][out], b0, W1, b1, ...
+struct NetShape {
+  int depth = 0;
+  int dims[kMaxLayers + 1] = {};
+  int out_act = ACT_NONE;
+  float out_scale = 1.0f;
+  size_t P = 0, stride = 0;
+  size_t woff[kMaxLayers] = {}, boff[kMaxLayers] = {};
+  void make(const std::vector<size_t>& d, int act, float scale);
+  int max_hidden() const;
+};
+
+// ------------------------------------------------------------------ GEMM launch descriptor
+// C[g](i,j) = epi( sum_k A[g](i,k) * B[g](k,j) ), k ascending (the reference order).
+// Operand element (r,c) of group g lives at base + grp*gs + r*rs + c*cs, where grp = g, or
+// the member id m = g % n_members when the operand is shared by the critics of one member.
+enum Epi {
+  EPI_STORE = 0,        // C = acc
+  EPI_BIAS = 1,         // C = acc + bias[j]
+  EPI_BIAS_RELU = 2,    // C = relu(acc + bias[j])
+  EPI_BIAS_TANH = 3,    // t = tanh(acc + bias[j]); C2 = t; C = t * scale
+  EPI_BIAS_TANH_NOISE = 4,  // as EPI_BIAS_TANH, then TD3 target smoothing noise on C
+  EPI_RELU_MASK = 5,    // C = aux(i,j) > 0 ? acc : 0       (activation_backward, relu)
+  EPI_TANH_GRAD = 6,    // g = acc * scale; C = g * (1 - aux^2)   (tanh backward, aux = t)
+};
+
+struct Operand {
+  const float* p = nullptr;
+  long long gs = 0, rs = 0, cs = 0;
+  int by_member = 0;
+};
+
+struct GemmArgs {
+  int M = 0, N = 0, K = 0, groups = 0, n_members = 1;
+  Operand A, B;
+  int a_ones_row = 0;  // row M-1 of A is all ones: C row M-1 = column sums of B (bias grad)
+  float* C = nullptr;
+  long long c_gs = 0, c_rs = 0;
+  int c_by_member = 0;
+  int epi = EPI_STORE;
+  Operand bias;        // bias row vector (cs = 1)
+  Operand aux;         // relu mask source / tanh values
+  float* C2 = nullptr; // tanh values out
+  long long c2_gs = 0, c2_rs = 0;
+  float scale = 1.0f;
+  float acc_init = 0.0f;     // -0.0f reproduces "first product assigned" (pop_tensor.hpp:158-160)
+  const int* active = nullptr;  // per-member gate (policy fire mask)
+  // target smoothing noise (algos.hpp:252-262)
+  const uint64_t* noise_key = nullptr;
+  const float* noise_sd = nullptr;
+  const float* noise_clip = nullptr;
+  float bound = 1.0f;
+};
+
+void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
+
+// ------------------------------------------------------------------ elementwise launchers
+struct Hyper;  // device per-member hyper floats
+
+void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const uint8_t* mask,
+                           int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
+                           uint64_t* steps, const uint64_t* streams, uint64_t seed,
+                           uint64_t* noise_key, cudaStream_t s);
+void launch_pack_batch(int n, int B, int ds, int da, const float* s, const float* a,
+                       const float* r, const float* s2, const float* d, float* in_sa,
+                       float* in_s2a, float* sa_pi, float* r_out, float* d_out, cudaStream_t st);
+void launch_td_target(int n, int B, const float* r, const float* d, const float* q2n,
+                      const float* gamma, float* y, cudaStream_t s);
+void launch_mse(int groups, int n, int B, const float* q, const float* y, float* dq, double* loss,
+                cudaStream_t s);
+void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, double* loss,
+                            float* gq, cudaStream_t s);
+// Adam (pop_tensor.hpp:328-366) over a [groups][stride] arena, first P floats per group, with
+// per-member lr, optional fire gate, and an optional fused Polyak update of a target arena
+// (soft_update_members_inplace, :412-428) gated per member by polyak_gate (NULL = always).
+void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m, float* v,
+                 const float* g, const int64_t* t, const float* corr1, const float* corr2,
+                 const float* lr, const int* active, float* tgt, const float* tau_a,
+                 const float* tau_b, const int* polyak_gate, cudaStream_t s);
+void launch_fill(float* p, size_t count, float v, cudaStream_t s);
+
+// SAC
+void launch_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2, int64_t* t_alpha,
+                           uint64_t* steps, const uint64_t* streams, uint64_t seed,
+                           uint64_t* key_eps, uint64_t* key_eps_t, cudaStream_t s);
+// split_policy_head + tanh_gaussian_logprob + squash (algos.hpp:534-616): head [n][B][2da] ->
+// act into sa (cols ds..), x, th, ls (clamped), clamped flag, logp.
+void launch_sac_head(int n, int B, int ds, int da, const float* head, const uint64_t* key,
+                     float bound, float* sa, float* x, float* th, float* ls, uint8_t* clamped,
+                     float* eps, float* logp, cudaStream_t s);
+void launch_sac_y(int n, int B, const float* r, const float* d, const float* q2n,
+                  const float* logp2, const float* log_alpha, const float* gamma,
+                  const float* rscale, float* y, cudaStream_t s);
+void launch_sac_policy_top(int n, int B, const float* q2n, const float* logp,
+                           const float* log_alpha, double* loss, float* gq2n, float* lw,
+                           cudaStream_t s);
+void launch_sac_head_grad(int n, int B, int da, const float* ga2n, const float* lw,
+                          const float* x, const float* th, const float* ls,
+                          const uint8_t* clamped, const float* eps, float bound, float* gh,
+                          cudaStream_t s);
+void launch_sac_alpha(int n, int B, const float* logp, const float* log_alpha_in,
+                      const double* target_entropy, float* log_alpha, float* am, float* av,
+                      const int64_t* t, const float* corr1, const float* corr2, const float* lr,
+                      cudaStream_t s);
+
+// replay
+void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t count, int rw,
+                           float* ring, cudaStream_t s);
+void launch_replay_gather(int n, int B, int ds, int da, int rw, const float* ring,
+                          uint64_t cap, int shared, const uint64_t* sizes,
+                          const uint64_t* streams, uint64_t seed, uint64_t draw_id,
+                          float* in_sa, float* in_s2a, float* sa_pi, float* r_out, float* d_out,
+                          cudaStream_t s);
+
+// PBT
+void launch_pbt_plan(int n, const double* fitness, int cut, uint64_t key, uint64_t next,
+                     uint64_t* order, uint64_t* replaced, uint64_t* donors, cudaStream_t s);
+void launch_member_copy(float* arena, size_t stride, size_t P, const uint64_t* src,
+                        const uint64_t* dst, int pairs, cudaStream_t s);
+void launch_member_zero(float* arena, size_t stride, const uint64_t* dst, int pairs,
+                        cudaStream_t s);
+
+void launch_synth(uint64_t count, uint64_t n, uint64_t b, uint64_t ds, uint64_t da, uint64_t seed,
+                  float* s, float* a, float* r, float* s2, float* d, cudaStream_t st);
+
+// init (init_pop_mlp, net_pop.hpp:69-100)
+void launch_init_net(const NetShape& sh, float* arena, int n, uint64_t member_offset,
+                     uint64_t seed, cudaStream_t s);
+
+}  // namespace pbrl

@@ -1,0 +1,162 @@
+// Population object (host side of the C ABI).
+#pragma once
+
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "pop.cuh"
+
+namespace pbrl {
+
+extern std::atomic<uint64_t> g_launches;
+
+// Owning device buffer.
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), count(o.count) {
+    o.p = nullptr;
+    o.count = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      count = o.count;
+      o.p = nullptr;
+      o.count = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+  void alloc(size_t c) {
+    if (c <= count && p) return;
+    release();
+    if (c == 0) return;
+    cudaError_t e = cudaMalloc(&p, c * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      throw Error(PBRL_E_RESOURCE, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    }
+    count = c;
+  }
+  void zero(cudaStream_t s) {
+    if (p) CUDA_CHECK(cudaMemsetAsync(p, 0, count * sizeof(T), s));
+  }
+  void upload(const T* h, size_t c, cudaStream_t s) {
+    CUDA_CHECK(cudaMemcpyAsync(p, h, c * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+// Per-step activations and cotangents for a batch of B rows (grown on demand).
+struct Scratch {
+  int B = 0;
+  DBuf<float> in_sa, in_s2a, sa_pi, r, d, y, tq_out, q, dq, qpi, gq, pt, ga, head, gtop;
+  DBuf<float> bs, ba, br, bs2, bd;  // staged batch
+  std::vector<DBuf<float>> tp_h, ph, pdh, tq_h, ch, dh, qh, qdh;
+  DBuf<float> x, th, ls, eps, logp, logp2, lw;
+  DBuf<uint8_t> clamped;
+};
+
+// HBM-resident replay rings (ReplayBuffer, replay.hpp:28-173).
+struct Replay {
+  int mode = PBRL_REPLAY_PER_AGENT;
+  uint64_t cap = 0;
+  int nbuf = 0, rw = 0;
+  DBuf<float> ring;             // [nbuf][cap][rw]
+  DBuf<uint64_t> sizes;         // [nbuf] min(inserts, cap)
+  std::vector<uint64_t> inserts;
+  DBuf<float> stage_rows;
+  DBuf<uint64_t> stage_dst;
+};
+
+struct Pop {
+  int algo = PBRL_ALGO_TD3, precision = PBRL_PREC_FFMA32, device = 0;
+  int n = 0, ds = 0, da = 0;
+  uint64_t member_offset = 0, n_global = 0;
+  float bound = 1.0f;
+  uint64_t seed = 0;
+  std::vector<size_t> hidden;
+  NetShape pol, cri;
+  cudaStream_t stream = nullptr;
+
+  DBuf<float> pol_p, pol_t, pol_m, pol_v, pol_g;
+  DBuf<float> cri_p, cri_t, cri_m, cri_v, cri_g;
+  DBuf<int64_t> t_pol, t_cri, t_alpha;
+  DBuf<uint64_t> steps, streams, key_a, key_b;
+  DBuf<int> fire;
+  DBuf<double> delay_acc, losses;
+  DBuf<float> log_alpha, alpha_m, alpha_v;
+  DBuf<uint8_t> mask_buf;
+
+  // hyperparameters: host doubles (reference Td3Hyper / SacHyper) + device casts
+  std::vector<std::string> fields;
+  std::vector<std::vector<double>> hyper;
+  DBuf<float> h_f0, h_f1, h_f2, h_f3, h_f4, h_f5, h_f6, h_f7;
+  DBuf<double> h_d0;
+
+  DBuf<float> corr1, corr2;
+  size_t corr_len = 0;
+  uint64_t t_bound = 0;  // upper bound of every Adam step counter
+
+  Scratch S;
+  Replay* replay = nullptr;
+
+  // PBT scratch
+  DBuf<double> pbt_fit;
+  DBuf<uint64_t> pbt_order, pbt_rep, pbt_don, pbt_src, pbt_dst;
+
+  explicit Pop(const pbrl_pop_desc& d);
+  ~Pop();
+
+  void sync();
+  int field_index(const std::string& f) const;
+  void validate_hyper() const;
+  void upload_hyper();
+  void ensure_corr(size_t need);
+  void ensure_scratch(int B);
+  void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+  void run_gemm(const GemmArgs& g);
+  void gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Operand X, float* Y,
+                long long y_gs, long long y_rs, int epi, const int* active = nullptr,
+                float* C2 = nullptr, long long c2_gs = 0, long long c2_rs = 0,
+                bool noise = false);
+  void gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Operand G,
+               Operand aux, float* DX, long long dx_gs, long long dx_rs, int epi, int col0,
+               int ncols, const int* active, float scale);
+  void gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Operand XT, Operand G,
+               const int* active);
+  void mlp_forward(const NetShape& sh, const float* W, int groups, int B, Operand x,
+                   std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_rs,
+                   int last_epi, const int* active = nullptr, float* C2 = nullptr,
+                   long long c2_gs = 0, long long c2_rs = 0, bool noise = false);
+  void mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Operand G,
+                    Operand x0t, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
+                    const int* active);
+  void critic_dx_to_action(int groups, int B, Operand G, std::vector<DBuf<float>>& hs,
+                           std::vector<DBuf<float>>& dhs, float* out, int epi, Operand aux,
+                           float scale, const int* active);
+  void critic_update(int B, const int* polyak_gate);
+  void td3_step(int B, const uint8_t* d_mask);
+  void sac_step(int B);
+  void step(int B, const uint8_t* d_mask);
+  void update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
+                      const uint8_t* policy_mask, bool device_ptrs);
+
+  // helpers for member-level access
+  float* net_row(int net, uint64_t member);
+  const NetShape& net_shape(int net) const;
+};
+
+}  // namespace pbrl

@@ -1,0 +1,699 @@
+"""Host mirror of the reference population-trainer API (proj/core, namespace pbrl).
+
+Same names, argument meanings and error behaviour as the reference C++ templates, backed by
+the B200 library through the C ABI (include/pbrl_b200.h):
+
+    make_td3_state / Td3Hyper / td3_update_step / update_k_steps        algos.hpp:32-422, :948-983
+    make_sac_state / SacHyper / sac_update_step                         algos.hpp:112-156, :470-837
+    make_synthetic_batches                                              bench.hpp:69-93
+    DeviceReplay (ReplayBuffer) / sample_batch                          replay.hpp:28-204
+    RngSequence                                                         rng.hpp:74-95
+    PBTState / pbt_rank / pbt_plan / pbt_evolve_trainer / priors        evolve.hpp:13-213
+
+State lives in HBM; numpy arrays cross the boundary only when the caller asks for them
+(flatten_member, counters, losses).  Batches may be numpy (host) or torch CUDA tensors (device).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from collections import deque
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import (ConfigError, DataStarvationError, NotReadyError, ShapeError, UsageError)
+
+PRECISIONS = {"ffma32": 0, "bf16": 1, "tf32": 2}
+NETS = {"policy": 0, "policy_target": 1, "critic1": 2, "critic2": 3, "critic1_target": 4,
+        "critic2_target": 5}
+TD3_FIELDS = ("critic_lr", "policy_lr", "policy_delay_ratio", "explore_std", "target_std",
+              "target_clip", "gamma", "tau")
+SAC_FIELDS = ("policy_lr", "critic_lr", "alpha_lr", "target_entropy", "reward_scale", "gamma",
+              "tau")
+RNG_USE = dict(kInitWeight=1, kInitBias=2, kExploreNoise=3, kTargetNoise=4, kSacEps=5,
+               kSacEpsTarget=6, kSample=7, kDonorChoice=8, kHyperDraw=9, kCemDraw=10,
+               kEnvReset=11, kGeneric=12)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+# ---------------------------------------------------------------------- RNG (rng.hpp)
+M64 = (1 << 64) - 1
+
+
+def mix64(x: int) -> int:
+    """SplitMix64 finalizer (rng.hpp:13-18)."""
+    x = (x + 0x9E3779B97F4A7C15) & M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M64
+    return x ^ (x >> 31)
+
+
+class RngStream:
+    """RngStream (rng.hpp:36-71): every draw is a pure function of (key, counter)."""
+
+    def __init__(self, key: int):
+        self.key = key & M64
+
+    @staticmethod
+    def of(seed: int, stream_id: int, use, step: int = 0) -> "RngStream":
+        use = RNG_USE[use] if isinstance(use, str) else int(use)
+        k = mix64(seed & M64)
+        k = mix64(k ^ (stream_id & M64))
+        k = mix64(k ^ use)
+        k = mix64(k ^ (step & M64))
+        return RngStream(k)
+
+    def bits(self, counter: int) -> int:
+        return mix64(self.key ^ mix64(counter & M64))
+
+    def uniform(self, counter: int, lo: float = None, hi: float = None) -> float:
+        u = float(self.bits(counter) >> 11) * 2.0 ** -53
+        return u if lo is None else lo + (hi - lo) * u
+
+
+class RngSequence:
+    """Stateful wrapper (rng.hpp:74-95); Python floats are IEEE doubles and math.exp/log are
+    the same libm calls the reference makes, so draws are bit-identical."""
+
+    def __init__(self, seed_or_stream, stream_id: int = 0, use="kGeneric", step: int = 0):
+        if isinstance(seed_or_stream, RngStream):
+            self.stream = seed_or_stream
+        else:
+            self.stream = RngStream.of(seed_or_stream, stream_id, use, step)
+        self.next = 0
+
+    def bits(self) -> int:
+        b = self.stream.bits(self.next)
+        self.next += 1
+        return b
+
+    def uniform(self, lo: float = 0.0, hi: float = 1.0) -> float:
+        v = self.stream.uniform(self.next, lo, hi)
+        self.next += 1
+        return v
+
+    def log_uniform(self, lo: float, hi: float) -> float:
+        return math.exp(self.uniform(math.log(lo), math.log(hi)))
+
+    def index(self, n: int) -> int:
+        return self.bits() % n
+
+
+# ---------------------------------------------------------------------- hyperparameters
+@dataclass
+class Td3Hyper:
+    """Per-member TD3 hyperparameters (algos.hpp:32-109)."""
+    critic_lr: List[float] = field(default_factory=list)
+    policy_lr: List[float] = field(default_factory=list)
+    policy_delay_ratio: List[float] = field(default_factory=list)
+    explore_std: List[float] = field(default_factory=list)
+    target_std: List[float] = field(default_factory=list)
+    target_clip: List[float] = field(default_factory=list)
+    gamma: List[float] = field(default_factory=list)
+    tau: List[float] = field(default_factory=list)
+    FIELDS = TD3_FIELDS
+
+    @staticmethod
+    def defaults(n: int) -> "Td3Hyper":
+        return Td3Hyper([3e-4] * n, [3e-4] * n, [0.5] * n, [0.1] * n, [0.2] * n, [0.5] * n,
+                        [0.99] * n, [0.005] * n)
+
+    def members(self) -> int:
+        return len(self.critic_lr)
+
+    def slice(self, i: int) -> "Td3Hyper":
+        return Td3Hyper(*[[getattr(self, f)[i]] for f in TD3_FIELDS])
+
+    def set_member(self, i: int, one: "Td3Hyper") -> None:
+        for f in TD3_FIELDS:
+            getattr(self, f)[i] = getattr(one, f)[0]
+
+    def validate(self, n: int) -> None:
+        for f in TD3_FIELDS:
+            if len(getattr(self, f)) != n:
+                raise ConfigError(f"Td3Hyper: {f} length != N")
+        for i in range(n):
+            if not (self.critic_lr[i] > 0) or not (self.policy_lr[i] > 0):
+                raise ConfigError("Td3Hyper: learning rates must be positive")
+            if not (0 < self.policy_delay_ratio[i] <= 1.0):
+                raise ConfigError("Td3Hyper: policy_delay_ratio must be in (0, 1]")
+            if self.explore_std[i] < 0 or self.target_std[i] < 0 or self.target_clip[i] < 0:
+                raise ConfigError("Td3Hyper: noise parameters must be >= 0")
+            if not (0.9 <= self.gamma[i] <= 1.0) and self.gamma[i] != 0.0:
+                raise ConfigError("Td3Hyper: discount must be in [0.9, 1] (or 0 in tests)")
+            if not (0 < self.tau[i] <= 1.0):
+                raise ConfigError("Td3Hyper: tau must be in (0, 1]")
+
+
+@dataclass
+class SacHyper:
+    """Per-member SAC hyperparameters (algos.hpp:112-156)."""
+    policy_lr: List[float] = field(default_factory=list)
+    critic_lr: List[float] = field(default_factory=list)
+    alpha_lr: List[float] = field(default_factory=list)
+    target_entropy: List[float] = field(default_factory=list)
+    reward_scale: List[float] = field(default_factory=list)
+    gamma: List[float] = field(default_factory=list)
+    tau: List[float] = field(default_factory=list)
+    FIELDS = SAC_FIELDS
+
+    @staticmethod
+    def defaults(n: int, action_dim: int) -> "SacHyper":
+        return SacHyper([3e-4] * n, [3e-4] * n, [3e-4] * n, [-float(action_dim)] * n, [1.0] * n,
+                        [0.99] * n, [0.005] * n)
+
+    def members(self) -> int:
+        return len(self.policy_lr)
+
+    def slice(self, i: int) -> "SacHyper":
+        return SacHyper(*[[getattr(self, f)[i]] for f in SAC_FIELDS])
+
+    def set_member(self, i: int, one: "SacHyper") -> None:
+        for f in SAC_FIELDS:
+            getattr(self, f)[i] = getattr(one, f)[0]
+
+    def validate(self, n: int) -> None:
+        for f in SAC_FIELDS:
+            if len(getattr(self, f)) != n:
+                raise ConfigError(f"SacHyper: {f} length != N")
+
+
+# ---------------------------------------------------------------------- batches
+@dataclass
+class TransitionBatch:
+    """Population batch (algos.hpp:14-24): s [N,B,ds], a [N,B,da], r [N,B,1], s2, done."""
+    s: object
+    a: object
+    r: object
+    s2: object
+    done: object
+
+    def members(self) -> int:
+        return int(self.s.shape[0])
+
+    def rows(self) -> int:
+        return int(self.s.shape[1])
+
+    def is_device(self) -> bool:
+        return hasattr(self.s, "is_cuda") and bool(self.s.is_cuda)
+
+
+def make_synthetic_batches(count: int, n: int, batch: int, obs_dim: int, act_dim: int,
+                           seed: int, device=None) -> List[TransitionBatch]:
+    """make_synthetic_batches (bench.hpp:69-93), generated on the GPU by the library.
+    Returns torch CUDA tensors on `device` (default cuda:0)."""
+    import torch
+    dev = torch.device(device if device is not None else "cuda:0")
+    shapes = [(count, n, batch, obs_dim), (count, n, batch, act_dim), (count, n, batch, 1),
+              (count, n, batch, obs_dim), (count, n, batch, 1)]
+    ts = [torch.empty(s, dtype=torch.float32, device=dev) for s in shapes]
+    with torch.cuda.device(dev):
+        _lib.call("pbrl_synthetic_batches_device", None, count, n, batch, obs_dim, act_dim, seed,
+                  C.byref(_lib.Batch(*[t.data_ptr() for t in ts])))
+        torch.cuda.synchronize(dev)
+    return [TransitionBatch(*[t[i] for t in ts]) for i in range(count)]
+
+
+def _batch_struct(b: TransitionBatch, keep: list):
+    if b.is_device():
+        arrs = [x.contiguous() for x in (b.s, b.a, b.r, b.s2, b.done)]
+        keep.extend(arrs)
+        return _lib.Batch(*[x.data_ptr() for x in arrs]), True
+    arrs = [_f32(np.asarray(x)) for x in (b.s, b.a, b.r, b.s2, b.done)]
+    keep.extend(arrs)
+    return _lib.Batch(*[x.ctypes.data for x in arrs]), False
+
+
+# ---------------------------------------------------------------------- population state
+class _Population:
+    algo = 0
+    FIELDS: Sequence[str] = ()
+
+    def __init__(self, n, obs_dim, act_dim, hidden, action_bound, seed, precision="ffma32",
+                 device=0, member_offset=0, n_global=None, mode="independent"):
+        if mode not in ("independent", "kIndependent"):
+            raise ConfigError("shared-critic mode is outside the B200 path (SURVEY.md §8(f))")
+        if precision not in PRECISIONS:
+            raise ConfigError(f"unknown precision {precision!r}")
+        self.n, self.obs_dim, self.act_dim = int(n), int(obs_dim), int(act_dim)
+        self.hidden = [int(h) for h in hidden]
+        self.seed = int(seed)
+        self.precision = precision
+        self.device = int(device)
+        self.member_offset = int(member_offset)
+        self.n_global = int(n_global or n)
+        self._action_bound = float(action_bound)
+        hid = (C.c_uint64 * max(1, len(self.hidden)))(*self.hidden)
+        desc = _lib.PopDesc(self.algo, self.n, self.obs_dim, self.act_dim, len(self.hidden),
+                            C.cast(hid, _lib.u64p), self._action_bound, self.seed,
+                            PRECISIONS[precision], self.device, self.member_offset,
+                            self.n_global)
+        h = C.c_void_p()
+        _lib.call("pbrl_pop_create", C.byref(desc), C.byref(h))
+        self._h = h
+        self._hyper_cache = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.lib().pbrl_pop_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # -- reference accessors
+    def members(self) -> int:
+        return self.n
+
+    @property
+    def handle(self):
+        return self._h
+
+    def param_count(self, net) -> int:
+        c = C.c_uint64()
+        _lib.call("pbrl_param_count", self._h, NETS.get(net, net), C.byref(c))
+        return c.value
+
+    def flatten_member(self, net, i: int) -> np.ndarray:
+        """flatten_member (net_pop.hpp:163-173) of one network."""
+        out = np.empty(self.param_count(net), np.float32)
+        _lib.call("pbrl_get_member", self._h, NETS.get(net, net), i, _ptr(out, _lib.f32p))
+        return out
+
+    def unflatten_member(self, net, i: int, vec) -> None:
+        """unflatten_member (net_pop.hpp:176-189)."""
+        vec = _f32(vec)
+        if vec.size != self.param_count(net):
+            raise ShapeError(f"unflatten_member: vector length {vec.size} != member parameter "
+                             f"count {self.param_count(net)}")
+        _lib.call("pbrl_set_member", self._h, NETS.get(net, net), i, _ptr(vec, _lib.f32p))
+
+    def copy_member(self, net, src: int, dst: int) -> None:
+        _lib.call("pbrl_copy_member", self._h, NETS.get(net, net), src, dst)
+
+    def params(self, net) -> np.ndarray:
+        return np.stack([self.flatten_member(net, i) for i in range(self.n)])
+
+    def adam(self, net, i: int):
+        P = self.param_count(net)
+        m, v = np.empty(P, np.float32), np.empty(P, np.float32)
+        t = C.c_int64()
+        _lib.call("pbrl_get_adam", self._h, NETS.get(net, net), i, _ptr(m, _lib.f32p),
+                  _ptr(v, _lib.f32p), C.byref(t))
+        return m, v, t.value
+
+    @property
+    def steps(self) -> np.ndarray:
+        st = np.empty(self.n, np.uint64)
+        _lib.call("pbrl_get_counters", self._h, None, _ptr(st, _lib.u64p))
+        return st
+
+    def last_losses(self):
+        out = [np.empty(self.n, np.float64) for _ in range(3)]
+        _lib.call("pbrl_last_losses", self._h, *[_ptr(o, _lib.f64p) for o in out])
+        return tuple(out)
+
+    def synchronize(self) -> None:
+        _lib.call("pbrl_synchronize", self._h)
+
+    def device_bytes(self) -> int:
+        b = C.c_uint64()
+        _lib.call("pbrl_device_bytes", self._h, C.byref(b))
+        return b.value
+
+    # -- hyper upload (cached: only re-sent when the host vectors change)
+    def _sync_hyper(self, hyper) -> None:
+        hyper.validate(self.n)
+        snap = tuple(tuple(float(x) for x in getattr(hyper, f)) for f in self.FIELDS)
+        if snap == self._hyper_cache:
+            return
+        for f, vals in zip(self.FIELDS, snap):
+            arr = np.asarray(vals, np.float64)
+            _lib.call("pbrl_set_hyper", self._h, f.encode(), _ptr(arr, _lib.f64p))
+        self._hyper_cache = snap
+
+    def get_hyper(self, f: str) -> np.ndarray:
+        out = np.empty(self.n, np.float64)
+        _lib.call("pbrl_get_hyper", self._h, f.encode(), _ptr(out, _lib.f64p))
+        return out
+
+    # -- updates
+    def _update(self, batches: Sequence[TransitionBatch], mask=None) -> None:
+        if not batches:
+            raise ConfigError("update_k_steps: k must be >= 1")
+        keep = []
+        structs, dev = [], None
+        rows = batches[0].rows()
+        for b in batches:
+            if b.members() != self.n:
+                raise ConfigError(f"update_step: batch population {b.members()} != state "
+                                  f"population {self.n}")
+            if b.rows() != rows:
+                raise ShapeError("all batches of one call must have the same row count")
+            s, d = _batch_struct(b, keep)
+            if dev is None:
+                dev = d
+            elif dev != d:
+                raise UsageError("mixing host and device batches in one call")
+            structs.append(s)
+        arr = (_lib.Batch * len(structs))(*structs)
+        m = None
+        if mask is not None:
+            mk = np.ascontiguousarray(np.asarray(mask, dtype=bool).astype(np.uint8))
+            keep.append(mk)
+            m = _ptr(mk, _lib.u8p)
+        fn = "pbrl_update_batches_device" if dev else "pbrl_update_batches"
+        _lib.call(fn, self._h, arr, len(structs), rows, m)
+
+    def launch_count(self) -> int:
+        c = C.c_uint64()
+        _lib.call("pbrl_launch_count", self._h, C.byref(c))
+        return c.value
+
+
+class Td3State(_Population):
+    """Td3State (algos.hpp:165-179) resident on one B200."""
+    algo = 0
+    FIELDS = TD3_FIELDS
+
+    @property
+    def action_bound(self) -> float:
+        return float(np.float32(self._action_bound))
+
+    @property
+    def delay_acc(self) -> np.ndarray:
+        d = np.empty(self.n, np.float64)
+        _lib.call("pbrl_get_counters", self._h, _ptr(d, _lib.f64p), None)
+        return d
+
+
+class SacState(_Population):
+    """SacState (algos.hpp:473-488) resident on one B200."""
+    algo = 1
+    FIELDS = SAC_FIELDS
+
+    def alpha_state(self):
+        la, m, v = (np.empty(self.n, np.float32) for _ in range(3))
+        t = np.empty(self.n, np.int64)
+        _lib.call("pbrl_get_alpha", self._h, _ptr(la, _lib.f32p), _ptr(m, _lib.f32p),
+                  _ptr(v, _lib.f32p), _ptr(t, _lib.i64p))
+        return la, m, v, t
+
+    @property
+    def log_alpha(self) -> np.ndarray:
+        return self.alpha_state()[0]
+
+
+def make_td3_state(n, obs_dim, act_dim, hidden, action_bound, seed, mode="independent",
+                   precision="ffma32", device=0, member_offset=0, n_global=None) -> Td3State:
+    """make_td3_state (algos.hpp:181-212)."""
+    return Td3State(n, obs_dim, act_dim, hidden, action_bound, seed, precision, device,
+                    member_offset, n_global, mode)
+
+
+def make_sac_state(n, obs_dim, act_dim, hidden, action_bound, seed, mode="independent",
+                   precision="ffma32", device=0, member_offset=0, n_global=None) -> SacState:
+    """make_sac_state (algos.hpp:490-521)."""
+    return SacState(n, obs_dim, act_dim, hidden, action_bound, seed, precision, device,
+                    member_offset, n_global, mode)
+
+
+def td3_update_step(st: Td3State, batch: TransitionBatch, hyper: Td3Hyper, hook=None,
+                    policy_member_mask=None) -> None:
+    """td3_update_step (algos.hpp:351-422)."""
+    if hook is not None:
+        raise ConfigError("policy-gradient hooks (DvD) are outside the B200 path")
+    st._sync_hyper(hyper)
+    st._update([batch], policy_member_mask)
+
+
+def sac_update_step(st: SacState, batch: TransitionBatch, hyper: SacHyper) -> None:
+    """sac_update_step (algos.hpp:781-837)."""
+    st._sync_hyper(hyper)
+    st._update([batch])
+
+
+def update_k_steps(st, sampler: Callable[[], Optional[TransitionBatch]], k: int, hyper) -> None:
+    """update_k_steps (algos.hpp:953-983): k chained steps, no export in between; the device
+    runs them back to back.  An exhausted sampler raises DataStarvationError."""
+    if k < 1:
+        raise ConfigError("update_k_steps: k must be >= 1")
+    batches = []
+    for i in range(k):
+        b = sampler()
+        if b is None:
+            raise DataStarvationError(f"update_k_steps: sampler exhausted after {i} of {k} steps")
+        batches.append(b)
+    st._sync_hyper(hyper)
+    st._update(batches)
+
+
+# ---------------------------------------------------------------------- replay
+@dataclass
+class Transition:
+    """Transition (replay.hpp:17-24)."""
+    s: Sequence[float]
+    a: Sequence[float]
+    s2: Sequence[float]
+    r: float = 0.0
+    done: float = 0.0
+    member: int = 0
+    seq: int = 0
+
+
+class DeviceReplay:
+    """ReplayBuffer (replay.hpp:28-173) for a whole population, resident in HBM.  Per-agent
+    mode keeps one ring per member (buffer m feeds member m); shared mode keeps one ring."""
+
+    def __init__(self, st: _Population, capacity: int, mode: str = "per_agent"):
+        self.st = st
+        self.capacity = int(capacity)
+        self.mode = mode
+        _lib.call("pbrl_replay_create", st.handle, self.capacity,
+                  0 if mode in ("per_agent", "kPerAgent") else 1)
+
+    def push(self, t: Transition) -> None:
+        if len(t.s) != self.st.obs_dim or len(t.s2) != self.st.obs_dim or \
+                len(t.a) != self.st.act_dim:
+            raise UsageError("ReplayBuffer::push: transition dims do not match buffer dims")
+        self.insert(np.asarray([t.s]), np.asarray([t.a]), np.asarray([t.r]),
+                    np.asarray([t.s2]), np.asarray([t.done]), np.asarray([t.member]))
+
+    def insert(self, s, a, r, s2, done, member) -> None:
+        """Batched push: rows in order, each to the ring of its member (per-agent mode)."""
+        s, a, r, s2, done = (_f32(x) for x in (s, a, r, s2, done))
+        member = np.ascontiguousarray(member, dtype=np.uint32)
+        cnt = member.size
+        if s.size != cnt * self.st.obs_dim or a.size != cnt * self.st.act_dim:
+            raise UsageError("ReplayBuffer::push: transition dims do not match buffer dims")
+        _lib.call("pbrl_replay_insert", self.st.handle, _ptr(s, _lib.f32p), _ptr(a, _lib.f32p),
+                  _ptr(r, _lib.f32p), _ptr(s2, _lib.f32p), _ptr(done, _lib.f32p),
+                  _ptr(member, _lib.u32p), cnt)
+
+    def size(self, buffer: int = 0) -> int:
+        c = C.c_uint64()
+        _lib.call("pbrl_replay_size", self.st.handle, buffer, C.byref(c))
+        return c.value
+
+
+def sample_batch(replay: DeviceReplay, batch_size: int, seed: int, draw_id: int,
+                 min_size: int = 1) -> Optional[TransitionBatch]:
+    """sample_batch (replay.hpp:181-204) gathered on device and returned to the host;
+    None when a source ring holds fewer than max(min_size, 1) transitions."""
+    st = replay.st
+    n, ds, da = st.n, st.obs_dim, st.act_dim
+    out = [np.empty((n, batch_size, ds), np.float32), np.empty((n, batch_size, da), np.float32),
+           np.empty((n, batch_size, 1), np.float32), np.empty((n, batch_size, ds), np.float32),
+           np.empty((n, batch_size, 1), np.float32)]
+    ready = C.c_int()
+    _lib.call("pbrl_sample_batch", st.handle, seed, draw_id, batch_size, min_size,
+              *[_ptr(o, _lib.f32p) for o in out], C.byref(ready))
+    return TransitionBatch(*out) if ready.value else None
+
+
+def update_k_from_replay(st, replay: DeviceReplay, k: int, hyper, batch_size: int, seed: int,
+                         first_draw_id: int, min_size: int = 1) -> bool:
+    """The prefetch + learner loop of run_training (pipeline_run.hpp:230-355) fused on device:
+    k x (sample_batch(draw_id = first + i) -> update step).  Returns False (nothing ran) when
+    the replay is not ready."""
+    st._sync_hyper(hyper)
+    ready = C.c_int()
+    _lib.call("pbrl_update_k", st.handle, k, seed, first_draw_id, batch_size, min_size,
+              C.byref(ready))
+    return bool(ready.value)
+
+
+# ---------------------------------------------------------------------- PBT (evolve.hpp)
+@dataclass
+class HyperRange:
+    """HyperRange (evolve.hpp:18-26)."""
+    log_scale: bool = False
+    lo: float = 0.0
+    hi: float = 1.0
+
+    def sample(self, rng: RngSequence) -> float:
+        return rng.log_uniform(self.lo, self.hi) if self.log_scale else rng.uniform(self.lo, self.hi)
+
+    def contains(self, v: float) -> bool:
+        return self.lo <= v <= self.hi
+
+
+@dataclass
+class Td3Prior:
+    """Td3Prior (evolve.hpp:31-49)."""
+    critic_lr: HyperRange = field(default_factory=lambda: HyperRange(True, 3e-5, 3e-3))
+    policy_lr: HyperRange = field(default_factory=lambda: HyperRange(True, 3e-5, 3e-3))
+    policy_delay_ratio: HyperRange = field(default_factory=lambda: HyperRange(False, 0.2, 1.0))
+    explore_std: HyperRange = field(default_factory=lambda: HyperRange(False, 0.0, 1.0))
+    target_std: HyperRange = field(default_factory=lambda: HyperRange(False, 0.0, 1.0))
+    discount: HyperRange = field(default_factory=lambda: HyperRange(False, 0.9, 1.0))
+
+    def sample_member(self, rng: RngSequence) -> Td3Hyper:
+        h = Td3Hyper.defaults(1)
+        h.critic_lr[0] = self.critic_lr.sample(rng)
+        h.policy_lr[0] = self.policy_lr.sample(rng)
+        h.policy_delay_ratio[0] = self.policy_delay_ratio.sample(rng)
+        h.explore_std[0] = self.explore_std.sample(rng)
+        h.target_std[0] = self.target_std.sample(rng)
+        h.gamma[0] = self.discount.sample(rng)
+        return h
+
+
+@dataclass
+class SacPrior:
+    """SacPrior (evolve.hpp:54-73)."""
+    policy_lr: HyperRange = field(default_factory=lambda: HyperRange(True, 3e-5, 3e-3))
+    critic_lr: HyperRange = field(default_factory=lambda: HyperRange(True, 3e-5, 3e-3))
+    alpha_lr: HyperRange = field(default_factory=lambda: HyperRange(True, 3e-5, 3e-3))
+    entropy_scale: HyperRange = field(default_factory=lambda: HyperRange(False, 0.2, 2.0))
+    reward_scale: HyperRange = field(default_factory=lambda: HyperRange(False, 0.1, 10.0))
+    discount: HyperRange = field(default_factory=lambda: HyperRange(False, 0.9, 1.0))
+    default_target_entropy: float = -1.0
+
+    def sample_member(self, rng: RngSequence) -> SacHyper:
+        h = SacHyper.defaults(1, 1)
+        h.policy_lr[0] = self.policy_lr.sample(rng)
+        h.critic_lr[0] = self.critic_lr.sample(rng)
+        h.alpha_lr[0] = self.alpha_lr.sample(rng)
+        h.target_entropy[0] = self.entropy_scale.sample(rng) * self.default_target_entropy
+        h.reward_scale[0] = self.reward_scale.sample(rng)
+        h.gamma[0] = self.discount.sample(rng)
+        return h
+
+
+class PBTState:
+    """PBTState (evolve.hpp:80-108): rolling returns per member + evolution cadence."""
+
+    def __init__(self, n: int = 0):
+        self.returns = [deque() for _ in range(n)]
+        self.ring_capacity = 10
+        self.steps_since_evolve = 0
+        self.evolve_interval = 100000
+        self.truncation_fraction = 0.3
+
+    def members(self) -> int:
+        return len(self.returns)
+
+    def record_return(self, member: int, ep_return: float) -> None:
+        ring = self.returns[member]
+        ring.append(float(ep_return))
+        while len(ring) > self.ring_capacity:
+            ring.popleft()
+
+    def every_member_scored(self) -> bool:
+        return bool(self.returns) and all(len(r) for r in self.returns)
+
+    def mean_return(self, member: int) -> float:
+        acc = 0.0
+        for v in self.returns[member]:  # std::accumulate, left to right
+            acc += v
+        return acc / float(len(self.returns[member]))
+
+    def fitness(self) -> np.ndarray:
+        if not self.every_member_scored():
+            raise NotReadyError("pbt_rank: every member needs at least one recorded return")
+        return np.asarray([self.mean_return(m) for m in range(self.members())], np.float64)
+
+
+@dataclass
+class EvolvePlan:
+    """EvolvePlan (evolve.hpp:125-128): replaced[i] copies from donors[i]."""
+    replaced: List[int]
+    donors: List[int]
+
+
+def pbt_rank(st: PBTState) -> List[int]:
+    """pbt_rank (evolve.hpp:112-122): best first, ties toward the lower index."""
+    f = st.fitness()
+    return sorted(range(len(f)), key=lambda i: (-f[i], i))
+
+
+def pbt_plan(st: PBTState, rng: RngSequence, pop: _Population) -> Optional[EvolvePlan]:
+    """pbt_plan (evolve.hpp:133-145), ranked and drawn on the device of `pop`."""
+    n = st.members()
+    if n < 4:
+        return None
+    fit = st.fitness()
+    rep = np.zeros(n, np.uint64)
+    don = np.zeros(n, np.uint64)
+    nxt = C.c_uint64(rng.next)
+    cnt = C.c_uint32()
+    _lib.call("pbrl_pbt_plan", pop.handle, _ptr(fit, _lib.f64p), n, st.truncation_fraction,
+              rng.stream.key, C.byref(nxt), _ptr(rep, _lib.u64p), _ptr(don, _lib.u64p),
+              C.byref(cnt))
+    rng.next = nxt.value
+    c = cnt.value
+    return EvolvePlan([int(x) for x in rep[:c]], [int(x) for x in don[:c]])
+
+
+def pbt_apply_returns_reset(st: PBTState, plan: EvolvePlan) -> None:
+    """pbt_apply_returns_reset (evolve.hpp:149-152)."""
+    for m in plan.replaced:
+        st.returns[m].clear()
+    st.steps_since_evolve = 0
+
+
+def pbt_evolve_trainer(st: PBTState, trainer: _Population, hyper, prior, rng: RngSequence
+                       ) -> Optional[EvolvePlan]:
+    """pbt_evolve_trainer (evolve.hpp:169-213): device ranking + donor draw, device copies of
+    every network and optimiser reset, hyper re-draw on the host (bit-exact libm)."""
+    plan = pbt_plan(st, rng, trainer)
+    if plan is None:
+        return None
+    apply_plan(trainer, plan)
+    for dst in plan.replaced:
+        hyper.set_member(dst - trainer.member_offset, prior.sample_member(rng))
+    pbt_apply_returns_reset(st, plan)
+    return plan
+
+
+def apply_plan(trainer: _Population, plan: EvolvePlan) -> None:
+    k = len(plan.replaced)
+    rep = np.asarray(plan.replaced, np.uint64)
+    don = np.asarray(plan.donors, np.uint64)
+    _lib.call("pbrl_pbt_apply", trainer.handle, _ptr(rep, _lib.u64p), _ptr(don, _lib.u64p), k)
+
+
+def member_blob_size(pop: _Population) -> int:
+    c = C.c_uint64()
+    _lib.call("pbrl_member_blob_size", pop.handle, C.byref(c))
+    return c.value
+
+
+def export_member(pop: _Population, member: int, dev_ptr: int) -> None:
+    _lib.call("pbrl_export_member", pop.handle, member, C.c_void_p(dev_ptr))
+
+
+def import_member(pop: _Population, member: int, dev_ptr: int) -> None:
+    _lib.call("pbrl_import_member", pop.handle, member, C.c_void_p(dev_ptr))
