@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Population TD3 update throughput on B200 (BASELINE.json metric: population agent-updates/s,
+TD3 pop=80, MLP 2x256, batch 256, obs 17 / act 6).
+
+One "step" = one td3_update_step of the whole population over one synthetic batch
+(make_synthetic_batches semantics, bench.hpp:69-93) -- exactly what the reference's
+bench_update times per step (bench.hpp:116-118).  Under torchrun the population is sharded in
+contiguous member blocks (80/N per GPU, RNG streams keyed by global member id), no per-step
+collective; the max over ranks of the device time is reported.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--precision P]
+
+Prints ONE JSON line (rank 0).  `value` = agent-updates/s with inputs resident in HBM (CUDA
+events on the library's stream); `e2e` = the same through the C ABI with pinned HOST batches
+(H2D of each step's batch and D2H of its losses inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: algo, total population, hidden, batch  (BASELINE.json configs)
+    "A": dict(algo="td3", pop=4, hidden=[256, 256], batch=256),
+    "B": dict(algo="td3", pop=10, hidden=[256, 256], batch=256),
+    "C": dict(algo="sac", pop=32, hidden=[256, 256], batch=256),
+    "D": dict(algo="td3", pop=80, hidden=[256, 256], batch=256),
+    "E": dict(algo="td3", pop=256, hidden=[512, 512, 512], batch=1024),
+}
+OBS, ACT, SEED = 17, 6, 7
+L2_BYTES = 126 * 2 ** 20
+METRIC = "population agent-updates/sec (TD3, pop=80) at 1/2/4/8 B200; % of roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="D", choices=sorted(CONFIGS))
+    ap.add_argument("--pop", type=int, default=None, help="override the total population")
+    ap.add_argument("--precision", default=os.environ.get("PBRL_PRECISION", "ffma32"),
+                    choices=["ffma32", "bf16", "tf32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-json", default=None, help="write the per-class profile here")
+    return ap.parse_args()
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm=d["hbm_gbs"], tensor=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    tensor_burst=d["bf16_tflops"], src="measured")
+    return dict(hbm=6650.0, tensor=1400.0, tensor_burst=1590.0, src="fallback")
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class Clocks:
+    """Samples SM clock and throttle reasons through NVML every 5 ms while the timed region
+    runs (the recipe's nvidia-smi clocks line, at a rate that resolves sub-second regions)."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.stop = gpu, [], threading.Event()
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis else self.gpu
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._loop, daemon=True)
+            self.t.start()
+        except Exception as e:  # pragma: no cover - no NVML
+            self.nv, self.err = None, str(e)
+        return self
+
+    def _loop(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.nv:
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({k for _, rs in self.rows for k, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml 5 ms"}
+
+
+# ------------------------------------------------------------------ CPU baseline (reference build)
+def cpu_reference(cfg, pop, k_steps=2, reps=3):
+    """Reference bench_update<float> vectorized (bench.hpp:137-227) on the host cores."""
+    from oracle.oracle import load_ref
+    ref = load_ref()
+    cores = os.cpu_count()
+    if ref is not None:
+        r = ref.bench_update(1, 0 if cfg["algo"] == "td3" else 1, pop, k_steps, reps,
+                             cfg["batch"], cfg["hidden"], budget=64 << 30)
+        v = pop * k_steps / (r["median_ms"] / 1e3)
+        return dict(value=v, unit="agent-updates/s", cores=cores, kind="reference",
+                    sample=f"reference bench_update<float> vectorized, pop {pop}, "
+                           f"{'x'.join(map(str, cfg['hidden']))} MLP, batch {cfg['batch']}, "
+                           f"k={k_steps} steps x {reps} reps (median), ThreadPool "
+                           f"{cores - 1} workers + caller")
+    # the reference could not be built on this host: the C restatement, single thread
+    from oracle.oracle import load_oracle, td3_defaults, sac_defaults
+    ora = load_oracle()
+    st = (ora.td3 if cfg["algo"] == "td3" else ora.sac)(pop, OBS, ACT, cfg["hidden"], 1.0, SEED)
+    hy = td3_defaults(pop) if cfg["algo"] == "td3" else sac_defaults(pop, ACT)
+    raw = ora.synthetic_batches(k_steps, pop, cfg["batch"], OBS, ACT, SEED)
+    t0 = time.perf_counter()
+    for k in range(k_steps):
+        st.step(tuple(x[k] for x in raw), hy)
+    dt = time.perf_counter() - t0
+    return dict(value=pop * k_steps / dt, unit="agent-updates/s", cores=1, kind="port",
+                sample=f"C restatement oracle, pop {pop}, k={k_steps} steps, one thread")
+
+
+def reference_arm(args, cfg, pop, rank):
+    if rank != 0:
+        return
+    k = 2 if args.steps >= 2 else 1
+    cb = cpu_reference(cfg, pop, k_steps=k, reps=3)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": cb["unit"],
+            "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": pop / cb["value"] * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (make_synthetic_batches, seed 7)",
+            "config": config_dict(args, cfg, pop, "host"),
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, cfg, pop, l2):
+    return {"workload": f"{cfg['algo'].upper()} population update, config {args.config}: "
+                        f"pop {pop}, MLP {'x'.join(map(str, cfg['hidden']))}, batch {cfg['batch']}, "
+                        f"obs {OBS} / act {ACT}",
+            "algo": cfg["algo"], "population": pop, "hidden": cfg["hidden"],
+            "batch": cfg["batch"], "obs_dim": OBS, "act_dim": ACT,
+            "parallelism": f"population shards x{args.gpus}", "precision": args.precision,
+            "l2": l2}
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    cfg = dict(CONFIGS[args.config])
+    pop = args.pop or cfg["pop"]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, cfg, pop, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2206_08888_b200 as pb
+    from paper_2206_08888_b200 import _lib
+
+    if pop % world:
+        raise SystemExit(f"population {pop} does not split over {world} GPUs")
+    n = pop // world
+    off = rank * n
+    make = pb.make_td3_state if cfg["algo"] == "td3" else pb.make_sac_state
+    st = make(n, OBS, ACT, cfg["hidden"], 1.0, SEED, precision=args.precision, device=local,
+              member_offset=off, n_global=pop)
+    hy = pb.Td3Hyper.defaults(n) if cfg["algo"] == "td3" else pb.SacHyper.defaults(n, ACT)
+    st._sync_hyper(hy)
+    L = _lib.lib()
+
+    # synthetic inputs in HBM: 50 distinct global batches (bench_update's k=50), local slice
+    nb = 50
+    gb = pb.make_synthetic_batches(nb, pop, cfg["batch"], OBS, ACT, SEED, device=dev)
+    batches = [pb.TransitionBatch(*[x[off:off + n].contiguous() for x in
+                                    (b.s, b.a, b.r, b.s2, b.done)]) for b in gb]
+    del gb
+    structs = [_lib.Batch(*[x.data_ptr() for x in (b.s, b.a, b.r, b.s2, b.done)])
+               for b in batches]
+    B = cfg["batch"]
+
+    def run(i):
+        arr = (_lib.Batch * 1)(structs[i % nb])
+        _lib.call("pbrl_update_batches_device", st.handle, arr, 1, B, None)
+
+    sp = C.c_void_p()
+    _lib.call("pbrl_get_stream", st.handle, C.byref(sp))
+    lstream = torch.cuda.ExternalStream(sp.value, device=dev)
+
+    state_bytes = st.device_bytes()
+    in_bytes = sum(x.numel() * 4 for b in batches for x in (b.s, b.a, b.r, b.s2, b.done))
+    flush = (state_bytes + in_bytes) < 2 * L2_BYTES
+    flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(args.warmup):
+        run(i)
+    st.synchronize()
+
+    # ---- timed region: K steps, device time on the library stream, max over ranks
+    K = args.steps
+    launches0 = st.launch_count()
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize(dev)
+        st.synchronize()
+        total_ms = 0.0
+        if not flush:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(lstream)
+            for i in range(K):
+                run(args.warmup + i)
+            e1.record(lstream)
+            e1.synchronize()
+            total_ms = e0.elapsed_time(e1)
+        else:
+            evs = []
+            for i in range(K):
+                with torch.cuda.stream(lstream):
+                    flush_buf.fill_(float(i))  # evict L2 between steps (outside the events)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(lstream)
+                run(args.warmup + i)
+                b.record(lstream)
+                evs.append((a, b))
+            st.synchronize()
+            total_ms = sum(a.elapsed_time(b) for a, b in evs)
+        st.synchronize()
+        torch.cuda.synchronize(dev)
+        barrier()
+    launches = st.launch_count() - launches0
+    total_ms = max_over_ranks(total_ms)
+    value = pop * K / (total_ms / 1e3)
+
+    # ---- event-instrumented pass over the same workload: per-kernel-class roofline
+    kp = min(K, 10) if K >= 2 else 1
+    _lib.call("pbrl_profile_begin", st.handle)
+    for i in range(kp):
+        run(args.warmup + K + i)
+    buf = C.create_string_buffer(1 << 16)
+    _lib.call("pbrl_profile_end", st.handle, buf, len(buf))
+    prof = json.loads(buf.value.decode())
+    if args.profile_json and rank == 0:
+        Path(args.profile_json).write_text(json.dumps(prof, indent=1))
+    pk = peaks()
+    cls = prof["classes"]
+    dom = max(cls, key=lambda c: cls[c]["ms"])
+    dc = cls[dom]
+    avg_ms = dc["ms"] / max(1, dc["launches"])
+    if dc["flops"] > 0:
+        achieved = dc["flops"] / (dc["ms"] / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tensor"], "unit": "TFLOP/s",
+                "frac": achieved / pk["tensor"]}
+    else:
+        achieved = dc["bytes"] / (dc["ms"] / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
+                "frac": achieved / pk["hbm"]}
+    tot_ms = sum(c["ms"] for c in cls.values())
+    roof.update({"traffic": None, "kernel": dom, "kernel_share_of_step": dc["ms"] / tot_ms,
+                 "avg_launch_ms": avg_ms, "peak_source": pk["src"]})
+    tfile = ROOT / "profiles" / f"traffic_{args.precision}_{args.config}.json"
+    if tfile.exists():
+        try:
+            roof["traffic"] = json.loads(tfile.read_text()).get(dom)
+        except Exception:
+            pass
+
+    # ---- e2e through the C ABI: pinned host batches, H2D + step + D2H of the losses per step
+    e2e = None
+    if not args.no_e2e:
+        hb = [[x.cpu().pin_memory() for x in (b.s, b.a, b.r, b.s2, b.done)] for b in batches[:8]]
+        hstructs = [_lib.Batch(*[x.data_ptr() for x in h]) for h in hb]
+        loss = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(3)]
+        lp = [C.cast(x.data_ptr(), _lib.f64p) for x in loss]
+        ke = max(2, min(K, 50))
+
+        def run_host(i):
+            arr = (_lib.Batch * 1)(hstructs[i % len(hstructs)])
+            _lib.call("pbrl_update_batches", st.handle, arr, 1, B, None)
+            _lib.call("pbrl_last_losses", st.handle, *lp)
+
+        run_host(0)
+        barrier()
+        st.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(lstream)
+        for i in range(ke):
+            run_host(i)
+        e1.record(lstream)
+        e1.synchronize()
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": pop * ke / (ems / 1e3), "unit": "agent-updates/s",
+               "h2d_bytes_per_step": n * B * (2 * OBS + ACT + 2) * 4,
+               "d2h_bytes_per_step": 3 * n * 8, "steps": ke}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(cfg, pop)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "agent-updates/s", "n_gpus": world,
+                "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": {"ffma32": "f32", "bf16": "bf16", "tf32": "tf32"}[args.precision],
+                "data": "synthetic (make_synthetic_batches semantics, seed 7, 50 batches in HBM)",
+                "config": config_dict(args, cfg, pop,
+                                      "flushed between steps" if flush else
+                                      f"inputs+state {(state_bytes + in_bytes) / 2**20:.0f} MiB "
+                                      f"per GPU > L2"),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "profile": {k: {kk: round(vv, 6) if isinstance(vv, float)
+                                                         else vv for kk, vv in v.items()}
+                                                     for k, v in cls.items()}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -171,9 +171,21 @@ int pbrl_synthetic_batches_device(pbrl_pop* pop, uint64_t count, uint64_t n, uin
                                   uint64_t obs_dim, uint64_t act_dim, uint64_t seed,
                                   const pbrl_batch* out);
 
+/* ---- diagnostics: the device ports of glibc tanhf (0), expf (1), log1pf (2) over a device
+ * array; used by the numerics tests to prove bit-equality with the host libm. */
+int pbrl_selftest_libm(int fn, const float* dev_in, float* dev_out, uint64_t count);
+
 /* ---- observability */
 int pbrl_launch_count(pbrl_pop* pop, uint64_t* launches); /* kernels launched (cf. kernel_invocations, pop_tensor.hpp:21-28) */
 int pbrl_synchronize(pbrl_pop* pop);
+/* The cudaStream_t every kernel of this population is launched on (for event timing). */
+int pbrl_get_stream(pbrl_pop* pop, void** stream);
+/* Event-instrumented profiling: between begin and end every launch is bracketed by CUDA events
+ * on the population stream; end writes a JSON summary per kernel class
+ * {"steps": S, "classes": {"gemm_fwd": {"launches", "ms", "flops", "bytes"}, ...}} where flops /
+ * bytes are the algorithmic work (fired members only for gated kernels). */
+int pbrl_profile_begin(pbrl_pop* pop);
+int pbrl_profile_end(pbrl_pop* pop, char* json, size_t len);
 /* Bytes of fp32 state this population keeps in HBM (params, targets, moments, replay). */
 int pbrl_device_bytes(pbrl_pop* pop, uint64_t* bytes);
 

@@ -69,7 +69,11 @@ SIGNATURES = {
     "pbrl_import_member": [vp, u64, vp],
     "pbrl_launch_count": [vp, u64p],
     "pbrl_synchronize": [vp],
+    "pbrl_get_stream": [vp, C.POINTER(vp)],
+    "pbrl_profile_begin": [vp],
+    "pbrl_profile_end": [vp, C.c_char_p, C.c_size_t],
     "pbrl_device_bytes": [vp, u64p],
+    "pbrl_selftest_libm": [C.c_int, vp, vp, u64],
     "pbrl_synthetic_batches_device": [vp, u64, u64, u64, u64, u64, u64, C.POINTER(Batch)],
 }
 

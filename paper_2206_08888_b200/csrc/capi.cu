@@ -603,6 +603,42 @@ int pbrl_synthetic_batches_device(pbrl_pop* pop, uint64_t count, uint64_t n, uin
   });
 }
 
+int pbrl_get_stream(pbrl_pop* pop, void** stream) {
+  return guarded([&] { *stream = reinterpret_cast<void*>(P(pop)->stream); });
+}
+
+int pbrl_profile_begin(pbrl_pop* pop) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    p->sync();
+    p->prof.clear();
+    p->prof_fired.clear();
+    p->prof_step = 0;
+    p->ev_used = 0;
+    p->prof_on = true;
+  });
+}
+
+int pbrl_profile_end(pbrl_pop* pop, char* json, size_t len) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    const std::string r = p->prof_report();
+    p->prof_on = false;
+    if (!json || len == 0) return;
+    std::strncpy(json, r.c_str(), len - 1);
+    json[len - 1] = '\0';
+  });
+}
+
+int pbrl_selftest_libm(int fn, const float* dev_in, float* dev_out, uint64_t count) {
+  return guarded([&] {
+    if (fn < 0 || fn > 2) PBRL_THROW(PBRL_E_USAGE, "fn: 0 tanhf, 1 expf, 2 log1pf");
+    launch_libm_selftest(fn, dev_in, dev_out, count, nullptr);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaDeviceSynchronize());
+  });
+}
+
 int pbrl_launch_count(pbrl_pop* pop, uint64_t* launches) {
   (void)pop;
   *launches = g_launches.load();

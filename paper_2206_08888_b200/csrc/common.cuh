@@ -147,6 +147,117 @@ __device__ inline float libm_tanhf(float x) {
   return jx >= 0 ? z : -z;
 }
 
+// ------------------------------------------------------------------ libm-exact expf / log1pf
+// SAC calls std::exp / std::log1p on floats (algos.hpp:527, :555, :590, :763).  glibc's expf is
+// the table-driven 2^(k/32) * poly(r) algorithm evaluated in double (x86-64 dispatches its FMA
+// build); log1pf is the fdlibm algorithm.  Both implementations below agree with the host libm on
+// all 2^32 inputs (exhaustive CPU check; device check in tests/test_gpu_numerics.py).
+__constant__ uint64_t kExp2Tab32[32] = {
+    0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
+    0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
+    0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,
+    0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,
+    0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,
+    0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,
+    0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,
+    0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull};
+
+// tab[i] = bits(2^(i/32)) - (i << 47), i.e. correctly rounded 2^(i/32) with the exponent
+// contribution removed; generated with 60-digit decimal arithmetic.
+__device__ inline float libm_expf(float x) {
+  const double InvLn2N = 0x1.71547652b82fep+0 * 32, Shift = 0x1.8p+52;
+  const double C0 = 0x1.c6af84b912394p-5 / 32 / 32 / 32, C1 = 0x1.ebfce50fac4f3p-3 / 32 / 32,
+               C2 = 0x1.62e42ff0c52d6p-1 / 32;
+  const double xd = static_cast<double>(x);
+  const uint32_t abstop = (fbits(x) >> 20) & 0x7ff;
+  if (abstop >= (fbits(88.0f) >> 20)) {
+    if (fbits(x) == 0xff800000u) return 0.0f;
+    if (abstop >= (0x7f800000u >> 20)) return x + x;
+    if (x > 0x1.62e42ep6f) return __int_as_float(0x7f800000);
+    if (x < -0x1.9fe368p6f) return 0.0f;
+  }
+  double kd = fma(InvLn2N, xd, Shift);
+  const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
+  kd -= Shift;
+  const double r = fma(InvLn2N, xd, -kd);
+  uint64_t t = kExp2Tab32[ki % 32];
+  t += ki << (52 - 5);
+  const double s = __longlong_as_double(static_cast<long long>(t));
+  const double z = fma(C0, r, C1);
+  const double r2 = r * r;
+  double y = fma(C2, r, 1.0);
+  y = fma(z, r2, y);
+  y = y * s;
+  return static_cast<float>(y);
+}
+
+__device__ inline float libm_log1pf(float x) {
+  const float ln2_hi = 6.9313812256e-01f, ln2_lo = 9.0580006145e-06f, two25 = 3.355443200e+07f,
+              Lp1 = 6.6666668653e-01f, Lp2 = 4.0000000596e-01f, Lp3 = 2.8571429849e-01f,
+              Lp4 = 2.2222198546e-01f, Lp5 = 1.8183572590e-01f, Lp6 = 1.5313838422e-01f,
+              Lp7 = 1.4798198640e-01f, zero = 0.0f;
+  float hfsq, f = 0.0f, c = 0.0f, s, z, R, u;
+  int32_t k, hu = 0;
+  const int32_t hx = static_cast<int32_t>(fbits(x));
+  const int32_t ax = hx & 0x7fffffff;
+  k = 1;
+  if (hx < 0x3ed413d7) {
+    if (ax >= 0x3f800000) {
+      if (x == -1.0f) return -two25 / zero;
+      return (x - x) / (x - x);
+    }
+    if (ax < 0x31000000) {
+      if (ax < 0x24800000) return x;
+      return x - x * x * 0.5f;
+    }
+    if (hx > 0 || hx <= static_cast<int32_t>(0xbe95f61f)) {
+      k = 0;
+      f = x;
+      hu = 1;
+    }
+  }
+  if (hx >= 0x7f800000) return x + x;
+  if (k != 0) {
+    if (hx < 0x5a000000) {
+      u = 1.0f + x;
+      hu = static_cast<int32_t>(fbits(u));
+      k = (hu >> 23) - 127;
+      c = (k > 0) ? 1.0f - (u - x) : x - (u - 1.0f);
+      c /= u;
+    } else {
+      u = x;
+      hu = static_cast<int32_t>(fbits(u));
+      k = (hu >> 23) - 127;
+      c = 0;
+    }
+    hu &= 0x007fffff;
+    if (hu < 0x3504f7) {
+      u = bitsf(static_cast<uint32_t>(hu) | 0x3f800000u);
+    } else {
+      k += 1;
+      u = bitsf(static_cast<uint32_t>(hu) | 0x3f000000u);
+      hu = (0x00800000 - hu) >> 2;
+    }
+    f = u - 1.0f;
+  }
+  hfsq = 0.5f * f * f;
+  if (hu == 0) {
+    if (f == zero) {
+      if (k == 0) return zero;
+      c += k * ln2_lo;
+      return k * ln2_hi + c;
+    }
+    R = hfsq * (1.0f - 0.66666666666666666f * f);
+    if (k == 0) return f - R;
+    return k * ln2_hi - ((R - (k * ln2_lo + c)) - f);
+  }
+  s = f / (2.0f + f);
+  z = s * s;
+  R = z * (Lp1 + z * (Lp2 + z * (Lp3 + z * (Lp4 + z * (Lp5 + z * (Lp6 + z * Lp7))))));
+  if (k == 0) return f - (hfsq - s * (hfsq + R));
+  return k * ln2_hi - ((hfsq - (s * (hfsq + R) + (k * ln2_lo + c))) - f);
+}
+
 // std::clamp / std::min / std::max comparison order (libstdc++)
 __device__ __forceinline__ float clampf_ref(float v, float lo, float hi) {
   return v < lo ? lo : (hi < v ? hi : v);

@@ -338,14 +338,21 @@ void launch_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2, 
                                                    seed, key_eps, key_eps_t);
 }
 
-// glibc-compatible float transcendentals for SAC: exp/log1p evaluated in double and rounded
-// (glibc's expf is within 0.502 ulp; log1pf is the fdlibm algorithm) -- agreement is
-// near-bitwise, and SAC parity is stated with a tolerance.
-__device__ __forceinline__ float sac_expf(float x) {
-  return static_cast<float>(exp(static_cast<double>(x)));
+// glibc-exact float transcendentals for SAC (common.cuh)
+__device__ __forceinline__ float sac_expf(float x) { return libm_expf(x); }
+__device__ __forceinline__ float sac_log1pf(float x) { return libm_log1pf(x); }
+
+// diagnostics: device libm ports over a host array (tests/test_gpu_numerics.py)
+__global__ void k_libm_selftest(int fn, const float* in, float* out, uint64_t count) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const float x = in[i];
+    out[i] = fn == 0 ? libm_tanhf(x) : (fn == 1 ? libm_expf(x) : libm_log1pf(x));
+  }
 }
-__device__ __forceinline__ float sac_log1pf(float x) {
-  return static_cast<float>(log1p(static_cast<double>(x)));
+
+void launch_libm_selftest(int fn, const float* in, float* out, uint64_t count, cudaStream_t s) {
+  k_libm_selftest<<<148 * 8, 256, 0, s>>>(fn, in, out, count);
 }
 
 // log_one_minus_tanh_sq (algos.hpp:523-529)

@@ -356,7 +356,7 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
     g.noise_clip = h_f3.p;
     g.bound = bound;
   }
-  run_gemm(g);
+  run_gemm(g, PC_GEMM_FWD);
 }
 
 // dX of layer l restricted to input columns [col0, col0+ncols): DX = epi(G W_l^T)
@@ -382,7 +382,7 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
   g.acc_init = 0.0f;
   g.active = active;
   g.scale = scale;
-  run_gemm(g);
+  run_gemm(g, PC_GEMM_DX);
 }
 
 // dW_l and db_l (as the ones row) into the gradient arena: [X;1]^T G
@@ -403,12 +403,85 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Opera
   g.epi = EPI_STORE;
   g.acc_init = 0.0f;
   g.active = active;
-  run_gemm(g);
+  run_gemm(g, PC_GEMM_DW);
 }
 
-void Pop::run_gemm(const GemmArgs& g) {
-  launch_gemm_simt(g, stream);
-  count_launch(1);
+void Pop::run_gemm(const GemmArgs& g, int cls) {
+  // algorithmic FLOPs: the bias ones-row of dW is bookkeeping, not work
+  const int M = g.a_ones_row ? g.M - 1 : g.M;
+  timed(cls, 2.0 * M * g.N * g.K * g.groups, 0.0, g.active != nullptr,
+        [&] { launch_gemm_simt(g, stream); });
+}
+
+// ------------------------------------------------------------------ profiling
+cudaEvent_t Pop::prof_event() {
+  if (ev_used == ev_pool.size()) {
+    cudaEvent_t e;
+    CUDA_CHECK(cudaEventCreate(&e));
+    ev_pool.push_back(e);
+  }
+  return ev_pool[ev_used++];
+}
+
+void Pop::prof_begin(cudaEvent_t* a) {
+  if (!prof_on) return;
+  *a = prof_event();
+  CUDA_CHECK(cudaEventRecord(*a, stream));
+}
+
+void Pop::prof_end(cudaEvent_t a, int cls, double flops, double bytes, int gated) {
+  if (!prof_on) return;
+  cudaEvent_t b = prof_event();
+  CUDA_CHECK(cudaEventRecord(b, stream));
+  prof.push_back(ProfRec{cls, flops, bytes, gated, prof_step, a, b, 0.0});
+}
+
+// critic targets are Polyak-updated only for fired members in TD3: extra gated bytes
+void Pop::prof_add_gated_bytes(double bytes) {
+  if (prof_on && !prof.empty()) prof.back().gbytes += bytes;
+}
+
+void Pop::prof_step_done() {
+  if (!prof_on) return;
+  int nf = n;
+  if (algo == PBRL_ALGO_TD3) {
+    std::vector<int> f(n);
+    CUDA_CHECK(cudaMemcpyAsync(f.data(), fire.p, 4 * n, cudaMemcpyDeviceToHost, stream));
+    sync();
+    nf = 0;
+    for (int v : f) nf += v;
+  }
+  prof_fired.push_back(nf);
+  ++prof_step;
+}
+
+std::string Pop::prof_report() {
+  sync();
+  static const char* names[PC_COUNT] = {"gemm_fwd", "gemm_dx", "gemm_dw", "adam_polyak",
+                                        "elementwise", "gather_pack"};
+  double ms[PC_COUNT] = {}, fl[PC_COUNT] = {}, by[PC_COUNT] = {};
+  long long cnt[PC_COUNT] = {};
+  for (const ProfRec& r : prof) {
+    float t = 0.0f;
+    CUDA_CHECK(cudaEventElapsedTime(&t, r.a, r.b));
+    const double frac = (r.gated && r.step < static_cast<int>(prof_fired.size()))
+                            ? static_cast<double>(prof_fired[r.step]) / n : 1.0;
+    ms[r.cls] += t;
+    fl[r.cls] += r.flops * frac;
+    by[r.cls] += r.bytes * frac;
+    if (r.gbytes > 0.0 && r.step < static_cast<int>(prof_fired.size()))
+      by[r.cls] += r.gbytes * static_cast<double>(prof_fired[r.step]) / n;
+    cnt[r.cls] += 1;
+  }
+  std::string out = "{\"steps\": " + std::to_string(prof_step) + ", \"classes\": {";
+  for (int c = 0; c < PC_COUNT; ++c) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "%s\"%s\": {\"launches\": %lld, \"ms\": %.6f, \"flops\": %.6e, "
+             "\"bytes\": %.6e}", c ? ", " : "", names[c], cnt[c], ms[c], fl[c], by[c]);
+    out += buf;
+  }
+  out += "}}";
+  return out;
 }
 
 // ------------------------------------------------------------------ critic update (shared)
@@ -425,8 +498,7 @@ void Pop::critic_update(int B, const int* polyak_gate) {
     gemm_fwd(cri, cri_p.p, l, n2, B, x, out, nbB * h, h, last ? EPI_BIAS : EPI_BIAS_RELU);
     x = fwd_in(out, nbB * h, h, 0);
   }
-  launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
   Operand G = fwd_in(S.dq.p, nbB, 1, 0);
   for (int l = L - 1; l >= 0; --l) {
     Operand xt = (l == 0) ? as_kmajor_t(S.in_sa.p, nbB * dsa, dsa, 1)
@@ -441,9 +513,12 @@ void Pop::critic_update(int B, const int* polyak_gate) {
     }
   }
   const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
-  launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
-              corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, stream);
-  count_launch(1);
+  timed(PC_ADAM, 0.0, static_cast<double>(cri.P) * (n2) * 28.0, 0,
+        [&] { launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
+              corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, stream); });
+  // fused target Polyak: +8 B/param (read + write target), every member (SAC) or fired (TD3)
+  if (polyak_gate) prof_add_gated_bytes(8.0 * cri.P * n2);
+  else if (prof_on && !prof.empty()) prof.back().bytes += 8.0 * cri.P * n2;
 }
 
 // forward of `sh` (groups x B rows) from input operand x; hidden activations into hs[l]
@@ -506,16 +581,14 @@ void Pop::critic_dx_to_action(int groups, int B, Operand G, std::vector<DBuf<flo
 void Pop::td3_step(int B, const uint8_t* d_mask) {
   const int dsa = ds + da;
   const long long nbB = B;
-  launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p, t_cri.p + n,
-                        steps.p, streams.p, seed, key_a.p, stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p, t_cri.p + n,
+                        steps.p, streams.p, seed, key_a.p, stream); });
   // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
   mlp_forward(pol, pol_t.p, n, B, fwd_in(S.in_s2a.p, nbB * dsa, dsa, 0), S.tp_h, S.in_s2a.p + ds,
               nbB * dsa, dsa, EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true);
   mlp_forward(cri, cri_t.p, 2 * n, B, fwd_in(S.in_s2a.p, nbB * dsa, dsa, 1), S.tq_h, S.tq_out.p,
               nbB, 1, EPI_BIAS);
-  launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
   // twin critic update; target Polyak fused for members whose policy fires (:401-418)
   critic_update(B, fire.p);
   // td3_policy_loss_grads (:318-338) on the UPDATED critic1, gated by the fire mask
@@ -523,16 +596,15 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
               nbB * dsa, dsa, EPI_BIAS_TANH, fire.p, S.pt.p, nbB * da, da);
   mlp_forward(cri, cri_p.p, n, B, fwd_in(S.sa_pi.p, nbB * dsa, dsa, 0), S.qh, S.qpi.p, nbB, 1,
               EPI_BIAS, fire.p);
-  launch_td3_policy_loss(n, B, S.qpi.p, fire.p, losses.p + 2 * n, S.gq.p, stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_td3_policy_loss(n, B, S.qpi.p, fire.p, losses.p + 2 * n, S.gq.p, stream); });
   Operand aux_t = fwd_in(S.pt.p, nbB * da, da, 0);
   critic_dx_to_action(n, B, fwd_in(S.gq.p, nbB, 1, 0), S.qh, S.qdh, S.gtop.p, EPI_TANH_GRAD,
                       aux_t, pol.out_scale, fire.p);
   mlp_backward(pol, pol_p.p, pol_g.p, n, B, fwd_in(S.gtop.p, nbB * da, da, 0),
                as_kmajor_t(S.in_sa.p, nbB * dsa, dsa, 0), S.ph, S.pdh, fire.p);
-  launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
-              corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, stream);
-  count_launch(1);
+  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * (n) * (28.0 + 8.0), 1,
+        [&] { launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
+              corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, stream); });
 }
 
 // ------------------------------------------------------------------ SAC step (algos.hpp:781-837)
@@ -540,45 +612,38 @@ void Pop::sac_step(int B) {
   const int dsa = ds + da, L = pol.depth;
   const long long nbB = B;
   const int hd = pol.dims[L];
-  launch_sac_step_begin(n, t_pol.p, t_cri.p, t_cri.p + n, t_alpha.p, steps.p, streams.p, seed,
-                        key_a.p, key_b.p, stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_step_begin(n, t_pol.p, t_cri.p, t_cri.p + n, t_alpha.p, steps.p, streams.p, seed,
+                        key_a.p, key_b.p, stream); });
   // sac_critic_target (algos.hpp:739-776): current policy on s2, eps' draws, twin targets
   mlp_forward(pol, pol_p.p, n, B, fwd_in(S.in_s2a.p, nbB * dsa, dsa, 0), S.tp_h, S.head.p,
               nbB * hd, hd, EPI_BIAS);
-  launch_sac_head(n, B, ds, da, S.head.p, key_b.p, bound, S.in_s2a.p, nullptr, nullptr, nullptr,
-                  nullptr, nullptr, S.logp2.p, stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_head(n, B, ds, da, S.head.p, key_b.p, bound, S.in_s2a.p, nullptr, nullptr, nullptr,
+                  nullptr, nullptr, S.logp2.p, stream); });
   mlp_forward(cri, cri_t.p, 2 * n, B, fwd_in(S.in_s2a.p, nbB * dsa, dsa, 1), S.tq_h, S.tq_out.p,
               nbB, 1, EPI_BIAS);
-  launch_sac_y(n, B, S.r.p, S.d.p, S.tq_out.p, S.logp2.p, log_alpha.p, h_f4.p, h_f3.p, S.y.p,
-               stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_y(n, B, S.r.p, S.d.p, S.tq_out.p, S.logp2.p, log_alpha.p, h_f4.p, h_f3.p, S.y.p,
+               stream); });
   critic_update(B, nullptr);  // critic targets tracked every step (:827-834)
   // sac_policy_loss_grads (:643-735) through both UPDATED critics
   mlp_forward(pol, pol_p.p, n, B, fwd_in(S.in_sa.p, nbB * dsa, dsa, 0), S.ph, S.head.p, nbB * hd,
               hd, EPI_BIAS);
-  launch_sac_head(n, B, ds, da, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p, S.ls.p,
-                  S.clamped.p, S.eps.p, S.logp.p, stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_head(n, B, ds, da, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p, S.ls.p,
+                  S.clamped.p, S.eps.p, S.logp.p, stream); });
   mlp_forward(cri, cri_p.p, 2 * n, B, fwd_in(S.sa_pi.p, nbB * dsa, dsa, 1), S.qh, S.qpi.p, nbB, 1,
               EPI_BIAS);
-  launch_sac_policy_top(n, B, S.qpi.p, S.logp.p, log_alpha.p, losses.p + 2 * n, S.gq.p, S.lw.p,
-                        stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_policy_top(n, B, S.qpi.p, S.logp.p, log_alpha.p, losses.p + 2 * n, S.gq.p, S.lw.p,
+                        stream); });
   critic_dx_to_action(2 * n, B, fwd_in(S.gq.p, nbB, 1, 0), S.qh, S.qdh, S.ga.p, EPI_STORE,
                       Operand{}, 1.0f, nullptr);
-  launch_sac_head_grad(n, B, da, S.ga.p, S.lw.p, S.x.p, S.th.p, S.ls.p, S.clamped.p, S.eps.p,
-                       bound, S.gtop.p, stream);
-  count_launch(1);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_head_grad(n, B, da, S.ga.p, S.lw.p, S.x.p, S.th.p, S.ls.p, S.clamped.p, S.eps.p,
+                       bound, S.gtop.p, stream); });
   mlp_backward(pol, pol_p.p, pol_g.p, n, B, fwd_in(S.gtop.p, nbB * hd, hd, 0),
                as_kmajor_t(S.in_sa.p, nbB * dsa, dsa, 0), S.ph, S.pdh, nullptr);
-  launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
-              corr2.p, h_f0.p, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
-  count_launch(1);
-  launch_sac_alpha(n, B, S.logp.p, log_alpha.p, h_d0.p, log_alpha.p, alpha_m.p, alpha_v.p,
-                   t_alpha.p, corr1.p, corr2.p, h_f2.p, stream);
-  count_launch(1);
+  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * (n) * (28.0 + 0.0), 0,
+        [&] { launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
+              corr2.p, h_f0.p, nullptr, nullptr, nullptr, nullptr, nullptr, stream); });
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_alpha(n, B, S.logp.p, log_alpha.p, h_d0.p, log_alpha.p, alpha_m.p, alpha_v.p,
+                   t_alpha.p, corr1.p, corr2.p, h_f2.p, stream); });
 }
 
 void Pop::step(int B, const uint8_t* d_mask) {
@@ -586,7 +651,9 @@ void Pop::step(int B, const uint8_t* d_mask) {
   if (algo == PBRL_ALGO_TD3) td3_step(B, d_mask);
   else sac_step(B);
   t_bound += 1;
+  prof_step_done();
 }
+
 
 // ------------------------------------------------------------------ update entry points
 void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
@@ -623,9 +690,8 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
       s2 = S.bs2.p;
       d = S.bd.p;
     }
-    launch_pack_batch(n, B, ds, da, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
-                      S.d.p, stream);
-    count_launch(1);
+    timed(PC_GATHER, 0.0, 0.0, 0, [&] { launch_pack_batch(n, B, ds, da, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
+                      S.d.p, stream); });
     step(B, d_mask);
   }
   CUDA_CHECK(cudaGetLastError());

@@ -156,6 +156,8 @@ void launch_member_zero(float* arena, size_t stride, const uint64_t* dst, int pa
 void launch_synth(uint64_t count, uint64_t n, uint64_t b, uint64_t ds, uint64_t da, uint64_t seed,
                   float* s, float* a, float* r, float* s2, float* d, cudaStream_t st);
 
+void launch_libm_selftest(int fn, const float* in, float* out, uint64_t count, cudaStream_t s);
+
 // init (init_pop_mlp, net_pop.hpp:69-100)
 void launch_init_net(const NetShape& sh, float* arena, int n, uint64_t member_offset,
                      uint64_t seed, cudaStream_t s);

@@ -80,6 +80,18 @@ struct Replay {
   DBuf<uint64_t> stage_dst;
 };
 
+// Event-instrumented profiling of one update program (bench.py's roofline numbers): every
+// launch is bracketed by events on the population stream and tagged with its algorithmic work.
+enum ProfClass { PC_GEMM_FWD = 0, PC_GEMM_DX, PC_GEMM_DW, PC_ADAM, PC_ELEM, PC_GATHER, PC_COUNT };
+struct ProfRec {
+  int cls;
+  double flops, bytes;
+  int gated;  // work scales with the number of fired members
+  int step;
+  cudaEvent_t a, b;
+  double gbytes;  // extra bytes that scale with the fired fraction (gated Polyak)
+};
+
 struct Pop {
   int algo = PBRL_ALGO_TD3, precision = PBRL_PREC_FFMA32, device = 0;
   int n = 0, ds = 0, da = 0;
@@ -112,6 +124,27 @@ struct Pop {
   Scratch S;
   Replay* replay = nullptr;
 
+  bool prof_on = false;
+  int prof_step = 0;
+  std::vector<ProfRec> prof;
+  std::vector<int> prof_fired;  // fired members per profiled step (TD3)
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t prof_event();
+  void prof_begin(cudaEvent_t* a);
+  void prof_end(cudaEvent_t a, int cls, double flops, double bytes, int gated);
+  void prof_step_done();
+  std::string prof_report();
+  void prof_add_gated_bytes(double bytes);
+  template <typename F>
+  void timed(int cls, double flops, double bytes, int gated, F&& f) {
+    cudaEvent_t a = nullptr;
+    prof_begin(&a);
+    f();
+    count_launch(1);
+    prof_end(a, cls, flops, bytes, gated);
+  }
+
   // PBT scratch
   DBuf<double> pbt_fit;
   DBuf<uint64_t> pbt_order, pbt_rep, pbt_don, pbt_src, pbt_dst;
@@ -127,7 +160,7 @@ struct Pop {
   void ensure_scratch(int B);
   void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
-  void run_gemm(const GemmArgs& g);
+  void run_gemm(const GemmArgs& g, int cls);
   void gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Operand X, float* Y,
                 long long y_gs, long long y_rs, int epi, const int* active = nullptr,
                 float* C2 = nullptr, long long c2_gs = 0, long long c2_rs = 0,
