@@ -175,6 +175,12 @@ int pbrl_synthetic_batches_device(pbrl_pop* pop, uint64_t count, uint64_t n, uin
  * array; used by the numerics tests to prove bit-equality with the host libm. */
 int pbrl_selftest_libm(int fn, const float* dev_in, float* dev_out, uint64_t count);
 
+/* C[g](i,j) = sum_k A[g](i,k) B[g](k,j) on the tcgen05 path (TF32), fp32 device operands.
+ * a_mn: A stored [g][K][M] (else [g][M][K]); b_mn: B stored [g][K][N] (else [g][N][K]). */
+int pbrl_selftest_tc_gemm(int a_mn, int b_mn, int M, int N, int K, int groups, const float* A,
+                          long long a_ld, long long a_gs, const float* B, long long b_ld,
+                          long long b_gs, float* C, long long c_ld, long long c_gs);
+
 /* ---- observability */
 int pbrl_launch_count(pbrl_pop* pop, uint64_t* launches); /* kernels launched (cf. kernel_invocations, pop_tensor.hpp:21-28) */
 int pbrl_synchronize(pbrl_pop* pop);

@@ -74,6 +74,9 @@ SIGNATURES = {
     "pbrl_profile_end": [vp, C.c_char_p, C.c_size_t],
     "pbrl_device_bytes": [vp, u64p],
     "pbrl_selftest_libm": [C.c_int, vp, vp, u64],
+    "pbrl_selftest_tc_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
+                              C.c_longlong, C.c_longlong, vp, C.c_longlong, C.c_longlong, vp,
+                              C.c_longlong, C.c_longlong],
     "pbrl_synthetic_batches_device": [vp, u64, u64, u64, u64, u64, u64, C.POINTER(Batch)],
 }
 

@@ -6,6 +6,7 @@
 #include <unordered_map>
 
 #include "pop_impl.cuh"
+#include "tc_gemm.cuh"
 
 namespace pbrl {
 
@@ -372,7 +373,7 @@ bool replay_ready(Pop* p, uint64_t min_size) {
 
 void gather(Pop* p, int B, uint64_t seed, uint64_t draw_id) {
   Replay* r = p->replay;
-  launch_replay_gather(p->n, B, p->ds, p->da, r->rw, r->ring.p, r->cap,
+  launch_replay_gather(p->n, B, p->ds, p->da, p->lsa, r->rw, r->ring.p, r->cap,
                        r->mode == PBRL_REPLAY_SHARED, r->sizes.p, p->streams.p, seed, draw_id,
                        p->S.in_sa.p, p->S.in_s2a.p, p->S.sa_pi.p, p->S.r.p, p->S.d.p, p->stream);
   p->count_launch(1);
@@ -390,7 +391,7 @@ int pbrl_sample_batch(pbrl_pop* pop, uint64_t seed, uint64_t draw_id, uint64_t r
     p->ensure_scratch(B);
     gather(p, B, seed, draw_id);
     const size_t nb = static_cast<size_t>(p->n) * B;
-    const int dsa = p->ds + p->da;
+    const int dsa = p->lsa;
     std::vector<float> sa(nb * dsa), s2a(nb * dsa);
     CUDA_CHECK(cudaMemcpyAsync(sa.data(), p->S.in_sa.p, 4 * nb * dsa, cudaMemcpyDeviceToHost, p->stream));
     CUDA_CHECK(cudaMemcpyAsync(s2a.data(), p->S.in_s2a.p, 4 * nb * dsa, cudaMemcpyDeviceToHost, p->stream));
@@ -634,6 +635,34 @@ int pbrl_selftest_libm(int fn, const float* dev_in, float* dev_out, uint64_t cou
   return guarded([&] {
     if (fn < 0 || fn > 2) PBRL_THROW(PBRL_E_USAGE, "fn: 0 tanhf, 1 expf, 2 log1pf");
     launch_libm_selftest(fn, dev_in, dev_out, count, nullptr);
+    CUDA_CHECK(cudaGetLastError());
+    CUDA_CHECK(cudaDeviceSynchronize());
+  });
+}
+
+int pbrl_selftest_tc_gemm(int a_mn, int b_mn, int M, int N, int K, int groups, const float* A,
+                          long long a_ld, long long a_gs, const float* B, long long b_ld,
+                          long long b_gs, float* C, long long c_ld, long long c_gs) {
+  return guarded([&] {
+    TcOperand a{A, static_cast<uint64_t>(a_mn ? M : K), static_cast<uint64_t>(a_mn ? K : M),
+                static_cast<uint64_t>(groups), static_cast<uint64_t>(a_ld),
+                static_cast<uint64_t>(a_gs)};
+    TcOperand b{B, static_cast<uint64_t>(b_mn ? N : K), static_cast<uint64_t>(b_mn ? K : N),
+                static_cast<uint64_t>(groups), static_cast<uint64_t>(b_ld),
+                static_cast<uint64_t>(b_gs)};
+    if (!tma_ok(A, a_ld, a_gs) || !tma_ok(B, b_ld, b_gs))
+      PBRL_THROW(PBRL_E_SHAPE, "operands are not TMA-aligned");
+    TcArgs g;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.groups = groups;
+    g.n_members = groups;
+    g.epi = EPI_STORE;
+    g.C = C;
+    g.c_gs = c_gs;
+    g.c_rs = c_ld;
+    launch_tc_gemm(a, b, a_mn != 0, b_mn != 0, g, nullptr);
     CUDA_CHECK(cudaGetLastError());
     CUDA_CHECK(cudaDeviceSynchronize());
   });

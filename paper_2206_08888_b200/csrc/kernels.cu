@@ -9,10 +9,50 @@ namespace pbrl {
 // ================================================================== grouped SIMT GEMM
 // Reference order: every output accumulates its products in ascending k in fp32 without FMA
 // (pop_tensor.hpp:155-166 forward, :194-206 backward), so results are bit-identical to the CPU.
+// Shared fused epilogue of the CUDA-core GEMM family (operation order = the reference's).
+__device__ __forceinline__ float simt_epilogue(const GemmArgs& g, float v, int gi, int gj, int grp,
+                                               int mem, const float* bias, const float* aux) {
+  switch (g.epi) {
+    case EPI_BIAS: v = v + bias[gj]; break;
+    case EPI_BIAS_RELU: {
+      const float z = v + bias[gj];
+      v = z > 0.0f ? z : 0.0f;
+      break;
+    }
+    case EPI_BIAS_TANH:
+    case EPI_BIAS_TANH_NOISE: {
+      const float t = libm_tanhf(v + bias[gj]);
+      if (g.C2) g.C2[grp * g.c2_gs + gi * g.c2_rs + gj] = t;
+      v = (g.scale != 1.0f) ? t * g.scale : t;
+      if (g.epi == EPI_BIAS_TANH_NOISE) {
+        // algos.hpp:252-262: eps = clamp((T)normal * sd, +-clip); a = clamp(a + eps, +-bound)
+        const uint64_t e = static_cast<uint64_t>(gi) * g.N + gj;
+        float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
+                    g.noise_sd[mem];
+        eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+        v = clampf_ref(v + eps, -g.bound, g.bound);
+      }
+      break;
+    }
+    case EPI_RELU_MASK:
+      if (!(aux[gi * g.aux.rs + gj * g.aux.cs] > 0.0f)) v = 0.0f;
+      break;
+    case EPI_TANH_GRAD: {
+      if (g.scale != 1.0f) v = v * g.scale;
+      const float t = aux[gi * g.aux.rs + gj * g.aux.cs];
+      v = v * (1.0f - t * t);
+      break;
+    }
+    default: break;
+  }
+  return v;
+}
+
 template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     k_gemm_simt(const GemmArgs g) {
   constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY, BK = 16;
+  constexpr int A_PER = BK * BM / NT, B_PER = (BK * BN + NT - 1) / NT;
   const int grp = blockIdx.z;
   const int mem = grp % g.n_members;
   if (g.active && !g.active[mem]) return;
@@ -23,30 +63,69 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   const float* B = g.B.p + (g.B.by_member ? mem : grp) * g.B.gs;
   const int tid = threadIdx.x;
   const int ty = tid / TX, tx = tid % TX;
+  const bool a_kc = g.A.cs == 1, b_nc = g.B.cs == 1;
   float acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = g.acc_init;
 
-  for (int k0 = 0; k0 < g.K; k0 += BK) {
-    for (int e = tid; e < BK * BM; e += NT) {
+  // register double buffering: the next K-chunk's global loads are in flight while the
+  // current chunk is multiplied out of shared memory
+  float ra[A_PER], rb[B_PER];
+  auto a_pos = [&](int e, int& kk, int& ii) {
+    if (a_kc) { kk = e % BK; ii = e / BK; } else { ii = e % BM; kk = e / BM; }
+  };
+  auto b_pos = [&](int e, int& kk, int& jj) {
+    if (b_nc) { jj = e % BN; kk = e / BN; } else { kk = e % BK; jj = e / BK; }
+  };
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < A_PER; ++q) {
       int kk, ii;
-      if (g.A.cs == 1) { kk = e % BK; ii = e / BK; } else { ii = e % BM; kk = e / BM; }
+      a_pos(tid + q * NT, kk, ii);
       const int gi = i0 + ii, gk = k0 + kk;
       float v = 0.0f;
-      if (gi < g.M && gk < g.K) {
+      if (gi < g.M && gk < g.K)
         v = (g.a_ones_row && gi == g.M - 1) ? 1.0f : A[gi * g.A.rs + gk * g.A.cs];
+      ra[q] = v;
+    }
+#pragma unroll
+    for (int q = 0; q < B_PER; ++q) {
+      const int e = tid + q * NT;
+      float v = 0.0f;
+      if (e < BK * BN) {
+        int kk, jj;
+        b_pos(e, kk, jj);
+        const int gj = j0 + jj, gk = k0 + kk;
+        if (gj < g.N && gk < g.K) v = B[gk * g.B.rs + gj * g.B.cs];
       }
-      As[kk][ii] = v;
+      rb[q] = v;
     }
-    for (int e = tid; e < BK * BN; e += NT) {
-      int kk, jj;
-      if (g.B.cs == 1) { jj = e % BN; kk = e / BN; } else { kk = e % BK; jj = e / BK; }
-      const int gj = j0 + jj, gk = k0 + kk;
-      Bs[kk][jj] = (gj < g.N && gk < g.K) ? B[gk * g.B.rs + gj * g.B.cs] : 0.0f;
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int q = 0; q < A_PER; ++q) {
+      int kk, ii;
+      a_pos(tid + q * NT, kk, ii);
+      As[kk][ii] = ra[q];
     }
+#pragma unroll
+    for (int q = 0; q < B_PER; ++q) {
+      const int e = tid + q * NT;
+      if (e < BK * BN) {
+        int kk, jj;
+        b_pos(e, kk, jj);
+        Bs[kk][jj] = rb[q];
+      }
+    }
+  };
+
+  load(0);
+  for (int k0 = 0; k0 < g.K; k0 += BK) {
+    stash();
     __syncthreads();
+    if (k0 + BK < g.K) load(k0 + BK);
     const int kmax = min(BK, g.K - k0);
     for (int kk = 0; kk < kmax; ++kk) {
       float a[TM], b[TN];
@@ -73,41 +152,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     for (int j = 0; j < TN; ++j) {
       const int gj = j0 + tx + j * TX;
       if (gj >= g.N) continue;
-      float v = acc[i][j];
-      switch (g.epi) {
-        case EPI_BIAS: v = v + bias[gj]; break;
-        case EPI_BIAS_RELU: {
-          const float z = v + bias[gj];
-          v = z > 0.0f ? z : 0.0f;
-          break;
-        }
-        case EPI_BIAS_TANH:
-        case EPI_BIAS_TANH_NOISE: {
-          const float t = libm_tanhf(v + bias[gj]);
-          if (g.C2) g.C2[grp * g.c2_gs + gi * g.c2_rs + gj] = t;
-          v = (g.scale != 1.0f) ? t * g.scale : t;
-          if (g.epi == EPI_BIAS_TANH_NOISE) {
-            // algos.hpp:252-262: eps = clamp((T)normal * sd, +-clip); a = clamp(a + eps, +-bound)
-            const uint64_t e = static_cast<uint64_t>(gi) * g.N + gj;
-            float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
-                        g.noise_sd[mem];
-            eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
-            v = clampf_ref(v + eps, -g.bound, g.bound);
-          }
-          break;
-        }
-        case EPI_RELU_MASK:
-          if (!(aux[gi * g.aux.rs + gj * g.aux.cs] > 0.0f)) v = 0.0f;
-          break;
-        case EPI_TANH_GRAD: {
-          if (g.scale != 1.0f) v = v * g.scale;
-          const float t = aux[gi * g.aux.rs + gj * g.aux.cs];
-          v = v * (1.0f - t * t);
-          break;
-        }
-        default: break;
-      }
-      C[gi * g.c_rs + gj] = v;
+      C[gi * g.c_rs + gj] = simt_epilogue(g, acc[i][j], gi, gj, grp, mem, bias, aux);
     }
   }
 }
@@ -115,7 +160,7 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0 || g.N <= 0 || g.groups <= 0) return;
   if (g.N <= 16) {
-    constexpr int BM = 128, BN = 16, TM = 4, TN = 2;
+    constexpr int BM = 64, BN = 16, TM = 2, TN = 2;
     dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.groups);
     k_gemm_simt<BM, BN, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, s>>>(g);
   } else {
@@ -123,6 +168,212 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
     dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.groups);
     k_gemm_simt<BM, BN, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, s>>>(g);
   }
+}
+
+// ------------------------------------------------------------------ skinny products
+// The output layers of the MLPs have N (forward, dW) or K (dX) of 1 (critic) or 6 / 12 (policy).
+// These get dedicated CUDA-core kernels with the same ascending-k accumulation (bit-exact in the
+// FFMA32 mode) and memory-friendly thread mappings.
+
+// forward, N <= 16: one thread per output row; the X tile is staged through shared memory
+// (coalesced), W [K][N] lives in shared memory; acc[o] runs k = 0..K-1.
+template <int NMAX>
+__global__ void __launch_bounds__(128) k_fwd_skinny(const GemmArgs g) {
+  constexpr int ROWS = 128, KC = 32;
+  const int grp = blockIdx.y;
+  const int mem = grp % g.n_members;
+  if (g.active && !g.active[mem]) return;
+  __shared__ float Xs[ROWS][KC + 1];
+  __shared__ float Ws[KC][NMAX];
+  const float* A = g.A.p + (g.A.by_member ? mem : grp) * g.A.gs;
+  const float* Bm = g.B.p + (g.B.by_member ? mem : grp) * g.B.gs;
+  const int r0 = blockIdx.x * ROWS, tid = threadIdx.x;
+  float acc[NMAX];
+#pragma unroll
+  for (int o = 0; o < NMAX; ++o) acc[o] = g.acc_init;
+  for (int k0 = 0; k0 < g.K; k0 += KC) {
+    const int kc = min(KC, g.K - k0);
+    for (int e = tid; e < ROWS * KC; e += ROWS) {
+      const int rr = e / KC, kk = e % KC;
+      const int row = r0 + rr;
+      Xs[rr][kk] = (row < g.M && kk < kc) ? A[row * g.A.rs + (k0 + kk) * g.A.cs] : 0.0f;
+    }
+    for (int e = tid; e < KC * NMAX; e += ROWS) {
+      const int kk = e / NMAX, o = e % NMAX;
+      Ws[kk][o] = (kk < kc && o < g.N) ? Bm[(k0 + kk) * g.B.rs + o * g.B.cs] : 0.0f;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < kc; ++kk) {
+      const float x = Xs[tid][kk];
+#pragma unroll
+      for (int o = 0; o < NMAX; ++o) acc[o] = acc[o] + x * Ws[kk][o];
+    }
+    __syncthreads();
+  }
+  const int row = r0 + tid;
+  if (row >= g.M) return;
+  float* C = g.C + (g.c_by_member ? mem : grp) * g.c_gs;
+  const float* bias = g.bias.p ? g.bias.p + (g.bias.by_member ? mem : grp) * g.bias.gs : nullptr;
+  const float* aux = g.aux.p ? g.aux.p + (g.aux.by_member ? mem : grp) * g.aux.gs : nullptr;
+#pragma unroll
+  for (int o = 0; o < NMAX; ++o) {
+    if (o < g.N) C[row * g.c_rs + o] = simt_epilogue(g, acc[o], row, o, grp, mem, bias, aux);
+  }
+}
+
+// dX with K <= 16 (through the output layer): one thread per (row, column), columns fastest, so
+// the relu-mask reads and the stores are coalesced; G rows are warp-broadcast.
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_dx_skinny(const GemmArgs g) {
+  constexpr int RPB = 8;  // rows per block
+  const int grp = blockIdx.z;
+  const int mem = grp % g.n_members;
+  if (g.active && !g.active[mem]) return;
+  const float* A = g.A.p + (g.A.by_member ? mem : grp) * g.A.gs;
+  const float* Bm = g.B.p + (g.B.by_member ? mem : grp) * g.B.gs;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= g.N) return;
+  float w[KMAX];
+#pragma unroll
+  for (int o = 0; o < KMAX; ++o) w[o] = (o < g.K) ? Bm[o * g.B.rs + j * g.B.cs] : 0.0f;
+  float* C = g.C + (g.c_by_member ? mem : grp) * g.c_gs;
+  const float* aux = g.aux.p ? g.aux.p + (g.aux.by_member ? mem : grp) * g.aux.gs : nullptr;
+  const int r0 = blockIdx.y * RPB;
+  for (int rr = 0; rr < RPB; ++rr) {
+    const int row = r0 + rr;
+    if (row >= g.M) break;
+    float acc = g.acc_init;
+#pragma unroll
+    for (int o = 0; o < KMAX; ++o)
+      if (o < g.K) acc = acc + A[row * g.A.rs + o * g.A.cs] * w[o];
+    C[row * g.c_rs + j] = simt_epilogue(g, acc, row, j, grp, mem, nullptr, aux);
+  }
+}
+
+// dW with N <= 16 (+ bias as the ones row): one thread per input feature i; x = X[b][i] is
+// coalesced across threads, G[b][o] is warp-broadcast; acc[o] runs b = 0..B-1.
+template <int NMAX>
+__global__ void __launch_bounds__(128) k_dw_skinny(const GemmArgs g) {
+  const int grp = blockIdx.y;
+  const int mem = grp % g.n_members;
+  if (g.active && !g.active[mem]) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.M) return;
+  const float* A = g.A.p + (g.A.by_member ? mem : grp) * g.A.gs;
+  const float* Bm = g.B.p + (g.B.by_member ? mem : grp) * g.B.gs;
+  const bool ones = g.a_ones_row && i == g.M - 1;
+  float acc[NMAX];
+#pragma unroll
+  for (int o = 0; o < NMAX; ++o) acc[o] = g.acc_init;
+  for (int b = 0; b < g.K; ++b) {
+    const float x = ones ? 1.0f : A[i * g.A.rs + b * g.A.cs];
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o)
+      if (o < g.N) acc[o] = acc[o] + x * Bm[b * g.B.rs + o * g.B.cs];
+  }
+  float* C = g.C + (g.c_by_member ? mem : grp) * g.c_gs;
+#pragma unroll
+  for (int o = 0; o < NMAX; ++o)
+    if (o < g.N) C[i * g.c_rs + o] = acc[o];
+}
+
+// Output-layer backward in one pass (N_out <= 16): for the layer y = X W + b with cotangent G,
+//   dW[i][o] = sum_b X[b][i] G[b][o]      (b ascending, from +0: pop_tensor.hpp:194-206)
+//   db[o]    = sum_b G[b][o]              (b ascending: :244-246)
+//   dX[b][i] = X[b][i] > 0 ? sum_o G[b][o] W[i][o] : 0   (o ascending; relu' of the layer below)
+// One block per (group, 256 input features); thread = input feature i, G staged in shared memory,
+// rows processed 8 at a time with the X loads batched.
+template <int NOUT>
+__global__ void __launch_bounds__(256) k_out_backward(OutBwdArgs a) {
+  extern __shared__ float Gs[];  // [B][NOUT]
+  const int grp = blockIdx.y;
+  const int mem = grp % a.n_members;
+  if (a.active && !a.active[mem]) return;
+  const float* X = a.X + (a.x_by_member ? mem : grp) * a.x_gs;
+  const float* G = a.G + grp * a.g_gs;
+  const float* W = a.W + grp * a.w_gs;
+  for (int e = threadIdx.x; e < a.B * NOUT; e += blockDim.x) {
+    const int b = e / NOUT, o = e % NOUT;
+    Gs[e] = o < a.nout ? G[static_cast<long long>(b) * a.g_ld + o] : 0.0f;
+  }
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  float* dW = a.dW + grp * a.dw_gs;
+  if (i < NOUT && blockIdx.x == 0 && i < a.nout) {  // bias gradient
+    float acc = 0.0f;
+    for (int b = 0; b < a.B; ++b) acc += Gs[b * NOUT + i];
+    dW[static_cast<long long>(a.H) * a.nout + i] = acc;
+  }
+  if (i >= a.H) return;
+  float w[NOUT], acc[NOUT];
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) {
+    w[o] = o < a.nout ? W[static_cast<long long>(i) * a.nout + o] : 0.0f;
+    acc[o] = 0.0f;
+  }
+  float* dX = a.dX ? a.dX + grp * a.dx_gs : nullptr;
+  for (int b0 = 0; b0 < a.B; b0 += 8) {
+    float x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      x[u] = (b0 + u < a.B) ? X[static_cast<long long>(b0 + u) * a.x_ld + i] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int b = b0 + u;
+      if (b >= a.B) break;
+      const float* g = Gs + b * NOUT;
+      float d = 0.0f;
+#pragma unroll
+      for (int o = 0; o < NOUT; ++o) {
+        if (o < a.nout) {
+          acc[o] = acc[o] + x[u] * g[o];
+          d = d + g[o] * w[o];
+        }
+      }
+      if (dX) dX[static_cast<long long>(b) * a.dx_ld + i] = (x[u] > 0.0f) ? d : 0.0f;
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o)
+    if (o < a.nout) dW[static_cast<long long>(i) * a.nout + o] = acc[o];
+}
+
+void launch_out_backward(const OutBwdArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_out_backward<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_out_backward<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    attr = true;
+  }
+  dim3 grid((a.H + 255) / 256, a.groups);
+  if (a.nout <= 1) {
+    k_out_backward<1><<<grid, 256, a.B * 1 * 4, s>>>(a);
+  } else if (a.nout <= 8) {
+    k_out_backward<8><<<grid, 256, a.B * 8 * 4, s>>>(a);
+  } else {
+    k_out_backward<16><<<grid, 256, a.B * 16 * 4, s>>>(a);
+  }
+}
+
+void launch_fwd_skinny(const GemmArgs& g, cudaStream_t s) {
+  dim3 grid((g.M + 127) / 128, g.groups);
+  if (g.N <= 1) k_fwd_skinny<1><<<grid, 128, 0, s>>>(g);
+  else if (g.N <= 8) k_fwd_skinny<8><<<grid, 128, 0, s>>>(g);
+  else k_fwd_skinny<16><<<grid, 128, 0, s>>>(g);
+}
+
+void launch_dx_skinny(const GemmArgs& g, cudaStream_t s) {
+  dim3 grid((g.N + 255) / 256, (g.M + 7) / 8, g.groups);
+  if (g.K <= 1) k_dx_skinny<1><<<grid, 256, 0, s>>>(g);
+  else if (g.K <= 8) k_dx_skinny<8><<<grid, 256, 0, s>>>(g);
+  else k_dx_skinny<16><<<grid, 256, 0, s>>>(g);
+}
+
+void launch_dw_skinny(const GemmArgs& g, cudaStream_t s) {
+  dim3 grid((g.M + 127) / 128, g.groups);
+  if (g.N <= 1) k_dw_skinny<1><<<grid, 128, 0, s>>>(g);
+  else if (g.N <= 8) k_dw_skinny<8><<<grid, 128, 0, s>>>(g);
+  else k_dw_skinny<16><<<grid, 128, 0, s>>>(g);
 }
 
 // ================================================================== TD3 step bookkeeping
@@ -159,9 +410,10 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts
-__global__ void k_pack_batch(int n, int B, int ds, int da, const float* s, const float* a,
-                             const float* r, const float* s2, const float* d, float* in_sa,
-                             float* in_s2a, float* sa_pi, float* r_out, float* d_out) {
+__global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float* s,
+                             const float* a, const float* r, const float* s2, const float* d,
+                             float* in_sa, float* in_s2a, float* sa_pi, float* r_out,
+                             float* d_out) {
   const int dsa = ds + da;
   const long long rows = static_cast<long long>(n) * B;
   const long long total = rows * dsa;
@@ -169,13 +421,14 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, const float* s, const
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long row = e / dsa;
     const int c = static_cast<int>(e % dsa);
+    const long long o = row * lsa + c;
     if (c < ds) {
       const float sv = s[row * ds + c];
-      in_sa[e] = sv;
-      sa_pi[e] = sv;
-      in_s2a[e] = s2[row * ds + c];
+      in_sa[o] = sv;
+      sa_pi[o] = sv;
+      in_s2a[o] = s2[row * ds + c];
     } else {
-      in_sa[e] = a[row * da + (c - ds)];
+      in_sa[o] = a[row * da + (c - ds)];
     }
     if (c == 0) {
       r_out[row] = r[row];
@@ -184,13 +437,13 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, const float* s, const
   }
 }
 
-void launch_pack_batch(int n, int B, int ds, int da, const float* s, const float* a,
+void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, float* in_sa,
                        float* in_s2a, float* sa_pi, float* r_out, float* d_out, cudaStream_t st) {
   const long long total = static_cast<long long>(n) * B * (ds + da);
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-  k_pack_batch<<<blocks, 256, 0, st>>>(n, B, ds, da, s, a, r, s2, d, in_sa, in_s2a, sa_pi, r_out,
-                                       d_out);
+  k_pack_batch<<<blocks, 256, 0, st>>>(n, B, ds, da, lsa, s, a, r, s2, d, in_sa, in_s2a, sa_pi,
+                                       r_out, d_out);
 }
 
 // y = r + gamma*(1-done)*min(Q1', Q2')   (algos.hpp:268-281)
@@ -305,6 +558,47 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
                                   tau_a, tau_b, polyak_gate);
 }
 
+// bias gradient for the tensor-core dW path: column sums of G over the batch, two-level and
+// deterministic (32 columns x 8 row segments per block, segments combined in a fixed order).
+__global__ void __launch_bounds__(256) k_colsum(int n, int B, int N, const float* G, long long g_gs,
+                                                long long g_ld, float* dst, long long dst_gs,
+                                                const int* active) {
+  const int grp = blockIdx.y;
+  if (active && !active[grp % n]) return;
+  __shared__ float part[8][33];
+  const int c = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  const int o = blockIdx.x * 32 + c;
+  const int rows = (B + 7) / 8;
+  const int b0 = seg * rows, b1 = min(B, b0 + rows);
+  float acc = 0.0f;
+  if (o < N) {
+    const float* g = G + grp * g_gs + o;
+    int b = b0;
+    for (; b + 8 <= b1; b += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = g[static_cast<long long>(b + u) * g_ld];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; b < b1; ++b) acc += g[static_cast<long long>(b) * g_ld];
+  }
+  part[seg][c] = acc;
+  __syncthreads();
+  if (seg == 0 && o < N) {
+    float t = part[0][c];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += part[q][c];
+    dst[grp * dst_gs + o] = t;
+  }
+}
+
+void launch_colsum(int groups, int n, int B, int N, const float* G, long long g_gs, long long g_ld,
+                   float* dst, long long dst_gs, const int* active, cudaStream_t s) {
+  dim3 grid((N + 31) / 32, groups);
+  k_colsum<<<grid, 256, 0, s>>>(n, B, N, G, g_gs, g_ld, dst, dst_gs, active);
+}
+
 __global__ void k_fill(float* p, size_t count, float v) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -363,7 +657,7 @@ __device__ __forceinline__ float l1mts(float x) {
 }
 
 // split_policy_head + draw_eps + tanh_gaussian_logprob + tanh squash (algos.hpp:534-629)
-__global__ void k_sac_head(int n, int B, int ds, int da, const float* head, const uint64_t* key,
+__global__ void k_sac_head(int n, int B, int ds, int da, int lsa, const float* head, const uint64_t* key,
                            float bound, float log_bound, float* sa, float* x, float* th,
                            float* ls_out, uint8_t* clamped, float* eps_out, float* logp) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;  // (m, b)
@@ -392,16 +686,16 @@ __global__ void k_sac_head(int n, int B, int ds, int da, const float* head, cons
     if (ls_out) ls_out[k] = ls;
     if (clamped) clamped[k] = c;
     if (eps_out) eps_out[k] = ep;
-    sa[static_cast<long long>(e) * (ds + da) + ds + j] = t * bound;
+    sa[static_cast<long long>(e) * lsa + ds + j] = t * bound;
   }
   logp[e] = acc;
 }
 
-void launch_sac_head(int n, int B, int ds, int da, const float* head, const uint64_t* key,
-                     float bound, float* sa, float* x, float* th, float* ls, uint8_t* clamped,
-                     float* eps, float* logp, cudaStream_t s) {
+void launch_sac_head(int n, int B, int ds, int da, int lsa, const float* head,
+                     const uint64_t* key, float bound, float* sa, float* x, float* th, float* ls,
+                     uint8_t* clamped, float* eps, float* logp, cudaStream_t s) {
   extern float host_logf(float);
-  k_sac_head<<<(n * B + 127) / 128, 128, 0, s>>>(n, B, ds, da, head, key, bound, host_logf(bound),
+  k_sac_head<<<(n * B + 127) / 128, 128, 0, s>>>(n, B, ds, da, lsa, head, key, bound, host_logf(bound),
                                                  sa, x, th, ls, clamped, eps, logp);
 }
 
@@ -544,7 +838,7 @@ void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t 
 // sample_batch (replay.hpp:181-204): slot = bits(key, b) % size with key =
 // RngStream::of(seed, streams[m], kSample, draw_id); one warp gathers one row (coalesced 4 B
 // lanes over the row) straight into the critic-input layouts.
-__global__ void k_replay_gather(int n, int B, int ds, int da, int rw, const float* ring,
+__global__ void k_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const float* ring,
                                 uint64_t cap, int shared, const uint64_t* sizes,
                                 const uint64_t* streams, uint64_t seed, uint64_t draw_id,
                                 float* in_sa, float* in_s2a, float* sa_pi, float* r_out,
@@ -558,7 +852,7 @@ __global__ void k_replay_gather(int n, int B, int ds, int da, int rw, const floa
   const uint64_t slot = rng_bits(key, static_cast<uint64_t>(b)) % sizes[buf];
   const float* row = ring + (static_cast<uint64_t>(buf) * cap + slot) * rw;
   const int dsa = ds + da;
-  const long long o = static_cast<long long>(warp) * dsa;
+  const long long o = static_cast<long long>(warp) * lsa;
   for (int c = lane; c < 2 * ds + da + 2; c += 32) {
     const float v = row[c];
     if (c < ds) {
@@ -576,14 +870,14 @@ __global__ void k_replay_gather(int n, int B, int ds, int da, int rw, const floa
   }
 }
 
-void launch_replay_gather(int n, int B, int ds, int da, int rw, const float* ring,
+void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const float* ring,
                           uint64_t cap, int shared, const uint64_t* sizes,
                           const uint64_t* streams, uint64_t seed, uint64_t draw_id,
                           float* in_sa, float* in_s2a, float* sa_pi, float* r_out, float* d_out,
                           cudaStream_t s) {
   const long long warps = static_cast<long long>(n) * B;
   const int blocks = static_cast<int>((warps * 32 + 255) / 256);
-  k_replay_gather<<<blocks, 256, 0, s>>>(n, B, ds, da, rw, ring, cap, shared, sizes, streams,
+  k_replay_gather<<<blocks, 256, 0, s>>>(n, B, ds, da, lsa, rw, ring, cap, shared, sizes, streams,
                                          seed, draw_id, in_sa, in_s2a, sa_pi, r_out, d_out);
 }
 

@@ -46,9 +46,10 @@ Pop::Pop(const pbrl_pop_desc& d) {
   if (d.n < 1) PBRL_THROW(PBRL_E_CONFIG, "population size must be >= 1");
   if (d.obs_dim < 1 || d.act_dim < 1) PBRL_THROW(PBRL_E_CONFIG, "obs_dim/act_dim must be >= 1");
   if (d.n_hidden > kMaxLayers - 1) PBRL_THROW(PBRL_E_CONFIG, "too many hidden layers");
-  if (d.precision != PBRL_PREC_FFMA32 && d.precision != PBRL_PREC_BF16 &&
-      d.precision != PBRL_PREC_TF32)
-    PBRL_THROW(PBRL_E_CONFIG, "unknown precision mode");
+  if (d.precision != PBRL_PREC_FFMA32 && d.precision != PBRL_PREC_TF32)
+    PBRL_THROW(PBRL_E_CONFIG, d.precision == PBRL_PREC_BF16
+                                  ? "bf16 operands are not built in this version (use tf32)"
+                                  : "unknown precision mode");
   algo = d.algo;
   precision = d.precision;
   device = d.device;
@@ -150,6 +151,8 @@ Pop::Pop(const pbrl_pop_desc& d) {
 }
 
 Pop::~Pop() {
+  invalidate_graphs();
+  for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
@@ -232,6 +235,7 @@ void Pop::ensure_corr(size_t need) {
     c1[t] = static_cast<float>(1.0 - std::pow(0.9, static_cast<double>(t)));
     c2[t] = static_cast<float>(1.0 - std::pow(0.999, static_cast<double>(t)));
   }
+  invalidate_graphs();
   corr1.alloc(len);
   corr2.alloc(len);
   corr1.upload(c1.data(), len, stream);
@@ -246,11 +250,12 @@ void Pop::ensure_scratch(int B) {
   S = Scratch{};
   S.B = B;
   const size_t nb = static_cast<size_t>(n) * B;
-  const int dsa = ds + da;
   const int L = pol.depth;
-  S.in_sa.alloc(nb * dsa);
-  S.in_s2a.alloc(nb * dsa);
-  S.sa_pi.alloc(nb * dsa);
+  // row strides padded to 4 floats: every activation is a legal TMA source (16 B strides)
+  lsa = pad4(ds + da);
+  S.in_sa.alloc(nb * lsa);
+  S.in_s2a.alloc(nb * lsa);
+  S.sa_pi.alloc(nb * lsa);
   S.r.alloc(nb);
   S.d.alloc(nb);
   S.y.alloc(nb);
@@ -262,30 +267,22 @@ void Pop::ensure_scratch(int B) {
   S.pt.alloc(nb * da);
   S.ga.alloc(2 * nb * da);
   S.head.alloc(nb * pol.dims[L]);
-  S.gtop.alloc(nb * pol.dims[L]);
+  S.gtop.alloc(nb * pad4(pol.dims[L]));
   S.bs.alloc(nb * ds);
   S.ba.alloc(nb * da);
   S.br.alloc(nb);
   S.bs2.alloc(nb * ds);
   S.bd.alloc(nb);
   for (int l = 0; l + 1 < L; ++l) {
-    const size_t h = static_cast<size_t>(pol.dims[l + 1]);
-    S.tp_h.emplace_back();
-    S.tp_h.back().alloc(nb * h);
-    S.ph.emplace_back();
-    S.ph.back().alloc(nb * h);
-    S.pdh.emplace_back();
-    S.pdh.back().alloc(nb * h);
-    S.tq_h.emplace_back();
-    S.tq_h.back().alloc(2 * nb * h);
-    S.ch.emplace_back();
-    S.ch.back().alloc(2 * nb * h);
-    S.dh.emplace_back();
-    S.dh.back().alloc(2 * nb * h);
-    S.qh.emplace_back();
-    S.qh.back().alloc(2 * nb * h);
-    S.qdh.emplace_back();
-    S.qdh.back().alloc(2 * nb * h);
+    const size_t h = static_cast<size_t>(pad4(pol.dims[l + 1]));
+    for (auto* v : {&S.tp_h, &S.ph, &S.pdh}) {
+      v->emplace_back();
+      v->back().alloc(nb * h);
+    }
+    for (auto* v : {&S.tq_h, &S.ch, &S.dh, &S.qh, &S.qdh}) {
+      v->emplace_back();
+      v->back().alloc(2 * nb * h);
+    }
   }
   if (algo == PBRL_ALGO_SAC) {
     S.x.alloc(nb * da);
@@ -297,363 +294,12 @@ void Pop::ensure_scratch(int B) {
     S.lw.alloc(nb);
     S.clamped.alloc(nb * da);
   }
+  // fresh buffers: zero so never-written padding columns cannot carry NaN bit patterns
+  for (auto* b : {&S.in_sa, &S.in_s2a, &S.sa_pi, &S.gtop}) b->zero(stream);
+  for (auto* v : {&S.tp_h, &S.ph, &S.pdh, &S.tq_h, &S.ch, &S.dh, &S.qh, &S.qdh})
+    for (auto& b : *v) b.zero(stream);
+  invalidate_graphs();
 }
-
-// ------------------------------------------------------------------ GEMM builders
-namespace {
-Operand fwd_in(const float* p, long long gs, long long ld, int by_member) {
-  Operand o;
-  o.p = p;
-  o.gs = gs;
-  o.rs = ld;
-  o.cs = 1;
-  o.by_member = by_member;
-  return o;
-}
-Operand as_kmajor_t(const float* p, long long gs, long long ld, int by_member) {
-  // X^T for dW: A(i = feature, k = row) = X[k*ld + i]
-  Operand o;
-  o.p = p;
-  o.gs = gs;
-  o.rs = 1;
-  o.cs = ld;
-  o.by_member = by_member;
-  return o;
-}
-}  // namespace
-
-// forward of layer l: Y = act(X W_l + b_l)
-void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Operand X,
-                   float* Y, long long y_gs, long long y_rs, int epi, const int* active,
-                   float* C2, long long c2_gs, long long c2_rs, bool noise) {
-  GemmArgs g;
-  g.M = B;
-  g.N = sh.dims[l + 1];
-  g.K = sh.dims[l];
-  g.groups = groups;
-  g.n_members = n;
-  g.A = X;
-  g.B.p = W + sh.woff[l];
-  g.B.gs = static_cast<long long>(sh.stride);
-  g.B.rs = sh.dims[l + 1];
-  g.B.cs = 1;
-  g.bias.p = W + sh.boff[l];
-  g.bias.gs = static_cast<long long>(sh.stride);
-  g.bias.cs = 1;
-  g.C = Y;
-  g.c_gs = y_gs;
-  g.c_rs = y_rs;
-  g.epi = epi;
-  g.acc_init = -0.0f;
-  g.active = active;
-  g.C2 = C2;
-  g.c2_gs = c2_gs;
-  g.c2_rs = c2_rs;
-  g.scale = sh.out_scale;
-  if (noise) {
-    g.noise_key = key_a.p;
-    g.noise_sd = h_f2.p;
-    g.noise_clip = h_f3.p;
-    g.bound = bound;
-  }
-  run_gemm(g, PC_GEMM_FWD);
-}
-
-// dX of layer l restricted to input columns [col0, col0+ncols): DX = epi(G W_l^T)
-void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Operand G,
-                  Operand aux, float* DX, long long dx_gs, long long dx_rs, int epi, int col0,
-                  int ncols, const int* active, float scale) {
-  GemmArgs g;
-  g.M = B;
-  g.N = ncols;
-  g.K = sh.dims[l + 1];
-  g.groups = groups;
-  g.n_members = n;
-  g.A = G;
-  g.B.p = W + sh.woff[l] + static_cast<size_t>(col0) * sh.dims[l + 1];
-  g.B.gs = static_cast<long long>(sh.stride);
-  g.B.rs = 1;
-  g.B.cs = sh.dims[l + 1];
-  g.C = DX;
-  g.c_gs = dx_gs;
-  g.c_rs = dx_rs;
-  g.epi = epi;
-  g.aux = aux;
-  g.acc_init = 0.0f;
-  g.active = active;
-  g.scale = scale;
-  run_gemm(g, PC_GEMM_DX);
-}
-
-// dW_l and db_l (as the ones row) into the gradient arena: [X;1]^T G
-void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Operand XT, Operand G,
-                  const int* active) {
-  GemmArgs g;
-  g.M = sh.dims[l] + 1;
-  g.N = sh.dims[l + 1];
-  g.K = B;
-  g.groups = groups;
-  g.n_members = n;
-  g.A = XT;
-  g.a_ones_row = 1;
-  g.B = G;
-  g.C = Gr + sh.woff[l];
-  g.c_gs = static_cast<long long>(sh.stride);
-  g.c_rs = sh.dims[l + 1];
-  g.epi = EPI_STORE;
-  g.acc_init = 0.0f;
-  g.active = active;
-  run_gemm(g, PC_GEMM_DW);
-}
-
-void Pop::run_gemm(const GemmArgs& g, int cls) {
-  // algorithmic FLOPs: the bias ones-row of dW is bookkeeping, not work
-  const int M = g.a_ones_row ? g.M - 1 : g.M;
-  timed(cls, 2.0 * M * g.N * g.K * g.groups, 0.0, g.active != nullptr,
-        [&] { launch_gemm_simt(g, stream); });
-}
-
-// ------------------------------------------------------------------ profiling
-cudaEvent_t Pop::prof_event() {
-  if (ev_used == ev_pool.size()) {
-    cudaEvent_t e;
-    CUDA_CHECK(cudaEventCreate(&e));
-    ev_pool.push_back(e);
-  }
-  return ev_pool[ev_used++];
-}
-
-void Pop::prof_begin(cudaEvent_t* a) {
-  if (!prof_on) return;
-  *a = prof_event();
-  CUDA_CHECK(cudaEventRecord(*a, stream));
-}
-
-void Pop::prof_end(cudaEvent_t a, int cls, double flops, double bytes, int gated) {
-  if (!prof_on) return;
-  cudaEvent_t b = prof_event();
-  CUDA_CHECK(cudaEventRecord(b, stream));
-  prof.push_back(ProfRec{cls, flops, bytes, gated, prof_step, a, b, 0.0});
-}
-
-// critic targets are Polyak-updated only for fired members in TD3: extra gated bytes
-void Pop::prof_add_gated_bytes(double bytes) {
-  if (prof_on && !prof.empty()) prof.back().gbytes += bytes;
-}
-
-void Pop::prof_step_done() {
-  if (!prof_on) return;
-  int nf = n;
-  if (algo == PBRL_ALGO_TD3) {
-    std::vector<int> f(n);
-    CUDA_CHECK(cudaMemcpyAsync(f.data(), fire.p, 4 * n, cudaMemcpyDeviceToHost, stream));
-    sync();
-    nf = 0;
-    for (int v : f) nf += v;
-  }
-  prof_fired.push_back(nf);
-  ++prof_step;
-}
-
-std::string Pop::prof_report() {
-  sync();
-  static const char* names[PC_COUNT] = {"gemm_fwd", "gemm_dx", "gemm_dw", "adam_polyak",
-                                        "elementwise", "gather_pack"};
-  double ms[PC_COUNT] = {}, fl[PC_COUNT] = {}, by[PC_COUNT] = {};
-  long long cnt[PC_COUNT] = {};
-  for (const ProfRec& r : prof) {
-    float t = 0.0f;
-    CUDA_CHECK(cudaEventElapsedTime(&t, r.a, r.b));
-    const double frac = (r.gated && r.step < static_cast<int>(prof_fired.size()))
-                            ? static_cast<double>(prof_fired[r.step]) / n : 1.0;
-    ms[r.cls] += t;
-    fl[r.cls] += r.flops * frac;
-    by[r.cls] += r.bytes * frac;
-    if (r.gbytes > 0.0 && r.step < static_cast<int>(prof_fired.size()))
-      by[r.cls] += r.gbytes * static_cast<double>(prof_fired[r.step]) / n;
-    cnt[r.cls] += 1;
-  }
-  std::string out = "{\"steps\": " + std::to_string(prof_step) + ", \"classes\": {";
-  for (int c = 0; c < PC_COUNT; ++c) {
-    char buf[256];
-    snprintf(buf, sizeof(buf), "%s\"%s\": {\"launches\": %lld, \"ms\": %.6f, \"flops\": %.6e, "
-             "\"bytes\": %.6e}", c ? ", " : "", names[c], cnt[c], ms[c], fl[c], by[c]);
-    out += buf;
-  }
-  out += "}}";
-  return out;
-}
-
-// ------------------------------------------------------------------ critic update (shared)
-// Twin critics as one grouped problem of 2n groups: forward on [s|a], MSE cotangent,
-// backward (dW for every layer, dX for layers > 0), fused Adam + target Polyak.
-void Pop::critic_update(int B, const int* polyak_gate) {
-  const int L = cri.depth, n2 = 2 * n, dsa = ds + da;
-  const long long nbB = B;
-  Operand x = fwd_in(S.in_sa.p, nbB * dsa, dsa, 1);
-  for (int l = 0; l < L; ++l) {
-    const bool last = l == L - 1;
-    const int h = cri.dims[l + 1];
-    float* out = last ? S.q.p : S.ch[l].p;
-    gemm_fwd(cri, cri_p.p, l, n2, B, x, out, nbB * h, h, last ? EPI_BIAS : EPI_BIAS_RELU);
-    x = fwd_in(out, nbB * h, h, 0);
-  }
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
-  Operand G = fwd_in(S.dq.p, nbB, 1, 0);
-  for (int l = L - 1; l >= 0; --l) {
-    Operand xt = (l == 0) ? as_kmajor_t(S.in_sa.p, nbB * dsa, dsa, 1)
-                          : as_kmajor_t(S.ch[l - 1].p, nbB * cri.dims[l], cri.dims[l], 0);
-    gemm_dw(cri, cri_g.p, l, n2, B, xt, G, nullptr);
-    if (l > 0) {
-      const int hin = cri.dims[l];
-      Operand mask = fwd_in(S.ch[l - 1].p, nbB * hin, hin, 0);
-      gemm_dx(cri, cri_p.p, l, n2, B, G, mask, S.dh[l - 1].p, nbB * hin, hin, EPI_RELU_MASK, 0,
-              hin, nullptr, 1.0f);
-      G = fwd_in(S.dh[l - 1].p, nbB * hin, hin, 0);
-    }
-  }
-  const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
-  timed(PC_ADAM, 0.0, static_cast<double>(cri.P) * (n2) * 28.0, 0,
-        [&] { launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
-              corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, stream); });
-  // fused target Polyak: +8 B/param (read + write target), every member (SAC) or fired (TD3)
-  if (polyak_gate) prof_add_gated_bytes(8.0 * cri.P * n2);
-  else if (prof_on && !prof.empty()) prof.back().bytes += 8.0 * cri.P * n2;
-}
-
-// forward of `sh` (groups x B rows) from input operand x; hidden activations into hs[l]
-void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Operand x,
-                      std::vector<DBuf<float>>& hs, float* out, long long out_gs,
-                      long long out_rs, int last_epi, const int* active, float* C2,
-                      long long c2_gs, long long c2_rs, bool noise) {
-  const int L = sh.depth;
-  for (int l = 0; l < L; ++l) {
-    const bool last = l == L - 1;
-    const int h = sh.dims[l + 1];
-    if (last) {
-      gemm_fwd(sh, W, l, groups, B, x, out, out_gs, out_rs, last_epi, active, C2, c2_gs, c2_rs,
-               noise);
-    } else {
-      gemm_fwd(sh, W, l, groups, B, x, hs[l].p, static_cast<long long>(B) * h, h, EPI_BIAS_RELU,
-               active);
-      x = fwd_in(hs[l].p, static_cast<long long>(B) * h, h, 0);
-    }
-  }
-}
-
-// backward of `sh` from the top cotangent G: dW for every layer, dX for layers > 0
-void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B,
-                       Operand G, Operand x0t, std::vector<DBuf<float>>& hs,
-                       std::vector<DBuf<float>>& dhs, const int* active) {
-  const int L = sh.depth;
-  for (int l = L - 1; l >= 0; --l) {
-    Operand xt = (l == 0) ? x0t
-                          : as_kmajor_t(hs[l - 1].p, static_cast<long long>(B) * sh.dims[l],
-                                        sh.dims[l], 0);
-    gemm_dw(sh, Gr, l, groups, B, xt, G, active);
-    if (l > 0) {
-      const int hin = sh.dims[l];
-      Operand mask = fwd_in(hs[l - 1].p, static_cast<long long>(B) * hin, hin, 0);
-      gemm_dx(sh, W, l, groups, B, G, mask, dhs[l - 1].p, static_cast<long long>(B) * hin, hin,
-              EPI_RELU_MASK, 0, hin, active, 1.0f);
-      G = fwd_in(dhs[l - 1].p, static_cast<long long>(B) * hin, hin, 0);
-    }
-  }
-}
-
-// critic dX chain from the output cotangent down to the action columns of the input
-void Pop::critic_dx_to_action(int groups, int B, Operand G, std::vector<DBuf<float>>& hs,
-                              std::vector<DBuf<float>>& dhs, float* out, int epi, Operand aux,
-                              float scale, const int* active) {
-  const int L = cri.depth;
-  for (int l = L - 1; l >= 1; --l) {
-    const int hin = cri.dims[l];
-    Operand mask = fwd_in(hs[l - 1].p, static_cast<long long>(B) * hin, hin, 0);
-    gemm_dx(cri, cri_p.p, l, groups, B, G, mask, dhs[l - 1].p, static_cast<long long>(B) * hin,
-            hin, EPI_RELU_MASK, 0, hin, active, 1.0f);
-    G = fwd_in(dhs[l - 1].p, static_cast<long long>(B) * hin, hin, 0);
-  }
-  gemm_dx(cri, cri_p.p, 0, groups, B, G, aux, out, static_cast<long long>(B) * da, da, epi, ds, da,
-          active, scale);
-}
-
-// ------------------------------------------------------------------ TD3 step (algos.hpp:351-422)
-void Pop::td3_step(int B, const uint8_t* d_mask) {
-  const int dsa = ds + da;
-  const long long nbB = B;
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p, t_cri.p + n,
-                        steps.p, streams.p, seed, key_a.p, stream); });
-  // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
-  mlp_forward(pol, pol_t.p, n, B, fwd_in(S.in_s2a.p, nbB * dsa, dsa, 0), S.tp_h, S.in_s2a.p + ds,
-              nbB * dsa, dsa, EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true);
-  mlp_forward(cri, cri_t.p, 2 * n, B, fwd_in(S.in_s2a.p, nbB * dsa, dsa, 1), S.tq_h, S.tq_out.p,
-              nbB, 1, EPI_BIAS);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
-  // twin critic update; target Polyak fused for members whose policy fires (:401-418)
-  critic_update(B, fire.p);
-  // td3_policy_loss_grads (:318-338) on the UPDATED critic1, gated by the fire mask
-  mlp_forward(pol, pol_p.p, n, B, fwd_in(S.in_sa.p, nbB * dsa, dsa, 0), S.ph, S.sa_pi.p + ds,
-              nbB * dsa, dsa, EPI_BIAS_TANH, fire.p, S.pt.p, nbB * da, da);
-  mlp_forward(cri, cri_p.p, n, B, fwd_in(S.sa_pi.p, nbB * dsa, dsa, 0), S.qh, S.qpi.p, nbB, 1,
-              EPI_BIAS, fire.p);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_td3_policy_loss(n, B, S.qpi.p, fire.p, losses.p + 2 * n, S.gq.p, stream); });
-  Operand aux_t = fwd_in(S.pt.p, nbB * da, da, 0);
-  critic_dx_to_action(n, B, fwd_in(S.gq.p, nbB, 1, 0), S.qh, S.qdh, S.gtop.p, EPI_TANH_GRAD,
-                      aux_t, pol.out_scale, fire.p);
-  mlp_backward(pol, pol_p.p, pol_g.p, n, B, fwd_in(S.gtop.p, nbB * da, da, 0),
-               as_kmajor_t(S.in_sa.p, nbB * dsa, dsa, 0), S.ph, S.pdh, fire.p);
-  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * (n) * (28.0 + 8.0), 1,
-        [&] { launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
-              corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, stream); });
-}
-
-// ------------------------------------------------------------------ SAC step (algos.hpp:781-837)
-void Pop::sac_step(int B) {
-  const int dsa = ds + da, L = pol.depth;
-  const long long nbB = B;
-  const int hd = pol.dims[L];
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_step_begin(n, t_pol.p, t_cri.p, t_cri.p + n, t_alpha.p, steps.p, streams.p, seed,
-                        key_a.p, key_b.p, stream); });
-  // sac_critic_target (algos.hpp:739-776): current policy on s2, eps' draws, twin targets
-  mlp_forward(pol, pol_p.p, n, B, fwd_in(S.in_s2a.p, nbB * dsa, dsa, 0), S.tp_h, S.head.p,
-              nbB * hd, hd, EPI_BIAS);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_head(n, B, ds, da, S.head.p, key_b.p, bound, S.in_s2a.p, nullptr, nullptr, nullptr,
-                  nullptr, nullptr, S.logp2.p, stream); });
-  mlp_forward(cri, cri_t.p, 2 * n, B, fwd_in(S.in_s2a.p, nbB * dsa, dsa, 1), S.tq_h, S.tq_out.p,
-              nbB, 1, EPI_BIAS);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_y(n, B, S.r.p, S.d.p, S.tq_out.p, S.logp2.p, log_alpha.p, h_f4.p, h_f3.p, S.y.p,
-               stream); });
-  critic_update(B, nullptr);  // critic targets tracked every step (:827-834)
-  // sac_policy_loss_grads (:643-735) through both UPDATED critics
-  mlp_forward(pol, pol_p.p, n, B, fwd_in(S.in_sa.p, nbB * dsa, dsa, 0), S.ph, S.head.p, nbB * hd,
-              hd, EPI_BIAS);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_head(n, B, ds, da, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p, S.ls.p,
-                  S.clamped.p, S.eps.p, S.logp.p, stream); });
-  mlp_forward(cri, cri_p.p, 2 * n, B, fwd_in(S.sa_pi.p, nbB * dsa, dsa, 1), S.qh, S.qpi.p, nbB, 1,
-              EPI_BIAS);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_policy_top(n, B, S.qpi.p, S.logp.p, log_alpha.p, losses.p + 2 * n, S.gq.p, S.lw.p,
-                        stream); });
-  critic_dx_to_action(2 * n, B, fwd_in(S.gq.p, nbB, 1, 0), S.qh, S.qdh, S.ga.p, EPI_STORE,
-                      Operand{}, 1.0f, nullptr);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_head_grad(n, B, da, S.ga.p, S.lw.p, S.x.p, S.th.p, S.ls.p, S.clamped.p, S.eps.p,
-                       bound, S.gtop.p, stream); });
-  mlp_backward(pol, pol_p.p, pol_g.p, n, B, fwd_in(S.gtop.p, nbB * hd, hd, 0),
-               as_kmajor_t(S.in_sa.p, nbB * dsa, dsa, 0), S.ph, S.pdh, nullptr);
-  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * (n) * (28.0 + 0.0), 0,
-        [&] { launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
-              corr2.p, h_f0.p, nullptr, nullptr, nullptr, nullptr, nullptr, stream); });
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_sac_alpha(n, B, S.logp.p, log_alpha.p, h_d0.p, log_alpha.p, alpha_m.p, alpha_v.p,
-                   t_alpha.p, corr1.p, corr2.p, h_f2.p, stream); });
-}
-
-void Pop::step(int B, const uint8_t* d_mask) {
-  ensure_corr(t_bound + 4);
-  if (algo == PBRL_ALGO_TD3) td3_step(B, d_mask);
-  else sac_step(B);
-  t_bound += 1;
-  prof_step_done();
-}
-
 
 // ------------------------------------------------------------------ update entry points
 void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
@@ -690,7 +336,7 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
       s2 = S.bs2.p;
       d = S.bd.p;
     }
-    timed(PC_GATHER, 0.0, 0.0, 0, [&] { launch_pack_batch(n, B, ds, da, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
+    timed(PC_GATHER, 0.0, 0.0, 0, [&] { launch_pack_batch(n, B, ds, da, lsa, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
                       S.d.p, stream); });
     step(B, d_mask);
   }

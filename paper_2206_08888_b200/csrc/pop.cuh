@@ -86,6 +86,28 @@ struct GemmArgs {
 };
 
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
+// Output-layer backward in one pass (dX with relu mask, dW, db), N_out <= 16.
+struct OutBwdArgs {
+  int B = 0, H = 0, nout = 0, groups = 0, n_members = 1;
+  const float* X = nullptr;  // [groups][B][x_ld]  input of the output layer (post-ReLU)
+  long long x_gs = 0, x_ld = 0;
+  int x_by_member = 0;
+  const float* G = nullptr;  // [groups][B][g_ld]  cotangent of the output
+  long long g_gs = 0, g_ld = 0;
+  const float* W = nullptr;  // [groups] weight rows, W [H][nout] at each group's base
+  long long w_gs = 0;
+  float* dW = nullptr;       // gradient rows: dW [H][nout] then db [nout]
+  long long dw_gs = 0;
+  float* dX = nullptr;       // [groups][B][dx_ld] (nullptr: input layer, no dX)
+  long long dx_gs = 0, dx_ld = 0;
+  const int* active = nullptr;
+};
+void launch_out_backward(const OutBwdArgs& a, cudaStream_t s);
+
+// skinny shapes (output layers): forward N <= 16, dX K <= 16, dW N <= 16
+void launch_fwd_skinny(const GemmArgs& g, cudaStream_t s);
+void launch_dx_skinny(const GemmArgs& g, cudaStream_t s);
+void launch_dw_skinny(const GemmArgs& g, cudaStream_t s);
 
 // ------------------------------------------------------------------ elementwise launchers
 struct Hyper;  // device per-member hyper floats
@@ -94,7 +116,7 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, cudaStream_t s);
-void launch_pack_batch(int n, int B, int ds, int da, const float* s, const float* a,
+void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, float* in_sa,
                        float* in_s2a, float* sa_pi, float* r_out, float* d_out, cudaStream_t st);
 void launch_td_target(int n, int B, const float* r, const float* d, const float* q2n,
@@ -111,6 +133,9 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
                  const float* lr, const int* active, float* tgt, const float* tau_a,
                  const float* tau_b, const int* polyak_gate, cudaStream_t s);
 void launch_fill(float* p, size_t count, float v, cudaStream_t s);
+// bias gradient of a layer: dst[g][o] = sum_b G[g][b][o] in row order (groups gated by active)
+void launch_colsum(int groups, int n, int B, int N, const float* G, long long g_gs, long long g_ld,
+                   float* dst, long long dst_gs, const int* active, cudaStream_t s);
 
 // SAC
 void launch_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2, int64_t* t_alpha,
@@ -118,7 +143,7 @@ void launch_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2, 
                            uint64_t* key_eps, uint64_t* key_eps_t, cudaStream_t s);
 // split_policy_head + tanh_gaussian_logprob + squash (algos.hpp:534-616): head [n][B][2da] ->
 // act into sa (cols ds..), x, th, ls (clamped), clamped flag, logp.
-void launch_sac_head(int n, int B, int ds, int da, const float* head, const uint64_t* key,
+void launch_sac_head(int n, int B, int ds, int da, int lsa, const float* head, const uint64_t* key,
                      float bound, float* sa, float* x, float* th, float* ls, uint8_t* clamped,
                      float* eps, float* logp, cudaStream_t s);
 void launch_sac_y(int n, int B, const float* r, const float* d, const float* q2n,
@@ -139,7 +164,7 @@ void launch_sac_alpha(int n, int B, const float* logp, const float* log_alpha_in
 // replay
 void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t count, int rw,
                            float* ring, cudaStream_t s);
-void launch_replay_gather(int n, int B, int ds, int da, int rw, const float* ring,
+void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const float* ring,
                           uint64_t cap, int shared, const uint64_t* sizes,
                           const uint64_t* streams, uint64_t seed, uint64_t draw_id,
                           float* in_sa, float* in_s2a, float* sa_pi, float* r_out, float* d_out,

@@ -92,6 +92,23 @@ struct ProfRec {
   double gbytes;  // extra bytes that scale with the fired fraction (gated Polyak)
 };
 
+// A [groups][rows][ld] activation block; by_member: shared by the critics of one member.
+struct Mat {
+  const float* p = nullptr;
+  long long gs = 0;
+  long long ld = 0;
+  int by_member = 0;
+};
+
+inline int pad4(int x) { return (x + 3) / 4 * 4; }
+
+struct StepGraph {
+  int B = 0;
+  bool masked = false;
+  cudaGraphExec_t exec = nullptr;
+  size_t nodes = 0;
+};
+
 struct Pop {
   int algo = PBRL_ALGO_TD3, precision = PBRL_PREC_FFMA32, device = 0;
   int n = 0, ds = 0, da = 0;
@@ -158,28 +175,36 @@ struct Pop {
   void upload_hyper();
   void ensure_corr(size_t need);
   void ensure_scratch(int B);
-  void count_launch(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+  void count_launch(uint64_t k) {
+    if (!capturing) g_launches.fetch_add(k, std::memory_order_relaxed);
+  }
+  bool use_tc() const { return precision == PBRL_PREC_TF32; }
+  int lsa = 0;  // padded row stride of the critic-input blocks [s | a]
+  bool use_graphs = true, capturing = false;
+  std::vector<StepGraph> graphs;
+  void invalidate_graphs();
+  void run_program(int B, const uint8_t* d_mask);
+  Mat hid(std::vector<DBuf<float>>& v, int l, int B, const NetShape& sh, int by_member);
 
-  void run_gemm(const GemmArgs& g, int cls);
-  void gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Operand X, float* Y,
-                long long y_gs, long long y_rs, int epi, const int* active = nullptr,
-                float* C2 = nullptr, long long c2_gs = 0, long long c2_rs = 0,
+  void gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, float* Y,
+                long long y_gs, long long y_ld, int epi, const int* active = nullptr,
+                float* C2 = nullptr, long long c2_gs = 0, long long c2_ld = 0,
                 bool noise = false);
-  void gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Operand G,
-               Operand aux, float* DX, long long dx_gs, long long dx_rs, int epi, int col0,
-               int ncols, const int* active, float scale);
-  void gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Operand XT, Operand G,
+  void gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Mat G, Mat aux,
+               float* DX, long long dx_gs, long long dx_ld, int epi, int col0, int ncols,
+               const int* active, float scale);
+  void gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
                const int* active);
-  void mlp_forward(const NetShape& sh, const float* W, int groups, int B, Operand x,
-                   std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_rs,
+  void mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
+                   std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                    int last_epi, const int* active = nullptr, float* C2 = nullptr,
-                   long long c2_gs = 0, long long c2_rs = 0, bool noise = false);
-  void mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Operand G,
-                    Operand x0t, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
+                   long long c2_gs = 0, long long c2_ld = 0, bool noise = false);
+  void mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
+                    Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
                     const int* active);
-  void critic_dx_to_action(int groups, int B, Operand G, std::vector<DBuf<float>>& hs,
-                           std::vector<DBuf<float>>& dhs, float* out, int epi, Operand aux,
-                           float scale, const int* active);
+  void critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>& hs,
+                           std::vector<DBuf<float>>& dhs, float* out, long long out_ld, int epi,
+                           Mat aux, float scale, const int* active);
   void critic_update(int B, const int* polyak_gate);
   void td3_step(int B, const uint8_t* d_mask);
   void sac_step(int B);

@@ -1,0 +1,532 @@
+// The TD3 / SAC update-step programs: every dense product of one population update as a
+// grouped GEMM launch (tcgen05 in TF32 mode wherever the operands are TMA-legal, the bit-exact
+// CUDA-core kernel otherwise and in FFMA32 mode), the fused elementwise steps, and the fused
+// Adam + Polyak update; one step is captured once into a CUDA graph and replayed.
+#include <cmath>
+
+#include "pop_impl.cuh"
+#include "tc_gemm.cuh"
+
+namespace pbrl {
+
+namespace {
+Operand simt_op(const float* p, long long gs, long long rs, long long cs, int by_member) {
+  Operand o;
+  o.p = p;
+  o.gs = gs;
+  o.rs = rs;
+  o.cs = cs;
+  o.by_member = by_member;
+  return o;
+}
+}  // namespace
+
+// ------------------------------------------------------------------ GEMM builders
+// forward of layer l: Y = act(X W_l + b_l); X is [groups][B][in] (stride X.ld)
+void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, float* Y,
+                   long long y_gs, long long y_ld, int epi, const int* active, float* C2,
+                   long long c2_gs, long long c2_ld, bool noise) {
+  const int in = sh.dims[l], out = sh.dims[l + 1];
+  const float* Wl = W + sh.woff[l];
+  const double flops = 2.0 * B * in * out * groups;
+  if (use_tc() && out >= 16 && tma_ok(X.p, X.ld, X.gs) && tma_ok(Wl, out, sh.stride)) {
+    TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
+                static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
+                static_cast<uint64_t>(X.gs)};
+    TcOperand Bw{Wl, static_cast<uint64_t>(out), static_cast<uint64_t>(in),
+                 static_cast<uint64_t>(groups), static_cast<uint64_t>(out), sh.stride};
+    TcArgs a;
+    a.M = B;
+    a.N = out;
+    a.K = in;
+    a.groups = groups;
+    a.n_members = n;
+    a.a_by_member = X.by_member;
+    a.epi = epi;
+    a.C = Y;
+    a.c_gs = y_gs;
+    a.c_rs = y_ld;
+    a.bias = W + sh.boff[l];
+    a.bias_gs = static_cast<long long>(sh.stride);
+    a.C2 = C2;
+    a.c2_gs = c2_gs;
+    a.c2_rs = c2_ld;
+    a.scale = sh.out_scale;
+    a.active = active;
+    if (noise) {
+      a.noise_key = key_a.p;
+      a.noise_sd = h_f2.p;
+      a.noise_clip = h_f3.p;
+      a.bound = bound;
+    }
+    timed(PC_GEMM_FWD, flops, 0.0, active != nullptr,
+          [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
+    return;
+  }
+  GemmArgs g;
+  g.M = B;
+  g.N = out;
+  g.K = in;
+  g.groups = groups;
+  g.n_members = n;
+  g.A = simt_op(X.p, X.gs, X.ld, 1, X.by_member);
+  g.B = simt_op(Wl, static_cast<long long>(sh.stride), out, 1, 0);
+  g.bias = simt_op(W + sh.boff[l], static_cast<long long>(sh.stride), 0, 1, 0);
+  g.C = Y;
+  g.c_gs = y_gs;
+  g.c_rs = y_ld;
+  g.epi = epi;
+  g.acc_init = -0.0f;  // "first product assigned" (pop_tensor.hpp:158-160)
+  g.active = active;
+  g.C2 = C2;
+  g.c2_gs = c2_gs;
+  g.c2_rs = c2_ld;
+  g.scale = sh.out_scale;
+  if (noise) {
+    g.noise_key = key_a.p;
+    g.noise_sd = h_f2.p;
+    g.noise_clip = h_f3.p;
+    g.bound = bound;
+  }
+  timed(PC_GEMM_FWD, flops, 0.0, active != nullptr, [&] {
+    if (out <= 16) launch_fwd_skinny(g, stream);
+    else launch_gemm_simt(g, stream);
+  });
+}
+
+// dX of layer l restricted to input columns [col0, col0+ncols): DX = epi(G W_l^T)
+void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Mat G, Mat aux,
+                  float* DX, long long dx_gs, long long dx_ld, int epi, int col0, int ncols,
+                  const int* active, float scale) {
+  const int out = sh.dims[l + 1];
+  const float* Wc = W + sh.woff[l] + static_cast<size_t>(col0) * out;
+  const double flops = 2.0 * B * out * ncols * groups;
+  if (use_tc() && out >= 8 && tma_ok(G.p, G.ld, G.gs) && tma_ok(Wc, out, sh.stride)) {
+    TcOperand A{G.p, static_cast<uint64_t>(out), static_cast<uint64_t>(B),
+                static_cast<uint64_t>(groups), static_cast<uint64_t>(G.ld),
+                static_cast<uint64_t>(G.gs)};
+    TcOperand Bw{Wc, static_cast<uint64_t>(out), static_cast<uint64_t>(ncols),
+                 static_cast<uint64_t>(groups), static_cast<uint64_t>(out), sh.stride};
+    TcArgs a;
+    a.M = B;
+    a.N = ncols;
+    a.K = out;
+    a.groups = groups;
+    a.n_members = n;
+    a.epi = epi;
+    a.C = DX;
+    a.c_gs = dx_gs;
+    a.c_rs = dx_ld;
+    a.aux = aux.p;
+    a.aux_gs = aux.gs;
+    a.aux_rs = aux.ld;
+    a.aux_by_member = aux.by_member;
+    a.scale = scale;
+    a.active = active;
+    timed(PC_GEMM_DX, flops, 0.0, active != nullptr,
+          [&] { launch_tc_gemm(A, Bw, false, false, a, stream); });
+    return;
+  }
+  GemmArgs g;
+  g.M = B;
+  g.N = ncols;
+  g.K = out;
+  g.groups = groups;
+  g.n_members = n;
+  g.A = simt_op(G.p, G.gs, G.ld, 1, G.by_member);
+  g.B = simt_op(Wc, static_cast<long long>(sh.stride), 1, out, 0);
+  g.C = DX;
+  g.c_gs = dx_gs;
+  g.c_rs = dx_ld;
+  g.epi = epi;
+  g.aux = simt_op(aux.p, aux.gs, aux.ld, 1, aux.by_member);
+  g.acc_init = 0.0f;
+  g.active = active;
+  g.scale = scale;
+  timed(PC_GEMM_DX, flops, 0.0, active != nullptr, [&] {
+    if (out <= 16) launch_dx_skinny(g, stream);
+    else launch_gemm_simt(g, stream);
+  });
+}
+
+// dW_l and db_l into the gradient arena rows: dW = X^T G, db = column sums of G
+void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
+                  const int* active) {
+  const int in = sh.dims[l], out = sh.dims[l + 1];
+  const double flops = 2.0 * B * in * out * groups;
+  if (use_tc() && out >= 32 && tma_ok(X.p, X.ld, X.gs) && tma_ok(G.p, G.ld, G.gs)) {
+    TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
+                static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
+                static_cast<uint64_t>(X.gs)};
+    TcOperand Bg{G.p, static_cast<uint64_t>(out), static_cast<uint64_t>(B),
+                 static_cast<uint64_t>(groups), static_cast<uint64_t>(G.ld),
+                 static_cast<uint64_t>(G.gs)};
+    TcArgs a;
+    a.M = in;
+    a.N = out;
+    a.K = B;
+    a.groups = groups;
+    a.n_members = n;
+    a.a_by_member = X.by_member;
+    a.epi = EPI_STORE;
+    a.C = Gr + sh.woff[l];
+    a.c_gs = static_cast<long long>(sh.stride);
+    a.c_rs = out;
+    a.active = active;
+    timed(PC_GEMM_DW, flops, 0.0, active != nullptr,
+          [&] { launch_tc_gemm(A, Bg, true, true, a, stream); });
+    // bias gradient: per-column sums of G in row order (pop_add_bias_backward, :236-250)
+    timed(PC_ELEM, 0.0, 4.0 * B * out * groups, active != nullptr, [&] {
+      launch_colsum(groups, n, B, out, G.p, G.gs, G.ld, Gr + sh.boff[l],
+                    static_cast<long long>(sh.stride), active, stream);
+    });
+    return;
+  }
+  GemmArgs g;
+  g.M = in + 1;  // ones row: C row `in` = column sums of G = the bias gradient (row order)
+  g.N = out;
+  g.K = B;
+  g.groups = groups;
+  g.n_members = n;
+  g.A = simt_op(X.p, X.gs, 1, X.ld, X.by_member);
+  g.a_ones_row = 1;
+  g.B = simt_op(G.p, G.gs, G.ld, 1, G.by_member);
+  g.C = Gr + sh.woff[l];
+  g.c_gs = static_cast<long long>(sh.stride);
+  g.c_rs = out;
+  g.epi = EPI_STORE;
+  g.acc_init = 0.0f;
+  g.active = active;
+  timed(PC_GEMM_DW, flops, 0.0, active != nullptr, [&] {
+    if (out <= 16) launch_dw_skinny(g, stream);
+    else launch_gemm_simt(g, stream);
+  });
+}
+
+// ------------------------------------------------------------------ profiling
+cudaEvent_t Pop::prof_event() {
+  if (ev_used == ev_pool.size()) {
+    cudaEvent_t e;
+    CUDA_CHECK(cudaEventCreate(&e));
+    ev_pool.push_back(e);
+  }
+  return ev_pool[ev_used++];
+}
+
+void Pop::prof_begin(cudaEvent_t* a) {
+  if (!prof_on) return;
+  *a = prof_event();
+  CUDA_CHECK(cudaEventRecord(*a, stream));
+}
+
+void Pop::prof_end(cudaEvent_t a, int cls, double flops, double bytes, int gated) {
+  if (!prof_on) return;
+  cudaEvent_t b = prof_event();
+  CUDA_CHECK(cudaEventRecord(b, stream));
+  prof.push_back(ProfRec{cls, flops, bytes, gated, prof_step, a, b, 0.0});
+}
+
+// critic targets are Polyak-updated only for fired members in TD3: extra gated bytes
+void Pop::prof_add_gated_bytes(double bytes) {
+  if (prof_on && !prof.empty()) prof.back().gbytes += bytes;
+}
+
+void Pop::prof_step_done() {
+  if (!prof_on) return;
+  int nf = n;
+  if (algo == PBRL_ALGO_TD3) {
+    std::vector<int> f(n);
+    CUDA_CHECK(cudaMemcpyAsync(f.data(), fire.p, 4 * n, cudaMemcpyDeviceToHost, stream));
+    sync();
+    nf = 0;
+    for (int v : f) nf += v;
+  }
+  prof_fired.push_back(nf);
+  ++prof_step;
+}
+
+std::string Pop::prof_report() {
+  sync();
+  static const char* names[PC_COUNT] = {"gemm_fwd", "gemm_dx", "gemm_dw", "adam_polyak",
+                                        "elementwise", "gather_pack"};
+  double ms[PC_COUNT] = {}, fl[PC_COUNT] = {}, by[PC_COUNT] = {};
+  long long cnt[PC_COUNT] = {};
+  for (const ProfRec& r : prof) {
+    float t = 0.0f;
+    CUDA_CHECK(cudaEventElapsedTime(&t, r.a, r.b));
+    const double frac = (r.gated && r.step < static_cast<int>(prof_fired.size()))
+                            ? static_cast<double>(prof_fired[r.step]) / n : 1.0;
+    ms[r.cls] += t;
+    fl[r.cls] += r.flops * frac;
+    by[r.cls] += r.bytes * frac;
+    if (r.gbytes > 0.0 && r.step < static_cast<int>(prof_fired.size()))
+      by[r.cls] += r.gbytes * static_cast<double>(prof_fired[r.step]) / n;
+    cnt[r.cls] += 1;
+  }
+  std::string out = "{\"steps\": " + std::to_string(prof_step) + ", \"classes\": {";
+  for (int c = 0; c < PC_COUNT; ++c) {
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "%s\"%s\": {\"launches\": %lld, \"ms\": %.6f, \"flops\": %.6e, \"bytes\": %.6e}",
+             c ? ", " : "", names[c], cnt[c], ms[c], fl[c], by[c]);
+    out += buf;
+  }
+  out += "}}";
+  return out;
+}
+
+// ------------------------------------------------------------------ shared building blocks
+Mat Pop::hid(std::vector<DBuf<float>>& v, int l, int B, const NetShape& sh, int by_member) {
+  const int ld = pad4(sh.dims[l + 1]);
+  return Mat{v[l].p, static_cast<long long>(B) * ld, ld, by_member};
+}
+
+// forward of `sh` (groups x B rows) from input x; hidden activations into hs[l]
+void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
+                      std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
+                      int last_epi, const int* active, float* C2, long long c2_gs,
+                      long long c2_ld, bool noise) {
+  const int L = sh.depth;
+  for (int l = 0; l < L; ++l) {
+    if (l == L - 1) {
+      gemm_fwd(sh, W, l, groups, B, x, out, out_gs, out_ld, last_epi, active, C2, c2_gs, c2_ld,
+               noise);
+    } else {
+      const Mat h = hid(hs, l, B, sh, 0);
+      gemm_fwd(sh, W, l, groups, B, x, const_cast<float*>(h.p), h.gs, h.ld, EPI_BIAS_RELU, active);
+      x = h;
+    }
+  }
+}
+
+// backward of `sh` from the top cotangent G: dW for every layer, dX for layers > 0
+void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
+                       Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
+                       const int* active) {
+  const int L = sh.depth;
+  for (int l = L - 1; l >= 0; --l) {
+    const Mat x = (l == 0) ? x0 : hid(hs, l - 1, B, sh, 0);
+    if (l == L - 1 && sh.dims[L] <= 16) {
+      // output layer: dX (masked), dW and db in one pass over the hidden activations
+      const int H = sh.dims[l], nout = sh.dims[L];
+      OutBwdArgs a;
+      a.B = B;
+      a.H = H;
+      a.nout = nout;
+      a.groups = groups;
+      a.n_members = n;
+      a.X = x.p;
+      a.x_gs = x.gs;
+      a.x_ld = x.ld;
+      a.x_by_member = x.by_member;
+      a.G = G.p;
+      a.g_gs = G.gs;
+      a.g_ld = G.ld;
+      a.W = W + sh.woff[l];
+      a.w_gs = static_cast<long long>(sh.stride);
+      a.dW = Gr + sh.woff[l];
+      a.dw_gs = static_cast<long long>(sh.stride);
+      a.active = active;
+      Mat dh{};
+      if (l > 0) {
+        dh = hid(dhs, l - 1, B, sh, 0);
+        a.dX = const_cast<float*>(dh.p);
+        a.dx_gs = dh.gs;
+        a.dx_ld = dh.ld;
+      }
+      timed(PC_GEMM_DW, 2.0 * B * H * nout * groups * (l > 0 ? 2.0 : 1.0), 0.0,
+            active != nullptr, [&] { launch_out_backward(a, stream); });
+      G = dh;
+      continue;
+    }
+    if (l > 0) {
+      // dX before dW: a fused optimiser in the dW epilogue must not race the dX read of W_l
+      const Mat dh = hid(dhs, l - 1, B, sh, 0);
+      gemm_dx(sh, W, l, groups, B, G, x, const_cast<float*>(dh.p), dh.gs, dh.ld, EPI_RELU_MASK,
+              0, sh.dims[l], active, 1.0f);
+      gemm_dw(sh, Gr, l, groups, B, x, G, active);
+      G = dh;
+    } else {
+      gemm_dw(sh, Gr, l, groups, B, x, G, active);
+    }
+  }
+}
+
+// critic dX chain from the output cotangent down to the action columns of the input
+void Pop::critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>& hs,
+                              std::vector<DBuf<float>>& dhs, float* out, long long out_ld,
+                              int epi, Mat aux, float scale, const int* active) {
+  const int L = cri.depth;
+  for (int l = L - 1; l >= 1; --l) {
+    const Mat mask = hid(hs, l - 1, B, cri, 0);
+    const Mat dh = hid(dhs, l - 1, B, cri, 0);
+    gemm_dx(cri, cri_p.p, l, groups, B, G, mask, const_cast<float*>(dh.p), dh.gs, dh.ld,
+            EPI_RELU_MASK, 0, cri.dims[l], active, 1.0f);
+    G = dh;
+  }
+  gemm_dx(cri, cri_p.p, 0, groups, B, G, aux, out, static_cast<long long>(B) * out_ld, out_ld,
+          epi, ds, da, active, scale);
+}
+
+// Twin critics as one grouped problem of 2n groups: forward on [s|a], MSE cotangent,
+// backward, fused Adam + target Polyak (algos.hpp:369-377, :401-418).
+void Pop::critic_update(int B, const int* polyak_gate) {
+  const int n2 = 2 * n;
+  const Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
+  mlp_forward(cri, cri_p.p, n2, B, x0, S.ch, S.q.p, B, 1, EPI_BIAS);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
+  mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr);
+  const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
+  timed(PC_ADAM, 0.0, static_cast<double>(cri.P) * n2 * 28.0, 0, [&] {
+    launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
+                corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, stream);
+  });
+  // fused target Polyak: +8 B/param (read + write target), every member (SAC) or fired (TD3)
+  if (polyak_gate) prof_add_gated_bytes(8.0 * cri.P * n2);
+  else if (prof_on && !prof.empty()) prof.back().bytes += 8.0 * cri.P * n2;
+}
+
+// ------------------------------------------------------------------ TD3 step (algos.hpp:351-422)
+void Pop::td3_step(int B, const uint8_t* d_mask) {
+  const long long nbB = B;
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p, t_cri.p + n,
+                          steps.p, streams.p, seed, key_a.p, stream);
+  });
+  // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
+  const Mat s2{S.in_s2a.p, nbB * lsa, lsa, 0};
+  mlp_forward(pol, pol_t.p, n, B, s2, S.tp_h, S.in_s2a.p + ds, nbB * lsa, lsa,
+              EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true);
+  mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
+              nbB, 1, EPI_BIAS);
+  timed(PC_ELEM, 0.0, 0.0, 0,
+        [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
+  // twin critic update; target Polyak fused for members whose policy fires
+  critic_update(B, fire.p);
+  // td3_policy_loss_grads (:318-338) on the UPDATED critic1, gated by the fire mask
+  const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
+  mlp_forward(pol, pol_p.p, n, B, s, S.ph, S.sa_pi.p + ds, nbB * lsa, lsa, EPI_BIAS_TANH, fire.p,
+              S.pt.p, nbB * da, da);
+  mlp_forward(cri, cri_p.p, n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 0}, S.qh, S.qpi.p, nbB, 1,
+              EPI_BIAS, fire.p);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_td3_policy_loss(n, B, S.qpi.p, fire.p, losses.p + 2 * n, S.gq.p, stream);
+  });
+  const int lt = pad4(da);
+  critic_dx_to_action(n, B, Mat{S.gq.p, nbB, 1, 0}, S.qh, S.qdh, S.gtop.p, lt, EPI_TANH_GRAD,
+                      Mat{S.pt.p, nbB * da, da, 0}, pol.out_scale, fire.p);
+  mlp_backward(pol, pol_p.p, pol_g.p, n, B, Mat{S.gtop.p, nbB * lt, lt, 0}, s, S.ph, S.pdh,
+               fire.p);
+  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * (28.0 + 8.0), 1, [&] {
+    launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
+                corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, stream);
+  });
+}
+
+// ------------------------------------------------------------------ SAC step (algos.hpp:781-837)
+void Pop::sac_step(int B) {
+  const int L = pol.depth;
+  const long long nbB = B;
+  const int hd = pol.dims[L];
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_sac_step_begin(n, t_pol.p, t_cri.p, t_cri.p + n, t_alpha.p, steps.p, streams.p, seed,
+                          key_a.p, key_b.p, stream);
+  });
+  // sac_critic_target (algos.hpp:739-776): current policy on s2, eps' draws, twin targets
+  mlp_forward(pol, pol_p.p, n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 0}, S.tp_h, S.head.p, nbB * hd,
+              hd, EPI_BIAS);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_sac_head(n, B, ds, da, lsa, S.head.p, key_b.p, bound, S.in_s2a.p, nullptr, nullptr,
+                    nullptr, nullptr, nullptr, S.logp2.p, stream);
+  });
+  mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
+              nbB, 1, EPI_BIAS);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_sac_y(n, B, S.r.p, S.d.p, S.tq_out.p, S.logp2.p, log_alpha.p, h_f4.p, h_f3.p, S.y.p,
+                 stream);
+  });
+  critic_update(B, nullptr);  // critic targets tracked every step (:827-834)
+  // sac_policy_loss_grads (:643-735) through both UPDATED critics
+  const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
+  mlp_forward(pol, pol_p.p, n, B, s, S.ph, S.head.p, nbB * hd, hd, EPI_BIAS);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_sac_head(n, B, ds, da, lsa, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p,
+                    S.ls.p, S.clamped.p, S.eps.p, S.logp.p, stream);
+  });
+  mlp_forward(cri, cri_p.p, 2 * n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 1}, S.qh, S.qpi.p, nbB, 1,
+              EPI_BIAS);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_sac_policy_top(n, B, S.qpi.p, S.logp.p, log_alpha.p, losses.p + 2 * n, S.gq.p, S.lw.p,
+                          stream);
+  });
+  critic_dx_to_action(2 * n, B, Mat{S.gq.p, nbB, 1, 0}, S.qh, S.qdh, S.ga.p, da, EPI_STORE,
+                      Mat{}, 1.0f, nullptr);
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_sac_head_grad(n, B, da, S.ga.p, S.lw.p, S.x.p, S.th.p, S.ls.p, S.clamped.p, S.eps.p,
+                         bound, S.gtop.p, stream);
+  });
+  mlp_backward(pol, pol_p.p, pol_g.p, n, B, Mat{S.gtop.p, nbB * hd, hd, 0}, s, S.ph, S.pdh,
+               nullptr);
+  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * 28.0, 0, [&] {
+    launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
+                corr2.p, h_f0.p, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+  });
+  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+    launch_sac_alpha(n, B, S.logp.p, log_alpha.p, h_d0.p, log_alpha.p, alpha_m.p, alpha_v.p,
+                     t_alpha.p, corr1.p, corr2.p, h_f2.p, stream);
+  });
+}
+
+// ------------------------------------------------------------------ one step (graph replay)
+void Pop::run_program(int B, const uint8_t* d_mask) {
+  if (algo == PBRL_ALGO_TD3) td3_step(B, d_mask);
+  else sac_step(B);
+}
+
+void Pop::invalidate_graphs() {
+  for (auto& g : graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  }
+  graphs.clear();
+}
+
+void Pop::step(int B, const uint8_t* d_mask) {
+  ensure_corr(t_bound + 4);
+  if (prof_on || !use_graphs) {
+    run_program(B, d_mask);
+  } else {
+    StepGraph* sg = nullptr;
+    for (auto& g : graphs)
+      if (g.B == B && g.masked == (d_mask != nullptr)) sg = &g;
+    if (!sg) {
+      StepGraph g;
+      g.B = B;
+      g.masked = d_mask != nullptr;
+      cudaGraph_t graph;
+      capturing = true;
+      CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        run_program(B, d_mask);
+      } catch (...) {
+        cudaStreamEndCapture(stream, &graph);
+        capturing = false;
+        throw;
+      }
+      CUDA_CHECK(cudaStreamEndCapture(stream, &graph));
+      capturing = false;
+      size_t nodes = 0;
+      CUDA_CHECK(cudaGraphGetNodes(graph, nullptr, &nodes));
+      g.nodes = nodes;
+      CUDA_CHECK(cudaGraphInstantiate(&g.exec, graph, 0));
+      CUDA_CHECK(cudaGraphDestroy(graph));
+      graphs.push_back(g);
+      sg = &graphs.back();
+    }
+    CUDA_CHECK(cudaGraphLaunch(sg->exec, stream));
+    count_launch(sg->nodes);
+  }
+  t_bound += 1;
+  prof_step_done();
+}
+
+}  // namespace pbrl

@@ -1,0 +1,51 @@
+// Host interface of the tcgen05 grouped GEMM (tc_gemm.cu).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace pbrl {
+
+// A 3-D fp32 operand in global memory: [groups][rows][cols] with element (r, c) of group g at
+// p + g*gs + r*ld + c.  rows / cols are the LOGICAL extents (TMA zero-fills past them).
+struct TcOperand {
+  const float* p = nullptr;
+  uint64_t cols = 0, rows = 0, groups = 0, ld = 0, gs = 0;
+};
+
+struct TcArgs {
+  int M = 0, N = 0, K = 0, groups = 0, n_members = 1;
+  int stages = 4;  // smem pipeline depth (set by the launcher)
+  int a_by_member = 0, b_by_member = 0;
+  int epi = 0;
+  float* C = nullptr;
+  long long c_gs = 0, c_rs = 0;
+  int c_by_member = 0;
+  const float* bias = nullptr;
+  long long bias_gs = 0;
+  const float* aux = nullptr;
+  long long aux_gs = 0, aux_rs = 0;
+  int aux_by_member = 0;
+  float* C2 = nullptr;
+  long long c2_gs = 0, c2_rs = 0;
+  float scale = 1.0f;
+  const int* active = nullptr;
+  const uint64_t* noise_key = nullptr;
+  const float* noise_sd = nullptr;
+  const float* noise_clip = nullptr;
+  float bound = 1.0f;
+};
+
+// TMA requirements: 16-byte aligned base and strides.
+bool tma_ok(const float* base, uint64_t row_stride_elems, uint64_t group_stride_elems);
+
+// a_mn / b_mn: operand is MN-major (the M / N index is the contiguous one in memory).
+//   A K-major : A(m, k) = A.p[g][m][k]  (rows = M extent, cols = K extent)
+//   A MN-major: A(m, k) = A.p[g][k][m]  (rows = K extent, cols = M extent)
+//   B K-major : B(n, k) = B.p[g][n][k]  (rows = N extent, cols = K extent)
+//   B MN-major: B(n, k) = B.p[g][k][n]  (rows = K extent, cols = N extent)
+void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn,
+                    const TcArgs& g, cudaStream_t s);
+
+}  // namespace pbrl
