@@ -1,0 +1,378 @@
+// pbrl_b200.hpp -- C++ facade over the C ABI (pbrl_b200.h) with the reference's names,
+// argument meanings and exception types (proj/core/include/pbrl/{algos,replay,evolve,errors}.hpp),
+// so code written against the reference population-trainer API switches by changing
+// `namespace pbrl` to `namespace pbrl::b200` and linking libpbrl_b200.so.
+//
+//   reference                                   here
+//   make_td3_state<T>(n, ds, da, hidden, ...)   make_td3_state(n, ds, da, hidden, bound, seed)
+//   td3_update_step(st, batch, hyper[, ...])    td3_update_step(st, batch, hyper[, mask])
+//   update_k_steps(st, sampler, k, hyper)       update_k_steps(st, sampler, k, hyper)
+//   make_sac_state / sac_update_step            same
+//   flatten_member(st.policy, i)                st.flatten_member(Net::kPolicy, i)
+//   ReplayBuffer + sample_batch                 DeviceReplay + sample_batch / update_k_from_replay
+//   pbt_plan / pbt_evolve_trainer               pbt_plan / pbt_evolve_trainer
+// State lives in HBM on the population's device; batches are host arrays laid out like
+// TransitionBatch (algos.hpp:14-24), row-major [N][B][dim].
+#pragma once
+
+#include <cstdint>
+#include <deque>
+#include <functional>
+#include <numeric>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "pbrl_b200.h"
+
+namespace pbrl::b200 {
+
+// ---------------------------------------------------------------- errors (errors.hpp:9-48)
+class ShapeError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+class ConfigError : public std::invalid_argument {
+ public:
+  using std::invalid_argument::invalid_argument;
+};
+class UsageError : public std::logic_error {
+ public:
+  using std::logic_error::logic_error;
+};
+class NotReadyError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ResourceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DataStarvationError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == PBRL_OK) return;
+  char buf[1024];
+  pbrl_last_error(buf, sizeof(buf));
+  const std::string m(buf);
+  switch (rc) {
+    case PBRL_E_SHAPE: throw ShapeError(m);
+    case PBRL_E_CONFIG: throw ConfigError(m);
+    case PBRL_E_USAGE: throw UsageError(m);
+    case PBRL_E_NOT_READY: throw NotReadyError(m);
+    case PBRL_E_RESOURCE: throw ResourceError(m);
+    case PBRL_E_STARVATION: throw DataStarvationError(m);
+    default: throw DeviceError(m);
+  }
+}
+
+enum class Net : int {
+  kPolicy = PBRL_NET_POLICY,
+  kPolicyTarget = PBRL_NET_POLICY_TARGET,
+  kCritic1 = PBRL_NET_CRITIC1,
+  kCritic2 = PBRL_NET_CRITIC2,
+  kCritic1Target = PBRL_NET_CRITIC1_TARGET,
+  kCritic2Target = PBRL_NET_CRITIC2_TARGET,
+};
+enum class Precision : int { kFfma32 = PBRL_PREC_FFMA32, kTf32 = PBRL_PREC_TF32 };
+
+// ---------------------------------------------------------------- batches (algos.hpp:14-24)
+struct TransitionBatch {
+  std::vector<float> s, a, r, s2, done;  // [N][B][ds], [N][B][da], [N][B], [N][B][ds], [N][B]
+  std::size_t n = 0, rows = 0;
+  std::size_t members() const { return n; }
+  pbrl_batch view() const { return pbrl_batch{s.data(), a.data(), r.data(), s2.data(), done.data()}; }
+};
+
+// ---------------------------------------------------------------- hyperparameters
+struct Td3Hyper {  // algos.hpp:32-109
+  std::vector<double> critic_lr, policy_lr, policy_delay_ratio, explore_std, target_std,
+      target_clip, gamma, tau;
+  static Td3Hyper defaults(std::size_t n) {
+    Td3Hyper h;
+    h.critic_lr.assign(n, 3e-4);
+    h.policy_lr.assign(n, 3e-4);
+    h.policy_delay_ratio.assign(n, 0.5);
+    h.explore_std.assign(n, 0.1);
+    h.target_std.assign(n, 0.2);
+    h.target_clip.assign(n, 0.5);
+    h.gamma.assign(n, 0.99);
+    h.tau.assign(n, 0.005);
+    return h;
+  }
+  std::vector<std::pair<const char*, const std::vector<double>*>> fields() const {
+    return {{"critic_lr", &critic_lr},     {"policy_lr", &policy_lr},
+            {"policy_delay_ratio", &policy_delay_ratio}, {"explore_std", &explore_std},
+            {"target_std", &target_std},   {"target_clip", &target_clip},
+            {"gamma", &gamma},             {"tau", &tau}};
+  }
+};
+
+struct SacHyper {  // algos.hpp:112-156
+  std::vector<double> policy_lr, critic_lr, alpha_lr, target_entropy, reward_scale, gamma, tau;
+  static SacHyper defaults(std::size_t n, std::size_t action_dim) {
+    SacHyper h;
+    h.policy_lr.assign(n, 3e-4);
+    h.critic_lr.assign(n, 3e-4);
+    h.alpha_lr.assign(n, 3e-4);
+    h.target_entropy.assign(n, -static_cast<double>(action_dim));
+    h.reward_scale.assign(n, 1.0);
+    h.gamma.assign(n, 0.99);
+    h.tau.assign(n, 0.005);
+    return h;
+  }
+  std::vector<std::pair<const char*, const std::vector<double>*>> fields() const {
+    return {{"policy_lr", &policy_lr},       {"critic_lr", &critic_lr},
+            {"alpha_lr", &alpha_lr},         {"target_entropy", &target_entropy},
+            {"reward_scale", &reward_scale}, {"gamma", &gamma},
+            {"tau", &tau}};
+  }
+};
+
+// ---------------------------------------------------------------- population state
+class Population {
+ public:
+  Population(int algo, std::size_t n, std::size_t obs_dim, std::size_t act_dim,
+             const std::vector<std::size_t>& hidden, double action_bound, std::uint64_t seed,
+             Precision precision = Precision::kFfma32, int device = 0,
+             std::uint64_t member_offset = 0, std::uint64_t n_global = 0)
+      : n_(n), ds_(obs_dim), da_(act_dim) {
+    std::vector<std::uint64_t> h(hidden.begin(), hidden.end());
+    pbrl_pop_desc d{};
+    d.algo = algo;
+    d.n = n;
+    d.obs_dim = obs_dim;
+    d.act_dim = act_dim;
+    d.n_hidden = static_cast<std::uint32_t>(h.size());
+    d.hidden = h.data();
+    d.action_bound = action_bound;
+    d.seed = seed;
+    d.precision = static_cast<int>(precision);
+    d.device = device;
+    d.member_offset = member_offset;
+    d.n_global = n_global;
+    check(pbrl_pop_create(&d, &h_));
+  }
+  ~Population() {
+    if (h_) pbrl_pop_destroy(h_);
+  }
+  Population(const Population&) = delete;
+  Population& operator=(const Population&) = delete;
+  Population(Population&& o) noexcept : h_(o.h_), n_(o.n_), ds_(o.ds_), da_(o.da_) { o.h_ = nullptr; }
+
+  std::size_t members() const { return n_; }
+  pbrl_pop* handle() const { return h_; }
+
+  std::vector<float> flatten_member(Net net, std::size_t i) const {  // net_pop.hpp:163-173
+    std::uint64_t c = 0;
+    check(pbrl_param_count(h_, static_cast<int>(net), &c));
+    std::vector<float> out(c);
+    check(pbrl_get_member(h_, static_cast<int>(net), i, out.data()));
+    return out;
+  }
+  void unflatten_member(Net net, std::size_t i, const std::vector<float>& v) {  // :176-189
+    check(pbrl_set_member(h_, static_cast<int>(net), i, v.data()));
+  }
+  void copy_member(Net net, std::size_t src, std::size_t dst) {  // :192-202
+    check(pbrl_copy_member(h_, static_cast<int>(net), src, dst));
+  }
+  std::vector<std::uint64_t> steps() const {
+    std::vector<std::uint64_t> s(n_);
+    check(pbrl_get_counters(h_, nullptr, s.data()));
+    return s;
+  }
+
+ protected:
+  template <typename H>
+  void sync_hyper(const H& hy) {
+    for (auto& [name, vec] : hy.fields()) {
+      if (vec->size() != n_) throw ConfigError(std::string("hyper: ") + name + " length != N");
+      check(pbrl_set_hyper(h_, name, vec->data()));
+    }
+  }
+  friend void td3_update_step(class Td3State&, const TransitionBatch&, const Td3Hyper&,
+                              const std::vector<char>*);
+  friend void sac_update_step(class SacState&, const TransitionBatch&, const SacHyper&);
+  template <typename S, typename H>
+  friend void update_k_steps(S&, const std::function<std::optional<TransitionBatch>()>&,
+                             std::size_t, const H&);
+
+  pbrl_pop* h_ = nullptr;
+  std::size_t n_, ds_, da_;
+};
+
+class Td3State : public Population {  // algos.hpp:165-212
+ public:
+  using Population::Population;
+  std::vector<double> delay_acc() const {
+    std::vector<double> d(n_);
+    check(pbrl_get_counters(h_, d.data(), nullptr));
+    return d;
+  }
+};
+
+class SacState : public Population {  // algos.hpp:473-521
+ public:
+  using Population::Population;
+};
+
+inline Td3State make_td3_state(std::size_t n, std::size_t obs_dim, std::size_t act_dim,
+                               const std::vector<std::size_t>& hidden, double action_bound,
+                               std::uint64_t seed, Precision precision = Precision::kFfma32,
+                               int device = 0) {
+  return Td3State(PBRL_ALGO_TD3, n, obs_dim, act_dim, hidden, action_bound, seed, precision,
+                  device);
+}
+
+inline SacState make_sac_state(std::size_t n, std::size_t obs_dim, std::size_t act_dim,
+                               const std::vector<std::size_t>& hidden, double action_bound,
+                               std::uint64_t seed, Precision precision = Precision::kFfma32,
+                               int device = 0) {
+  return SacState(PBRL_ALGO_SAC, n, obs_dim, act_dim, hidden, action_bound, seed, precision,
+                  device);
+}
+
+// td3_update_step (algos.hpp:351-422); policy_member_mask as in the reference
+inline void td3_update_step(Td3State& st, const TransitionBatch& batch, const Td3Hyper& hyper,
+                            const std::vector<char>* policy_member_mask = nullptr) {
+  if (batch.members() != st.members())
+    throw ConfigError("td3_update_step: batch population != state population");
+  st.sync_hyper(hyper);
+  const pbrl_batch b = batch.view();
+  std::vector<std::uint8_t> mask;
+  if (policy_member_mask) mask.assign(policy_member_mask->begin(), policy_member_mask->end());
+  check(pbrl_update_batches(st.h_, &b, 1, batch.rows, mask.empty() ? nullptr : mask.data()));
+}
+
+inline void sac_update_step(SacState& st, const TransitionBatch& batch, const SacHyper& hyper) {
+  if (batch.members() != st.members())
+    throw ConfigError("sac_update_step: batch population != state population");
+  st.sync_hyper(hyper);
+  const pbrl_batch b = batch.view();
+  check(pbrl_update_batches(st.h_, &b, 1, batch.rows, nullptr));
+}
+
+// update_k_steps (algos.hpp:953-983): k chained steps, DataStarvationError if the sampler runs dry
+template <typename S, typename H>
+void update_k_steps(S& st, const std::function<std::optional<TransitionBatch>()>& sampler,
+                    std::size_t k, const H& hyper) {
+  if (k < 1) throw ConfigError("update_k_steps: k must be >= 1");
+  std::vector<TransitionBatch> batches;
+  for (std::size_t i = 0; i < k; ++i) {
+    auto b = sampler();
+    if (!b)
+      throw DataStarvationError("update_k_steps: sampler exhausted after " + std::to_string(i) +
+                                " of " + std::to_string(k) + " steps");
+    batches.push_back(std::move(*b));
+  }
+  st.sync_hyper(hyper);
+  std::vector<pbrl_batch> views;
+  for (auto& b : batches) views.push_back(b.view());
+  check(pbrl_update_batches(st.h_, views.data(), static_cast<std::uint32_t>(k), batches[0].rows,
+                            nullptr));
+}
+
+// ---------------------------------------------------------------- replay (replay.hpp)
+enum class BufferMode { kPerAgent = PBRL_REPLAY_PER_AGENT, kShared = PBRL_REPLAY_SHARED };
+
+class DeviceReplay {
+ public:
+  DeviceReplay(Population& pop, std::size_t capacity, BufferMode mode = BufferMode::kPerAgent)
+      : pop_(pop) {
+    check(pbrl_replay_create(pop.handle(), capacity, static_cast<int>(mode)));
+  }
+  // batched ReplayBuffer::push (replay.hpp:56-69)
+  void insert(const std::vector<float>& s, const std::vector<float>& a,
+              const std::vector<float>& r, const std::vector<float>& s2,
+              const std::vector<float>& done, const std::vector<std::uint32_t>& member) {
+    check(pbrl_replay_insert(pop_.handle(), s.data(), a.data(), r.data(), s2.data(), done.data(),
+                             member.data(), member.size()));
+  }
+  std::size_t size(std::size_t buffer = 0) const {
+    std::uint64_t s = 0;
+    check(pbrl_replay_size(pop_.handle(), buffer, &s));
+    return s;
+  }
+  Population& pop() { return pop_; }
+
+ private:
+  Population& pop_;
+};
+
+// sample_batch (replay.hpp:181-204): nullopt when a source buffer holds < max(min_size, 1)
+inline std::optional<TransitionBatch> sample_batch(DeviceReplay& rb, std::size_t batch_size,
+                                                   std::uint64_t seed, std::uint64_t draw_id,
+                                                   std::size_t obs_dim, std::size_t act_dim,
+                                                   std::size_t min_size = 1) {
+  const std::size_t n = rb.pop().members();
+  TransitionBatch b;
+  b.n = n;
+  b.rows = batch_size;
+  b.s.resize(n * batch_size * obs_dim);
+  b.a.resize(n * batch_size * act_dim);
+  b.r.resize(n * batch_size);
+  b.s2.resize(n * batch_size * obs_dim);
+  b.done.resize(n * batch_size);
+  int ready = 0;
+  check(pbrl_sample_batch(rb.pop().handle(), seed, draw_id, batch_size, min_size, b.s.data(),
+                          b.a.data(), b.r.data(), b.s2.data(), b.done.data(), &ready));
+  if (!ready) return std::nullopt;
+  return b;
+}
+
+// ---------------------------------------------------------------- PBT (evolve.hpp)
+struct PBTState {  // evolve.hpp:80-108
+  std::vector<std::deque<double>> returns;
+  std::size_t ring_capacity = 10;
+  std::uint64_t steps_since_evolve = 0;
+  std::uint64_t evolve_interval = 100000;
+  double truncation_fraction = 0.3;
+  explicit PBTState(std::size_t n = 0) : returns(n) {}
+  void record_return(std::size_t m, double v) {
+    auto& ring = returns.at(m);
+    ring.push_back(v);
+    while (ring.size() > ring_capacity) ring.pop_front();
+  }
+  std::vector<double> fitness() const {
+    std::vector<double> f;
+    for (const auto& r : returns) {
+      if (r.empty()) throw NotReadyError("pbt_rank: every member needs at least one recorded return");
+      f.push_back(std::accumulate(r.begin(), r.end(), 0.0) / static_cast<double>(r.size()));
+    }
+    return f;
+  }
+};
+
+struct EvolvePlan {
+  std::vector<std::size_t> replaced, donors;
+};
+
+// pbt_evolve_trainer (evolve.hpp:169-213) with the default priors; rng = (key, next) of the
+// RngSequence the caller owns (rng.hpp:74-95)
+inline std::optional<EvolvePlan> pbt_evolve_trainer(PBTState& st, Population& trainer,
+                                                    std::uint64_t rng_key, std::uint64_t& rng_next) {
+  const auto fit = st.fitness();
+  std::vector<std::uint64_t> rep(fit.size()), don(fit.size());
+  std::uint32_t cnt = 0;
+  check(pbrl_pbt_evolve(trainer.handle(), fit.data(), rng_key, &rng_next, rep.data(), don.data(),
+                        &cnt));
+  if (cnt == 0) return std::nullopt;
+  EvolvePlan plan;
+  for (std::uint32_t i = 0; i < cnt; ++i) {
+    plan.replaced.push_back(rep[i]);
+    plan.donors.push_back(don[i]);
+    st.returns[rep[i]].clear();
+  }
+  st.steps_since_evolve = 0;
+  return plan;
+}
+
+}  // namespace pbrl::b200

@@ -281,78 +281,79 @@ __global__ void __launch_bounds__(128) k_dw_skinny(const GemmArgs g) {
 //   dW[i][o] = sum_b X[b][i] G[b][o]      (b ascending, from +0: pop_tensor.hpp:194-206)
 //   db[o]    = sum_b G[b][o]              (b ascending: :244-246)
 //   dX[b][i] = X[b][i] > 0 ? sum_o G[b][o] W[i][o] : 0   (o ascending; relu' of the layer below)
-// One block per (group, 256 input features); thread = input feature i, G staged in shared memory,
-// rows processed 8 at a time with the X loads batched.
-template <int NOUT>
+// One block per (group, 32 input features): the X column tile [B][32] and G [B][nout] are staged
+// in shared memory with coalesced loads, then every sequential reduction runs out of smem.
+constexpr int kObCols = 32;
+
 __global__ void __launch_bounds__(256) k_out_backward(OutBwdArgs a) {
-  extern __shared__ float Gs[];  // [B][NOUT]
+  extern __shared__ float sm[];
+  const int nout = a.nout, B = a.B;
+  float* Xs = sm;                          // [B][kObCols + 1]
+  float* Gs = Xs + B * (kObCols + 1);      // [B][nout]
+  float* Ws = Gs + B * nout;               // [kObCols][nout]
   const int grp = blockIdx.y;
   const int mem = grp % a.n_members;
   if (a.active && !a.active[mem]) return;
+  const int i0 = blockIdx.x * kObCols;
   const float* X = a.X + (a.x_by_member ? mem : grp) * a.x_gs;
   const float* G = a.G + grp * a.g_gs;
   const float* W = a.W + grp * a.w_gs;
-  for (int e = threadIdx.x; e < a.B * NOUT; e += blockDim.x) {
-    const int b = e / NOUT, o = e % NOUT;
-    Gs[e] = o < a.nout ? G[static_cast<long long>(b) * a.g_ld + o] : 0.0f;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < B * kObCols; e += blockDim.x) {
+    const int b = e / kObCols, c = e % kObCols;
+    Xs[b * (kObCols + 1) + c] =
+        (i0 + c < a.H) ? X[static_cast<long long>(b) * a.x_ld + i0 + c] : 0.0f;
+  }
+  for (int e = tid; e < B * nout; e += blockDim.x) {
+    const int b = e / nout, o = e % nout;
+    Gs[e] = G[static_cast<long long>(b) * a.g_ld + o];
+  }
+  for (int e = tid; e < kObCols * nout; e += blockDim.x) {
+    const int c = e / nout, o = e % nout;
+    Ws[e] = (i0 + c < a.H) ? W[static_cast<long long>(i0 + c) * nout + o] : 0.0f;
   }
   __syncthreads();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
   float* dW = a.dW + grp * a.dw_gs;
-  if (i < NOUT && blockIdx.x == 0 && i < a.nout) {  // bias gradient
+  // dW: one thread per (i, o)
+  for (int e = tid; e < kObCols * nout; e += blockDim.x) {
+    const int c = e / nout, o = e % nout;
+    if (i0 + c >= a.H) continue;
     float acc = 0.0f;
-    for (int b = 0; b < a.B; ++b) acc += Gs[b * NOUT + i];
-    dW[static_cast<long long>(a.H) * a.nout + i] = acc;
+    for (int b = 0; b < B; ++b) acc = acc + Xs[b * (kObCols + 1) + c] * Gs[b * nout + o];
+    dW[static_cast<long long>(i0 + c) * nout + o] = acc;
   }
-  if (i >= a.H) return;
-  float w[NOUT], acc[NOUT];
-#pragma unroll
-  for (int o = 0; o < NOUT; ++o) {
-    w[o] = o < a.nout ? W[static_cast<long long>(i) * a.nout + o] : 0.0f;
-    acc[o] = 0.0f;
-  }
-  float* dX = a.dX ? a.dX + grp * a.dx_gs : nullptr;
-  for (int b0 = 0; b0 < a.B; b0 += 8) {
-    float x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      x[u] = (b0 + u < a.B) ? X[static_cast<long long>(b0 + u) * a.x_ld + i] : 0.0f;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int b = b0 + u;
-      if (b >= a.B) break;
-      const float* g = Gs + b * NOUT;
-      float d = 0.0f;
-#pragma unroll
-      for (int o = 0; o < NOUT; ++o) {
-        if (o < a.nout) {
-          acc[o] = acc[o] + x[u] * g[o];
-          d = d + g[o] * w[o];
-        }
-      }
-      if (dX) dX[static_cast<long long>(b) * a.dx_ld + i] = (x[u] > 0.0f) ? d : 0.0f;
+  // db: first column block only
+  if (blockIdx.x == 0) {
+    for (int o = tid; o < nout; o += blockDim.x) {
+      float acc = 0.0f;
+      for (int b = 0; b < B; ++b) acc += Gs[b * nout + o];
+      dW[static_cast<long long>(a.H) * nout + o] = acc;
     }
   }
-#pragma unroll
-  for (int o = 0; o < NOUT; ++o)
-    if (o < a.nout) dW[static_cast<long long>(i) * a.nout + o] = acc[o];
+  // dX: one thread per (b, i), columns fastest (coalesced stores)
+  if (a.dX) {
+    float* dX = a.dX + grp * a.dx_gs;
+    for (int e = tid; e < B * kObCols; e += blockDim.x) {
+      const int b = e / kObCols, c = e % kObCols;
+      if (i0 + c >= a.H) continue;
+      float d = 0.0f;
+      for (int o = 0; o < nout; ++o) d = d + Gs[b * nout + o] * Ws[c * nout + o];
+      dX[static_cast<long long>(b) * a.dx_ld + i0 + c] =
+          (Xs[b * (kObCols + 1) + c] > 0.0f) ? d : 0.0f;
+    }
+  }
 }
 
 void launch_out_backward(const OutBwdArgs& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_out_backward<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(k_out_backward<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(k_out_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
-  dim3 grid((a.H + 255) / 256, a.groups);
-  if (a.nout <= 1) {
-    k_out_backward<1><<<grid, 256, a.B * 1 * 4, s>>>(a);
-  } else if (a.nout <= 8) {
-    k_out_backward<8><<<grid, 256, a.B * 8 * 4, s>>>(a);
-  } else {
-    k_out_backward<16><<<grid, 256, a.B * 16 * 4, s>>>(a);
-  }
+  const size_t smem = (static_cast<size_t>(a.B) * (kObCols + 1) + static_cast<size_t>(a.B) * a.nout +
+                       kObCols * a.nout) * 4;
+  dim3 grid((a.H + kObCols - 1) / kObCols, a.groups);
+  k_out_backward<<<grid, 256, smem, s>>>(a);
 }
 
 void launch_fwd_skinny(const GemmArgs& g, cudaStream_t s) {

@@ -198,7 +198,11 @@ struct Pop {
   void mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
                    std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                    int last_epi, const int* active = nullptr, float* C2 = nullptr,
-                   long long c2_gs = 0, long long c2_ld = 0, bool noise = false);
+                   long long c2_gs = 0, long long c2_ld = 0, bool noise = false,
+                   bool keep_hidden = true);
+  bool gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, Mat H,
+                      bool keep_hidden, float* Y, long long y_gs, long long y_ld, int out_epi,
+                      const int* active, float* C2, long long c2_gs, long long c2_ld, bool noise);
   void mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
                     Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
                     const int* active);

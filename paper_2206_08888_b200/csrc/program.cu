@@ -285,7 +285,7 @@ Mat Pop::hid(std::vector<DBuf<float>>& v, int l, int B, const NetShape& sh, int 
 void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
                       std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                       int last_epi, const int* active, float* C2, long long c2_gs,
-                      long long c2_ld, bool noise) {
+                      long long c2_ld, bool noise, bool keep_hidden) {
   const int L = sh.depth;
   for (int l = 0; l < L; ++l) {
     if (l == L - 1) {
@@ -293,10 +293,68 @@ void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat
                noise);
     } else {
       const Mat h = hid(hs, l, B, sh, 0);
+      if (l == L - 2 && gemm_fwd_fused(sh, W, l, groups, B, x, h, keep_hidden, out, out_gs, out_ld,
+                                       last_epi, active, C2, c2_gs, c2_ld, noise))
+        return;  // the output layer ran in this layer's epilogue
       gemm_fwd(sh, W, l, groups, B, x, const_cast<float*>(h.p), h.gs, h.ld, EPI_BIAS_RELU, active);
       x = h;
     }
   }
+}
+
+// Last hidden layer + output layer in one tcgen05 launch (TF32 mode): the output layer's few
+// columns (1 or 2*act) are evaluated from the hidden row in the epilogue; the hidden activation
+// is written only when the backward pass needs it.  Returns false when not applicable.
+bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, int B, Mat X,
+                         Mat H, bool keep_hidden, float* Y, long long y_gs, long long y_ld,
+                         int out_epi, const int* active, float* C2, long long c2_gs,
+                         long long c2_ld, bool noise) {
+  const int in = sh.dims[l], hdim = sh.dims[l + 1], nout = sh.dims[l + 2];
+  const float* Wl = W + sh.woff[l];
+  if (!use_tc() || hdim < 16 || hdim > 256 || nout > 16 || !tma_ok(X.p, X.ld, X.gs) ||
+      !tma_ok(Wl, hdim, sh.stride))
+    return false;
+  TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
+              static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
+              static_cast<uint64_t>(X.gs)};
+  TcOperand Bw{Wl, static_cast<uint64_t>(hdim), static_cast<uint64_t>(in),
+               static_cast<uint64_t>(groups), static_cast<uint64_t>(hdim), sh.stride};
+  TcArgs a;
+  a.M = B;
+  a.N = hdim;
+  a.K = in;
+  a.groups = groups;
+  a.n_members = n;
+  a.a_by_member = X.by_member;
+  a.epi = EPI_BIAS_RELU;
+  a.C = const_cast<float*>(H.p);
+  a.c_gs = H.gs;
+  a.c_rs = H.ld;
+  a.bias = W + sh.boff[l];
+  a.bias_gs = static_cast<long long>(sh.stride);
+  a.active = active;
+  a.nout = nout;
+  a.ow = W + sh.woff[l + 1];
+  a.ow_gs = static_cast<long long>(sh.stride);
+  a.out_epi = out_epi;
+  a.oC = Y;
+  a.oc_gs = y_gs;
+  a.oc_rs = y_ld;
+  a.oC2 = C2;
+  a.oc2_gs = c2_gs;
+  a.oc2_rs = c2_ld;
+  a.out_scale = sh.out_scale;
+  a.store_hidden = keep_hidden ? 1 : 0;
+  if (noise) {
+    a.noise_key = key_a.p;
+    a.noise_sd = h_f2.p;
+    a.noise_clip = h_f3.p;
+    a.bound = bound;
+  }
+  const double flops = 2.0 * B * groups * (static_cast<double>(in) * hdim + hdim * nout);
+  timed(PC_GEMM_FWD, flops, 0.0, active != nullptr,
+        [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
+  return true;
 }
 
 // backward of `sh` from the top cotangent G: dW for every layer, dX for layers > 0
@@ -396,9 +454,9 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
   const Mat s2{S.in_s2a.p, nbB * lsa, lsa, 0};
   mlp_forward(pol, pol_t.p, n, B, s2, S.tp_h, S.in_s2a.p + ds, nbB * lsa, lsa,
-              EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true);
+              EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true, false);
   mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
-              nbB, 1, EPI_BIAS);
+              nbB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
   timed(PC_ELEM, 0.0, 0.0, 0,
         [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
   // twin critic update; target Polyak fused for members whose policy fires
@@ -434,13 +492,13 @@ void Pop::sac_step(int B) {
   });
   // sac_critic_target (algos.hpp:739-776): current policy on s2, eps' draws, twin targets
   mlp_forward(pol, pol_p.p, n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 0}, S.tp_h, S.head.p, nbB * hd,
-              hd, EPI_BIAS);
+              hd, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_head(n, B, ds, da, lsa, S.head.p, key_b.p, bound, S.in_s2a.p, nullptr, nullptr,
                     nullptr, nullptr, nullptr, S.logp2.p, stream);
   });
   mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
-              nbB, 1, EPI_BIAS);
+              nbB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_y(n, B, S.r.p, S.d.p, S.tq_out.p, S.logp2.p, log_alpha.p, h_f4.p, h_f3.p, S.y.p,
                  stream);

@@ -134,11 +134,23 @@ __global__ void __launch_bounds__(128, 2)
   uint64_t* tmem_full = empty + kMaxStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
+  // fused output layer: bias [BN] and W_out [BN][nout] staged after the barriers
+  float* fz_bias = reinterpret_cast<float*>(smem + kStages * STAGE + 256);
+  float* fz_w = fz_bias + BN;
+
   const int grp = blockIdx.z;
   const int mem = grp % g.n_members;
   if (g.active && !g.active[mem]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
+  const int nout = g.nout;
+  if (nout > 0) {
+    const float* bsrc = g.bias + grp * g.bias_gs;
+    const float* wsrc = g.ow + grp * g.ow_gs;
+    for (int e = threadIdx.x; e < BN; e += blockDim.x) fz_bias[e] = e < g.N ? bsrc[e] : 0.0f;
+    for (int e = threadIdx.x; e < BN * nout; e += blockDim.x)
+      fz_w[e] = e < g.N * nout ? wsrc[e] : 0.0f;
+  }
   const int ga = g.a_by_member ? mem : grp;
   const int gb = g.b_by_member ? mem : grp;
   const int nk = (g.K + kBK - 1) / kBK;
@@ -227,6 +239,73 @@ __global__ void __launch_bounds__(128, 2)
   const float* aux = g.aux ? g.aux + (g.aux_by_member ? mem : grp) * g.aux_gs : nullptr;
   const int epi = g.epi;
   constexpr int CW = BN < 32 ? BN : 32;  // chunk width
+  if (nout > 0) {
+    // hidden layer + output layer: thread = accumulator row; h = relu(acc + b) chunk by chunk,
+    // y[o] += h[j] * W_out[j][o] in ascending j; h optionally stored (transposed, coalesced)
+    float oacc[16];
+#pragma unroll
+    for (int o = 0; o < 16; ++o) oacc[o] = 0.0f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += CW) {
+      if (c0 >= g.N) break;
+      float v[32];
+      const uint32_t taddr =
+          tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c0);
+      tmem_ld16(taddr, v);
+      if (CW == 32) tmem_ld16(taddr + 16, v + 16);
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const float z = v[j] + fz_bias[c0 + j];
+        const float h = (c0 + j < g.N && z > 0.0f) ? z : 0.0f;
+        v[j] = h;
+        const float* wr = fz_w + (c0 + j) * nout;
+#pragma unroll
+        for (int o = 0; o < 16; ++o)
+          if (o < nout) oacc[o] = oacc[o] + h * wr[o];
+      }
+      if (g.store_hidden) {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) T[lane * 33 + j] = v[j];
+        __syncwarp();
+        const int col = n0 + c0 + lane;
+        if (lane < CW && col < g.N) {
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr) {
+            const int row = row0 + rr;
+            if (row < g.M) C[static_cast<long long>(row) * g.c_rs + col] = T[rr * 33 + lane];
+          }
+        }
+        __syncwarp();
+      }
+    }
+    const int row = row0 + lane;
+    if (row < g.M) {
+      const float* ob = fz_w + g.N * nout;  // b_out follows W_out in the arena row
+      const float* obg = g.ow + grp * g.ow_gs + static_cast<long long>(g.N) * nout;
+      (void)ob;
+      float* oC = g.oC + grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
+      const bool tanh_out = g.out_epi == EPI_BIAS_TANH || g.out_epi == EPI_BIAS_TANH_NOISE;
+#pragma unroll
+      for (int o = 0; o < 16; ++o) {
+        if (o >= nout) break;
+        const float y = oacc[o] + obg[o];
+        float r = y;
+        if (tanh_out) {
+          const float t = libm_tanhf(y);
+          if (g.oC2) g.oC2[grp * g.oc2_gs + static_cast<long long>(row) * g.oc2_rs + o] = t;
+          r = (g.out_scale != 1.0f) ? t * g.out_scale : t;
+          if (g.out_epi == EPI_BIAS_TANH_NOISE) {
+            const uint64_t e = static_cast<uint64_t>(row) * nout + o;
+            float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
+                        g.noise_sd[mem];
+            eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+            r = clampf_ref(r + eps, -g.bound, g.bound);
+          }
+        }
+        oC[o] = r;
+      }
+    }
+  } else
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += CW) {
     if (n0 + c0 >= g.N) break;
@@ -334,10 +413,11 @@ void load_encode() {
 }
 
 template <int BN>
-size_t smem_bytes(int stages) {
-  // stages, barriers, and at least the 4 x 32 x 33 float epilogue transpose tiles
+size_t smem_bytes(int stages, int nout) {
+  // stages (>= the 4 x 32 x 33 float epilogue transpose tiles), barriers, fused-output staging
   const size_t st = static_cast<size_t>(stages) * (kBM * kBK * 4 + BN * kBK * 4);
-  return std::max<size_t>(st, 4 * 32 * 33 * 4) + 1024 + 256;
+  return std::max<size_t>(st, 4 * 32 * 33 * 4) + 1024 + 256 +
+         (nout > 0 ? static_cast<size_t>(BN) * (1 + nout) * 4 : 0);
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -346,14 +426,15 @@ void launch_tpl(const CUtensorMap& a, const CUtensorMap& b, TcArgs g, cudaStream
   if (!attr_set) {
     CUDA_CHECK(cudaFuncSetAttribute(k_tc_gemm<BN, A_MN, B_MN>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem_bytes<BN>(kMaxStages))));
+                                    static_cast<int>(smem_bytes<BN>(kMaxStages, 16))));
     attr_set = true;
   }
   // pipeline depth: enough to cover K, capped so two CTAs share an SM (TMEM 2 x 256 columns)
   const int nk = (g.K + kBK - 1) / kBK;
   g.stages = std::max(1, std::min(nk, BN >= 256 ? 2 : 3));
   dim3 grid((g.N + BN - 1) / BN, (g.M + kBM - 1) / kBM, g.groups);
-  k_tc_gemm<BN, A_MN, B_MN><<<grid, 128, smem_bytes<BN>(g.stages), s>>>(a, b, g);
+  if (g.nout > 0 && (g.N > BN || g.nout > 16)) PBRL_THROW(PBRL_E_USAGE, "tc_gemm: bad fused output");
+  k_tc_gemm<BN, A_MN, B_MN><<<grid, 128, smem_bytes<BN>(g.stages, g.nout), s>>>(a, b, g);
 }
 
 template <bool A_MN, bool B_MN>

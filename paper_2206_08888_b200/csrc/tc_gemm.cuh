@@ -35,6 +35,19 @@ struct TcArgs {
   const float* noise_sd = nullptr;
   const float* noise_clip = nullptr;
   float bound = 1.0f;
+  // Fused output layer (requires the whole hidden width in one tile, N <= BN): the epilogue
+  // applies bias + ReLU to its hidden row h and evaluates y[o] = sum_j h[j] * ow[j][o] + ob[o]
+  // (j ascending) followed by out_epi; the hidden row is stored only if store_hidden.
+  int nout = 0;
+  const float* ow = nullptr;  // W_out [N][nout] of group g at ow + g * ow_gs; b_out follows it
+  long long ow_gs = 0;
+  int out_epi = 0;
+  float* oC = nullptr;
+  long long oc_gs = 0, oc_rs = 0;
+  float* oC2 = nullptr;
+  long long oc2_gs = 0, oc2_rs = 0;
+  float out_scale = 1.0f;
+  int store_hidden = 1;
 };
 
 // TMA requirements: 16-byte aligned base and strides.

@@ -1,0 +1,146 @@
+"""Population sharding across GPUs: the PBT exchange step (evolve.hpp:169-213) over
+torch.distributed (NCCL over NVLink/NVSwitch on the B200 box; gloo in the CPU tests).
+
+Each rank owns the contiguous member block [offset, offset + n_local) of an n_total population,
+with RNG streams keyed by GLOBAL member id, so a shard computes exactly what the unsharded
+population computes for those members and the update step needs no communication at all.  The
+one exchange is PBT, every pbt_interval updates:
+
+  1. all_gather of per-member fitness (mean of the last 10 returns, float64);
+  2. every rank computes the identical plan (stable rank + donor draws from the shared
+     RngSequence; on device via pbrl_pbt_plan);
+  3. exploit copies: a replaced member whose donor lives on another rank receives the donor's
+     full state blob (every network, plus log_alpha for SAC) with batched send/recv;
+     same-rank pairs are copied on device;
+  4. optimiser reset + delay reset on the owner (pbrl_pbt_apply) and the hyper re-draw: every
+     rank draws the same 6-value prior sample per replaced member (keeping the RngSequence in
+     lock-step) and applies the ones it owns.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib
+from .pbrl import (EvolvePlan, PBTState, RngSequence, member_blob_size, export_member,
+                   import_member)
+
+
+class DeviceShard:
+    """Adapter binding ShardedPBT to a population resident on this rank's GPU."""
+
+    def __init__(self, pop, hyper):
+        import torch
+        self.pop, self.hyper = pop, hyper
+        self.n_local = pop.n
+        self.offset = pop.member_offset
+        self.device = torch.device("cuda", pop.device)
+
+    def blob_size(self) -> int:
+        return member_blob_size(self.pop)
+
+    def new_blob(self):
+        import torch
+        return torch.empty(self.blob_size(), dtype=torch.float32, device=self.device)
+
+    def export(self, m_local: int, blob) -> None:
+        export_member(self.pop, m_local, blob.data_ptr())
+
+    def import_(self, m_local: int, blob) -> None:
+        import torch
+        torch.cuda.synchronize(self.device)
+        import_member(self.pop, m_local, blob.data_ptr())
+
+    def plan(self, fitness: np.ndarray, trunc: float, rng: RngSequence) -> Tuple[list, list]:
+        n = fitness.size
+        fit = np.ascontiguousarray(fitness, np.float64)
+        rep = np.zeros(n, np.uint64)
+        don = np.zeros(n, np.uint64)
+        nxt = C.c_uint64(rng.next)
+        cnt = C.c_uint32()
+        _lib.call("pbrl_pbt_plan", self.pop.handle, fit.ctypes.data_as(_lib.f64p), n, trunc,
+                  rng.stream.key, C.byref(nxt), rep.ctypes.data_as(_lib.u64p),
+                  don.ctypes.data_as(_lib.u64p), C.byref(cnt))
+        rng.next = nxt.value
+        c = cnt.value
+        return [int(x) for x in rep[:c]], [int(x) for x in don[:c]]
+
+    def apply(self, replaced: Sequence[int], donors: Sequence[int]) -> None:
+        rep = np.asarray(replaced, np.uint64)
+        don = np.asarray(donors, np.uint64)
+        _lib.call("pbrl_pbt_apply", self.pop.handle, rep.ctypes.data_as(_lib.u64p),
+                  don.ctypes.data_as(_lib.u64p), len(rep))
+
+    def set_hyper(self, m_local: int, one) -> None:
+        self.hyper.set_member(m_local, one)
+
+    def fitness_tensor(self, values: np.ndarray):
+        import torch
+        return torch.as_tensor(values, dtype=torch.float64, device=self.device)
+
+
+class ShardedPBT:
+    """The PBT exchange for one rank of a sharded population."""
+
+    def __init__(self, shard, n_total: int, group=None, truncation_fraction: float = 0.3):
+        import torch.distributed as dist
+        self.dist = dist
+        self.shard = shard
+        self.n_total = n_total
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.trunc = truncation_fraction
+        if n_total % self.world:
+            raise ValueError("population must split evenly over the ranks")
+        self.per_rank = n_total // self.world
+
+    def owner(self, member: int) -> int:
+        return member // self.per_rank
+
+    def gather_fitness(self, local: np.ndarray) -> np.ndarray:
+        import torch
+        t = self.shard.fitness_tensor(np.asarray(local, np.float64))
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return torch.cat(out).cpu().numpy()
+
+    def evolve(self, pbt_local: PBTState, rng: RngSequence, prior) -> Optional[EvolvePlan]:
+        """pbt_evolve_trainer for the sharded population.  pbt_local holds this rank's members'
+        return rings (local indices); returns the global plan (identical on every rank)."""
+        if self.n_total < 4:
+            return None
+        fitness = self.gather_fitness(pbt_local.fitness())
+        replaced, donors = self.shard.plan(fitness, self.trunc, rng)
+        lo = self.shard.offset
+        # exploit copies across ranks (batched point-to-point, one blob per remote pair)
+        ops, recv = [], []
+        for dst, src in zip(replaced, donors):
+            od, os_ = self.owner(dst), self.owner(src)
+            if od == os_:
+                continue
+            if os_ == self.rank:
+                blob = self.shard.new_blob()
+                self.shard.export(src - lo, blob)
+                ops.append(self.dist.P2POp(self.dist.isend, blob, od, self.group))
+            elif od == self.rank:
+                blob = self.shard.new_blob()
+                recv.append((dst - lo, blob))
+                ops.append(self.dist.P2POp(self.dist.irecv, blob, os_, self.group))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+        for m_local, blob in recv:
+            self.shard.import_(m_local, blob)
+        # local copies + optimiser / delay reset of the local receivers
+        self.shard.apply(replaced, donors)
+        # hyper re-draw: every rank draws for every replaced member (RngSequence in lock-step)
+        for dst in replaced:
+            one = prior.sample_member(rng)
+            if self.owner(dst) == self.rank:
+                self.shard.set_hyper(dst - lo, one)
+                pbt_local.returns[dst - lo].clear()
+        pbt_local.steps_since_evolve = 0
+        return EvolvePlan(list(replaced), list(donors))

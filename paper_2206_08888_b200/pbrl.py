@@ -19,7 +19,7 @@ import ctypes as C
 import math
 from collections import deque
 from dataclasses import dataclass, field
-from typing import Callable, List, Optional, Sequence
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -697,3 +697,20 @@ def export_member(pop: _Population, member: int, dev_ptr: int) -> None:
 
 def import_member(pop: _Population, member: int, dev_ptr: int) -> None:
     _lib.call("pbrl_import_member", pop.handle, member, C.c_void_p(dev_ptr))
+
+
+def plan_from_fitness(fitness: Sequence[float], trunc: float, rng: RngSequence
+                      ) -> Tuple[List[int], List[int]]:
+    """pbt_plan (evolve.hpp:133-145) on the host from per-member fitness: stable rank (best
+    first, ties toward the lower index), bottom ceil(trunc*N) replaced by donors drawn uniformly
+    from the top ceil(trunc*N).  Same semantics as the device kernel behind pbrl_pbt_plan."""
+    n = len(fitness)
+    if n < 4:
+        return [], []
+    order = sorted(range(n), key=lambda i: (-fitness[i], i))
+    cut = int(math.ceil(trunc * n))
+    replaced, donors = [], []
+    for i in range(cut):
+        replaced.append(order[n - 1 - i])
+        donors.append(order[rng.index(cut)])
+    return replaced, donors

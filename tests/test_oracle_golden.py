@@ -1,0 +1,101 @@
+"""The C restatement oracle against golden vectors produced by the unmodified reference build
+(tests/golden/, written by oracle/make_golden.py).  Runs without /root/reference and without a
+GPU, so the checker used by the GPU parity tests is pinned on every machine."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from helpers import SAC_NETS, TD3_NETS, bits_equal, raw_at
+
+GOLD = Path(__file__).resolve().parent / "golden"
+
+
+def _load(name):
+    p = GOLD / f"{name}.npz"
+    if not p.exists():
+        pytest.skip(f"{p} missing (python oracle/make_golden.py)")
+    return np.load(p)
+
+
+@pytest.mark.parametrize("name", ["td3_small", "td3_halfcheetah"])
+def test_td3_golden(ora, name):
+    g = _load(name)
+    n, ds, da, B, K = (int(g[k]) for k in ("n", "ds", "da", "B", "K"))
+    st = ora.td3(n, ds, da, [int(h) for h in g["hidden"]], float(g["bound"]), int(g["seed"]))
+    for k in TD3_NETS:
+        assert bits_equal(st.get_net(k), g[f"init_{k}"]), k
+    hy = {f[len("hyper_"):]: list(g[f]) for f in g.files if f.startswith("hyper_")}
+    raw = ora.synthetic_batches(K, n, B, ds, da, int(g["bseed"]))
+    for k in range(K):
+        lo = st.step(raw_at(raw, k), hy)
+        assert lo[0].sum() == pytest.approx(g["losses"][k][0], rel=1e-12)
+        assert lo[1].sum() == pytest.approx(g["losses"][k][1], rel=1e-12)
+    for k in TD3_NETS:
+        assert bits_equal(st.get_net(k), g[f"final_{k}"]), k
+    for k in ("policy", "critic1", "critic2"):
+        for m in range(n):
+            mo, vo, t = st.get_adam(k, m)
+            assert bits_equal(mo, g[f"adam_m_{k}"][m]) and bits_equal(vo, g[f"adam_v_{k}"][m])
+            assert t == g[f"adam_t_{k}"][m]
+    da_, steps = st.counters()
+    assert np.array_equal(da_, g["delay_acc"]) and np.array_equal(steps, g["steps"])
+
+
+def test_sac_golden(ora):
+    g = _load("sac_small")
+    n, ds, da, B, K = (int(g[k]) for k in ("n", "ds", "da", "B", "K"))
+    st = ora.sac(n, ds, da, [int(h) for h in g["hidden"]], 1.0, int(g["seed"]))
+    from oracle.oracle import sac_defaults
+    hy = sac_defaults(n, da)
+    raw = ora.synthetic_batches(K, n, B, ds, da, int(g["bseed"]))
+    for k in range(K):
+        st.step(raw_at(raw, k), hy)
+    for k in SAC_NETS:
+        assert bits_equal(st.get_net(k), g[f"final_{k}"]), k
+    la, am, av, at, steps = st.counters()
+    assert bits_equal(la, g["log_alpha"]) and bits_equal(am, g["alpha_m"])
+    assert np.array_equal(at, g["alpha_t"]) and np.array_equal(steps, g["steps"])
+
+
+def test_rng_golden(ora):
+    g = _load("rng")
+    for row, uni, nrm in zip(g["keys"], g["uniform"], g["normal"]):
+        seed, stream, use, step, key = (int(x) for x in row)
+        assert ora.stream_key(seed, stream, use, step) == key
+        assert [ora.uniform(key, c) for c in range(16)] == list(uni)
+        assert [ora.normal_pair(key, 2 * c) for c in range(16)] == list(nrm)
+
+
+def test_replay_golden(ora):
+    g = _load("replay")
+    n, cap, B = 3, int(g["cap"]), int(g["B"])
+    bufs = [ora.replay(cap, 4, 2) for _ in range(n)]
+    for i, m in enumerate(g["member"]):
+        bufs[m].push(g["s"][i], g["a"][i], g["r"][i], g["s2"][i], g["d"][i], int(m))
+    for draw in (0, 3):
+        got = ora.sample_batch(bufs, B, 0, n, 77, [0, 1, 2], draw)
+        for x, k in zip(got[:5], ("s", "a", "r", "s2", "d")):
+            assert bits_equal(x, g[f"draw{draw}_{k}"])
+
+
+def test_pbt_golden(ora):
+    g = _load("pbt")
+    for n in (4, 10, 33, 80):
+        rings, counts = g[f"n{n}_rings"], g[f"n{n}_counts"]
+        assert np.array_equal(ora.pbt_rank(rings, counts), g[f"n{n}_order"])
+        rep, don, nxt = ora.pbt_plan(rings, counts, 0.3, int(g[f"n{n}_key"]), 7)
+        assert np.array_equal(rep, g[f"n{n}_replaced"]) and np.array_equal(don, g[f"n{n}_donors"])
+        assert nxt == int(g[f"n{n}_next"])
+
+
+def test_tanhf_golden():
+    """The libm tanhf the reference calls (glibc fdlibm) == the fixture; the device port of the
+    same algorithm is checked on the GPU in test_gpu_numerics.py."""
+    import ctypes as C
+    g = _load("tanhf")
+    libm = C.CDLL("libm.so.6")
+    libm.tanhf.restype = C.c_float
+    libm.tanhf.argtypes = [C.c_float]
+    got = np.asarray([libm.tanhf(float(v)) for v in g["x"]], np.float32)
+    assert bits_equal(got, g["y"])
