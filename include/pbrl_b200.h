@@ -181,6 +181,13 @@ int pbrl_selftest_tc_gemm(int a_mn, int b_mn, int M, int N, int K, int groups, c
                           long long a_ld, long long a_gs, const float* B, long long b_ld,
                           long long b_gs, float* C, long long c_ld, long long c_gs);
 
+/* Phase timeline of the tcgen05 GEMM launches recorded since process start when the environment
+ * variable PBRL_TC_TRACE is set (diagnostics only; off by default).  Copies up to max_launches
+ * launches: stamps[launch][160][64] (globaltimer ns per CTA: entry, setup, per tile producer /
+ * MMA start / MMA commit / epilogue start / epilogue end, drain, exit) and meta[launch][10]
+ * (BN, A MN-major, B MN-major, fused n_out, M, N, K, groups, epilogue, 0); *n = launches copied. */
+int pbrl_debug_tc_trace(uint64_t* stamps, int* meta, int max_launches, int* n);
+
 /* ---- observability */
 int pbrl_launch_count(pbrl_pop* pop, uint64_t* launches); /* kernels launched (cf. kernel_invocations, pop_tensor.hpp:21-28) */
 int pbrl_synchronize(pbrl_pop* pop);

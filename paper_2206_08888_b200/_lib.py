@@ -68,6 +68,7 @@ SIGNATURES = {
     "pbrl_export_member": [vp, u64, vp],
     "pbrl_import_member": [vp, u64, vp],
     "pbrl_launch_count": [vp, u64p],
+    "pbrl_debug_tc_trace": [u64p, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int)],
     "pbrl_synchronize": [vp],
     "pbrl_get_stream": [vp, C.POINTER(vp)],
     "pbrl_profile_begin": [vp],

@@ -668,6 +668,15 @@ int pbrl_selftest_tc_gemm(int a_mn, int b_mn, int M, int N, int K, int groups, c
   });
 }
 
+int pbrl_debug_tc_trace(uint64_t* stamps, int* meta, int max_launches, int* n) {
+  return guarded([&] {
+    if (!stamps || !meta || !n || max_launches < 0) PBRL_THROW(PBRL_E_USAGE, "null argument");
+    std::vector<TcTraceMeta> m(static_cast<size_t>(max_launches));
+    *n = tc_trace_dump(reinterpret_cast<unsigned long long*>(stamps), m.data(), max_launches);
+    for (int i = 0; i < *n; ++i) std::memcpy(meta + 10 * i, &m[i], sizeof(TcTraceMeta));
+  });
+}
+
 int pbrl_launch_count(pbrl_pop* pop, uint64_t* launches) {
   (void)pop;
   *launches = g_launches.load();

@@ -281,79 +281,135 @@ __global__ void __launch_bounds__(128) k_dw_skinny(const GemmArgs g) {
 //   dW[i][o] = sum_b X[b][i] G[b][o]      (b ascending, from +0: pop_tensor.hpp:194-206)
 //   db[o]    = sum_b G[b][o]              (b ascending: :244-246)
 //   dX[b][i] = X[b][i] > 0 ? sum_o G[b][o] W[i][o] : 0   (o ascending; relu' of the layer below)
-// One block per (group, 32 input features): the X column tile [B][32] and G [B][nout] are staged
-// in shared memory with coalesced loads, then every sequential reduction runs out of smem.
-constexpr int kObCols = 32;
+// One block per (group, 64 input features).  Thread (column i, row slice s) streams its rows of
+// X once: dW partials stay in registers, dX is produced and stored on the fly, W[i][:] sits in
+// registers and G in shared memory (broadcast reads).  Exact mode uses one slice (b ascending in
+// a single accumulator, the reference order); the fast mode splits B into kObSlices slices whose
+// partials are combined in slice order through shared memory (deterministic).
+constexpr int kObCols = 64, kObSlices = 4;
 
-__global__ void __launch_bounds__(256) k_out_backward(OutBwdArgs a) {
+template <int NO>  // fused output width: exact for 1 / 6 / 12, runtime-guarded up to 16
+__global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs a) {
   extern __shared__ float sm[];
-  const int nout = a.nout, B = a.B;
-  float* Xs = sm;                          // [B][kObCols + 1]
-  float* Gs = Xs + B * (kObCols + 1);      // [B][nout]
-  float* Ws = Gs + B * nout;               // [kObCols][nout]
+  constexpr int NA = NO;
+  const int nout = NO < 16 ? NO : a.nout, B = a.B;
+  float* Gs = sm;                         // [B][nout]
+  float* Ps = Gs + B * nout;              // [kObSlices][kObCols][nout] dW partials
   const int grp = blockIdx.y;
   const int mem = grp % a.n_members;
   if (a.active && !a.active[mem]) return;
-  const int i0 = blockIdx.x * kObCols;
+  const int slices = blockDim.x / kObCols;
+  const int col = threadIdx.x % kObCols, sl = threadIdx.x / kObCols;
+  const int i = blockIdx.x * kObCols + col;
   const float* X = a.X + (a.x_by_member ? mem : grp) * a.x_gs;
   const float* G = a.G + grp * a.g_gs;
   const float* W = a.W + grp * a.w_gs;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < B * kObCols; e += blockDim.x) {
-    const int b = e / kObCols, c = e % kObCols;
-    Xs[b * (kObCols + 1) + c] =
-        (i0 + c < a.H) ? X[static_cast<long long>(b) * a.x_ld + i0 + c] : 0.0f;
-  }
-  for (int e = tid; e < B * nout; e += blockDim.x) {
-    const int b = e / nout, o = e % nout;
+  for (int e = threadIdx.x; e < B * nout; e += blockDim.x) {
+    const int b = e / nout, o = e - b * nout;
     Gs[e] = G[static_cast<long long>(b) * a.g_ld + o];
   }
-  for (int e = tid; e < kObCols * nout; e += blockDim.x) {
-    const int c = e / nout, o = e % nout;
-    Ws[e] = (i0 + c < a.H) ? W[static_cast<long long>(i0 + c) * nout + o] : 0.0f;
+  float w[NA], acc[NA];
+#pragma unroll
+  for (int o = 0; o < NA; ++o) {
+    acc[o] = 0.0f;
+    w[o] = (o < nout && i < a.H) ? W[static_cast<long long>(i) * nout + o] : 0.0f;
   }
   __syncthreads();
-  float* dW = a.dW + grp * a.dw_gs;
-  // dW: one thread per (i, o)
-  for (int e = tid; e < kObCols * nout; e += blockDim.x) {
-    const int c = e / nout, o = e % nout;
-    if (i0 + c >= a.H) continue;
-    float acc = 0.0f;
-    for (int b = 0; b < B; ++b) acc = acc + Xs[b * (kObCols + 1) + c] * Gs[b * nout + o];
-    dW[static_cast<long long>(i0 + c) * nout + o] = acc;
-  }
-  // db: first column block only
-  if (blockIdx.x == 0) {
-    for (int o = tid; o < nout; o += blockDim.x) {
-      float acc = 0.0f;
-      for (int b = 0; b < B; ++b) acc += Gs[b * nout + o];
-      dW[static_cast<long long>(a.H) * nout + o] = acc;
+  const int rows = (B + slices - 1) / slices;
+  const int b0 = sl * rows, b1 = min(B, b0 + rows);
+  float* dX = a.dX ? a.dX + grp * a.dx_gs : nullptr;
+  if (i < a.H) {
+    constexpr int U = 8;  // independent loads in flight per thread
+    int b = b0;
+    for (; b + U <= b1; b += U) {
+      float xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = __ldg(X + static_cast<long long>(b + u) * a.x_ld + i);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float* g = Gs + (b + u) * nout;
+        float d = 0.0f;
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          if (NO == 16 && o >= nout) break;
+          acc[o] = acc[o] + xv[u] * g[o];
+          d = d + g[o] * w[o];
+        }
+        if (dX) dX[static_cast<long long>(b + u) * a.dx_ld + i] = xv[u] > 0.0f ? d : 0.0f;
+      }
+    }
+    for (; b < b1; ++b) {
+      const float xv = __ldg(X + static_cast<long long>(b) * a.x_ld + i);
+      const float* g = Gs + b * nout;
+      float d = 0.0f;
+#pragma unroll
+      for (int o = 0; o < NA; ++o) {
+        if (NO == 16 && o >= nout) break;
+        acc[o] = acc[o] + xv * g[o];
+        d = d + g[o] * w[o];
+      }
+      if (dX) dX[static_cast<long long>(b) * a.dx_ld + i] = xv > 0.0f ? d : 0.0f;
     }
   }
-  // dX: one thread per (b, i), columns fastest (coalesced stores)
-  if (a.dX) {
-    float* dX = a.dX + grp * a.dx_gs;
-    for (int e = tid; e < B * kObCols; e += blockDim.x) {
-      const int b = e / kObCols, c = e % kObCols;
-      if (i0 + c >= a.H) continue;
-      float d = 0.0f;
-      for (int o = 0; o < nout; ++o) d = d + Gs[b * nout + o] * Ws[c * nout + o];
-      dX[static_cast<long long>(b) * a.dx_ld + i0 + c] =
-          (Xs[b * (kObCols + 1) + c] > 0.0f) ? d : 0.0f;
+  float* dW = a.dW + grp * a.dw_gs;
+  if (slices > 1) {
+#pragma unroll
+    for (int o = 0; o < NA; ++o)
+      if (o < nout) Ps[(sl * kObCols + col) * nout + o] = acc[o];
+    __syncthreads();
+    for (int e = threadIdx.x; e < kObCols * nout; e += blockDim.x) {
+      const int c = e / nout, o = e - c * nout;
+      if (blockIdx.x * kObCols + c >= a.H) continue;
+      float t = Ps[c * nout + o];
+      for (int q = 1; q < slices; ++q) t += Ps[(q * kObCols + c) * nout + o];
+      dW[static_cast<long long>(blockIdx.x * kObCols + c) * nout + o] = t;
+    }
+  } else if (i < a.H) {
+#pragma unroll
+    for (int o = 0; o < NA; ++o)
+      if (o < nout) dW[static_cast<long long>(i) * nout + o] = acc[o];
+  }
+  if (blockIdx.x == 0) {  // db: b ascending (exact) / warp tree (fast)
+    if (a.exact) {
+      for (int o = threadIdx.x; o < nout; o += blockDim.x) {
+        float t = 0.0f;
+        for (int b = 0; b < B; ++b) t += Gs[b * nout + o];
+        dW[static_cast<long long>(a.H) * nout + o] = t;
+      }
+    } else {
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      for (int o = warp; o < nout; o += blockDim.x >> 5) {
+        float t = 0.0f;
+        for (int b = lane; b < B; b += 32) t += Gs[b * nout + o];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (lane == 0) dW[static_cast<long long>(a.H) * nout + o] = t;
+      }
     }
   }
 }
 
-void launch_out_backward(const OutBwdArgs& a, cudaStream_t s) {
+template <int NO>
+static void launch_ob(const OutBwdArgs& a, cudaStream_t s) {
+  const int slices = a.exact ? 1 : kObSlices;
+  const size_t smem = (static_cast<size_t>(a.B) * a.nout + kObSlices * kObCols * a.nout) * 4;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_out_backward, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_out_backward<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr = true;
   }
-  const size_t smem = (static_cast<size_t>(a.B) * (kObCols + 1) + static_cast<size_t>(a.B) * a.nout +
-                       kObCols * a.nout) * 4;
   dim3 grid((a.H + kObCols - 1) / kObCols, a.groups);
-  k_out_backward<<<grid, 256, smem, s>>>(a);
+  k_out_backward<NO><<<grid, kObCols * slices, smem, s>>>(a);
+}
+
+void launch_out_backward(const OutBwdArgs& a, cudaStream_t s) {
+  switch (a.nout) {
+    case 1: launch_ob<1>(a, s); return;
+    case 6: launch_ob<6>(a, s); return;
+    case 12: launch_ob<12>(a, s); return;
+    default: launch_ob<16>(a, s); return;
+  }
 }
 
 void launch_fwd_skinny(const GemmArgs& g, cudaStream_t s) {
@@ -512,38 +568,84 @@ void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, doubl
 // adam_step_inplace (pop_tensor.hpp:328-366) with the bias corrections looked up from
 // host-computed tables (corr[t] = (float)(1 - pow(beta, t)) in double, exactly :347-350), and
 // the target update tgt = (T)tau*on + (T)(1-tau)*tgt (:422-426) fused on the fresh parameter.
-__global__ void k_adam(int n, size_t P, size_t stride, float* __restrict__ p,
-                       float* __restrict__ mo, float* __restrict__ vo,
-                       const float* __restrict__ g, const int64_t* t, const float* corr1,
-                       const float* corr2, const float* lr, const int* active,
-                       float* __restrict__ tgt, const float* tau_a, const float* tau_b,
-                       const int* polyak_gate) {
+struct AdamScalars {
+  float b1, b2, c1, c2, step, epsv, ta, tb;
+  bool polyak;
+};
+
+__device__ __forceinline__ float adam_one(const AdamScalars& a, float& p, float& mo, float& vo,
+                                          float gk) {
+  const float mk = a.b1 * mo + (1.0f - a.b1) * gk;
+  const float vk = a.b2 * vo + (1.0f - a.b2) * gk * gk;
+  mo = mk;
+  vo = vk;
+  const float mhat = mk / a.c1;
+  const float vhat = vk / a.c2;
+  p = p - a.step * mhat / (sqrtf(vhat) + a.epsv);
+  return p;
+}
+
+// Member rows start 256-byte aligned (stride = P rounded up to 64), so each row is processed as
+// float4 vectors (5 x 128-bit loads, 3-4 x 128-bit stores per thread) plus a scalar tail.
+__global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
+                                              float* __restrict__ p, float* __restrict__ mo,
+                                              float* __restrict__ vo, const float* __restrict__ g,
+                                              const int64_t* t, const float* corr1,
+                                              const float* corr2, const float* lr,
+                                              const int* active, float* __restrict__ tgt,
+                                              const float* tau_a, const float* tau_b,
+                                              const int* polyak_gate) {
   const int grp = blockIdx.y;
   const int m = grp % n;
   if (active && !active[m]) return;
   const long long base = static_cast<long long>(grp) * stride;
-  const float b1 = static_cast<float>(0.9);
-  const float b2 = static_cast<float>(0.999);
-  const float c1 = corr1[t[grp]];
-  const float c2 = corr2[t[grp]];
-  const float step = lr[m];
-  const float epsv = static_cast<float>(1e-8);
-  const bool do_polyak = tgt && (!polyak_gate || polyak_gate[m]);
-  const float ta = do_polyak ? tau_a[m] : 0.0f;
-  const float tb = do_polyak ? tau_b[m] : 0.0f;
-  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < P;
+  AdamScalars a;
+  a.b1 = static_cast<float>(0.9);
+  a.b2 = static_cast<float>(0.999);
+  a.c1 = corr1[t[grp]];
+  a.c2 = corr2[t[grp]];
+  a.step = lr[m];
+  a.epsv = static_cast<float>(1e-8);
+  a.polyak = tgt && (!polyak_gate || polyak_gate[m]);
+  a.ta = a.polyak ? tau_a[m] : 0.0f;
+  a.tb = a.polyak ? tau_b[m] : 0.0f;
+  const size_t P4 = P / 4;
+  float4* p4 = reinterpret_cast<float4*>(p + base);
+  float4* m4 = reinterpret_cast<float4*>(mo + base);
+  float4* v4 = reinterpret_cast<float4*>(vo + base);
+  const float4* g4 = reinterpret_cast<const float4*>(g + base);
+  float4* t4 = a.polyak ? reinterpret_cast<float4*>(tgt + base) : nullptr;
+  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < P4;
        k += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const long long e = base + static_cast<long long>(k);
-    const float gk = g[e];
-    const float mk = b1 * mo[e] + (1.0f - b1) * gk;
-    const float vk = b2 * vo[e] + (1.0f - b2) * gk * gk;
-    mo[e] = mk;
-    vo[e] = vk;
-    const float mhat = mk / c1;
-    const float vhat = vk / c2;
-    const float pk = p[e] - step * mhat / (sqrtf(vhat) + epsv);
-    p[e] = pk;
-    if (do_polyak) tgt[e] = ta * pk + tb * tgt[e];
+    float4 pv = p4[k], mv = m4[k], vv = v4[k];
+    const float4 gv = g4[k];
+    float4 tv;
+    if (a.polyak) tv = t4[k];
+    adam_one(a, pv.x, mv.x, vv.x, gv.x);
+    adam_one(a, pv.y, mv.y, vv.y, gv.y);
+    adam_one(a, pv.z, mv.z, vv.z, gv.z);
+    adam_one(a, pv.w, mv.w, vv.w, gv.w);
+    p4[k] = pv;
+    m4[k] = mv;
+    v4[k] = vv;
+    if (a.polyak) {
+      tv.x = a.ta * pv.x + a.tb * tv.x;
+      tv.y = a.ta * pv.y + a.tb * tv.y;
+      tv.z = a.ta * pv.z + a.tb * tv.z;
+      tv.w = a.ta * pv.w + a.tb * tv.w;
+      t4[k] = tv;
+    }
+  }
+  if (blockIdx.x == 0) {
+    for (size_t k = P4 * 4 + threadIdx.x; k < P; k += blockDim.x) {
+      const long long e = base + static_cast<long long>(k);
+      float pk = p[e], mk = mo[e], vk = vo[e];
+      adam_one(a, pk, mk, vk, g[e]);
+      p[e] = pk;
+      mo[e] = mk;
+      vo[e] = vk;
+      if (a.polyak) tgt[e] = a.ta * pk + a.tb * tgt[e];
+    }
   }
 }
 
@@ -552,7 +654,7 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
                  const float* lr, const int* active, float* tgt, const float* tau_a,
                  const float* tau_b, const int* polyak_gate, cudaStream_t s) {
   const int threads = 256;
-  int bx = static_cast<int>((P + threads * 4 - 1) / (threads * 4));
+  int bx = static_cast<int>((P / 4 + threads - 1) / threads);
   bx = bx < 1 ? 1 : bx;
   dim3 grid(bx, groups);
   k_adam<<<grid, threads, 0, s>>>(n, P, stride, p, m, v, g, t, corr1, corr2, lr, active, tgt,
@@ -598,6 +700,54 @@ void launch_colsum(int groups, int n, int B, int N, const float* G, long long g_
                    float* dst, long long dst_gs, const int* active, cudaStream_t s) {
   dim3 grid((N + 31) / 32, groups);
   k_colsum<<<grid, 256, 0, s>>>(n, B, N, G, g_gs, g_ld, dst, dst_gs, active);
+}
+
+// one thread per (group, row, 32-column word)
+__global__ void k_mask_bits(int groups, int B, int H, int mw, const float* h, long long h_gs,
+                            long long h_ld, uint32_t* mask, long long m_gs, long long m_ld,
+                            const int* active, int n) {
+  const long long total = static_cast<long long>(groups) * B * mw;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int w = static_cast<int>(e % mw);
+    const long long gr = e / mw;
+    const int r = static_cast<int>(gr % B), grp = static_cast<int>(gr / B);
+    if (active && !active[grp % n]) continue;
+    const float* row = h + grp * h_gs + static_cast<long long>(r) * h_ld;
+    uint32_t bits = 0u;
+    for (int j = 0; j < 32 && 32 * w + j < H; ++j) bits |= (row[32 * w + j] > 0.0f ? 1u : 0u) << j;
+    mask[grp * m_gs + static_cast<long long>(r) * m_ld + w] = bits;
+  }
+}
+
+void launch_mask_bits(int groups, int B, int H, const float* h, long long h_gs, long long h_ld,
+                      uint32_t* mask, long long m_gs, long long m_ld, const int* active, int n,
+                      cudaStream_t s) {
+  const int mw = (H + 31) / 32;
+  const long long total = static_cast<long long>(groups) * B * mw;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 8));
+  k_mask_bits<<<blocks, 256, 0, s>>>(groups, B, H, mw, h, h_gs, h_ld, mask, m_gs, m_ld, active,
+                                     n);
+}
+
+__global__ void k_td3_target_noise(int n, int B, int da, const uint64_t* key, const float* sd,
+                                   const float* clip, float* eps) {
+  const long long per = static_cast<long long>(B) * da;
+  const long long total = per * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(e / per);
+    const uint64_t i = static_cast<uint64_t>(e - m * per);  // b * da + o
+    const float v = static_cast<float>(rng_normal_pair(key[m], 2 * i)) * sd[m];
+    eps[e] = clampf_ref(v, -clip[m], clip[m]);
+  }
+}
+
+void launch_td3_target_noise(int n, int B, int da, const uint64_t* key, const float* sd,
+                             const float* clip, float* eps, cudaStream_t s) {
+  const long long total = static_cast<long long>(n) * B * da;
+  const int blocks = static_cast<int>(std::min<long long>((total + 127) / 128, 148 * 16));
+  k_td3_target_noise<<<blocks, 128, 0, s>>>(n, B, da, key, sd, clip, eps);
 }
 
 __global__ void k_fill(float* p, size_t count, float v) {

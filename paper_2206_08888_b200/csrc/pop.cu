@@ -8,6 +8,7 @@
 // Each member row holds its parameters in flatten_member order (net_pop.hpp:162-173), so
 // get/set_member and PBT copies are single contiguous row copies.
 #include "pop_impl.cuh"
+#include "tc_gemm.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -66,6 +67,7 @@ Pop::Pop(const pbrl_pop_desc& d) {
   }
   CUDA_CHECK(cudaSetDevice(device));
   CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  tc_trace_init();
 
   std::vector<size_t> pd{static_cast<size_t>(ds)};
   pd.insert(pd.end(), hidden.begin(), hidden.end());
@@ -274,7 +276,8 @@ void Pop::ensure_scratch(int B) {
   S.bs2.alloc(nb * ds);
   S.bd.alloc(nb);
   for (int l = 0; l + 1 < L; ++l) {
-    const size_t h = static_cast<size_t>(pad4(pol.dims[l + 1]));
+    // activations [rows][pad4(H)] + the ReLU mask bits [rows][ceil(H / 32)] (see Pop::hid)
+    const size_t h = static_cast<size_t>(pad4(pol.dims[l + 1])) + (pol.dims[l + 1] + 31) / 32;
     for (auto* v : {&S.tp_h, &S.ph, &S.pdh}) {
       v->emplace_back();
       v->back().alloc(nb * h);
@@ -284,6 +287,7 @@ void Pop::ensure_scratch(int B) {
       v->back().alloc(2 * nb * h);
     }
   }
+  if (algo == PBRL_ALGO_TD3) S.tnoise.alloc(nb * da);
   if (algo == PBRL_ALGO_SAC) {
     S.x.alloc(nb * da);
     S.th.alloc(nb * da);

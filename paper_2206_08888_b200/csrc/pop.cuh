@@ -101,6 +101,7 @@ struct OutBwdArgs {
   float* dX = nullptr;       // [groups][B][dx_ld] (nullptr: input layer, no dX)
   long long dx_gs = 0, dx_ld = 0;
   const int* active = nullptr;
+  int exact = 1;  // 1: reference summation order (FFMA32); 0: warp-parallel tree (TF32)
 };
 void launch_out_backward(const OutBwdArgs& a, cudaStream_t s);
 
@@ -136,6 +137,16 @@ void launch_fill(float* p, size_t count, float v, cudaStream_t s);
 // bias gradient of a layer: dst[g][o] = sum_b G[g][b][o] in row order (groups gated by active)
 void launch_colsum(int groups, int n, int B, int N, const float* G, long long g_gs, long long g_ld,
                    float* dst, long long dst_gs, const int* active, cudaStream_t s);
+
+// ReLU mask bits of a hidden activation (TF32 mode, CUDA-core fallback layers):
+// mask[g][r][w] bit j = (h[g][r][32w + j] > 0)
+void launch_mask_bits(int groups, int B, int H, const float* h, long long h_gs, long long h_ld,
+                      uint32_t* mask, long long m_gs, long long m_ld, const int* active, int n,
+                      cudaStream_t s);
+// TD3 target-policy smoothing noise for the fused tcgen05 epilogue (algos.hpp:252-262):
+// eps[m][b][o] = clamp((T)normal(key_m, 2 (b da + o)) * sd_m, -clip_m, clip_m)
+void launch_td3_target_noise(int n, int B, int da, const uint64_t* key, const float* sd,
+                             const float* clip, float* eps, cudaStream_t s);
 
 // SAC
 void launch_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2, int64_t* t_alpha,

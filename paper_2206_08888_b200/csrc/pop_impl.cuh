@@ -64,7 +64,7 @@ struct Scratch {
   DBuf<float> in_sa, in_s2a, sa_pi, r, d, y, tq_out, q, dq, qpi, gq, pt, ga, head, gtop;
   DBuf<float> bs, ba, br, bs2, bd;  // staged batch
   std::vector<DBuf<float>> tp_h, ph, pdh, tq_h, ch, dh, qh, qdh;
-  DBuf<float> x, th, ls, eps, logp, logp2, lw;
+  DBuf<float> x, th, ls, eps, logp, logp2, lw, tnoise;
   DBuf<uint8_t> clamped;
 };
 
@@ -98,6 +98,9 @@ struct Mat {
   long long gs = 0;
   long long ld = 0;
   int by_member = 0;
+  // TF32 mode, hidden activations: ReLU mask bits [groups][rows][mld] next to the activations
+  uint32_t* mask = nullptr;
+  long long mgs = 0, mld = 0;
 };
 
 inline int pad4(int x) { return (x + 3) / 4 * 4; }
@@ -189,7 +192,7 @@ struct Pop {
   void gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, float* Y,
                 long long y_gs, long long y_ld, int epi, const int* active = nullptr,
                 float* C2 = nullptr, long long c2_gs = 0, long long c2_ld = 0,
-                bool noise = false);
+                bool noise = false, const Mat* ymask = nullptr);
   void gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Mat G, Mat aux,
                float* DX, long long dx_gs, long long dx_ld, int epi, int col0, int ncols,
                const int* active, float scale);

@@ -25,7 +25,7 @@ Operand simt_op(const float* p, long long gs, long long rs, long long cs, int by
 // forward of layer l: Y = act(X W_l + b_l); X is [groups][B][in] (stride X.ld)
 void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, float* Y,
                    long long y_gs, long long y_ld, int epi, const int* active, float* C2,
-                   long long c2_gs, long long c2_ld, bool noise) {
+                   long long c2_gs, long long c2_ld, bool noise, const Mat* ymask) {
   const int in = sh.dims[l], out = sh.dims[l + 1];
   const float* Wl = W + sh.woff[l];
   const double flops = 2.0 * B * in * out * groups;
@@ -58,6 +58,11 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
       a.noise_sd = h_f2.p;
       a.noise_clip = h_f3.p;
       a.bound = bound;
+    }
+    if (ymask && ymask->mask && epi == EPI_BIAS_RELU) {
+      a.mask_out = ymask->mask;
+      a.mo_gs = ymask->mgs;
+      a.mo_ld = ymask->mld;
     }
     timed(PC_GEMM_FWD, flops, 0.0, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
@@ -92,6 +97,12 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
     if (out <= 16) launch_fwd_skinny(g, stream);
     else launch_gemm_simt(g, stream);
   });
+  if (ymask && ymask->mask && epi == EPI_BIAS_RELU) {
+    timed(PC_ELEM, 0.0, 0.0, active != nullptr, [&] {
+      launch_mask_bits(groups, B, out, Y, y_gs, y_ld, ymask->mask, ymask->mgs, ymask->mld, active,
+                       n, stream);
+    });
+  }
 }
 
 // dX of layer l restricted to input columns [col0, col0+ncols): DX = epi(G W_l^T)
@@ -121,6 +132,12 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
     a.aux_gs = aux.gs;
     a.aux_rs = aux.ld;
     a.aux_by_member = aux.by_member;
+    if (epi == EPI_RELU_MASK && aux.mask) {
+      a.mask_in = aux.mask;
+      a.mi_gs = aux.mgs;
+      a.mi_ld = aux.mld;
+      a.mi_by_member = aux.by_member;
+    }
     a.scale = scale;
     a.active = active;
     timed(PC_GEMM_DX, flops, 0.0, active != nullptr,
@@ -276,9 +293,20 @@ std::string Pop::prof_report() {
 }
 
 // ------------------------------------------------------------------ shared building blocks
+// hidden-activation buffers hold [rows][ld] floats followed (TF32 mode) by the ReLU mask bits
+// [rows][ceil(H / 32)] (ensure_scratch sizes them)
 Mat Pop::hid(std::vector<DBuf<float>>& v, int l, int B, const NetShape& sh, int by_member) {
-  const int ld = pad4(sh.dims[l + 1]);
-  return Mat{v[l].p, static_cast<long long>(B) * ld, ld, by_member};
+  const int H = sh.dims[l + 1];
+  const int ld = pad4(H);
+  Mat m{v[l].p, static_cast<long long>(B) * ld, ld, by_member};
+  if (use_tc()) {
+    const long long mw = (H + 31) / 32;
+    const long long rows = static_cast<long long>(v[l].count) / (ld + mw);
+    m.mask = reinterpret_cast<uint32_t*>(v[l].p + rows * ld);
+    m.mgs = static_cast<long long>(B) * mw;
+    m.mld = mw;
+  }
+  return m;
 }
 
 // forward of `sh` (groups x B rows) from input x; hidden activations into hs[l]
@@ -296,7 +324,8 @@ void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat
       if (l == L - 2 && gemm_fwd_fused(sh, W, l, groups, B, x, h, keep_hidden, out, out_gs, out_ld,
                                        last_epi, active, C2, c2_gs, c2_ld, noise))
         return;  // the output layer ran in this layer's epilogue
-      gemm_fwd(sh, W, l, groups, B, x, const_cast<float*>(h.p), h.gs, h.ld, EPI_BIAS_RELU, active);
+      gemm_fwd(sh, W, l, groups, B, x, const_cast<float*>(h.p), h.gs, h.ld, EPI_BIAS_RELU, active,
+               nullptr, 0, 0, false, keep_hidden ? &h : nullptr);
       x = h;
     }
   }
@@ -345,11 +374,21 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
   a.oc2_rs = c2_ld;
   a.out_scale = sh.out_scale;
   a.store_hidden = keep_hidden ? 1 : 0;
+  if (keep_hidden && H.mask) {
+    a.mask_out = H.mask;
+    a.mo_gs = H.mgs;
+    a.mo_ld = H.mld;
+  }
   if (noise) {
     a.noise_key = key_a.p;
     a.noise_sd = h_f2.p;
     a.noise_clip = h_f3.p;
     a.bound = bound;
+    if (algo == PBRL_ALGO_TD3 && nout == da) {  // precomputed by launch_td3_target_noise
+      a.noise_eps = S.tnoise.p;
+      a.ne_gs = static_cast<long long>(B) * da;
+      a.ne_rs = da;
+    }
   }
   const double flops = 2.0 * B * groups * (static_cast<double>(in) * hdim + hdim * nout);
   timed(PC_GEMM_FWD, flops, 0.0, active != nullptr,
@@ -364,7 +403,7 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
   const int L = sh.depth;
   for (int l = L - 1; l >= 0; --l) {
     const Mat x = (l == 0) ? x0 : hid(hs, l - 1, B, sh, 0);
-    if (l == L - 1 && sh.dims[L] <= 16) {
+    if (l == L - 1 && sh.dims[L] <= 16 && static_cast<long long>(B) * sh.dims[L] <= 32768) {
       // output layer: dX (masked), dW and db in one pass over the hidden activations
       const int H = sh.dims[l], nout = sh.dims[L];
       OutBwdArgs a;
@@ -385,6 +424,7 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       a.dW = Gr + sh.woff[l];
       a.dw_gs = static_cast<long long>(sh.stride);
       a.active = active;
+      a.exact = use_tc() ? 0 : 1;
       Mat dh{};
       if (l > 0) {
         dh = hid(dhs, l - 1, B, sh, 0);
@@ -452,6 +492,11 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
                           steps.p, streams.p, seed, key_a.p, stream);
   });
   // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
+  if (use_tc()) {
+    timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+      launch_td3_target_noise(n, B, da, key_a.p, h_f2.p, h_f3.p, S.tnoise.p, stream);
+    });
+  }
   const Mat s2{S.in_s2a.p, nbB * lsa, lsa, 0};
   mlp_forward(pol, pol_t.p, n, B, s2, S.tp_h, S.in_s2a.p + ds, nbB * lsa, lsa,
               EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true, false);

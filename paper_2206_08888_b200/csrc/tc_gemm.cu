@@ -14,6 +14,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "pop_impl.cuh"
@@ -96,18 +97,31 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
-  uint32_t r[16];
+// 32 consecutive accumulator columns of this thread's TMEM lane; asynchronous until
+// tmem_ld_wait(v), which also orders every later use of v after the wait
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
-      "%12, %13, %14, %15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+      "%30, %31}, [%32];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7]), "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]),
+        "=f"(v[14]), "=f"(v[15]), "=f"(v[16]), "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]),
+        "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]), "=f"(v[25]), "=f"(v[26]), "=f"(v[27]),
+        "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
       : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait(float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+  asm volatile(""
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
+                 "+f"(v[6]), "+f"(v[7]), "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]),
+                 "+f"(v[12]), "+f"(v[13]), "+f"(v[14]), "+f"(v[15]));
+  asm volatile(""
+               : "+f"(v[16]), "+f"(v[17]), "+f"(v[18]), "+f"(v[19]), "+f"(v[20]), "+f"(v[21]),
+                 "+f"(v[22]), "+f"(v[23]), "+f"(v[24]), "+f"(v[25]), "+f"(v[26]), "+f"(v[27]),
+                 "+f"(v[28]), "+f"(v[29]), "+f"(v[30]), "+f"(v[31]));
 }
 
 template <int BN>
@@ -117,50 +131,132 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
 
 }  // namespace
 
-template <int BN, bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(128, 2)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant (column halves)
+constexpr int kEpiThreads = kEpiWarps * 32;
+
+__device__ __forceinline__ void epi_bar_sync() {  // the epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
+
+__device__ __forceinline__ void quad_bar_sync(int q) {  // the two warps of lane quadrant q
+  asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// 1-D bulk copy global -> shared, completion on an mbarrier (size and addresses 16 B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// 32 rows x 128 B box with the 128-byte swizzle: 16-byte chunk j of row r lives at
+// r * 128 + ((j ^ (r & 7)) << 4)
+__device__ __forceinline__ uint32_t sw128(int r, int j) {
+  return static_cast<uint32_t>(r * 128 + ((j ^ (r & 7)) << 4));
+}
+
+// Optional phase timeline (TcArgs::trace, diagnostics only): per CTA kTraceSlots globaltimer
+// stamps -- [0] entry, [1] after setup, per tile it < kTraceTiles: [2+6it+0] producer issues the
+// first TMA, [+1] MMA sees the first stage, [+2] MMA commits the tile, [+3] epilogue sees the
+// accumulator, [+4] epilogue done; [62] epilogue drained its TMA stores, [63] exit.
+constexpr int kTraceSlots = 64, kTraceTiles = 10;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_TRACE(slot)                                                    \
+  do {                                                                    \
+    if (g.trace) g.trace[blockIdx.x * kTraceSlots + (slot)] = gtimer();   \
+  } while (0)
+#define TC_TRACE_TILE(it, k)                                              \
+  do {                                                                    \
+    if (g.trace && (it) < kTraceTiles) TC_TRACE(2 + 6 * (it) + (k));      \
+  } while (0)
+
+constexpr uint32_t kEpiBufBytes = 4096;                  // one 32 x 32 fp32 box
+constexpr uint32_t kEpiWarpBytes = 2 * kEpiBufBytes;     // per warp: 2 boxes
+constexpr uint32_t kEpiBytes = kEpiWarps * kEpiWarpBytes;
+
+// Persistent, warp-specialised grouped GEMM.  Grid <= #SMs; CTA b walks tiles b, b+grid, ...
+// (tile = group x M-tile x N-tile).  warp 0: TMA producer over a `stages`-deep smem ring;
+// warp 1: TMEM allocation + single-thread tcgen05.mma issue into one of TWO accumulator buffers;
+// warps 2-9: epilogue, two warps per TMEM lane quadrant (warp % 4) splitting the tile's columns
+// -- each thread keeps its accumulator row (32-column tcgen05.ld, next chunk in flight while
+// the current one is processed), adds the bias / applies ReLU / the ReLU' mask (bit masks),
+// writes 128B-swizzled 32 x 32 boxes with 128-bit stores and TMA-stores them.  The
+// double-buffered accumulator lets the epilogue of tile i run while tile i+1's MMAs run.
+template <int BN, bool A_MN, bool B_MN, int NO>
+__global__ void __launch_bounds__(64 + kEpiThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
               const TcArgs g) {
   constexpr uint32_t A_BYTES = kBM * kBK * 4;  // 16 KB
   constexpr uint32_t B_BYTES = BN * kBK * 4;
   constexpr uint32_t STAGE = A_BYTES + B_BYTES;
+  constexpr uint32_t ACC_COLS = tmem_cols<BN>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1 KB alignment for the 128B swizzle atoms, by offsetting within the shared array so the
+  // 1 KB alignment for the swizzle atoms, by offsetting within the shared array so the
   // compiler keeps the shared address space (LDS/STS, not generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int kStages = g.stages;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * STAGE);
+  const int S = g.stages;
+  uint8_t* epi_smem = smem + S * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + kEpiBytes);
   uint64_t* empty = full + kMaxStages;
-  uint64_t* tmem_full = empty + kMaxStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-
-  // fused output layer: bias [BN] and W_out [BN][nout] staged after the barriers
-  float* fz_bias = reinterpret_cast<float*>(smem + kStages * STAGE + 256);
+  uint64_t* tfull = empty + kMaxStages;  // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint64_t* abar = tempty + 2;           // [epilogue warp] mask-box barriers
+  uint64_t* sbar = abar + kEpiWarps;      // bias / output-layer staging
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sbar + 1);
+  float* fz_bias = reinterpret_cast<float*>(epi_smem + kEpiBytes + 256);
   float* fz_w = fz_bias + BN;
+  float* osum = fz_w + BN * (NO > 0 ? NO : 0);  // [2][4][32][NO] fused-output partial sums
 
-  const int grp = blockIdx.z;
-  const int mem = grp % g.n_members;
-  if (g.active && !g.active[mem]) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
-  const int nout = g.nout;
-  if (nout > 0) {
-    const float* bsrc = g.bias + grp * g.bias_gs;
-    const float* wsrc = g.ow + grp * g.ow_gs;
-    for (int e = threadIdx.x; e < BN; e += blockDim.x) fz_bias[e] = e < g.N ? bsrc[e] : 0.0f;
-    for (int e = threadIdx.x; e < BN * nout; e += blockDim.x)
-      fz_w[e] = e < g.N * nout ? wsrc[e] : 0.0f;
-  }
-  const int ga = g.a_by_member ? mem : grp;
-  const int gb = g.b_by_member ? mem : grp;
+  const int m_tiles = (g.M + kBM - 1) / kBM, n_tiles = (g.N + BN - 1) / BN;
+  const int num_tiles = g.groups * m_tiles * n_tiles;
   const int nk = (g.K + kBK - 1) / kBK;
+  // fused output width: compile-time for the common 1 / 6 / 12, runtime-guarded up to 16
+  const int nout = (NO > 0 && NO < 16) ? NO : (NO == 0 ? 0 : g.nout);
+  if (threadIdx.x == 0) TC_TRACE(0);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+    }
+    for (int a = 0; a < kEpiWarps; ++a) mbar_init(&abar[a], 1);
+    mbar_init(sbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -168,230 +264,468 @@ __global__ void __launch_bounds__(128, 2)
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(tmem_cols<BN>()));
+                 "r"(2 * ACC_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TC_TRACE(1);
 
-  if (warp == 0 && lane == 0) {
+  auto decode = [&](int t, int& grp, int& m0, int& n0) {
+    const int nt = t % n_tiles;
+    const int r = t / n_tiles;
+    m0 = (r % m_tiles) * kBM;
+    grp = r / m_tiles;
+    n0 = nt * BN;
+  };
+  auto active = [&](int grp) { return !g.active || g.active[grp % g.n_members]; };
+
+  if (warp == 0) {
     // ---------------- TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kStages;
-      if (kb >= kStages) mbar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-      uint8_t* sa = smem + s * STAGE;
-      uint8_t* sb = sa + A_BYTES;
-      mbar_expect_tx(&full[s], STAGE);
-      const int k0 = kb * kBK;
-      if (A_MN) {
+    if (lane == 0) {
+      int cnt = 0, pit = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int grp, m0, n0;
+        decode(t, grp, m0, n0);
+        if (!active(grp)) continue;
+        TC_TRACE_TILE(pit, 0);
+        ++pit;
+        const int mem = grp % g.n_members;
+        const int ga = g.a_by_member ? mem : grp;
+        const int gb = g.b_by_member ? mem : grp;
+        for (int kb = 0; kb < nk; ++kb, ++cnt) {
+          const int s = cnt % S;
+          if (cnt >= S) mbar_wait(&empty[s], ((cnt / S) - 1) & 1);
+          uint8_t* sa = smem + s * STAGE;
+          uint8_t* sb = sa + A_BYTES;
+          mbar_expect_tx(&full[s], STAGE);
+          const int k0 = kb * kBK;
+          if (A_MN) {
 #pragma unroll
-        for (int j = 0; j < kBM / 32; ++j) tma_load_3d(&tmA, &full[s], sa + j * 4096, m0 + 32 * j, k0, ga);
-      } else {
-        tma_load_3d(&tmA, &full[s], sa, k0, m0, ga);
-      }
-      if (B_MN) {
+            for (int j = 0; j < kBM / 32; ++j)
+              tma_load_3d(&tmA, &full[s], sa + j * 4096, m0 + 32 * j, k0, ga);
+          } else {
+            tma_load_3d(&tmA, &full[s], sa, k0, m0, ga);
+          }
+          if (B_MN) {
 #pragma unroll
-        for (int j = 0; j < BN / 32; ++j) tma_load_3d(&tmB, &full[s], sb + j * 4096, n0 + 32 * j, k0, gb);
-      } else {
-        tma_load_3d(&tmB, &full[s], sb, k0, n0, gb);
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
-    // instruction descriptor: D f32, A/B tf32, majorness, N >> 3, M >> 4
-    constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
-                               ((B_MN ? 1u : 0u) << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
-                               (static_cast<uint32_t>(kBM >> 4) << 24);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kStages;
-      mbar_wait(&full[s], (kb / kStages) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t a_base = smem_u32(smem + s * STAGE);
-      const uint32_t b_base = a_base + A_BYTES;
-#pragma unroll
-      for (int kk = 0; kk < kBK / 8; ++kk) {
-        // K-major: +32 B inside the 128 B swizzle row (SBO = 8 rows = 1 KB);
-        // MN-major: +1 KB = the next 8 K-rows (SBO = 4 rows = 512 B, LBO = next 32-wide MN box)
-        const uint64_t da = A_MN ? sdesc(a_base + kk * 1024, 4096, 512, 1)
-                                 : sdesc(a_base + kk * 32, 16, 1024, 2);
-        const uint64_t db = B_MN ? sdesc(b_base + kk * 1024, 4096, 512, 1)
-                                 : sdesc(b_base + kk * 32, 16, 1024, 2);
-        mma_tf32(tmem, da, db, idesc, (kb | kk) ? 1u : 0u);
-      }
-      mma_commit(&empty[s]);
-    }
-    mma_commit(tmem_full);
-  }
-
-  // ---------------- epilogue: all four warps.  tcgen05.ld gives thread `lane` of warp w the
-  // accumulator row 32w + lane; each 32-column chunk is transposed through shared memory (the
-  // pipeline stages are idle once every MMA has completed) so that lanes map to columns: bias /
-  // aux loads and the C stores are then 128-byte coalesced and all issued before they are used.
-  __syncwarp();
-  mbar_wait(tmem_full, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  float* T = reinterpret_cast<float*>(smem) + warp * (32 * 33);
-  const int row0 = m0 + warp * 32;
-  float* C = g.C + (g.c_by_member ? mem : grp) * g.c_gs;
-  const float* bias = g.bias ? g.bias + grp * g.bias_gs : nullptr;
-  const float* aux = g.aux ? g.aux + (g.aux_by_member ? mem : grp) * g.aux_gs : nullptr;
-  const int epi = g.epi;
-  constexpr int CW = BN < 32 ? BN : 32;  // chunk width
-  if (nout > 0) {
-    // hidden layer + output layer: thread = accumulator row; h = relu(acc + b) chunk by chunk,
-    // y[o] += h[j] * W_out[j][o] in ascending j; h optionally stored (transposed, coalesced)
-    float oacc[16];
-#pragma unroll
-    for (int o = 0; o < 16; ++o) oacc[o] = 0.0f;
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += CW) {
-      if (c0 >= g.N) break;
-      float v[32];
-      const uint32_t taddr =
-          tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c0);
-      tmem_ld16(taddr, v);
-      if (CW == 32) tmem_ld16(taddr + 16, v + 16);
-#pragma unroll
-      for (int j = 0; j < CW; ++j) {
-        const float z = v[j] + fz_bias[c0 + j];
-        const float h = (c0 + j < g.N && z > 0.0f) ? z : 0.0f;
-        v[j] = h;
-        const float* wr = fz_w + (c0 + j) * nout;
-#pragma unroll
-        for (int o = 0; o < 16; ++o)
-          if (o < nout) oacc[o] = oacc[o] + h * wr[o];
-      }
-      if (g.store_hidden) {
-#pragma unroll
-        for (int j = 0; j < CW; ++j) T[lane * 33 + j] = v[j];
-        __syncwarp();
-        const int col = n0 + c0 + lane;
-        if (lane < CW && col < g.N) {
-#pragma unroll
-          for (int rr = 0; rr < 32; ++rr) {
-            const int row = row0 + rr;
-            if (row < g.M) C[static_cast<long long>(row) * g.c_rs + col] = T[rr * 33 + lane];
+            for (int j = 0; j < BN / 32; ++j)
+              tma_load_3d(&tmB, &full[s], sb + j * 4096, n0 + 32 * j, k0, gb);
+          } else {
+            tma_load_3d(&tmB, &full[s], sb, k0, n0, gb);
           }
         }
-        __syncwarp();
       }
     }
-    const int row = row0 + lane;
-    if (row < g.M) {
-      const float* ob = fz_w + g.N * nout;  // b_out follows W_out in the arena row
-      const float* obg = g.ow + grp * g.ow_gs + static_cast<long long>(g.N) * nout;
-      (void)ob;
-      float* oC = g.oC + grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
-      const bool tanh_out = g.out_epi == EPI_BIAS_TANH || g.out_epi == EPI_BIAS_TANH_NOISE;
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (instruction descriptor: D f32, A/B tf32, majorness, N, M)
+    if (lane == 0) {
+      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                                 ((B_MN ? 1u : 0u) << 16) |
+                                 (static_cast<uint32_t>(BN >> 3) << 17) |
+                                 (static_cast<uint32_t>(kBM >> 4) << 24);
+      int cnt = 0, it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int grp, m0, n0;
+        decode(t, grp, m0, n0);
+        if (!active(grp)) continue;
+        const int acc = it & 1;
+        if (it >= 2) mbar_wait(&tempty[acc], ((it >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dtmem = tmem + static_cast<uint32_t>(acc) * ACC_COLS;
+        for (int kb = 0; kb < nk; ++kb, ++cnt) {
+          const int s = cnt % S;
+          mbar_wait(&full[s], (cnt / S) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (kb == 0) TC_TRACE_TILE(it, 1);
+          const uint32_t a_base = smem_u32(smem + s * STAGE);
+          const uint32_t b_base = a_base + A_BYTES;
 #pragma unroll
-      for (int o = 0; o < 16; ++o) {
-        if (o >= nout) break;
-        const float y = oacc[o] + obg[o];
-        float r = y;
-        if (tanh_out) {
-          const float t = libm_tanhf(y);
-          if (g.oC2) g.oC2[grp * g.oc2_gs + static_cast<long long>(row) * g.oc2_rs + o] = t;
-          r = (g.out_scale != 1.0f) ? t * g.out_scale : t;
-          if (g.out_epi == EPI_BIAS_TANH_NOISE) {
-            const uint64_t e = static_cast<uint64_t>(row) * nout + o;
-            float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
-                        g.noise_sd[mem];
-            eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
-            r = clampf_ref(r + eps, -g.bound, g.bound);
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            // K-major: +32 B inside the 128 B swizzle row (SBO = 8 rows = 1 KB);
+            // MN-major: +1 KB = the next 8 K-rows (SBO = 4 rows = 512 B, LBO = next MN box)
+            const uint64_t da = A_MN ? sdesc(a_base + kk * 1024, 4096, 512, 1)
+                                     : sdesc(a_base + kk * 32, 16, 1024, 2);
+            const uint64_t db = B_MN ? sdesc(b_base + kk * 1024, 4096, 512, 1)
+                                     : sdesc(b_base + kk * 32, 16, 1024, 2);
+            mma_tf32(dtmem, da, db, idesc, (kb | kk) ? 1u : 0u);
           }
+          mma_commit(&empty[s]);
         }
-        oC[o] = r;
+        mma_commit(&tfull[acc]);
+        TC_TRACE_TILE(it, 2);
+        ++it;
       }
     }
-  } else
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += CW) {
-    if (n0 + c0 >= g.N) break;
-    {
-      float v[32];
-      const uint32_t taddr =
-          tmem + (static_cast<uint32_t>(warp * 32) << 16) + static_cast<uint32_t>(c0);
-      tmem_ld16(taddr, v);
-      if (CW == 32) tmem_ld16(taddr + 16, v + 16);
-#pragma unroll
-      for (int j = 0; j < CW; ++j) T[lane * 33 + j] = v[j];
-    }
-    __syncwarp();
-    const int col = n0 + c0 + lane;
-    const bool col_ok = lane < CW && col < g.N;
-    if (epi == EPI_BIAS_TANH || epi == EPI_BIAS_TANH_NOISE) {
-      // transcendental epilogue (policy output layer): row loop straight out of shared memory
-      if (col_ok) {
-        const float bv = bias ? bias[col] : 0.0f;
-#pragma unroll 1
-        for (int rr = 0; rr < 32; ++rr) {
-          const int row = row0 + rr;
-          if (row >= g.M) break;
-          const float t = libm_tanhf(T[rr * 33 + lane] + bv);
-          if (g.C2) g.C2[grp * g.c2_gs + static_cast<long long>(row) * g.c2_rs + col] = t;
-          float y = (g.scale != 1.0f) ? t * g.scale : t;
-          if (epi == EPI_BIAS_TANH_NOISE) {
-            const uint64_t e = static_cast<uint64_t>(row) * g.N + col;
-            float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
-                        g.noise_sd[mem];
-            eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
-            y = clampf_ref(y + eps, -g.bound, g.bound);
+  } else {
+    // ---------------- epilogue warps: warp w reads TMEM lane quadrant q = w % 4 (tile rows
+    // 32q..32q+31, one row per thread) and processes column half hf = (w - 2) / 4 of the tile
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int hf = ew >> 2;
+    uint8_t* wbuf = epi_smem + ew * kEpiWarpBytes;  // this warp's two 4 KB boxes
+    float* T = reinterpret_cast<float*>(wbuf);        // general path: 32 x 33 transpose tile
+    uint64_t* wbar = abar + ew;
+    const int epi = g.epi;
+    const bool mask_bits = epi == EPI_RELU_MASK && g.mask_in != nullptr;
+    const bool aux_boxes = epi == EPI_RELU_MASK && !mask_bits;
+    const bool fast = g.c_tma &&
+                      (epi == EPI_STORE || epi == EPI_BIAS || epi == EPI_BIAS_RELU ||
+                       (epi == EPI_RELU_MASK && (g.aux_tma || mask_bits))) && BN >= 32;
+    const int nbox = aux_boxes ? 1 : 2;  // C boxes in flight per warp (the other one: mask box)
+    constexpr int MW = BN >= 32 ? BN / 32 : 1;  // mask words per row of a tile
+    constexpr int CW = BN < 32 ? BN : 32;       // chunk width
+    constexpr int NCH = BN / CW;                // chunks per tile
+    constexpr int HCH = NCH >= 2 ? NCH / 2 : 1;  // chunks per column half
+    const int cbeg = hf * HCH;
+    const bool half_active = NCH >= 2 || hf == 0;
+    const bool need_bias = g.bias && (epi == EPI_BIAS || epi == EPI_BIAS_RELU || nout > 0);
+    constexpr int NA = NO > 0 ? NO : 1;
+    int it = 0, nchunk = 0, nstage = 0;
+    // zero the staging area once: columns past N (never bulk-written) must read as 0
+    for (int e = threadIdx.x - 64; e < BN * (1 + (nout > 0 ? nout : 0)); e += kEpiThreads)
+      fz_bias[e] = 0.0f;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int grp, m0, n0;
+      decode(t, grp, m0, n0);
+      if (!active(grp)) continue;
+      const int mem = grp % g.n_members;
+      const int acc = it & 1;
+      const int row0 = m0 + q * 32;
+      const int row = row0 + lane;
+      const int cg = g.c_by_member ? mem : grp;
+      const int xg = g.aux_by_member ? mem : grp;
+      float* C = g.C + cg * g.c_gs;
+      const float* bias = g.bias ? g.bias + grp * g.bias_gs : nullptr;
+      const float* aux = g.aux ? g.aux + xg * g.aux_gs : nullptr;
+      if (need_bias) {
+        // stage this tile's bias (and output-layer weights) once the previous tile is consumed:
+        // one bulk copy issued before waiting for the accumulator, so it overlaps the MMAs
+        epi_bar_sync();
+        const float* bsrc = bias + n0;
+        const float* wsrc = nout > 0 ? g.ow + grp * g.ow_gs : nullptr;
+        const uint32_t bbytes = static_cast<uint32_t>(min(BN, g.N - n0)) * 4;
+        const uint32_t wbytes = static_cast<uint32_t>(g.N * nout) * 4;
+        const bool bulk = (reinterpret_cast<uintptr_t>(bsrc) % 16 == 0) && bbytes % 16 == 0 &&
+                          (nout == 0 || ((reinterpret_cast<uintptr_t>(wsrc) % 16 == 0) &&
+                                         wbytes % 16 == 0));
+        if (bulk) {
+          if (threadIdx.x == 64) {
+            mbar_expect_tx(sbar, bbytes + (nout > 0 ? wbytes : 0));
+            bulk_g2s(fz_bias, bsrc, bbytes, sbar);
+            if (nout > 0) bulk_g2s(fz_w, wsrc, wbytes, sbar);
           }
-          C[static_cast<long long>(row) * g.c_rs + col] = y;
+          mbar_wait(sbar, nstage & 1);
+          ++nstage;
+        } else {
+          for (int e = threadIdx.x - 64; e < BN; e += kEpiThreads)
+            fz_bias[e] = (n0 + e < g.N) ? bias[n0 + e] : 0.0f;
+          if (nout > 0)
+            for (int e = threadIdx.x - 64; e < BN * nout; e += kEpiThreads)
+              fz_w[e] = e < g.N * nout ? wsrc[e] : 0.0f;
+          epi_bar_sync();
         }
       }
-      __syncwarp();
-      continue;
-    }
-    float x[32];
+      // per-row operands of the epilogue, loaded before the accumulator wait (overlaps the MMAs)
+      uint32_t mw[MW];
 #pragma unroll
-    for (int rr = 0; rr < 32; ++rr) x[rr] = T[rr * 33 + lane];
-    __syncwarp();
-    if (col_ok) {
-      const float bv = bias ? bias[col] : 0.0f;
-      if (epi == EPI_RELU_MASK || epi == EPI_TANH_GRAD) {
-        float av[32];
+      for (int k = 0; k < MW; ++k) mw[k] = 0u;
+      if (mask_bits && row < g.M) {
+        const uint32_t* mp = g.mask_in + (g.mi_by_member ? mem : grp) * g.mi_gs +
+                             static_cast<long long>(row) * g.mi_ld + (n0 >> 5);
+        const int nw = min(MW, (g.N - n0 + 31) >> 5);
+        if (MW % 4 == 0 && nw == MW && (g.mi_ld & 3) == 0 && ((n0 >> 5) & 3) == 0) {
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-          const int row = min(row0 + rr, g.M - 1);  // clamped: rows >= M are not stored
-          av[rr] = aux[static_cast<long long>(row) * g.aux_rs + col];
-        }
-        if (epi == EPI_RELU_MASK) {
-#pragma unroll
-          for (int rr = 0; rr < 32; ++rr) x[rr] = (av[rr] > 0.0f) ? x[rr] : 0.0f;
+          for (int k = 0; k < MW; k += 4) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(mp + k));
+            mw[k] = u.x;
+            mw[k + 1] = u.y;
+            mw[k + 2] = u.z;
+            mw[k + 3] = u.w;
+          }
         } else {
 #pragma unroll
-          for (int rr = 0; rr < 32; ++rr) {
-            float y = x[rr];
-            if (g.scale != 1.0f) y = y * g.scale;
-            x[rr] = y * (1.0f - av[rr] * av[rr]);
+          for (int k = 0; k < MW; ++k) mw[k] = k < nw ? __ldg(mp + k) : 0u;
+        }
+      }
+      float ob[NA], ep[NA];
+      if (nout > 0 && hf == 0) {
+        const float* obg = g.ow + grp * g.ow_gs + static_cast<long long>(g.N) * nout;
+        const bool noisy = g.out_epi == EPI_BIAS_TANH_NOISE && g.noise_eps && row < g.M;
+        const float* eg =
+            noisy ? g.noise_eps + grp * g.ne_gs + static_cast<long long>(row) * g.ne_rs : nullptr;
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          ob[o] = o < nout ? __ldg(obg + o) : 0.0f;
+          ep[o] = (noisy && o < nout) ? __ldg(eg + o) : 0.0f;
+        }
+      }
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (threadIdx.x == 64) TC_TRACE_TILE(it, 3);
+      const uint32_t tacc =
+          tmem + static_cast<uint32_t>(acc) * ACC_COLS + (static_cast<uint32_t>(q * 32) << 16);
+
+      // one 32-column chunk of this thread's row -> swizzled box -> TMA store
+      auto store_box = [&](const float* v, int c0) {
+        if (g.dbg == 1) return;
+        uint8_t* box = wbuf + (nbox == 2 ? (nchunk & 1) : 0) * kEpiBufBytes;
+        if (lane == 0 && nchunk >= nbox) {  // box reused nbox chunks later
+          if (nbox == 2) tma_store_wait_read<1>();
+          else tma_store_wait_read<0>();
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float4 w4 = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          *reinterpret_cast<float4*>(box + sw128(lane, j)) = w4;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) tma_store_3d(&tmC, box, n0 + c0, row0, cg);
+        ++nchunk;
+      };
+      // bit j of the returned word = (v[j] > 0): the ReLU mask of one 32-column chunk
+      auto mask_word = [&](const float* v) {
+        uint32_t bits = 0u;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) bits |= (v[j] > 0.0f ? 1u : 0u) << j;
+        return bits;
+      };
+      uint32_t* mrow = (g.mask_out && row < g.M)
+                           ? g.mask_out + grp * g.mo_gs + static_cast<long long>(row) * g.mo_ld
+                           : nullptr;
+
+      if (nout > 0) {
+        // hidden layer + fused output layer: y[o] += relu(acc + b)[j] * W_out[j][o], j ascending
+        // within each column half; the halves are added in order (deterministic)
+        float oacc[NA];
+#pragma unroll
+        for (int o = 0; o < NA; ++o) oacc[o] = 0.0f;
+        float v[2][32];
+        if (half_active) tmem_ld32(tacc + static_cast<uint32_t>(cbeg * CW), v[0]);
+#pragma unroll 2
+        for (int ci = 0; ci < HCH; ++ci) {
+          const int c0 = (cbeg + ci) * CW;
+          float* cur = v[ci & 1];
+          if (half_active) {
+            tmem_ld_wait(cur);
+            if (ci + 1 < HCH && c0 + CW < g.N)
+              tmem_ld32(tacc + static_cast<uint32_t>(c0 + CW), v[(ci + 1) & 1]);
+          }
+          if (!half_active || c0 >= g.N) continue;
+#pragma unroll
+          for (int j = 0; j < CW; ++j) {
+            const float z = cur[j] + fz_bias[c0 + j];
+            const float h = (c0 + j < g.N && z > 0.0f) ? z : 0.0f;
+            cur[j] = h;
+            const float* wr = fz_w + (c0 + j) * nout;
+#pragma unroll
+            for (int o = 0; o < NA; ++o) {
+              if (NO == 16 && o >= nout) break;
+              oacc[o] = oacc[o] + h * wr[o];
+            }
+          }
+          if (g.store_hidden) {
+            store_box(cur, c0);
+            if (mrow && CW == 32) mrow[c0 >> 5] = mask_word(cur);
           }
         }
-      } else if (epi == EPI_BIAS) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (threadIdx.x == 64) TC_TRACE_TILE(it, 4);
+        // half 1 hands its partial sums to half 0 (double-buffered by tile parity)
+        float* os = osum + ((acc * 4 + q) * 32 + lane) * NA;
+        if (hf == 1) {
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) x[rr] = x[rr] + bv;
-      } else if (epi == EPI_BIAS_RELU) {
+          for (int o = 0; o < NA; ++o) os[o] = oacc[o];
+        }
+        quad_bar_sync(q);
+        if (hf == 0 && row < g.M) {
+          float* oC = g.oC + grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
+          const bool tanh_out = g.out_epi == EPI_BIAS_TANH || g.out_epi == EPI_BIAS_TANH_NOISE;
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr) {
-          const float z = x[rr] + bv;
-          x[rr] = z > 0.0f ? z : 0.0f;
+          for (int o = 0; o < NA; ++o) {
+            if (o >= nout) break;
+            const float y = (oacc[o] + os[o]) + ob[o];
+            float r = y;
+            if (tanh_out) {
+              const float th = libm_tanhf(y);
+              if (g.oC2) g.oC2[grp * g.oc2_gs + static_cast<long long>(row) * g.oc2_rs + o] = th;
+              r = (g.out_scale != 1.0f) ? th * g.out_scale : th;
+              if (g.out_epi == EPI_BIAS_TANH_NOISE) {
+                float eps;
+                if (g.noise_eps) {
+                  eps = ep[o];
+                } else {
+                  const uint64_t e = static_cast<uint64_t>(row) * nout + o;
+                  eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
+                        g.noise_sd[mem];
+                  eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+                }
+                r = clampf_ref(r + eps, -g.bound, g.bound);
+              }
+            }
+            oC[o] = r;
+          }
+        }
+        ++it;
+        continue;
+      }
+
+      if (fast) {
+        float v[2][32];
+        if (half_active) tmem_ld32(tacc + static_cast<uint32_t>(cbeg * 32), v[0]);
+#pragma unroll 2
+        for (int ci = 0; ci < HCH; ++ci) {
+          const int c0 = (cbeg + ci) * 32;
+          float* cur = v[ci & 1];
+          if (half_active) {
+            tmem_ld_wait(cur);
+            if (ci + 1 < HCH && n0 + c0 + 32 < g.N)
+              tmem_ld32(tacc + static_cast<uint32_t>(c0 + 32), v[(ci + 1) & 1]);
+          }
+          if (!half_active || n0 + c0 >= g.N) continue;
+          if (aux_boxes && lane == 0) {
+            mbar_expect_tx(wbar, kEpiBufBytes);
+            tma_load_3d(&tmX, wbar, wbuf + kEpiBufBytes, n0 + c0, row0, xg);
+          }
+          if (epi == EPI_BIAS) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cur[j] = cur[j] + fz_bias[c0 + j];
+          } else if (epi == EPI_BIAS_RELU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float z = cur[j] + fz_bias[c0 + j];
+              cur[j] = z > 0.0f ? z : 0.0f;
+            }
+          } else if (mask_bits) {
+            uint32_t bits = 0u;
+#pragma unroll
+            for (int k = 0; k < MW; ++k)  // register select (no local-memory indexing)
+              if (k == cbeg + ci) bits = mw[k];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) cur[j] = ((bits >> j) & 1u) ? cur[j] : 0.0f;
+          } else if (aux_boxes) {
+            // the k-th use of this warp's mask box completes phase k
+            mbar_wait(wbar, nchunk & 1);
+            const uint8_t* xbox = wbuf + kEpiBufBytes;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 m4 = *reinterpret_cast<const float4*>(xbox + sw128(lane, j));
+              cur[4 * j] = m4.x > 0.0f ? cur[4 * j] : 0.0f;
+              cur[4 * j + 1] = m4.y > 0.0f ? cur[4 * j + 1] : 0.0f;
+              cur[4 * j + 2] = m4.z > 0.0f ? cur[4 * j + 2] : 0.0f;
+              cur[4 * j + 3] = m4.w > 0.0f ? cur[4 * j + 3] : 0.0f;
+            }
+            __syncwarp();  // box consumed before the next chunk's load overwrites it
+          }
+          store_box(cur, c0);
+          if (mrow && epi == EPI_BIAS_RELU) mrow[(n0 + c0) >> 5] = mask_word(cur);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (threadIdx.x == 64) TC_TRACE_TILE(it, 4);
+        ++it;
+        continue;
+      }
+
+      // ---- general path (tanh / noise / tanh-grad epilogues, narrow tiles): transpose the
+      // chunk through shared memory so lanes map to columns, coalesced loads and stores
+      if (half_active) {
+#pragma unroll 1
+        for (int ci = 0; ci < HCH; ++ci) {
+          const int c0 = (cbeg + ci) * CW;
+          if (n0 + c0 >= g.N) break;
+          {
+            float v[32];
+            tmem_ld32(tacc + static_cast<uint32_t>(c0), v);
+            tmem_ld_wait(v);
+#pragma unroll
+            for (int j = 0; j < CW; ++j) T[lane * 33 + j] = v[j];
+          }
+          __syncwarp();
+          const int col = n0 + c0 + lane;
+          const bool col_ok = lane < CW && col < g.N;
+          const bool need_aux = epi == EPI_RELU_MASK || epi == EPI_TANH_GRAD;
+          if (col_ok) {
+            const float bv = bias ? bias[col] : 0.0f;
+#pragma unroll 1
+            for (int r8 = 0; r8 < 32; r8 += 8) {
+              // the 8 aux loads of this row group are issued together (independent round trips)
+              float av[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int rw = row0 + r8 + u;
+                av[u] = (need_aux && rw < g.M)
+                            ? __ldg(aux + static_cast<long long>(rw) * g.aux_rs + col)
+                            : 0.0f;
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int rr = r8 + u;
+                const int rw = row0 + rr;
+                if (rw >= g.M) break;
+                float x = T[rr * 33 + lane];
+                switch (epi) {
+                  case EPI_BIAS: x = x + bv; break;
+                  case EPI_BIAS_RELU: {
+                    const float z = x + bv;
+                    x = z > 0.0f ? z : 0.0f;
+                    break;
+                  }
+                  case EPI_BIAS_TANH:
+                  case EPI_BIAS_TANH_NOISE: {
+                    const float th = libm_tanhf(x + bv);
+                    if (g.C2) g.C2[grp * g.c2_gs + static_cast<long long>(rw) * g.c2_rs + col] = th;
+                    x = (g.scale != 1.0f) ? th * g.scale : th;
+                    if (epi == EPI_BIAS_TANH_NOISE) {
+                      const uint64_t e = static_cast<uint64_t>(rw) * g.N + col;
+                      float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
+                                  g.noise_sd[mem];
+                      eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+                      x = clampf_ref(x + eps, -g.bound, g.bound);
+                    }
+                    break;
+                  }
+                  case EPI_RELU_MASK:
+                    if (!(av[u] > 0.0f)) x = 0.0f;
+                    break;
+                  case EPI_TANH_GRAD: {
+                    if (g.scale != 1.0f) x = x * g.scale;
+                    const float th = av[u];
+                    x = x * (1.0f - th * th);
+                    break;
+                  }
+                  default: break;
+                }
+                C[static_cast<long long>(rw) * g.c_rs + col] = x;
+              }
+            }
+          }
+          __syncwarp();
         }
       }
-#pragma unroll
-      for (int rr = 0; rr < 32; ++rr) {
-        const int row = row0 + rr;
-        if (row < g.M) C[static_cast<long long>(row) * g.c_rs + col] = x[rr];
-      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (threadIdx.x == 64) TC_TRACE_TILE(it, 4);
+      ++it;
     }
+    if (lane == 0) tma_store_wait_all();
+    if (threadIdx.x == 64) TC_TRACE(62);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"(tmem_cols<BN>()));
+                 "r"(2 * ACC_COLS));
   }
+  if (threadIdx.x == 0) TC_TRACE(63);
 }
 
 // ------------------------------------------------------------------ host side
@@ -412,39 +746,75 @@ void load_encode() {
   if (!g_encode) PBRL_THROW(PBRL_E_CUDA, "cuTensorMapEncodeTiled unavailable");
 }
 
-template <int BN>
-size_t smem_bytes(int stages, int nout) {
-  // stages (>= the 4 x 32 x 33 float epilogue transpose tiles), barriers, fused-output staging
-  const size_t st = static_cast<size_t>(stages) * (kBM * kBK * 4 + BN * kBK * 4);
-  return std::max<size_t>(st, 4 * 32 * 33 * 4) + 1024 + 256 +
-         (nout > 0 ? static_cast<size_t>(BN) * (1 + nout) * 4 : 0);
+template <int BN, int NO>
+constexpr size_t smem_bytes(int stages) {
+  // stage ring, epilogue boxes, barriers, bias / output-layer staging, fused-output partial
+  // sums, 1 KB alignment slack
+  return static_cast<size_t>(stages) * (kBM * kBK * 4 + BN * kBK * 4) + kEpiBytes + 256 + 1024 +
+         static_cast<size_t>(BN) * (1 + NO) * 4 + static_cast<size_t>(2 * kBM) * NO * 4;
+}
+constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block (sm_100)
+
+template <int BN, int NO>
+constexpr int max_stages() {
+  int s = BN >= 256 ? 3 : kMaxStages;
+  while (s > 1 && smem_bytes<BN, NO>(s) > kMaxSmem) --s;
+  return s;
 }
 
-template <int BN, bool A_MN, bool B_MN>
-void launch_tpl(const CUtensorMap& a, const CUtensorMap& b, TcArgs g, cudaStream_t s) {
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <int BN, bool A_MN, bool B_MN, int NO>
+void launch_tpl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                const CUtensorMap& x, TcArgs g, cudaStream_t s) {
+  constexpr int smax = max_stages<BN, NO>();
+  static_assert(smem_bytes<BN, NO>(smax) <= kMaxSmem, "tc_gemm: shared memory budget");
   static bool attr_set = false;
   if (!attr_set) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_tc_gemm<BN, A_MN, B_MN>,
+    CUDA_CHECK(cudaFuncSetAttribute(k_tc_gemm<BN, A_MN, B_MN, NO>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem_bytes<BN>(kMaxStages, 16))));
+                                    static_cast<int>(smem_bytes<BN, NO>(smax))));
     attr_set = true;
   }
-  // pipeline depth: enough to cover K, capped so two CTAs share an SM (TMEM 2 x 256 columns)
+  // persistent: one CTA per SM (TMEM holds two BN-column accumulators)
   const int nk = (g.K + kBK - 1) / kBK;
-  g.stages = std::max(1, std::min(nk, BN >= 256 ? 2 : 3));
-  dim3 grid((g.N + BN - 1) / BN, (g.M + kBM - 1) / kBM, g.groups);
+  g.stages = std::max(1, std::min(nk, smax));
+  const int tiles = g.groups * ((g.M + kBM - 1) / kBM) * ((g.N + BN - 1) / BN);
   if (g.nout > 0 && (g.N > BN || g.nout > 16)) PBRL_THROW(PBRL_E_USAGE, "tc_gemm: bad fused output");
-  k_tc_gemm<BN, A_MN, B_MN><<<grid, 128, smem_bytes<BN>(g.stages, g.nout), s>>>(a, b, g);
+  k_tc_gemm<BN, A_MN, B_MN, NO><<<std::min(tiles, num_sms()), 64 + kEpiThreads,
+                                  smem_bytes<BN, NO>(g.stages), s>>>(a, b, c, x, g);
 }
 
 template <bool A_MN, bool B_MN>
-void launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const TcArgs& g,
-               cudaStream_t s) {
+void launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+               const CUtensorMap& x, const TcArgs& g, cudaStream_t s) {
+  if (g.nout > 0) {  // fused output layer: forward GEMMs only (K-major A, MN-major B)
+    if constexpr (!A_MN && B_MN) {
+      if (bn == 256) {
+        switch (g.nout) {
+          case 1: launch_tpl<256, false, true, 1>(a, b, c, x, g, s); return;
+          case 6: launch_tpl<256, false, true, 6>(a, b, c, x, g, s); return;
+          case 12: launch_tpl<256, false, true, 12>(a, b, c, x, g, s); return;
+          default: launch_tpl<256, false, true, 16>(a, b, c, x, g, s); return;
+        }
+      }
+    }
+    PBRL_THROW(PBRL_E_USAGE, "tc_gemm: fused output layer needs the 256-wide forward tile");
+  }
   switch (bn) {
-    case 16: if constexpr (!B_MN) { launch_tpl<16, A_MN, B_MN>(a, b, g, s); return; } break;
-    case 64: launch_tpl<64, A_MN, B_MN>(a, b, g, s); return;
-    case 128: launch_tpl<128, A_MN, B_MN>(a, b, g, s); return;
-    case 256: launch_tpl<256, A_MN, B_MN>(a, b, g, s); return;
+    case 16: if constexpr (!B_MN) { launch_tpl<16, A_MN, B_MN, 0>(a, b, c, x, g, s); return; } break;
+    case 64: launch_tpl<64, A_MN, B_MN, 0>(a, b, c, x, g, s); return;
+    case 128: launch_tpl<128, A_MN, B_MN, 0>(a, b, c, x, g, s); return;
+    case 256: launch_tpl<256, A_MN, B_MN, 0>(a, b, c, x, g, s); return;
     default: break;
   }
   PBRL_THROW(PBRL_E_USAGE, "tc_gemm: unsupported tile width");
@@ -481,18 +851,64 @@ int pick_bn(int N, bool b_mn) {
   return 256;
 }
 
+// Diagnostics: with PBRL_TC_TRACE set, every launch (in issue / capture order) gets its own
+// slice of a device trace buffer; pbrl_debug_tc_trace copies it out with per-launch metadata.
+namespace {
+constexpr int kTraceLaunches = 96, kTraceCtas = 160;
+unsigned long long* g_trace = nullptr;
+int g_trace_n = 0;
+TcTraceMeta g_trace_meta[kTraceLaunches];
+}  // namespace
+
+void tc_trace_init() {  // outside stream capture (population construction)
+  if (g_trace || std::getenv("PBRL_TC_TRACE") == nullptr) return;
+  const size_t bytes = static_cast<size_t>(kTraceLaunches) * kTraceCtas * kTraceSlots * 8;
+  CUDA_CHECK(cudaMalloc(&g_trace, bytes));
+  CUDA_CHECK(cudaMemset(g_trace, 0, bytes));
+}
+
+int tc_trace_dump(unsigned long long* host, TcTraceMeta* meta, int max_launches) {
+  if (!g_trace) return 0;
+  const int n = std::min(std::min(g_trace_n, kTraceLaunches), max_launches);
+  CUDA_CHECK(cudaDeviceSynchronize());
+  CUDA_CHECK(cudaMemcpy(host, g_trace, static_cast<size_t>(n) * kTraceCtas * kTraceSlots * 8,
+                        cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i) meta[i] = g_trace_meta[i];
+  return n;
+}
+
 void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn,
-                    const TcArgs& g, cudaStream_t s) {
+                    const TcArgs& g0, cudaStream_t s) {
+  TcArgs g = g0;
   const int bn = pick_bn(g.N, b_mn);
+  static const int dbg = std::getenv("PBRL_TC_DBG") ? std::atoi(std::getenv("PBRL_TC_DBG")) : 0;
+  g.dbg = dbg;
+  if (g_trace && g_trace_n < kTraceLaunches) {
+    g.trace = g_trace + static_cast<size_t>(g_trace_n) * kTraceCtas * kTraceSlots;
+    g_trace_meta[g_trace_n] = TcTraceMeta{bn, a_mn ? 1 : 0, b_mn ? 1 : 0, g.nout, g.M, g.N, g.K,
+                                          g.groups, g.epi, 0};
+    ++g_trace_n;
+  }
   // A: K-major tile = 32 (K) x 128 (M) box; MN-major = 32 (M) x 32 (K) boxes
   const CUtensorMap ta = a_mn ? make_tmap(A.p, A.cols, A.rows, A.groups, A.ld, A.gs, 32, 32, true)
                               : make_tmap(A.p, A.cols, A.rows, A.groups, A.ld, A.gs, 32, kBM, false);
   const CUtensorMap tb = b_mn ? make_tmap(B.p, B.cols, B.rows, B.groups, B.ld, B.gs, 32, 32, true)
                               : make_tmap(B.p, B.cols, B.rows, B.groups, B.ld, B.gs, 32, bn, false);
-  if (a_mn && b_mn) launch_bn<true, true>(bn, ta, tb, g, s);
-  else if (a_mn) launch_bn<true, false>(bn, ta, tb, g, s);
-  else if (b_mn) launch_bn<false, true>(bn, ta, tb, g, s);
-  else launch_bn<false, false>(bn, ta, tb, g, s);
+  // epilogue boxes: C stores and ReLU'-mask loads as 32 x 32 fp32 boxes, 128B swizzle
+  CUtensorMap tc{}, tx{};
+  g.c_tma = bn >= 32 && !g.c_by_member && g.C && tma_ok(g.C, g.c_rs, g.c_gs) ? 1 : 0;
+  if (g.c_tma)
+    tc = make_tmap(g.C, g.N, g.M, g.groups, g.c_rs, g.c_gs, 32, 32, false);
+  g.aux_tma = bn >= 32 && g.aux && tma_ok(g.aux, g.aux_rs, g.aux_gs) ? 1 : 0;
+  if (g.aux_tma)
+    tx = make_tmap(g.aux, g.N, g.M, g.aux_by_member ? g.n_members : g.groups, g.aux_rs, g.aux_gs,
+                   32, 32, false);
+  if (g.nout > 0 && g.store_hidden && !g.c_tma)
+    PBRL_THROW(PBRL_E_USAGE, "tc_gemm: fused output layer needs a TMA-legal hidden buffer");
+  if (a_mn && b_mn) launch_bn<true, true>(bn, ta, tb, tc, tx, g, s);
+  else if (a_mn) launch_bn<true, false>(bn, ta, tb, tc, tx, g, s);
+  else if (b_mn) launch_bn<false, true>(bn, ta, tb, tc, tx, g, s);
+  else launch_bn<false, false>(bn, ta, tb, tc, tx, g, s);
 }
 
 }  // namespace pbrl

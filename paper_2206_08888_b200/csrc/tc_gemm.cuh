@@ -48,7 +48,27 @@ struct TcArgs {
   long long oc2_gs = 0, oc2_rs = 0;
   float out_scale = 1.0f;
   int store_hidden = 1;
+  // ReLU masks as bits: a storing BIAS_RELU / fused epilogue writes bit (c % 32) of word c / 32
+  // of row r = (h[r][c] > 0) to mask_out; EPI_RELU_MASK reads mask_in (when set) instead of aux
+  uint32_t* mask_out = nullptr;
+  long long mo_gs = 0, mo_ld = 0;
+  const uint32_t* mask_in = nullptr;
+  long long mi_gs = 0, mi_ld = 0;
+  int mi_by_member = 0;
+  // precomputed clipped target-policy noise [group][row][nout] for out_epi BIAS_TANH_NOISE
+  const float* noise_eps = nullptr;
+  long long ne_gs = 0, ne_rs = 0;
+  int c_tma = 0, aux_tma = 0;  // set by launch_tc_gemm
+  unsigned long long* trace = nullptr;
+  int dbg = 0;  // diagnostics (PBRL_TC_DBG): 1 = skip C stores, 2 = direct per-row global stores  // diagnostics timeline (PBRL_TC_TRACE), see tc_gemm.cu
 };
+
+struct TcTraceMeta {
+  int bn, a_mn, b_mn, nout, M, N, K, groups, epi, pad;
+};
+// copies the recorded launch timelines ([launch][160 CTAs][64 stamps], ns) and their metadata
+void tc_trace_init();  // allocates the trace buffer when PBRL_TC_TRACE is set
+int tc_trace_dump(unsigned long long* host, TcTraceMeta* meta, int max_launches);
 
 // TMA requirements: 16-byte aligned base and strides.
 bool tma_ok(const float* base, uint64_t row_stride_elems, uint64_t group_stride_elems);

@@ -24,8 +24,7 @@ def pb(cuda):
     return pb
 
 
-def _compare(pb, ora, algo, n, hidden, B, K, seed=7):
-    ds, da = 17, 6
+def _compare(pb, ora, algo, n, hidden, B, K, seed=7, ds=17, da=6):
     make = pb.make_td3_state if algo == "td3" else pb.make_sac_state
     st = make(n, ds, da, hidden, 1.0, seed, precision="tf32")
     ref = (ora.td3 if algo == "td3" else ora.sac)(n, ds, da, hidden, 1.0, seed)
@@ -52,6 +51,15 @@ def test_tf32_matches_oracle_within_tolerance(pb, ora, algo):
     lerr, werr = _compare(pb, ora, algo, 4, [256, 256], 256, 6)
     print(f"\n{algo} tf32: max loss rel err per step {np.round(lerr, 6).tolist()}")
     print(f"{algo} tf32: weight-delta rel-L2 {{{', '.join(f'{k}: {v:.4f}' for k, v in werr.items())}}}")
+    assert lerr.max() <= 5e-2
+    for net, e in werr.items():
+        assert e <= 0.10, (net, e)
+
+
+@pytest.mark.parametrize("algo,ds,da", [("td3", 11, 3), ("sac", 9, 8)])
+def test_tf32_other_action_widths(pb, ora, algo, ds, da):
+    """Fused output widths outside the specialised 1 / 6 / 12 (generic runtime-guarded path)."""
+    lerr, werr = _compare(pb, ora, algo, 3, [256, 256], 128, 4, seed=11, ds=ds, da=da)
     assert lerr.max() <= 5e-2
     for net, e in werr.items():
         assert e <= 0.10, (net, e)
