@@ -6,6 +6,11 @@
 
 namespace pbrl {
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("PBRL_NO_PDL") == nullptr;
+  return on;
+}
+
 // ================================================================== grouped SIMT GEMM
 // Reference order: every output accumulates its products in ascending k in fp32 without FMA
 // (pop_tensor.hpp:155-166 forward, :194-206 backward), so results are bit-identical to the CPU.
@@ -51,6 +56,7 @@ __device__ __forceinline__ float simt_epilogue(const GemmArgs& g, float v, int g
 template <int BM, int BN, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     k_gemm_simt(const GemmArgs g) {
+  PDL_ENTRY();
   constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY, BK = 16;
   constexpr int A_PER = BK * BM / NT, B_PER = (BK * BN + NT - 1) / NT;
   const int grp = blockIdx.z;
@@ -162,11 +168,11 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
   if (g.N <= 16) {
     constexpr int BM = 64, BN = 16, TM = 2, TN = 2;
     dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.groups);
-    k_gemm_simt<BM, BN, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, s>>>(g);
+    launch_k(k_gemm_simt<BM, BN, TM, TN>, grid, (BM / TM) * (BN / TN), 0, s, g);
   } else {
     constexpr int BM = 64, BN = 64, TM = 4, TN = 4;
     dim3 grid((g.N + BN - 1) / BN, (g.M + BM - 1) / BM, g.groups);
-    k_gemm_simt<BM, BN, TM, TN><<<grid, (BM / TM) * (BN / TN), 0, s>>>(g);
+    launch_k(k_gemm_simt<BM, BN, TM, TN>, grid, (BM / TM) * (BN / TN), 0, s, g);
   }
 }
 
@@ -179,6 +185,7 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
 // (coalesced), W [K][N] lives in shared memory; acc[o] runs k = 0..K-1.
 template <int NMAX>
 __global__ void __launch_bounds__(128) k_fwd_skinny(const GemmArgs g) {
+  PDL_ENTRY();
   constexpr int ROWS = 128, KC = 32;
   const int grp = blockIdx.y;
   const int mem = grp % g.n_members;
@@ -225,6 +232,7 @@ __global__ void __launch_bounds__(128) k_fwd_skinny(const GemmArgs g) {
 // the relu-mask reads and the stores are coalesced; G rows are warp-broadcast.
 template <int KMAX>
 __global__ void __launch_bounds__(256) k_dx_skinny(const GemmArgs g) {
+  PDL_ENTRY();
   constexpr int RPB = 8;  // rows per block
   const int grp = blockIdx.z;
   const int mem = grp % g.n_members;
@@ -254,6 +262,7 @@ __global__ void __launch_bounds__(256) k_dx_skinny(const GemmArgs g) {
 // coalesced across threads, G[b][o] is warp-broadcast; acc[o] runs b = 0..B-1.
 template <int NMAX>
 __global__ void __launch_bounds__(128) k_dw_skinny(const GemmArgs g) {
+  PDL_ENTRY();
   const int grp = blockIdx.y;
   const int mem = grp % g.n_members;
   if (g.active && !g.active[mem]) return;
@@ -290,6 +299,7 @@ constexpr int kObCols = 64, kObSlices = 4;
 
 template <int NO>  // fused output width: exact for 1 / 6 / 12, runtime-guarded up to 16
 __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs a) {
+  PDL_ENTRY();
   extern __shared__ float sm[];
   constexpr int NA = NO;
   const int nout = NO < 16 ? NO : a.nout, B = a.B;
@@ -400,7 +410,7 @@ static void launch_ob(const OutBwdArgs& a, cudaStream_t s) {
     attr = true;
   }
   dim3 grid((a.H + kObCols - 1) / kObCols, a.groups);
-  k_out_backward<NO><<<grid, kObCols * slices, smem, s>>>(a);
+  launch_k(k_out_backward<NO>, grid, kObCols * slices, smem, s, a);
 }
 
 void launch_out_backward(const OutBwdArgs& a, cudaStream_t s) {
@@ -414,23 +424,23 @@ void launch_out_backward(const OutBwdArgs& a, cudaStream_t s) {
 
 void launch_fwd_skinny(const GemmArgs& g, cudaStream_t s) {
   dim3 grid((g.M + 127) / 128, g.groups);
-  if (g.N <= 1) k_fwd_skinny<1><<<grid, 128, 0, s>>>(g);
-  else if (g.N <= 8) k_fwd_skinny<8><<<grid, 128, 0, s>>>(g);
-  else k_fwd_skinny<16><<<grid, 128, 0, s>>>(g);
+  if (g.N <= 1) launch_k(k_fwd_skinny<1>, grid, 128, 0, s, g);
+  else if (g.N <= 8) launch_k(k_fwd_skinny<8>, grid, 128, 0, s, g);
+  else launch_k(k_fwd_skinny<16>, grid, 128, 0, s, g);
 }
 
 void launch_dx_skinny(const GemmArgs& g, cudaStream_t s) {
   dim3 grid((g.N + 255) / 256, (g.M + 7) / 8, g.groups);
-  if (g.K <= 1) k_dx_skinny<1><<<grid, 256, 0, s>>>(g);
-  else if (g.K <= 8) k_dx_skinny<8><<<grid, 256, 0, s>>>(g);
-  else k_dx_skinny<16><<<grid, 256, 0, s>>>(g);
+  if (g.K <= 1) launch_k(k_dx_skinny<1>, grid, 256, 0, s, g);
+  else if (g.K <= 8) launch_k(k_dx_skinny<8>, grid, 256, 0, s, g);
+  else launch_k(k_dx_skinny<16>, grid, 256, 0, s, g);
 }
 
 void launch_dw_skinny(const GemmArgs& g, cudaStream_t s) {
   dim3 grid((g.M + 127) / 128, g.groups);
-  if (g.N <= 1) k_dw_skinny<1><<<grid, 128, 0, s>>>(g);
-  else if (g.N <= 8) k_dw_skinny<8><<<grid, 128, 0, s>>>(g);
-  else k_dw_skinny<16><<<grid, 128, 0, s>>>(g);
+  if (g.N <= 1) launch_k(k_dw_skinny<1>, grid, 128, 0, s, g);
+  else if (g.N <= 8) launch_k(k_dw_skinny<8>, grid, 128, 0, s, g);
+  else launch_k(k_dw_skinny<16>, grid, 128, 0, s, g);
 }
 
 // ================================================================== TD3 step bookkeeping
@@ -440,6 +450,7 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
                                  const uint8_t* mask, int* fire, int64_t* t_pol, int64_t* t_c1,
                                  int64_t* t_c2, uint64_t* steps, const uint64_t* streams,
                                  uint64_t seed, uint64_t* noise_key) {
+  PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
   int f = 0;
@@ -462,7 +473,7 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, cudaStream_t s) {
-  k_td3_step_begin<<<(n + 127) / 128, 128, 0, s>>>(n, delay_acc, ratio, mask, fire, t_pol, t_c1,
+  launch_k(k_td3_step_begin, (n + 127) / 128, 128, 0, s, n, delay_acc, ratio, mask, fire, t_pol, t_c1,
                                                    t_c2, steps, streams, seed, noise_key);
 }
 
@@ -471,6 +482,7 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float*
                              const float* a, const float* r, const float* s2, const float* d,
                              float* in_sa, float* in_s2a, float* sa_pi, float* r_out,
                              float* d_out) {
+  PDL_ENTRY();
   const int dsa = ds + da;
   const long long rows = static_cast<long long>(n) * B;
   const long long total = rows * dsa;
@@ -499,13 +511,14 @@ void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, co
                        float* in_s2a, float* sa_pi, float* r_out, float* d_out, cudaStream_t st) {
   const long long total = static_cast<long long>(n) * B * (ds + da);
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-  k_pack_batch<<<blocks, 256, 0, st>>>(n, B, ds, da, lsa, s, a, r, s2, d, in_sa, in_s2a, sa_pi,
+  launch_k(k_pack_batch, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d, in_sa, in_s2a, sa_pi,
                                        r_out, d_out);
 }
 
 // y = r + gamma*(1-done)*min(Q1', Q2')   (algos.hpp:268-281)
 __global__ void k_td_target(int n, int B, const float* r, const float* d, const float* q2n,
                             const float* gamma, float* y) {
+  PDL_ENTRY();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n * B) return;
   const int m = e / B;
@@ -515,11 +528,12 @@ __global__ void k_td_target(int n, int B, const float* r, const float* d, const 
 
 void launch_td_target(int n, int B, const float* r, const float* d, const float* q2n,
                       const float* gamma, float* y, cudaStream_t s) {
-  k_td_target<<<(n * B + 255) / 256, 256, 0, s>>>(n, B, r, d, q2n, gamma, y);
+  launch_k(k_td_target, (n * B + 255) / 256, 256, 0, s, n, B, r, d, q2n, gamma, y);
 }
 
 // mse_loss_grads (algos.hpp:288-314): dq = (2/B)(q - y); loss = sum (double) d^2 / B in row order
 __global__ void k_mse(int n, int B, const float* q, const float* y, float* dq, double* loss) {
+  PDL_ENTRY();
   const int grp = blockIdx.x;
   const int m = grp % n;
   const float scale = 2.0f / static_cast<float>(B);
@@ -540,12 +554,13 @@ __global__ void k_mse(int n, int B, const float* q, const float* y, float* dq, d
 
 void launch_mse(int groups, int n, int B, const float* q, const float* y, float* dq, double* loss,
                 cudaStream_t s) {
-  k_mse<<<groups, 256, 0, s>>>(n, B, q, y, dq, loss);
+  launch_k(k_mse, groups, 256, 0, s, n, B, q, y, dq, loss);
 }
 
 // td3_policy_loss_grads (algos.hpp:318-338): loss = -sum q / B; cotangent -1/B everywhere
 __global__ void k_td3_policy_loss(int n, int B, const float* q, const int* fire, double* loss,
                                   float* gq) {
+  PDL_ENTRY();
   const int m = blockIdx.x;
   const float gv = -1.0f / static_cast<float>(B);
   for (int b = threadIdx.x; b < B; b += blockDim.x) gq[static_cast<long long>(m) * B + b] = gv;
@@ -561,7 +576,7 @@ __global__ void k_td3_policy_loss(int n, int B, const float* q, const int* fire,
 
 void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, double* loss,
                             float* gq, cudaStream_t s) {
-  k_td3_policy_loss<<<n, 256, 0, s>>>(n, B, q, fire, loss, gq);
+  launch_k(k_td3_policy_loss, n, 256, 0, s, n, B, q, fire, loss, gq);
 }
 
 // ================================================================== fused Adam + Polyak
@@ -595,6 +610,7 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
                                               const int* active, float* __restrict__ tgt,
                                               const float* tau_a, const float* tau_b,
                                               const int* polyak_gate) {
+  PDL_ENTRY();
   const int grp = blockIdx.y;
   const int m = grp % n;
   if (active && !active[m]) return;
@@ -657,7 +673,7 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
   int bx = static_cast<int>((P / 4 + threads - 1) / threads);
   bx = bx < 1 ? 1 : bx;
   dim3 grid(bx, groups);
-  k_adam<<<grid, threads, 0, s>>>(n, P, stride, p, m, v, g, t, corr1, corr2, lr, active, tgt,
+  launch_k(k_adam, grid, threads, 0, s, n, P, stride, p, m, v, g, t, corr1, corr2, lr, active, tgt,
                                   tau_a, tau_b, polyak_gate);
 }
 
@@ -666,6 +682,7 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
 __global__ void __launch_bounds__(256) k_colsum(int n, int B, int N, const float* G, long long g_gs,
                                                 long long g_ld, float* dst, long long dst_gs,
                                                 const int* active) {
+  PDL_ENTRY();
   const int grp = blockIdx.y;
   if (active && !active[grp % n]) return;
   __shared__ float part[8][33];
@@ -699,13 +716,14 @@ __global__ void __launch_bounds__(256) k_colsum(int n, int B, int N, const float
 void launch_colsum(int groups, int n, int B, int N, const float* G, long long g_gs, long long g_ld,
                    float* dst, long long dst_gs, const int* active, cudaStream_t s) {
   dim3 grid((N + 31) / 32, groups);
-  k_colsum<<<grid, 256, 0, s>>>(n, B, N, G, g_gs, g_ld, dst, dst_gs, active);
+  launch_k(k_colsum, grid, 256, 0, s, n, B, N, G, g_gs, g_ld, dst, dst_gs, active);
 }
 
 // one thread per (group, row, 32-column word)
 __global__ void k_mask_bits(int groups, int B, int H, int mw, const float* h, long long h_gs,
                             long long h_ld, uint32_t* mask, long long m_gs, long long m_ld,
                             const int* active, int n) {
+  PDL_ENTRY();
   const long long total = static_cast<long long>(groups) * B * mw;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -726,12 +744,13 @@ void launch_mask_bits(int groups, int B, int H, const float* h, long long h_gs, 
   const int mw = (H + 31) / 32;
   const long long total = static_cast<long long>(groups) * B * mw;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 8));
-  k_mask_bits<<<blocks, 256, 0, s>>>(groups, B, H, mw, h, h_gs, h_ld, mask, m_gs, m_ld, active,
+  launch_k(k_mask_bits, blocks, 256, 0, s, groups, B, H, mw, h, h_gs, h_ld, mask, m_gs, m_ld, active,
                                      n);
 }
 
 __global__ void k_td3_target_noise(int n, int B, int da, const uint64_t* key, const float* sd,
                                    const float* clip, float* eps) {
+  PDL_ENTRY();
   const long long per = static_cast<long long>(B) * da;
   const long long total = per * n;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
@@ -747,10 +766,11 @@ void launch_td3_target_noise(int n, int B, int da, const uint64_t* key, const fl
                              const float* clip, float* eps, cudaStream_t s) {
   const long long total = static_cast<long long>(n) * B * da;
   const int blocks = static_cast<int>(std::min<long long>((total + 127) / 128, 148 * 16));
-  k_td3_target_noise<<<blocks, 128, 0, s>>>(n, B, da, key, sd, clip, eps);
+  launch_k(k_td3_target_noise, blocks, 128, 0, s, n, B, da, key, sd, clip, eps);
 }
 
 __global__ void k_fill(float* p, size_t count, float v) {
+  PDL_ENTRY();
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     p[i] = v;
@@ -758,13 +778,14 @@ __global__ void k_fill(float* p, size_t count, float v) {
 
 void launch_fill(float* p, size_t count, float v, cudaStream_t s) {
   const int blocks = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 8));
-  k_fill<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(p, count, v);
+  launch_k(k_fill, blocks > 0 ? blocks : 1, 256, 0, s, p, count, v);
 }
 
 // ================================================================== SAC
 __global__ void k_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                                  int64_t* t_alpha, uint64_t* steps, const uint64_t* streams,
                                  uint64_t seed, uint64_t* key_eps, uint64_t* key_eps_t) {
+  PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
   t_pol[m] += 1;
@@ -779,7 +800,7 @@ __global__ void k_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* 
 void launch_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2, int64_t* t_alpha,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* key_eps, uint64_t* key_eps_t, cudaStream_t s) {
-  k_sac_step_begin<<<(n + 127) / 128, 128, 0, s>>>(n, t_pol, t_c1, t_c2, t_alpha, steps, streams,
+  launch_k(k_sac_step_begin, (n + 127) / 128, 128, 0, s, n, t_pol, t_c1, t_c2, t_alpha, steps, streams,
                                                    seed, key_eps, key_eps_t);
 }
 
@@ -789,6 +810,7 @@ __device__ __forceinline__ float sac_log1pf(float x) { return libm_log1pf(x); }
 
 // diagnostics: device libm ports over a host array (tests/test_gpu_numerics.py)
 __global__ void k_libm_selftest(int fn, const float* in, float* out, uint64_t count) {
+  PDL_ENTRY();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const float x = in[i];
@@ -797,7 +819,7 @@ __global__ void k_libm_selftest(int fn, const float* in, float* out, uint64_t co
 }
 
 void launch_libm_selftest(int fn, const float* in, float* out, uint64_t count, cudaStream_t s) {
-  k_libm_selftest<<<148 * 8, 256, 0, s>>>(fn, in, out, count);
+  launch_k(k_libm_selftest, 148 * 8, 256, 0, s, fn, in, out, count);
 }
 
 // log_one_minus_tanh_sq (algos.hpp:523-529)
@@ -811,6 +833,7 @@ __device__ __forceinline__ float l1mts(float x) {
 __global__ void k_sac_head(int n, int B, int ds, int da, int lsa, const float* head, const uint64_t* key,
                            float bound, float log_bound, float* sa, float* x, float* th,
                            float* ls_out, uint8_t* clamped, float* eps_out, float* logp) {
+  PDL_ENTRY();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;  // (m, b)
   if (e >= n * B) return;
   const int m = e / B, b = e % B;
@@ -846,7 +869,7 @@ void launch_sac_head(int n, int B, int ds, int da, int lsa, const float* head,
                      const uint64_t* key, float bound, float* sa, float* x, float* th, float* ls,
                      uint8_t* clamped, float* eps, float* logp, cudaStream_t s) {
   extern float host_logf(float);
-  k_sac_head<<<(n * B + 127) / 128, 128, 0, s>>>(n, B, ds, da, lsa, head, key, bound, host_logf(bound),
+  launch_k(k_sac_head, (n * B + 127) / 128, 128, 0, s, n, B, ds, da, lsa, head, key, bound, host_logf(bound),
                                                  sa, x, th, ls, clamped, eps, logp);
 }
 
@@ -854,6 +877,7 @@ void launch_sac_head(int n, int B, int ds, int da, int lsa, const float* head,
 __global__ void k_sac_y(int n, int B, const float* r, const float* d, const float* q2n,
                         const float* logp2, const float* log_alpha, const float* gamma,
                         const float* rscale, float* y) {
+  PDL_ENTRY();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n * B) return;
   const int m = e / B;
@@ -865,7 +889,7 @@ __global__ void k_sac_y(int n, int B, const float* r, const float* d, const floa
 void launch_sac_y(int n, int B, const float* r, const float* d, const float* q2n,
                   const float* logp2, const float* log_alpha, const float* gamma,
                   const float* rscale, float* y, cudaStream_t s) {
-  k_sac_y<<<(n * B + 255) / 256, 256, 0, s>>>(n, B, r, d, q2n, logp2, log_alpha, gamma, rscale,
+  launch_k(k_sac_y, (n * B + 255) / 256, 256, 0, s, n, B, r, d, q2n, logp2, log_alpha, gamma, rscale,
                                               y);
 }
 
@@ -873,6 +897,7 @@ void launch_sac_y(int n, int B, const float* r, const float* d, const float* q2n
 // alpha/B, loss accumulated per member in row order (double).
 __global__ void k_sac_policy_top(int n, int B, const float* q2n, const float* logp,
                                  const float* log_alpha, double* loss, float* gq2n, float* lw) {
+  PDL_ENTRY();
   const int m = blockIdx.x;
   const float am = static_cast<float>(exp(static_cast<double>(log_alpha[m])));
   const float inv_rows = 1.0f / static_cast<float>(B);
@@ -897,7 +922,7 @@ __global__ void k_sac_policy_top(int n, int B, const float* q2n, const float* lo
 void launch_sac_policy_top(int n, int B, const float* q2n, const float* logp,
                            const float* log_alpha, double* loss, float* gq2n, float* lw,
                            cudaStream_t s) {
-  k_sac_policy_top<<<n, 256, 0, s>>>(n, B, q2n, logp, log_alpha, loss, gq2n, lw);
+  launch_k(k_sac_policy_top, n, 256, 0, s, n, B, q2n, logp, log_alpha, loss, gq2n, lw);
 }
 
 // tanh_gaussian_logprob_backward + the action path (algos.hpp:571-595, :705-724) -> head grad
@@ -905,6 +930,7 @@ __global__ void k_sac_head_grad(int n, int B, int da, const float* ga2n, const f
                                 const float* x, const float* th, const float* ls,
                                 const uint8_t* clamped, const float* eps, float bound,
                                 float* gh) {
+  PDL_ENTRY();
   const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;  // (m,b,j)
   const long long total = static_cast<long long>(n) * B * da;
   if (e >= total) return;
@@ -931,7 +957,7 @@ void launch_sac_head_grad(int n, int B, int da, const float* ga2n, const float* 
                           const uint8_t* clamped, const float* eps, float bound, float* gh,
                           cudaStream_t s) {
   const long long total = static_cast<long long>(n) * B * da;
-  k_sac_head_grad<<<static_cast<int>((total + 255) / 256), 256, 0, s>>>(
+  launch_k(k_sac_head_grad, static_cast<int>((total + 255) / 256), 256, 0, s, 
       n, B, da, ga2n, lw, x, th, ls, clamped, eps, bound, gh);
 }
 
@@ -940,6 +966,7 @@ void launch_sac_head_grad(int n, int B, int da, const float* ga2n, const float* 
 __global__ void k_sac_alpha(int n, int B, const float* logp, const double* te,
                             float* log_alpha, float* am, float* av, const int64_t* t,
                             const float* corr1, const float* corr2, const float* lr) {
+  PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= n) return;
   const double alpha = exp(static_cast<double>(log_alpha[m]));
@@ -962,7 +989,7 @@ void launch_sac_alpha(int n, int B, const float* logp, const float* log_alpha_in
                       const int64_t* t, const float* corr1, const float* corr2, const float* lr,
                       cudaStream_t s) {
   (void)log_alpha_in;
-  k_sac_alpha<<<(n + 127) / 128, 128, 0, s>>>(n, B, logp, target_entropy, log_alpha, am, av, t,
+  launch_k(k_sac_alpha, (n + 127) / 128, 128, 0, s, n, B, logp, target_entropy, log_alpha, am, av, t,
                                               corr1, corr2, lr);
 }
 
@@ -970,6 +997,7 @@ void launch_sac_alpha(int n, int B, const float* logp, const float* log_alpha_in
 // ReplayBuffer rows live in HBM as [buffer][cap][rw] floats: s | a | s2 | r | done | pad.
 __global__ void k_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t count,
                                  int rw, float* ring) {
+  PDL_ENTRY();
   const long long total = static_cast<long long>(count) * rw;
   for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -983,7 +1011,7 @@ void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t 
                            float* ring, cudaStream_t s) {
   const long long total = static_cast<long long>(count) * rw;
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-  k_replay_scatter<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(rows, dst_row, count, rw, ring);
+  launch_k(k_replay_scatter, blocks > 0 ? blocks : 1, 256, 0, s, rows, dst_row, count, rw, ring);
 }
 
 // sample_batch (replay.hpp:181-204): slot = bits(key, b) % size with key =
@@ -994,6 +1022,7 @@ __global__ void k_replay_gather(int n, int B, int ds, int da, int lsa, int rw, c
                                 const uint64_t* streams, uint64_t seed, uint64_t draw_id,
                                 float* in_sa, float* in_s2a, float* sa_pi, float* r_out,
                                 float* d_out) {
+  PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= n * B) return;
@@ -1028,7 +1057,7 @@ void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const f
                           cudaStream_t s) {
   const long long warps = static_cast<long long>(n) * B;
   const int blocks = static_cast<int>((warps * 32 + 255) / 256);
-  k_replay_gather<<<blocks, 256, 0, s>>>(n, B, ds, da, lsa, rw, ring, cap, shared, sizes, streams,
+  launch_k(k_replay_gather, blocks, 256, 0, s, n, B, ds, da, lsa, rw, ring, cap, shared, sizes, streams,
                                          seed, draw_id, in_sa, in_s2a, sa_pi, r_out, d_out);
 }
 
@@ -1038,6 +1067,7 @@ void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const f
 // donors[i] = order[bits(key, next + i) % cut].  One block.
 __global__ void k_pbt_plan(int n, const double* fitness, int cut, uint64_t key, uint64_t next,
                            uint64_t* order, uint64_t* replaced, uint64_t* donors) {
+  PDL_ENTRY();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const double fi = fitness[i];
     int pos = 0;
@@ -1056,12 +1086,13 @@ __global__ void k_pbt_plan(int n, const double* fitness, int cut, uint64_t key, 
 
 void launch_pbt_plan(int n, const double* fitness, int cut, uint64_t key, uint64_t next,
                      uint64_t* order, uint64_t* replaced, uint64_t* donors, cudaStream_t s) {
-  k_pbt_plan<<<1, 256, 0, s>>>(n, fitness, cut, key, next, order, replaced, donors);
+  launch_k(k_pbt_plan, 1, 256, 0, s, n, fitness, cut, key, next, order, replaced, donors);
 }
 
 // copy_member (net_pop.hpp:192-202) for many (src, dst) pairs of one arena
 __global__ void k_member_copy(float* arena, size_t stride, size_t P, const uint64_t* src,
                               const uint64_t* dst) {
+  PDL_ENTRY();
   const int pr = blockIdx.y;
   const uint64_t s = src[pr], d = dst[pr];
   if (s == d) return;
@@ -1077,10 +1108,11 @@ void launch_member_copy(float* arena, size_t stride, size_t P, const uint64_t* s
   if (pairs <= 0) return;
   dim3 grid(static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((P + 1023) / 1024, 64))),
             pairs);
-  k_member_copy<<<grid, 256, 0, s>>>(arena, stride, P, src, dst);
+  launch_k(k_member_copy, grid, 256, 0, s, arena, stride, P, src, dst);
 }
 
 __global__ void k_member_zero(float* arena, size_t stride, const uint64_t* dst) {
+  PDL_ENTRY();
   float* b = arena + dst[blockIdx.y] * stride;
   for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < stride;
        k += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -1092,7 +1124,7 @@ void launch_member_zero(float* arena, size_t stride, const uint64_t* dst, int pa
   if (pairs <= 0) return;
   dim3 grid(static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((stride + 1023) / 1024, 64))),
             pairs);
-  k_member_zero<<<grid, 256, 0, s>>>(arena, stride, dst);
+  launch_k(k_member_zero, grid, 256, 0, s, arena, stride, dst);
 }
 
 // ================================================================== init
@@ -1100,6 +1132,7 @@ void launch_member_zero(float* arena, size_t stride, const uint64_t* dst, int pa
 // stream; exact on the device (IEEE double ops, no contraction).
 __global__ void k_init_layer(float* arena, size_t stride, size_t woff, size_t boff, int fi,
                              int fo, uint64_t member_offset, uint64_t seed, int layer) {
+  PDL_ENTRY();
   const int m = blockIdx.y;
   const uint64_t gm = member_offset + static_cast<uint64_t>(m);
   const double wb = sqrt(1.0 / static_cast<double>(fi));
@@ -1126,7 +1159,7 @@ void launch_init_net(const NetShape& sh, float* arena, int n, uint64_t member_of
     const size_t cnt = static_cast<size_t>(sh.dims[l]) * sh.dims[l + 1] + sh.dims[l + 1];
     dim3 grid(static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((cnt + 255) / 256, 64))),
               n);
-    k_init_layer<<<grid, 256, 0, s>>>(arena, sh.stride, sh.woff[l], sh.boff[l], sh.dims[l],
+    launch_k(k_init_layer, grid, 256, 0, s, arena, sh.stride, sh.woff[l], sh.boff[l], sh.dims[l],
                                       sh.dims[l + 1], member_offset, seed, l);
   }
 }
@@ -1135,6 +1168,7 @@ void launch_init_net(const NetShape& sh, float* arena, int n, uint64_t member_of
 // RngStream::of(seed, i, kGeneric, 1..4) and done = U < 0.02 from step 5; element e counters.
 __global__ void k_synth(uint64_t n_elems_s, uint64_t n_elems_a, uint64_t n_elems_r, uint64_t seed,
                         uint64_t batch, float* s, float* a, float* r, float* s2, float* d) {
+  PDL_ENTRY();
   const uint64_t ks = stream_key(seed, batch, kGeneric, 1), ka = stream_key(seed, batch, kGeneric, 2),
                  kr = stream_key(seed, batch, kGeneric, 3), k2 = stream_key(seed, batch, kGeneric, 4),
                  kd = stream_key(seed, batch, kGeneric, 5);
@@ -1160,7 +1194,7 @@ void launch_synth(uint64_t count, uint64_t n, uint64_t b, uint64_t ds, uint64_t 
   for (uint64_t i = 0; i < count; ++i) {
     const uint64_t total = 2 * es + ea + 2 * er;
     const int blocks = static_cast<int>(std::min<uint64_t>((total + 255) / 256, 148 * 16));
-    k_synth<<<blocks, 256, 0, st>>>(es, ea, er, seed, i, s + i * es, a + i * ea, r + i * er,
+    launch_k(k_synth, blocks, 256, 0, st, es, ea, er, seed, i, s + i * es, a + i * ea, r + i * er,
                                     s2 + i * es, d + i * er);
   }
 }

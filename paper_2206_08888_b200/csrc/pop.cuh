@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -28,6 +30,36 @@ struct Error : std::runtime_error {
     if (e_ != cudaSuccess)                                                                  \
       throw ::pbrl::Error(PBRL_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
   } while (0)
+
+// ---- programmatic dependent launch (PDL).  Every kernel is launched with
+// programmaticStreamSerialization, so it may start while its stream predecessor is still
+// draining; PDL_ENTRY() (the first statement of every kernel) waits for the predecessor grid to
+// complete and be visible (griddepcontrol.wait) and then lets this grid's own successor start
+// launching (griddepcontrol.launch_dependents).  Kernel launch latency and the prologue of the
+// next kernel overlap the tail of the previous one; CUDA-graph capture keeps the edges.
+#define PDL_ENTRY()                                                   \
+  do {                                                                \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   \
+  } while (0)
+
+bool pdl_enabled();  // PBRL_NO_PDL=1 disables the attribute (diagnostics)
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // A population of identically shaped MLPs (PopMLPParams, net_pop.hpp:17-43).  On device every
 // member occupies `stride` floats (P rounded up to 64 so member rows are 256 B aligned); the

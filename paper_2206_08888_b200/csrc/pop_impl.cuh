@@ -156,6 +156,10 @@ struct Pop {
   void prof_step_done();
   std::string prof_report();
   void prof_add_gated_bytes(double bytes);
+  // true when the latest kernel on the stream wrote parameters (Adam, PBT copies, init): the
+  // next tcgen05 launch must not read its weight operand before the PDL wait
+  bool last_wrote_weights = true;
+
   template <typename F>
   void timed(int cls, double flops, double bytes, int gated, F&& f) {
     cudaEvent_t a = nullptr;
@@ -163,6 +167,7 @@ struct Pop {
     f();
     count_launch(1);
     prof_end(a, cls, flops, bytes, gated);
+    last_wrote_weights = cls == PC_ADAM;
   }
 
   // PBT scratch

@@ -64,6 +64,7 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
       a.mo_gs = ymask->mgs;
       a.mo_ld = ymask->mld;
     }
+    a.b_prefetch = last_wrote_weights ? 0 : 1;
     timed(PC_GEMM_FWD, flops, 0.0, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
     return;
@@ -140,6 +141,7 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
     }
     a.scale = scale;
     a.active = active;
+    a.b_prefetch = last_wrote_weights ? 0 : 1;
     timed(PC_GEMM_DX, flops, 0.0, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, false, a, stream); });
     return;
@@ -391,6 +393,7 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
     }
   }
   const double flops = 2.0 * B * groups * (static_cast<double>(in) * hdim + hdim * nout);
+  a.b_prefetch = last_wrote_weights ? 0 : 1;
   timed(PC_GEMM_FWD, flops, 0.0, active != nullptr,
         [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
   return true;

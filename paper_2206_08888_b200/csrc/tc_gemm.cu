@@ -271,7 +271,10 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) TC_TRACE(1);
+  if (threadIdx.x == 0) {
+    TC_TRACE(1);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see PDL_ENTRY (pop.cuh)
+  }
 
   auto decode = [&](int t, int& grp, int& m0, int& n0) {
     const int nt = t % n_tiles;
@@ -285,6 +288,28 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
+      // PDL: the weight operand B of the first tile's first stages is independent of the
+      // predecessor kernel (b_prefetch: the host knows the predecessor wrote no weights), so it
+      // is requested before griddepcontrol.wait; everything else waits for the predecessor.
+      int npre = 0;
+      if (g.b_prefetch && !g.active && static_cast<int>(blockIdx.x) < num_tiles) {
+        int grp, m0, n0;
+        decode(blockIdx.x, grp, m0, n0);
+        const int gb = g.b_by_member ? grp % g.n_members : grp;
+        npre = min(S, nk);
+        for (int kb = 0; kb < npre; ++kb) {
+          uint8_t* sb = smem + kb * STAGE + A_BYTES;
+          mbar_expect_tx(&full[kb], STAGE);
+          if (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j)
+              tma_load_3d(&tmB, &full[kb], sb + j * 4096, n0 + 32 * j, kb * kBK, gb);
+          } else {
+            tma_load_3d(&tmB, &full[kb], sb, kb * kBK, n0, gb);
+          }
+        }
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       int cnt = 0, pit = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int grp, m0, n0;
@@ -300,7 +325,8 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           if (cnt >= S) mbar_wait(&empty[s], ((cnt / S) - 1) & 1);
           uint8_t* sa = smem + s * STAGE;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[s], STAGE);
+          const bool pre = cnt < npre;  // B already requested before the PDL wait
+          if (!pre) mbar_expect_tx(&full[s], STAGE);
           const int k0 = kb * kBK;
           if (A_MN) {
 #pragma unroll
@@ -309,7 +335,8 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           } else {
             tma_load_3d(&tmA, &full[s], sa, k0, m0, ga);
           }
-          if (B_MN) {
+          if (pre) {
+          } else if (B_MN) {
 #pragma unroll
             for (int j = 0; j < BN / 32; ++j)
               tma_load_3d(&tmB, &full[s], sb + j * 4096, n0 + 32 * j, k0, gb);
@@ -384,6 +411,7 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
     const bool need_bias = g.bias && (epi == EPI_BIAS || epi == EPI_BIAS_RELU || nout > 0);
     constexpr int NA = NO > 0 ? NO : 1;
     int it = 0, nchunk = 0, nstage = 0;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // predecessor's outputs are visible
     // zero the staging area once: columns past N (never bulk-written) must read as 0
     for (int e = threadIdx.x - 64; e < BN * (1 + (nout > 0 ? nout : 0)); e += kEpiThreads)
       fz_bias[e] = 0.0f;
@@ -790,8 +818,8 @@ void launch_tpl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
   g.stages = std::max(1, std::min(nk, smax));
   const int tiles = g.groups * ((g.M + kBM - 1) / kBM) * ((g.N + BN - 1) / BN);
   if (g.nout > 0 && (g.N > BN || g.nout > 16)) PBRL_THROW(PBRL_E_USAGE, "tc_gemm: bad fused output");
-  k_tc_gemm<BN, A_MN, B_MN, NO><<<std::min(tiles, num_sms()), 64 + kEpiThreads,
-                                  smem_bytes<BN, NO>(g.stages), s>>>(a, b, c, x, g);
+  launch_k(k_tc_gemm<BN, A_MN, B_MN, NO>, std::min(tiles, num_sms()), 64 + kEpiThreads,
+           smem_bytes<BN, NO>(g.stages), s, a, b, c, x, g);
 }
 
 template <bool A_MN, bool B_MN>

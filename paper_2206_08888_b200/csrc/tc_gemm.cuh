@@ -60,7 +60,8 @@ struct TcArgs {
   long long ne_gs = 0, ne_rs = 0;
   int c_tma = 0, aux_tma = 0;  // set by launch_tc_gemm
   unsigned long long* trace = nullptr;
-  int dbg = 0;  // diagnostics (PBRL_TC_DBG): 1 = skip C stores, 2 = direct per-row global stores  // diagnostics timeline (PBRL_TC_TRACE), see tc_gemm.cu
+  int dbg = 0;
+  int b_prefetch = 0;  // B (weights) may be read before the PDL wait (predecessor wrote none)  // diagnostics (PBRL_TC_DBG): 1 = skip C stores, 2 = direct per-row global stores  // diagnostics timeline (PBRL_TC_TRACE), see tc_gemm.cu
 };
 
 struct TcTraceMeta {
