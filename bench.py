@@ -57,13 +57,43 @@ def parse():
     return ap.parse_args()
 
 
-def peaks():
+def peaks(precision="bf16"):
+    """Roofline denominators: HBM GB/s and the dense tensor peak of the arithmetic the kernels
+    use -- bf16 from the driver-written MEASURED_PEAKS.json; TF32 (which that file lacks) from
+    profiles/measured_tf32.json (tools/measure_tf32_peak.py, same method), else half of bf16."""
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return dict(hbm=d["hbm_gbs"], tensor=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
-                    tensor_burst=d["bf16_tflops"], src="measured")
-    return dict(hbm=6650.0, tensor=1400.0, tensor_burst=1590.0, src="fallback")
+        pk = dict(hbm=d["hbm_gbs"], tensor=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                  tensor_burst=d["bf16_tflops"], src="measured (MEASURED_PEAKS.json)")
+    else:
+        pk = dict(hbm=6650.0, tensor=1400.0, tensor_burst=1590.0,
+                  src="fallback (B200_PROFILING.md)")
+    if precision == "tf32":
+        t = ROOT / "profiles" / "measured_tf32.json"
+        if t.exists():
+            d = json.loads(t.read_text())
+            pk.update(tensor=d["tf32_tflops_sustained"], tensor_burst=d["tf32_tflops"])
+            pk["src"] += "; tf32 measured (profiles/measured_tf32.json)"
+        else:
+            pk.update(tensor=pk["tensor"] / 2, tensor_burst=pk["tensor_burst"] / 2)
+            pk["src"] += "; tf32 = bf16 / 2 (nominal ratio)"
+    return pk
+
+
+def td3_member_update_work(hidden, batch, f=0.5, ds=OBS, da=ACT):
+    """minimal FLOP and compulsory HBM bytes of one TD3 member-update (policy
+    fires every 1/f steps): MACs/row = F_P + 2F_C + 2(3F_C - F_C1)
+    + f(2F_P + (F_P - F_P1) + 2F_C - F_C1 + da H1); bytes = 28(2P_C + f P_P) + 8f(P_P + 2P_C)
+    (fused Adam + Polyak, fp32) + 2 B 42 4 (replay gather read + write)."""
+    pd, cd = [ds] + list(hidden) + [da], [ds + da] + list(hidden) + [1]
+    F = lambda d: sum(d[i] * d[i + 1] for i in range(len(d) - 1))
+    P = lambda d: sum(d[i] * d[i + 1] + d[i + 1] for i in range(len(d) - 1))
+    FP, FC, FP1, FC1, H1 = F(pd), F(cd), pd[0] * pd[1], cd[0] * cd[1], hidden[0]
+    macs = FP + 2 * FC + 2 * (3 * FC - FC1) + f * (2 * FP + (FP - FP1) + 2 * FC - FC1 + da * H1)
+    PP, PC = P(pd), P(cd)
+    byt = 28 * (2 * PC + f * PP) + 8 * f * (PP + 2 * PC) + 2 * batch * (2 * ds + da + 2) * 4
+    return 2.0 * batch * macs, float(byt)
 
 
 # ------------------------------------------------------------------ clocks during the timed region
@@ -287,12 +317,17 @@ def main():
     prof = json.loads(buf.value.decode())
     if args.profile_json and rank == 0:
         Path(args.profile_json).write_text(json.dumps(prof, indent=1))
-    pk = peaks()
+    pk = peaks(args.precision)
     cls = prof["classes"]
     dom = max(cls, key=lambda c: cls[c]["ms"])
     dc = cls[dom]
     avg_ms = dc["ms"] / max(1, dc["launches"])
-    if dc["flops"] > 0:
+    # the kernel class's bound is whichever of its algorithmic FLOPs (at the tensor peak) and
+    # algorithmic bytes (at the HBM peak) takes longer: with fp32 activations at these shapes
+    # (256-row batches, 256-wide layers: ~43 FLOP/B) the grouped GEMMs sit below the ridge
+    t_tc = dc["flops"] / (pk["tensor"] * 1e12)
+    t_mem = dc["bytes"] / (pk["hbm"] * 1e9)
+    if t_tc >= t_mem:
         achieved = dc["flops"] / (dc["ms"] / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": pk["tensor"], "unit": "TFLOP/s",
                 "frac": achieved / pk["tensor"]}
@@ -300,9 +335,23 @@ def main():
         achieved = dc["bytes"] / (dc["ms"] / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
                 "frac": achieved / pk["hbm"]}
+    roof["tensor_frac"] = (dc["flops"] / (dc["ms"] / 1e3) / 1e12) / pk["tensor"]
     tot_ms = sum(c["ms"] for c in cls.values())
     roof.update({"traffic": None, "kernel": dom, "kernel_share_of_step": dc["ms"] / tot_ms,
-                 "avg_launch_ms": avg_ms, "peak_source": pk["src"]})
+                 "avg_launch_ms": avg_ms, "peak_source": pk["src"],
+                 "algorithmic_flops_per_launch": dc["flops"] / max(1, dc["launches"]),
+                 "algorithmic_bytes_per_launch": dc["bytes"] / max(1, dc["launches"])})
+    # whole-step roofline: T_roof = max(n F / P_tc, n Bytes / BW_hbm)
+    step_roof = None
+    if cfg["algo"] == "td3":
+        fl, by = td3_member_update_work(cfg["hidden"], cfg["batch"])
+        t_roof = max(n * fl / (pk["tensor"] * 1e12), n * by / (pk["hbm"] * 1e9))
+        step_roof = {"flops_per_member_update": fl, "bytes_per_member_update": by,
+                     "t_roof_ms_per_step": t_roof * 1e3,
+                     "bound": "tensor" if n * fl / pk["tensor"] / 1e12 > n * by / pk["hbm"] / 1e9
+                     else "hbm",
+                     "frac": t_roof * 1e3 / (total_ms / K),
+                     "roofline_agent_updates_per_s": pop / t_roof}
     tfile = ROOT / "profiles" / f"traffic_{args.precision}_{args.config}.json"
     if tfile.exists():
         try:
@@ -352,7 +401,7 @@ def main():
                                       "flushed between steps" if flush else
                                       f"inputs+state {(state_bytes + in_bytes) / 2**20:.0f} MiB "
                                       f"per GPU > L2"),
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "profile": {k: {kk: round(vv, 6) if isinstance(vv, float)
                                                          else vv for kk, vv in v.items()}
                                                      for k, v in cls.items()}}

@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
   const int nout = NO < 16 ? NO : a.nout, B = a.B;
   float* Gs = sm;                         // [B][nout]
   float* Ps = Gs + B * nout;              // [kObSlices][kObCols][nout] dW partials
+  float* Cs = Ps + kObSlices * kObCols * nout;  // [kObSlices][kObCols] dX column sums
   const int grp = blockIdx.y;
   const int mem = grp % a.n_members;
   if (a.active && !a.active[mem]) return;
@@ -328,6 +329,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
   const int rows = (B + slices - 1) / slices;
   const int b0 = sl * rows, b1 = min(B, b0 + rows);
   float* dX = a.dX ? a.dX + grp * a.dx_gs : nullptr;
+  float csum = 0.0f;  // column sum of this thread's dX rows (bias gradient of the layer below)
   if (i < a.H) {
     constexpr int U = 8;  // independent loads in flight per thread
     int b = b0;
@@ -345,7 +347,9 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
           acc[o] = acc[o] + xv[u] * g[o];
           d = d + g[o] * w[o];
         }
-        if (dX) dX[static_cast<long long>(b + u) * a.dx_ld + i] = xv[u] > 0.0f ? d : 0.0f;
+        const float dv = xv[u] > 0.0f ? d : 0.0f;
+        csum = csum + dv;
+        if (dX) dX[static_cast<long long>(b + u) * a.dx_ld + i] = dv;
       }
     }
     for (; b < b1; ++b) {
@@ -358,7 +362,23 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
         acc[o] = acc[o] + xv * g[o];
         d = d + g[o] * w[o];
       }
-      if (dX) dX[static_cast<long long>(b) * a.dx_ld + i] = xv > 0.0f ? d : 0.0f;
+      const float dv = xv > 0.0f ? d : 0.0f;
+      csum = csum + dv;
+      if (dX) dX[static_cast<long long>(b) * a.dx_ld + i] = dv;
+    }
+  }
+  if (a.dbx) {  // fused bias gradient of the layer below: slices combined in slice order
+    float* db = a.dbx + grp * a.dbx_gs;
+    if (slices > 1) {
+      Cs[sl * kObCols + col] = csum;
+      __syncthreads();
+      if (sl == 0 && i < a.H) {
+        float t = Cs[col];
+        for (int q = 1; q < slices; ++q) t += Cs[q * kObCols + col];
+        db[i] = t;
+      }
+    } else if (i < a.H) {
+      db[i] = csum;
     }
   }
   float* dW = a.dW + grp * a.dw_gs;
@@ -402,7 +422,8 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
 template <int NO>
 static void launch_ob(const OutBwdArgs& a, cudaStream_t s) {
   const int slices = a.exact ? 1 : kObSlices;
-  const size_t smem = (static_cast<size_t>(a.B) * a.nout + kObSlices * kObCols * a.nout) * 4;
+  const size_t smem =
+      (static_cast<size_t>(a.B) * a.nout + kObSlices * kObCols * (a.nout + 1)) * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_out_backward<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -449,32 +470,42 @@ void launch_dw_skinny(const GemmArgs& g, cudaStream_t s) {
 __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
                                  const uint8_t* mask, int* fire, int64_t* t_pol, int64_t* t_c1,
                                  int64_t* t_c2, uint64_t* steps, const uint64_t* streams,
-                                 uint64_t seed, uint64_t* noise_key) {
+                                 uint64_t seed, uint64_t* noise_key, double* policy_loss,
+                                 cudaGraphConditionalHandle any_fire, int set_cond) {
   PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= n) return;
   int f = 0;
-  double acc = delay_acc[m] + ratio[m];
-  if (acc >= 1.0 - 1e-12) {
-    acc -= 1.0;
-    f = 1;
+  if (m < n) {
+    double acc = delay_acc[m] + ratio[m];
+    if (acc >= 1.0 - 1e-12) {
+      acc -= 1.0;
+      f = 1;
+    }
+    delay_acc[m] = acc;
+    if (mask && !mask[m]) f = 0;
+    fire[m] = f;
+    t_c1[m] += 1;
+    t_c2[m] += 1;
+    if (f) t_pol[m] += 1;
+    // members that do not fire report a zero policy loss (k_td3_policy_loss writes the rest);
+    // written here because the policy half may be skipped altogether
+    if (!f) policy_loss[m] = 0.0;
+    noise_key[m] = stream_key(seed, streams[m], kTargetNoise, steps[m]);
+    steps[m] += 1;
   }
-  delay_acc[m] = acc;
-  if (mask && !mask[m]) f = 0;
-  fire[m] = f;
-  t_c1[m] += 1;
-  t_c2[m] += 1;
-  if (f) t_pol[m] += 1;
-  noise_key[m] = stream_key(seed, streams[m], kTargetNoise, steps[m]);
-  steps[m] += 1;
+  // graph mode: the policy half of the step is an IF node on "some member fires"
+  // (default 0 at every graph launch; any block with a firing member sets it)
+  const int any = __syncthreads_or(f);
+  if (set_cond && any && threadIdx.x == 0) cudaGraphSetConditional(any_fire, 1u);
 }
 
 void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const uint8_t* mask,
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
-                           uint64_t* noise_key, cudaStream_t s) {
-  launch_k(k_td3_step_begin, (n + 127) / 128, 128, 0, s, n, delay_acc, ratio, mask, fire, t_pol, t_c1,
-                                                   t_c2, steps, streams, seed, noise_key);
+                           uint64_t* noise_key, double* policy_loss,
+                           cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s) {
+  launch_k(k_td3_step_begin, (n + 127) / 128, 128, 0, s, n, delay_acc, ratio, mask, fire, t_pol,
+           t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, set_cond);
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts

@@ -158,6 +158,7 @@ Pop::~Pop() {
   if (stream) {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
+    if (side) cudaStreamDestroy(side);
   }
 }
 

@@ -132,6 +132,8 @@ struct OutBwdArgs {
   long long dw_gs = 0;
   float* dX = nullptr;       // [groups][B][dx_ld] (nullptr: input layer, no dX)
   long long dx_gs = 0, dx_ld = 0;
+  float* dbx = nullptr;      // optional: column sums of dX = the bias gradient of the layer below
+  long long dbx_gs = 0;
   const int* active = nullptr;
   int exact = 1;  // 1: reference summation order (FFMA32); 0: warp-parallel tree (TF32)
 };
@@ -148,7 +150,8 @@ struct Hyper;  // device per-member hyper floats
 void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const uint8_t* mask,
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
-                           uint64_t* noise_key, cudaStream_t s);
+                           uint64_t* noise_key, double* policy_loss,
+                           cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s);
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, float* in_sa,
                        float* in_s2a, float* sa_pi, float* r_out, float* d_out, cudaStream_t st);

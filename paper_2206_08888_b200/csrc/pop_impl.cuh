@@ -121,6 +121,8 @@ struct Pop {
   std::vector<size_t> hidden;
   NetShape pol, cri;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // capture stream of conditional graph bodies
+  size_t cond_body_nodes = 0;
 
   DBuf<float> pol_p, pol_t, pol_m, pol_v, pol_g;
   DBuf<float> cri_p, cri_t, cri_m, cri_v, cri_g;
@@ -202,7 +204,7 @@ struct Pop {
                float* DX, long long dx_gs, long long dx_ld, int epi, int col0, int ncols,
                const int* active, float scale);
   void gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
-               const int* active);
+               const int* active, bool bias_done = false);
   void mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
                    std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                    int last_epi, const int* active = nullptr, float* C2 = nullptr,
@@ -219,6 +221,7 @@ struct Pop {
                            Mat aux, float scale, const int* active);
   void critic_update(int B, const int* polyak_gate);
   void td3_step(int B, const uint8_t* d_mask);
+  void td3_policy_half(int B);
   void sac_step(int B);
   void step(int B, const uint8_t* d_mask);
   void update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,

@@ -29,6 +29,10 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
   const int in = sh.dims[l], out = sh.dims[l + 1];
   const float* Wl = W + sh.woff[l];
   const double flops = 2.0 * B * in * out * groups;
+  // algorithmic bytes: X (once per member when shared by the critics), W, b, Y (+ mask bits)
+  const double bytes = 4.0 * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
+                              static_cast<double>(groups) * (in * out + out + B * out)) +
+                       ((ymask && ymask->mask) ? groups * B * ((out + 31) / 32) * 4.0 : 0.0);
   if (use_tc() && out >= 16 && tma_ok(X.p, X.ld, X.gs) && tma_ok(Wl, out, sh.stride)) {
     TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
                 static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
@@ -65,7 +69,7 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
       a.mo_ld = ymask->mld;
     }
     a.b_prefetch = last_wrote_weights ? 0 : 1;
-    timed(PC_GEMM_FWD, flops, 0.0, active != nullptr,
+    timed(PC_GEMM_FWD, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
     return;
   }
@@ -94,7 +98,7 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
     g.noise_clip = h_f3.p;
     g.bound = bound;
   }
-  timed(PC_GEMM_FWD, flops, 0.0, active != nullptr, [&] {
+  timed(PC_GEMM_FWD, flops, bytes, active != nullptr, [&] {
     if (out <= 16) launch_fwd_skinny(g, stream);
     else launch_gemm_simt(g, stream);
   });
@@ -113,6 +117,12 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
   const int out = sh.dims[l + 1];
   const float* Wc = W + sh.woff[l] + static_cast<size_t>(col0) * out;
   const double flops = 2.0 * B * out * ncols * groups;
+  // algorithmic bytes: G, the W columns, DX, the ReLU' mask bits (or the tanh values)
+  const double bytes =
+      4.0 * groups * (static_cast<double>(B) * out + static_cast<double>(out) * ncols +
+                      static_cast<double>(B) * ncols) +
+      (epi == EPI_RELU_MASK ? groups * B * ((ncols + 31) / 32) * 4.0
+                            : (epi == EPI_TANH_GRAD ? 4.0 * groups * B * ncols : 0.0));
   if (use_tc() && out >= 8 && tma_ok(G.p, G.ld, G.gs) && tma_ok(Wc, out, sh.stride)) {
     TcOperand A{G.p, static_cast<uint64_t>(out), static_cast<uint64_t>(B),
                 static_cast<uint64_t>(groups), static_cast<uint64_t>(G.ld),
@@ -142,7 +152,7 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
     a.scale = scale;
     a.active = active;
     a.b_prefetch = last_wrote_weights ? 0 : 1;
-    timed(PC_GEMM_DX, flops, 0.0, active != nullptr,
+    timed(PC_GEMM_DX, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, false, a, stream); });
     return;
   }
@@ -162,7 +172,7 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
   g.acc_init = 0.0f;
   g.active = active;
   g.scale = scale;
-  timed(PC_GEMM_DX, flops, 0.0, active != nullptr, [&] {
+  timed(PC_GEMM_DX, flops, bytes, active != nullptr, [&] {
     if (out <= 16) launch_dx_skinny(g, stream);
     else launch_gemm_simt(g, stream);
   });
@@ -170,9 +180,12 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
 
 // dW_l and db_l into the gradient arena rows: dW = X^T G, db = column sums of G
 void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
-                  const int* active) {
+                  const int* active, bool bias_done) {
   const int in = sh.dims[l], out = sh.dims[l + 1];
   const double flops = 2.0 * B * in * out * groups;
+  // algorithmic bytes: X (once per member when shared), G, dW
+  const double bytes = 4.0 * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
+                              static_cast<double>(groups) * (B * out + in * out));
   if (use_tc() && out >= 32 && tma_ok(X.p, X.ld, X.gs) && tma_ok(G.p, G.ld, G.gs)) {
     TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
                 static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
@@ -192,10 +205,11 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
     a.c_gs = static_cast<long long>(sh.stride);
     a.c_rs = out;
     a.active = active;
-    timed(PC_GEMM_DW, flops, 0.0, active != nullptr,
+    timed(PC_GEMM_DW, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bg, true, true, a, stream); });
-    // bias gradient: per-column sums of G in row order (pop_add_bias_backward, :236-250)
-    timed(PC_ELEM, 0.0, 4.0 * B * out * groups, active != nullptr, [&] {
+    // bias gradient: per-column sums of G in row order (pop_add_bias_backward, :236-250),
+    // unless the kernel that produced G already wrote them
+    if (!bias_done) timed(PC_ELEM, 0.0, 4.0 * B * out * groups, active != nullptr, [&] {
       launch_colsum(groups, n, B, out, G.p, G.gs, G.ld, Gr + sh.boff[l],
                     static_cast<long long>(sh.stride), active, stream);
     });
@@ -216,7 +230,7 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
   g.epi = EPI_STORE;
   g.acc_init = 0.0f;
   g.active = active;
-  timed(PC_GEMM_DW, flops, 0.0, active != nullptr, [&] {
+  timed(PC_GEMM_DW, flops, bytes + 4.0 * groups * out, active != nullptr, [&] {
     if (out <= 16) launch_dw_skinny(g, stream);
     else launch_gemm_simt(g, stream);
   });
@@ -393,8 +407,13 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
     }
   }
   const double flops = 2.0 * B * groups * (static_cast<double>(in) * hdim + hdim * nout);
+  const double bytes =
+      4.0 * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
+             static_cast<double>(groups) *
+                 (in * hdim + hdim + hdim * nout + nout + B * nout +
+                  (keep_hidden ? B * hdim + B * ((hdim + 31) / 32) : 0)));
   a.b_prefetch = last_wrote_weights ? 0 : 1;
-  timed(PC_GEMM_FWD, flops, 0.0, active != nullptr,
+  timed(PC_GEMM_FWD, flops, bytes, active != nullptr,
         [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
   return true;
 }
@@ -404,6 +423,7 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
                        Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
                        const int* active) {
   const int L = sh.depth;
+  bool bias_done = false;  // the bias gradient of layer l was produced with its cotangent
   for (int l = L - 1; l >= 0; --l) {
     const Mat x = (l == 0) ? x0 : hid(hs, l - 1, B, sh, 0);
     if (l == L - 1 && sh.dims[L] <= 16 && static_cast<long long>(B) * sh.dims[L] <= 32768) {
@@ -434,10 +454,20 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
         a.dX = const_cast<float*>(dh.p);
         a.dx_gs = dh.gs;
         a.dx_ld = dh.ld;
+        if (use_tc() && sh.dims[l] >= 32) {  // the tcgen05 dW of layer l-1 skips its colsum
+          a.dbx = Gr + sh.boff[l - 1];
+          a.dbx_gs = static_cast<long long>(sh.stride);
+        }
       }
-      timed(PC_GEMM_DW, 2.0 * B * H * nout * groups * (l > 0 ? 2.0 : 1.0), 0.0,
+      // algorithmic bytes: X, G, W, dW + db, dX (+ the fused bias gradient below)
+      const double obytes =
+          4.0 * (static_cast<double>(B) * H * (x.by_member ? n : groups) +
+                 static_cast<double>(groups) *
+                     (B * nout + 2.0 * (H * nout + nout) + (l > 0 ? B * H + H : 0)));
+      timed(PC_GEMM_DW, 2.0 * B * H * nout * groups * (l > 0 ? 2.0 : 1.0), obytes,
             active != nullptr, [&] { launch_out_backward(a, stream); });
       G = dh;
+      bias_done = a.dbx != nullptr;
       continue;
     }
     if (l > 0) {
@@ -445,11 +475,12 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       const Mat dh = hid(dhs, l - 1, B, sh, 0);
       gemm_dx(sh, W, l, groups, B, G, x, const_cast<float*>(dh.p), dh.gs, dh.ld, EPI_RELU_MASK,
               0, sh.dims[l], active, 1.0f);
-      gemm_dw(sh, Gr, l, groups, B, x, G, active);
+      gemm_dw(sh, Gr, l, groups, B, x, G, active, bias_done);
       G = dh;
     } else {
-      gemm_dw(sh, Gr, l, groups, B, x, G, active);
+      gemm_dw(sh, Gr, l, groups, B, x, G, active, bias_done);
     }
+    bias_done = false;
   }
 }
 
@@ -490,9 +521,20 @@ void Pop::critic_update(int B, const int* polyak_gate) {
 // ------------------------------------------------------------------ TD3 step (algos.hpp:351-422)
 void Pop::td3_step(int B, const uint8_t* d_mask) {
   const long long nbB = B;
+  // graph capture: the policy half below becomes the body of a conditional IF node whose
+  // condition k_td3_step_begin sets when any member fires (steps where no policy fires replay
+  // only the critic half); eager mode runs it with every launch gated per member instead
+  cudaGraphConditionalHandle any_fire = 0;
+  if (capturing) {
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g = nullptr;
+    CUDA_CHECK(cudaStreamGetCaptureInfo(stream, &st, nullptr, &g, nullptr, nullptr));
+    CUDA_CHECK(cudaGraphConditionalHandleCreate(&any_fire, g, 0, cudaGraphCondAssignDefault));
+  }
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p, t_cri.p + n,
-                          steps.p, streams.p, seed, key_a.p, stream);
+                          steps.p, streams.p, seed, key_a.p, losses.p + 2 * n, any_fire,
+                          capturing ? 1 : 0, stream);
   });
   // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
   if (use_tc()) {
@@ -509,7 +551,47 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
         [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
   // twin critic update; target Polyak fused for members whose policy fires
   critic_update(B, fire.p);
-  // td3_policy_loss_grads (:318-338) on the UPDATED critic1, gated by the fire mask
+  if (capturing) {
+    cudaStreamCaptureStatus st;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CUDA_CHECK(cudaStreamGetCaptureInfo_v3(stream, &st, nullptr, &g, &deps, nullptr, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = any_fire;
+    cp.conditional.type = cudaGraphCondTypeIf;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CUDA_CHECK(cudaGraphAddNode(&node, g, deps, nd, &cp));
+    CUDA_CHECK(cudaStreamUpdateCaptureDependencies(stream, &node, 1,
+                                                   cudaStreamSetCaptureDependencies));
+    if (!side) CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CUDA_CHECK(cudaStreamBeginCaptureToGraph(side, body, nullptr, nullptr, 0,
+                                             cudaStreamCaptureModeThreadLocal));
+    std::swap(stream, side);
+    try {
+      td3_policy_half(B);
+    } catch (...) {
+      std::swap(stream, side);
+      cudaStreamEndCapture(side, &body);
+      throw;
+    }
+    std::swap(stream, side);
+    CUDA_CHECK(cudaStreamEndCapture(side, &body));
+    size_t nb = 0;
+    CUDA_CHECK(cudaGraphGetNodes(body, nullptr, &nb));
+    cond_body_nodes += nb;
+  } else {
+    td3_policy_half(B);
+  }
+}
+
+// td3_policy_loss_grads (:318-338) on the UPDATED critic1, policy Adam and the target Polyak,
+// every launch gated by the fire mask
+void Pop::td3_policy_half(int B) {
+  const long long nbB = B;
   const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
   mlp_forward(pol, pol_p.p, n, B, s, S.ph, S.sa_pi.p + ds, nbB * lsa, lsa, EPI_BIAS_TANH, fire.p,
               S.pt.p, nbB * da, da);
@@ -610,6 +692,7 @@ void Pop::step(int B, const uint8_t* d_mask) {
       g.masked = d_mask != nullptr;
       cudaGraph_t graph;
       capturing = true;
+      cond_body_nodes = 0;
       CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
       try {
         run_program(B, d_mask);
@@ -622,7 +705,8 @@ void Pop::step(int B, const uint8_t* d_mask) {
       capturing = false;
       size_t nodes = 0;
       CUDA_CHECK(cudaGraphGetNodes(graph, nullptr, &nodes));
-      g.nodes = nodes;
+      // kernel nodes: the conditional node stands for its body (the policy half)
+      g.nodes = nodes + cond_body_nodes - (cond_body_nodes ? 1 : 0);
       CUDA_CHECK(cudaGraphInstantiate(&g.exec, graph, 0));
       CUDA_CHECK(cudaGraphDestroy(graph));
       graphs.push_back(g);
