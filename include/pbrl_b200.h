@@ -180,6 +180,12 @@ int pbrl_selftest_libm(int fn, const float* dev_in, float* dev_out, uint64_t cou
 int pbrl_selftest_tc_gemm(int a_mn, int b_mn, int M, int N, int K, int groups, const float* A,
                           long long a_ld, long long a_gs, const float* B, long long b_ld,
                           long long b_gs, float* C, long long c_ld, long long c_gs);
+/* The same on the BF16 path (tcgen05 kind::f16): A and B are bf16 device arrays (uint16 bit
+ * patterns), C is fp32. */
+int pbrl_selftest_tc_gemm_bf16(int a_mn, int b_mn, int M, int N, int K, int groups,
+                               const void* A, long long a_ld, long long a_gs, const void* B,
+                               long long b_ld, long long b_gs, float* C, long long c_ld,
+                               long long c_gs);
 
 /* Phase timeline of the tcgen05 GEMM launches recorded since process start when the environment
  * variable PBRL_TC_TRACE is set (diagnostics only; off by default).  Copies up to max_launches

@@ -78,6 +78,9 @@ SIGNATURES = {
     "pbrl_selftest_tc_gemm": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
                               C.c_longlong, C.c_longlong, vp, C.c_longlong, C.c_longlong, vp,
                               C.c_longlong, C.c_longlong],
+    "pbrl_selftest_tc_gemm_bf16": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, vp,
+                                   C.c_longlong, C.c_longlong, vp, C.c_longlong, C.c_longlong,
+                                   vp, C.c_longlong, C.c_longlong],
     "pbrl_synthetic_batches_device": [vp, u64, u64, u64, u64, u64, u64, C.POINTER(Batch)],
 }
 

@@ -185,6 +185,7 @@ int pbrl_set_member(pbrl_pop* pop, int net, uint64_t member, const float* flat) 
     float* dst = p->net_row(net, member);
     CUDA_CHECK(cudaMemcpyAsync(dst, flat, p->net_shape(net).P * 4, cudaMemcpyHostToDevice,
                                p->stream));
+    p->weights_dirty = true;
     p->sync();
   });
 }
@@ -197,6 +198,7 @@ int pbrl_copy_member(pbrl_pop* pop, int net, uint64_t src, uint64_t dst) {
     if (src == dst) return;
     CUDA_CHECK(cudaMemcpyAsync(p->net_row(net, dst), p->net_row(net, src),
                                p->net_shape(net).P * 4, cudaMemcpyDeviceToDevice, p->stream));
+    p->weights_dirty = true;
     p->sync();
   });
 }
@@ -371,11 +373,14 @@ bool replay_ready(Pop* p, uint64_t min_size) {
   return true;
 }
 
-void gather(Pop* p, int B, uint64_t seed, uint64_t draw_id) {
+// act16: the critic-input buffers are bf16 (BF16-mode update); sample_batch reads them back
+// as fp32 rows, so it gathers with act16 = 0 (the buffers hold enough bytes for either)
+void gather(Pop* p, int B, uint64_t seed, uint64_t draw_id, int act16) {
   Replay* r = p->replay;
   launch_replay_gather(p->n, B, p->ds, p->da, p->lsa, r->rw, r->ring.p, r->cap,
                        r->mode == PBRL_REPLAY_SHARED, r->sizes.p, p->streams.p, seed, draw_id,
-                       p->S.in_sa.p, p->S.in_s2a.p, p->S.sa_pi.p, p->S.r.p, p->S.d.p, p->stream);
+                       p->S.in_sa.p, p->S.in_s2a.p, p->S.sa_pi.p, p->S.r.p, p->S.d.p, act16,
+                       p->stream);
   p->count_launch(1);
 }
 }  // namespace
@@ -389,7 +394,7 @@ int pbrl_sample_batch(pbrl_pop* pop, uint64_t seed, uint64_t draw_id, uint64_t r
     if (!replay_ready(p, min_size)) return;
     const int B = static_cast<int>(rows);
     p->ensure_scratch(B);
-    gather(p, B, seed, draw_id);
+    gather(p, B, seed, draw_id, 0);
     const size_t nb = static_cast<size_t>(p->n) * B;
     const int dsa = p->lsa;
     std::vector<float> sa(nb * dsa), s2a(nb * dsa);
@@ -419,7 +424,7 @@ int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t seed, uint64_t first_draw_
     p->ensure_scratch(B);
     p->ensure_corr(p->t_bound + k + 4);
     for (uint32_t i = 0; i < k; ++i) {
-      gather(p, B, seed, first_draw_id + i);
+      gather(p, B, seed, first_draw_id + i, p->act16() ? 1 : 0);
       p->step(B, nullptr);
     }
     CUDA_CHECK(cudaGetLastError());
@@ -491,6 +496,7 @@ int pbrl_pbt_apply(pbrl_pop* pop, const uint64_t* replaced, const uint64_t* dono
                                      cudaMemcpyDeviceToDevice, p->stream));
       }
       p->count_launch(p->algo == PBRL_ALGO_TD3 ? 6 : 5);
+      p->weights_dirty = true;
     }
     // MlpAdam::reset_member (optim.hpp:32-35), delay_acc = 0 (evolve.hpp:185)
     const int nr = static_cast<int>(reset.size());
@@ -586,6 +592,7 @@ int pbrl_import_member(pbrl_pop* pop, uint64_t member, const float* buf) {
     }
     if (p->algo == PBRL_ALGO_SAC)
       CUDA_CHECK(cudaMemcpyAsync(p->log_alpha.p + member, buf + at, 4, cudaMemcpyDeviceToDevice, p->stream));
+    p->weights_dirty = true;
     p->sync();
   });
 }
@@ -641,31 +648,47 @@ int pbrl_selftest_libm(int fn, const float* dev_in, float* dev_out, uint64_t cou
   });
 }
 
+static void selftest_tc(int eb, int a_mn, int b_mn, int M, int N, int K, int groups,
+                        const void* A, long long a_ld, long long a_gs, const void* B,
+                        long long b_ld, long long b_gs, float* C, long long c_ld, long long c_gs) {
+  TcOperand a{A, static_cast<uint64_t>(a_mn ? M : K), static_cast<uint64_t>(a_mn ? K : M),
+              static_cast<uint64_t>(groups), static_cast<uint64_t>(a_ld),
+              static_cast<uint64_t>(a_gs)};
+  TcOperand b{B, static_cast<uint64_t>(b_mn ? N : K), static_cast<uint64_t>(b_mn ? K : N),
+              static_cast<uint64_t>(groups), static_cast<uint64_t>(b_ld),
+              static_cast<uint64_t>(b_gs)};
+  if (!tma_ok(A, a_ld, a_gs, eb) || !tma_ok(B, b_ld, b_gs, eb))
+    PBRL_THROW(PBRL_E_SHAPE, "operands are not TMA-aligned");
+  TcArgs g;
+  g.eb = eb;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.groups = groups;
+  g.n_members = groups;
+  g.epi = EPI_STORE;
+  g.C = C;
+  g.c_gs = c_gs;
+  g.c_rs = c_ld;
+  launch_tc_gemm(a, b, a_mn != 0, b_mn != 0, g, nullptr);
+  CUDA_CHECK(cudaGetLastError());
+  CUDA_CHECK(cudaDeviceSynchronize());
+}
+
 int pbrl_selftest_tc_gemm(int a_mn, int b_mn, int M, int N, int K, int groups, const float* A,
                           long long a_ld, long long a_gs, const float* B, long long b_ld,
                           long long b_gs, float* C, long long c_ld, long long c_gs) {
   return guarded([&] {
-    TcOperand a{A, static_cast<uint64_t>(a_mn ? M : K), static_cast<uint64_t>(a_mn ? K : M),
-                static_cast<uint64_t>(groups), static_cast<uint64_t>(a_ld),
-                static_cast<uint64_t>(a_gs)};
-    TcOperand b{B, static_cast<uint64_t>(b_mn ? N : K), static_cast<uint64_t>(b_mn ? K : N),
-                static_cast<uint64_t>(groups), static_cast<uint64_t>(b_ld),
-                static_cast<uint64_t>(b_gs)};
-    if (!tma_ok(A, a_ld, a_gs) || !tma_ok(B, b_ld, b_gs))
-      PBRL_THROW(PBRL_E_SHAPE, "operands are not TMA-aligned");
-    TcArgs g;
-    g.M = M;
-    g.N = N;
-    g.K = K;
-    g.groups = groups;
-    g.n_members = groups;
-    g.epi = EPI_STORE;
-    g.C = C;
-    g.c_gs = c_gs;
-    g.c_rs = c_ld;
-    launch_tc_gemm(a, b, a_mn != 0, b_mn != 0, g, nullptr);
-    CUDA_CHECK(cudaGetLastError());
-    CUDA_CHECK(cudaDeviceSynchronize());
+    selftest_tc(4, a_mn, b_mn, M, N, K, groups, A, a_ld, a_gs, B, b_ld, b_gs, C, c_ld, c_gs);
+  });
+}
+
+int pbrl_selftest_tc_gemm_bf16(int a_mn, int b_mn, int M, int N, int K, int groups,
+                               const void* A, long long a_ld, long long a_gs, const void* B,
+                               long long b_ld, long long b_gs, float* C, long long c_ld,
+                               long long c_gs) {
+  return guarded([&] {
+    selftest_tc(2, a_mn, b_mn, M, N, K, groups, A, a_ld, a_gs, B, b_ld, b_gs, C, c_ld, c_gs);
   });
 }
 

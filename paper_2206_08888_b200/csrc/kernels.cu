@@ -183,7 +183,8 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t s) {
 
 // forward, N <= 16: one thread per output row; the X tile is staged through shared memory
 // (coalesced), W [K][N] lives in shared memory; acc[o] runs k = 0..K-1.
-template <int NMAX>
+// AT: element type of A (bf16 activations in BF16 mode); C is bf16 when g.c16
+template <int NMAX, typename AT>
 __global__ void __launch_bounds__(128) k_fwd_skinny(const GemmArgs g) {
   PDL_ENTRY();
   constexpr int ROWS = 128, KC = 32;
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(128) k_fwd_skinny(const GemmArgs g) {
   if (g.active && !g.active[mem]) return;
   __shared__ float Xs[ROWS][KC + 1];
   __shared__ float Ws[KC][NMAX];
-  const float* A = g.A.p + (g.A.by_member ? mem : grp) * g.A.gs;
+  const AT* A = reinterpret_cast<const AT*>(g.A.p) + (g.A.by_member ? mem : grp) * g.A.gs;
   const float* Bm = g.B.p + (g.B.by_member ? mem : grp) * g.B.gs;
   const int r0 = blockIdx.x * ROWS, tid = threadIdx.x;
   float acc[NMAX];
@@ -203,7 +204,8 @@ __global__ void __launch_bounds__(128) k_fwd_skinny(const GemmArgs g) {
     for (int e = tid; e < ROWS * KC; e += ROWS) {
       const int rr = e / KC, kk = e % KC;
       const int row = r0 + rr;
-      Xs[rr][kk] = (row < g.M && kk < kc) ? A[row * g.A.rs + (k0 + kk) * g.A.cs] : 0.0f;
+      Xs[rr][kk] =
+          (row < g.M && kk < kc) ? act_ld(A, row * g.A.rs + (k0 + kk) * g.A.cs) : 0.0f;
     }
     for (int e = tid; e < KC * NMAX; e += ROWS) {
       const int kk = e / NMAX, o = e % NMAX;
@@ -219,12 +221,15 @@ __global__ void __launch_bounds__(128) k_fwd_skinny(const GemmArgs g) {
   }
   const int row = r0 + tid;
   if (row >= g.M) return;
-  float* C = g.C + (g.c_by_member ? mem : grp) * g.c_gs;
+  const long long cbase = (g.c_by_member ? mem : grp) * g.c_gs;
   const float* bias = g.bias.p ? g.bias.p + (g.bias.by_member ? mem : grp) * g.bias.gs : nullptr;
   const float* aux = g.aux.p ? g.aux.p + (g.aux.by_member ? mem : grp) * g.aux.gs : nullptr;
 #pragma unroll
   for (int o = 0; o < NMAX; ++o) {
-    if (o < g.N) C[row * g.c_rs + o] = simt_epilogue(g, acc[o], row, o, grp, mem, bias, aux);
+    if (o >= g.N) continue;
+    const float v = simt_epilogue(g, acc[o], row, o, grp, mem, bias, aux);
+    if (g.c16) act_st(reinterpret_cast<__nv_bfloat16*>(g.C), cbase + row * g.c_rs + o, v);
+    else g.C[cbase + row * g.c_rs + o] = v;
   }
 }
 
@@ -297,7 +302,9 @@ __global__ void __launch_bounds__(128) k_dw_skinny(const GemmArgs g) {
 // partials are combined in slice order through shared memory (deterministic).
 constexpr int kObCols = 64, kObSlices = 4;
 
-template <int NO>  // fused output width: exact for 1 / 6 / 12, runtime-guarded up to 16
+// AT: activation storage of X / dX (fp32, or bf16 in BF16 mode).  dW == nullptr: dX only (the
+// output layer of a critic inside the policy-loss chain, whose weight gradients are discarded).
+template <int NO, typename AT>  // fused output width: exact for 1 / 6 / 12, runtime-guarded up to 16
 __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs a) {
   PDL_ENTRY();
   extern __shared__ float sm[];
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
   const int slices = blockDim.x / kObCols;
   const int col = threadIdx.x % kObCols, sl = threadIdx.x / kObCols;
   const int i = blockIdx.x * kObCols + col;
-  const float* X = a.X + (a.x_by_member ? mem : grp) * a.x_gs;
+  const AT* X = static_cast<const AT*>(a.X) + (a.x_by_member ? mem : grp) * a.x_gs;
   const float* G = a.G + grp * a.g_gs;
   const float* W = a.W + grp * a.w_gs;
   for (int e = threadIdx.x; e < B * nout; e += blockDim.x) {
@@ -328,7 +335,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
   __syncthreads();
   const int rows = (B + slices - 1) / slices;
   const int b0 = sl * rows, b1 = min(B, b0 + rows);
-  float* dX = a.dX ? a.dX + grp * a.dx_gs : nullptr;
+  AT* dX = a.dX ? static_cast<AT*>(a.dX) + grp * a.dx_gs : nullptr;
   float csum = 0.0f;  // column sum of this thread's dX rows (bias gradient of the layer below)
   if (i < a.H) {
     constexpr int U = 8;  // independent loads in flight per thread
@@ -336,7 +343,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
     for (; b + U <= b1; b += U) {
       float xv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = __ldg(X + static_cast<long long>(b + u) * a.x_ld + i);
+      for (int u = 0; u < U; ++u) xv[u] = act_ld(X, static_cast<long long>(b + u) * a.x_ld + i);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const float* g = Gs + (b + u) * nout;
@@ -349,11 +356,11 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
         }
         const float dv = xv[u] > 0.0f ? d : 0.0f;
         csum = csum + dv;
-        if (dX) dX[static_cast<long long>(b + u) * a.dx_ld + i] = dv;
+        if (dX) act_st(dX, static_cast<long long>(b + u) * a.dx_ld + i, dv);
       }
     }
     for (; b < b1; ++b) {
-      const float xv = __ldg(X + static_cast<long long>(b) * a.x_ld + i);
+      const float xv = act_ld(X, static_cast<long long>(b) * a.x_ld + i);
       const float* g = Gs + b * nout;
       float d = 0.0f;
 #pragma unroll
@@ -364,7 +371,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
       }
       const float dv = xv > 0.0f ? d : 0.0f;
       csum = csum + dv;
-      if (dX) dX[static_cast<long long>(b) * a.dx_ld + i] = dv;
+      if (dX) act_st(dX, static_cast<long long>(b) * a.dx_ld + i, dv);
     }
   }
   if (a.dbx) {  // fused bias gradient of the layer below: slices combined in slice order
@@ -381,6 +388,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
       db[i] = csum;
     }
   }
+  if (!a.dW) return;
   float* dW = a.dW + grp * a.dw_gs;
   if (slices > 1) {
 #pragma unroll
@@ -419,35 +427,47 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
   }
 }
 
-template <int NO>
+template <int NO, typename AT>
 static void launch_ob(const OutBwdArgs& a, cudaStream_t s) {
   const int slices = a.exact ? 1 : kObSlices;
   const size_t smem =
       (static_cast<size_t>(a.B) * a.nout + kObSlices * kObCols * (a.nout + 1)) * 4;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_out_backward<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_out_backward<NO, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr = true;
   }
   dim3 grid((a.H + kObCols - 1) / kObCols, a.groups);
-  launch_k(k_out_backward<NO>, grid, kObCols * slices, smem, s, a);
+  launch_k(k_out_backward<NO, AT>, grid, kObCols * slices, smem, s, a);
 }
 
-void launch_out_backward(const OutBwdArgs& a, cudaStream_t s) {
+template <typename AT>
+static void launch_ob_t(const OutBwdArgs& a, cudaStream_t s) {
   switch (a.nout) {
-    case 1: launch_ob<1>(a, s); return;
-    case 6: launch_ob<6>(a, s); return;
-    case 12: launch_ob<12>(a, s); return;
-    default: launch_ob<16>(a, s); return;
+    case 1: launch_ob<1, AT>(a, s); return;
+    case 6: launch_ob<6, AT>(a, s); return;
+    case 12: launch_ob<12, AT>(a, s); return;
+    default: launch_ob<16, AT>(a, s); return;
   }
 }
 
-void launch_fwd_skinny(const GemmArgs& g, cudaStream_t s) {
+void launch_out_backward(const OutBwdArgs& a, cudaStream_t s) {
+  if (a.act16) launch_ob_t<__nv_bfloat16>(a, s);
+  else launch_ob_t<float>(a, s);
+}
+
+template <typename AT>
+static void launch_fwd_skinny_t(const GemmArgs& g, cudaStream_t s) {
   dim3 grid((g.M + 127) / 128, g.groups);
-  if (g.N <= 1) launch_k(k_fwd_skinny<1>, grid, 128, 0, s, g);
-  else if (g.N <= 8) launch_k(k_fwd_skinny<8>, grid, 128, 0, s, g);
-  else launch_k(k_fwd_skinny<16>, grid, 128, 0, s, g);
+  if (g.N <= 1) launch_k(k_fwd_skinny<1, AT>, grid, 128, 0, s, g);
+  else if (g.N <= 8) launch_k(k_fwd_skinny<8, AT>, grid, 128, 0, s, g);
+  else launch_k(k_fwd_skinny<16, AT>, grid, 128, 0, s, g);
+}
+
+void launch_fwd_skinny(const GemmArgs& g, cudaStream_t s) {
+  if (g.a16) launch_fwd_skinny_t<__nv_bfloat16>(g, s);
+  else launch_fwd_skinny_t<float>(g, s);
 }
 
 void launch_dx_skinny(const GemmArgs& g, cudaStream_t s) {
@@ -509,10 +529,10 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts
+template <typename AT>
 __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float* s,
                              const float* a, const float* r, const float* s2, const float* d,
-                             float* in_sa, float* in_s2a, float* sa_pi, float* r_out,
-                             float* d_out) {
+                             AT* in_sa, AT* in_s2a, AT* sa_pi, float* r_out, float* d_out) {
   PDL_ENTRY();
   const int dsa = ds + da;
   const long long rows = static_cast<long long>(n) * B;
@@ -524,11 +544,11 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float*
     const long long o = row * lsa + c;
     if (c < ds) {
       const float sv = s[row * ds + c];
-      in_sa[o] = sv;
-      sa_pi[o] = sv;
-      in_s2a[o] = s2[row * ds + c];
+      act_st(in_sa, o, sv);
+      act_st(sa_pi, o, sv);
+      act_st(in_s2a, o, s2[row * ds + c]);
     } else {
-      in_sa[o] = a[row * da + (c - ds)];
+      act_st(in_sa, o, a[row * da + (c - ds)]);
     }
     if (c == 0) {
       r_out[row] = r[row];
@@ -538,12 +558,19 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float*
 }
 
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
-                       const float* r, const float* s2, const float* d, float* in_sa,
-                       float* in_s2a, float* sa_pi, float* r_out, float* d_out, cudaStream_t st) {
+                       const float* r, const float* s2, const float* d, void* in_sa,
+                       void* in_s2a, void* sa_pi, float* r_out, float* d_out, int act16,
+                       cudaStream_t st) {
   const long long total = static_cast<long long>(n) * B * (ds + da);
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-  launch_k(k_pack_batch, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d, in_sa, in_s2a, sa_pi,
-                                       r_out, d_out);
+  if (act16)
+    launch_k(k_pack_batch<__nv_bfloat16>, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d,
+             static_cast<__nv_bfloat16*>(in_sa), static_cast<__nv_bfloat16*>(in_s2a),
+             static_cast<__nv_bfloat16*>(sa_pi), r_out, d_out);
+  else
+    launch_k(k_pack_batch<float>, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d,
+             static_cast<float*>(in_sa), static_cast<float*>(in_s2a), static_cast<float*>(sa_pi),
+             r_out, d_out);
 }
 
 // y = r + gamma*(1-done)*min(Q1', Q2')   (algos.hpp:268-281)
@@ -640,7 +667,9 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
                                               const float* corr2, const float* lr,
                                               const int* active, float* __restrict__ tgt,
                                               const float* tau_a, const float* tau_b,
-                                              const int* polyak_gate) {
+                                              const int* polyak_gate,
+                                              __nv_bfloat16* __restrict__ p16,
+                                              __nv_bfloat16* __restrict__ t16) {
   PDL_ENTRY();
   const int grp = blockIdx.y;
   const int m = grp % n;
@@ -675,12 +704,22 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
     p4[k] = pv;
     m4[k] = mv;
     v4[k] = vv;
+    if (p16) {  // BF16 mode: the tensor-core copy of the fresh parameters
+      __nv_bfloat162* d2 = reinterpret_cast<__nv_bfloat162*>(p16 + base) + 2 * k;
+      d2[0] = __floats2bfloat162_rn(pv.x, pv.y);
+      d2[1] = __floats2bfloat162_rn(pv.z, pv.w);
+    }
     if (a.polyak) {
       tv.x = a.ta * pv.x + a.tb * tv.x;
       tv.y = a.ta * pv.y + a.tb * tv.y;
       tv.z = a.ta * pv.z + a.tb * tv.z;
       tv.w = a.ta * pv.w + a.tb * tv.w;
       t4[k] = tv;
+      if (t16) {
+        __nv_bfloat162* d2 = reinterpret_cast<__nv_bfloat162*>(t16 + base) + 2 * k;
+        d2[0] = __floats2bfloat162_rn(tv.x, tv.y);
+        d2[1] = __floats2bfloat162_rn(tv.z, tv.w);
+      }
     }
   }
   if (blockIdx.x == 0) {
@@ -691,7 +730,11 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
       p[e] = pk;
       mo[e] = mk;
       vo[e] = vk;
-      if (a.polyak) tgt[e] = a.ta * pk + a.tb * tgt[e];
+      if (p16) p16[e] = __float2bfloat16_rn(pk);
+      if (a.polyak) {
+        tgt[e] = a.ta * pk + a.tb * tgt[e];
+        if (t16) t16[e] = __float2bfloat16_rn(tgt[e]);
+      }
     }
   }
 }
@@ -699,18 +742,33 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
 void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m, float* v,
                  const float* g, const int64_t* t, const float* corr1, const float* corr2,
                  const float* lr, const int* active, float* tgt, const float* tau_a,
-                 const float* tau_b, const int* polyak_gate, cudaStream_t s) {
+                 const float* tau_b, const int* polyak_gate, __nv_bfloat16* p16,
+                 __nv_bfloat16* t16, cudaStream_t s) {
   const int threads = 256;
   int bx = static_cast<int>((P / 4 + threads - 1) / threads);
   bx = bx < 1 ? 1 : bx;
   dim3 grid(bx, groups);
   launch_k(k_adam, grid, threads, 0, s, n, P, stride, p, m, v, g, t, corr1, corr2, lr, active, tgt,
-                                  tau_a, tau_b, polyak_gate);
+           tau_a, tau_b, polyak_gate, p16, t16);
+}
+
+__global__ void k_to_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                          size_t count) {
+  PDL_ENTRY();
+  for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[e] = __float2bfloat16_rn(src[e]);
+}
+
+void launch_to_bf16(const float* src, __nv_bfloat16* dst, size_t count, cudaStream_t s) {
+  const int blocks = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 8));
+  launch_k(k_to_bf16, std::max(blocks, 1), 256, 0, s, src, dst, count);
 }
 
 // bias gradient for the tensor-core dW path: column sums of G over the batch, two-level and
 // deterministic (32 columns x 8 row segments per block, segments combined in a fixed order).
-__global__ void __launch_bounds__(256) k_colsum(int n, int B, int N, const float* G, long long g_gs,
+template <typename AT>
+__global__ void __launch_bounds__(256) k_colsum(int n, int B, int N, const AT* G, long long g_gs,
                                                 long long g_ld, float* dst, long long dst_gs,
                                                 const int* active) {
   PDL_ENTRY();
@@ -723,16 +781,16 @@ __global__ void __launch_bounds__(256) k_colsum(int n, int B, int N, const float
   const int b0 = seg * rows, b1 = min(B, b0 + rows);
   float acc = 0.0f;
   if (o < N) {
-    const float* g = G + grp * g_gs + o;
+    const AT* g = G + grp * g_gs + o;
     int b = b0;
     for (; b + 8 <= b1; b += 8) {
       float v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = g[static_cast<long long>(b + u) * g_ld];
+      for (int u = 0; u < 8; ++u) v[u] = act_ld(g, static_cast<long long>(b + u) * g_ld);
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc += v[u];
     }
-    for (; b < b1; ++b) acc += g[static_cast<long long>(b) * g_ld];
+    for (; b < b1; ++b) acc += act_ld(g, static_cast<long long>(b) * g_ld);
   }
   part[seg][c] = acc;
   __syncthreads();
@@ -744,10 +802,15 @@ __global__ void __launch_bounds__(256) k_colsum(int n, int B, int N, const float
   }
 }
 
-void launch_colsum(int groups, int n, int B, int N, const float* G, long long g_gs, long long g_ld,
-                   float* dst, long long dst_gs, const int* active, cudaStream_t s) {
+void launch_colsum(int groups, int n, int B, int N, const void* G, long long g_gs, long long g_ld,
+                   float* dst, long long dst_gs, const int* active, int act16, cudaStream_t s) {
   dim3 grid((N + 31) / 32, groups);
-  launch_k(k_colsum, grid, 256, 0, s, n, B, N, G, g_gs, g_ld, dst, dst_gs, active);
+  if (act16)
+    launch_k(k_colsum<__nv_bfloat16>, grid, 256, 0, s, n, B, N,
+             static_cast<const __nv_bfloat16*>(G), g_gs, g_ld, dst, dst_gs, active);
+  else
+    launch_k(k_colsum<float>, grid, 256, 0, s, n, B, N, static_cast<const float*>(G), g_gs, g_ld,
+             dst, dst_gs, active);
 }
 
 // one thread per (group, row, 32-column word)
@@ -861,8 +924,9 @@ __device__ __forceinline__ float l1mts(float x) {
 }
 
 // split_policy_head + draw_eps + tanh_gaussian_logprob + tanh squash (algos.hpp:534-629)
+template <typename AT>
 __global__ void k_sac_head(int n, int B, int ds, int da, int lsa, const float* head, const uint64_t* key,
-                           float bound, float log_bound, float* sa, float* x, float* th,
+                           float bound, float log_bound, AT* sa, float* x, float* th,
                            float* ls_out, uint8_t* clamped, float* eps_out, float* logp) {
   PDL_ENTRY();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;  // (m, b)
@@ -891,17 +955,22 @@ __global__ void k_sac_head(int n, int B, int ds, int da, int lsa, const float* h
     if (ls_out) ls_out[k] = ls;
     if (clamped) clamped[k] = c;
     if (eps_out) eps_out[k] = ep;
-    sa[static_cast<long long>(e) * lsa + ds + j] = t * bound;
+    act_st(sa, static_cast<long long>(e) * lsa + ds + j, t * bound);
   }
   logp[e] = acc;
 }
 
 void launch_sac_head(int n, int B, int ds, int da, int lsa, const float* head,
-                     const uint64_t* key, float bound, float* sa, float* x, float* th, float* ls,
-                     uint8_t* clamped, float* eps, float* logp, cudaStream_t s) {
+                     const uint64_t* key, float bound, void* sa, float* x, float* th, float* ls,
+                     uint8_t* clamped, float* eps, float* logp, int act16, cudaStream_t s) {
   extern float host_logf(float);
-  launch_k(k_sac_head, (n * B + 127) / 128, 128, 0, s, n, B, ds, da, lsa, head, key, bound, host_logf(bound),
-                                                 sa, x, th, ls, clamped, eps, logp);
+  if (act16)
+    launch_k(k_sac_head<__nv_bfloat16>, (n * B + 127) / 128, 128, 0, s, n, B, ds, da, lsa, head,
+             key, bound, host_logf(bound), static_cast<__nv_bfloat16*>(sa), x, th, ls, clamped,
+             eps, logp);
+  else
+    launch_k(k_sac_head<float>, (n * B + 127) / 128, 128, 0, s, n, B, ds, da, lsa, head, key,
+             bound, host_logf(bound), static_cast<float*>(sa), x, th, ls, clamped, eps, logp);
 }
 
 // y = rs*r + gamma*(1-d)*(min(Q1',Q2') - alpha*logp')  (algos.hpp:759-774)
@@ -1048,11 +1117,11 @@ void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t 
 // sample_batch (replay.hpp:181-204): slot = bits(key, b) % size with key =
 // RngStream::of(seed, streams[m], kSample, draw_id); one warp gathers one row (coalesced 4 B
 // lanes over the row) straight into the critic-input layouts.
+template <typename AT>
 __global__ void k_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const float* ring,
                                 uint64_t cap, int shared, const uint64_t* sizes,
                                 const uint64_t* streams, uint64_t seed, uint64_t draw_id,
-                                float* in_sa, float* in_s2a, float* sa_pi, float* r_out,
-                                float* d_out) {
+                                AT* in_sa, AT* in_s2a, AT* sa_pi, float* r_out, float* d_out) {
   PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1067,12 +1136,12 @@ __global__ void k_replay_gather(int n, int B, int ds, int da, int lsa, int rw, c
   for (int c = lane; c < 2 * ds + da + 2; c += 32) {
     const float v = row[c];
     if (c < ds) {
-      in_sa[o + c] = v;
-      if (sa_pi) sa_pi[o + c] = v;
+      act_st(in_sa, o + c, v);
+      if (sa_pi) act_st(sa_pi, o + c, v);
     } else if (c < dsa) {
-      in_sa[o + c] = v;
+      act_st(in_sa, o + c, v);
     } else if (c < dsa + ds) {
-      in_s2a[o + (c - dsa)] = v;
+      act_st(in_s2a, o + (c - dsa), v);
     } else if (c == dsa + ds) {
       r_out[warp] = v;
     } else {
@@ -1084,12 +1153,19 @@ __global__ void k_replay_gather(int n, int B, int ds, int da, int lsa, int rw, c
 void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const float* ring,
                           uint64_t cap, int shared, const uint64_t* sizes,
                           const uint64_t* streams, uint64_t seed, uint64_t draw_id,
-                          float* in_sa, float* in_s2a, float* sa_pi, float* r_out, float* d_out,
-                          cudaStream_t s) {
+                          void* in_sa, void* in_s2a, void* sa_pi, float* r_out, float* d_out,
+                          int act16, cudaStream_t s) {
   const long long warps = static_cast<long long>(n) * B;
   const int blocks = static_cast<int>((warps * 32 + 255) / 256);
-  launch_k(k_replay_gather, blocks, 256, 0, s, n, B, ds, da, lsa, rw, ring, cap, shared, sizes, streams,
-                                         seed, draw_id, in_sa, in_s2a, sa_pi, r_out, d_out);
+  if (act16)
+    launch_k(k_replay_gather<__nv_bfloat16>, blocks, 256, 0, s, n, B, ds, da, lsa, rw, ring, cap,
+             shared, sizes, streams, seed, draw_id, static_cast<__nv_bfloat16*>(in_sa),
+             static_cast<__nv_bfloat16*>(in_s2a), static_cast<__nv_bfloat16*>(sa_pi), r_out,
+             d_out);
+  else
+    launch_k(k_replay_gather<float>, blocks, 256, 0, s, n, B, ds, da, lsa, rw, ring, cap, shared,
+             sizes, streams, seed, draw_id, static_cast<float*>(in_sa),
+             static_cast<float*>(in_s2a), static_cast<float*>(sa_pi), r_out, d_out);
 }
 
 // ================================================================== PBT

@@ -47,10 +47,9 @@ Pop::Pop(const pbrl_pop_desc& d) {
   if (d.n < 1) PBRL_THROW(PBRL_E_CONFIG, "population size must be >= 1");
   if (d.obs_dim < 1 || d.act_dim < 1) PBRL_THROW(PBRL_E_CONFIG, "obs_dim/act_dim must be >= 1");
   if (d.n_hidden > kMaxLayers - 1) PBRL_THROW(PBRL_E_CONFIG, "too many hidden layers");
-  if (d.precision != PBRL_PREC_FFMA32 && d.precision != PBRL_PREC_TF32)
-    PBRL_THROW(PBRL_E_CONFIG, d.precision == PBRL_PREC_BF16
-                                  ? "bf16 operands are not built in this version (use tf32)"
-                                  : "unknown precision mode");
+  if (d.precision != PBRL_PREC_FFMA32 && d.precision != PBRL_PREC_TF32 &&
+      d.precision != PBRL_PREC_BF16)
+    PBRL_THROW(PBRL_E_CONFIG, "unknown precision mode");
   algo = d.algo;
   precision = d.precision;
   device = d.device;
@@ -132,6 +131,13 @@ Pop::Pop(const pbrl_pop_desc& d) {
   if (algo == PBRL_ALGO_TD3)
     CUDA_CHECK(cudaMemcpyAsync(pol_t.p, pol_p.p, np * 4, cudaMemcpyDeviceToDevice, stream));
   CUDA_CHECK(cudaMemcpyAsync(cri_t.p, cri_p.p, nc * 4, cudaMemcpyDeviceToDevice, stream));
+  if (act16()) {
+    pol_p16.alloc(np);
+    if (algo == PBRL_ALGO_TD3) pol_t16.alloc(np);
+    cri_p16.alloc(nc);
+    cri_t16.alloc(nc);
+  }
+  weights_dirty = true;
 
   // hyper defaults (Td3Hyper::defaults algos.hpp:42-53, SacHyper::defaults :121-131)
   if (algo == PBRL_ALGO_TD3) {
@@ -163,6 +169,32 @@ Pop::~Pop() {
 }
 
 void Pop::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
+
+// BF16 mode: re-derive the bf16 tensor-core copies from the fp32 master weights (after init,
+// set_member, PBT exploit copies, imports); the update step itself keeps them current
+void Pop::refresh_shadows() {
+  if (!act16()) return;
+  const size_t np = static_cast<size_t>(n) * pol.stride;
+  const size_t nc = 2 * static_cast<size_t>(n) * cri.stride;
+  launch_to_bf16(pol_p.p, pol_p16.p, np, stream);
+  if (pol_t16.p) launch_to_bf16(pol_t.p, pol_t16.p, np, stream);
+  launch_to_bf16(cri_p.p, cri_p16.p, nc, stream);
+  launch_to_bf16(cri_t.p, cri_t16.p, nc, stream);
+  count_launch(pol_t16.p ? 4 : 3);
+  last_wrote_weights = true;
+  weights_dirty = false;
+}
+
+const void* Pop::wop(const float* W) const {
+  if (!act16()) return W;
+  const std::pair<const DBuf<float>*, const DBuf<__nv_bfloat16>*> arenas[] = {
+      {&pol_p, &pol_p16}, {&pol_t, &pol_t16}, {&cri_p, &cri_p16}, {&cri_t, &cri_t16}};
+  for (const auto& a : arenas) {
+    if (a.first->p && W >= a.first->p && W < a.first->p + a.first->count)
+      return a.second->p + (W - a.first->p);
+  }
+  PBRL_THROW(PBRL_E_USAGE, "bf16 mode: weight operand outside the parameter arenas");
+}
 
 int Pop::field_index(const std::string& f) const {
   for (size_t i = 0; i < fields.size(); ++i)
@@ -255,7 +287,7 @@ void Pop::ensure_scratch(int B) {
   const size_t nb = static_cast<size_t>(n) * B;
   const int L = pol.depth;
   // row strides padded to 4 floats: every activation is a legal TMA source (16 B strides)
-  lsa = pad4(ds + da);
+  lsa = padl(ds + da);
   S.in_sa.alloc(nb * lsa);
   S.in_s2a.alloc(nb * lsa);
   S.sa_pi.alloc(nb * lsa);
@@ -278,7 +310,7 @@ void Pop::ensure_scratch(int B) {
   S.bd.alloc(nb);
   for (int l = 0; l + 1 < L; ++l) {
     // activations [rows][pad4(H)] + the ReLU mask bits [rows][ceil(H / 32)] (see Pop::hid)
-    const size_t h = static_cast<size_t>(pad4(pol.dims[l + 1])) + (pol.dims[l + 1] + 31) / 32;
+    const size_t h = static_cast<size_t>(padl(pol.dims[l + 1])) + (pol.dims[l + 1] + 31) / 32;
     for (auto* v : {&S.tp_h, &S.ph, &S.pdh}) {
       v->emplace_back();
       v->back().alloc(nb * h);
@@ -341,8 +373,10 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
       s2 = S.bs2.p;
       d = S.bd.p;
     }
-    timed(PC_GATHER, 0.0, 0.0, 0, [&] { launch_pack_batch(n, B, ds, da, lsa, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
-                      S.d.p, stream); });
+    timed(PC_GATHER, 0.0, 0.0, 0, [&] {
+      launch_pack_batch(n, B, ds, da, lsa, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
+                        S.d.p, act16() ? 1 : 0, stream);
+    });
     step(B, d_mask);
   }
   CUDA_CHECK(cudaGetLastError());

@@ -1,6 +1,7 @@
 // Internal declarations of the B200 population-update library.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -44,6 +45,16 @@ struct Error : std::runtime_error {
   } while (0)
 
 bool pdl_enabled();  // PBRL_NO_PDL=1 disables the attribute (diagnostics)
+
+// Activation storage: fp32 (FFMA32 / TF32 modes) or bf16 (BF16 mode); arithmetic is fp32.
+__device__ __forceinline__ float act_ld(const float* p, long long i) { return p[i]; }
+__device__ __forceinline__ float act_ld(const __nv_bfloat16* p, long long i) {
+  return __bfloat162float(p[i]);
+}
+__device__ __forceinline__ void act_st(float* p, long long i, float v) { p[i] = v; }
+__device__ __forceinline__ void act_st(__nv_bfloat16* p, long long i, float v) {
+  p[i] = __float2bfloat16_rn(v);
+}
 
 template <typename... KArgs, typename... Args>
 void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -99,6 +110,7 @@ struct GemmArgs {
   int M = 0, N = 0, K = 0, groups = 0, n_members = 1;
   Operand A, B;
   int a_ones_row = 0;  // row M-1 of A is all ones: C row M-1 = column sums of B (bias grad)
+  int a16 = 0, c16 = 0;  // BF16 mode (k_fwd_skinny only): A / C are bf16 activations
   float* C = nullptr;
   long long c_gs = 0, c_rs = 0;
   int c_by_member = 0;
@@ -121,16 +133,17 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 // Output-layer backward in one pass (dX with relu mask, dW, db), N_out <= 16.
 struct OutBwdArgs {
   int B = 0, H = 0, nout = 0, groups = 0, n_members = 1;
-  const float* X = nullptr;  // [groups][B][x_ld]  input of the output layer (post-ReLU)
+  int act16 = 0;             // X and dX are bf16 activations (BF16 mode)
+  const void* X = nullptr;   // [groups][B][x_ld]  input of the output layer (post-ReLU)
   long long x_gs = 0, x_ld = 0;
   int x_by_member = 0;
   const float* G = nullptr;  // [groups][B][g_ld]  cotangent of the output
   long long g_gs = 0, g_ld = 0;
   const float* W = nullptr;  // [groups] weight rows, W [H][nout] at each group's base
   long long w_gs = 0;
-  float* dW = nullptr;       // gradient rows: dW [H][nout] then db [nout]
+  float* dW = nullptr;       // gradient rows: dW [H][nout] then db [nout] (nullptr: dX only)
   long long dw_gs = 0;
-  float* dX = nullptr;       // [groups][B][dx_ld] (nullptr: input layer, no dX)
+  void* dX = nullptr;        // [groups][B][dx_ld] (nullptr: input layer, no dX)
   long long dx_gs = 0, dx_ld = 0;
   float* dbx = nullptr;      // optional: column sums of dX = the bias gradient of the layer below
   long long dbx_gs = 0;
@@ -152,9 +165,11 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
                            cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s);
+// in_sa / in_s2a / sa_pi are activation buffers: fp32, or bf16 when act16
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
-                       const float* r, const float* s2, const float* d, float* in_sa,
-                       float* in_s2a, float* sa_pi, float* r_out, float* d_out, cudaStream_t st);
+                       const float* r, const float* s2, const float* d, void* in_sa,
+                       void* in_s2a, void* sa_pi, float* r_out, float* d_out, int act16,
+                       cudaStream_t st);
 void launch_td_target(int n, int B, const float* r, const float* d, const float* q2n,
                       const float* gamma, float* y, cudaStream_t s);
 void launch_mse(int groups, int n, int B, const float* q, const float* y, float* dq, double* loss,
@@ -167,11 +182,14 @@ void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, doubl
 void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m, float* v,
                  const float* g, const int64_t* t, const float* corr1, const float* corr2,
                  const float* lr, const int* active, float* tgt, const float* tau_a,
-                 const float* tau_b, const int* polyak_gate, cudaStream_t s);
+                 const float* tau_b, const int* polyak_gate, __nv_bfloat16* p16,
+                 __nv_bfloat16* t16, cudaStream_t s);
+// bf16 copy of an fp32 arena (the BF16 mode's tensor-core weight operands)
+void launch_to_bf16(const float* src, __nv_bfloat16* dst, size_t count, cudaStream_t s);
 void launch_fill(float* p, size_t count, float v, cudaStream_t s);
 // bias gradient of a layer: dst[g][o] = sum_b G[g][b][o] in row order (groups gated by active)
-void launch_colsum(int groups, int n, int B, int N, const float* G, long long g_gs, long long g_ld,
-                   float* dst, long long dst_gs, const int* active, cudaStream_t s);
+void launch_colsum(int groups, int n, int B, int N, const void* G, long long g_gs, long long g_ld,
+                   float* dst, long long dst_gs, const int* active, int act16, cudaStream_t s);
 
 // ReLU mask bits of a hidden activation (TF32 mode, CUDA-core fallback layers):
 // mask[g][r][w] bit j = (h[g][r][32w + j] > 0)
@@ -190,8 +208,8 @@ void launch_sac_step_begin(int n, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2, 
 // split_policy_head + tanh_gaussian_logprob + squash (algos.hpp:534-616): head [n][B][2da] ->
 // act into sa (cols ds..), x, th, ls (clamped), clamped flag, logp.
 void launch_sac_head(int n, int B, int ds, int da, int lsa, const float* head, const uint64_t* key,
-                     float bound, float* sa, float* x, float* th, float* ls, uint8_t* clamped,
-                     float* eps, float* logp, cudaStream_t s);
+                     float bound, void* sa, float* x, float* th, float* ls, uint8_t* clamped,
+                     float* eps, float* logp, int act16, cudaStream_t s);
 void launch_sac_y(int n, int B, const float* r, const float* d, const float* q2n,
                   const float* logp2, const float* log_alpha, const float* gamma,
                   const float* rscale, float* y, cudaStream_t s);
@@ -213,8 +231,8 @@ void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t 
 void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const float* ring,
                           uint64_t cap, int shared, const uint64_t* sizes,
                           const uint64_t* streams, uint64_t seed, uint64_t draw_id,
-                          float* in_sa, float* in_s2a, float* sa_pi, float* r_out, float* d_out,
-                          cudaStream_t s);
+                          void* in_sa, void* in_s2a, void* sa_pi, float* r_out, float* d_out,
+                          int act16, cudaStream_t s);
 
 // PBT
 void launch_pbt_plan(int n, const double* fitness, int cut, uint64_t key, uint64_t next,

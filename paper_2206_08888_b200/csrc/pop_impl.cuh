@@ -126,6 +126,12 @@ struct Pop {
 
   DBuf<float> pol_p, pol_t, pol_m, pol_v, pol_g;
   DBuf<float> cri_p, cri_t, cri_m, cri_v, cri_g;
+  // BF16 mode: bf16 copies of the online / target weights (the tensor-core B operands), kept in
+  // step by the fused Adam + Polyak kernel and refreshed after any other weight write
+  DBuf<__nv_bfloat16> pol_p16, pol_t16, cri_p16, cri_t16;
+  bool weights_dirty = true;
+  void refresh_shadows();
+  const void* wop(const float* W) const;  // tensor-core operand copy of master weights W
   DBuf<int64_t> t_pol, t_cri, t_alpha;
   DBuf<uint64_t> steps, streams, key_a, key_b;
   DBuf<int> fire;
@@ -188,7 +194,17 @@ struct Pop {
   void count_launch(uint64_t k) {
     if (!capturing) g_launches.fetch_add(k, std::memory_order_relaxed);
   }
-  bool use_tc() const { return precision == PBRL_PREC_TF32; }
+  bool use_tc() const { return precision == PBRL_PREC_TF32 || precision == PBRL_PREC_BF16; }
+  // BF16 mode: activations (critic / policy inputs, hidden activations and their cotangents)
+  // are stored as bf16; parameters, optimizer state, outputs and losses stay fp32
+  bool act16() const { return precision == PBRL_PREC_BF16; }
+  int aeb() const { return act16() ? 2 : 4; }
+  int padl(int x) const { return act16() ? (x + 7) / 8 * 8 : pad4(x); }
+  // element offset into an activation buffer
+  float* aoff(const float* p, long long elems) const {
+    return reinterpret_cast<float*>(const_cast<char*>(reinterpret_cast<const char*>(p)) +
+                                    elems * aeb());
+  }
   int lsa = 0;  // padded row stride of the critic-input blocks [s | a]
   bool use_graphs = true, capturing = false;
   std::vector<StepGraph> graphs;
@@ -199,7 +215,7 @@ struct Pop {
   void gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, float* Y,
                 long long y_gs, long long y_ld, int epi, const int* active = nullptr,
                 float* C2 = nullptr, long long c2_gs = 0, long long c2_ld = 0,
-                bool noise = false, const Mat* ymask = nullptr);
+                bool noise = false, const Mat* ymask = nullptr, bool y_act = true);
   void gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Mat G, Mat aux,
                float* DX, long long dx_gs, long long dx_ld, int epi, int col0, int ncols,
                const int* active, float scale);
@@ -209,10 +225,11 @@ struct Pop {
                    std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                    int last_epi, const int* active = nullptr, float* C2 = nullptr,
                    long long c2_gs = 0, long long c2_ld = 0, bool noise = false,
-                   bool keep_hidden = true);
+                   bool keep_hidden = true, bool out_act = false);
   bool gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, Mat H,
                       bool keep_hidden, float* Y, long long y_gs, long long y_ld, int out_epi,
-                      const int* active, float* C2, long long c2_gs, long long c2_ld, bool noise);
+                      const int* active, float* C2, long long c2_gs, long long c2_ld, bool noise,
+                      bool out_act);
   void mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
                     Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
                     const int* active);

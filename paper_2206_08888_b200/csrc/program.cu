@@ -25,21 +25,28 @@ Operand simt_op(const float* p, long long gs, long long rs, long long cs, int by
 // forward of layer l: Y = act(X W_l + b_l); X is [groups][B][in] (stride X.ld)
 void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, float* Y,
                    long long y_gs, long long y_ld, int epi, const int* active, float* C2,
-                   long long c2_gs, long long c2_ld, bool noise, const Mat* ymask) {
+                   long long c2_gs, long long c2_ld, bool noise, const Mat* ymask, bool y_act) {
   const int in = sh.dims[l], out = sh.dims[l + 1];
   const float* Wl = W + sh.woff[l];
   const double flops = 2.0 * B * in * out * groups;
-  // algorithmic bytes: X (once per member when shared by the critics), W, b, Y (+ mask bits)
-  const double bytes = 4.0 * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
-                              static_cast<double>(groups) * (in * out + out + B * out)) +
+  // algorithmic bytes: X (once per member when shared by the critics), W (the operand copy),
+  // b, Y (+ mask bits); activations / operand weights are aeb() bytes wide, Y as stored
+  const double ae = aeb(), ye = y_act ? ae : 4.0;
+  const double bytes = ae * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
+                             static_cast<double>(groups) * in * out) +
+                       4.0 * groups * out + ye * groups * B * out +
                        ((ymask && ymask->mask) ? groups * B * ((out + 31) / 32) * 4.0 : 0.0);
-  if (use_tc() && out >= 16 && tma_ok(X.p, X.ld, X.gs) && tma_ok(Wl, out, sh.stride)) {
+  const int eb = aeb();
+  const void* Wo = use_tc() ? wop(Wl) : Wl;
+  if (use_tc() && out >= 16 && tma_ok(X.p, X.ld, X.gs, eb) && tma_ok(Wo, out, sh.stride, eb)) {
     TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
                 static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
                 static_cast<uint64_t>(X.gs)};
-    TcOperand Bw{Wl, static_cast<uint64_t>(out), static_cast<uint64_t>(in),
+    TcOperand Bw{Wo, static_cast<uint64_t>(out), static_cast<uint64_t>(in),
                  static_cast<uint64_t>(groups), static_cast<uint64_t>(out), sh.stride};
     TcArgs a;
+    a.eb = eb;
+    a.c16 = act16() && y_act ? 1 : 0;
     a.M = B;
     a.N = out;
     a.K = in;
@@ -73,12 +80,16 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
           [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
     return;
   }
+  if (act16() && out > 16)
+    PBRL_THROW(PBRL_E_CONFIG, "bf16 mode: hidden layers need TMA-legal widths (multiples of 8, >= 16)");
   GemmArgs g;
   g.M = B;
   g.N = out;
   g.K = in;
   g.groups = groups;
   g.n_members = n;
+  g.a16 = act16() ? 1 : 0;
+  g.c16 = act16() && y_act ? 1 : 0;
   g.A = simt_op(X.p, X.gs, X.ld, 1, X.by_member);
   g.B = simt_op(Wl, static_cast<long long>(sh.stride), out, 1, 0);
   g.bias = simt_op(W + sh.boff[l], static_cast<long long>(sh.stride), 0, 1, 0);
@@ -118,18 +129,23 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
   const float* Wc = W + sh.woff[l] + static_cast<size_t>(col0) * out;
   const double flops = 2.0 * B * out * ncols * groups;
   // algorithmic bytes: G, the W columns, DX, the ReLU' mask bits (or the tanh values)
+  const double ae = aeb(), de = epi == EPI_RELU_MASK ? ae : 4.0;
   const double bytes =
-      4.0 * groups * (static_cast<double>(B) * out + static_cast<double>(out) * ncols +
-                      static_cast<double>(B) * ncols) +
+      ae * groups * (static_cast<double>(B) * out + static_cast<double>(out) * ncols) +
+      de * groups * static_cast<double>(B) * ncols +
       (epi == EPI_RELU_MASK ? groups * B * ((ncols + 31) / 32) * 4.0
                             : (epi == EPI_TANH_GRAD ? 4.0 * groups * B * ncols : 0.0));
-  if (use_tc() && out >= 8 && tma_ok(G.p, G.ld, G.gs) && tma_ok(Wc, out, sh.stride)) {
+  const int eb = aeb();
+  const void* Wco = use_tc() ? wop(Wc) : Wc;
+  if (use_tc() && out >= 8 && tma_ok(G.p, G.ld, G.gs, eb) && tma_ok(Wco, out, sh.stride, eb)) {
     TcOperand A{G.p, static_cast<uint64_t>(out), static_cast<uint64_t>(B),
                 static_cast<uint64_t>(groups), static_cast<uint64_t>(G.ld),
                 static_cast<uint64_t>(G.gs)};
-    TcOperand Bw{Wc, static_cast<uint64_t>(out), static_cast<uint64_t>(ncols),
+    TcOperand Bw{Wco, static_cast<uint64_t>(out), static_cast<uint64_t>(ncols),
                  static_cast<uint64_t>(groups), static_cast<uint64_t>(out), sh.stride};
     TcArgs a;
+    a.eb = eb;
+    a.c16 = act16() && epi == EPI_RELU_MASK ? 1 : 0;  // hidden cotangents are activations
     a.M = B;
     a.N = ncols;
     a.K = out;
@@ -156,6 +172,7 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
           [&] { launch_tc_gemm(A, Bw, false, false, a, stream); });
     return;
   }
+  if (act16()) PBRL_THROW(PBRL_E_CONFIG, "bf16 mode: dX product without a tensor-core shape");
   GemmArgs g;
   g.M = B;
   g.N = ncols;
@@ -184,9 +201,12 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
   const int in = sh.dims[l], out = sh.dims[l + 1];
   const double flops = 2.0 * B * in * out * groups;
   // algorithmic bytes: X (once per member when shared), G, dW
-  const double bytes = 4.0 * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
-                              static_cast<double>(groups) * (B * out + in * out));
-  if (use_tc() && out >= 32 && tma_ok(X.p, X.ld, X.gs) && tma_ok(G.p, G.ld, G.gs)) {
+  const double ae = aeb();
+  const double bytes = ae * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
+                             static_cast<double>(groups) * B * out) +
+                       4.0 * groups * in * out;
+  const int eb = aeb();
+  if (use_tc() && out >= 32 && tma_ok(X.p, X.ld, X.gs, eb) && tma_ok(G.p, G.ld, G.gs, eb)) {
     TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
                 static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
                 static_cast<uint64_t>(X.gs)};
@@ -194,6 +214,7 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
                  static_cast<uint64_t>(groups), static_cast<uint64_t>(G.ld),
                  static_cast<uint64_t>(G.gs)};
     TcArgs a;
+    a.eb = eb;
     a.M = in;
     a.N = out;
     a.K = B;
@@ -211,10 +232,11 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
     // unless the kernel that produced G already wrote them
     if (!bias_done) timed(PC_ELEM, 0.0, 4.0 * B * out * groups, active != nullptr, [&] {
       launch_colsum(groups, n, B, out, G.p, G.gs, G.ld, Gr + sh.boff[l],
-                    static_cast<long long>(sh.stride), active, stream);
+                    static_cast<long long>(sh.stride), active, act16() ? 1 : 0, stream);
     });
     return;
   }
+  if (act16()) PBRL_THROW(PBRL_E_CONFIG, "bf16 mode: dW product without a tensor-core shape");
   GemmArgs g;
   g.M = in + 1;  // ones row: C row `in` = column sums of G = the bias gradient (row order)
   g.N = out;
@@ -313,12 +335,12 @@ std::string Pop::prof_report() {
 // [rows][ceil(H / 32)] (ensure_scratch sizes them)
 Mat Pop::hid(std::vector<DBuf<float>>& v, int l, int B, const NetShape& sh, int by_member) {
   const int H = sh.dims[l + 1];
-  const int ld = pad4(H);
+  const int ld = padl(H);
   Mat m{v[l].p, static_cast<long long>(B) * ld, ld, by_member};
   if (use_tc()) {
     const long long mw = (H + 31) / 32;
     const long long rows = static_cast<long long>(v[l].count) / (ld + mw);
-    m.mask = reinterpret_cast<uint32_t*>(v[l].p + rows * ld);
+    m.mask = reinterpret_cast<uint32_t*>(aoff(v[l].p, rows * ld));
     m.mgs = static_cast<long long>(B) * mw;
     m.mld = mw;
   }
@@ -329,16 +351,16 @@ Mat Pop::hid(std::vector<DBuf<float>>& v, int l, int B, const NetShape& sh, int 
 void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
                       std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                       int last_epi, const int* active, float* C2, long long c2_gs,
-                      long long c2_ld, bool noise, bool keep_hidden) {
+                      long long c2_ld, bool noise, bool keep_hidden, bool out_act) {
   const int L = sh.depth;
   for (int l = 0; l < L; ++l) {
     if (l == L - 1) {
       gemm_fwd(sh, W, l, groups, B, x, out, out_gs, out_ld, last_epi, active, C2, c2_gs, c2_ld,
-               noise);
+               noise, nullptr, out_act);
     } else {
       const Mat h = hid(hs, l, B, sh, 0);
       if (l == L - 2 && gemm_fwd_fused(sh, W, l, groups, B, x, h, keep_hidden, out, out_gs, out_ld,
-                                       last_epi, active, C2, c2_gs, c2_ld, noise))
+                                       last_epi, active, C2, c2_gs, c2_ld, noise, out_act))
         return;  // the output layer ran in this layer's epilogue
       gemm_fwd(sh, W, l, groups, B, x, const_cast<float*>(h.p), h.gs, h.ld, EPI_BIAS_RELU, active,
                nullptr, 0, 0, false, keep_hidden ? &h : nullptr);
@@ -353,18 +375,23 @@ void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat
 bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, int B, Mat X,
                          Mat H, bool keep_hidden, float* Y, long long y_gs, long long y_ld,
                          int out_epi, const int* active, float* C2, long long c2_gs,
-                         long long c2_ld, bool noise) {
+                         long long c2_ld, bool noise, bool out_act) {
   const int in = sh.dims[l], hdim = sh.dims[l + 1], nout = sh.dims[l + 2];
+  const int eb = aeb();
   const float* Wl = W + sh.woff[l];
-  if (!use_tc() || hdim < 16 || hdim > 256 || nout > 16 || !tma_ok(X.p, X.ld, X.gs) ||
-      !tma_ok(Wl, hdim, sh.stride))
+  const void* Wo = use_tc() ? wop(Wl) : Wl;
+  if (!use_tc() || hdim < 16 || hdim > 256 || nout > 16 || !tma_ok(X.p, X.ld, X.gs, eb) ||
+      !tma_ok(Wo, hdim, sh.stride, eb))
     return false;
   TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
               static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
               static_cast<uint64_t>(X.gs)};
-  TcOperand Bw{Wl, static_cast<uint64_t>(hdim), static_cast<uint64_t>(in),
+  TcOperand Bw{Wo, static_cast<uint64_t>(hdim), static_cast<uint64_t>(in),
                static_cast<uint64_t>(groups), static_cast<uint64_t>(hdim), sh.stride};
   TcArgs a;
+  a.eb = eb;
+  a.c16 = act16() ? 1 : 0;
+  a.oc16 = act16() && out_act ? 1 : 0;
   a.M = B;
   a.N = hdim;
   a.K = in;
@@ -407,11 +434,12 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
     }
   }
   const double flops = 2.0 * B * groups * (static_cast<double>(in) * hdim + hdim * nout);
+  const double ae = eb, oe = out_act ? ae : 4.0;
   const double bytes =
-      4.0 * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
-             static_cast<double>(groups) *
-                 (in * hdim + hdim + hdim * nout + nout + B * nout +
-                  (keep_hidden ? B * hdim + B * ((hdim + 31) / 32) : 0)));
+      ae * (static_cast<double>(B) * in * (X.by_member ? n : groups) +
+            static_cast<double>(groups) * in * hdim) +
+      4.0 * groups * (hdim + hdim * nout + nout) + oe * groups * B * nout +
+      (keep_hidden ? groups * B * (ae * hdim + 4.0 * ((hdim + 31) / 32)) : 0.0);
   a.b_prefetch = last_wrote_weights ? 0 : 1;
   timed(PC_GEMM_FWD, flops, bytes, active != nullptr,
         [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
@@ -430,6 +458,7 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       // output layer: dX (masked), dW and db in one pass over the hidden activations
       const int H = sh.dims[l], nout = sh.dims[L];
       OutBwdArgs a;
+      a.act16 = act16() ? 1 : 0;
       a.B = B;
       a.H = H;
       a.nout = nout;
@@ -451,7 +480,7 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       Mat dh{};
       if (l > 0) {
         dh = hid(dhs, l - 1, B, sh, 0);
-        a.dX = const_cast<float*>(dh.p);
+        a.dX = const_cast<float*>(dh.p);  // activation buffer (fp32 or bf16)
         a.dx_gs = dh.gs;
         a.dx_ld = dh.ld;
         if (use_tc() && sh.dims[l] >= 32) {  // the tcgen05 dW of layer l-1 skips its colsum
@@ -461,9 +490,9 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       }
       // algorithmic bytes: X, G, W, dW + db, dX (+ the fused bias gradient below)
       const double obytes =
-          4.0 * (static_cast<double>(B) * H * (x.by_member ? n : groups) +
-                 static_cast<double>(groups) *
-                     (B * nout + 2.0 * (H * nout + nout) + (l > 0 ? B * H + H : 0)));
+          aeb() * (static_cast<double>(B) * H * (x.by_member ? n : groups) +
+                   (l > 0 ? static_cast<double>(groups) * B * H : 0.0)) +
+          4.0 * groups * (B * nout + 2.0 * (H * nout + nout) + (l > 0 ? H : 0));
       timed(PC_GEMM_DW, 2.0 * B * H * nout * groups * (l > 0 ? 2.0 : 1.0), obytes,
             active != nullptr, [&] { launch_out_backward(a, stream); });
       G = dh;
@@ -492,6 +521,37 @@ void Pop::critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>
   for (int l = L - 1; l >= 1; --l) {
     const Mat mask = hid(hs, l - 1, B, cri, 0);
     const Mat dh = hid(dhs, l - 1, B, cri, 0);
+    if (l == L - 1 && use_tc() && cri.dims[L] <= 16) {
+      // output layer (N_out = 1): dX = relu'(h) * (G W_out^T) by the output-layer backward
+      // kernel without its weight gradients (the policy loss discards them, algos.hpp:330-334)
+      const int H = cri.dims[l];
+      OutBwdArgs a;
+      a.act16 = act16() ? 1 : 0;
+      a.B = B;
+      a.H = H;
+      a.nout = cri.dims[L];
+      a.groups = groups;
+      a.n_members = n;
+      a.X = mask.p;
+      a.x_gs = mask.gs;
+      a.x_ld = mask.ld;
+      a.G = G.p;
+      a.g_gs = G.gs;
+      a.g_ld = G.ld;
+      a.W = cri_p.p + cri.woff[l];
+      a.w_gs = static_cast<long long>(cri.stride);
+      a.dX = const_cast<float*>(dh.p);
+      a.dx_gs = dh.gs;
+      a.dx_ld = dh.ld;
+      a.active = active;
+      a.exact = 0;
+      const double obytes = 4.0 * groups *
+          (static_cast<double>(B) * a.nout + H * a.nout) + 2.0 * aeb() * groups * B * H;
+      timed(PC_GEMM_DX, 2.0 * B * H * a.nout * groups, obytes, active != nullptr,
+            [&] { launch_out_backward(a, stream); });
+      G = dh;
+      continue;
+    }
     gemm_dx(cri, cri_p.p, l, groups, B, G, mask, const_cast<float*>(dh.p), dh.gs, dh.ld,
             EPI_RELU_MASK, 0, cri.dims[l], active, 1.0f);
     G = dh;
@@ -509,13 +569,16 @@ void Pop::critic_update(int B, const int* polyak_gate) {
   timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
   mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr);
   const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
-  timed(PC_ADAM, 0.0, static_cast<double>(cri.P) * n2 * 28.0, 0, [&] {
+  // 28 B/param Adam (+2 B/param bf16 operand copy in BF16 mode)
+  timed(PC_ADAM, 0.0, static_cast<double>(cri.P) * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
     launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
-                corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, stream);
+                corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, cri_p16.p, cri_t16.p,
+                stream);
   });
   // fused target Polyak: +8 B/param (read + write target), every member (SAC) or fired (TD3)
-  if (polyak_gate) prof_add_gated_bytes(8.0 * cri.P * n2);
-  else if (prof_on && !prof.empty()) prof.back().bytes += 8.0 * cri.P * n2;
+  const double pb = act16() ? 10.0 : 8.0;
+  if (polyak_gate) prof_add_gated_bytes(pb * cri.P * n2);
+  else if (prof_on && !prof.empty()) prof.back().bytes += pb * cri.P * n2;
 }
 
 // ------------------------------------------------------------------ TD3 step (algos.hpp:351-422)
@@ -543,8 +606,8 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
     });
   }
   const Mat s2{S.in_s2a.p, nbB * lsa, lsa, 0};
-  mlp_forward(pol, pol_t.p, n, B, s2, S.tp_h, S.in_s2a.p + ds, nbB * lsa, lsa,
-              EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true, false);
+  mlp_forward(pol, pol_t.p, n, B, s2, S.tp_h, aoff(S.in_s2a.p, ds), nbB * lsa, lsa,
+              EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true, false, true);
   mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
               nbB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
   timed(PC_ELEM, 0.0, 0.0, 0,
@@ -593,8 +656,8 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
 void Pop::td3_policy_half(int B) {
   const long long nbB = B;
   const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
-  mlp_forward(pol, pol_p.p, n, B, s, S.ph, S.sa_pi.p + ds, nbB * lsa, lsa, EPI_BIAS_TANH, fire.p,
-              S.pt.p, nbB * da, da);
+  mlp_forward(pol, pol_p.p, n, B, s, S.ph, aoff(S.sa_pi.p, ds), nbB * lsa, lsa, EPI_BIAS_TANH,
+              fire.p, S.pt.p, nbB * da, da, false, true, true);
   mlp_forward(cri, cri_p.p, n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 0}, S.qh, S.qpi.p, nbB, 1,
               EPI_BIAS, fire.p);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
@@ -605,9 +668,10 @@ void Pop::td3_policy_half(int B) {
                       Mat{S.pt.p, nbB * da, da, 0}, pol.out_scale, fire.p);
   mlp_backward(pol, pol_p.p, pol_g.p, n, B, Mat{S.gtop.p, nbB * lt, lt, 0}, s, S.ph, S.pdh,
                fire.p);
-  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * (28.0 + 8.0), 1, [&] {
+  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * (act16() ? 40.0 : 36.0), 1, [&] {
     launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
-                corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, stream);
+                corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, pol_p16.p, pol_t16.p,
+                stream);
   });
 }
 
@@ -625,7 +689,7 @@ void Pop::sac_step(int B) {
               hd, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_head(n, B, ds, da, lsa, S.head.p, key_b.p, bound, S.in_s2a.p, nullptr, nullptr,
-                    nullptr, nullptr, nullptr, S.logp2.p, stream);
+                    nullptr, nullptr, nullptr, S.logp2.p, act16() ? 1 : 0, stream);
   });
   mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
               nbB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
@@ -639,7 +703,7 @@ void Pop::sac_step(int B) {
   mlp_forward(pol, pol_p.p, n, B, s, S.ph, S.head.p, nbB * hd, hd, EPI_BIAS);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_head(n, B, ds, da, lsa, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p,
-                    S.ls.p, S.clamped.p, S.eps.p, S.logp.p, stream);
+                    S.ls.p, S.clamped.p, S.eps.p, S.logp.p, act16() ? 1 : 0, stream);
   });
   mlp_forward(cri, cri_p.p, 2 * n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 1}, S.qh, S.qpi.p, nbB, 1,
               EPI_BIAS);
@@ -657,7 +721,8 @@ void Pop::sac_step(int B) {
                nullptr);
   timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * 28.0, 0, [&] {
     launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
-                corr2.p, h_f0.p, nullptr, nullptr, nullptr, nullptr, nullptr, stream);
+                corr2.p, h_f0.p, nullptr, nullptr, nullptr, nullptr, nullptr, pol_p16.p, nullptr,
+                stream);
   });
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_alpha(n, B, S.logp.p, log_alpha.p, h_d0.p, log_alpha.p, alpha_m.p, alpha_v.p,
@@ -680,6 +745,7 @@ void Pop::invalidate_graphs() {
 
 void Pop::step(int B, const uint8_t* d_mask) {
   ensure_corr(t_bound + 4);
+  if (act16() && weights_dirty) refresh_shadows();
   if (prof_on || !use_graphs) {
     run_program(B, d_mask);
   } else {

@@ -25,7 +25,7 @@ namespace pbrl {
 namespace {
 
 constexpr int kBM = 128;        // UMMA M (cta_group::1)
-constexpr int kBK = 32;         // fp32 K per stage = one 128-byte swizzle row
+constexpr int kRowBytes = 128;  // K per stage = one 128-byte swizzle row (32 fp32 / 64 bf16)
 constexpr int kMaxStages = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -91,6 +91,17 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t 
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -130,6 +141,14 @@ __host__ __device__ constexpr uint32_t tmem_cols() {
 }
 
 }  // namespace
+
+// Out-of-line transcendentals for the epilogues: every inlined copy of these long code paths
+// is cold instruction memory the first time a launch reaches it (one L2 round trip per 128-byte
+// line); a single shared copy is fetched once per SM and then stays in the instruction cache.
+__device__ __noinline__ float epi_tanhf(float x) { return libm_tanhf(x); }
+__device__ __noinline__ float epi_normal(uint64_t key, uint64_t c) {
+  return static_cast<float>(rng_normal_pair(key, c));
+}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -180,6 +199,16 @@ __device__ __forceinline__ void tma_store_wait_all() {
 __device__ __forceinline__ uint32_t sw128(int r, int j) {
   return static_cast<uint32_t>(r * 128 + ((j ^ (r & 7)) << 4));
 }
+// 32 rows x 64 B box (32 bf16) with the 64-byte swizzle: chunk j (0..3) of row r at
+// r * 64 + ((j ^ ((r >> 1) & 3)) << 4)
+__device__ __forceinline__ uint32_t sw64(int r, int j) {
+  return static_cast<uint32_t>(r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
+  const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
+  return a | (b << 16);
+}
 
 // Optional phase timeline (TcArgs::trace, diagnostics only): per CTA kTraceSlots globaltimer
 // stamps -- [0] entry, [1] after setup, per tile it < kTraceTiles: [2+6it+0] producer issues the
@@ -212,13 +241,22 @@ constexpr uint32_t kEpiBytes = kEpiWarps * kEpiWarpBytes;
 // the current one is processed), adds the bias / applies ReLU / the ReLU' mask (bit masks),
 // writes 128B-swizzled 32 x 32 boxes with 128-bit stores and TMA-stores them.  The
 // double-buffered accumulator lets the epilogue of tile i run while tile i+1's MMAs run.
-template <int BN, bool A_MN, bool B_MN, int NO>
+//
+// EB = operand element bytes: 4 -> fp32 operands, kind::tf32 (8 K per MMA; MN-major operands as
+// 32 x 32 boxes in the 128B_BASE32B layout); 2 -> bf16 operands, kind::f16 (16 K per MMA;
+// MN-major operands as 64 x 64 boxes in the plain 128B swizzle).  A stage is one 128-byte K row
+// of every operand row either way (32 fp32 or 64 bf16 K values).
+template <int BN, bool A_MN, bool B_MN, int NO, int EB>
 __global__ void __launch_bounds__(64 + kEpiThreads, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmX,
               const TcArgs g) {
-  constexpr uint32_t A_BYTES = kBM * kBK * 4;  // 16 KB
-  constexpr uint32_t B_BYTES = BN * kBK * 4;
+  constexpr int kBK = kRowBytes / EB;          // K elements per stage
+  constexpr int MNBOX = EB == 4 ? 32 : 64;     // MN extent of one MN-major TMA box
+  constexpr uint32_t MNBOX_BYTES = MNBOX * kBK * EB;  // 4 KB (fp32) / 8 KB (bf16)
+  constexpr int KMMA = EB == 4 ? 8 : 16;       // K per tcgen05.mma
+  constexpr uint32_t A_BYTES = kBM * kRowBytes;  // 16 KB
+  constexpr uint32_t B_BYTES = BN * kRowBytes;
   constexpr uint32_t STAGE = A_BYTES + B_BYTES;
   constexpr uint32_t ACC_COLS = tmem_cols<BN>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -302,8 +340,8 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           mbar_expect_tx(&full[kb], STAGE);
           if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j)
-              tma_load_3d(&tmB, &full[kb], sb + j * 4096, n0 + 32 * j, kb * kBK, gb);
+            for (int j = 0; j < BN / MNBOX; ++j)
+              tma_load_3d(&tmB, &full[kb], sb + j * MNBOX_BYTES, n0 + MNBOX * j, kb * kBK, gb);
           } else {
             tma_load_3d(&tmB, &full[kb], sb, kb * kBK, n0, gb);
           }
@@ -330,16 +368,16 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           const int k0 = kb * kBK;
           if (A_MN) {
 #pragma unroll
-            for (int j = 0; j < kBM / 32; ++j)
-              tma_load_3d(&tmA, &full[s], sa + j * 4096, m0 + 32 * j, k0, ga);
+            for (int j = 0; j < kBM / MNBOX; ++j)
+              tma_load_3d(&tmA, &full[s], sa + j * MNBOX_BYTES, m0 + MNBOX * j, k0, ga);
           } else {
             tma_load_3d(&tmA, &full[s], sa, k0, m0, ga);
           }
           if (pre) {
           } else if (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j)
-              tma_load_3d(&tmB, &full[s], sb + j * 4096, n0 + 32 * j, k0, gb);
+            for (int j = 0; j < BN / MNBOX; ++j)
+              tma_load_3d(&tmB, &full[s], sb + j * MNBOX_BYTES, n0 + MNBOX * j, k0, gb);
           } else {
             tma_load_3d(&tmB, &full[s], sb, k0, n0, gb);
           }
@@ -349,7 +387,8 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (instruction descriptor: D f32, A/B tf32, majorness, N, M)
     if (lane == 0) {
-      constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+      constexpr uint32_t fmt = EB == 4 ? 2u : 1u;  // TF32 / BF16
+      constexpr uint32_t idesc = (1u << 4) | (fmt << 7) | (fmt << 10) | ((A_MN ? 1u : 0u) << 15) |
                                  ((B_MN ? 1u : 0u) << 16) |
                                  (static_cast<uint32_t>(BN >> 3) << 17) |
                                  (static_cast<uint32_t>(kBM >> 4) << 24);
@@ -370,14 +409,22 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           const uint32_t a_base = smem_u32(smem + s * STAGE);
           const uint32_t b_base = a_base + A_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 8; ++kk) {
+          for (int kk = 0; kk < kBK / KMMA; ++kk) {
             // K-major: +32 B inside the 128 B swizzle row (SBO = 8 rows = 1 KB);
-            // MN-major: +1 KB = the next 8 K-rows (SBO = 4 rows = 512 B, LBO = next MN box)
-            const uint64_t da = A_MN ? sdesc(a_base + kk * 1024, 4096, 512, 1)
-                                     : sdesc(a_base + kk * 32, 16, 1024, 2);
-            const uint64_t db = B_MN ? sdesc(b_base + kk * 1024, 4096, 512, 1)
-                                     : sdesc(b_base + kk * 32, 16, 1024, 2);
-            mma_tf32(dtmem, da, db, idesc, (kb | kk) ? 1u : 0u);
+            // MN-major fp32: +1 KB = the next 8 K-rows (128B_BASE32B: SBO = 4 rows = 512 B,
+            // LBO = next 32-wide MN box); MN-major bf16: +2 KB = the next 16 K-rows (128B
+            // swizzle: SBO = 8 rows = 1 KB, LBO = next 64-wide MN box)
+            const uint32_t mn_step = KMMA * kRowBytes;
+            const uint64_t da =
+                A_MN ? (EB == 4 ? sdesc(a_base + kk * mn_step, MNBOX_BYTES, 512, 1)
+                                : sdesc(a_base + kk * mn_step, MNBOX_BYTES, 1024, 2))
+                     : sdesc(a_base + kk * 32, 16, 1024, 2);
+            const uint64_t db =
+                B_MN ? (EB == 4 ? sdesc(b_base + kk * mn_step, MNBOX_BYTES, 512, 1)
+                                : sdesc(b_base + kk * mn_step, MNBOX_BYTES, 1024, 2))
+                     : sdesc(b_base + kk * 32, 16, 1024, 2);
+            if (EB == 4) mma_tf32(dtmem, da, db, idesc, (kb | kk) ? 1u : 0u);
+            else mma_bf16(dtmem, da, db, idesc, (kb | kk) ? 1u : 0u);
           }
           mma_commit(&empty[s]);
         }
@@ -425,7 +472,12 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
       const int row = row0 + lane;
       const int cg = g.c_by_member ? mem : grp;
       const int xg = g.aux_by_member ? mem : grp;
-      float* C = g.C + cg * g.c_gs;
+      // C element (r, c) of this group: fp32, or bf16 when c16
+      char* Cb = static_cast<char*>(g.C) + cg * g.c_gs * (g.c16 ? 2 : 4);
+      auto cstore = [&](long long idx, float x) {
+        if (g.c16) reinterpret_cast<__nv_bfloat16*>(Cb)[idx] = __float2bfloat16_rn(x);
+        else reinterpret_cast<float*>(Cb)[idx] = x;
+      };
       const float* bias = g.bias ? g.bias + grp * g.bias_gs : nullptr;
       const float* aux = g.aux ? g.aux + xg * g.aux_gs : nullptr;
       if (need_bias) {
@@ -505,10 +557,21 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           else tma_store_wait_read<0>();
         }
         __syncwarp();
+        if (g.c16) {  // 32 rows x 64 B bf16 box, 64-byte swizzle
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 w4 = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          *reinterpret_cast<float4*>(box + sw128(lane, j)) = w4;
+          for (int j = 0; j < 4; ++j) {
+            uint4 w4 = make_uint4(pack_bf16x2(v[8 * j], v[8 * j + 1]),
+                                  pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                                  pack_bf16x2(v[8 * j + 4], v[8 * j + 5]),
+                                  pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+            *reinterpret_cast<uint4*>(box + sw64(lane, j)) = w4;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 w4 = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            *reinterpret_cast<float4*>(box + sw128(lane, j)) = w4;
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
@@ -572,8 +635,9 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           for (int o = 0; o < NA; ++o) os[o] = oacc[o];
         }
         quad_bar_sync(q);
+        if (threadIdx.x == 64) TC_TRACE_TILE(it, 5);
         if (hf == 0 && row < g.M) {
-          float* oC = g.oC + grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
+          const long long obase = grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
           const bool tanh_out = g.out_epi == EPI_BIAS_TANH || g.out_epi == EPI_BIAS_TANH_NOISE;
 #pragma unroll
           for (int o = 0; o < NA; ++o) {
@@ -581,7 +645,7 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
             const float y = (oacc[o] + os[o]) + ob[o];
             float r = y;
             if (tanh_out) {
-              const float th = libm_tanhf(y);
+              const float th = epi_tanhf(y);
               if (g.oC2) g.oC2[grp * g.oc2_gs + static_cast<long long>(row) * g.oc2_rs + o] = th;
               r = (g.out_scale != 1.0f) ? th * g.out_scale : th;
               if (g.out_epi == EPI_BIAS_TANH_NOISE) {
@@ -590,14 +654,14 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
                   eps = ep[o];
                 } else {
                   const uint64_t e = static_cast<uint64_t>(row) * nout + o;
-                  eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
-                        g.noise_sd[mem];
+                  eps = epi_normal(g.noise_key[mem], 2 * e) * g.noise_sd[mem];
                   eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
                 }
                 r = clampf_ref(r + eps, -g.bound, g.bound);
               }
             }
-            oC[o] = r;
+            if (g.oc16) static_cast<__nv_bfloat16*>(g.oC)[obase + o] = __float2bfloat16_rn(r);
+            else static_cast<float*>(g.oC)[obase + o] = r;
           }
         }
         ++it;
@@ -708,13 +772,12 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
                   }
                   case EPI_BIAS_TANH:
                   case EPI_BIAS_TANH_NOISE: {
-                    const float th = libm_tanhf(x + bv);
+                    const float th = epi_tanhf(x + bv);
                     if (g.C2) g.C2[grp * g.c2_gs + static_cast<long long>(rw) * g.c2_rs + col] = th;
                     x = (g.scale != 1.0f) ? th * g.scale : th;
                     if (epi == EPI_BIAS_TANH_NOISE) {
                       const uint64_t e = static_cast<uint64_t>(rw) * g.N + col;
-                      float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
-                                  g.noise_sd[mem];
+                      float eps = epi_normal(g.noise_key[mem], 2 * e) * g.noise_sd[mem];
                       eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
                       x = clampf_ref(x + eps, -g.bound, g.bound);
                     }
@@ -731,7 +794,7 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
                   }
                   default: break;
                 }
-                C[static_cast<long long>(rw) * g.c_rs + col] = x;
+                cstore(static_cast<long long>(rw) * g.c_rs + col, x);
               }
             }
           }
@@ -778,7 +841,7 @@ template <int BN, int NO>
 constexpr size_t smem_bytes(int stages) {
   // stage ring, epilogue boxes, barriers, bias / output-layer staging, fused-output partial
   // sums, 1 KB alignment slack
-  return static_cast<size_t>(stages) * (kBM * kBK * 4 + BN * kBK * 4) + kEpiBytes + 256 + 1024 +
+  return static_cast<size_t>(stages) * (kBM + BN) * kRowBytes + kEpiBytes + 256 + 1024 +
          static_cast<size_t>(BN) * (1 + NO) * 4 + static_cast<size_t>(2 * kBM) * NO * 4;
 }
 constexpr size_t kMaxSmem = 232448;  // 227 KB opt-in per block (sm_100)
@@ -801,75 +864,82 @@ int num_sms() {
   return sms;
 }
 
-template <int BN, bool A_MN, bool B_MN, int NO>
+template <int BN, bool A_MN, bool B_MN, int NO, int EB>
 void launch_tpl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                 const CUtensorMap& x, TcArgs g, cudaStream_t s) {
   constexpr int smax = max_stages<BN, NO>();
   static_assert(smem_bytes<BN, NO>(smax) <= kMaxSmem, "tc_gemm: shared memory budget");
   static bool attr_set = false;
   if (!attr_set) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_tc_gemm<BN, A_MN, B_MN, NO>,
+    CUDA_CHECK(cudaFuncSetAttribute(k_tc_gemm<BN, A_MN, B_MN, NO, EB>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem_bytes<BN, NO>(smax))));
     attr_set = true;
   }
   // persistent: one CTA per SM (TMEM holds two BN-column accumulators)
-  const int nk = (g.K + kBK - 1) / kBK;
+  const int kbk = kRowBytes / EB;
+  const int nk = (g.K + kbk - 1) / kbk;
   g.stages = std::max(1, std::min(nk, smax));
   const int tiles = g.groups * ((g.M + kBM - 1) / kBM) * ((g.N + BN - 1) / BN);
   if (g.nout > 0 && (g.N > BN || g.nout > 16)) PBRL_THROW(PBRL_E_USAGE, "tc_gemm: bad fused output");
-  launch_k(k_tc_gemm<BN, A_MN, B_MN, NO>, std::min(tiles, num_sms()), 64 + kEpiThreads,
+  launch_k(k_tc_gemm<BN, A_MN, B_MN, NO, EB>, std::min(tiles, num_sms()), 64 + kEpiThreads,
            smem_bytes<BN, NO>(g.stages), s, a, b, c, x, g);
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int EB>
 void launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                const CUtensorMap& x, const TcArgs& g, cudaStream_t s) {
   if (g.nout > 0) {  // fused output layer: forward GEMMs only (K-major A, MN-major B)
     if constexpr (!A_MN && B_MN) {
       if (bn == 256) {
         switch (g.nout) {
-          case 1: launch_tpl<256, false, true, 1>(a, b, c, x, g, s); return;
-          case 6: launch_tpl<256, false, true, 6>(a, b, c, x, g, s); return;
-          case 12: launch_tpl<256, false, true, 12>(a, b, c, x, g, s); return;
-          default: launch_tpl<256, false, true, 16>(a, b, c, x, g, s); return;
+          case 1: launch_tpl<256, false, true, 1, EB>(a, b, c, x, g, s); return;
+          case 6: launch_tpl<256, false, true, 6, EB>(a, b, c, x, g, s); return;
+          case 12: launch_tpl<256, false, true, 12, EB>(a, b, c, x, g, s); return;
+          default: launch_tpl<256, false, true, 16, EB>(a, b, c, x, g, s); return;
         }
       }
     }
     PBRL_THROW(PBRL_E_USAGE, "tc_gemm: fused output layer needs the 256-wide forward tile");
   }
   switch (bn) {
-    case 16: if constexpr (!B_MN) { launch_tpl<16, A_MN, B_MN, 0>(a, b, c, x, g, s); return; } break;
-    case 64: launch_tpl<64, A_MN, B_MN, 0>(a, b, c, x, g, s); return;
-    case 128: launch_tpl<128, A_MN, B_MN, 0>(a, b, c, x, g, s); return;
-    case 256: launch_tpl<256, A_MN, B_MN, 0>(a, b, c, x, g, s); return;
+    case 16: if constexpr (!B_MN) { launch_tpl<16, A_MN, B_MN, 0, EB>(a, b, c, x, g, s); return; } break;
+    case 64: launch_tpl<64, A_MN, B_MN, 0, EB>(a, b, c, x, g, s); return;
+    case 128: launch_tpl<128, A_MN, B_MN, 0, EB>(a, b, c, x, g, s); return;
+    case 256: launch_tpl<256, A_MN, B_MN, 0, EB>(a, b, c, x, g, s); return;
     default: break;
   }
   PBRL_THROW(PBRL_E_USAGE, "tc_gemm: unsupported tile width");
 }
 }  // namespace
 
-CUtensorMap make_tmap(const float* base, uint64_t cols, uint64_t rows, uint64_t groups,
+// 3-D tensor map over [groups][rows][cols] elements of eb bytes (fp32 or bf16); swizzle: 128B
+// for K-major operand tiles (and 32 x 32 fp32 epilogue boxes), 128B_ATOM_32B for MN-major fp32
+// operand boxes, 64B for 32 x 32 bf16 epilogue boxes
+enum TmapSwz { SWZ_128 = 0, SWZ_128_ATOM32 = 1, SWZ_64 = 2 };
+CUtensorMap make_tmap(const void* base, int eb, uint64_t cols, uint64_t rows, uint64_t groups,
                       uint64_t row_stride_elems, uint64_t group_stride_elems, uint32_t box_cols,
-                      uint32_t box_rows, bool mn_major) {
+                      uint32_t box_rows, int swz) {
   load_encode();
   CUtensorMap m;
   cuuint64_t dims[3] = {cols, rows, groups};
-  cuuint64_t strides[2] = {row_stride_elems * 4, group_stride_elems * 4};
+  cuuint64_t strides[2] = {row_stride_elems * eb, group_stride_elems * eb};
   cuuint32_t box[3] = {box_cols, box_rows, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims,
-                        strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const CUtensorMapSwizzle sw = swz == SWZ_128_ATOM32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                : swz == SWZ_64      ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                     : CU_TENSOR_MAP_SWIZZLE_128B;
+  CUresult r = g_encode(&m, eb == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                        3, const_cast<void*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) PBRL_THROW(PBRL_E_CUDA, "cuTensorMapEncodeTiled failed");
   return m;
 }
 
-bool tma_ok(const float* base, uint64_t row_stride_elems, uint64_t group_stride_elems) {
-  return (reinterpret_cast<uintptr_t>(base) % 16 == 0) && (row_stride_elems % 4 == 0) &&
-         (group_stride_elems % 4 == 0);
+bool tma_ok(const void* base, uint64_t row_stride_elems, uint64_t group_stride_elems, int eb) {
+  return (reinterpret_cast<uintptr_t>(base) % 16 == 0) && ((row_stride_elems * eb) % 16 == 0) &&
+         ((group_stride_elems * eb) % 16 == 0);
 }
 
 int pick_bn(int N, bool b_mn) {
@@ -917,26 +987,43 @@ void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn
                                           g.groups, g.epi, 0};
     ++g_trace_n;
   }
-  // A: K-major tile = 32 (K) x 128 (M) box; MN-major = 32 (M) x 32 (K) boxes
-  const CUtensorMap ta = a_mn ? make_tmap(A.p, A.cols, A.rows, A.groups, A.ld, A.gs, 32, 32, true)
-                              : make_tmap(A.p, A.cols, A.rows, A.groups, A.ld, A.gs, 32, kBM, false);
-  const CUtensorMap tb = b_mn ? make_tmap(B.p, B.cols, B.rows, B.groups, B.ld, B.gs, 32, 32, true)
-                              : make_tmap(B.p, B.cols, B.rows, B.groups, B.ld, B.gs, 32, bn, false);
-  // epilogue boxes: C stores and ReLU'-mask loads as 32 x 32 fp32 boxes, 128B swizzle
+  // operand boxes: K-major = one 128-byte K row x (128 | BN) rows; MN-major = 32 x 32 fp32
+  // (128B_ATOM_32B) or 64 x 64 bf16 (128B) boxes
+  const int eb = g.eb;
+  const uint32_t kbk = 128 / eb, mnb = eb == 4 ? 32 : 64;
+  const int mn_swz = eb == 4 ? SWZ_128_ATOM32 : SWZ_128;
+  const CUtensorMap ta =
+      a_mn ? make_tmap(A.p, eb, A.cols, A.rows, A.groups, A.ld, A.gs, mnb, kbk, mn_swz)
+           : make_tmap(A.p, eb, A.cols, A.rows, A.groups, A.ld, A.gs, kbk, kBM, SWZ_128);
+  const CUtensorMap tb =
+      b_mn ? make_tmap(B.p, eb, B.cols, B.rows, B.groups, B.ld, B.gs, mnb, kbk, mn_swz)
+           : make_tmap(B.p, eb, B.cols, B.rows, B.groups, B.ld, B.gs, kbk, bn, SWZ_128);
+  // epilogue boxes: C stores as 32 x 32 boxes (fp32: 128B swizzle, bf16: 64B swizzle) and
+  // fp32 ReLU'-mask loads
   CUtensorMap tc{}, tx{};
-  g.c_tma = bn >= 32 && !g.c_by_member && g.C && tma_ok(g.C, g.c_rs, g.c_gs) ? 1 : 0;
+  const int ceb = g.c16 ? 2 : 4;
+  g.c_tma = bn >= 32 && !g.c_by_member && g.C && tma_ok(g.C, g.c_rs, g.c_gs, ceb) ? 1 : 0;
   if (g.c_tma)
-    tc = make_tmap(g.C, g.N, g.M, g.groups, g.c_rs, g.c_gs, 32, 32, false);
+    tc = make_tmap(g.C, ceb, g.N, g.M, g.groups, g.c_rs, g.c_gs, 32, 32, g.c16 ? SWZ_64 : SWZ_128);
   g.aux_tma = bn >= 32 && g.aux && tma_ok(g.aux, g.aux_rs, g.aux_gs) ? 1 : 0;
   if (g.aux_tma)
-    tx = make_tmap(g.aux, g.N, g.M, g.aux_by_member ? g.n_members : g.groups, g.aux_rs, g.aux_gs,
-                   32, 32, false);
+    tx = make_tmap(g.aux, 4, g.N, g.M, g.aux_by_member ? g.n_members : g.groups, g.aux_rs,
+                   g.aux_gs, 32, 32, SWZ_128);
   if (g.nout > 0 && g.store_hidden && !g.c_tma)
     PBRL_THROW(PBRL_E_USAGE, "tc_gemm: fused output layer needs a TMA-legal hidden buffer");
-  if (a_mn && b_mn) launch_bn<true, true>(bn, ta, tb, tc, tx, g, s);
-  else if (a_mn) launch_bn<true, false>(bn, ta, tb, tc, tx, g, s);
-  else if (b_mn) launch_bn<false, true>(bn, ta, tb, tc, tx, g, s);
-  else launch_bn<false, false>(bn, ta, tb, tc, tx, g, s);
+  if (eb == 2 && g.epi == EPI_RELU_MASK && !g.mask_in)
+    PBRL_THROW(PBRL_E_USAGE, "tc_gemm: bf16 ReLU' epilogues need the mask bits");
+  if (eb == 4) {
+    if (a_mn && b_mn) launch_bn<true, true, 4>(bn, ta, tb, tc, tx, g, s);
+    else if (a_mn) launch_bn<true, false, 4>(bn, ta, tb, tc, tx, g, s);
+    else if (b_mn) launch_bn<false, true, 4>(bn, ta, tb, tc, tx, g, s);
+    else launch_bn<false, false, 4>(bn, ta, tb, tc, tx, g, s);
+  } else {
+    if (a_mn && b_mn) launch_bn<true, true, 2>(bn, ta, tb, tc, tx, g, s);
+    else if (a_mn) launch_bn<true, false, 2>(bn, ta, tb, tc, tx, g, s);
+    else if (b_mn) launch_bn<false, true, 2>(bn, ta, tb, tc, tx, g, s);
+    else launch_bn<false, false, 2>(bn, ta, tb, tc, tx, g, s);
+  }
 }
 
 }  // namespace pbrl

@@ -7,19 +7,23 @@
 
 namespace pbrl {
 
-// A 3-D fp32 operand in global memory: [groups][rows][cols] with element (r, c) of group g at
-// p + g*gs + r*ld + c.  rows / cols are the LOGICAL extents (TMA zero-fills past them).
+// A 3-D operand in global memory: [groups][rows][cols] with element (r, c) of group g at
+// p + g*gs + r*ld + c (elements of TcArgs::eb bytes: fp32 in TF32 mode, bf16 in BF16 mode).
+// rows / cols are the LOGICAL extents (TMA zero-fills past them).
 struct TcOperand {
-  const float* p = nullptr;
+  const void* p = nullptr;
   uint64_t cols = 0, rows = 0, groups = 0, ld = 0, gs = 0;
 };
 
 struct TcArgs {
   int M = 0, N = 0, K = 0, groups = 0, n_members = 1;
+  int eb = 4;   // operand element bytes: 4 = fp32 (kind::tf32), 2 = bf16 (kind::f16)
+  int c16 = 0;  // C (incl. the fused hidden store) is bf16 (activations in BF16 mode)
+  int oc16 = 0; // the fused output layer's oC is bf16 (actions written into critic inputs)
   int stages = 4;  // smem pipeline depth (set by the launcher)
   int a_by_member = 0, b_by_member = 0;
   int epi = 0;
-  float* C = nullptr;
+  void* C = nullptr;
   long long c_gs = 0, c_rs = 0;
   int c_by_member = 0;
   const float* bias = nullptr;
@@ -42,7 +46,7 @@ struct TcArgs {
   const float* ow = nullptr;  // W_out [N][nout] of group g at ow + g * ow_gs; b_out follows it
   long long ow_gs = 0;
   int out_epi = 0;
-  float* oC = nullptr;
+  void* oC = nullptr;
   long long oc_gs = 0, oc_rs = 0;
   float* oC2 = nullptr;
   long long oc2_gs = 0, oc2_rs = 0;
@@ -71,8 +75,8 @@ struct TcTraceMeta {
 void tc_trace_init();  // allocates the trace buffer when PBRL_TC_TRACE is set
 int tc_trace_dump(unsigned long long* host, TcTraceMeta* meta, int max_launches);
 
-// TMA requirements: 16-byte aligned base and strides.
-bool tma_ok(const float* base, uint64_t row_stride_elems, uint64_t group_stride_elems);
+// TMA requirements: 16-byte aligned base and strides (elements of eb bytes).
+bool tma_ok(const void* base, uint64_t row_stride_elems, uint64_t group_stride_elems, int eb = 4);
 
 // a_mn / b_mn: operand is MN-major (the M / N index is the contiguous one in memory).
 //   A K-major : A(m, k) = A.p[g][m][k]  (rows = M extent, cols = K extent)

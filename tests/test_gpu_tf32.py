@@ -24,9 +24,9 @@ def pb(cuda):
     return pb
 
 
-def _compare(pb, ora, algo, n, hidden, B, K, seed=7, ds=17, da=6):
+def _compare(pb, ora, algo, n, hidden, B, K, seed=7, ds=17, da=6, precision="tf32"):
     make = pb.make_td3_state if algo == "td3" else pb.make_sac_state
-    st = make(n, ds, da, hidden, 1.0, seed, precision="tf32")
+    st = make(n, ds, da, hidden, 1.0, seed, precision=precision)
     ref = (ora.td3 if algo == "td3" else ora.sac)(n, ds, da, hidden, 1.0, seed)
     hy = pb.Td3Hyper.defaults(n) if algo == "td3" else pb.SacHyper.defaults(n, da)
     if algo == "td3":

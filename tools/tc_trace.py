@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--pop", type=int, default=80)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16"])
     args = ap.parse_args()
     os.environ.setdefault("PBRL_TC_TRACE", "1")
     import torch
@@ -34,7 +35,7 @@ def main():
     from paper_2206_08888_b200 import _lib
 
     n, B = args.pop, 256
-    st = pb.make_td3_state(n, 17, 6, [256, 256], 1.0, 7, precision="tf32")
+    st = pb.make_td3_state(n, 17, 6, [256, 256], 1.0, 7, precision=args.precision)
     hy = pb.Td3Hyper.defaults(n)
     st._sync_hyper(hy)
     gb = pb.make_synthetic_batches(4, n, B, 17, 6, 7, device=torch.device("cuda", 0))
@@ -51,10 +52,11 @@ def main():
     _lib.call("pbrl_debug_tc_trace", stamps.ctypes.data_as(C.POINTER(C.c_uint64)),
               meta.ctypes.data_as(C.POINTER(C.c_int)), maxl, C.byref(cnt))
     nl = cnt.value
-    lines = [f"# tcgen05 GEMM phase timeline (TD3 pop {n}, 2x256, B={B}, last replayed step)", "",
+    lines = [f"# tcgen05 GEMM phase timeline (TD3 pop {n}, 2x256, B={B}, {args.precision}, "
+             "last replayed step)", "",
              "| # | tile | op | M,N,K x groups | span us | setup us | tiles/CTA | first TMA->data us"
-             " | MMA us | commit->epi us | epilogue us | drain us |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             " | MMA us | commit->epi us | epilogue us | out-layer wait us | drain us |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     # launches recorded during the first (eager / capture) pass; the captured ones hold the
     # stamps of the last replay
     for li in range(nl):
@@ -66,7 +68,7 @@ def main():
         t0 = s[:, 0].min()
         span = (s[:, 63].max() - t0) / 1e3
         setup = np.median(s[:, 1] - s[:, 0]) / 1e3
-        ph = {k: [] for k in range(5)}
+        ph = {k: [] for k in range(6)}
         tiles = []
         for c in s:
             nt = 0
@@ -79,6 +81,8 @@ def main():
                 ph[1].append(c[b + 2] - c[b + 1])
                 ph[2].append(c[b + 3] - c[b + 2])
                 ph[3].append(c[b + 4] - c[b + 3])
+                if c[b + 5]:
+                    ph[5].append(c[b + 5] - c[b + 4])
             tiles.append(nt)
             if c[62]:
                 last = 2 + 6 * (nt - 1) + 4 if nt else 1
@@ -90,7 +94,7 @@ def main():
             f"| {li} | {m[0]},{'MN' if m[1] else 'K'},{'MN' if m[2] else 'K'} | {op} | "
             f"{m[4]},{m[5]},{m[6]} x {m[7]} | {span:.1f} | {setup:.2f} | "
             f"{min(tiles)}-{max(tiles)} | {med[0]:.2f} | {med[1]:.2f} | {med[2]:.2f} | "
-            f"{med[3]:.2f} | {med[4]:.2f} |")
+            f"{med[3]:.2f} | {med[5]:.2f} | {med[4]:.2f} |")
     # step timeline: launch windows and the gaps between consecutive GEMM launches
     win = []
     for li in range(nl):
