@@ -395,6 +395,7 @@ int pbrl_sample_batch(pbrl_pop* pop, uint64_t seed, uint64_t draw_id, uint64_t r
     const int B = static_cast<int>(rows);
     p->ensure_scratch(B);
     gather(p, B, seed, draw_id, 0);
+    p->ones_dirty = true;  // the fp32 rows overwrote the critic-input block
     const size_t nb = static_cast<size_t>(p->n) * B;
     const int dsa = p->lsa;
     std::vector<float> sa(nb * dsa), s2a(nb * dsa);
@@ -422,6 +423,7 @@ int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t seed, uint64_t first_draw_
     p->validate_hyper();
     const int B = static_cast<int>(rows);
     p->ensure_scratch(B);
+    p->ensure_ones();
     p->ensure_corr(p->t_bound + k + 4);
     for (uint32_t i = 0; i < k; ++i) {
       gather(p, B, seed, first_draw_id + i, p->act16() ? 1 : 0);

@@ -589,25 +589,34 @@ void launch_td_target(int n, int B, const float* r, const float* d, const float*
   launch_k(k_td_target, (n * B + 255) / 256, 256, 0, s, n, B, r, d, q2n, gamma, y);
 }
 
-// mse_loss_grads (algos.hpp:288-314): dq = (2/B)(q - y); loss = sum (double) d^2 / B in row order
+// mse_loss_grads (algos.hpp:288-314): dq = (2/B)(q - y); loss = sum (double) d^2 / B in row order.
+// The squares are staged through shared memory by the whole block (coalesced loads, exact
+// double products) and summed by one thread in row order (the reference's double rounding).
+constexpr int kLossChunk = 1024;
+
 __global__ void k_mse(int n, int B, const float* q, const float* y, float* dq, double* loss) {
   PDL_ENTRY();
+  __shared__ double sq[kLossChunk];
   const int grp = blockIdx.x;
   const int m = grp % n;
   const float scale = 2.0f / static_cast<float>(B);
   const float* qg = q + static_cast<long long>(grp) * B;
   const float* yg = y + static_cast<long long>(m) * B;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    dq[static_cast<long long>(grp) * B + b] = scale * (qg[b] - yg[b]);
-  }
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    for (int b = 0; b < B; ++b) {
+  double acc = 0.0;
+  for (int b0 = 0; b0 < B; b0 += kLossChunk) {
+    const int nb = min(kLossChunk, B - b0);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) {
+      const int b = b0 + i;
       const float dl = qg[b] - yg[b];
-      acc += static_cast<double>(dl) * static_cast<double>(dl);
+      dq[static_cast<long long>(grp) * B + b] = scale * dl;
+      sq[i] = static_cast<double>(dl) * static_cast<double>(dl);
     }
-    loss[grp] = acc / static_cast<double>(B);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < nb; ++i) acc += sq[i];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) loss[grp] = acc / static_cast<double>(B);
 }
 
 void launch_mse(int groups, int n, int B, const float* q, const float* y, float* dq, double* loss,
@@ -619,17 +628,25 @@ void launch_mse(int groups, int n, int B, const float* q, const float* y, float*
 __global__ void k_td3_policy_loss(int n, int B, const float* q, const int* fire, double* loss,
                                   float* gq) {
   PDL_ENTRY();
+  __shared__ double sq[kLossChunk];
   const int m = blockIdx.x;
   const float gv = -1.0f / static_cast<float>(B);
   for (int b = threadIdx.x; b < B; b += blockDim.x) gq[static_cast<long long>(m) * B + b] = gv;
-  if (threadIdx.x == 0) {
-    double acc = 0.0;
-    if (fire[m]) {
-      for (int b = 0; b < B; ++b) acc -= static_cast<double>(q[static_cast<long long>(m) * B + b]);
-      acc /= static_cast<double>(B);
-    }
-    loss[m] = acc;
+  if (!fire[m]) {
+    if (threadIdx.x == 0) loss[m] = 0.0;
+    return;
   }
+  double acc = 0.0;
+  for (int b0 = 0; b0 < B; b0 += kLossChunk) {
+    const int nb = min(kLossChunk, B - b0);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+      sq[i] = static_cast<double>(q[static_cast<long long>(m) * B + b0 + i]);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int i = 0; i < nb; ++i) acc -= sq[i];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) loss[m] = acc / static_cast<double>(B);
 }
 
 void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, double* loss,
@@ -873,6 +890,23 @@ __global__ void k_fill(float* p, size_t count, float v) {
 void launch_fill(float* p, size_t count, float v, cudaStream_t s) {
   const int blocks = static_cast<int>(std::min<size_t>((count + 255) / 256, 148 * 8));
   launch_k(k_fill, blocks > 0 ? blocks : 1, 256, 0, s, p, count, v);
+}
+
+template <typename AT>
+__global__ void k_fill_col(AT* p, long long rows, int ld, int col, float v) {
+  PDL_ENTRY();
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<long long>(gridDim.x) * blockDim.x)
+    act_st(p, r * ld + col, v);
+}
+
+void launch_fill_col(void* p, long long rows, int ld, int col, float v, int act16, cudaStream_t s) {
+  const int blocks = static_cast<int>(std::min<long long>((rows + 255) / 256, 148 * 4));
+  if (act16)
+    launch_k(k_fill_col<__nv_bfloat16>, blocks, 256, 0, s, static_cast<__nv_bfloat16*>(p), rows,
+             ld, col, v);
+  else
+    launch_k(k_fill_col<float>, blocks, 256, 0, s, static_cast<float*>(p), rows, ld, col, v);
 }
 
 // ================================================================== SAC

@@ -67,6 +67,7 @@ Pop::Pop(const pbrl_pop_desc& d) {
   CUDA_CHECK(cudaSetDevice(device));
   CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   tc_trace_init();
+  use_graphs = std::getenv("PBRL_NO_GRAPH") == nullptr;  // eager replay (ncu kernel profiles)
 
   std::vector<size_t> pd{static_cast<size_t>(ds)};
   pd.insert(pd.end(), hidden.begin(), hidden.end());
@@ -335,7 +336,20 @@ void Pop::ensure_scratch(int B) {
   for (auto* b : {&S.in_sa, &S.in_s2a, &S.sa_pi, &S.gtop}) b->zero(stream);
   for (auto* v : {&S.tp_h, &S.ph, &S.pdh, &S.tq_h, &S.ch, &S.dh, &S.qh, &S.qdh})
     for (auto& b : *v) b.zero(stream);
+  ones_dirty = true;
   invalidate_graphs();
+}
+
+// Tensor-core modes: the padding column ds+da of the critic-input block [s | a] holds 1.0 so the
+// critics' first-layer dW product (M = ds+da+1 rows) also produces the first-layer bias gradient
+// (its extra row lands on b0, which follows W0 in the flat layout).  Forward products never read
+// it (their K extent is ds+da).
+void Pop::ensure_ones() {
+  if (!ones_dirty) return;
+  if (use_tc() && lsa > ds + da)
+    launch_fill_col(S.in_sa.p, static_cast<long long>(n) * S.B, lsa, ds + da, 1.0f,
+                    act16() ? 1 : 0, stream);
+  ones_dirty = false;
 }
 
 // ------------------------------------------------------------------ update entry points
@@ -348,6 +362,7 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     PBRL_THROW(PBRL_E_USAGE, "policy_member_mask is a TD3 option");
   const int B = static_cast<int>(rows);
   ensure_scratch(B);
+  ensure_ones();
   ensure_corr(t_bound + k + 4);
   const uint8_t* d_mask = nullptr;
   if (policy_mask) {

@@ -101,6 +101,9 @@ struct Mat {
   // TF32 mode, hidden activations: ReLU mask bits [groups][rows][mld] next to the activations
   uint32_t* mask = nullptr;
   long long mgs = 0, mld = 0;
+  // input blocks: column `ones_col` (a padding column) holds 1.0 in every row, so the dW product
+  // of the first layer also yields the bias gradient as its extra row (0: no such column)
+  int ones_col = 0;
 };
 
 inline int pad4(int x) { return (x + 3) / 4 * 4; }
@@ -130,6 +133,8 @@ struct Pop {
   // step by the fused Adam + Polyak kernel and refreshed after any other weight write
   DBuf<__nv_bfloat16> pol_p16, pol_t16, cri_p16, cri_t16;
   bool weights_dirty = true;
+  bool ones_dirty = true;  // the critic-input ones column must be (re)written
+  void ensure_ones();
   void refresh_shadows();
   const void* wop(const float* W) const;  // tensor-core operand copy of master weights W
   DBuf<int64_t> t_pol, t_cri, t_alpha;

@@ -207,7 +207,10 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
                        4.0 * groups * in * out;
   const int eb = aeb();
   if (use_tc() && out >= 32 && tma_ok(X.p, X.ld, X.gs, eb) && tma_ok(G.p, G.ld, G.gs, eb)) {
-    TcOperand A{X.p, static_cast<uint64_t>(in), static_cast<uint64_t>(B),
+    // input block with a ones column at index `in`: one more output row = the bias gradient
+    const int mrows = (X.ones_col == in && in + 1 <= X.ld) ? in + 1 : in;
+    if (mrows > in) bias_done = true;
+    TcOperand A{X.p, static_cast<uint64_t>(mrows), static_cast<uint64_t>(B),
                 static_cast<uint64_t>(X.by_member ? n : groups), static_cast<uint64_t>(X.ld),
                 static_cast<uint64_t>(X.gs)};
     TcOperand Bg{G.p, static_cast<uint64_t>(out), static_cast<uint64_t>(B),
@@ -215,7 +218,7 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
                  static_cast<uint64_t>(G.gs)};
     TcArgs a;
     a.eb = eb;
-    a.M = in;
+    a.M = mrows;
     a.N = out;
     a.K = B;
     a.groups = groups;
@@ -564,7 +567,8 @@ void Pop::critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>
 // backward, fused Adam + target Polyak (algos.hpp:369-377, :401-418).
 void Pop::critic_update(int B, const int* polyak_gate) {
   const int n2 = 2 * n;
-  const Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
+  Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
+  if (use_tc() && lsa > ds + da) x0.ones_col = ds + da;  // see Pop::ensure_ones
   mlp_forward(cri, cri_p.p, n2, B, x0, S.ch, S.q.p, B, 1, EPI_BIAS);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
   mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr);

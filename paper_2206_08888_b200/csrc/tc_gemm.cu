@@ -942,11 +942,33 @@ bool tma_ok(const void* base, uint64_t row_stride_elems, uint64_t group_stride_e
          ((group_stride_elems * eb) % 16 == 0);
 }
 
-int pick_bn(int N, bool b_mn) {
+// Tile width: the persistent grid walks `tiles` tiles on #SM CTAs, so a launch lasts
+// ceil(tiles / #SM) tile-times -- with a few hundred tiles the last partial wave is a large share
+// (80 members x 2 row tiles = 160 tiles on 148 SMs: 2 waves for 1.08 waves of work).  Narrower
+// tiles make the waves finer at the cost of re-reading A per N tile and a per-tile epilogue
+// start-up; the model below (cost ~ waves x (BN + 48)) picks the cheapest legal width.
+// PBRL_TC_BN=<64|128|256> pins it (diagnostics).
+int pick_bn(const TcArgs& g, bool b_mn) {
+  const int N = g.N;
   if (N <= 16 && !b_mn) return 16;
-  if (N <= 64) return 64;
-  if (N <= 128) return 128;
-  return 256;
+  if (g.nout > 0) return 256;  // the fused output layer needs the whole hidden row
+  static const int pin = std::getenv("PBRL_TC_BN") ? std::atoi(std::getenv("PBRL_TC_BN")) : 0;
+  if (pin == 64 || pin == 128 || pin == 256) return pin;
+  const int m_tiles = (g.M + kBM - 1) / kBM;
+  const int sms = num_sms();
+  int best = 256;
+  double best_cost = 1e30;
+  for (int bn : {64, 128, 256}) {
+    const long long tiles = static_cast<long long>(g.groups) * m_tiles * ((N + bn - 1) / bn);
+    const double waves = static_cast<double>((tiles + sms - 1) / sms);
+    const double cost = waves * (std::min(bn, ((N + 31) / 32) * 32) + 48);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = bn;
+    }
+    if (bn >= N) break;  // wider tiles only add padding
+  }
+  return best;
 }
 
 // Diagnostics: with PBRL_TC_TRACE set, every launch (in issue / capture order) gets its own
@@ -978,7 +1000,7 @@ int tc_trace_dump(unsigned long long* host, TcTraceMeta* meta, int max_launches)
 void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn,
                     const TcArgs& g0, cudaStream_t s) {
   TcArgs g = g0;
-  const int bn = pick_bn(g.N, b_mn);
+  const int bn = pick_bn(g, b_mn);
   static const int dbg = std::getenv("PBRL_TC_DBG") ? std::atoi(std::getenv("PBRL_TC_DBG")) : 0;
   g.dbg = dbg;
   if (g_trace && g_trace_n < kTraceLaunches) {

@@ -112,7 +112,7 @@ def main():
     traffic = {}
     for r in reps:
         traffic.update(full(r, tag))
-    prec = "tf32" if "tf32" in tag else "ffma32"
+    prec = "bf16" if "bf16" in tag else ("tf32" if "tf32" in tag else "ffma32")
     cls_map = {"gemm_fwd": "k_tc_gemm", "adam_polyak": "k_adam"}
     out = {c: next((v for k, v in traffic.items() if k.startswith(kn)), None)
            for c, kn in cls_map.items()}
