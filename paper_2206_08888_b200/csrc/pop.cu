@@ -68,6 +68,7 @@ Pop::Pop(const pbrl_pop_desc& d) {
   CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   tc_trace_init();
   use_graphs = std::getenv("PBRL_NO_GRAPH") == nullptr;  // eager replay (ncu kernel profiles)
+  fwd2_off = std::getenv("PBRL_NO_FWD2") != nullptr;
 
   std::vector<size_t> pd{static_cast<size_t>(ds)};
   pd.insert(pd.end(), hidden.begin(), hidden.end());

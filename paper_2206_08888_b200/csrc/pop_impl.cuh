@@ -231,6 +231,11 @@ struct Pop {
                    int last_epi, const int* active = nullptr, float* C2 = nullptr,
                    long long c2_gs = 0, long long c2_ld = 0, bool noise = false,
                    bool keep_hidden = true, bool out_act = false);
+  bool mlp_forward2(const NetShape& sh, const float* W, int groups, int B, Mat x,
+                    std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
+                    int last_epi, const int* active, float* C2, long long c2_gs, long long c2_ld,
+                    bool noise, bool keep_hidden, bool out_act);
+  bool fwd2_off = false;  // PBRL_NO_FWD2=1: per-layer launches instead (diagnostics)
   bool gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, Mat H,
                       bool keep_hidden, float* Y, long long y_gs, long long y_ld, int out_epi,
                       const int* active, float* C2, long long c2_gs, long long c2_ld, bool noise,

@@ -356,6 +356,9 @@ void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat
                       int last_epi, const int* active, float* C2, long long c2_gs,
                       long long c2_ld, bool noise, bool keep_hidden, bool out_act) {
   const int L = sh.depth;
+  if (mlp_forward2(sh, W, groups, B, x, hs, out, out_gs, out_ld, last_epi, active, C2, c2_gs,
+                   c2_ld, noise, keep_hidden, out_act))
+    return;  // both hidden layers and the output layer in one launch (BF16 mode)
   for (int l = 0; l < L; ++l) {
     if (l == L - 1) {
       gemm_fwd(sh, W, l, groups, B, x, out, out_gs, out_ld, last_epi, active, C2, c2_gs, c2_ld,
@@ -370,6 +373,84 @@ void Pop::mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat
       x = h;
     }
   }
+}
+
+// BF16 mode, two hidden layers: the whole forward in one launch (launch_mlp_fwd2); h1 stays in
+// shared memory and reaches HBM (with h2 and the mask bits) only when the backward needs it.
+bool Pop::mlp_forward2(const NetShape& sh, const float* W, int groups, int B, Mat x,
+                       std::vector<DBuf<float>>& hs, float* out, long long out_gs,
+                       long long out_ld, int last_epi, const int* active, float* C2,
+                       long long c2_gs, long long c2_ld, bool noise, bool keep_hidden,
+                       bool out_act) {
+  if (!act16() || sh.depth != 3 || fwd2_off) return false;
+  Fwd2Args a;
+  a.M = B;
+  a.in = sh.dims[0];
+  a.H1 = sh.dims[1];
+  a.H2 = sh.dims[2];
+  a.nout = sh.dims[3];
+  a.groups = groups;
+  a.n_members = n;
+  a.X = x.p;
+  a.x_ld = x.ld;
+  a.x_gs = x.gs;
+  a.x_by_member = x.by_member;
+  a.W1 = wop(W + sh.woff[0]);
+  a.W2 = wop(W + sh.woff[1]);
+  a.w_gs = static_cast<long long>(sh.stride);
+  a.b1 = W + sh.boff[0];
+  a.b2 = W + sh.boff[1];
+  a.ow = W + sh.woff[2];
+  a.p_gs = static_cast<long long>(sh.stride);
+  a.out_epi = last_epi;
+  a.out_scale = sh.out_scale;
+  a.oC = out;
+  a.oc_gs = out_gs;
+  a.oc_rs = out_ld;
+  a.oc16 = out_act ? 1 : 0;
+  a.oC2 = C2;
+  a.oc2_gs = c2_gs;
+  a.oc2_rs = c2_ld;
+  Mat h1{}, h2{};
+  if (keep_hidden) {
+    h1 = hid(hs, 0, B, sh, 0);
+    h2 = hid(hs, 1, B, sh, 0);
+    a.H1g = const_cast<float*>(h1.p);
+    a.h1_gs = h1.gs;
+    a.h1_ld = h1.ld;
+    a.m1 = h1.mask;
+    a.m1_gs = h1.mgs;
+    a.m1_ld = h1.mld;
+    a.H2g = const_cast<float*>(h2.p);
+    a.h2_gs = h2.gs;
+    a.h2_ld = h2.ld;
+    a.m2 = h2.mask;
+    a.m2_gs = h2.mgs;
+    a.m2_ld = h2.mld;
+  }
+  a.active = active;
+  if (noise) {
+    a.noise_key = key_a.p;
+    a.noise_sd = h_f2.p;
+    a.noise_clip = h_f3.p;
+    a.bound = bound;
+    if (algo == PBRL_ALGO_TD3 && a.nout == da) {  // precomputed by launch_td3_target_noise
+      a.noise_eps = S.tnoise.p;
+      a.ne_gs = static_cast<long long>(B) * da;
+      a.ne_rs = da;
+    }
+  }
+  if (!mlp_fwd2_ok(a)) return false;
+  const int in = a.in, H1 = a.H1, H2 = a.H2, no = a.nout;
+  const double flops = 2.0 * B * groups * (static_cast<double>(in) * H1 + H1 * H2 + H2 * no);
+  const double bytes =
+      2.0 * (static_cast<double>(B) * in * (x.by_member ? n : groups) +
+             static_cast<double>(groups) * (in * H1 + H1 * H2)) +
+      4.0 * groups * (H1 + H2 + H2 * no + no) + (out_act ? 2.0 : 4.0) * groups * B * no +
+      (keep_hidden ? groups * B * (2.0 * (H1 + H2) + 4.0 * ((H1 + 31) / 32 + (H2 + 31) / 32))
+                   : 0.0);
+  timed(PC_GEMM_FWD, flops, bytes, active != nullptr, [&] { launch_mlp_fwd2(a, stream); });
+  return true;
 }
 
 // Last hidden layer + output layer in one tcgen05 launch (TF32 mode): the output layer's few

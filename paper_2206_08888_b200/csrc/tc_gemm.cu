@@ -819,6 +819,373 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   if (threadIdx.x == 0) TC_TRACE(63);
 }
 
+// ------------------------------------------------------------------ fused two-layer forward
+// k_mlp_fwd2 (BF16 mode): one persistent launch evaluates hidden layer 1, hidden layer 2 and the
+// output layer of an MLP population.  Per 128-row tile of a group:
+//   producer : X tile (one 64-wide K chunk: in <= 64) and W1 into the layer-1 buffers, then W2
+//              through a 2-deep ring of 64-row K chunks
+//   MMA      : acc1 (TMEM cols 0..255) = X W1; after the epilogue has turned acc1 into h1 in
+//              shared memory, acc2 (cols 256..511) = h1 W2 with A read from that shared-memory
+//              copy (K-major, 128B swizzle) -- h1 never round-trips through HBM
+//   epilogue : E1 relu(acc1 + b1) -> bf16 K-major operand tile (+ HBM copy and mask bits when
+//              kept); E2 relu(acc2 + b2) -> output layer on CUDA cores (+ h2 to HBM when kept)
+// The layer-1 MMA of tile i+1 overlaps E2 of tile i (acc1 is free once E1 consumed it).
+constexpr uint32_t kF2H1 = 65536;  // h1 operand: 4 K chunks x (128 rows x 128 B); E2 staging
+constexpr uint32_t kF2X = kBM * kRowBytes;   // 16 KB
+constexpr uint32_t kF2W = 256 * kRowBytes;   // 32 KB: 64 K rows x 256 N, as 4 boxes of 64 x 64
+constexpr uint32_t kF2Ring = 2;
+
+template <int NO>
+__host__ __device__ constexpr size_t fwd2_smem() {
+  return kF2H1 + kF2X + kF2W + kF2Ring * kF2W + 256 + 2 * 256 * 4 + 256 * NO * 4 +
+         2 * kBM * NO * 4 + 1024;
+}
+
+template <int NO>
+__global__ void __launch_bounds__(64 + kEpiThreads, 1)
+    k_mlp_fwd2(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
+               const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmH1,
+               const __grid_constant__ CUtensorMap tmH2, const Fwd2Args g) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sH1 = smem;
+  uint8_t* sX = sH1 + kF2H1;
+  uint8_t* sW1 = sX + kF2X;
+  uint8_t* sW2 = sW1 + kF2W;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW2 + kF2Ring * kF2W);
+  uint64_t* l1full = bars;
+  uint64_t* l1empty = bars + 1;
+  uint64_t* w2full = bars + 2;   // [2]
+  uint64_t* w2empty = bars + 4;  // [2]
+  uint64_t* acc1full = bars + 6;
+  uint64_t* h1ready = bars + 7;
+  uint64_t* acc2full = bars + 8;
+  uint64_t* acc2empty = bars + 9;
+  uint64_t* sbar = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  float* fz_b1 = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
+  float* fz_b2 = fz_b1 + 256;
+  float* fz_w = fz_b2 + 256;
+  float* osum = fz_w + 256 * NO;  // [2][4][32][NO]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m_tiles = (g.M + kBM - 1) / kBM;
+  const int num_tiles = g.groups * m_tiles;
+  const int nk2 = g.H1 / 64;
+  const int nout = NO < 16 ? NO : g.nout;
+  if (threadIdx.x == 0) TC_TRACE(0);
+
+  if (threadIdx.x == 0) {
+    mbar_init(l1full, 1);
+    mbar_init(l1empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&w2full[s], 1);
+      mbar_init(&w2empty[s], 1);
+    }
+    mbar_init(acc1full, 1);
+    mbar_init(h1ready, kEpiWarps);
+    mbar_init(acc2full, 1);
+    mbar_init(acc2empty, kEpiWarps);
+    mbar_init(sbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW1)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW2)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) {
+    TC_TRACE(1);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
+  auto active = [&](int grp) { return !g.active || g.active[grp % g.n_members]; };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      int it = 0, cnt = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int grp = t / m_tiles, m0 = (t % m_tiles) * kBM;
+        if (!active(grp)) continue;
+        const int mem = grp % g.n_members;
+        if (it > 0) mbar_wait(l1empty, (it - 1) & 1);
+        mbar_expect_tx(l1full, kF2X + kF2W);
+        tma_load_3d(&tmX, l1full, sX, 0, m0, g.x_by_member ? mem : grp);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) tma_load_3d(&tmW1, l1full, sW1 + j * 8192, 64 * j, 0, grp);
+        for (int kc = 0; kc < nk2; ++kc, ++cnt) {
+          const int s = cnt & 1;
+          if (cnt >= 2) mbar_wait(&w2empty[s], ((cnt >> 1) - 1) & 1);
+          mbar_expect_tx(&w2full[s], kF2W);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            tma_load_3d(&tmW2, &w2full[s], sW2 + s * kF2W + j * 8192, 64 * j, 64 * kc, grp);
+        }
+        ++it;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer (bf16 x bf16 -> f32, A K-major, B MN-major)
+      constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                                 (static_cast<uint32_t>(256 >> 3) << 17) |
+                                 (static_cast<uint32_t>(kBM >> 4) << 24);
+      int it = 0, cnt = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        if (!active(t / m_tiles)) continue;
+        mbar_wait(l1full, it & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16(tmem, sdesc(smem_u32(sX) + kk * 32, 16, 1024, 2),
+                   sdesc(smem_u32(sW1) + kk * 2048, 8192, 1024, 2), idesc, kk ? 1u : 0u);
+        mma_commit(l1empty);
+        mma_commit(acc1full);
+        mbar_wait(h1ready, it & 1);  // h1 in shared memory, acc1 drained
+        if (it > 0) mbar_wait(acc2empty, (it - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int kc = 0; kc < nk2; ++kc, ++cnt) {
+          const int s = cnt & 1;
+          mbar_wait(&w2full[s], (cnt >> 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16(tmem + 256, sdesc(smem_u32(sH1) + kc * 16384 + kk * 32, 16, 1024, 2),
+                     sdesc(smem_u32(sW2) + s * kF2W + kk * 2048, 8192, 1024, 2), idesc,
+                     (kc | kk) ? 1u : 0u);
+          mma_commit(&w2empty[s]);
+        }
+        mma_commit(acc2full);
+        ++it;
+      }
+    }
+  } else {
+    // ---------------- epilogue: warp w reads TMEM lane quadrant q = w % 4 and handles the
+    // column half hf of each layer
+    const int ew = warp - 2, q = warp & 3, hf = ew >> 2;
+    uint8_t* wbuf = sH1 + ew * 4096;  // E2 staging: two 2 KB bf16 boxes per warp (inside sH1)
+    constexpr int NA = NO;
+    const int hc1 = g.H1 / 64;               // 32-column chunks of h1 per half
+    const int hc2 = (g.H2 + 63) / 64;        // 32-column chunks of h2 per half
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int e = threadIdx.x - 64; e < 2 * 256 + 256 * NO; e += kEpiThreads) fz_b1[e] = 0.0f;
+    int it = 0, nchunk = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int grp = t / m_tiles, m0 = (t % m_tiles) * kBM;
+      if (!active(grp)) continue;
+      const int mem = grp % g.n_members;
+      const int row0 = m0 + q * 32, row = row0 + lane;
+      const int r = q * 32 + lane;  // row inside the tile
+      if (threadIdx.x == 64) TC_TRACE_TILE(it, 0);
+      // ---- stage b1, b2, W_out of this group; the previous tile's staging stores (inside sH1)
+      // must have been read out before E1 rewrites sH1
+      if (lane == 0) tma_store_wait_read<0>();
+      __syncwarp();
+      epi_bar_sync();
+      if (threadIdx.x == 64) {
+        const uint32_t by1 = g.H1 * 4, by2 = g.H2 * 4, byw = g.H2 * nout * 4;
+        mbar_expect_tx(sbar, by1 + by2 + byw);
+        bulk_g2s(fz_b1, g.b1 + grp * g.p_gs, by1, sbar);
+        bulk_g2s(fz_b2, g.b2 + grp * g.p_gs, by2, sbar);
+        bulk_g2s(fz_w, g.ow + grp * g.p_gs, byw, sbar);
+      }
+      float ob[NA], ep[NA];
+      if (hf == 0) {
+        const float* obg = g.ow + grp * g.p_gs + static_cast<long long>(g.H2) * nout;
+        const bool noisy = g.out_epi == EPI_BIAS_TANH_NOISE && g.noise_eps && row < g.M;
+        const float* eg =
+            noisy ? g.noise_eps + grp * g.ne_gs + static_cast<long long>(row) * g.ne_rs : nullptr;
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          ob[o] = o < nout ? __ldg(obg + o) : 0.0f;
+          ep[o] = (noisy && o < nout) ? __ldg(eg + o) : 0.0f;
+        }
+      }
+      mbar_wait(sbar, it & 1);
+
+      // ---- E1: h1 = relu(acc1 + b1) -> sH1 (K-major, 128B swizzle) [+ HBM, mask bits]
+      mbar_wait(acc1full, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (threadIdx.x == 64) TC_TRACE_TILE(it, 1);
+      {
+        const uint32_t tacc = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        uint32_t* mrow = (g.m1 && row < g.M)
+                             ? g.m1 + grp * g.m1_gs + static_cast<long long>(row) * g.m1_ld
+                             : nullptr;
+        // chunks in register pairs (va, vb): the next chunk's tcgen05.ld is in flight while the
+        // current one is processed; static register names (no local-memory arrays)
+        auto e1_chunk = [&](float* cur, int c0) {
+          uint32_t bits = 0u;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float z = cur[j] + fz_b1[c0 + j];
+            cur[j] = z > 0.0f ? z : 0.0f;
+            bits |= (z > 0.0f ? 1u : 0u) << j;
+          }
+          uint8_t* rowp = sH1 + (c0 >> 6) * 16384 + r * 128;
+          const int j0 = (c0 & 63) >> 3;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint4 w4 = make_uint4(pack_bf16x2(cur[8 * u], cur[8 * u + 1]),
+                                        pack_bf16x2(cur[8 * u + 2], cur[8 * u + 3]),
+                                        pack_bf16x2(cur[8 * u + 4], cur[8 * u + 5]),
+                                        pack_bf16x2(cur[8 * u + 6], cur[8 * u + 7]));
+            *reinterpret_cast<uint4*>(rowp + (((j0 + u) ^ (r & 7)) << 4)) = w4;
+          }
+          if (mrow) mrow[c0 >> 5] = bits;
+        };
+        float va[32], vb[32];
+        const int cb = hf * hc1 * 32;
+        tmem_ld32(tacc + static_cast<uint32_t>(cb), va);
+#pragma unroll 1
+        for (int ci = 0; ci < hc1; ci += 2) {
+          tmem_ld_wait(va);
+          if (ci + 1 < hc1) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 1) * 32), vb);
+          e1_chunk(va, cb + ci * 32);
+          if (ci + 1 < hc1) {
+            tmem_ld_wait(vb);
+            if (ci + 2 < hc1) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 2) * 32), va);
+            e1_chunk(vb, cb + (ci + 1) * 32);
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        if (g.H1g) {  // this warp's 32 rows of its K chunks -> HBM (box 64 cols x 32 rows)
+          for (int kc = hf * hc1 / 2; kc < (hf + 1) * hc1 / 2; ++kc)
+            tma_store_3d(&tmH1, sH1 + kc * 16384 + q * 4096, kc * 64, row0, grp);
+        }
+        mbar_arrive(h1ready);
+      }
+      if (threadIdx.x == 64) TC_TRACE_TILE(it, 2);
+
+      // ---- E2: relu(acc2 + b2) -> output layer (+ h2 to HBM)
+      mbar_wait(acc2full, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (threadIdx.x == 64) TC_TRACE_TILE(it, 3);
+      // sH1 becomes staging: h1's HBM copies must have been read out by every warp
+      if (lane == 0) tma_store_wait_read<0>();
+      __syncwarp();
+      epi_bar_sync();
+      {
+        const uint32_t tacc = tmem + 256u + (static_cast<uint32_t>(q * 32) << 16);
+        uint32_t* mrow = (g.m2 && row < g.M)
+                             ? g.m2 + grp * g.m2_gs + static_cast<long long>(row) * g.m2_ld
+                             : nullptr;
+        float oacc[NA];
+#pragma unroll
+        for (int o = 0; o < NA; ++o) oacc[o] = 0.0f;
+        auto e2_chunk = [&](float* cur, int c0) {
+          uint32_t bits = 0u;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float z = cur[j] + fz_b2[c0 + j];
+            const float h = z > 0.0f ? z : 0.0f;
+            cur[j] = h;
+            bits |= (z > 0.0f ? 1u : 0u) << j;
+            const float* wr = fz_w + (c0 + j) * nout;
+#pragma unroll
+            for (int o = 0; o < NA; ++o) {
+              if (NO == 16 && o >= nout) break;
+              oacc[o] = oacc[o] + h * wr[o];
+            }
+          }
+          if (g.H2g) {
+            uint8_t* box = wbuf + (nchunk & 1) * 2048;
+            if (lane == 0 && nchunk >= 2) tma_store_wait_read<1>();
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint4 w4 = make_uint4(pack_bf16x2(cur[8 * u], cur[8 * u + 1]),
+                                          pack_bf16x2(cur[8 * u + 2], cur[8 * u + 3]),
+                                          pack_bf16x2(cur[8 * u + 4], cur[8 * u + 5]),
+                                          pack_bf16x2(cur[8 * u + 6], cur[8 * u + 7]));
+              *reinterpret_cast<uint4*>(box + sw64(lane, u)) = w4;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tma_store_3d(&tmH2, box, c0, row0, grp);
+            ++nchunk;
+            if (mrow) mrow[c0 >> 5] = bits;
+          }
+        };
+        const int cb = hf * hc2 * 32;
+        const int nc = max(0, min(hc2, (g.H2 - cb + 31) / 32));  // this half's chunks < H2
+        float va[32], vb[32];
+        if (nc > 0) tmem_ld32(tacc + static_cast<uint32_t>(cb), va);
+#pragma unroll 1
+        for (int ci = 0; ci < nc; ci += 2) {
+          tmem_ld_wait(va);
+          if (ci + 1 < nc) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 1) * 32), vb);
+          e2_chunk(va, cb + ci * 32);
+          if (ci + 1 < nc) {
+            tmem_ld_wait(vb);
+            if (ci + 2 < nc) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 2) * 32), va);
+            e2_chunk(vb, cb + (ci + 1) * 32);
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc2empty);
+        if (threadIdx.x == 64) TC_TRACE_TILE(it, 4);
+        // half 1 hands its partial sums to half 0 (double-buffered by tile parity)
+        float* os = osum + (((it & 1) * 4 + q) * 32 + lane) * NA;
+        if (hf == 1) {
+#pragma unroll
+          for (int o = 0; o < NA; ++o) os[o] = oacc[o];
+        }
+        quad_bar_sync(q);
+        if (hf == 0 && row < g.M) {
+          const long long obase = grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
+          const bool tanh_out = g.out_epi == EPI_BIAS_TANH || g.out_epi == EPI_BIAS_TANH_NOISE;
+#pragma unroll
+          for (int o = 0; o < NA; ++o) {
+            if (o >= nout) break;
+            const float y = (oacc[o] + os[o]) + ob[o];
+            float rr = y;
+            if (tanh_out) {
+              const float th = epi_tanhf(y);
+              if (g.oC2) g.oC2[grp * g.oc2_gs + static_cast<long long>(row) * g.oc2_rs + o] = th;
+              rr = (g.out_scale != 1.0f) ? th * g.out_scale : th;
+              if (g.out_epi == EPI_BIAS_TANH_NOISE) {
+                float eps;
+                if (g.noise_eps) {
+                  eps = ep[o];
+                } else {
+                  const uint64_t e = static_cast<uint64_t>(row) * nout + o;
+                  eps = epi_normal(g.noise_key[mem], 2 * e) * g.noise_sd[mem];
+                  eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+                }
+                rr = clampf_ref(rr + eps, -g.bound, g.bound);
+              }
+            }
+            if (g.oc16) static_cast<__nv_bfloat16*>(g.oC)[obase + o] = __float2bfloat16_rn(rr);
+            else static_cast<float*>(g.oC)[obase + o] = rr;
+          }
+        }
+      }
+      ++it;
+    }
+    if (lane == 0) tma_store_wait_all();
+    if (threadIdx.x == 64) TC_TRACE(62);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+  if (threadIdx.x == 0) TC_TRACE(63);
+}
+
 // ------------------------------------------------------------------ host side
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1045,6 +1412,57 @@ void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn
     else if (a_mn) launch_bn<true, false, 2>(bn, ta, tb, tc, tx, g, s);
     else if (b_mn) launch_bn<false, true, 2>(bn, ta, tb, tc, tx, g, s);
     else launch_bn<false, false, 2>(bn, ta, tb, tc, tx, g, s);
+  }
+}
+
+bool mlp_fwd2_ok(const Fwd2Args& a) {
+  auto al16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  return a.in >= 1 && a.in <= 64 && a.H1 % 128 == 0 && a.H1 <= 256 && a.H2 % 32 == 0 &&
+         a.H2 >= 32 && a.H2 <= 256 && a.nout >= 1 && a.nout <= 16 && a.x_ld % 8 == 0 &&
+         a.x_gs % 8 == 0 && a.w_gs % 8 == 0 && a.p_gs % 4 == 0 && al16(a.X) && al16(a.W1) &&
+         al16(a.W2) && al16(a.b1) && al16(a.b2) && al16(a.ow) &&
+         (!a.H1g || (al16(a.H1g) && a.h1_ld % 8 == 0 && a.h1_gs % 8 == 0)) &&
+         (!a.H2g || (al16(a.H2g) && a.h2_ld % 8 == 0 && a.h2_gs % 8 == 0));
+}
+
+namespace {
+template <int NO>
+void launch_fwd2_tpl(const Fwd2Args& a, cudaStream_t s) {
+  constexpr size_t smem = fwd2_smem<NO>();
+  static_assert(smem <= kMaxSmem, "fwd2: shared memory budget");
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_mlp_fwd2<NO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+    attr_set = true;
+  }
+  const CUtensorMap tx = make_tmap(a.X, 2, a.in, a.M, a.x_by_member ? a.n_members : a.groups,
+                                   a.x_ld, a.x_gs, 64, kBM, SWZ_128);
+  const CUtensorMap tw1 = make_tmap(a.W1, 2, a.H1, a.in, a.groups, a.H1, a.w_gs, 64, 64, SWZ_128);
+  const CUtensorMap tw2 = make_tmap(a.W2, 2, a.H2, a.H1, a.groups, a.H2, a.w_gs, 64, 64, SWZ_128);
+  CUtensorMap th1{}, th2{};
+  if (a.H1g) th1 = make_tmap(a.H1g, 2, a.H1, a.M, a.groups, a.h1_ld, a.h1_gs, 64, 32, SWZ_128);
+  if (a.H2g) th2 = make_tmap(a.H2g, 2, a.H2, a.M, a.groups, a.h2_ld, a.h2_gs, 32, 32, SWZ_64);
+  const int tiles = a.groups * ((a.M + kBM - 1) / kBM);
+  launch_k(k_mlp_fwd2<NO>, std::min(tiles, num_sms()), 64 + kEpiThreads, smem, s, tx, tw1, tw2,
+           th1, th2, a);
+}
+}  // namespace
+
+void launch_mlp_fwd2(const Fwd2Args& a0, cudaStream_t s) {
+  Fwd2Args a = a0;
+  if (!mlp_fwd2_ok(a)) PBRL_THROW(PBRL_E_USAGE, "fused forward: unsupported shape / alignment");
+  if (g_trace && g_trace_n < kTraceLaunches) {
+    a.trace = g_trace + static_cast<size_t>(g_trace_n) * kTraceCtas * kTraceSlots;
+    // epi 99 marks the fused two-layer forward in the trace metadata (tools/tc_trace.py)
+    g_trace_meta[g_trace_n] = TcTraceMeta{256, 0, 1, a.nout, a.M, a.H2, a.H1, a.groups, 99, 0};
+    ++g_trace_n;
+  }
+  switch (a.nout) {
+    case 1: launch_fwd2_tpl<1>(a, s); return;
+    case 6: launch_fwd2_tpl<6>(a, s); return;
+    case 12: launch_fwd2_tpl<12>(a, s); return;
+    default: launch_fwd2_tpl<16>(a, s); return;
   }
 }
 

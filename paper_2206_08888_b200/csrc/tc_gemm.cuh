@@ -86,4 +86,49 @@ bool tma_ok(const void* base, uint64_t row_stride_elems, uint64_t group_stride_e
 void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn,
                     const TcArgs& g, cudaStream_t s);
 
+// Two hidden layers and the output layer of one MLP forward in ONE persistent launch (BF16
+// mode): per 128-row tile of a group, h1 = relu(X W1 + b1) is written by the epilogue straight
+// into shared memory as the K-major tcgen05 operand of h2 = relu(h1 W2 + b2), whose epilogue
+// evaluates the output layer (out_epi as in TcArgs).  h1 / h2 and their ReLU mask bits reach HBM
+// only when kept for the backward pass (H1g / H2g non-null).  Requirements: in <= 64, H1 a
+// multiple of 64 and <= 256, H2 a multiple of 32 and <= 256, nout <= 16.
+struct Fwd2Args {
+  int M = 0, in = 0, H1 = 0, H2 = 0, groups = 0, n_members = 1;
+  const void* X = nullptr;  // bf16 [groups or members][M][x_ld]
+  long long x_ld = 0, x_gs = 0;
+  int x_by_member = 0;
+  const void* W1 = nullptr;  // bf16 operand copies, W1 [in][H1], W2 [H1][H2], group stride w_gs
+  const void* W2 = nullptr;
+  long long w_gs = 0;
+  const float* b1 = nullptr;  // fp32 master rows (group stride p_gs): b1, b2, W_out [H2][nout]
+  const float* b2 = nullptr;  // followed by b_out
+  const float* ow = nullptr;
+  long long p_gs = 0;
+  int nout = 0, out_epi = 0;
+  float out_scale = 1.0f;
+  void* oC = nullptr;
+  long long oc_gs = 0, oc_rs = 0;
+  int oc16 = 0;
+  float* oC2 = nullptr;
+  long long oc2_gs = 0, oc2_rs = 0;
+  void* H1g = nullptr;  // bf16 [groups][M][h1_ld] + mask bits m1 (nullptr: not kept)
+  long long h1_gs = 0, h1_ld = 0;
+  uint32_t* m1 = nullptr;
+  long long m1_gs = 0, m1_ld = 0;
+  void* H2g = nullptr;
+  long long h2_gs = 0, h2_ld = 0;
+  uint32_t* m2 = nullptr;
+  long long m2_gs = 0, m2_ld = 0;
+  const int* active = nullptr;
+  const uint64_t* noise_key = nullptr;
+  const float* noise_sd = nullptr;
+  const float* noise_clip = nullptr;
+  float bound = 1.0f;
+  const float* noise_eps = nullptr;
+  long long ne_gs = 0, ne_rs = 0;
+  unsigned long long* trace = nullptr;  // diagnostics (PBRL_TC_TRACE)
+};
+bool mlp_fwd2_ok(const Fwd2Args& a);
+void launch_mlp_fwd2(const Fwd2Args& a, cudaStream_t s);
+
 }  // namespace pbrl

@@ -89,7 +89,8 @@ def main():
                 ph[4].append(c[62] - c[last])
         med = {k: (np.median(v) / 1e3 if v else float("nan")) for k, v in ph.items()}
         m = meta[li]
-        op = f"{EPI[m[8]] if m[8] < len(EPI) else m[8]}" + (f"+out{m[3]}" if m[3] else "")
+        op = (f"{EPI[m[8]] if m[8] < len(EPI) else m[8]}" if m[8] != 99 else
+              "FWD2 [cols: stage+MMA1 | E1 | MMA2 | E2]") + (f"+out{m[3]}" if m[3] else "")
         lines.append(
             f"| {li} | {m[0]},{'MN' if m[1] else 'K'},{'MN' if m[2] else 'K'} | {op} | "
             f"{m[4]},{m[5]},{m[6]} x {m[7]} | {span:.1f} | {setup:.2f} | "
