@@ -858,11 +858,11 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   uint64_t* w2full = bars + 2;   // [2]
   uint64_t* w2empty = bars + 4;  // [2]
   uint64_t* acc1full = bars + 6;
-  uint64_t* h1ready = bars + 7;
-  uint64_t* acc2full = bars + 8;
-  uint64_t* acc2empty = bars + 9;
-  uint64_t* sbar = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* acc2full = bars + 7;
+  uint64_t* acc2empty = bars + 8;
+  uint64_t* sbar = bars + 9;
+  uint64_t* h1kc = bars + 10;  // [4]: K chunk kc of h1 written (4 warps of its column half)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   float* fz_b1 = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
   float* fz_b2 = fz_b1 + 256;
   float* fz_w = fz_b2 + 256;
@@ -872,6 +872,9 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   const int m_tiles = (g.M + kBM - 1) / kBM;
   const int num_tiles = g.groups * m_tiles;
   const int nk2 = g.H1 / 64;
+  // layer-2 K chunk order: the two column halves of E1 are written concurrently, so the MMAs
+  // alternate halves (0, 2, 1, 3 for H1 = 256) and start after the first chunk of each half
+  auto korder = [&](int j) { return (j & 1) * (nk2 / 2) + (j >> 1); };
   const int nout = NO < 16 ? NO : g.nout;
   if (threadIdx.x == 0) TC_TRACE(0);
 
@@ -883,7 +886,7 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
       mbar_init(&w2empty[s], 1);
     }
     mbar_init(acc1full, 1);
-    mbar_init(h1ready, kEpiWarps);
+    for (int k = 0; k < 4; ++k) mbar_init(&h1kc[k], kEpiWarps / 2);
     mbar_init(acc2full, 1);
     mbar_init(acc2empty, kEpiWarps);
     mbar_init(sbar, 1);
@@ -927,7 +930,8 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           mbar_expect_tx(&w2full[s], kF2W);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            tma_load_3d(&tmW2, &w2full[s], sW2 + s * kF2W + j * 8192, 64 * j, 64 * kc, grp);
+            tma_load_3d(&tmW2, &w2full[s], sW2 + s * kF2W + j * 8192, 64 * j, 64 * korder(kc),
+                        grp);
         }
         ++it;
       }
@@ -948,18 +952,17 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
                    sdesc(smem_u32(sW1) + kk * 2048, 8192, 1024, 2), idesc, kk ? 1u : 0u);
         mma_commit(l1empty);
         mma_commit(acc1full);
-        mbar_wait(h1ready, it & 1);  // h1 in shared memory, acc1 drained
         if (it > 0) mbar_wait(acc2empty, (it - 1) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int kc = 0; kc < nk2; ++kc, ++cnt) {
-          const int s = cnt & 1;
+        for (int j = 0; j < nk2; ++j, ++cnt) {
+          const int kc = korder(j), s = cnt & 1;
+          mbar_wait(&h1kc[kc], it & 1);  // this K chunk of h1 is in shared memory
           mbar_wait(&w2full[s], (cnt >> 1) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             mma_bf16(tmem + 256, sdesc(smem_u32(sH1) + kc * 16384 + kk * 32, 16, 1024, 2),
                      sdesc(smem_u32(sW2) + s * kF2W + kk * 2048, 8192, 1024, 2), idesc,
-                     (kc | kk) ? 1u : 0u);
+                     (j | kk) ? 1u : 0u);
           mma_commit(&w2empty[s]);
         }
         mma_commit(acc2full);
@@ -1042,29 +1045,26 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           if (mrow) mrow[c0 >> 5] = bits;
         };
         float va[32], vb[32];
-        const int cb = hf * hc1 * 32;
+        const int cb = hf * hc1 * 32;  // a multiple of 64: each pair is one K chunk of h1
         tmem_ld32(tacc + static_cast<uint32_t>(cb), va);
 #pragma unroll 1
         for (int ci = 0; ci < hc1; ci += 2) {
           tmem_ld_wait(va);
-          if (ci + 1 < hc1) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 1) * 32), vb);
+          tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 1) * 32), vb);
           e1_chunk(va, cb + ci * 32);
-          if (ci + 1 < hc1) {
-            tmem_ld_wait(vb);
-            if (ci + 2 < hc1) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 2) * 32), va);
-            e1_chunk(vb, cb + (ci + 1) * 32);
+          tmem_ld_wait(vb);
+          if (ci + 2 < hc1) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 2) * 32), va);
+          e1_chunk(vb, cb + (ci + 1) * 32);
+          // K chunk kc complete in this warp's rows: visible to the MMA (async proxy), to HBM
+          const int kc = (cb + ci * 32) >> 6;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            if (g.H1g) tma_store_3d(&tmH1, sH1 + kc * 16384 + q * 4096, kc * 64, row0, grp);
+            mbar_arrive(&h1kc[kc]);
           }
         }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) {
-        if (g.H1g) {  // this warp's 32 rows of its K chunks -> HBM (box 64 cols x 32 rows)
-          for (int kc = hf * hc1 / 2; kc < (hf + 1) * hc1 / 2; ++kc)
-            tma_store_3d(&tmH1, sH1 + kc * 16384 + q * 4096, kc * 64, row0, grp);
-        }
-        mbar_arrive(h1ready);
       }
       if (threadIdx.x == 64) TC_TRACE_TILE(it, 2);
 
