@@ -491,7 +491,8 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
                                  const uint8_t* mask, int* fire, int64_t* t_pol, int64_t* t_c1,
                                  int64_t* t_c2, uint64_t* steps, const uint64_t* streams,
                                  uint64_t seed, uint64_t* noise_key, double* policy_loss,
-                                 cudaGraphConditionalHandle any_fire, int set_cond) {
+                                 cudaGraphConditionalHandle any_fire,
+                                 cudaGraphConditionalHandle any_fire2, int set_cond) {
   PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   int f = 0;
@@ -516,16 +517,21 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
   // graph mode: the policy half of the step is an IF node on "some member fires"
   // (default 0 at every graph launch; any block with a firing member sets it)
   const int any = __syncthreads_or(f);
-  if (set_cond && any && threadIdx.x == 0) cudaGraphSetConditional(any_fire, 1u);
+  if (set_cond && any && threadIdx.x == 0) {
+    cudaGraphSetConditional(any_fire, 1u);
+    if (set_cond > 1) cudaGraphSetConditional(any_fire2, 1u);
+  }
 }
 
 void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const uint8_t* mask,
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
-                           cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s) {
+                           cudaGraphConditionalHandle any_fire,
+                           cudaGraphConditionalHandle any_fire2, int set_cond, cudaStream_t s) {
   launch_k(k_td3_step_begin, (n + 127) / 128, 128, 0, s, n, delay_acc, ratio, mask, fire, t_pol,
-           t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, set_cond);
+           t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, any_fire2,
+           set_cond);
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts

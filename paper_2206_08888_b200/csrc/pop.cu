@@ -167,6 +167,12 @@ Pop::~Pop() {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
+    if (side2) cudaStreamDestroy(side2);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side3) cudaStreamDestroy(side3);
+    if (ev_pfork) cudaEventDestroy(ev_pfork);
+    if (ev_pjoin) cudaEventDestroy(ev_pjoin);
   }
 }
 

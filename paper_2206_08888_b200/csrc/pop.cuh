@@ -164,7 +164,8 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
-                           cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s);
+                           cudaGraphConditionalHandle any_fire,
+                           cudaGraphConditionalHandle any_fire2, int set_cond, cudaStream_t s);
 // in_sa / in_s2a / sa_pi are activation buffers: fp32, or bf16 when act16
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, void* in_sa,

@@ -246,9 +246,20 @@ struct Pop {
   void critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>& hs,
                            std::vector<DBuf<float>>& dhs, float* out, long long out_ld, int epi,
                            Mat aux, float scale, const int* active);
-  void critic_update(int B, const int* polyak_gate);
+  void critic_forward(int B);
+  bool gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long long out_ld, int epi,
+                         Mat aux, float scale, const int* active);
+  void critic_update(int B, const int* polyak_gate, bool forward_done = false);
+  cudaStream_t side2 = nullptr;  // parallel graph branch (critic forward)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void td3_step(int B, const uint8_t* d_mask);
-  void td3_policy_half(int B);
+  void td3_policy_half(int B, bool forward_done);
+  void td3_policy_forward(int B);
+  template <typename F>
+  void capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body);
+  size_t cond_nodes = 0;
+  cudaStream_t side3 = nullptr;
+  cudaEvent_t ev_pfork = nullptr, ev_pjoin = nullptr;
   void sac_step(int B);
   void step(int B, const uint8_t* d_mask);
   void update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,

@@ -605,6 +605,8 @@ void Pop::critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>
   for (int l = L - 1; l >= 1; --l) {
     const Mat mask = hid(hs, l - 1, B, cri, 0);
     const Mat dh = hid(dhs, l - 1, B, cri, 0);
+    if (l == 1 && gemm_dx_to_action(groups, B, G, mask, out, out_ld, epi, aux, scale, active))
+      return;  // this layer's dX and the action-column dX of the input layer in one launch
     if (l == L - 1 && use_tc() && cri.dims[L] <= 16) {
       // output layer (N_out = 1): dX = relu'(h) * (G W_out^T) by the output-layer backward
       // kernel without its weight gradients (the policy loss discards them, algos.hpp:330-334)
@@ -644,13 +646,73 @@ void Pop::critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>
           epi, ds, da, active, scale);
 }
 
+// Tensor-core modes: the first hidden layer's dX and the input layer's action-column dX in one
+// launch -- dh1 = relu'(h1) (G W1^T) stays in the epilogue registers and is contracted on CUDA
+// cores with the action rows of W0 (a_grad[o] = sum_j dh1[j] W0[ds + o][j]) then the tanh
+// backward (or a plain store); dh1 never reaches HBM.  Returns false when not applicable.
+bool Pop::gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long long out_ld,
+                            int epi, Mat aux, float scale, const int* active) {
+  const int H = cri.dims[1], Hn = cri.dims[2];
+  const int eb = aeb();
+  const float* W1 = cri_p.p + cri.woff[1];
+  const void* W1o = wop(W1);
+  if (!use_tc() || H > 256 || H < 32 || da > 16 || Hn < 8 || !mask.mask ||
+      !tma_ok(G.p, G.ld, G.gs, eb) || !tma_ok(W1o, Hn, cri.stride, eb))
+    return false;
+  TcOperand A{G.p, static_cast<uint64_t>(Hn), static_cast<uint64_t>(B),
+              static_cast<uint64_t>(groups), static_cast<uint64_t>(G.ld),
+              static_cast<uint64_t>(G.gs)};
+  TcOperand Bw{W1o, static_cast<uint64_t>(Hn), static_cast<uint64_t>(H),
+               static_cast<uint64_t>(groups), static_cast<uint64_t>(Hn), cri.stride};
+  TcArgs a;
+  a.eb = eb;
+  a.M = B;
+  a.N = H;
+  a.K = Hn;
+  a.groups = groups;
+  a.n_members = n;
+  a.epi = EPI_RELU_MASK;
+  a.mask_in = mask.mask;
+  a.mi_gs = mask.mgs;
+  a.mi_ld = mask.mld;
+  a.mi_by_member = mask.by_member;
+  a.store_hidden = 0;
+  a.nout = da;
+  a.ow = cri_p.p + cri.woff[0] + static_cast<size_t>(ds) * H;
+  a.ow_gs = static_cast<long long>(cri.stride);
+  a.ow_tr = 1;
+  a.ow_ld = H;
+  a.out_epi = epi;
+  a.oC = out;
+  a.oc_gs = static_cast<long long>(B) * out_ld;
+  a.oc_rs = out_ld;
+  a.aux = aux.p;
+  a.aux_gs = aux.gs;
+  a.aux_rs = aux.ld;
+  a.aux_by_member = aux.by_member;
+  a.scale = scale;
+  a.active = active;
+  a.b_prefetch = last_wrote_weights ? 0 : 1;
+  const double flops = 2.0 * B * groups * (static_cast<double>(Hn) * H + H * da);
+  const double bytes = eb * groups * (static_cast<double>(B) * Hn + static_cast<double>(Hn) * H) +
+                       4.0 * groups * (B * ((H + 31) / 32) + H * da + 2.0 * B * da);
+  timed(PC_GEMM_DX, flops, bytes, active != nullptr,
+        [&] { launch_tc_gemm(A, Bw, false, false, a, stream); });
+  return true;
+}
+
 // Twin critics as one grouped problem of 2n groups: forward on [s|a], MSE cotangent,
 // backward, fused Adam + target Polyak (algos.hpp:369-377, :401-418).
-void Pop::critic_update(int B, const int* polyak_gate) {
+void Pop::critic_forward(int B) {
+  const Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
+  mlp_forward(cri, cri_p.p, 2 * n, B, x0, S.ch, S.q.p, B, 1, EPI_BIAS);
+}
+
+void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
   const int n2 = 2 * n;
   Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
   if (use_tc() && lsa > ds + da) x0.ones_col = ds + da;  // see Pop::ensure_ones
-  mlp_forward(cri, cri_p.p, n2, B, x0, S.ch, S.q.p, B, 1, EPI_BIAS);
+  if (!forward_done) critic_forward(B);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
   mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr);
   const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
@@ -667,23 +729,82 @@ void Pop::critic_update(int B, const int* polyak_gate) {
 }
 
 // ------------------------------------------------------------------ TD3 step (algos.hpp:351-422)
+// Graph capture: append an IF node on `h` at the current capture point of `stream` and capture
+// body() into its body graph (on cap, a stream of its own).
+template <typename F>
+void Pop::capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body) {
+  cudaStreamCaptureStatus st;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CUDA_CHECK(cudaStreamGetCaptureInfo_v3(stream, &st, nullptr, &g, &deps, nullptr, &nd));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CUDA_CHECK(cudaGraphAddNode(&node, g, deps, nd, &cp));
+  CUDA_CHECK(cudaStreamUpdateCaptureDependencies(stream, &node, 1,
+                                                 cudaStreamSetCaptureDependencies));
+  if (!cap) CUDA_CHECK(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+  cudaGraph_t bg = cp.conditional.phGraph_out[0];
+  CUDA_CHECK(cudaStreamBeginCaptureToGraph(cap, bg, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeThreadLocal));
+  std::swap(stream, cap);
+  try {
+    body();
+  } catch (...) {
+    std::swap(stream, cap);
+    cudaStreamEndCapture(cap, &bg);
+    throw;
+  }
+  std::swap(stream, cap);
+  CUDA_CHECK(cudaStreamEndCapture(cap, &bg));
+  size_t nb = 0;
+  CUDA_CHECK(cudaGraphGetNodes(bg, nullptr, &nb));
+  cond_body_nodes += nb;
+  ++cond_nodes;
+}
+
 void Pop::td3_step(int B, const uint8_t* d_mask) {
   const long long nbB = B;
-  // graph capture: the policy half below becomes the body of a conditional IF node whose
-  // condition k_td3_step_begin sets when any member fires (steps where no policy fires replay
-  // only the critic half); eager mode runs it with every launch gated per member instead
-  cudaGraphConditionalHandle any_fire = 0;
+  // graph capture: the policy half of the step sits in conditional IF nodes whose condition
+  // k_td3_step_begin sets when any member fires (steps where no policy fires replay only the
+  // critic half); eager mode runs it with every launch gated per member instead
+  const bool fork = capturing && use_tc();
+  // PBRL_PFORK=1: policy forward on a parallel conditional branch (measured neutral on B200)
+  static const bool pfork = std::getenv("PBRL_PFORK") != nullptr;
+  cudaGraphConditionalHandle any_fire = 0, any_fire_fwd = 0;
   if (capturing) {
     cudaStreamCaptureStatus st;
     cudaGraph_t g = nullptr;
     CUDA_CHECK(cudaStreamGetCaptureInfo(stream, &st, nullptr, &g, nullptr, nullptr));
     CUDA_CHECK(cudaGraphConditionalHandleCreate(&any_fire, g, 0, cudaGraphCondAssignDefault));
+    if (fork && pfork)
+      CUDA_CHECK(
+          cudaGraphConditionalHandleCreate(&any_fire_fwd, g, 0, cudaGraphCondAssignDefault));
   }
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p, t_cri.p + n,
                           steps.p, streams.p, seed, key_a.p, losses.p + 2 * n, any_fire,
-                          capturing ? 1 : 0, stream);
+                          any_fire_fwd, capturing ? (fork && pfork ? 2 : 1) : 0, stream);
   });
+  // graph mode: the online critics' forward on [s | a] does not depend on the target chain, so
+  // it runs on a parallel graph branch (its tiles fill the target chain's partial waves)
+  if (fork) {
+    if (!side2) CUDA_CHECK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+    if (!ev_fork) {
+      for (cudaEvent_t* e : {&ev_fork, &ev_join, &ev_pfork, &ev_pjoin})
+        CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    CUDA_CHECK(cudaEventRecord(ev_fork, stream));
+    CUDA_CHECK(cudaStreamWaitEvent(side2, ev_fork, 0));
+    std::swap(stream, side2);
+    critic_forward(B);
+    std::swap(stream, side2);
+    CUDA_CHECK(cudaEventRecord(ev_join, side2));
+  }
   // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
   if (use_tc()) {
     timed(PC_ELEM, 0.0, 0.0, 0, [&] {
@@ -697,52 +818,37 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
               nbB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
   timed(PC_ELEM, 0.0, 0.0, 0,
         [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
-  // twin critic update; target Polyak fused for members whose policy fires
-  critic_update(B, fire.p);
-  if (capturing) {
-    cudaStreamCaptureStatus st;
-    cudaGraph_t g = nullptr;
-    const cudaGraphNode_t* deps = nullptr;
-    size_t nd = 0;
-    CUDA_CHECK(cudaStreamGetCaptureInfo_v3(stream, &st, nullptr, &g, &deps, nullptr, &nd));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = any_fire;
-    cp.conditional.type = cudaGraphCondTypeIf;
-    cp.conditional.size = 1;
-    cudaGraphNode_t node;
-    CUDA_CHECK(cudaGraphAddNode(&node, g, deps, nd, &cp));
-    CUDA_CHECK(cudaStreamUpdateCaptureDependencies(stream, &node, 1,
-                                                   cudaStreamSetCaptureDependencies));
-    if (!side) CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    CUDA_CHECK(cudaStreamBeginCaptureToGraph(side, body, nullptr, nullptr, 0,
-                                             cudaStreamCaptureModeThreadLocal));
-    std::swap(stream, side);
-    try {
-      td3_policy_half(B);
-    } catch (...) {
-      std::swap(stream, side);
-      cudaStreamEndCapture(side, &body);
-      throw;
-    }
-    std::swap(stream, side);
-    CUDA_CHECK(cudaStreamEndCapture(side, &body));
-    size_t nb = 0;
-    CUDA_CHECK(cudaGraphGetNodes(body, nullptr, &nb));
-    cond_body_nodes += nb;
-  } else {
-    td3_policy_half(B);
+  if (fork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
+  if (fork && pfork) {
+    // the policy forward pi(s) reads only the batch and the (not yet updated) policy: a second
+    // conditional branch overlaps it with the critic backward and Adam
+    CUDA_CHECK(cudaEventRecord(ev_pfork, stream));
+    CUDA_CHECK(cudaStreamWaitEvent(side2, ev_pfork, 0));
+    std::swap(stream, side2);
+    capture_if(any_fire_fwd, side3, [&] { td3_policy_forward(B); });
+    std::swap(stream, side2);
+    CUDA_CHECK(cudaEventRecord(ev_pjoin, side2));
   }
+  // twin critic update; target Polyak fused for members whose policy fires
+  critic_update(B, fire.p, fork);
+  if (fork && pfork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_pjoin, 0));
+  if (capturing) capture_if(any_fire, side, [&] { td3_policy_half(B, fork && pfork); });
+  else td3_policy_half(B, false);
 }
 
-// td3_policy_loss_grads (:318-338) on the UPDATED critic1, policy Adam and the target Polyak,
-// every launch gated by the fire mask
-void Pop::td3_policy_half(int B) {
+void Pop::td3_policy_forward(int B) {
   const long long nbB = B;
   const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
   mlp_forward(pol, pol_p.p, n, B, s, S.ph, aoff(S.sa_pi.p, ds), nbB * lsa, lsa, EPI_BIAS_TANH,
               fire.p, S.pt.p, nbB * da, da, false, true, true);
+}
+
+// td3_policy_loss_grads (:318-338) on the UPDATED critic1, policy Adam and the target Polyak,
+// every launch gated by the fire mask
+void Pop::td3_policy_half(int B, bool forward_done) {
+  const long long nbB = B;
+  const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
+  if (!forward_done) td3_policy_forward(B);
   mlp_forward(cri, cri_p.p, n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 0}, S.qh, S.qpi.p, nbB, 1,
               EPI_BIAS, fire.p);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
@@ -844,6 +950,7 @@ void Pop::step(int B, const uint8_t* d_mask) {
       cudaGraph_t graph;
       capturing = true;
       cond_body_nodes = 0;
+      cond_nodes = 0;
       CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
       try {
         run_program(B, d_mask);
@@ -857,7 +964,7 @@ void Pop::step(int B, const uint8_t* d_mask) {
       size_t nodes = 0;
       CUDA_CHECK(cudaGraphGetNodes(graph, nullptr, &nodes));
       // kernel nodes: the conditional node stands for its body (the policy half)
-      g.nodes = nodes + cond_body_nodes - (cond_body_nodes ? 1 : 0);
+      g.nodes = nodes + cond_body_nodes - cond_nodes;
       CUDA_CHECK(cudaGraphInstantiate(&g.exec, graph, 0));
       CUDA_CHECK(cudaGraphDestroy(graph));
       graphs.push_back(g);

@@ -480,7 +480,16 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
       };
       const float* bias = g.bias ? g.bias + grp * g.bias_gs : nullptr;
       const float* aux = g.aux ? g.aux + xg * g.aux_gs : nullptr;
-      if (need_bias) {
+      if (nout > 0 && g.ow_tr) {
+        // dX variant: gather the transposed output-layer weights (a few KB) into fz_w
+        epi_bar_sync();
+        const float* wsrc = g.ow + grp * g.ow_gs;
+        for (int e = threadIdx.x - 64; e < BN * nout; e += kEpiThreads) {
+          const int j = e / nout, o = e - j * nout;
+          fz_w[e] = j < g.N ? __ldg(wsrc + o * g.ow_ld + j) : 0.0f;
+        }
+        epi_bar_sync();
+      } else if (need_bias) {
         // stage this tile's bias (and output-layer weights) once the previous tile is consumed:
         // one bulk copy issued before waiting for the accumulator, so it overlaps the MMAs
         epi_bar_sync();
@@ -538,7 +547,7 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
             noisy ? g.noise_eps + grp * g.ne_gs + static_cast<long long>(row) * g.ne_rs : nullptr;
 #pragma unroll
         for (int o = 0; o < NA; ++o) {
-          ob[o] = o < nout ? __ldg(obg + o) : 0.0f;
+          ob[o] = (o < nout && !g.ow_tr) ? __ldg(obg + o) : 0.0f;
           ep[o] = (noisy && o < nout) ? __ldg(eg + o) : 0.0f;
         }
       }
@@ -607,16 +616,34 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
               tmem_ld32(tacc + static_cast<uint32_t>(c0 + CW), v[(ci + 1) & 1]);
           }
           if (!half_active || c0 >= g.N) continue;
+          if (mask_bits) {  // dX variant: relu'(h_below) from the mask bits
+            uint32_t bits = 0u;
 #pragma unroll
-          for (int j = 0; j < CW; ++j) {
-            const float z = cur[j] + fz_bias[c0 + j];
-            const float h = (c0 + j < g.N && z > 0.0f) ? z : 0.0f;
-            cur[j] = h;
-            const float* wr = fz_w + (c0 + j) * nout;
+            for (int k = 0; k < MW; ++k)
+              if (k == cbeg + ci) bits = mw[k];
 #pragma unroll
-            for (int o = 0; o < NA; ++o) {
-              if (NO == 16 && o >= nout) break;
-              oacc[o] = oacc[o] + h * wr[o];
+            for (int j = 0; j < CW; ++j) {
+              const float h = ((bits >> j) & 1u) ? cur[j] : 0.0f;
+              cur[j] = h;
+              const float* wr = fz_w + (c0 + j) * nout;
+#pragma unroll
+              for (int o = 0; o < NA; ++o) {
+                if (NO == 16 && o >= nout) break;
+                oacc[o] = oacc[o] + h * wr[o];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+              const float z = cur[j] + fz_bias[c0 + j];
+              const float h = (c0 + j < g.N && z > 0.0f) ? z : 0.0f;
+              cur[j] = h;
+              const float* wr = fz_w + (c0 + j) * nout;
+#pragma unroll
+              for (int o = 0; o < NA; ++o) {
+                if (NO == 16 && o >= nout) break;
+                oacc[o] = oacc[o] + h * wr[o];
+              }
             }
           }
           if (g.store_hidden) {
@@ -639,12 +666,18 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
         if (hf == 0 && row < g.M) {
           const long long obase = grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
           const bool tanh_out = g.out_epi == EPI_BIAS_TANH || g.out_epi == EPI_BIAS_TANH_NOISE;
+          const float* arow = (g.out_epi == EPI_TANH_GRAD && aux)
+                                  ? aux + static_cast<long long>(row) * g.aux_rs : nullptr;
 #pragma unroll
           for (int o = 0; o < NA; ++o) {
             if (o >= nout) break;
             const float y = (oacc[o] + os[o]) + ob[o];
             float r = y;
-            if (tanh_out) {
+            if (arow) {  // tanh backward of the policy head (activation_backward, tanh)
+              const float gy = (g.scale != 1.0f) ? y * g.scale : y;
+              const float th = arow[o];
+              r = gy * (1.0f - th * th);
+            } else if (tanh_out) {
               const float th = epi_tanhf(y);
               if (g.oC2) g.oC2[grp * g.oc2_gs + static_cast<long long>(row) * g.oc2_rs + o] = th;
               r = (g.out_scale != 1.0f) ? th * g.out_scale : th;
@@ -1256,7 +1289,7 @@ void launch_tpl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
 template <bool A_MN, bool B_MN, int EB>
 void launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                const CUtensorMap& x, const TcArgs& g, cudaStream_t s) {
-  if (g.nout > 0) {  // fused output layer: forward GEMMs only (K-major A, MN-major B)
+  if (g.nout > 0) {  // fused output layer: forward (K-major A, MN-major B) or dX (K / K)
     if constexpr (!A_MN && B_MN) {
       if (bn == 256) {
         switch (g.nout) {
@@ -1265,6 +1298,13 @@ void launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtenso
           case 12: launch_tpl<256, false, true, 12, EB>(a, b, c, x, g, s); return;
           default: launch_tpl<256, false, true, 16, EB>(a, b, c, x, g, s); return;
         }
+      }
+    }
+    if constexpr (!A_MN && !B_MN) {
+      if (bn == 256) {
+        if (g.nout == 6) launch_tpl<256, false, false, 6, EB>(a, b, c, x, g, s);
+        else launch_tpl<256, false, false, 16, EB>(a, b, c, x, g, s);
+        return;
       }
     }
     PBRL_THROW(PBRL_E_USAGE, "tc_gemm: fused output layer needs the 256-wide forward tile");
@@ -1400,6 +1440,8 @@ void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn
                    g.aux_gs, 32, 32, SWZ_128);
   if (g.nout > 0 && g.store_hidden && !g.c_tma)
     PBRL_THROW(PBRL_E_USAGE, "tc_gemm: fused output layer needs a TMA-legal hidden buffer");
+  if (g.nout > 0 && g.ow_tr && !g.mask_in)
+    PBRL_THROW(PBRL_E_USAGE, "tc_gemm: fused dX output needs the ReLU mask bits");
   if (eb == 2 && g.epi == EPI_RELU_MASK && !g.mask_in)
     PBRL_THROW(PBRL_E_USAGE, "tc_gemm: bf16 ReLU' epilogues need the mask bits");
   if (eb == 4) {

@@ -52,6 +52,12 @@ struct TcArgs {
   long long oc2_gs = 0, oc2_rs = 0;
   float out_scale = 1.0f;
   int store_hidden = 1;
+  // dX variant of the fused output layer (the policy-loss chain's last critic dX straight into
+  // the action columns): hidden = ReLU'-masked accumulator (mask bits, no bias), output-layer
+  // weights read transposed, w(j, o) = ow[g * ow_gs + o * ow_ld + j], no output bias; out_epi
+  // EPI_TANH_GRAD (aux = tanh values, scale) or EPI_STORE
+  int ow_tr = 0;
+  long long ow_ld = 0;
   // ReLU masks as bits: a storing BIAS_RELU / fused epilogue writes bit (c % 32) of word c / 32
   // of row r = (h[r][c] > 0) to mask_out; EPI_RELU_MASK reads mask_in (when set) instead of aux
   uint32_t* mask_out = nullptr;
