@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
   float* Gs = sm;                         // [B][nout]
   float* Ps = Gs + B * nout;              // [kObSlices][kObCols][nout] dW partials
   float* Cs = Ps + kObSlices * kObCols * nout;  // [kObSlices][kObCols] dX column sums
+  float* Ls = Cs + kObSlices * kObCols;          // [B] loss terms (fused top cotangent)
   const int grp = blockIdx.y;
   const int mem = grp % a.n_members;
   if (a.active && !a.active[mem]) return;
@@ -320,11 +321,34 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
   const int col = threadIdx.x % kObCols, sl = threadIdx.x / kObCols;
   const int i = blockIdx.x * kObCols + col;
   const AT* X = static_cast<const AT*>(a.X) + (a.x_by_member ? mem : grp) * a.x_gs;
-  const float* G = a.G + grp * a.g_gs;
   const float* W = a.W + grp * a.w_gs;
-  for (int e = threadIdx.x; e < B * nout; e += blockDim.x) {
-    const int b = e / nout, o = e - b * nout;
-    Gs[e] = G[static_cast<long long>(b) * a.g_ld + o];
+  if (a.top) {  // nout == 1: the top cotangent from the network output (see OutBwdArgs::top)
+    const float* qg = a.q + static_cast<long long>(grp) * B;
+    const long long mb = static_cast<long long>(mem) * B;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+      const float qv = qg[b];
+      if (a.top == 3) {
+        Gs[b] = -1.0f / static_cast<float>(B);
+        Ls[b] = qv;
+      } else {
+        float yv;
+        if (a.top == 1) {
+          const float qmin = minf_ref(a.tq[mb + b], a.tq[static_cast<long long>(a.n_members) * B + mb + b]);
+          yv = a.r[mb + b] + a.gamma[mem] * (1.0f - a.d[mb + b]) * qmin;
+        } else {
+          yv = a.y[mb + b];
+        }
+        const float dl = qv - yv;
+        Gs[b] = (2.0f / static_cast<float>(B)) * dl;
+        Ls[b] = dl;
+      }
+    }
+  } else {
+    const float* G = a.G + grp * a.g_gs;
+    for (int e = threadIdx.x; e < B * nout; e += blockDim.x) {
+      const int b = e / nout, o = e - b * nout;
+      Gs[e] = G[static_cast<long long>(b) * a.g_ld + o];
+    }
   }
   float w[NA], acc[NA];
 #pragma unroll
@@ -388,6 +412,15 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
       db[i] = csum;
     }
   }
+  if (a.top && a.loss && blockIdx.x == 0 && threadIdx.x == 0) {  // row order, double
+    double acc = 0.0;
+    if (a.top == 3) {
+      for (int b = 0; b < B; ++b) acc -= static_cast<double>(Ls[b]);
+    } else {
+      for (int b = 0; b < B; ++b) acc += static_cast<double>(Ls[b]) * static_cast<double>(Ls[b]);
+    }
+    a.loss[grp] = acc / static_cast<double>(B);
+  }
   if (!a.dW) return;
   float* dW = a.dW + grp * a.dw_gs;
   if (slices > 1) {
@@ -431,7 +464,7 @@ template <int NO, typename AT>
 static void launch_ob(const OutBwdArgs& a, cudaStream_t s) {
   const int slices = a.exact ? 1 : kObSlices;
   const size_t smem =
-      (static_cast<size_t>(a.B) * a.nout + kObSlices * kObCols * (a.nout + 1)) * 4;
+      (static_cast<size_t>(a.B) * (a.nout + 1) + kObSlices * kObCols * (a.nout + 1)) * 4;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_out_backward<NO, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,

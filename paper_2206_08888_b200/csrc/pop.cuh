@@ -147,6 +147,15 @@ struct OutBwdArgs {
   long long dx_gs = 0, dx_ld = 0;
   float* dbx = nullptr;      // optional: column sums of dX = the bias gradient of the layer below
   long long dbx_gs = 0;
+  // nout == 1 only: the cotangent G computed in the kernel from the network output q [groups][B]
+  //   top 1: TD3 critic, dq = (2/B)(q - y), y = r + gamma (1 - d) min(tq1, tq2) (td3_critic_target
+  //          + mse_loss_grads, algos.hpp:268-307); loss[grp] = sum_b (q - y)^2 / B (double)
+  //   top 2: critic with a given TD target y [members][B] (SAC)
+  //   top 3: TD3 policy loss through critic 1, dq = -1/B; loss[grp] = -sum_b q / B
+  int top = 0;
+  const float* q = nullptr;
+  const float *r = nullptr, *d = nullptr, *tq = nullptr, *gamma = nullptr, *y = nullptr;
+  double* loss = nullptr;
   const int* active = nullptr;
   int exact = 1;  // 1: reference summation order (FFMA32); 0: warp-parallel tree (TF32)
 };

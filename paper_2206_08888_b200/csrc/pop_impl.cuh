@@ -242,10 +242,11 @@ struct Pop {
                       bool out_act);
   void mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
                     Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
-                    const int* active);
+                    const int* active, const OutBwdArgs* top = nullptr);
   void critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>& hs,
                            std::vector<DBuf<float>>& dhs, float* out, long long out_ld, int epi,
-                           Mat aux, float scale, const int* active);
+                           Mat aux, float scale, const int* active,
+                           const OutBwdArgs* top = nullptr);
   void critic_forward(int B);
   bool gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long long out_ld, int epi,
                          Mat aux, float scale, const int* active);

@@ -533,7 +533,7 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
 // backward of `sh` from the top cotangent G: dW for every layer, dX for layers > 0
 void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
                        Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
-                       const int* active) {
+                       const int* active, const OutBwdArgs* top) {
   const int L = sh.depth;
   bool bias_done = false;  // the bias gradient of layer l was produced with its cotangent
   for (int l = L - 1; l >= 0; --l) {
@@ -561,6 +561,16 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       a.dw_gs = static_cast<long long>(sh.stride);
       a.active = active;
       a.exact = use_tc() ? 0 : 1;
+      if (top && top->top) {  // top cotangent (TD target / MSE / losses) fused into this launch
+        a.top = top->top;
+        a.q = top->q;
+        a.r = top->r;
+        a.d = top->d;
+        a.tq = top->tq;
+        a.gamma = top->gamma;
+        a.y = top->y;
+        a.loss = top->loss;
+      }
       Mat dh{};
       if (l > 0) {
         dh = hid(dhs, l - 1, B, sh, 0);
@@ -600,7 +610,7 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
 // critic dX chain from the output cotangent down to the action columns of the input
 void Pop::critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>& hs,
                               std::vector<DBuf<float>>& dhs, float* out, long long out_ld,
-                              int epi, Mat aux, float scale, const int* active) {
+                              int epi, Mat aux, float scale, const int* active, const OutBwdArgs* top) {
   const int L = cri.depth;
   for (int l = L - 1; l >= 1; --l) {
     const Mat mask = hid(hs, l - 1, B, cri, 0);
@@ -631,6 +641,11 @@ void Pop::critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>
       a.dx_ld = dh.ld;
       a.active = active;
       a.exact = 0;
+      if (top && top->top) {
+        a.top = top->top;
+        a.q = top->q;
+        a.loss = top->loss;
+      }
       const double obytes = 4.0 * groups *
           (static_cast<double>(B) * a.nout + H * a.nout) + 2.0 * aeb() * groups * B * H;
       timed(PC_GEMM_DX, 2.0 * B * H * a.nout * groups, obytes, active != nullptr,
@@ -713,8 +728,24 @@ void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
   Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
   if (use_tc() && lsa > ds + da) x0.ones_col = ds + da;  // see Pop::ensure_ones
   if (!forward_done) critic_forward(B);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
-  mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr);
+  // tensor-core modes: the TD target (TD3) and mse_loss_grads run inside the output-layer
+  // backward; FFMA32 keeps the separate kernels (the reference's operation order)
+  OutBwdArgs top;
+  if (use_tc() && cri.dims[cri.depth] == 1 && B <= 32768) {
+    top.top = algo == PBRL_ALGO_TD3 ? 1 : 2;
+    top.q = S.q.p;
+    top.r = S.r.p;
+    top.d = S.d.p;
+    top.tq = S.tq_out.p;
+    top.gamma = h_f4.p;
+    top.y = S.y.p;
+    top.loss = losses.p;
+  } else {
+    timed(PC_ELEM, 0.0, 0.0, 0,
+          [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
+  }
+  mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr,
+               &top);
   const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
   // 28 B/param Adam (+2 B/param bf16 operand copy in BF16 mode)
   timed(PC_ADAM, 0.0, static_cast<double>(cri.P) * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
@@ -816,8 +847,9 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
               EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true, false, true);
   mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
               nbB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
-  timed(PC_ELEM, 0.0, 0.0, 0,
-        [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
+  if (!(use_tc() && cri.dims[cri.depth] == 1 && B <= 32768))  // else fused (critic_update)
+    timed(PC_ELEM, 0.0, 0.0, 0,
+          [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
   if (fork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
   if (fork && pfork) {
     // the policy forward pi(s) reads only the batch and the (not yet updated) policy: a second
@@ -851,12 +883,19 @@ void Pop::td3_policy_half(int B, bool forward_done) {
   if (!forward_done) td3_policy_forward(B);
   mlp_forward(cri, cri_p.p, n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 0}, S.qh, S.qpi.p, nbB, 1,
               EPI_BIAS, fire.p);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
-    launch_td3_policy_loss(n, B, S.qpi.p, fire.p, losses.p + 2 * n, S.gq.p, stream);
-  });
+  OutBwdArgs top;
+  if (use_tc() && cri.dims[cri.depth] == 1 && B <= 32768) {  // fused: critic output-layer dX
+    top.top = 3;
+    top.q = S.qpi.p;
+    top.loss = losses.p + 2 * n;
+  } else {
+    timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+      launch_td3_policy_loss(n, B, S.qpi.p, fire.p, losses.p + 2 * n, S.gq.p, stream);
+    });
+  }
   const int lt = pad4(da);
   critic_dx_to_action(n, B, Mat{S.gq.p, nbB, 1, 0}, S.qh, S.qdh, S.gtop.p, lt, EPI_TANH_GRAD,
-                      Mat{S.pt.p, nbB * da, da, 0}, pol.out_scale, fire.p);
+                      Mat{S.pt.p, nbB * da, da, 0}, pol.out_scale, fire.p, &top);
   mlp_backward(pol, pol_p.p, pol_g.p, n, B, Mat{S.gtop.p, nbB * lt, lt, 0}, s, S.ph, S.pdh,
                fire.p);
   timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * (act16() ? 40.0 : 36.0), 1, [&] {
