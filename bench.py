@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="D", choices=sorted(CONFIGS))
     ap.add_argument("--pop", type=int, default=None, help="override the total population")
-    ap.add_argument("--precision", default=os.environ.get("PBRL_PRECISION", "tf32"),
+    ap.add_argument("--precision", default=os.environ.get("PBRL_PRECISION", "bf16"),
                     choices=["ffma32", "bf16", "tf32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

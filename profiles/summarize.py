@@ -19,7 +19,7 @@ from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
 
-CLASS = [("k_tc_gemm", "gemm (tcgen05)"), ("k_gemm_simt", "gemm (cuda-core)"),
+CLASS = [("k_mlp_fwd2", "gemm (tcgen05, fused 2-layer forward)"), ("k_tc_gemm", "gemm (tcgen05)"), ("k_gemm_simt", "gemm (cuda-core)"),
          ("k_out_backward", "output-layer backward"), ("k_fwd_skinny", "output-layer fwd"),
          ("k_dx_skinny", "dX skinny"), ("k_adam", "adam_polyak"), ("k_colsum", "bias grad"),
          ("k_replay_gather", "gather_pack"), ("k_pack_batch", "gather_pack")]
@@ -113,9 +113,9 @@ def main():
     for r in reps:
         traffic.update(full(r, tag))
     prec = "bf16" if "bf16" in tag else ("tf32" if "tf32" in tag else "ffma32")
-    cls_map = {"gemm_fwd": "k_tc_gemm", "adam_polyak": "k_adam"}
-    out = {c: next((v for k, v in traffic.items() if k.startswith(kn)), None)
-           for c, kn in cls_map.items()}
+    cls_map = {"gemm_fwd": ("k_mlp_fwd2", "k_tc_gemm"), "adam_polyak": ("k_adam",)}
+    out = {c: next((v for kn in kns for k, v in traffic.items() if k.startswith(kn)), None)
+           for c, kns in cls_map.items()}
     out["_note"] = "DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) from one ncu --set full capture"
     (HERE / f"traffic_{prec}_D.json").write_text(json.dumps(out, indent=1))
     print("wrote", sorted(p.name for p in HERE.glob(f"{tag}_*")))

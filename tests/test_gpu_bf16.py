@@ -88,3 +88,15 @@ def test_bf16_deterministic(pb, ora):
         pb.td3_update_step(b, to_batch(pb, raw, k), hy)
     for net in TD3_NETS:
         assert np.array_equal(a.params(net), b.params(net))
+
+
+@pytest.mark.parametrize("algo,hidden", [("td3", [128, 96]), ("sac", [128, 128]),
+                                         ("td3", [256, 64])])
+def test_bf16_fused_forward_hidden_shapes(pb, ora, algo, hidden):
+    """The fused two-layer forward (k_mlp_fwd2) at hidden widths other than 256: 128-wide
+    layer 1 (two K chunks), layer-2 widths that leave TMEM columns / epilogue chunks unused."""
+    lerr, werr = _compare(pb, ora, algo, 3, hidden, 128, 4, seed=5, precision="bf16")
+    print(f"\n{algo} bf16 {hidden}: loss {lerr.max():.4f} deltas {werr}")
+    assert lerr.max() <= LOSS_TOL
+    for net, e in werr.items():
+        assert e <= DELTA_TOL, (net, e)

@@ -1,23 +1,21 @@
 #!/bin/bash
-# Round evidence on one B200: GPU tests, bench lines (tf32 + bf16), ncu launch lists and one
-# `ncu --set full` capture of the forward GEMM launches of one step per precision.
+# Round evidence on one B200: GPU tests, bench lines (bf16 default + tf32), the reference arm,
+# ncu launch lists (eager replay) and `ncu --set full` captures of the top kernels.
 set -u
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
-for P in tf32 bf16; do
-  timeout 300 python bench.py --precision $P > gpurun_out/bench_$P.json 2> gpurun_out/bench_$P.err
-  head -c 400 gpurun_out/bench_$P.json; echo
-  timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python bench.py > gpurun_out/bench_bf16.json 2> gpurun_out/bench_bf16.err; head -c 300 gpurun_out/bench_bf16.json; echo
+timeout 300 python bench.py --precision tf32 --no-cpu-baseline > gpurun_out/bench_tf32.json 2> gpurun_out/bench_tf32.err; head -c 300 gpurun_out/bench_tf32.json; echo
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1; tail -1 gpurun_out/bench_ref.json | head -c 200; echo
+for P in bf16 tf32; do
+  PBRL_NO_GRAPH=1 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_$P.csv python bench.py --precision $P --steps 4 --warmup 3 \
     --no-cpu-baseline --no-e2e > /dev/null 2>&1
-  PBRL_NO_GRAPH=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_tc_gemm \
-    --launch-skip 60 --launch-count 10 -o gpurun_out/full_gemm_$P -f python bench.py --precision $P \
-    --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_$P.log 2>&1
-  tail -2 gpurun_out/ncu_full_$P.log
-  PBRL_NO_GRAPH=1 timeout 300 ncu --set full --clock-control none -k regex:k_adam --launch-skip 6 --launch-count 2 \
-    -o gpurun_out/full_adam_$P -f python bench.py --precision $P --steps 2 --warmup 3 \
-    --no-cpu-baseline --no-e2e > /dev/null 2>&1
 done
-timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1
-tail -1 gpurun_out/bench_ref.json | head -c 300; echo
+# one full capture per top kernel class (bf16): fused forward, dW GEMM, dX GEMM, Adam, output backward
+PBRL_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:"k_mlp_fwd2|k_tc_gemm|k_adam|k_out_backward" --launch-skip 60 --launch-count 24 \
+  -o gpurun_out/full_bf16 -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
+  > gpurun_out/ncu_full_bf16.log 2>&1
+tail -2 gpurun_out/ncu_full_bf16.log
 ls gpurun_out
