@@ -460,8 +460,203 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
   }
 }
 
+// Tensor-core modes: the same pass with 4 adjacent columns per thread (one 8-byte bf16x4 or
+// 16-byte fp32x4 load / store per row instead of four scalar ones), 64 columns x 16 row slices
+// per block (enough blocks and loads in flight to cover HBM latency); slices combined in slice
+// order (deterministic).  Requires H % 4 == 0 and 4-element
+// aligned rows (launch_out_backward checks and otherwise uses k_out_backward).
+constexpr int kOvQuads = 16, kOvSlices = 16;  // 64 columns x 16 row slices per block
+
+template <typename AT> struct Vec4;
+template <> struct Vec4<float> {
+  __device__ static void ld(const float* p, float* v) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
+  }
+  __device__ static void st(float* p, const float* v) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <> struct Vec4<__nv_bfloat16> {
+  __device__ static void ld(const __nv_bfloat16* p, float* v) {
+    const uint2 u = *reinterpret_cast<const uint2*>(p);
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+  __device__ static void st(__nv_bfloat16* p, const float* v) {
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v[0], v[1]);
+    const __nv_bfloat162 b = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<const uint32_t*>(&a);
+    u.y = *reinterpret_cast<const uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(p) = u;
+  }
+};
+
+template <int NO, typename AT>
+__global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdArgs a) {
+  PDL_ENTRY();
+  extern __shared__ float sm[];
+  constexpr int NA = NO, CB = 4 * kOvQuads;  // columns per block
+  const int nout = NO < 16 ? NO : a.nout, B = a.B;
+  float* Gs = sm;                                // [B][nout]
+  float* Ls = Gs + B * nout;                     // [B]
+  float* Ps = Ls + B;                            // [kOvSlices][CB][nout]
+  float* Cs = Ps + kOvSlices * CB * nout;        // [kOvSlices][CB]
+  const int grp = blockIdx.y;
+  const int mem = grp % a.n_members;
+  if (a.active && !a.active[mem]) return;
+  const int cq = threadIdx.x % kOvQuads, sl = threadIdx.x / kOvQuads;
+  const int c0 = blockIdx.x * CB + 4 * cq;  // first of this thread's 4 columns
+  const bool live = c0 < a.H;
+  const AT* X = static_cast<const AT*>(a.X) + (a.x_by_member ? mem : grp) * a.x_gs;
+  const float* W = a.W + grp * a.w_gs;
+  if (a.top) {
+    const float* qg = a.q + static_cast<long long>(grp) * B;
+    const long long mb = static_cast<long long>(mem) * B;
+    for (int b = threadIdx.x; b < B; b += blockDim.x) {
+      const float qv = qg[b];
+      if (a.top == 3) {
+        Gs[b] = -1.0f / static_cast<float>(B);
+        Ls[b] = qv;
+      } else {
+        float yv;
+        if (a.top == 1) {
+          const float qmin =
+              minf_ref(a.tq[mb + b], a.tq[static_cast<long long>(a.n_members) * B + mb + b]);
+          yv = a.r[mb + b] + a.gamma[mem] * (1.0f - a.d[mb + b]) * qmin;
+        } else {
+          yv = a.y[mb + b];
+        }
+        const float dl = qv - yv;
+        Gs[b] = (2.0f / static_cast<float>(B)) * dl;
+        Ls[b] = dl;
+      }
+    }
+  } else {
+    const float* G = a.G + grp * a.g_gs;
+    for (int e = threadIdx.x; e < B * nout; e += blockDim.x) {
+      const int b = e / nout, o = e - b * nout;
+      Gs[e] = G[static_cast<long long>(b) * a.g_ld + o];
+    }
+  }
+  float w[4][NA], acc[4][NA], csum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int o = 0; o < NA; ++o) {
+      acc[c][o] = 0.0f;
+      w[c][o] = (live && o < nout) ? W[static_cast<long long>(c0 + c) * nout + o] : 0.0f;
+    }
+  __syncthreads();
+  const int rows = (B + kOvSlices - 1) / kOvSlices;
+  const int b0 = sl * rows, b1 = min(B, b0 + rows);
+  AT* dX = a.dX ? static_cast<AT*>(a.dX) + grp * a.dx_gs : nullptr;
+  if (live) {
+    constexpr int U = 8;
+    for (int b = b0; b < b1; b += U) {
+      float xv[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (b + u < b1) Vec4<AT>::ld(X + static_cast<long long>(b + u) * a.x_ld + c0, xv[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (b + u >= b1) break;
+        const float* g = Gs + (b + u) * nout;
+        float dv[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float d = 0.0f;
+#pragma unroll
+          for (int o = 0; o < NA; ++o) {
+            if (NO == 16 && o >= nout) break;
+            acc[c][o] = acc[c][o] + xv[u][c] * g[o];
+            d = d + g[o] * w[c][o];
+          }
+          dv[c] = xv[u][c] > 0.0f ? d : 0.0f;
+          csum[c] = csum[c] + dv[c];
+        }
+        if (dX) Vec4<AT>::st(dX + static_cast<long long>(b + u) * a.dx_ld + c0, dv);
+      }
+    }
+  }
+  if (a.dbx) {  // fused bias gradient of the layer below
+#pragma unroll
+    for (int c = 0; c < 4; ++c) Cs[sl * CB + 4 * cq + c] = csum[c];
+    __syncthreads();
+    for (int cc = threadIdx.x; cc < CB; cc += blockDim.x) {
+      const int col = blockIdx.x * CB + cc;
+      if (col >= a.H) continue;
+      float t = Cs[cc];
+      for (int q = 1; q < kOvSlices; ++q) t += Cs[q * CB + cc];
+      a.dbx[grp * a.dbx_gs + col] = t;
+    }
+  }
+  if (a.top && a.loss && blockIdx.x == 0 && threadIdx.x == 0) {  // row order, double
+    double s = 0.0;
+    if (a.top == 3) {
+      for (int b = 0; b < B; ++b) s -= static_cast<double>(Ls[b]);
+    } else {
+      for (int b = 0; b < B; ++b) s += static_cast<double>(Ls[b]) * static_cast<double>(Ls[b]);
+    }
+    a.loss[grp] = s / static_cast<double>(B);
+  }
+  if (!a.dW) return;
+  float* dW = a.dW + grp * a.dw_gs;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int o = 0; o < NA; ++o)
+      if (o < nout) Ps[(sl * CB + 4 * cq + c) * nout + o] = acc[c][o];
+  __syncthreads();
+  for (int e = threadIdx.x; e < CB * nout; e += blockDim.x) {
+    const int cc = e / nout, o = e - cc * nout;
+    const int col = blockIdx.x * CB + cc;
+    if (col >= a.H) continue;
+    float t = Ps[cc * nout + o];
+    for (int q = 1; q < kOvSlices; ++q) t += Ps[(q * CB + cc) * nout + o];
+    dW[static_cast<long long>(col) * nout + o] = t;
+  }
+  if (blockIdx.x == 0) {  // db of the output layer: warp tree
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int o = warp; o < nout; o += blockDim.x >> 5) {
+      float t = 0.0f;
+      for (int b = lane; b < B; b += 32) t += Gs[b * nout + o];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+      if (lane == 0) dW[static_cast<long long>(a.H) * nout + o] = t;
+    }
+  }
+}
+
+template <int NO, typename AT>
+static bool launch_ob_v(const OutBwdArgs& a, cudaStream_t s) {
+  const int eb = sizeof(AT);
+  auto al = [&](const void* p) { return reinterpret_cast<uintptr_t>(p) % (4 * eb) == 0; };
+  // single-output layers only: with NO > 1 the 4-column register tiles (w, acc: 8 NO floats)
+  // cut the occupancy below what the scalar kernel reaches (measured slower for NO = 6)
+  if (NO != 1 || a.exact || a.H % 4 || a.x_ld % 4 || a.x_gs % 4 || !al(a.X) ||
+      (a.dX && (a.dx_ld % 4 || a.dx_gs % 4 || !al(a.dX))))
+    return false;
+  constexpr int CB = 4 * kOvQuads;
+  const size_t smem = (static_cast<size_t>(a.B) * (a.nout + 1) +
+                       static_cast<size_t>(kOvSlices) * CB * (a.nout + 1)) * 4;
+  if (smem > 200 * 1024) return false;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_out_backward_v<NO, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  dim3 grid((a.H + CB - 1) / CB, a.groups);
+  launch_k(k_out_backward_v<NO, AT>, grid, kOvQuads * kOvSlices, smem, s, a);
+  return true;
+}
+
 template <int NO, typename AT>
 static void launch_ob(const OutBwdArgs& a, cudaStream_t s) {
+  if (launch_ob_v<NO, AT>(a, s)) return;
   const int slices = a.exact ? 1 : kObSlices;
   const size_t smem =
       (static_cast<size_t>(a.B) * (a.nout + 1) + kObSlices * kObCols * (a.nout + 1)) * 4;
