@@ -173,8 +173,15 @@ struct Pop {
   // next tcgen05 launch must not read its weight operand before the PDL wait
   bool last_wrote_weights = true;
 
+  // diagnostics only (PBRL_SKIP_CLASSES=bitmask of ProfClass): launches of those classes are
+  // dropped, so the step time without them shows their marginal cost in the replayed graph
+  static int skip_classes() {
+    static const int m = std::getenv("PBRL_SKIP_CLASSES") ? std::atoi(std::getenv("PBRL_SKIP_CLASSES")) : 0;
+    return m;
+  }
   template <typename F>
   void timed(int cls, double flops, double bytes, int gated, F&& f) {
+    if (skip_classes() & (1 << cls)) return;
     cudaEvent_t a = nullptr;
     prof_begin(&a);
     f();
