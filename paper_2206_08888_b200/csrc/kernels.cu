@@ -892,22 +892,6 @@ void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, doubl
 // adam_step_inplace (pop_tensor.hpp:328-366) with the bias corrections looked up from
 // host-computed tables (corr[t] = (float)(1 - pow(beta, t)) in double, exactly :347-350), and
 // the target update tgt = (T)tau*on + (T)(1-tau)*tgt (:422-426) fused on the fresh parameter.
-struct AdamScalars {
-  float b1, b2, c1, c2, step, epsv, ta, tb;
-  bool polyak;
-};
-
-__device__ __forceinline__ float adam_one(const AdamScalars& a, float& p, float& mo, float& vo,
-                                          float gk) {
-  const float mk = a.b1 * mo + (1.0f - a.b1) * gk;
-  const float vk = a.b2 * vo + (1.0f - a.b2) * gk * gk;
-  mo = mk;
-  vo = vk;
-  const float mhat = mk / a.c1;
-  const float vhat = vk / a.c2;
-  p = p - a.step * mhat / (sqrtf(vhat) + a.epsv);
-  return p;
-}
 
 // Member rows start 256-byte aligned (stride = P rounded up to 64), so each row is processed as
 // float4 vectors (5 x 128-bit loads, 3-4 x 128-bit stores per thread) plus a scalar tail.
@@ -920,7 +904,8 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
                                               const float* tau_a, const float* tau_b,
                                               const int* polyak_gate,
                                               __nv_bfloat16* __restrict__ p16,
-                                              __nv_bfloat16* __restrict__ t16) {
+                                              __nv_bfloat16* __restrict__ t16, size_t skip0,
+                                              size_t skip1) {
   PDL_ENTRY();
   const int grp = blockIdx.y;
   const int m = grp % n;
@@ -942,8 +927,11 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
   float4* v4 = reinterpret_cast<float4*>(vo + base);
   const float4* g4 = reinterpret_cast<const float4*>(g + base);
   float4* t4 = a.polyak ? reinterpret_cast<float4*>(tgt + base) : nullptr;
-  for (size_t k = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k < P4;
-       k += static_cast<size_t>(gridDim.x) * blockDim.x) {
+  // [skip0, skip1) (float4-aligned) was updated by the dW epilogue of its layer (EPI_ADAM)
+  const size_t s0 = skip0 / 4, sk = (skip1 - skip0) / 4;
+  for (size_t kq = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; kq < P4 - sk;
+       kq += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t k = kq < s0 ? kq : kq + sk;
     float4 pv = p4[k], mv = m4[k], vv = v4[k];
     const float4 gv = g4[k];
     float4 tv;
@@ -994,13 +982,14 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
                  const float* g, const int64_t* t, const float* corr1, const float* corr2,
                  const float* lr, const int* active, float* tgt, const float* tau_a,
                  const float* tau_b, const int* polyak_gate, __nv_bfloat16* p16,
-                 __nv_bfloat16* t16, cudaStream_t s) {
+                 __nv_bfloat16* t16, cudaStream_t s, size_t skip0, size_t skip1) {
   const int threads = 256;
-  int bx = static_cast<int>((P / 4 + threads - 1) / threads);
+  if (skip0 % 4 || skip1 % 4 || skip1 < skip0 || skip1 > P / 4 * 4) skip0 = skip1 = 0;
+  int bx = static_cast<int>((P / 4 - (skip1 - skip0) / 4 + threads - 1) / threads);
   bx = bx < 1 ? 1 : bx;
   dim3 grid(bx, groups);
   launch_k(k_adam, grid, threads, 0, s, n, P, stride, p, m, v, g, t, corr1, corr2, lr, active, tgt,
-           tau_a, tau_b, polyak_gate, p16, t16);
+           tau_a, tau_b, polyak_gate, p16, t16, skip0, skip1);
 }
 
 __global__ void k_to_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,

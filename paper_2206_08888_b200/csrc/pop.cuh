@@ -98,6 +98,7 @@ enum Epi {
   EPI_BIAS_TANH_NOISE = 4,  // as EPI_BIAS_TANH, then TD3 target smoothing noise on C
   EPI_RELU_MASK = 5,    // C = aux(i,j) > 0 ? acc : 0       (activation_backward, relu)
   EPI_TANH_GRAD = 6,    // g = acc * scale; C = g * (1 - aux^2)   (tanh backward, aux = t)
+  EPI_ADAM = 7,         // dW product: Adam (+ Polyak) on the parameters with g = acc (TcArgs)
 };
 
 struct Operand {
@@ -130,6 +131,25 @@ struct GemmArgs {
 };
 
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
+
+// adam_step_inplace per element (pop_tensor.hpp:345-363): shared by k_adam and the EPI_ADAM
+// epilogue of the tensor-core dW product, so both produce the same bits
+struct AdamScalars {
+  float b1, b2, c1, c2, step, epsv, ta, tb;
+  bool polyak;
+};
+
+__device__ __forceinline__ float adam_one(const AdamScalars& a, float& p, float& mo, float& vo,
+                                          float gk) {
+  const float mk = a.b1 * mo + (1.0f - a.b1) * gk;
+  const float vk = a.b2 * vo + (1.0f - a.b2) * gk * gk;
+  mo = mk;
+  vo = vk;
+  const float mhat = mk / a.c1;
+  const float vhat = vk / a.c2;
+  p = p - a.step * mhat / (sqrtf(vhat) + a.epsv);
+  return p;
+}
 // Output-layer backward in one pass (dX with relu mask, dW, db), N_out <= 16.
 struct OutBwdArgs {
   int B = 0, H = 0, nout = 0, groups = 0, n_members = 1;
@@ -193,7 +213,7 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
                  const float* g, const int64_t* t, const float* corr1, const float* corr2,
                  const float* lr, const int* active, float* tgt, const float* tau_a,
                  const float* tau_b, const int* polyak_gate, __nv_bfloat16* p16,
-                 __nv_bfloat16* t16, cudaStream_t s);
+                 __nv_bfloat16* t16, cudaStream_t s, size_t skip0 = 0, size_t skip1 = 0);
 // bf16 copy of an fp32 arena (the BF16 mode's tensor-core weight operands)
 void launch_to_bf16(const float* src, __nv_bfloat16* dst, size_t count, cudaStream_t s);
 void launch_fill(float* p, size_t count, float v, cudaStream_t s);

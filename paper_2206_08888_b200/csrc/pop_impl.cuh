@@ -108,6 +108,17 @@ struct Mat {
 
 inline int pad4(int x) { return (x + 3) / 4 * 4; }
 
+// Adam of one network arena applied inside the tensor-core dW product of its largest layer
+// (EPI_ADAM); the separate k_adam launch then skips that parameter block.
+struct AdamFuse {
+  float *p = nullptr, *m = nullptr, *v = nullptr, *tgt = nullptr;
+  __nv_bfloat16 *p16 = nullptr, *t16 = nullptr;
+  const int64_t* t = nullptr;
+  const float *lr = nullptr, *ta = nullptr, *tb = nullptr;
+  const int* gate = nullptr;
+  size_t skip0 = 0, skip1 = 0;  // set when a layer was fused: the block k_adam must skip
+};
+
 struct StepGraph {
   int B = 0;
   bool masked = false;
@@ -231,8 +242,8 @@ struct Pop {
   void gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Mat G, Mat aux,
                float* DX, long long dx_gs, long long dx_ld, int epi, int col0, int ncols,
                const int* active, float scale);
-  void gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
-               const int* active, bool bias_done = false);
+  bool gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
+               const int* active, bool bias_done = false, AdamFuse* af = nullptr);
   void mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
                    std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                    int last_epi, const int* active = nullptr, float* C2 = nullptr,
@@ -243,13 +254,14 @@ struct Pop {
                     int last_epi, const int* active, float* C2, long long c2_gs, long long c2_ld,
                     bool noise, bool keep_hidden, bool out_act);
   bool fwd2_off = false;  // PBRL_NO_FWD2=1: per-layer launches instead (diagnostics)
+  bool fused_adam_off = true;  // PBRL_FUSED_ADAM=1: Adam in the dW epilogue (see pop.cu)
   bool gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, Mat H,
                       bool keep_hidden, float* Y, long long y_gs, long long y_ld, int out_epi,
                       const int* active, float* C2, long long c2_gs, long long c2_ld, bool noise,
                       bool out_act);
   void mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
                     Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
-                    const int* active, const OutBwdArgs* top = nullptr);
+                    const int* active, const OutBwdArgs* top = nullptr, AdamFuse* af = nullptr);
   void critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>& hs,
                            std::vector<DBuf<float>>& dhs, float* out, long long out_ld, int epi,
                            Mat aux, float scale, const int* active,

@@ -196,8 +196,8 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
 }
 
 // dW_l and db_l into the gradient arena rows: dW = X^T G, db = column sums of G
-void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
-                  const int* active, bool bias_done) {
+bool Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
+                  const int* active, bool bias_done, AdamFuse* af) {
   const int in = sh.dims[l], out = sh.dims[l + 1];
   const double flops = 2.0 * B * in * out * groups;
   // algorithmic bytes: X (once per member when shared), G, dW
@@ -221,23 +221,55 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
     a.M = mrows;
     a.N = out;
     a.K = B;
+    // Adam fused into this product: the layer's parameters are updated in place from the fp32
+    // accumulator (identical bits to k_adam on a stored gradient); the gradient is not stored
+    const size_t w0 = sh.woff[l], w1 = sh.woff[l] + static_cast<size_t>(in) * out;
+    const bool fuse_adam = af && mrows == in && w0 % 4 == 0 && w1 % 4 == 0 && !fused_adam_off;
+    if (fuse_adam) {
+      a.epi = EPI_ADAM;
+      a.ad_p = af->p + w0;
+      a.ad_m = af->m + w0;
+      a.ad_v = af->v + w0;
+      a.ad_tgt = af->tgt ? af->tgt + w0 : nullptr;
+      a.ad_p16 = af->p16 ? af->p16 + w0 : nullptr;
+      a.ad_t16 = af->t16 ? af->t16 + w0 : nullptr;
+      a.ad_gs = static_cast<long long>(sh.stride);
+      a.ad_t = af->t;
+      a.ad_c1 = corr1.p;
+      a.ad_c2 = corr2.p;
+      a.ad_lr = af->lr;
+      a.ad_ta = af->ta;
+      a.ad_tb = af->tb;
+      a.ad_gate = af->gate;
+      af->skip0 = w0;
+      af->skip1 = w1;
+    }
     a.groups = groups;
     a.n_members = n;
     a.a_by_member = X.by_member;
-    a.epi = EPI_STORE;
-    a.C = Gr + sh.woff[l];
+    if (!fuse_adam) a.epi = EPI_STORE;
+    a.C = fuse_adam ? nullptr : Gr + sh.woff[l];
     a.c_gs = static_cast<long long>(sh.stride);
     a.c_rs = out;
     a.active = active;
-    timed(PC_GEMM_DW, flops, bytes, active != nullptr,
+    const double abytes = fuse_adam ? (static_cast<double>(in) * out * groups *
+                                       (24.0 + (af->p16 ? 2.0 : 0.0)) -
+                                       4.0 * groups * in * out)
+                                    : 0.0;
+    timed(PC_GEMM_DW, flops, bytes + abytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bg, true, true, a, stream); });
+    if (fuse_adam && af->tgt) {  // Polyak target traffic (+ its bf16 copy), gated like k_adam's
+      const double tb = static_cast<double>(in) * out * groups * (af->t16 ? 10.0 : 8.0);
+      if (af->gate) prof_add_gated_bytes(tb);
+      else if (prof_on && !prof.empty()) prof.back().bytes += tb;
+    }
     // bias gradient: per-column sums of G in row order (pop_add_bias_backward, :236-250),
     // unless the kernel that produced G already wrote them
     if (!bias_done) timed(PC_ELEM, 0.0, 4.0 * B * out * groups, active != nullptr, [&] {
       launch_colsum(groups, n, B, out, G.p, G.gs, G.ld, Gr + sh.boff[l],
                     static_cast<long long>(sh.stride), active, act16() ? 1 : 0, stream);
     });
-    return;
+    return fuse_adam;
   }
   if (act16()) PBRL_THROW(PBRL_E_CONFIG, "bf16 mode: dW product without a tensor-core shape");
   GemmArgs g;
@@ -259,6 +291,7 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
     if (out <= 16) launch_dw_skinny(g, stream);
     else launch_gemm_simt(g, stream);
   });
+  return false;
 }
 
 // ------------------------------------------------------------------ profiling
@@ -533,7 +566,8 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
 // backward of `sh` from the top cotangent G: dW for every layer, dX for layers > 0
 void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
                        Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
-                       const int* active, const OutBwdArgs* top) {
+                       const int* active, const OutBwdArgs* top,
+                       AdamFuse* af) {
   const int L = sh.depth;
   bool bias_done = false;  // the bias gradient of layer l was produced with its cotangent
   for (int l = L - 1; l >= 0; --l) {
@@ -598,7 +632,8 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       const Mat dh = hid(dhs, l - 1, B, sh, 0);
       gemm_dx(sh, W, l, groups, B, G, x, const_cast<float*>(dh.p), dh.gs, dh.ld, EPI_RELU_MASK,
               0, sh.dims[l], active, 1.0f);
-      gemm_dw(sh, Gr, l, groups, B, x, G, active, bias_done);
+      gemm_dw(sh, Gr, l, groups, B, x, G, active, bias_done,
+              (af && l == 1 && sh.depth == 3) ? af : nullptr);
       G = dh;
     } else {
       gemm_dw(sh, Gr, l, groups, B, x, G, active, bias_done);
@@ -744,19 +779,32 @@ void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
     timed(PC_ELEM, 0.0, 0.0, 0,
           [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
   }
-  mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr,
-               &top);
   const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
+  AdamFuse af;
+  af.p = cri_p.p;
+  af.m = cri_m.p;
+  af.v = cri_v.p;
+  af.tgt = cri_t.p;
+  af.p16 = cri_p16.p;
+  af.t16 = cri_t16.p;
+  af.t = t_cri.p;
+  af.lr = clr;
+  af.ta = h_f5.p;
+  af.tb = h_f6.p;
+  af.gate = polyak_gate;
+  mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr,
+               &top, use_tc() ? &af : nullptr);
   // 28 B/param Adam (+2 B/param bf16 operand copy in BF16 mode)
-  timed(PC_ADAM, 0.0, static_cast<double>(cri.P) * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
+  const double cP = static_cast<double>(cri.P - (af.skip1 - af.skip0));  // k_adam's share
+  timed(PC_ADAM, 0.0, cP * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
     launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
                 corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, cri_p16.p, cri_t16.p,
-                stream);
+                stream, af.skip0, af.skip1);
   });
   // fused target Polyak: +8 B/param (read + write target), every member (SAC) or fired (TD3)
   const double pb = act16() ? 10.0 : 8.0;
-  if (polyak_gate) prof_add_gated_bytes(pb * cri.P * n2);
-  else if (prof_on && !prof.empty()) prof.back().bytes += pb * cri.P * n2;
+  if (polyak_gate) prof_add_gated_bytes(pb * cP * n2);
+  else if (prof_on && !prof.empty()) prof.back().bytes += pb * cP * n2;
 }
 
 // ------------------------------------------------------------------ TD3 step (algos.hpp:351-422)
@@ -896,12 +944,26 @@ void Pop::td3_policy_half(int B, bool forward_done) {
   const int lt = pad4(da);
   critic_dx_to_action(n, B, Mat{S.gq.p, nbB, 1, 0}, S.qh, S.qdh, S.gtop.p, lt, EPI_TANH_GRAD,
                       Mat{S.pt.p, nbB * da, da, 0}, pol.out_scale, fire.p, &top);
+  AdamFuse af;
+  af.p = pol_p.p;
+  af.m = pol_m.p;
+  af.v = pol_v.p;
+  af.tgt = pol_t.p;
+  af.p16 = pol_p16.p;
+  af.t16 = pol_t16.p;
+  af.t = t_pol.p;
+  af.lr = h_f1.p;
+  af.ta = h_f5.p;
+  af.tb = h_f6.p;
+  af.gate = nullptr;  // the policy half only updates fired members (tiles gated by fire)
   mlp_backward(pol, pol_p.p, pol_g.p, n, B, Mat{S.gtop.p, nbB * lt, lt, 0}, s, S.ph, S.pdh,
-               fire.p);
-  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * (act16() ? 40.0 : 36.0), 1, [&] {
+               fire.p, nullptr, use_tc() ? &af : nullptr);
+  timed(PC_ADAM, 0.0,
+        static_cast<double>(pol.P - (af.skip1 - af.skip0)) * n * (act16() ? 40.0 : 36.0), 1,
+        [&] {
     launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
                 corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, pol_p16.p, pol_t16.p,
-                stream);
+                stream, af.skip0, af.skip1);
   });
 }
 

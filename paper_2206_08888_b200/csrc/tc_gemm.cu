@@ -777,7 +777,52 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           const int col = n0 + c0 + lane;
           const bool col_ok = lane < CW && col < g.N;
           const bool need_aux = epi == EPI_RELU_MASK || epi == EPI_TANH_GRAD;
-          if (col_ok) {
+          if (col_ok && epi == EPI_ADAM) {
+            // Adam (+ Polyak, + bf16 copies) on this column of the parameter block; the rows of
+            // a chunk are loaded 8 at a time (independent round trips), lanes = columns
+            AdamScalars as;
+            as.b1 = static_cast<float>(0.9);
+            as.b2 = static_cast<float>(0.999);
+            as.c1 = g.ad_c1[g.ad_t[grp]];
+            as.c2 = g.ad_c2[g.ad_t[grp]];
+            as.step = g.ad_lr[mem];
+            as.epsv = static_cast<float>(1e-8);
+            as.polyak = g.ad_tgt && (!g.ad_gate || g.ad_gate[mem]);
+            as.ta = as.polyak ? g.ad_ta[mem] : 0.0f;
+            as.tb = as.polyak ? g.ad_tb[mem] : 0.0f;
+            const long long gb = static_cast<long long>(grp) * g.ad_gs + col;
+#pragma unroll 1
+            for (int r8 = 0; r8 < 32; r8 += 8) {
+              float pv[8], mv[8], vv[8], tv[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int rw = row0 + r8 + u;
+                const long long e = gb + static_cast<long long>(rw) * g.c_rs;
+                const bool ok = rw < g.M;
+                pv[u] = ok ? g.ad_p[e] : 0.0f;
+                mv[u] = ok ? g.ad_m[e] : 0.0f;
+                vv[u] = ok ? g.ad_v[e] : 0.0f;
+                tv[u] = (ok && as.polyak) ? g.ad_tgt[e] : 0.0f;
+              }
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int rr = r8 + u;
+                const int rw = row0 + rr;
+                if (rw >= g.M) break;
+                const long long e = gb + static_cast<long long>(rw) * g.c_rs;
+                adam_one(as, pv[u], mv[u], vv[u], T[rr * 33 + lane]);
+                g.ad_p[e] = pv[u];
+                g.ad_m[e] = mv[u];
+                g.ad_v[e] = vv[u];
+                if (g.ad_p16) g.ad_p16[e] = __float2bfloat16_rn(pv[u]);
+                if (as.polyak) {
+                  const float tn = as.ta * pv[u] + as.tb * tv[u];
+                  g.ad_tgt[e] = tn;
+                  if (g.ad_t16) g.ad_t16[e] = __float2bfloat16_rn(tn);
+                }
+              }
+            }
+          } else if (col_ok) {
             const float bv = bias ? bias[col] : 0.0f;
 #pragma unroll 1
             for (int r8 = 0; r8 < 32; r8 += 8) {

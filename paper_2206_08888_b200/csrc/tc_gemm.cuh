@@ -3,6 +3,7 @@
 
 #include <cstdint>
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace pbrl {
@@ -58,6 +59,23 @@ struct TcArgs {
   // EPI_TANH_GRAD (aux = tanh values, scale) or EPI_STORE
   int ow_tr = 0;
   long long ow_ld = 0;
+  // EPI_ADAM (a dW product): instead of storing the gradient, apply adam_step_inplace (+ the
+  // Polyak target update, + the bf16 operand copies) to the parameter block it belongs to:
+  // element (r, c) of group g is parameter ad_*[g * ad_gs + r * c_rs + c]
+  float* ad_p = nullptr;
+  float* ad_m = nullptr;
+  float* ad_v = nullptr;
+  float* ad_tgt = nullptr;
+  __nv_bfloat16* ad_p16 = nullptr;
+  __nv_bfloat16* ad_t16 = nullptr;
+  long long ad_gs = 0;
+  const int64_t* ad_t = nullptr;
+  const float* ad_c1 = nullptr;  // bias-correction tables indexed by t
+  const float* ad_c2 = nullptr;
+  const float* ad_lr = nullptr;  // per member
+  const float* ad_ta = nullptr;
+  const float* ad_tb = nullptr;
+  const int* ad_gate = nullptr;  // Polyak gate per member (nullptr: always)
   // ReLU masks as bits: a storing BIAS_RELU / fused epilogue writes bit (c % 32) of word c / 32
   // of row r = (h[r][c] > 0) to mask_out; EPI_RELU_MASK reads mask_in (when set) instead of aux
   uint32_t* mask_out = nullptr;
