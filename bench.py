@@ -359,33 +359,40 @@ def main():
         except Exception:
             pass
 
-    # ---- e2e through the C ABI: pinned host batches, H2D + step + D2H of the losses per step
+    # ---- e2e through the C ABI: pinned host batches, every step's H2D copy and the D2H of every
+    # step's losses inside the timed region.  update_k_steps semantics (algos.hpp:953-983): each
+    # call runs KC host batches (the copy of batch i+1 overlaps step i) and returns the KC steps'
+    # critic1 / critic2 / policy losses.
     e2e = None
     if not args.no_e2e:
-        hb = [[x.cpu().pin_memory() for x in (b.s, b.a, b.r, b.s2, b.done)] for b in batches[:8]]
+        hb = [[x.cpu().pin_memory() for x in (b.s, b.a, b.r, b.s2, b.done)] for b in batches[:10]]
         hstructs = [_lib.Batch(*[x.data_ptr() for x in h]) for h in hb]
-        loss = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(3)]
-        lp = [C.cast(x.data_ptr(), _lib.f64p) for x in loss]
-        ke = max(2, min(K, 50))
+        KC = 10
+        loss = torch.empty(KC * 3 * n, dtype=torch.float64).pin_memory()
+        lptr = C.cast(loss.data_ptr(), _lib.f64p)
+        calls = max(1, min(K, 50) // KC)
 
-        def run_host(i):
-            arr = (_lib.Batch * 1)(hstructs[i % len(hstructs)])
-            _lib.call("pbrl_update_batches", st.handle, arr, 1, B, None)
-            _lib.call("pbrl_last_losses", st.handle, *lp)
+        def run_host(c):
+            arr = (_lib.Batch * KC)(*[hstructs[(c * KC + j) % len(hstructs)] for j in range(KC)])
+            _lib.call("pbrl_update_batches_losses", st.handle, arr, KC, B, None, lptr)
 
         run_host(0)
         barrier()
         st.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
         e0.record(lstream)
-        for i in range(ke):
-            run_host(i)
+        for c in range(calls):
+            run_host(c + 1)
         e1.record(lstream)
         e1.synchronize()
+        wall = time.perf_counter() - t0
         ems = max_over_ranks(e0.elapsed_time(e1))
+        ke = calls * KC
         e2e = {"value": pop * ke / (ems / 1e3), "unit": "agent-updates/s",
                "h2d_bytes_per_step": n * B * (2 * OBS + ACT + 2) * 4,
-               "d2h_bytes_per_step": 3 * n * 8, "steps": ke}
+               "d2h_bytes_per_step": 3 * n * 8, "steps": ke, "steps_per_call": KC,
+               "host_wall_value": pop * ke / wall}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

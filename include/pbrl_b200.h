@@ -121,6 +121,12 @@ int pbrl_update_batches(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k, ui
 /* Same with device-resident batches (pointers valid on the population's device). */
 int pbrl_update_batches_device(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k,
                                uint64_t batch_rows, const uint8_t* policy_mask);
+/* update_k_steps over k HOST batches with every step's losses returned: losses[i][0..2][n] =
+ * critic1 / critic2 / policy losses of step i (as pbrl_last_losses).  The H2D copy of batch
+ * i+1 overlaps step i (double-buffered staging on a copy stream); returns when all k steps and
+ * their loss copies are done.  Pinned host memory recommended. */
+int pbrl_update_batches_losses(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k,
+                               uint64_t batch_rows, const uint8_t* policy_mask, double* losses);
 /* update_k_steps fed by the device replay: per step i, sample_batch(..., draw_id = first+i)
  * (replay.hpp:181-204) then one update.  *ready = 0 (and nothing runs) when a source buffer
  * holds fewer than max(min_size, 1) transitions (sample_batch's nullopt). */

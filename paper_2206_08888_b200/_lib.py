@@ -55,6 +55,7 @@ SIGNATURES = {
     "pbrl_get_alpha": [vp, f32p, f32p, f32p, i64p],
     "pbrl_update_batches": [vp, C.POINTER(Batch), u32, u64, u8p],
     "pbrl_update_batches_device": [vp, C.POINTER(Batch), u32, u64, u8p],
+    "pbrl_update_batches_losses": [vp, C.POINTER(Batch), u32, u64, u8p, f64p],
     "pbrl_update_k": [vp, u32, u64, u64, u64, u64, intp],
     "pbrl_last_losses": [vp, f64p, f64p, f64p],
     "pbrl_replay_create": [vp, u64, C.c_int],

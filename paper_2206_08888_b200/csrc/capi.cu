@@ -267,6 +267,14 @@ int pbrl_update_batches_device(pbrl_pop* pop, const pbrl_batch* batches, uint32_
   return guarded([&] { P(pop)->update_batches(batches, k, rows, policy_mask, true); });
 }
 
+int pbrl_update_batches_losses(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k,
+                               uint64_t rows, const uint8_t* policy_mask, double* losses) {
+  return guarded([&] {
+    if (!losses) PBRL_THROW(PBRL_E_USAGE, "null losses buffer");
+    P(pop)->update_batches(batches, k, rows, policy_mask, false, losses);
+  });
+}
+
 int pbrl_last_losses(pbrl_pop* pop, double* c1, double* c2, double* pl) {
   return guarded([&] {
     Pop* p = P(pop);

@@ -177,6 +177,9 @@ Pop::~Pop() {
     if (side3) cudaStreamDestroy(side3);
     if (ev_pfork) cudaEventDestroy(ev_pfork);
     if (ev_pjoin) cudaEventDestroy(ev_pjoin);
+    if (cstream) cudaStreamDestroy(cstream);
+    for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1]})
+      if (e) cudaEventDestroy(e);
   }
 }
 
@@ -315,11 +318,14 @@ void Pop::ensure_scratch(int B) {
   S.ga.alloc(2 * nb * da);
   S.head.alloc(nb * pol.dims[L]);
   S.gtop.alloc(nb * pad4(pol.dims[L]));
-  S.bs.alloc(nb * ds);
-  S.ba.alloc(nb * da);
-  S.br.alloc(nb);
-  S.bs2.alloc(nb * ds);
-  S.bd.alloc(nb);
+  for (int sl = 0; sl < 2; ++sl) {
+    S.bs[sl].alloc(nb * ds);
+    S.ba[sl].alloc(nb * da);
+    S.br[sl].alloc(nb);
+    S.bs2[sl].alloc(nb * ds);
+    S.bd[sl].alloc(nb);
+  }
+  slot_used[0] = slot_used[1] = false;
   for (int l = 0; l + 1 < L; ++l) {
     // activations [rows][pad4(H)] + the ReLU mask bits [rows][ceil(H / 32)] (see Pop::hid)
     const size_t h = static_cast<size_t>(padl(pol.dims[l + 1])) + (pol.dims[l + 1] + 31) / 32;
@@ -365,7 +371,7 @@ void Pop::ensure_ones() {
 
 // ------------------------------------------------------------------ update entry points
 void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
-                         const uint8_t* policy_mask, bool device_ptrs) {
+                         const uint8_t* policy_mask, bool device_ptrs, double* losses_out) {
   if (k < 1) PBRL_THROW(PBRL_E_CONFIG, "update_k_steps: k must be >= 1");
   if (rows < 1) PBRL_THROW(PBRL_E_SHAPE, "batch rows must be >= 1");
   validate_hyper();
@@ -382,29 +388,57 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     d_mask = mask_buf.p;
   }
   const size_t nb = static_cast<size_t>(n) * B;
-  const cudaMemcpyKind kind = device_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   for (uint32_t i = 0; i < k; ++i) {
     const pbrl_batch& b = batches[i];
     if (!b.s || !b.a || !b.r || !b.s2 || !b.done) PBRL_THROW(PBRL_E_USAGE, "null batch pointer");
+  }
+  if (!device_ptrs && !cstream) {
+    CUDA_CHECK(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
+    for (int sl = 0; sl < 2; ++sl) {
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_copied[sl], cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_free[sl], cudaEventDisableTiming));
+    }
+  }
+  // H2D of host batch i into staging slot i % 2 on the copy stream, after the pack that last
+  // read that slot (ev_free); the step's pack waits for the copy (ev_copied)
+  auto stage = [&](uint32_t i) {
+    const pbrl_batch& b = batches[i];
+    const int sl = static_cast<int>(i & 1u);
+    if (slot_used[sl]) CUDA_CHECK(cudaStreamWaitEvent(cstream, ev_free[sl], 0));
+    const cudaMemcpyKind h2d = cudaMemcpyHostToDevice;
+    CUDA_CHECK(cudaMemcpyAsync(S.bs[sl].p, b.s, nb * ds * 4, h2d, cstream));
+    CUDA_CHECK(cudaMemcpyAsync(S.ba[sl].p, b.a, nb * da * 4, h2d, cstream));
+    CUDA_CHECK(cudaMemcpyAsync(S.br[sl].p, b.r, nb * 4, h2d, cstream));
+    CUDA_CHECK(cudaMemcpyAsync(S.bs2[sl].p, b.s2, nb * ds * 4, h2d, cstream));
+    CUDA_CHECK(cudaMemcpyAsync(S.bd[sl].p, b.done, nb * 4, h2d, cstream));
+    CUDA_CHECK(cudaEventRecord(ev_copied[sl], cstream));
+    slot_used[sl] = true;
+  };
+  if (!device_ptrs) stage(0);
+  for (uint32_t i = 0; i < k; ++i) {
+    const pbrl_batch& b = batches[i];
     const float *s = b.s, *a = b.a, *r = b.r, *s2 = b.s2, *d = b.done;
     if (!device_ptrs) {
-      CUDA_CHECK(cudaMemcpyAsync(S.bs.p, b.s, nb * ds * 4, kind, stream));
-      CUDA_CHECK(cudaMemcpyAsync(S.ba.p, b.a, nb * da * 4, kind, stream));
-      CUDA_CHECK(cudaMemcpyAsync(S.br.p, b.r, nb * 4, kind, stream));
-      CUDA_CHECK(cudaMemcpyAsync(S.bs2.p, b.s2, nb * ds * 4, kind, stream));
-      CUDA_CHECK(cudaMemcpyAsync(S.bd.p, b.done, nb * 4, kind, stream));
-      s = S.bs.p;
-      a = S.ba.p;
-      r = S.br.p;
-      s2 = S.bs2.p;
-      d = S.bd.p;
+      if (i + 1 < k) stage(i + 1);  // overlaps this step
+      const int sl = static_cast<int>(i & 1u);
+      CUDA_CHECK(cudaStreamWaitEvent(stream, ev_copied[sl], 0));
+      s = S.bs[sl].p;
+      a = S.ba[sl].p;
+      r = S.br[sl].p;
+      s2 = S.bs2[sl].p;
+      d = S.bd[sl].p;
     }
     timed(PC_GATHER, 0.0, 0.0, 0, [&] {
       launch_pack_batch(n, B, ds, da, lsa, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
                         S.d.p, act16() ? 1 : 0, stream);
     });
+    if (!device_ptrs) CUDA_CHECK(cudaEventRecord(ev_free[i & 1u], stream));
     step(B, d_mask);
+    if (losses_out)  // this step's critic1 / critic2 / policy losses -> host (async)
+      CUDA_CHECK(cudaMemcpyAsync(losses_out + static_cast<size_t>(i) * 3 * n, losses.p,
+                                 3 * n * sizeof(double), cudaMemcpyDeviceToHost, stream));
   }
+  if (losses_out) sync();
   CUDA_CHECK(cudaGetLastError());
 }
 

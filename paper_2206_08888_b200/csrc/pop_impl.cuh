@@ -62,7 +62,7 @@ struct DBuf {
 struct Scratch {
   int B = 0;
   DBuf<float> in_sa, in_s2a, sa_pi, r, d, y, tq_out, q, dq, qpi, gq, pt, ga, head, gtop;
-  DBuf<float> bs, ba, br, bs2, bd;  // staged batch
+  DBuf<float> bs[2], ba[2], br[2], bs2[2], bd[2];  // host batches staged (double-buffered)
   std::vector<DBuf<float>> tp_h, ph, pdh, tq_h, ch, dh, qh, qdh;
   DBuf<float> x, th, ls, eps, logp, logp2, lw, tnoise;
   DBuf<uint8_t> clamped;
@@ -283,7 +283,12 @@ struct Pop {
   void sac_step(int B);
   void step(int B, const uint8_t* d_mask);
   void update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
-                      const uint8_t* policy_mask, bool device_ptrs);
+                      const uint8_t* policy_mask, bool device_ptrs, double* losses_out = nullptr);
+  // host-batch staging: H2D copies on their own stream, double-buffered, so the copy of batch
+  // i+1 overlaps the update step of batch i
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  bool slot_used[2] = {false, false};
 
   // helpers for member-level access
   float* net_row(int net, uint64_t member);

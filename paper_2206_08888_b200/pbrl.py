@@ -349,7 +349,8 @@ class _Population:
         return out
 
     # -- updates
-    def _update(self, batches: Sequence[TransitionBatch], mask=None) -> None:
+    def _update(self, batches: Sequence[TransitionBatch], mask=None,
+                return_losses: bool = False) -> Optional[np.ndarray]:
         if not batches:
             raise ConfigError("update_k_steps: k must be >= 1")
         keep = []
@@ -373,8 +374,22 @@ class _Population:
             mk = np.ascontiguousarray(np.asarray(mask, dtype=bool).astype(np.uint8))
             keep.append(mk)
             m = _ptr(mk, _lib.u8p)
+        if return_losses and not dev:
+            # every step's losses, H2D of batch i+1 overlapping step i (one host round trip)
+            out = np.empty((len(structs), 3, self.n), np.float64)
+            _lib.call("pbrl_update_batches_losses", self._h, arr, len(structs), rows, m,
+                      _ptr(out, _lib.f64p))
+            return out
+        if return_losses:  # device batches: step by step
+            out = np.empty((len(structs), 3, self.n), np.float64)
+            for i in range(len(structs)):
+                one = (_lib.Batch * 1)(structs[i])
+                _lib.call("pbrl_update_batches_device", self._h, one, 1, rows, m)
+                out[i] = np.stack(self.last_losses())
+            return out
         fn = "pbrl_update_batches_device" if dev else "pbrl_update_batches"
         _lib.call(fn, self._h, arr, len(structs), rows, m)
+        return None
 
     def launch_count(self) -> int:
         c = C.c_uint64()
@@ -444,9 +459,12 @@ def sac_update_step(st: SacState, batch: TransitionBatch, hyper: SacHyper) -> No
     st._update([batch])
 
 
-def update_k_steps(st, sampler: Callable[[], Optional[TransitionBatch]], k: int, hyper) -> None:
+def update_k_steps(st, sampler: Callable[[], Optional[TransitionBatch]], k: int, hyper,
+                   return_losses: bool = False) -> Optional[np.ndarray]:
     """update_k_steps (algos.hpp:953-983): k chained steps, no export in between; the device
-    runs them back to back.  An exhausted sampler raises DataStarvationError."""
+    runs them back to back.  An exhausted sampler raises DataStarvationError.  return_losses:
+    the k steps' critic1 / critic2 / policy losses as a [k, 3, n] array (with host batches the
+    H2D copy of batch i+1 overlaps step i)."""
     if k < 1:
         raise ConfigError("update_k_steps: k must be >= 1")
     batches = []
@@ -456,7 +474,7 @@ def update_k_steps(st, sampler: Callable[[], Optional[TransitionBatch]], k: int,
             raise DataStarvationError(f"update_k_steps: sampler exhausted after {i} of {k} steps")
         batches.append(b)
     st._sync_hyper(hyper)
-    st._update(batches)
+    return st._update(batches, return_losses=return_losses)
 
 
 # ---------------------------------------------------------------------- replay

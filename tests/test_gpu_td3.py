@@ -160,3 +160,28 @@ def test_launch_count_independent_of_population(pb, ora):
             pb.td3_update_step(st, to_batch(pb, raw, k), hy)
         counts.append(st.launch_count() - before)
     assert counts[0] == counts[1] == counts[2]
+
+
+@pytest.mark.parametrize("precision", ["ffma32", "bf16"])
+def test_update_k_steps_with_losses_matches_single_steps(pb, ora, precision):
+    """pbrl_update_batches_losses (k host batches, overlapped H2D staging, every step's losses)
+    leaves the same state and reports the same per-step losses as k single-step calls."""
+    n, B, K = 3, 128, 5
+    raw = ora.synthetic_batches(K, n, B, 17, 6, 13)
+    hy = pb.Td3Hyper.defaults(n)
+    a = pb.make_td3_state(n, 17, 6, [64, 64] if precision == "ffma32" else [256, 256], 1.0, 13,
+                          precision=precision)
+    b = pb.make_td3_state(n, 17, 6, [64, 64] if precision == "ffma32" else [256, 256], 1.0, 13,
+                          precision=precision)
+    batches = [to_batch(pb, raw, k) for k in range(K)]
+    it = iter(batches)
+    la = pb.update_k_steps(a, lambda: next(it), K, hy, return_losses=True)
+    lb = []
+    for k in range(K):
+        pb.td3_update_step(b, batches[k], hy)
+        lb.append(np.stack(b.last_losses()))
+    assert la.shape == (K, 3, n)
+    assert np.array_equal(la, np.stack(lb))
+    for net in ("policy", "policy_target", "critic1", "critic2", "critic1_target",
+                "critic2_target"):
+        assert np.array_equal(a.params(net), b.params(net)), net
