@@ -137,6 +137,14 @@ int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t sample_seed, uint64_t firs
  * each [n] (TD3 policy entries are 0 for members that did not fire). */
 int pbrl_last_losses(pbrl_pop* pop, double* critic1, double* critic2, double* policy);
 
+/* ---- action selection: act (TD3, algos.hpp:895-915) / sac_act (SAC, :918-942) for every
+ * member on rows observations each, keyed by the population's member streams: obs [n][rows][ds]
+ * and actions [n][rows][da] are host arrays; steps [n] key the per-member kExploreNoise streams;
+ * noise_std [n] (TD3: exploration std in action-bound units, 0 = none; ignored by SAC, may be
+ * NULL when deterministic). */
+int pbrl_act(pbrl_pop* pop, const float* obs, uint64_t rows, const double* noise_std,
+             uint64_t seed, const uint64_t* steps, int deterministic, float* actions);
+
 /* ---- replay: ReplayBuffer (replay.hpp:28-173) held in HBM, one ring per member (per-agent) or
  * one shared ring.  Insert is the batched equivalent of push (:56-69). */
 int pbrl_replay_create(pbrl_pop* pop, uint64_t capacity, int mode);

@@ -115,9 +115,27 @@ def tanh_case(ref: Ref):
     np.savez_compressed(OUT / "tanhf.npz", x=x, y=np.asarray([ref.tanhf(float(v)) for v in x], np.float32))
 
 
+def act_case(ref: Ref):
+    """act / sac_act (algos.hpp:895-942) on fixed observations, stochastic and deterministic."""
+    out = {}
+    obs = np.random.default_rng(5).uniform(-1, 1, (3, 4, 17)).astype(np.float32)
+    steps = np.asarray([3, 0, 11], np.uint64)
+    noise = np.asarray([0.1, 0.0, 0.3])
+    out.update(obs=obs, steps=steps, noise=noise, seed=99, hidden=np.asarray([32, 32]), n=3,
+               ds=17, da=6, state_seed=7)
+    for algo in ("td3", "sac"):
+        st = (ref.td3 if algo == "td3" else ref.sac)(3, 17, 6, [32, 32], 1.0, 7)
+        for det in (0, 1):
+            out[f"{algo}_det{det}"] = st.act(obs, 99, steps, noise, bool(det))
+    np.savez_compressed(OUT / "act.npz", **out)
+
+
 def main():
     ref = Ref()
     OUT.mkdir(parents=True, exist_ok=True)
+    if sys.argv[1:] == ["act"]:
+        act_case(ref)
+        return
     td3_case(ref, "td3_small", 3, 4, 2, [8, 8], 8, 20, 11, 12,
              hyper=dict(policy_delay_ratio=[0.5, 1.0, 0.3], critic_lr=[3e-4, 1e-3, 3e-4]))
     td3_case(ref, "td3_halfcheetah", 2, 17, 6, [64, 64], 32, 4, 7, 7)
@@ -126,6 +144,7 @@ def main():
     replay_case(ref)
     pbt_case(ref)
     tanh_case(ref)
+    act_case(ref)
     print("golden fixtures written to", OUT)
 
 

@@ -116,6 +116,8 @@ class Oracle(_Lib):
         F("ora_td3_step", C.c_int, vp, f32p, f32p, f32p, f32p, f32p, u64, f64p, C.c_char_p, f64p)
         F("ora_sac_get_alpha", None, vp, f32p, f32p, f32p, i64p, u64p)
         F("ora_sac_step", C.c_int, vp, f32p, f32p, f32p, f32p, f32p, u64, f64p, f64p)
+        F("ora_td3_act", None, vp, f32p, u64, f64p, u64, u64p, C.c_int, f32p)
+        F("ora_sac_act", None, vp, f32p, u64, u64, u64p, C.c_int, f32p)
         F("ora_synthetic_batches", None, u64, u64, u64, u64, u64, u64, f32p, f32p, f32p, f32p, f32p)
         F("ora_replay_create", vp, u64, u64, u64)
         F("ora_replay_destroy", None, vp)
@@ -219,6 +221,8 @@ class Ref(_Lib):
                 F(f"ref_{algo}_losses", C.c_int, vp, fp, fp, fp, fp, fp, u64, f64p, f64p)
         F("ref_synthetic_batches_f", None, u64, u64, u64, u64, u64, u64, f32p, f32p, f32p, f32p,
           f32p)
+        F("ref_td3f_act", C.c_int, vp, f32p, u64, f64p, u64, u64p, C.c_int, f32p)
+        F("ref_sacf_act", C.c_int, vp, f32p, u64, u64, u64p, C.c_int, f32p)
         F("ref_replay_create", vp, u64, u64, u64)
         F("ref_replay_destroy", None, vp)
         F("ref_replay_push", None, vp, f32p, f32p, C.c_float, f32p, C.c_float, u32)
@@ -400,6 +404,25 @@ class _State:
         if rc == -2:
             raise ValueError("config error")
         return losses
+
+    def act(self, obs, seed, steps, noise_std=None, deterministic=False):
+        """act / sac_act (algos.hpp:895-942): actions [n][rows][da] for obs [n][rows][ds]."""
+        obs = np.ascontiguousarray(obs, np.float32)
+        rows = obs.shape[1]
+        steps = np.ascontiguousarray(steps, np.uint64)
+        out = np.zeros((self.n, rows, self.da), np.float32)
+        det = 1 if deterministic else 0
+        if self.algo == "td3":
+            ns = np.ascontiguousarray(noise_std if noise_std is not None else [0.0] * self.n,
+                                      np.float64)
+            rc = self._f("act")(self.h, _ptr(obs, f32p), rows, _ptr(ns, f64p), seed,
+                                _ptr(steps, u64p), det, _ptr(out, f32p))
+        else:
+            rc = self._f("act")(self.h, _ptr(obs, f32p), rows, seed, _ptr(steps, u64p), det,
+                                _ptr(out, f32p))
+        if rc is not None and rc < 0:
+            raise ValueError(self.o.lib.ref_last_error().decode())
+        return out
 
     def target(self, batch, hyper):
         s, a, r, s2, d, b = self._batch(batch)

@@ -682,6 +682,53 @@ static void split_head(const float* h, uint64_t cnt, uint64_t da, float* mu, flo
   }
 }
 
+/* act, algos.hpp:895-915: tanh policy output (already scaled by the bound) plus clipped
+ * Gaussian exploration noise; std per member in action-bound units, stream (seed, streams[m],
+ * kExploreNoise, steps[m]), counter 2e over the member's [rows][da] block.  out [n][rows][da]. */
+void ora_td3_act(const ora_td3* st, const float* obs, uint64_t rows, const double* noise_std,
+                 uint64_t seed, const uint64_t* steps, int deterministic, float* out) {
+  ora_cache c;
+  mlp_forward(&st->pol, st->net[0], st->n, rows, obs, &c);
+  const uint64_t per = rows * st->da;
+  memcpy(out, c.out, sizeof(float) * st->n * per);
+  cache_free(&c);
+  if (deterministic) return;
+  const float bound = st->pol.out_scale;
+  for (uint64_t m = 0; m < st->n; ++m) {
+    if (noise_std[m] == 0.0) continue;
+    const uint64_t key = ora_stream_key(seed, st->streams[m], USE_EXPLORE, steps[m]);
+    const float sd = (float)(noise_std[m] * (double)bound);
+    float* am = out + m * per;
+    for (uint64_t e = 0; e < per; ++e)
+      am[e] = clampf_(am[e] + (float)ora_normal_pair(key, 2 * e) * sd, -bound, bound);
+  }
+}
+
+/* sac_act, algos.hpp:918-942: a = bound * tanh(mu + exp(log_std) * eps) (the mode when
+ * deterministic), log_std clamped by split_policy_head. */
+void ora_sac_act(const ora_sac* st, const float* obs, uint64_t rows, uint64_t seed,
+                 const uint64_t* steps, int deterministic, float* out) {
+  ora_cache c;
+  mlp_forward(&st->pol, st->net[0], st->n, rows, obs, &c);
+  const uint64_t cnt = st->n * rows, da = st->da, per = rows * da;
+  float* mu = (float*)malloc(sizeof(float) * cnt * da);
+  float* ls = (float*)malloc(sizeof(float) * cnt * da);
+  char* cl = (char*)malloc(cnt * da);
+  split_head(c.out, cnt, da, mu, ls, cl);
+  cache_free(&c);
+  if (!deterministic) {
+    for (uint64_t m = 0; m < st->n; ++m) {
+      const uint64_t key = ora_stream_key(seed, st->streams[m], USE_EXPLORE, steps[m]);
+      for (uint64_t e = 0; e < per; ++e)
+        mu[m * per + e] += expf(ls[m * per + e]) * (float)ora_normal_pair(key, 2 * e);
+    }
+  }
+  for (uint64_t i = 0; i < cnt * da; ++i) out[i] = tanhf(mu[i]) * st->bound;
+  free(mu);
+  free(ls);
+  free(cl);
+}
+
 /* draw_eps, algos.hpp:618-629 */
 static void draw_eps(const ora_sac* st, uint64_t b, uint64_t use, float* eps) {
   const uint64_t da = st->da;

@@ -48,6 +48,9 @@ void ora_td3_target(const ora_td3* st, const float* s2, const float* r, const fl
                     const double* hyper, float* y);
 /* one td3_update_step; losses (optional) [3][n]: critic1 MSE, critic2 MSE, policy loss
  * (per member; the policy entry is 0 for members that did not fire).  returns 0 or -2 (config). */
+/* act / sac_act (algos.hpp:895-942): actions [n][rows][da] for obs [n][rows][ds] */
+void ora_td3_act(const ora_td3* st, const float* obs, uint64_t rows, const double* noise_std,
+                 uint64_t seed, const uint64_t* steps, int deterministic, float* out);
 int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, const float* s2,
                  const float* d, uint64_t b, const double* hyper, const char* policy_mask,
                  double* losses);
@@ -65,6 +68,8 @@ void ora_sac_set_net(ora_sac* st, int net, uint64_t m, const float* in);
 void ora_sac_get_adam(const ora_sac* st, int net, uint64_t m, float* mo, float* vo, int64_t* t);
 void ora_sac_get_alpha(const ora_sac* st, float* log_alpha, float* am, float* av, int64_t* at,
                        uint64_t* steps);
+void ora_sac_act(const ora_sac* st, const float* obs, uint64_t rows, uint64_t seed,
+                 const uint64_t* steps, int deterministic, float* out);
 int ora_sac_step(ora_sac* st, const float* s, const float* a, const float* r, const float* s2,
                  const float* d, uint64_t b, const double* hyper, double* losses);
 

@@ -357,6 +357,31 @@ PBRL_REF_TD3(d, double)
 PBRL_REF_SAC(f, float)
 PBRL_REF_SAC(d, double)
 
+// ---------------------------------------------------------------- action selection (float)
+int ref_td3f_act(void* h, const float* obs, std::uint64_t rows, const double* noise_std,
+                 std::uint64_t seed, const std::uint64_t* steps, int deterministic, float* out) {
+  return guarded([&] {
+    auto& st = *static_cast<Td3State<float>*>(h);
+    const std::size_t n = st.members(), ds = st.policy.in_dim();
+    PopTensor<float> o({n, rows, ds}, std::vector<float>(obs, obs + n * rows * ds));
+    auto a = act(st.policy, o, std::vector<double>(noise_std, noise_std + n), seed, st.streams,
+                 std::vector<std::uint64_t>(steps, steps + n), deterministic != 0);
+    std::memcpy(out, a.data.data(), a.data.size() * sizeof(float));
+  });
+}
+
+int ref_sacf_act(void* h, const float* obs, std::uint64_t rows, std::uint64_t seed,
+                 const std::uint64_t* steps, int deterministic, float* out) {
+  return guarded([&] {
+    auto& st = *static_cast<SacState<float>*>(h);
+    const std::size_t n = st.members(), ds = st.policy.in_dim();
+    PopTensor<float> o({n, rows, ds}, std::vector<float>(obs, obs + n * rows * ds));
+    auto a = sac_act(st.policy, o, st.action_bound, seed, st.streams,
+                     std::vector<std::uint64_t>(steps, steps + n), deterministic != 0);
+    std::memcpy(out, a.data.data(), a.data.size() * sizeof(float));
+  });
+}
+
 // ---------------------------------------------------------------- synthetic batches
 void ref_synthetic_batches_f(std::uint64_t count, std::uint64_t n, std::uint64_t b,
                              std::uint64_t ds, std::uint64_t da, std::uint64_t seed, float* s,

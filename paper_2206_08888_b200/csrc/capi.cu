@@ -275,6 +275,11 @@ int pbrl_update_batches_losses(pbrl_pop* pop, const pbrl_batch* batches, uint32_
   });
 }
 
+int pbrl_act(pbrl_pop* pop, const float* obs, uint64_t rows, const double* noise_std,
+             uint64_t seed, const uint64_t* steps, int deterministic, float* actions) {
+  return guarded([&] { P(pop)->act(obs, rows, noise_std, seed, steps, deterministic, actions); });
+}
+
 int pbrl_last_losses(pbrl_pop* pop, double* c1, double* c2, double* pl) {
   return guarded([&] {
     Pop* p = P(pop);

@@ -1230,6 +1230,94 @@ void launch_sac_head(int n, int B, int ds, int da, int lsa, const float* head,
              bound, host_logf(bound), static_cast<float*>(sa), x, th, ls, clamped, eps, logp);
 }
 
+// ================================================================== action selection
+// act (algos.hpp:895-915): a = clamp(a + (T)normal(key_m, 2e) * (T)(std_m * bound), +-bound) for
+// members with std_m != 0, key_m = (seed, streams[m], kExploreNoise, steps[m]), e over the
+// member's [rows][da] block; a already holds tanh * bound from the forward.
+__global__ void k_td3_act_noise(int n, long long per, float* a, const double* noise_std,
+                                const uint64_t* streams, const uint64_t* steps, uint64_t seed,
+                                float bound) {
+  PDL_ENTRY();
+  const long long total = static_cast<long long>(n) * per;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / per);
+    if (noise_std[m] == 0.0) continue;
+    const uint64_t e = static_cast<uint64_t>(i - static_cast<long long>(m) * per);
+    const uint64_t key = stream_key(seed, streams[m], kExploreNoise, steps[m]);
+    const float sd = static_cast<float>(noise_std[m] * static_cast<double>(bound));
+    a[i] = clampf_ref(a[i] + static_cast<float>(rng_normal_pair(key, 2 * e)) * sd, -bound, bound);
+  }
+}
+
+void launch_td3_act_noise(int n, long long per, float* a, const double* noise_std,
+                          const uint64_t* streams, const uint64_t* steps, uint64_t seed,
+                          float bound, cudaStream_t s) {
+  const long long total = static_cast<long long>(n) * per;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 8));
+  launch_k(k_td3_act_noise, std::max(blocks, 1), 256, 0, s, n, per, a, noise_std, streams, steps,
+           seed, bound);
+}
+
+// sac_act (algos.hpp:918-942): head [n][rows][2 da] -> mu, log_std clamped to [-20, 2]
+// (split_policy_head :599-616); mu += exp(log_std) * (T)normal(key_m, 2e) unless deterministic;
+// a = tanh(mu) * bound.
+__global__ void k_sac_act(int n, int rows, int da, const float* head, const uint64_t* streams,
+                          const uint64_t* steps, uint64_t seed, int deterministic, float bound,
+                          float* a) {
+  PDL_ENTRY();
+  const long long per = static_cast<long long>(rows) * da, total = per * n;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int m = static_cast<int>(i / per);
+    const long long e = i - static_cast<long long>(m) * per;
+    const long long row = e / da, j = e - row * da;
+    const float* h = head + (static_cast<long long>(m) * rows + row) * 2 * da;
+    float mu = h[j];
+    float ls = h[da + j];
+    if (ls < static_cast<float>(-20.0)) ls = static_cast<float>(-20.0);
+    else if (ls > static_cast<float>(2.0)) ls = static_cast<float>(2.0);
+    if (!deterministic) {
+      const uint64_t key = stream_key(seed, streams[m], kExploreNoise, steps[m]);
+      mu = mu + sac_expf(ls) * static_cast<float>(rng_normal_pair(key, 2 * static_cast<uint64_t>(e)));
+    }
+    a[i] = libm_tanhf(mu) * bound;
+  }
+}
+
+void launch_sac_act(int n, int rows, int da, const float* head, const uint64_t* streams,
+                    const uint64_t* steps, uint64_t seed, int deterministic, float bound, float* a,
+                    cudaStream_t s) {
+  const long long total = static_cast<long long>(n) * rows * da;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 8));
+  launch_k(k_sac_act, std::max(blocks, 1), 256, 0, s, n, rows, da, head, streams, steps, seed,
+           deterministic, bound, a);
+}
+
+// observations [n][rows][ds] (fp32) -> policy-input block [n][rows][ld] (fp32 or bf16)
+template <typename AT>
+__global__ void k_pack_obs(long long rows_total, int ds, int ld, const float* obs, AT* out) {
+  PDL_ENTRY();
+  const long long total = rows_total * ds;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long r = i / ds;
+    act_st(out, r * ld + (i - r * ds), obs[i]);
+  }
+}
+
+void launch_pack_obs(long long rows_total, int ds, int ld, const float* obs, void* out, int act16,
+                     cudaStream_t s) {
+  const long long total = rows_total * ds;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 8));
+  if (act16)
+    launch_k(k_pack_obs<__nv_bfloat16>, std::max(blocks, 1), 256, 0, s, rows_total, ds, ld, obs,
+             static_cast<__nv_bfloat16*>(out));
+  else
+    launch_k(k_pack_obs<float>, std::max(blocks, 1), 256, 0, s, rows_total, ds, ld, obs,
+             static_cast<float*>(out));
+}
+
 // y = rs*r + gamma*(1-d)*(min(Q1',Q2') - alpha*logp')  (algos.hpp:759-774)
 __global__ void k_sac_y(int n, int B, const float* r, const float* d, const float* q2n,
                         const float* logp2, const float* log_alpha, const float* gamma,

@@ -257,6 +257,16 @@ void launch_sac_alpha(int n, int B, const float* logp, const float* log_alpha_in
                       const int64_t* t, const float* corr1, const float* corr2, const float* lr,
                       cudaStream_t s);
 
+// action selection (act / sac_act, algos.hpp:895-942)
+void launch_td3_act_noise(int n, long long per, float* a, const double* noise_std,
+                          const uint64_t* streams, const uint64_t* steps, uint64_t seed,
+                          float bound, cudaStream_t s);
+void launch_sac_act(int n, int rows, int da, const float* head, const uint64_t* streams,
+                    const uint64_t* steps, uint64_t seed, int deterministic, float bound, float* a,
+                    cudaStream_t s);
+void launch_pack_obs(long long rows_total, int ds, int ld, const float* obs, void* out, int act16,
+                     cudaStream_t s);
+
 // replay
 void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t count, int rw,
                            float* ring, cudaStream_t s);

@@ -68,6 +68,15 @@ struct Scratch {
   DBuf<uint8_t> clamped;
 };
 
+// Action-selection scratch (act / sac_act): rows observations per member.
+struct ActScratch {
+  int rows = 0;
+  DBuf<float> obs, in, out, act;       // obs [n][rows][ds] fp32, in: policy-input block
+  std::vector<DBuf<float>> h;          // hidden activations (+ mask bits)
+  DBuf<uint64_t> steps;
+  DBuf<double> noise;
+};
+
 // HBM-resident replay rings (ReplayBuffer, replay.hpp:28-173).
 struct Replay {
   int mode = PBRL_REPLAY_PER_AGENT;
@@ -166,6 +175,9 @@ struct Pop {
   uint64_t t_bound = 0;  // upper bound of every Adam step counter
 
   Scratch S;
+  ActScratch AS;
+  void act(const float* obs, uint64_t rows, const double* noise_std, uint64_t seed,
+           const uint64_t* steps, int deterministic, float* actions);
   Replay* replay = nullptr;
 
   bool prof_on = false;

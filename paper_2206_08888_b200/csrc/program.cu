@@ -1022,6 +1022,64 @@ void Pop::sac_step(int B) {
   });
 }
 
+// ------------------------------------------------------------------ action selection
+// act / sac_act (algos.hpp:895-942) for the whole population: H2D of obs [n][rows][ds], the
+// policy forward in the population's precision mode (bit-exact in FFMA32), exploration noise
+// keyed (seed, streams[m], kExploreNoise, steps[m]), D2H of the actions [n][rows][da].
+void Pop::act(const float* obs, uint64_t rows_, const double* noise_std, uint64_t seed,
+              const uint64_t* steps_h, int deterministic, float* actions) {
+  if (rows_ < 1) PBRL_THROW(PBRL_E_SHAPE, "act: observations need at least one row");
+  if (!obs || !actions || !steps_h) PBRL_THROW(PBRL_E_USAGE, "act: null argument");
+  if (algo == PBRL_ALGO_TD3 && !deterministic && !noise_std)
+    PBRL_THROW(PBRL_E_USAGE, "act: noise_std is required unless deterministic");
+  const int rows = static_cast<int>(rows_);
+  const int L = pol.depth, nout = pol.dims[L];
+  const long long nr = static_cast<long long>(n) * rows;
+  const int ldi = padl(ds);
+  if (rows > AS.rows) {
+    AS = ActScratch{};
+    AS.rows = rows;
+    AS.obs.alloc(nr * ds);
+    AS.in.alloc(nr * ldi);
+    AS.in.zero(stream);
+    AS.out.alloc(nr * nout);
+    AS.act.alloc(nr * da);
+    for (int l = 0; l + 1 < L; ++l) {
+      const size_t h = static_cast<size_t>(padl(pol.dims[l + 1])) + (pol.dims[l + 1] + 31) / 32;
+      AS.h.emplace_back();
+      AS.h.back().alloc(nr * h);
+      AS.h.back().zero(stream);
+    }
+    AS.steps.alloc(n);
+    AS.noise.alloc(n);
+  }
+  if (act16() && weights_dirty) refresh_shadows();
+  AS.steps.upload(steps_h, n, stream);
+  if (noise_std) AS.noise.upload(noise_std, n, stream);
+  CUDA_CHECK(cudaMemcpyAsync(AS.obs.p, obs, nr * ds * 4, cudaMemcpyHostToDevice, stream));
+  launch_pack_obs(nr, ds, ldi, AS.obs.p, AS.in.p, act16() ? 1 : 0, stream);
+  count_launch(1);
+  const Mat x{AS.in.p, static_cast<long long>(rows) * ldi, ldi, 0};
+  if (algo == PBRL_ALGO_TD3) {
+    mlp_forward(pol, pol_p.p, n, rows, x, AS.h, AS.act.p, static_cast<long long>(rows) * da, da,
+                EPI_BIAS_TANH, nullptr, nullptr, 0, 0, false, false, false);
+    if (!deterministic) {
+      launch_td3_act_noise(n, static_cast<long long>(rows) * da, AS.act.p, AS.noise.p, streams.p,
+                           AS.steps.p, seed, bound, stream);
+      count_launch(1);
+    }
+  } else {
+    mlp_forward(pol, pol_p.p, n, rows, x, AS.h, AS.out.p, static_cast<long long>(rows) * nout,
+                nout, EPI_BIAS, nullptr, nullptr, 0, 0, false, false, false);
+    launch_sac_act(n, rows, da, AS.out.p, streams.p, AS.steps.p, seed, deterministic, bound,
+                   AS.act.p, stream);
+    count_launch(1);
+  }
+  CUDA_CHECK(cudaMemcpyAsync(actions, AS.act.p, nr * da * 4, cudaMemcpyDeviceToHost, stream));
+  sync();
+  CUDA_CHECK(cudaGetLastError());
+}
+
 // ------------------------------------------------------------------ one step (graph replay)
 void Pop::run_program(int B, const uint8_t* d_mask) {
   if (algo == PBRL_ALGO_TD3) td3_step(B, d_mask);

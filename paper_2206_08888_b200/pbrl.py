@@ -477,6 +477,39 @@ def update_k_steps(st, sampler: Callable[[], Optional[TransitionBatch]], k: int,
     return st._update(batches, return_losses=return_losses)
 
 
+# ---------------------------------------------------------------------- action selection
+def _act(st, obs, noise_std, seed, steps, deterministic):
+    obs = np.ascontiguousarray(obs, np.float32)
+    if obs.ndim != 3 or obs.shape[0] != st.n or obs.shape[2] != st.obs_dim:
+        raise ShapeError(f"act: observations {list(obs.shape)} do not match "
+                         f"[{st.n}, rows, {st.obs_dim}]")
+    steps = np.ascontiguousarray(steps, np.uint64)
+    if steps.shape != (st.n,):
+        raise ShapeError("act: one step counter per member")
+    ns = None
+    if noise_std is not None:
+        ns = np.ascontiguousarray(noise_std, np.float64)
+        if ns.shape != (st.n,):
+            raise ShapeError("act: one noise_std per member")
+    out = np.empty((st.n, obs.shape[1], st.act_dim), np.float32)
+    _lib.call("pbrl_act", st._h, _ptr(obs, _lib.f32p), obs.shape[1],
+              _ptr(ns, _lib.f64p) if ns is not None else None, seed, _ptr(steps, _lib.u64p),
+              1 if deterministic else 0, _ptr(out, _lib.f32p))
+    return out
+
+
+def act(st: "Td3State", obs, noise_std, seed: int, steps, deterministic: bool = False):
+    """act (algos.hpp:895-915): tanh policy output plus clipped Gaussian exploration noise for
+    every member, obs [n, rows, obs_dim] -> actions [n, rows, act_dim]; noise keyed by
+    (seed, the state's member streams, kExploreNoise, steps[m])."""
+    return _act(st, obs, noise_std, seed, steps, deterministic)
+
+
+def sac_act(st: "SacState", obs, seed: int, steps, deterministic: bool = False):
+    """sac_act (algos.hpp:918-942): bound * tanh(mu + sigma * eps), or the mode."""
+    return _act(st, obs, None, seed, steps, deterministic)
+
+
 # ---------------------------------------------------------------------- replay
 @dataclass
 class Transition:

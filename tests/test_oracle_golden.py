@@ -99,3 +99,15 @@ def test_tanhf_golden():
     libm.tanhf.argtypes = [C.c_float]
     got = np.asarray([libm.tanhf(float(v)) for v in g["x"]], np.float32)
     assert bits_equal(got, g["y"])
+
+
+def test_act_golden(ora):
+    """act / sac_act of the restatement vs the reference's outputs (algos.hpp:895-942)."""
+    g = _load("act")
+    for algo in ("td3", "sac"):
+        st = (ora.td3 if algo == "td3" else ora.sac)(int(g["n"]), int(g["ds"]), int(g["da"]),
+                                                     [int(h) for h in g["hidden"]], 1.0,
+                                                     int(g["state_seed"]))
+        for det in (0, 1):
+            got = st.act(g["obs"], int(g["seed"]), g["steps"], g["noise"], bool(det))
+            assert bits_equal(got, g[f"{algo}_det{det}"]), (algo, det)

@@ -147,3 +147,19 @@ def test_pbt_evolve_trainer(ora, ref):
     assert np.array_equal(a[0], b[0]) and a[2] == b[2]
     for f in a[3]:
         assert np.array_equal(a[3][f], b[3][f]), f
+
+
+@pytest.mark.parametrize("algo", ["td3", "sac"])
+def test_act_bitexact(ora, ref, algo):
+    """act / sac_act (algos.hpp:895-942): restatement == reference, several row counts."""
+    rng = np.random.default_rng(3)
+    for rows, hidden in ((1, [16, 16]), (7, [32, 32])):
+        o = (ora.td3 if algo == "td3" else ora.sac)(4, 11, 3, hidden, 2.0, 9)
+        r = (ref.td3 if algo == "td3" else ref.sac)(4, 11, 3, hidden, 2.0, 9)
+        obs = rng.uniform(-1, 1, (4, rows, 11)).astype(np.float32)
+        steps = np.asarray([0, 5, 17, 2], np.uint64)
+        noise = [0.1, 0.0, 0.5, 0.2]
+        for det in (False, True):
+            a = o.act(obs, 123, steps, noise, det)
+            b = r.act(obs, 123, steps, noise, det)
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (rows, det)
