@@ -26,6 +26,10 @@ int main() {
   for (float x : st.flatten_member(pb::Net::kPolicy, 0)) sum += x;
   std::printf("policy[0] checksum %.6f steps %llu\n", sum,
               static_cast<unsigned long long>(st.steps()[0]));
+  // act (algos.hpp:895-915): one observation per member, exploration std 0.1
+  std::vector<float> obs(n * ds, 0.5f);
+  const auto acts = pb::act(st, obs, 1, std::vector<double>(n, 0.1), 7, st.steps(), false);
+  std::printf("act: %zu actions, a[0] = %.4f\n", acts.size(), acts[0]);
   try {
     hy.tau[0] = 2.0;
     pb::td3_update_step(st, b, hy);

@@ -169,6 +169,8 @@ class Population {
   Population(Population&& o) noexcept : h_(o.h_), n_(o.n_), ds_(o.ds_), da_(o.da_) { o.h_ = nullptr; }
 
   std::size_t members() const { return n_; }
+  std::size_t obs_dim() const { return ds_; }
+  std::size_t act_dim() const { return da_; }
   pbrl_pop* handle() const { return h_; }
 
   std::vector<float> flatten_member(Net net, std::size_t i) const {  // net_pop.hpp:163-173
@@ -250,6 +252,31 @@ inline void td3_update_step(Td3State& st, const TransitionBatch& batch, const Td
   std::vector<std::uint8_t> mask;
   if (policy_member_mask) mask.assign(policy_member_mask->begin(), policy_member_mask->end());
   check(pbrl_update_batches(st.h_, &b, 1, batch.rows, mask.empty() ? nullptr : mask.data()));
+}
+
+// act (algos.hpp:895-915) / sac_act (:918-942): obs [n][rows][obs_dim] -> actions
+// [n][rows][act_dim], exploration noise keyed by (seed, member streams, kExploreNoise, steps[m])
+inline std::vector<float> act(Td3State& st, const std::vector<float>& obs, std::size_t rows,
+                              const std::vector<double>& noise_std, std::uint64_t seed,
+                              const std::vector<std::uint64_t>& steps, bool deterministic) {
+  if (obs.size() != st.members() * rows * st.obs_dim() || steps.size() != st.members() ||
+      noise_std.size() != st.members())
+    throw ShapeError("act: observation / steps / noise_std extents do not match the population");
+  std::vector<float> out(st.members() * rows * st.act_dim());
+  check(pbrl_act(st.handle(), obs.data(), rows, noise_std.data(), seed, steps.data(),
+                 deterministic ? 1 : 0, out.data()));
+  return out;
+}
+
+inline std::vector<float> sac_act(SacState& st, const std::vector<float>& obs, std::size_t rows,
+                                  std::uint64_t seed, const std::vector<std::uint64_t>& steps,
+                                  bool deterministic) {
+  if (obs.size() != st.members() * rows * st.obs_dim() || steps.size() != st.members())
+    throw ShapeError("sac_act: observation / steps extents do not match the population");
+  std::vector<float> out(st.members() * rows * st.act_dim());
+  check(pbrl_act(st.handle(), obs.data(), rows, nullptr, seed, steps.data(),
+                 deterministic ? 1 : 0, out.data()));
+  return out;
 }
 
 inline void sac_update_step(SacState& st, const TransitionBatch& batch, const SacHyper& hyper) {
