@@ -137,6 +137,15 @@ int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t sample_seed, uint64_t firs
  * each [n] (TD3 policy entries are 0 for members that did not fire). */
 int pbrl_last_losses(pbrl_pop* pop, double* critic1, double* critic2, double* policy);
 
+/* ---- checkpoints: save_checkpoint / load_checkpoint (PBRLNET1, net_pop.hpp:224-304) of one
+ * network (PBRL_NET_*) of the population, fp32, byte-compatible with the reference's files;
+ * load requires the file's population size / extents / output activation / scale to match
+ * (ConfigError otherwise, like a bad magic or truncated file).  serialize_state
+ * (algos.hpp:989-1015, TD3): the reference's full-state export byte for byte. */
+int pbrl_save_checkpoint(pbrl_pop* pop, int net, const char* path);
+int pbrl_load_checkpoint(pbrl_pop* pop, int net, const char* path);
+int pbrl_serialize_state(pbrl_pop* pop, const char* path);
+
 /* ---- action selection: act (TD3, algos.hpp:895-915) / sac_act (SAC, :918-942) for every
  * member on rows observations each, keyed by the population's member streams: obs [n][rows][ds]
  * and actions [n][rows][da] are host arrays; steps [n] key the per-member kExploreNoise streams;

@@ -222,6 +222,9 @@ class Ref(_Lib):
         F("ref_synthetic_batches_f", None, u64, u64, u64, u64, u64, u64, f32p, f32p, f32p, f32p,
           f32p)
         F("ref_td3f_act", C.c_int, vp, f32p, u64, f64p, u64, u64p, C.c_int, f32p)
+        F("ref_td3f_save_checkpoint", C.c_int, vp, C.c_int, C.c_char_p)
+        F("ref_td3f_load_checkpoint", C.c_int, vp, C.c_int, C.c_char_p)
+        F("ref_td3f_serialize_state", C.c_int, vp, C.c_char_p)
         F("ref_sacf_act", C.c_int, vp, f32p, u64, u64, u64p, C.c_int, f32p)
         F("ref_replay_create", vp, u64, u64, u64)
         F("ref_replay_destroy", None, vp)

@@ -14,6 +14,7 @@
 //   pbt_rank / pbt_plan / pbt_evolve_trainer   evolve.hpp:112, :133, :169, :192
 //   bench_update                     bench.hpp:137
 #include <cstring>
+#include <fstream>
 #include <memory>
 #include <optional>
 #include <vector>
@@ -379,6 +380,22 @@ int ref_sacf_act(void* h, const float* obs, std::uint64_t rows, std::uint64_t se
     auto a = sac_act(st.policy, o, st.action_bound, seed, st.streams,
                      std::vector<std::uint64_t>(steps, steps + n), deterministic != 0);
     std::memcpy(out, a.data.data(), a.data.size() * sizeof(float));
+  });
+}
+
+// ---------------------------------------------------------------- checkpoints (float)
+int ref_td3f_save_checkpoint(void* h, int net, const char* path) {
+  return guarded([&] { save_checkpoint(td3_net(*static_cast<Td3State<float>*>(h), net), std::string(path)); });
+}
+int ref_td3f_load_checkpoint(void* h, int net, const char* path) {
+  return guarded([&] {
+    td3_net(*static_cast<Td3State<float>*>(h), net) = load_checkpoint<float>(std::string(path));
+  });
+}
+int ref_td3f_serialize_state(void* h, const char* path) {
+  return guarded([&] {
+    std::ofstream os(path, std::ios::binary);
+    serialize_state(*static_cast<Td3State<float>*>(h), os);
   });
 }
 

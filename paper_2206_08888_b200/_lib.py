@@ -57,6 +57,9 @@ SIGNATURES = {
     "pbrl_update_batches_device": [vp, C.POINTER(Batch), u32, u64, u8p],
     "pbrl_update_batches_losses": [vp, C.POINTER(Batch), u32, u64, u8p, f64p],
     "pbrl_act": [vp, f32p, u64, f64p, u64, u64p, C.c_int, f32p],
+    "pbrl_save_checkpoint": [vp, C.c_int, C.c_char_p],
+    "pbrl_load_checkpoint": [vp, C.c_int, C.c_char_p],
+    "pbrl_serialize_state": [vp, C.c_char_p],
     "pbrl_update_k": [vp, u32, u64, u64, u64, u64, intp],
     "pbrl_last_losses": [vp, f64p, f64p, f64p],
     "pbrl_replay_create": [vp, u64, C.c_int],

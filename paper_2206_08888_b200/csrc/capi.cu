@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <string>
 #include <unordered_map>
 
@@ -97,11 +98,157 @@ const NetShape& Pop::net_shape(int net) const {
   return (net == PBRL_NET_POLICY || net == PBRL_NET_POLICY_TARGET) ? pol : cri;
 }
 
+// ---------------------------------------------------------------- PBRLNET1 (net_pop.hpp:224-304)
+namespace {
+constexpr char kNetMagic[8] = {'P', 'B', 'R', 'L', 'N', 'E', 'T', '1'};
+
+template <typename V>
+void put(std::ostream& os, const V& v) {
+  os.write(reinterpret_cast<const char*>(&v), sizeof(V));
+}
+template <typename V>
+V get(std::istream& is) {
+  V v{};
+  is.read(reinterpret_cast<char*>(&v), sizeof(V));
+  return v;
+}
+
+// the whole population of one network, member rows in flatten_member order
+std::vector<float> net_rows(Pop* p, int net) {
+  const NetShape& sh = p->net_shape(net);
+  std::vector<float> flat(static_cast<size_t>(p->n) * sh.P);
+  CUDA_CHECK(cudaMemcpy2DAsync(flat.data(), sh.P * 4, p->net_row(net, 0), sh.stride * 4,
+                               sh.P * 4, p->n, cudaMemcpyDeviceToHost, p->stream));
+  p->sync();
+  return flat;
+}
+
+// save_checkpoint (net_pop.hpp:245-261): magic, u32 value bytes, u64 N, u64 extent count,
+// u64 extents, u8 output activation, f64 output scale, members flattened in index order
+void save_net(Pop* p, int net, std::ostream& os) {
+  const NetShape& sh = p->net_shape(net);
+  const std::vector<float> flat = net_rows(p, net);
+  os.write(kNetMagic, sizeof(kNetMagic));
+  put<uint32_t>(os, 4);
+  put<uint64_t>(os, static_cast<uint64_t>(p->n));
+  put<uint64_t>(os, static_cast<uint64_t>(sh.depth + 1));
+  for (int l = 0; l <= sh.depth; ++l) put<uint64_t>(os, static_cast<uint64_t>(sh.dims[l]));
+  put<uint8_t>(os, static_cast<uint8_t>(sh.out_act));
+  put<double>(os, static_cast<double>(sh.out_scale));
+  os.write(reinterpret_cast<const char*>(flat.data()),
+           static_cast<std::streamsize>(flat.size() * 4));
+}
+}  // namespace
+
 }  // namespace pbrl
 
 using namespace pbrl;
 
 extern "C" {
+
+int pbrl_save_checkpoint(pbrl_pop* pop, int net, const char* path) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    p->net_row(net, 0);  // validates the network id
+    std::ofstream os(path ? path : "", std::ios::binary);
+    if (!path || !os) PBRL_THROW(PBRL_E_CONFIG, std::string("save_checkpoint: cannot open ") + (path ? path : "(null)"));
+    save_net(p, net, os);
+    if (!os) PBRL_THROW(PBRL_E_RESOURCE, "save_checkpoint: write failed");
+  });
+}
+
+// load_checkpoint (net_pop.hpp:264-296) into an existing population: the file's population
+// size, extents, activation and scale must match this network (ConfigError otherwise, as the
+// reference raises for a bad magic / precision / truncated file)
+int pbrl_load_checkpoint(pbrl_pop* pop, int net, const char* path) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    const NetShape& sh = p->net_shape(net);
+    float* dst0 = p->net_row(net, 0);
+    std::ifstream is(path ? path : "", std::ios::binary);
+    if (!path || !is) PBRL_THROW(PBRL_E_CONFIG, std::string("load_checkpoint: cannot open ") + (path ? path : "(null)"));
+    char magic[8];
+    is.read(magic, sizeof(magic));
+    if (!is || std::memcmp(magic, kNetMagic, sizeof(magic)) != 0)
+      PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: bad magic");
+    const uint32_t prec = get<uint32_t>(is);
+    if (prec != 4)
+      PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: file stores " + std::to_string(prec * 8) +
+                                    "-bit values but 32-bit was requested");
+    const uint64_t fn = get<uint64_t>(is), nd = get<uint64_t>(is);
+    if (fn != static_cast<uint64_t>(p->n))
+      PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: population size " + std::to_string(fn) +
+                                    " != " + std::to_string(p->n));
+    if (nd != static_cast<uint64_t>(sh.depth + 1))
+      PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: network depth mismatch");
+    for (int l = 0; l <= sh.depth; ++l)
+      if (get<uint64_t>(is) != static_cast<uint64_t>(sh.dims[l]))
+        PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: layer extents mismatch");
+    const uint8_t act = get<uint8_t>(is);
+    const double scale = get<double>(is);
+    if (act != static_cast<uint8_t>(sh.out_act) ||
+        static_cast<float>(scale) != sh.out_scale)
+      PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: output activation / scale mismatch");
+    std::vector<float> flat(static_cast<size_t>(p->n) * sh.P);
+    is.read(reinterpret_cast<char*>(flat.data()), static_cast<std::streamsize>(flat.size() * 4));
+    if (!is) PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: truncated file");
+    CUDA_CHECK(cudaMemcpy2DAsync(dst0, sh.stride * 4, flat.data(), sh.P * 4, sh.P * 4, p->n,
+                                 cudaMemcpyHostToDevice, p->stream));
+    p->weights_dirty = true;
+    p->sync();
+  });
+}
+
+// serialize_state (algos.hpp:989-1015), TD3: six PBRLNET1 checkpoints, then per optimizer
+// (policy, critic1, critic2) for every layer the weight AdamState (m, v, t) and then every
+// layer's bias AdamState, then delay_acc and steps
+int pbrl_serialize_state(pbrl_pop* pop, const char* path) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    if (p->algo != PBRL_ALGO_TD3) PBRL_THROW(PBRL_E_USAGE, "serialize_state: TD3 only (as the reference)");
+    std::ofstream os(path ? path : "", std::ios::binary);
+    if (!path || !os) PBRL_THROW(PBRL_E_CONFIG, std::string("serialize_state: cannot open ") + (path ? path : "(null)"));
+    for (int net = 0; net < 6; ++net) save_net(p, net, os);
+    const int n = p->n;
+    auto dump_adam = [&](const NetShape& sh, const float* m_arena, const float* v_arena,
+                         const int64_t* t_dev) {
+      std::vector<float> m(static_cast<size_t>(n) * sh.P), v(m.size());
+      std::vector<int64_t> t(n);
+      CUDA_CHECK(cudaMemcpy2DAsync(m.data(), sh.P * 4, m_arena, sh.stride * 4, sh.P * 4, n,
+                                   cudaMemcpyDeviceToHost, p->stream));
+      CUDA_CHECK(cudaMemcpy2DAsync(v.data(), sh.P * 4, v_arena, sh.stride * 4, sh.P * 4, n,
+                                   cudaMemcpyDeviceToHost, p->stream));
+      CUDA_CHECK(cudaMemcpyAsync(t.data(), t_dev, 8 * n, cudaMemcpyDeviceToHost, p->stream));
+      p->sync();
+      auto seg = [&](const std::vector<float>& a, size_t off, size_t cnt) {
+        for (int mm = 0; mm < n; ++mm)
+          os.write(reinterpret_cast<const char*>(a.data() + static_cast<size_t>(mm) * sh.P + off),
+                   static_cast<std::streamsize>(cnt * 4));
+      };
+      for (int pass = 0; pass < 2; ++pass) {  // weights of every layer, then biases
+        for (int l = 0; l < sh.depth; ++l) {
+          const size_t off = pass == 0 ? sh.woff[l] : sh.boff[l];
+          const size_t cnt = static_cast<size_t>(sh.dims[l + 1]) * (pass == 0 ? sh.dims[l] : 1);
+          seg(m, off, cnt);
+          seg(v, off, cnt);
+          os.write(reinterpret_cast<const char*>(t.data()), 8 * n);
+        }
+      }
+    };
+    dump_adam(p->pol, p->pol_m.p, p->pol_v.p, p->t_pol.p);
+    dump_adam(p->cri, p->cri_m.p, p->cri_v.p, p->t_cri.p);
+    dump_adam(p->cri, p->cri_m.p + static_cast<size_t>(n) * p->cri.stride,
+              p->cri_v.p + static_cast<size_t>(n) * p->cri.stride, p->t_cri.p + n);
+    std::vector<double> acc(n);
+    std::vector<uint64_t> steps(n);
+    CUDA_CHECK(cudaMemcpyAsync(acc.data(), p->delay_acc.p, 8 * n, cudaMemcpyDeviceToHost, p->stream));
+    CUDA_CHECK(cudaMemcpyAsync(steps.data(), p->steps.p, 8 * n, cudaMemcpyDeviceToHost, p->stream));
+    p->sync();
+    os.write(reinterpret_cast<const char*>(acc.data()), 8 * n);
+    os.write(reinterpret_cast<const char*>(steps.data()), 8 * n);
+    if (!os) PBRL_THROW(PBRL_E_RESOURCE, "serialize_state: write failed");
+  });
+}
 
 int pbrl_version(int* major, int* minor) {
   if (major) *major = 0;

@@ -477,6 +477,24 @@ def update_k_steps(st, sampler: Callable[[], Optional[TransitionBatch]], k: int,
     return st._update(batches, return_losses=return_losses)
 
 
+# ---------------------------------------------------------------------- checkpoints
+def save_checkpoint(st, net, path) -> None:
+    """save_checkpoint (net_pop.hpp:245-261): one network of the population as a PBRLNET1 file
+    (fp32), readable by the reference's load_checkpoint."""
+    _lib.call("pbrl_save_checkpoint", st._h, NETS.get(net, net), str(path).encode())
+
+
+def load_checkpoint(st, net, path) -> None:
+    """load_checkpoint (net_pop.hpp:264-296) into network `net` of an existing population (the
+    file's population size, extents, activation and scale must match)."""
+    _lib.call("pbrl_load_checkpoint", st._h, NETS.get(net, net), str(path).encode())
+
+
+def serialize_state(st, path) -> None:
+    """serialize_state (algos.hpp:989-1015): the TD3 state export, byte-identical layout."""
+    _lib.call("pbrl_serialize_state", st._h, str(path).encode())
+
+
 # ---------------------------------------------------------------------- action selection
 def _act(st, obs, noise_std, seed, steps, deterministic):
     obs = np.ascontiguousarray(obs, np.float32)

@@ -1,0 +1,73 @@
+"""On-disk formats of the device state: PBRLNET1 checkpoints
+(net_pop.hpp:224-304) and serialize_state (algos.hpp:989-1015), byte-compatible with the
+reference build (oracle/_ref, travels with the repo as a built .so)."""
+import numpy as np
+import pytest
+
+from helpers import TD3_NETS, raw_at, to_batch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb(cuda):
+    import paper_2206_08888_b200 as pb
+    return pb
+
+
+def _stepped(pb, ref, n, hidden, K, seed):
+    from oracle.oracle import td3_defaults
+    st = pb.make_td3_state(n, 17, 6, hidden, 1.0, seed, precision="ffma32")
+    r = ref.td3(n, 17, 6, hidden, 1.0, seed)
+    raw = ref.synthetic_batches(K, n, 32, 17, 6, seed)
+    hy = pb.Td3Hyper.defaults(n)
+    for k in range(K):
+        pb.td3_update_step(st, to_batch(pb, raw, k), hy)
+        r.step(raw_at(raw, k), td3_defaults(n))
+    return st, r
+
+
+def test_serialize_state_matches_reference_bytes(pb, ref, tmp_path):
+    st, r = _stepped(pb, ref, 3, [32, 32], 4, 21)
+    pb.serialize_state(st, tmp_path / "dev.bin")
+    assert ref.lib.ref_td3f_serialize_state(r.h, str(tmp_path / "ref.bin").encode()) == 0
+    a = (tmp_path / "dev.bin").read_bytes()
+    b = (tmp_path / "ref.bin").read_bytes()
+    assert len(a) == len(b) and a == b
+
+
+def test_checkpoint_roundtrip_with_reference(pb, ref, tmp_path):
+    st, r = _stepped(pb, ref, 2, [32, 32], 2, 5)
+    for k, net in enumerate(TD3_NETS):
+        # device -> reference
+        p = tmp_path / f"dev_{net}.pbrl"
+        pb.save_checkpoint(st, net, p)
+        fresh = ref.td3(2, 17, 6, [32, 32], 1.0, 99)
+        assert ref.lib.ref_td3f_load_checkpoint(fresh.h, k, str(p).encode()) == 0
+        assert np.array_equal(fresh.get_net(net), st.params(net)), net
+        # reference -> device
+        q = tmp_path / f"ref_{net}.pbrl"
+        assert ref.lib.ref_td3f_save_checkpoint(r.h, k, str(q).encode()) == 0
+        assert p.read_bytes() == q.read_bytes()
+        other = pb.make_td3_state(2, 17, 6, [32, 32], 1.0, 77, precision="bf16")
+        pb.load_checkpoint(other, net, q)
+        assert np.array_equal(other.params(net), r.get_net(net)), net
+
+
+def test_load_checkpoint_rejects_mismatch(pb, tmp_path):
+    a = pb.make_td3_state(2, 17, 6, [32, 32], 1.0, 1, precision="ffma32")
+    b = pb.make_td3_state(3, 17, 6, [32, 32], 1.0, 1, precision="ffma32")
+    p = tmp_path / "a.pbrl"
+    pb.save_checkpoint(a, "policy", p)
+    with pytest.raises(pb.ConfigError):
+        pb.load_checkpoint(b, "policy", p)
+    with pytest.raises(pb.ConfigError):
+        pb.load_checkpoint(a, "critic1", p)
+    bad = tmp_path / "bad.pbrl"
+    bad.write_bytes(b"NOTPBRL!" + p.read_bytes()[8:])
+    with pytest.raises(pb.ConfigError):
+        pb.load_checkpoint(a, "policy", bad)
+    trunc = tmp_path / "trunc.pbrl"
+    trunc.write_bytes(p.read_bytes()[:-8])
+    with pytest.raises(pb.ConfigError):
+        pb.load_checkpoint(a, "policy", trunc)
