@@ -159,6 +159,10 @@ int pbrl_act(pbrl_pop* pop, const float* obs, uint64_t rows, const double* noise
 int pbrl_replay_create(pbrl_pop* pop, uint64_t capacity, int mode);
 int pbrl_replay_insert(pbrl_pop* pop, const float* s, const float* a, const float* r,
                        const float* s2, const float* done, const uint32_t* member, uint64_t count);
+/* ReplayBuffer::save_snapshot / load_snapshot (PBRLBUF1, replay.hpp:113-165) of ring `buffer`,
+ * byte-compatible with the reference's files; load requires the same capacity / dims. */
+int pbrl_replay_save_snapshot(pbrl_pop* pop, uint64_t buffer, const char* path);
+int pbrl_replay_load_snapshot(pbrl_pop* pop, uint64_t buffer, const char* path);
 int pbrl_replay_size(pbrl_pop* pop, uint64_t buffer, uint64_t* size);
 /* sample_batch (replay.hpp:181-204) into host arrays shaped like pbrl_batch; *ready as above */
 int pbrl_sample_batch(pbrl_pop* pop, uint64_t sample_seed, uint64_t draw_id, uint64_t batch_rows,

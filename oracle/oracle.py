@@ -230,6 +230,8 @@ class Ref(_Lib):
         F("ref_replay_destroy", None, vp)
         F("ref_replay_push", None, vp, f32p, f32p, C.c_float, f32p, C.c_float, u32)
         F("ref_replay_size", u64, vp)
+        F("ref_replay_save_snapshot", C.c_int, vp, C.c_char_p)
+        F("ref_replay_load_snapshot", vp, C.c_char_p)
         F("ref_sample_batch", C.c_int, C.POINTER(vp), u64, u64, C.c_int, u64, u64, u64p, u64, u64,
           f32p, f32p, f32p, f32p, f32p)
         F("ref_pbt_rank", C.c_int, f64p, u32p, u64, u64, u64p)

@@ -383,6 +383,18 @@ int ref_sacf_act(void* h, const float* obs, std::uint64_t rows, std::uint64_t se
   });
 }
 
+// ---------------------------------------------------------------- replay snapshots (float)
+int ref_replay_save_snapshot(void* h, const char* path) {
+  return guarded([&] {
+    std::ofstream os(path, std::ios::binary);
+    static_cast<ReplayBuffer<float>*>(h)->save_snapshot(os);
+  });
+}
+void* ref_replay_load_snapshot(const char* path) {
+  std::ifstream is(path, std::ios::binary);
+  return ReplayBuffer<float>::load_snapshot(is).release();
+}
+
 // ---------------------------------------------------------------- checkpoints (float)
 int ref_td3f_save_checkpoint(void* h, int net, const char* path) {
   return guarded([&] { save_checkpoint(td3_net(*static_cast<Td3State<float>*>(h), net), std::string(path)); });

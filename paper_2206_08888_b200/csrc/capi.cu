@@ -460,6 +460,7 @@ int pbrl_replay_create(pbrl_pop* pop, uint64_t capacity, int mode) {
       throw;
     }
     r->inserts.assign(r->nbuf, 0);
+    r->member.assign(static_cast<size_t>(r->nbuf) * capacity, 0u);
     delete p->replay;
     p->replay = r;
     p->sync();
@@ -481,6 +482,7 @@ int pbrl_replay_insert(pbrl_pop* pop, const float* s, const float* a, const floa
       if (buf >= static_cast<uint64_t>(r->nbuf))
         PBRL_THROW(PBRL_E_USAGE, "replay insert: member id out of range");
       dst[i] = buf * r->cap + (r->inserts[buf] % r->cap);
+      r->member[dst[i]] = member[i];
       r->inserts[buf]++;
     }
     std::unordered_map<uint64_t, uint64_t> last;
@@ -506,6 +508,89 @@ int pbrl_replay_insert(pbrl_pop* pop, const float* s, const float* a, const floa
     r->stage_dst.upload(rdst.data(), rdst.size(), p->stream);
     launch_replay_scatter(r->stage_rows.p, r->stage_dst.p, rdst.size(), rw, r->ring.p, p->stream);
     p->count_launch(1);
+    std::vector<uint64_t> sz(r->nbuf);
+    for (int b = 0; b < r->nbuf; ++b) sz[b] = std::min<uint64_t>(r->inserts[b], r->cap);
+    r->sizes.upload(sz.data(), r->nbuf, p->stream);
+    p->sync();
+  });
+}
+
+// ReplayBuffer::save_snapshot (replay.hpp:113-139): "PBRLBUF1", u32 value bytes, u64 capacity,
+// obs_dim, act_dim, insert count, then s [cap][ds], a [cap][da], s2 [cap][ds], r [cap],
+// done [cap] (every physical slot) and the u32 member ids
+int pbrl_replay_save_snapshot(pbrl_pop* pop, uint64_t buffer, const char* path) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    Replay* r = p->replay;
+    if (!r) PBRL_THROW(PBRL_E_USAGE, "replay buffer not created");
+    if (buffer >= static_cast<uint64_t>(r->nbuf)) PBRL_THROW(PBRL_E_USAGE, "replay: buffer out of range");
+    std::ofstream os(path ? path : "", std::ios::binary);
+    if (!path || !os) PBRL_THROW(PBRL_E_CONFIG, "save_snapshot: cannot open file");
+    const uint64_t cap = r->cap, ds = p->ds, da = p->da;
+    std::vector<float> ring(cap * r->rw);
+    CUDA_CHECK(cudaMemcpyAsync(ring.data(), r->ring.p + buffer * cap * r->rw, ring.size() * 4,
+                               cudaMemcpyDeviceToHost, p->stream));
+    p->sync();
+    os.write("PBRLBUF1", 8);
+    put<uint32_t>(os, 4);
+    put<uint64_t>(os, cap);
+    put<uint64_t>(os, ds);
+    put<uint64_t>(os, da);
+    put<uint64_t>(os, r->inserts[buffer]);
+    auto cols = [&](uint64_t c0, uint64_t w) {
+      std::vector<float> v(cap * w);
+      for (uint64_t i = 0; i < cap; ++i)
+        std::memcpy(&v[i * w], &ring[i * r->rw + c0], 4 * w);
+      os.write(reinterpret_cast<const char*>(v.data()), static_cast<std::streamsize>(v.size() * 4));
+    };
+    cols(0, ds);                  // s
+    cols(ds, da);                 // a
+    cols(ds + da, ds);            // s2
+    cols(2 * ds + da, 1);         // r
+    cols(2 * ds + da + 1, 1);     // done
+    os.write(reinterpret_cast<const char*>(r->member.data() + buffer * cap),
+             static_cast<std::streamsize>(cap * 4));
+    if (!os) PBRL_THROW(PBRL_E_RESOURCE, "save_snapshot: write failed");
+  });
+}
+
+// ReplayBuffer::load_snapshot (replay.hpp:141-165) into ring `buffer` of this population's
+// replay (the file's capacity / obs_dim / act_dim must match it)
+int pbrl_replay_load_snapshot(pbrl_pop* pop, uint64_t buffer, const char* path) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    Replay* r = p->replay;
+    if (!r) PBRL_THROW(PBRL_E_USAGE, "replay buffer not created");
+    if (buffer >= static_cast<uint64_t>(r->nbuf)) PBRL_THROW(PBRL_E_USAGE, "replay: buffer out of range");
+    std::ifstream is(path ? path : "", std::ios::binary);
+    if (!path || !is) PBRL_THROW(PBRL_E_CONFIG, "load_snapshot: cannot open file");
+    char magic[8];
+    is.read(magic, 8);
+    if (!is || std::memcmp(magic, "PBRLBUF1", 8) != 0)
+      PBRL_THROW(PBRL_E_CONFIG, "ReplayBuffer::load_snapshot: bad magic");
+    if (get<uint32_t>(is) != 4) PBRL_THROW(PBRL_E_CONFIG, "ReplayBuffer::load_snapshot: precision mismatch");
+    const uint64_t cap = get<uint64_t>(is), ds = get<uint64_t>(is), da = get<uint64_t>(is);
+    const uint64_t ins = get<uint64_t>(is);
+    if (cap != r->cap || ds != static_cast<uint64_t>(p->ds) || da != static_cast<uint64_t>(p->da))
+      PBRL_THROW(PBRL_E_CONFIG, "load_snapshot: capacity / dims differ from this replay buffer");
+    std::vector<float> ring(cap * r->rw, 0.0f);
+    auto cols = [&](uint64_t c0, uint64_t w) {
+      std::vector<float> v(cap * w);
+      is.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(v.size() * 4));
+      for (uint64_t i = 0; i < cap; ++i) std::memcpy(&ring[i * r->rw + c0], &v[i * w], 4 * w);
+    };
+    cols(0, ds);
+    cols(ds, da);
+    cols(ds + da, ds);
+    cols(2 * ds + da, 1);
+    cols(2 * ds + da + 1, 1);
+    std::vector<uint32_t> mem(cap);
+    is.read(reinterpret_cast<char*>(mem.data()), static_cast<std::streamsize>(cap * 4));
+    if (!is) PBRL_THROW(PBRL_E_CONFIG, "ReplayBuffer::load_snapshot: truncated file");
+    CUDA_CHECK(cudaMemcpyAsync(r->ring.p + buffer * cap * r->rw, ring.data(), ring.size() * 4,
+                               cudaMemcpyHostToDevice, p->stream));
+    std::memcpy(r->member.data() + buffer * cap, mem.data(), cap * 4);
+    r->inserts[buffer] = ins;
     std::vector<uint64_t> sz(r->nbuf);
     for (int b = 0; b < r->nbuf; ++b) sz[b] = std::min<uint64_t>(r->inserts[b], r->cap);
     r->sizes.upload(sz.data(), r->nbuf, p->stream);

@@ -85,6 +85,7 @@ struct Replay {
   DBuf<float> ring;             // [nbuf][cap][rw]
   DBuf<uint64_t> sizes;         // [nbuf] min(inserts, cap)
   std::vector<uint64_t> inserts;
+  std::vector<uint32_t> member;  // [nbuf][cap] Transition::member per slot (host metadata)
   DBuf<float> stage_rows;
   DBuf<uint64_t> stage_dst;
 };

@@ -575,6 +575,14 @@ class DeviceReplay:
         _lib.call("pbrl_replay_size", self.st.handle, buffer, C.byref(c))
         return c.value
 
+    def save_snapshot(self, path, buffer: int = 0) -> None:
+        """ReplayBuffer::save_snapshot (replay.hpp:113-139) of one ring, PBRLBUF1 format."""
+        _lib.call("pbrl_replay_save_snapshot", self.st.handle, buffer, str(path).encode())
+
+    def load_snapshot(self, path, buffer: int = 0) -> None:
+        """ReplayBuffer::load_snapshot (replay.hpp:141-165) into one ring (same capacity / dims)."""
+        _lib.call("pbrl_replay_load_snapshot", self.st.handle, buffer, str(path).encode())
+
 
 def sample_batch(replay: DeviceReplay, batch_size: int, seed: int, draw_id: int,
                  min_size: int = 1) -> Optional[TransitionBatch]:

@@ -71,3 +71,39 @@ def test_load_checkpoint_rejects_mismatch(pb, tmp_path):
     trunc.write_bytes(p.read_bytes()[:-8])
     with pytest.raises(pb.ConfigError):
         pb.load_checkpoint(a, "policy", trunc)
+
+
+def test_replay_snapshot_matches_reference(pb, ref, tmp_path):
+    """PBRLBUF1 (replay.hpp:113-165): device ring snapshots == the reference buffer's bytes
+    (wrap-around included), and a reference snapshot loaded on the device samples identically."""
+    n, ds, da, cap = 2, 17, 6, 40
+    st = pb.make_td3_state(n, ds, da, [8], 1.0, 3)
+    rep = pb.DeviceReplay(st, cap, "per_agent")
+    rbufs = [ref.replay(cap, ds, da) for _ in range(n)]
+    rng = np.random.default_rng(4)
+    fills = [25, 95]
+    mem = np.concatenate([np.full(f, m, np.uint32) for m, f in enumerate(fills)])
+    rng.shuffle(mem)
+    s, a = rng.standard_normal((mem.size, ds)), rng.standard_normal((mem.size, da))
+    r, s2 = rng.standard_normal(mem.size), rng.standard_normal((mem.size, ds))
+    d = (rng.random(mem.size) < 0.1).astype(np.float32)
+    rep.insert(s, a, r, s2, d, mem)
+    for i in range(mem.size):
+        rbufs[mem[i]].push(s[i].astype(np.float32), a[i].astype(np.float32), float(r[i]),
+                           s2[i].astype(np.float32), float(d[i]), int(mem[i]))
+    for b in range(n):
+        rep.save_snapshot(tmp_path / f"dev{b}.buf", b)
+        assert ref.lib.ref_replay_save_snapshot(rbufs[b].h, str(tmp_path / f"ref{b}.buf").encode()) == 0
+        assert (tmp_path / f"dev{b}.buf").read_bytes() == (tmp_path / f"ref{b}.buf").read_bytes()
+    # reference snapshots -> a fresh device replay: same sampled batches as the original one
+    st2 = pb.make_td3_state(n, ds, da, [8], 1.0, 3)
+    rep2 = pb.DeviceReplay(st2, cap, "per_agent")
+    for b in range(n):
+        rep2.load_snapshot(tmp_path / f"ref{b}.buf", b)
+        assert rep2.size(b) == rep.size(b)
+    x = pb.sample_batch(rep, 64, seed=5, draw_id=3)
+    y = pb.sample_batch(rep2, 64, seed=5, draw_id=3)
+    for u, v in zip((x.s, x.a, x.r, x.s2, x.done), (y.s, y.a, y.r, y.s2, y.done)):
+        assert np.array_equal(u, v)
+    with pytest.raises(pb.ConfigError):
+        pb.DeviceReplay(st2, cap + 1, "per_agent").load_snapshot(tmp_path / "ref0.buf", 0)
