@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--pop", type=int, default=None, help="override the total population")
     ap.add_argument("--precision", default=os.environ.get("PBRL_PRECISION", "bf16"),
                     choices=["ffma32", "bf16", "tf32"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU runs the config's population (members keyed by global "
+                         "id, total = pop x N); strong: the config's population split over N")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-json", default=None, help="write the per-class profile here")
@@ -176,30 +179,34 @@ def cpu_reference(cfg, pop, k_steps=2, reps=3):
                 sample=f"C restatement oracle, pop {pop}, k={k_steps} steps, one thread")
 
 
-def reference_arm(args, cfg, pop, rank):
+def reference_arm(args, cfg, pop, rank, world):
     if rank != 0:
         return
     k = 2 if args.steps >= 2 else 1
-    cb = cpu_reference(cfg, pop, k_steps=k, reps=3)
+    gpus = max(world, args.gpus)
+    total = pop * gpus if args.scaling == "weak" else pop  # the same workload as our arm
+    cb = cpu_reference(cfg, total, k_steps=k, reps=3)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": cb["unit"],
-            "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": pop / cb["value"] * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (make_synthetic_batches, seed 7)",
-            "config": config_dict(args, cfg, pop, "host"),
+            "n_gpus": gpus, "steps": k, "warmup": 1, "ms_per_step": total / cb["value"] * 1e3,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (make_synthetic_batches, seed 7)",
+            "config": config_dict(args, cfg, total, "host", gpus),
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": cb["unit"], "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def config_dict(args, cfg, pop, l2):
+def config_dict(args, cfg, pop, l2, gpus):
+    per = pop // max(1, gpus)
     return {"workload": f"{cfg['algo'].upper()} population update, config {args.config}: "
-                        f"pop {pop}, MLP {'x'.join(map(str, cfg['hidden']))}, batch {cfg['batch']}, "
+                        f"pop {per} per GPU ({pop} total), MLP "
+                        f"{'x'.join(map(str, cfg['hidden']))}, batch {cfg['batch']}, "
                         f"obs {OBS} / act {ACT}",
-            "algo": cfg["algo"], "population": pop, "hidden": cfg["hidden"],
-            "batch": cfg["batch"], "obs_dim": OBS, "act_dim": ACT,
-            "parallelism": f"population shards x{args.gpus}", "precision": args.precision,
-            "l2": l2}
+            "algo": cfg["algo"], "population": pop, "population_per_gpu": per,
+            "hidden": cfg["hidden"], "batch": cfg["batch"], "obs_dim": OBS, "act_dim": ACT,
+            "parallelism": f"population shards x{gpus} ({args.scaling} scaling, no per-step "
+                           f"collective)", "precision": args.precision, "l2": l2}
 
 
 # ------------------------------------------------------------------ our arm
@@ -211,24 +218,35 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        reference_arm(args, cfg, pop, rank)
+        reference_arm(args, cfg, pop, rank, world)
         return
 
     import torch
     import torch.distributed as dist
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # PBRL_BENCH_BACKEND=gloo (tests only): run the sharded path with several ranks on however
+    # many GPUs exist (ranks share devices round-robin), collectives on the host
+    backend = os.environ.get("PBRL_BENCH_BACKEND", "nccl")
+    gpu = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_2206_08888_b200 as pb
     from paper_2206_08888_b200 import _lib
 
-    if pop % world:
-        raise SystemExit(f"population {pop} does not split over {world} GPUs")
-    n = pop // world
+    if args.scaling == "weak":  # every rank: the config's population, global member ids
+        n = pop
+        pop = pop * world
+    else:
+        if pop % world:
+            raise SystemExit(f"population {pop} does not split over {world} GPUs")
+        n = pop // world
     off = rank * n
     make = pb.make_td3_state if cfg["algo"] == "td3" else pb.make_sac_state
-    st = make(n, OBS, ACT, cfg["hidden"], 1.0, SEED, precision=args.precision, device=local,
+    st = make(n, OBS, ACT, cfg["hidden"], 1.0, SEED, precision=args.precision, device=gpu,
               member_offset=off, n_global=pop)
     hy = pb.Td3Hyper.defaults(n) if cfg["algo"] == "td3" else pb.SacHyper.defaults(n, ACT)
     st._sync_hyper(hy)
@@ -264,7 +282,7 @@ def main():
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -275,7 +293,7 @@ def main():
     # ---- timed region: K steps, device time on the library stream, max over ranks
     K = args.steps
     launches0 = st.launch_count()
-    with Clocks(local) as clk:
+    with Clocks(gpu) as clk:
         barrier()
         torch.cuda.synchronize(dev)
         st.synchronize()
@@ -401,13 +419,13 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "agent-updates/s", "n_gpus": world,
                 "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                 "dtype": {"ffma32": "f32", "bf16": "bf16", "tf32": "tf32"}[args.precision],
                 "data": "synthetic (make_synthetic_batches semantics, seed 7, 50 batches in HBM)",
                 "config": config_dict(args, cfg, pop,
                                       "flushed between steps" if flush else
                                       f"inputs+state {(state_bytes + in_bytes) / 2**20:.0f} MiB "
-                                      f"per GPU > L2"),
+                                      f"per GPU > L2", world),
                 "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "profile": {k: {kk: round(vv, 6) if isinstance(vv, float)
                                                          else vv for kk, vv in v.items()}
