@@ -625,7 +625,7 @@ void gather(Pop* p, int B, uint64_t seed, uint64_t draw_id, int act16) {
   launch_replay_gather(p->n, B, p->ds, p->da, p->lsa, r->rw, r->ring.p, r->cap,
                        r->mode == PBRL_REPLAY_SHARED, r->sizes.p, p->streams.p, seed, draw_id,
                        p->S.in_sa.p, p->S.in_s2a.p, p->S.sa_pi.p, p->S.r.p, p->S.d.p, act16,
-                       p->stream);
+                       p->stream, p->S.in_s.p, p->lsp);
   p->count_launch(1);
 }
 }  // namespace

@@ -467,8 +467,8 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
 // aligned rows (launch_out_backward checks and otherwise uses k_out_backward).
 constexpr int kOvQuads = 16, kOvSlices = 16;  // 64 columns x 16 row slices per block
 
-template <typename AT> struct Vec4;
-template <> struct Vec4<float> {
+template <typename AT, int CW> struct VecN;
+template <> struct VecN<float, 4> {
   __device__ static void ld(const float* p, float* v) {
     const float4 u = *reinterpret_cast<const float4*>(p);
     v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w;
@@ -477,7 +477,7 @@ template <> struct Vec4<float> {
     *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
   }
 };
-template <> struct Vec4<__nv_bfloat16> {
+template <> struct VecN<__nv_bfloat16, 4> {
   __device__ static void ld(const __nv_bfloat16* p, float* v) {
     const uint2 u = *reinterpret_cast<const uint2*>(p);
     const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
@@ -493,12 +493,30 @@ template <> struct Vec4<__nv_bfloat16> {
     *reinterpret_cast<uint2*>(p) = u;
   }
 };
+template <> struct VecN<float, 2> {
+  __device__ static void ld(const float* p, float* v) {
+    const float2 u = *reinterpret_cast<const float2*>(p);
+    v[0] = u.x; v[1] = u.y;
+  }
+  __device__ static void st(float* p, const float* v) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  }
+};
+template <> struct VecN<__nv_bfloat16, 2> {
+  __device__ static void ld(const __nv_bfloat16* p, float* v) {
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p));
+    v[0] = a.x; v[1] = a.y;
+  }
+  __device__ static void st(__nv_bfloat16* p, const float* v) {
+    *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(v[0], v[1]);
+  }
+};
 
-template <int NO, typename AT>
+template <int NO, typename AT, int CW>
 __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdArgs a) {
   PDL_ENTRY();
   extern __shared__ float sm[];
-  constexpr int NA = NO, CB = 4 * kOvQuads;  // columns per block
+  constexpr int NA = NO, CB = CW * kOvQuads;  // columns per block
   const int nout = NO < 16 ? NO : a.nout, B = a.B;
   float* Gs = sm;                                // [B][nout]
   float* Ls = Gs + B * nout;                     // [B]
@@ -508,7 +526,7 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
   const int mem = grp % a.n_members;
   if (a.active && !a.active[mem]) return;
   const int cq = threadIdx.x % kOvQuads, sl = threadIdx.x / kOvQuads;
-  const int c0 = blockIdx.x * CB + 4 * cq;  // first of this thread's 4 columns
+  const int c0 = blockIdx.x * CB + CW * cq;  // first of this thread's CW columns
   const bool live = c0 < a.H;
   const AT* X = static_cast<const AT*>(a.X) + (a.x_by_member ? mem : grp) * a.x_gs;
   const float* W = a.W + grp * a.w_gs;
@@ -541,14 +559,16 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
       Gs[e] = G[static_cast<long long>(b) * a.g_ld + o];
     }
   }
-  float w[4][NA], acc[4][NA], csum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  float w[CW][NA], acc[CW][NA], csum[CW];
 #pragma unroll
-  for (int c = 0; c < 4; ++c)
+  for (int c = 0; c < CW; ++c) {
+    csum[c] = 0.0f;
 #pragma unroll
     for (int o = 0; o < NA; ++o) {
       acc[c][o] = 0.0f;
       w[c][o] = (live && o < nout) ? W[static_cast<long long>(c0 + c) * nout + o] : 0.0f;
     }
+  }
   __syncthreads();
   const int rows = (B + kOvSlices - 1) / kOvSlices;
   const int b0 = sl * rows, b1 = min(B, b0 + rows);
@@ -556,17 +576,17 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
   if (live) {
     constexpr int U = 8;
     for (int b = b0; b < b1; b += U) {
-      float xv[U][4];
+      float xv[U][CW];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (b + u < b1) Vec4<AT>::ld(X + static_cast<long long>(b + u) * a.x_ld + c0, xv[u]);
+        if (b + u < b1) VecN<AT, CW>::ld(X + static_cast<long long>(b + u) * a.x_ld + c0, xv[u]);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (b + u >= b1) break;
         const float* g = Gs + (b + u) * nout;
-        float dv[4];
+        float dv[CW];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < CW; ++c) {
           float d = 0.0f;
 #pragma unroll
           for (int o = 0; o < NA; ++o) {
@@ -577,13 +597,13 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
           dv[c] = xv[u][c] > 0.0f ? d : 0.0f;
           csum[c] = csum[c] + dv[c];
         }
-        if (dX) Vec4<AT>::st(dX + static_cast<long long>(b + u) * a.dx_ld + c0, dv);
+        if (dX) VecN<AT, CW>::st(dX + static_cast<long long>(b + u) * a.dx_ld + c0, dv);
       }
     }
   }
   if (a.dbx) {  // fused bias gradient of the layer below
 #pragma unroll
-    for (int c = 0; c < 4; ++c) Cs[sl * CB + 4 * cq + c] = csum[c];
+    for (int c = 0; c < CW; ++c) Cs[sl * CB + CW * cq + c] = csum[c];
     __syncthreads();
     for (int cc = threadIdx.x; cc < CB; cc += blockDim.x) {
       const int col = blockIdx.x * CB + cc;
@@ -605,10 +625,10 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
   if (!a.dW) return;
   float* dW = a.dW + grp * a.dw_gs;
 #pragma unroll
-  for (int c = 0; c < 4; ++c)
+  for (int c = 0; c < CW; ++c)
 #pragma unroll
     for (int o = 0; o < NA; ++o)
-      if (o < nout) Ps[(sl * CB + 4 * cq + c) * nout + o] = acc[c][o];
+      if (o < nout) Ps[(sl * CB + CW * cq + c) * nout + o] = acc[c][o];
   __syncthreads();
   for (int e = threadIdx.x; e < CB * nout; e += blockDim.x) {
     const int cc = e / nout, o = e - cc * nout;
@@ -632,26 +652,31 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
 
 template <int NO, typename AT>
 static bool launch_ob_v(const OutBwdArgs& a, cudaStream_t s) {
-  const int eb = sizeof(AT);
-  auto al = [&](const void* p) { return reinterpret_cast<uintptr_t>(p) % (4 * eb) == 0; };
-  // single-output layers only: with NO > 1 the 4-column register tiles (w, acc: 8 NO floats)
-  // cut the occupancy below what the scalar kernel reaches (measured slower for NO = 6)
-  if (NO != 1 || a.exact || a.H % 4 || a.x_ld % 4 || a.x_gs % 4 || !al(a.X) ||
-      (a.dX && (a.dx_ld % 4 || a.dx_gs % 4 || !al(a.dX))))
+  // CW adjacent columns per thread: 4 for single-output layers, 2 for NO <= 8 (the w / acc
+  // register tiles are CW x NO floats each); wider outputs keep the scalar kernel
+  constexpr int CW = NO == 1 ? 4 : 2;
+  if constexpr (NO > 8) {
     return false;
-  constexpr int CB = 4 * kOvQuads;
-  const size_t smem = (static_cast<size_t>(a.B) * (a.nout + 1) +
-                       static_cast<size_t>(kOvSlices) * CB * (a.nout + 1)) * 4;
-  if (smem > 200 * 1024) return false;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_out_backward_v<NO, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr = true;
+  } else {
+    const int eb = sizeof(AT);
+    auto al = [&](const void* p) { return reinterpret_cast<uintptr_t>(p) % (CW * eb) == 0; };
+    if (a.exact || a.H % CW || a.x_ld % CW || a.x_gs % CW || !al(a.X) ||
+        (a.dX && (a.dx_ld % CW || a.dx_gs % CW || !al(a.dX))))
+      return false;
+    constexpr int CB = CW * kOvQuads;
+    const size_t smem = (static_cast<size_t>(a.B) * (a.nout + 1) +
+                         static_cast<size_t>(kOvSlices) * CB * (a.nout + 1)) * 4;
+    if (smem > 200 * 1024) return false;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_out_backward_v<NO, AT, CW>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    dim3 grid((a.H + CB - 1) / CB, a.groups);
+    launch_k(k_out_backward_v<NO, AT, CW>, grid, kOvQuads * kOvSlices, smem, s, a);
+    return true;
   }
-  dim3 grid((a.H + CB - 1) / CB, a.groups);
-  launch_k(k_out_backward_v<NO, AT>, grid, kOvQuads * kOvSlices, smem, s, a);
-  return true;
 }
 
 template <int NO, typename AT>
@@ -766,7 +791,8 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
 template <typename AT>
 __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float* s,
                              const float* a, const float* r, const float* s2, const float* d,
-                             AT* in_sa, AT* in_s2a, AT* sa_pi, float* r_out, float* d_out) {
+                             AT* in_sa, AT* in_s2a, AT* sa_pi, float* r_out, float* d_out,
+                             AT* in_s, int lsp) {
   PDL_ENTRY();
   const int dsa = ds + da;
   const long long rows = static_cast<long long>(n) * B;
@@ -781,6 +807,7 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float*
       act_st(in_sa, o, sv);
       act_st(sa_pi, o, sv);
       act_st(in_s2a, o, s2[row * ds + c]);
+      if (in_s) act_st(in_s, row * lsp + c, sv);
     } else {
       act_st(in_sa, o, a[row * da + (c - ds)]);
     }
@@ -794,17 +821,18 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float*
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, void* in_sa,
                        void* in_s2a, void* sa_pi, float* r_out, float* d_out, int act16,
-                       cudaStream_t st) {
+                       cudaStream_t st, void* in_s, int lsp) {
   const long long total = static_cast<long long>(n) * B * (ds + da);
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
   if (act16)
     launch_k(k_pack_batch<__nv_bfloat16>, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d,
              static_cast<__nv_bfloat16*>(in_sa), static_cast<__nv_bfloat16*>(in_s2a),
-             static_cast<__nv_bfloat16*>(sa_pi), r_out, d_out);
+             static_cast<__nv_bfloat16*>(sa_pi), r_out, d_out,
+             static_cast<__nv_bfloat16*>(in_s), lsp);
   else
     launch_k(k_pack_batch<float>, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d,
              static_cast<float*>(in_sa), static_cast<float*>(in_s2a), static_cast<float*>(sa_pi),
-             r_out, d_out);
+             r_out, d_out, static_cast<float*>(in_s), lsp);
 }
 
 // y = r + gamma*(1-done)*min(Q1', Q2')   (algos.hpp:268-281)
@@ -1466,7 +1494,8 @@ template <typename AT>
 __global__ void k_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const float* ring,
                                 uint64_t cap, int shared, const uint64_t* sizes,
                                 const uint64_t* streams, uint64_t seed, uint64_t draw_id,
-                                AT* in_sa, AT* in_s2a, AT* sa_pi, float* r_out, float* d_out) {
+                                AT* in_sa, AT* in_s2a, AT* sa_pi, float* r_out, float* d_out,
+                                AT* in_s, int lsp) {
   PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -1483,6 +1512,7 @@ __global__ void k_replay_gather(int n, int B, int ds, int da, int lsa, int rw, c
     if (c < ds) {
       act_st(in_sa, o + c, v);
       if (sa_pi) act_st(sa_pi, o + c, v);
+      if (in_s) act_st(in_s, static_cast<long long>(warp) * lsp + c, v);
     } else if (c < dsa) {
       act_st(in_sa, o + c, v);
     } else if (c < dsa + ds) {
@@ -1499,18 +1529,19 @@ void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const f
                           uint64_t cap, int shared, const uint64_t* sizes,
                           const uint64_t* streams, uint64_t seed, uint64_t draw_id,
                           void* in_sa, void* in_s2a, void* sa_pi, float* r_out, float* d_out,
-                          int act16, cudaStream_t s) {
+                          int act16, cudaStream_t s, void* in_s, int lsp) {
   const long long warps = static_cast<long long>(n) * B;
   const int blocks = static_cast<int>((warps * 32 + 255) / 256);
   if (act16)
     launch_k(k_replay_gather<__nv_bfloat16>, blocks, 256, 0, s, n, B, ds, da, lsa, rw, ring, cap,
              shared, sizes, streams, seed, draw_id, static_cast<__nv_bfloat16*>(in_sa),
              static_cast<__nv_bfloat16*>(in_s2a), static_cast<__nv_bfloat16*>(sa_pi), r_out,
-             d_out);
+             d_out, static_cast<__nv_bfloat16*>(in_s), lsp);
   else
     launch_k(k_replay_gather<float>, blocks, 256, 0, s, n, B, ds, da, lsa, rw, ring, cap, shared,
              sizes, streams, seed, draw_id, static_cast<float*>(in_sa),
-             static_cast<float*>(in_s2a), static_cast<float*>(sa_pi), r_out, d_out);
+             static_cast<float*>(in_s2a), static_cast<float*>(sa_pi), r_out, d_out,
+             static_cast<float*>(in_s), lsp);
 }
 
 // ================================================================== PBT

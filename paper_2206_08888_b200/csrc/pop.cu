@@ -303,6 +303,8 @@ void Pop::ensure_scratch(int B) {
   const int L = pol.depth;
   // row strides padded to 4 floats: every activation is a legal TMA source (16 B strides)
   lsa = padl(ds + da);
+  lsp = padl(ds + 1);
+  S.in_s.alloc(nb * lsp);
   S.in_sa.alloc(nb * lsa);
   S.in_s2a.alloc(nb * lsa);
   S.sa_pi.alloc(nb * lsa);
@@ -350,7 +352,7 @@ void Pop::ensure_scratch(int B) {
     S.clamped.alloc(nb * da);
   }
   // fresh buffers: zero so never-written padding columns cannot carry NaN bit patterns
-  for (auto* b : {&S.in_sa, &S.in_s2a, &S.sa_pi, &S.gtop}) b->zero(stream);
+  for (auto* b : {&S.in_sa, &S.in_s2a, &S.sa_pi, &S.gtop, &S.in_s}) b->zero(stream);
   for (auto* v : {&S.tp_h, &S.ph, &S.pdh, &S.tq_h, &S.ch, &S.dh, &S.qh, &S.qdh})
     for (auto& b : *v) b.zero(stream);
   ones_dirty = true;
@@ -366,6 +368,9 @@ void Pop::ensure_ones() {
   if (use_tc() && lsa > ds + da)
     launch_fill_col(S.in_sa.p, static_cast<long long>(n) * S.B, lsa, ds + da, 1.0f,
                     act16() ? 1 : 0, stream);
+  if (use_tc() && lsp > ds)  // the policy input's ones column (its first-layer bias gradient)
+    launch_fill_col(S.in_s.p, static_cast<long long>(n) * S.B, lsp, ds, 1.0f, act16() ? 1 : 0,
+                    stream);
   ones_dirty = false;
 }
 
@@ -430,7 +435,7 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     }
     timed(PC_GATHER, 0.0, 0.0, 0, [&] {
       launch_pack_batch(n, B, ds, da, lsa, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
-                        S.d.p, act16() ? 1 : 0, stream);
+                        S.d.p, act16() ? 1 : 0, stream, S.in_s.p, lsp);
     });
     if (!device_ptrs) CUDA_CHECK(cudaEventRecord(ev_free[i & 1u], stream));
     step(B, d_mask);

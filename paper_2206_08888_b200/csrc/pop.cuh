@@ -199,7 +199,7 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, void* in_sa,
                        void* in_s2a, void* sa_pi, float* r_out, float* d_out, int act16,
-                       cudaStream_t st);
+                       cudaStream_t st, void* in_s = nullptr, int lsp = 0);
 void launch_td_target(int n, int B, const float* r, const float* d, const float* q2n,
                       const float* gamma, float* y, cudaStream_t s);
 void launch_mse(int groups, int n, int B, const float* q, const float* y, float* dq, double* loss,
@@ -274,7 +274,7 @@ void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const f
                           uint64_t cap, int shared, const uint64_t* sizes,
                           const uint64_t* streams, uint64_t seed, uint64_t draw_id,
                           void* in_sa, void* in_s2a, void* sa_pi, float* r_out, float* d_out,
-                          int act16, cudaStream_t s);
+                          int act16, cudaStream_t s, void* in_s = nullptr, int lsp = 0);
 
 // PBT
 void launch_pbt_plan(int n, const double* fitness, int cut, uint64_t key, uint64_t next,

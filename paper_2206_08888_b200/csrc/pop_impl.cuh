@@ -62,6 +62,7 @@ struct DBuf {
 struct Scratch {
   int B = 0;
   DBuf<float> in_sa, in_s2a, sa_pi, r, d, y, tq_out, q, dq, qpi, gq, pt, ga, head, gtop;
+  DBuf<float> in_s;  // policy input [s | 1 | pad] (row stride lsp; the ones column as in_sa's)
   DBuf<float> bs[2], ba[2], br[2], bs2[2], bd[2];  // host batches staged (double-buffered)
   std::vector<DBuf<float>> tp_h, ph, pdh, tq_h, ch, dh, qh, qdh;
   DBuf<float> x, th, ls, eps, logp, logp2, lw, tnoise;
@@ -242,6 +243,12 @@ struct Pop {
                                     elems * aeb());
   }
   int lsa = 0;  // padded row stride of the critic-input blocks [s | a]
+  int lsp = 0;  // padded row stride of the policy-input block [s | 1]
+  Mat policy_input(int B) const {  // the policy's x0: s, with the ones column in TC modes
+    Mat m{S.in_s.p, static_cast<long long>(B) * lsp, lsp, 0};
+    if (use_tc() && lsp > ds) m.ones_col = ds;
+    return m;
+  }
   bool use_graphs = true, capturing = false;
   std::vector<StepGraph> graphs;
   void invalidate_graphs();

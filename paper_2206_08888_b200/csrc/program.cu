@@ -918,7 +918,7 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
 
 void Pop::td3_policy_forward(int B) {
   const long long nbB = B;
-  const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
+  const Mat s = policy_input(B);
   mlp_forward(pol, pol_p.p, n, B, s, S.ph, aoff(S.sa_pi.p, ds), nbB * lsa, lsa, EPI_BIAS_TANH,
               fire.p, S.pt.p, nbB * da, da, false, true, true);
 }
@@ -927,7 +927,7 @@ void Pop::td3_policy_forward(int B) {
 // every launch gated by the fire mask
 void Pop::td3_policy_half(int B, bool forward_done) {
   const long long nbB = B;
-  const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
+  const Mat s = policy_input(B);
   if (!forward_done) td3_policy_forward(B);
   mlp_forward(cri, cri_p.p, n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 0}, S.qh, S.qpi.p, nbB, 1,
               EPI_BIAS, fire.p);
@@ -991,7 +991,7 @@ void Pop::sac_step(int B) {
   });
   critic_update(B, nullptr);  // critic targets tracked every step (:827-834)
   // sac_policy_loss_grads (:643-735) through both UPDATED critics
-  const Mat s{S.in_sa.p, nbB * lsa, lsa, 0};
+  const Mat s = policy_input(B);
   mlp_forward(pol, pol_p.p, n, B, s, S.ph, S.head.p, nbB * hd, hd, EPI_BIAS);
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_head(n, B, ds, da, lsa, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p,
