@@ -767,6 +767,7 @@ int pbrl_pbt_apply(pbrl_pop* pop, const uint64_t* replaced, const uint64_t* dono
         CUDA_CHECK(cudaMemcpyAsync(p->t_cri.p + p->n + m, &zero, 8, cudaMemcpyHostToDevice, p->stream));
         if (p->algo == PBRL_ALGO_TD3) {
           CUDA_CHECK(cudaMemcpyAsync(p->delay_acc.p + m, &dz, 8, cudaMemcpyHostToDevice, p->stream));
+          if (p->delay_host.size() > m) p->delay_host[m] = 0.0;
         } else {
           CUDA_CHECK(cudaMemcpyAsync(p->t_alpha.p + m, &zero, 8, cudaMemcpyHostToDevice, p->stream));
           CUDA_CHECK(cudaMemcpyAsync(p->alpha_m.p + m, &fz, 4, cudaMemcpyHostToDevice, p->stream));

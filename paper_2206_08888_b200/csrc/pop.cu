@@ -387,6 +387,7 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
   ensure_ones();
   ensure_corr(t_bound + k + 4);
   const uint8_t* d_mask = nullptr;
+  host_mask = policy_mask;
   if (policy_mask) {
     mask_buf.alloc(n);
     mask_buf.upload(policy_mask, n, stream);
@@ -443,6 +444,7 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
       CUDA_CHECK(cudaMemcpyAsync(losses_out + static_cast<size_t>(i) * 3 * n, losses.p,
                                  3 * n * sizeof(double), cudaMemcpyDeviceToHost, stream));
   }
+  host_mask = nullptr;
   if (losses_out) sync();
   CUDA_CHECK(cudaGetLastError());
 }

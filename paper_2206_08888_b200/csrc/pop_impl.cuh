@@ -134,7 +134,8 @@ struct StepGraph {
   int B = 0;
   bool masked = false;
   cudaGraphExec_t exec = nullptr;
-  size_t nodes = 0;
+  size_t nodes = 0;       // kernel nodes outside conditional bodies
+  size_t cond_nodes = 0;  // kernel nodes inside the policy-half conditional bodies
 };
 
 struct Pop {
@@ -298,6 +299,11 @@ struct Pop {
   template <typename F>
   void capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body);
   size_t cond_nodes = 0;
+  // host mirror of the TD3 fire accumulator (k_td3_step_begin's double arithmetic), used only to
+  // count the kernels a replayed graph actually runs (the conditional policy half)
+  std::vector<double> delay_host;
+  const uint8_t* host_mask = nullptr;
+  bool host_fires();
   cudaStream_t side3 = nullptr;
   cudaEvent_t ev_pfork = nullptr, ev_pjoin = nullptr;
   void sac_step(int B);

@@ -1086,6 +1086,23 @@ void Pop::run_program(int B, const uint8_t* d_mask) {
   else sac_step(B);
 }
 
+bool Pop::host_fires() {
+  if (delay_host.size() != static_cast<size_t>(n)) delay_host.assign(n, 0.0);
+  bool any = false;
+  for (int m = 0; m < n; ++m) {
+    double acc = delay_host[m] + hyper[2][m];
+    bool f = false;
+    if (acc >= 1.0 - 1e-12) {
+      acc -= 1.0;
+      f = true;
+    }
+    delay_host[m] = acc;
+    if (host_mask && !host_mask[m]) f = false;
+    any = any || f;
+  }
+  return any;
+}
+
 void Pop::invalidate_graphs() {
   for (auto& g : graphs) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -1095,6 +1112,7 @@ void Pop::invalidate_graphs() {
 
 void Pop::step(int B, const uint8_t* d_mask) {
   ensure_corr(t_bound + 4);
+  const bool fires = algo == PBRL_ALGO_TD3 ? host_fires() : true;  // advances the mirror
   if (act16() && weights_dirty) refresh_shadows();
   if (prof_on || !use_graphs) {
     run_program(B, d_mask);
@@ -1122,15 +1140,16 @@ void Pop::step(int B, const uint8_t* d_mask) {
       capturing = false;
       size_t nodes = 0;
       CUDA_CHECK(cudaGraphGetNodes(graph, nullptr, &nodes));
-      // kernel nodes: the conditional node stands for its body (the policy half)
-      g.nodes = nodes + cond_body_nodes - cond_nodes;
+      // kernel nodes: the conditional nodes stand for their bodies (the policy half)
+      g.nodes = nodes - cond_nodes;
+      g.cond_nodes = cond_body_nodes;
       CUDA_CHECK(cudaGraphInstantiate(&g.exec, graph, 0));
       CUDA_CHECK(cudaGraphDestroy(graph));
       graphs.push_back(g);
       sg = &graphs.back();
     }
     CUDA_CHECK(cudaGraphLaunch(sg->exec, stream));
-    count_launch(sg->nodes);
+    count_launch(sg->nodes + (fires ? sg->cond_nodes : 0));
   }
   t_bound += 1;
   prof_step_done();
