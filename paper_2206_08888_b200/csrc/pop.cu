@@ -175,6 +175,9 @@ Pop::~Pop() {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side3) cudaStreamDestroy(side3);
+    if (side4) cudaStreamDestroy(side4);
+    if (ev_c2) cudaEventDestroy(ev_c2);
+    if (ev_c2done) cudaEventDestroy(ev_c2done);
     if (ev_pfork) cudaEventDestroy(ev_pfork);
     if (ev_pjoin) cudaEventDestroy(ev_pjoin);
     if (cstream) cudaStreamDestroy(cstream);

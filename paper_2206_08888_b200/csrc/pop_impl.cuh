@@ -290,7 +290,10 @@ struct Pop {
   void critic_forward(int B);
   bool gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long long out_ld, int epi,
                          Mat aux, float scale, const int* active);
-  void critic_update(int B, const int* polyak_gate, bool forward_done = false);
+  void critic_update(int B, const int* polyak_gate, bool forward_done = false,
+                     bool split_c2 = false);
+  cudaStream_t side4 = nullptr;  // critic 2's Adam branch
+  cudaEvent_t ev_c2 = nullptr, ev_c2done = nullptr;
   cudaStream_t side2 = nullptr;  // parallel graph branch (critic forward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void td3_step(int B, const uint8_t* d_mask);

@@ -758,7 +758,7 @@ void Pop::critic_forward(int B) {
   mlp_forward(cri, cri_p.p, 2 * n, B, x0, S.ch, S.q.p, B, 1, EPI_BIAS);
 }
 
-void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
+void Pop::critic_update(int B, const int* polyak_gate, bool forward_done, bool split_c2) {
   const int n2 = 2 * n;
   Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
   if (use_tc() && lsa > ds + da) x0.ones_col = ds + da;  // see Pop::ensure_ones
@@ -796,11 +796,34 @@ void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
                &top, use_tc() ? &af : nullptr);
   // 28 B/param Adam (+2 B/param bf16 operand copy in BF16 mode)
   const double cP = static_cast<double>(cri.P - (af.skip1 - af.skip0));  // k_adam's share
-  timed(PC_ADAM, 0.0, cP * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
-    launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
-                corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, cri_p16.p, cri_t16.p,
-                stream, af.skip0, af.skip1);
-  });
+  if (split_c2) {
+    // TD3 graph mode: critic 2's Adam runs on a parallel branch (the policy half reads critic 1
+    // only, algos.hpp:318-338), so on fire steps it overlaps the policy-loss chain; joined at
+    // the end of the step
+    const size_t o = static_cast<size_t>(n) * cri.stride;
+    CUDA_CHECK(cudaEventRecord(ev_c2, stream));
+    CUDA_CHECK(cudaStreamWaitEvent(side4, ev_c2, 0));
+    std::swap(stream, side4);
+    timed(PC_ADAM, 0.0, cP * n * (act16() ? 30.0 : 28.0), 0, [&] {
+      launch_adam(n, n, cri.P, cri.stride, cri_p.p + o, cri_m.p + o, cri_v.p + o, cri_g.p + o,
+                  t_cri.p + n, corr1.p, corr2.p, clr, nullptr, cri_t.p + o, h_f5.p, h_f6.p,
+                  polyak_gate, cri_p16.p ? cri_p16.p + o : nullptr,
+                  cri_t16.p ? cri_t16.p + o : nullptr, stream, af.skip0, af.skip1);
+    });
+    std::swap(stream, side4);
+    CUDA_CHECK(cudaEventRecord(ev_c2done, side4));
+    timed(PC_ADAM, 0.0, cP * n * (act16() ? 30.0 : 28.0), 0, [&] {
+      launch_adam(n, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
+                  corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, cri_p16.p,
+                  cri_t16.p, stream, af.skip0, af.skip1);
+    });
+  } else {
+    timed(PC_ADAM, 0.0, cP * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
+      launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
+                  corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, cri_p16.p,
+                  cri_t16.p, stream, af.skip0, af.skip1);
+    });
+  }
   // fused target Polyak: +8 B/param (read + write target), every member (SAC) or fired (TD3)
   const double pb = act16() ? 10.0 : 8.0;
   if (polyak_gate) prof_add_gated_bytes(pb * cP * n2);
@@ -910,10 +933,21 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
     CUDA_CHECK(cudaEventRecord(ev_pjoin, side2));
   }
   // twin critic update; target Polyak fused for members whose policy fires
-  critic_update(B, fire.p, fork);
+  // PBRL_C2FORK=1: critic 2's Adam on a parallel branch next to the policy half (measured
+  // neutral on B200: a 1-CTA/SM GEMM leaves room for one Adam block per SM)
+  const bool split = fork && std::getenv("PBRL_C2FORK") != nullptr;
+  if (split) {
+    if (!side4) CUDA_CHECK(cudaStreamCreateWithFlags(&side4, cudaStreamNonBlocking));
+    if (!ev_c2) {
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_c2, cudaEventDisableTiming));
+      CUDA_CHECK(cudaEventCreateWithFlags(&ev_c2done, cudaEventDisableTiming));
+    }
+  }
+  critic_update(B, fire.p, fork, split);
   if (fork && pfork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_pjoin, 0));
   if (capturing) capture_if(any_fire, side, [&] { td3_policy_half(B, fork && pfork); });
   else td3_policy_half(B, false);
+  if (split) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_c2done, 0));  // join critic 2's Adam
 }
 
 void Pop::td3_policy_forward(int B) {
