@@ -718,7 +718,108 @@ static void launch_fwd_skinny_t(const GemmArgs& g, cudaStream_t s) {
   else launch_k(k_fwd_skinny<16, AT>, grid, 128, 0, s, g);
 }
 
+// Tensor-core modes (no reference summation order to keep): an output layer (N <= 16) too wide
+// to be fused into the previous layer's epilogue (hidden > 256) as one warp per row -- each lane
+// accumulates 8-element slices of K (one 16-byte bf16 / two 16-byte fp32 loads), the N partial
+// sums are warp-reduced, lane o applies the epilogue of output o.  W [K][N] of the block's group
+// is staged in shared memory.
+template <int NMAX, typename AT>
+__global__ void __launch_bounds__(256) k_fwd_rowdot(const GemmArgs g) {
+  PDL_ENTRY();
+  extern __shared__ float Ws[];  // [NMAX][K]: lane slices of 8 consecutive k read as 2 x 16 B
+  const int grp = blockIdx.y;
+  const int mem = grp % g.n_members;
+  if (g.active && !g.active[mem]) return;
+  const AT* A = reinterpret_cast<const AT*>(g.A.p) + (g.A.by_member ? mem : grp) * g.A.gs;
+  const float* Bm = g.B.p + (g.B.by_member ? mem : grp) * g.B.gs;
+  for (int e = threadIdx.x; e < g.K * NMAX; e += blockDim.x) {
+    const int o = e / g.K, k = e - o * g.K;
+    Ws[e] = o < g.N ? Bm[k * g.B.rs + o * g.B.cs] : 0.0f;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long cbase = (g.c_by_member ? mem : grp) * g.c_gs;
+  const float* bias = g.bias.p ? g.bias.p + (g.bias.by_member ? mem : grp) * g.bias.gs : nullptr;
+  const float* aux = g.aux.p ? g.aux.p + (g.aux.by_member ? mem : grp) * g.aux.gs : nullptr;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int row = blockIdx.x * (blockDim.x >> 5) + warp; row < g.M; row += nwarps) {
+    const AT* xr = A + static_cast<long long>(row) * g.A.rs;
+    float acc[NMAX];
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o) acc[o] = 0.0f;
+    for (int k0 = lane * 8; k0 < g.K; k0 += 256) {
+      float x[8];
+      if (sizeof(AT) == 2) {
+        const uint4 u = *reinterpret_cast<const uint4*>(xr + k0);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(h[j]);
+          x[2 * j] = f.x;
+          x[2 * j + 1] = f.y;
+        }
+      } else {
+        const float4 u0 = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xr) + k0);
+        const float4 u1 =
+            *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xr) + k0 + 4);
+        x[0] = u0.x; x[1] = u0.y; x[2] = u0.z; x[3] = u0.w;
+        x[4] = u1.x; x[5] = u1.y; x[6] = u1.z; x[7] = u1.w;
+      }
+#pragma unroll
+      for (int o = 0; o < NMAX; ++o) {
+        if (NMAX > 1 && o >= g.N) break;
+        const float4 w0 = *reinterpret_cast<const float4*>(Ws + o * g.K + k0);
+        const float4 w1 = *reinterpret_cast<const float4*>(Ws + o * g.K + k0 + 4);
+        acc[o] = acc[o] + x[0] * w0.x + x[1] * w0.y + x[2] * w0.z + x[3] * w0.w + x[4] * w1.x +
+                 x[5] * w1.y + x[6] * w1.z + x[7] * w1.w;
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o)
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], off);
+    if (lane < g.N) {
+      float v = 0.0f;
+#pragma unroll
+      for (int o = 0; o < NMAX; ++o)
+        if (o == lane) v = acc[o];
+      v = simt_epilogue(g, v, row, lane, grp, mem, bias, aux);
+      if (g.c16) act_st(reinterpret_cast<__nv_bfloat16*>(g.C), cbase + row * g.c_rs + lane, v);
+      else g.C[cbase + row * g.c_rs + lane] = v;
+    }
+  }
+}
+
+template <typename AT>
+static bool launch_fwd_rowdot_t(const GemmArgs& g, cudaStream_t s) {
+  const int eb = sizeof(AT);
+  if (g.K % 8 || g.A.cs != 1 || g.A.rs % 8 || g.A.gs % 8 ||
+      reinterpret_cast<uintptr_t>(g.A.p) % (8 * eb) || g.N > 16)
+    return false;
+  const int nmax = g.N <= 1 ? 1 : (g.N <= 8 ? 8 : 16);
+  const size_t smem = static_cast<size_t>(g.K) * nmax * 4;
+  if (smem > 96 * 1024) return false;
+  // ~16 rows per warp: W is staged once per block, so few blocks per group
+  dim3 grid(std::max(1, std::min((g.M + 127) / 128, 16)), g.groups);
+  auto go = [&](auto kern) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      attr = true;
+    }
+    launch_k(kern, grid, 256, smem, s, g);
+  };
+  if (nmax == 1) go(k_fwd_rowdot<1, AT>);
+  else if (nmax == 8) go(k_fwd_rowdot<8, AT>);
+  else go(k_fwd_rowdot<16, AT>);
+  return true;
+}
+
 void launch_fwd_skinny(const GemmArgs& g, cudaStream_t s) {
+  if (g.rowdot) {
+    if (g.a16 ? launch_fwd_rowdot_t<__nv_bfloat16>(g, s) : launch_fwd_rowdot_t<float>(g, s))
+      return;
+  }
   if (g.a16) launch_fwd_skinny_t<__nv_bfloat16>(g, s);
   else launch_fwd_skinny_t<float>(g, s);
 }

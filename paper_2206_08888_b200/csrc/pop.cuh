@@ -112,6 +112,7 @@ struct GemmArgs {
   Operand A, B;
   int a_ones_row = 0;  // row M-1 of A is all ones: C row M-1 = column sums of B (bias grad)
   int a16 = 0, c16 = 0;  // BF16 mode (k_fwd_skinny only): A / C are bf16 activations
+  int rowdot = 0;        // tensor-core modes: k_fwd_skinny may use the warp-per-row kernel
   float* C = nullptr;
   long long c_gs = 0, c_rs = 0;
   int c_by_member = 0;

@@ -90,6 +90,7 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
   g.n_members = n;
   g.a16 = act16() ? 1 : 0;
   g.c16 = act16() && y_act ? 1 : 0;
+  g.rowdot = use_tc() ? 1 : 0;  // no reference summation order to keep outside FFMA32
   g.A = simt_op(X.p, X.gs, X.ld, 1, X.by_member);
   g.B = simt_op(Wl, static_cast<long long>(sh.stride), out, 1, 0);
   g.bias = simt_op(W + sh.boff[l], static_cast<long long>(sh.stride), 0, 1, 0);
