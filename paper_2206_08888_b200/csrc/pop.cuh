@@ -56,9 +56,22 @@ __device__ __forceinline__ void act_st(__nv_bfloat16* p, long long i, float v) {
   p[i] = __float2bfloat16_rn(v);
 }
 
+// Every kernel states the same preferred shared-memory carveout (a kernel that needs more gets
+// more), so the small kernels between the big tensor-core ones do not flip the SMs' L1 /
+// shared-memory split back and forth; the value was picked by measurement (kernels.cu).
+// PBRL_CARVEOUT=<percent> overrides (diagnostics; -1 = driver default).
+int carveout_pref();
+
 template <typename... KArgs, typename... Args>
 void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
               Args&&... args) {
+  static bool carve_set = false;
+  if (!carve_set) {
+    const int c = carveout_pref();
+    if (c >= 0)
+      CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, c));
+    carve_set = true;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
