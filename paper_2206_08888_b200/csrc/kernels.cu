@@ -1065,13 +1065,9 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
   float4* t4 = a.polyak ? reinterpret_cast<float4*>(tgt + base) : nullptr;
   // [skip0, skip1) (float4-aligned) was updated by the dW epilogue of its layer (EPI_ADAM)
   const size_t s0 = skip0 / 4, sk = (skip1 - skip0) / 4;
-  for (size_t kq = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; kq < P4 - sk;
-       kq += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t k = kq < s0 ? kq : kq + sk;
-    float4 pv = p4[k], mv = m4[k], vv = v4[k];
-    const float4 gv = g4[k];
-    float4 tv;
-    if (a.polyak) tv = t4[k];
+  // two float4 slots per thread per trip, both slots' loads issued before either is updated
+  // (more bytes in flight per thread for the HBM-bound stream)
+  auto update = [&](size_t k, float4 pv, float4 mv, float4 vv, float4 gv, float4 tv) {
     adam_one(a, pv.x, mv.x, vv.x, gv.x);
     adam_one(a, pv.y, mv.y, vv.y, gv.y);
     adam_one(a, pv.z, mv.z, vv.z, gv.z);
@@ -1096,6 +1092,27 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
         d2[1] = __floats2bfloat162_rn(tv.z, tv.w);
       }
     }
+  };
+  const size_t cnt = P4 - sk, str = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t kq = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; kq < cnt;
+       kq += 2 * str) {
+    const size_t k0 = kq < s0 ? kq : kq + sk;
+    const bool two = kq + str < cnt;
+    const size_t k1q = kq + str;
+    const size_t k1 = k1q < s0 ? k1q : k1q + sk;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 p0 = p4[k0], m0 = m4[k0], v0 = v4[k0], g0 = g4[k0];
+    const float4 t0 = a.polyak ? t4[k0] : z;
+    float4 p1 = z, m1 = z, v1 = z, g1 = z, t1 = z;
+    if (two) {
+      p1 = p4[k1];
+      m1 = m4[k1];
+      v1 = v4[k1];
+      g1 = g4[k1];
+      if (a.polyak) t1 = t4[k1];
+    }
+    update(k0, p0, m0, v0, g0, t0);
+    if (two) update(k1, p1, m1, v1, g1, t1);
   }
   if (blockIdx.x == 0) {
     for (size_t k = P4 * 4 + threadIdx.x; k < P; k += blockDim.x) {
@@ -1121,7 +1138,7 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
                  __nv_bfloat16* t16, cudaStream_t s, size_t skip0, size_t skip1) {
   const int threads = 256;
   if (skip0 % 4 || skip1 % 4 || skip1 < skip0 || skip1 > P / 4 * 4) skip0 = skip1 = 0;
-  int bx = static_cast<int>((P / 4 - (skip1 - skip0) / 4 + threads - 1) / threads);
+  int bx = static_cast<int>((P / 4 - (skip1 - skip0) / 4 + 2 * threads - 1) / (2 * threads));
   bx = bx < 1 ? 1 : bx;
   dim3 grid(bx, groups);
   launch_k(k_adam, grid, threads, 0, s, n, P, stride, p, m, v, g, t, corr1, corr2, lr, active, tgt,
