@@ -3,6 +3,7 @@ member-state blobs (export/import, the payload of cross-GPU exploit copies), Sha
 device adapter in a single-rank NCCL group (== pbt_evolve_trainer), and the C++ demo binary."""
 import os
 import subprocess
+import sys
 from pathlib import Path
 
 import numpy as np
@@ -69,3 +70,14 @@ def test_cpp_facade_demo_runs(cuda):
                        text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert "checksum" in r.stdout and "ConfigError as in the reference" in r.stdout
+
+
+def test_learner_loop_example_runs(cuda, tmp_path):
+    """examples/learner_loop.py: act -> replay insert -> update_k from replay -> PBT -> checkpoint
+    on the device (the run_training learner loop)."""
+    out = tmp_path / "policy.pbrl"
+    r = subprocess.run([sys.executable, str(ROOT / "examples" / "learner_loop.py"), "--pop", "6",
+                        "--envs", "4", "--iters", "8", "--pbt-interval", "4", "--out", str(out)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "done:" in r.stdout and out.exists() and out.read_bytes()[:8] == b"PBRLNET1"
