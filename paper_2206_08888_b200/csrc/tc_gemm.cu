@@ -484,8 +484,9 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
         // dX variant: gather the transposed output-layer weights (a few KB) into fz_w
         epi_bar_sync();
         const float* wsrc = g.ow + grp * g.ow_gs;
+        const int nd = nout > 0 ? nout : 1;  // (NO = 0 instantiations: dead code)
         for (int e = threadIdx.x - 64; e < BN * nout; e += kEpiThreads) {
-          const int j = e / nout, o = e - j * nout;
+          const int j = e / nd, o = e - j * nd;
           fz_w[e] = j < g.N ? __ldg(wsrc + o * g.ow_ld + j) : 0.0f;
         }
         epi_bar_sync();
