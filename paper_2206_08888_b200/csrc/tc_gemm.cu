@@ -135,6 +135,25 @@ __device__ __forceinline__ void tmem_ld_wait(float* v) {
                  "+f"(v[28]), "+f"(v[29]), "+f"(v[30]), "+f"(v[31]));
 }
 
+// 16-column variants (half the registers per in-flight buffer)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+        "=f"(v[7]), "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]),
+        "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld_wait16(float* v) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  asm volatile(""
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]),
+                 "+f"(v[6]), "+f"(v[7]), "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]),
+                 "+f"(v[12]), "+f"(v[13]), "+f"(v[14]), "+f"(v[15]));
+}
+
 template <int BN>
 __host__ __device__ constexpr uint32_t tmem_cols() {
   return BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
@@ -902,48 +921,64 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
 // k_mlp_fwd2 (BF16 mode): one persistent launch evaluates hidden layer 1, hidden layer 2 and the
 // output layer of an MLP population.  Per 128-row tile of a group:
 //   producer : X tile (one 64-wide K chunk: in <= 64) and W1 into the layer-1 buffers, then W2
-//              through a 2-deep ring of 64-row K chunks
-//   MMA      : acc1 (TMEM cols 0..255) = X W1; after the epilogue has turned acc1 into h1 in
+//              through a ring of 64-row K chunks (3 deep: most of the next tile's W2 lands
+//              while the current tile's layer-2 epilogue runs)
+//   MMA      : acc1 (TMEM cols 0..255) = X W1; after the E1 warps have turned acc1 into h1 in
 //              shared memory, acc2 (cols 256..511) = h1 W2 with A read from that shared-memory
 //              copy (K-major, 128B swizzle) -- h1 never round-trips through HBM
-//   epilogue : E1 relu(acc1 + b1) -> bf16 K-major operand tile (+ HBM copy and mask bits when
-//              kept); E2 relu(acc2 + b2) -> output layer on CUDA cores (+ h2 to HBM when kept)
-// The layer-1 MMA of tile i+1 overlaps E2 of tile i (acc1 is free once E1 consumed it).
-constexpr uint32_t kF2H1 = 65536;  // h1 operand: 4 K chunks x (128 rows x 128 B); E2 staging
+//   E1 warps : relu(acc1 + b1) -> bf16 K-major operand tile (+ HBM copy and mask bits when kept)
+//   E2 warps : relu(acc2 + b2) -> output layer on CUDA cores (+ h2 to HBM when kept, stored
+//              straight from registers: the W2 ring holds the shared memory a staging box would)
+// E1 and E2 are separate warp groups: E1 of tile i+1 runs while E2 drains tile i (acc1 and acc2
+// are disjoint TMEM columns; E1 only waits until the layer-2 MMA of tile i has read sH1), so
+// the per-tile period is E1 + the layer-2 MMA tail instead of E1 + MMA + E2.
+constexpr uint32_t kF2H1 = 65536;  // h1 operand: 4 K chunks x (128 rows x 128 B)
 constexpr uint32_t kF2X = kBM * kRowBytes;   // 16 KB
 constexpr uint32_t kF2W = 256 * kRowBytes;   // 32 KB: 64 K rows x 256 N, as 4 boxes of 64 x 64
-constexpr uint32_t kF2Ring = 2;
+constexpr int kF2Threads = 64 + 2 * kEpiThreads;  // TMA, MMA, 8 E1 warps, 8 E2 warps
+// W2 ring depth (2 when the output layer's shared memory is large)
+template <int NO>
+__host__ __device__ constexpr int f2_ring() { return NO <= 6 ? 3 : 2; }
 
 template <int NO>
 __host__ __device__ constexpr size_t fwd2_smem() {
-  return kF2H1 + kF2X + kF2W + kF2Ring * kF2W + 256 + 2 * 256 * 4 + 256 * NO * 4 +
+  return kF2H1 + kF2X + kF2W + f2_ring<NO>() * kF2W + 256 + 3 * 256 * 4 + 256 * NO * 4 +
          2 * kBM * NO * 4 + 1024;
 }
 
+__device__ __forceinline__ void e2_bar_sync() {  // the E2 warps only
+  asm volatile("bar.sync 6, %0;" ::"n"(kEpiThreads) : "memory");
+}
+
+// NO = 1, 6: exact output width; NO = 12: any width <= 12 (runtime g.nout)
 template <int NO>
-__global__ void __launch_bounds__(64 + kEpiThreads, 1)
+__global__ void __launch_bounds__(kF2Threads, 1)
     k_mlp_fwd2(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmH1,
-               const __grid_constant__ CUtensorMap tmH2, const Fwd2Args g) {
+               const Fwd2Args g) {
+  constexpr bool kRt = NO == 12;
+  constexpr int R = f2_ring<NO>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sH1 = smem;
   uint8_t* sX = sH1 + kF2H1;
   uint8_t* sW1 = sX + kF2X;
   uint8_t* sW2 = sW1 + kF2W;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sW2 + kF2Ring * kF2W);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW2 + R * kF2W);
   uint64_t* l1full = bars;
   uint64_t* l1empty = bars + 1;
-  uint64_t* w2full = bars + 2;   // [2]
-  uint64_t* w2empty = bars + 4;  // [2]
-  uint64_t* acc1full = bars + 6;
-  uint64_t* acc2full = bars + 7;
-  uint64_t* acc2empty = bars + 8;
-  uint64_t* sbar = bars + 9;
-  uint64_t* h1kc = bars + 10;  // [4]: K chunk kc of h1 written (4 warps of its column half)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-  float* fz_b1 = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);
-  float* fz_b2 = fz_b1 + 256;
+  uint64_t* w2full = bars + 2;   // [R <= 3]
+  uint64_t* w2empty = bars + 5;  // [R <= 3]
+  uint64_t* acc1full = bars + 8;
+  uint64_t* acc2full = bars + 9;
+  uint64_t* acc2empty = bars + 10;
+  uint64_t* sbar1 = bars + 11;   // [2] b1 staging (E1, double-buffered: the next tile's b1 is
+                                 // fetched while this tile's E1 runs)
+  uint64_t* h1kc = bars + 13;    // [4]: K chunk kc of h1 written (4 warps of its column half)
+  uint64_t* sbar2 = bars + 17;   // b2 / W_out staging (E2)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  float* fz_b1 = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256);  // [2][256]
+  float* fz_b2 = fz_b1 + 512;
   float* fz_w = fz_b2 + 256;
   float* osum = fz_w + 256 * NO;  // [2][4][32][NO]
 
@@ -954,13 +989,13 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   // layer-2 K chunk order: the two column halves of E1 are written concurrently, so the MMAs
   // alternate halves (0, 2, 1, 3 for H1 = 256) and start after the first chunk of each half
   auto korder = [&](int j) { return (j & 1) * (nk2 / 2) + (j >> 1); };
-  const int nout = NO < 16 ? NO : g.nout;
+  const int nout = kRt ? g.nout : NO;
   if (threadIdx.x == 0) TC_TRACE(0);
 
   if (threadIdx.x == 0) {
     mbar_init(l1full, 1);
     mbar_init(l1empty, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < R; ++s) {
       mbar_init(&w2full[s], 1);
       mbar_init(&w2empty[s], 1);
     }
@@ -968,7 +1003,9 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
     for (int k = 0; k < 4; ++k) mbar_init(&h1kc[k], kEpiWarps / 2);
     mbar_init(acc2full, 1);
     mbar_init(acc2empty, kEpiWarps);
-    mbar_init(sbar, 1);
+    mbar_init(&sbar1[0], 1);
+    mbar_init(&sbar1[1], 1);
+    mbar_init(sbar2, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW1)) : "memory");
@@ -1004,8 +1041,8 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) tma_load_3d(&tmW1, l1full, sW1 + j * 8192, 64 * j, 0, grp);
         for (int kc = 0; kc < nk2; ++kc, ++cnt) {
-          const int s = cnt & 1;
-          if (cnt >= 2) mbar_wait(&w2empty[s], ((cnt >> 1) - 1) & 1);
+          const int s = cnt % R;
+          if (cnt >= R) mbar_wait(&w2empty[s], (cnt / R - 1) & 1);
           mbar_expect_tx(&w2full[s], kF2W);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -1023,6 +1060,8 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
       int it = 0, cnt = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         if (!active(t / m_tiles)) continue;
+        // acc1 is free: every h1 chunk of the previous tile was waited on below, i.e. E1 has
+        // read acc1 out
         mbar_wait(l1full, it & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
@@ -1033,9 +1072,9 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
         mma_commit(acc1full);
         if (it > 0) mbar_wait(acc2empty, (it - 1) & 1);
         for (int j = 0; j < nk2; ++j, ++cnt) {
-          const int kc = korder(j), s = cnt & 1;
+          const int kc = korder(j), s = cnt % R;
           mbar_wait(&h1kc[kc], it & 1);  // this K chunk of h1 is in shared memory
-          mbar_wait(&w2full[s], (cnt >> 1) & 1);
+          mbar_wait(&w2full[s], (cnt / R) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
@@ -1044,98 +1083,97 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
                      (j | kk) ? 1u : 0u);
           mma_commit(&w2empty[s]);
         }
-        mma_commit(acc2full);
+        mma_commit(acc2full);  // also: the layer-2 MMAs have read sH1
         ++it;
       }
     }
-  } else {
-    // ---------------- epilogue: warp w reads TMEM lane quadrant q = w % 4 and handles the
-    // column half hf of each layer
+  } else if (warp < 2 + kEpiWarps) {
+    // ---------------- E1: warp w reads TMEM lane quadrant q = w % 4, column half hf of acc1
     const int ew = warp - 2, q = warp & 3, hf = ew >> 2;
-    uint8_t* wbuf = sH1 + ew * 4096;  // E2 staging: two 2 KB bf16 boxes per warp (inside sH1)
-    constexpr int NA = NO;
-    const int hc1 = g.H1 / 64;               // 32-column chunks of h1 per half
-    const int hc2 = (g.H2 + 63) / 64;        // 32-column chunks of h2 per half
+    const int hc1 = g.H1 / 64;  // 32-column chunks of h1 per half
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    for (int e = threadIdx.x - 64; e < 2 * 256 + 256 * NO; e += kEpiThreads) fz_b1[e] = 0.0f;
-    int it = 0, nchunk = 0;
+    int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
       const int grp = t / m_tiles, m0 = (t % m_tiles) * kBM;
       if (!active(grp)) continue;
-      const int mem = grp % g.n_members;
       const int row0 = m0 + q * 32, row = row0 + lane;
       const int r = q * 32 + lane;  // row inside the tile
       if (threadIdx.x == 64) TC_TRACE_TILE(it, 0);
-      // ---- stage b1, b2, W_out of this group; the previous tile's staging stores (inside sH1)
-      // must have been read out before E1 rewrites sH1
+      // every E1 warp is done with the previous tile (its b1 buffer is free, its h1 stores have
+      // read sH1 out); prefetch the next active tile's b1 into that buffer
       if (lane == 0) tma_store_wait_read<0>();
       __syncwarp();
       epi_bar_sync();
       if (threadIdx.x == 64) {
-        const uint32_t by1 = g.H1 * 4, by2 = g.H2 * 4, byw = g.H2 * nout * 4;
-        mbar_expect_tx(sbar, by1 + by2 + byw);
-        bulk_g2s(fz_b1, g.b1 + grp * g.p_gs, by1, sbar);
-        bulk_g2s(fz_b2, g.b2 + grp * g.p_gs, by2, sbar);
-        bulk_g2s(fz_w, g.ow + grp * g.p_gs, byw, sbar);
-      }
-      float ob[NA], ep[NA];
-      if (hf == 0) {
-        const float* obg = g.ow + grp * g.p_gs + static_cast<long long>(g.H2) * nout;
-        const bool noisy = g.out_epi == EPI_BIAS_TANH_NOISE && g.noise_eps && row < g.M;
-        const float* eg =
-            noisy ? g.noise_eps + grp * g.ne_gs + static_cast<long long>(row) * g.ne_rs : nullptr;
-#pragma unroll
-        for (int o = 0; o < NA; ++o) {
-          ob[o] = o < nout ? __ldg(obg + o) : 0.0f;
-          ep[o] = (noisy && o < nout) ? __ldg(eg + o) : 0.0f;
+        auto stage_b1 = [&](int tt, int buf) {
+          mbar_expect_tx(&sbar1[buf], g.H1 * 4);
+          bulk_g2s(fz_b1 + buf * 256, g.b1 + (tt / m_tiles) * g.p_gs, g.H1 * 4, &sbar1[buf]);
+        };
+        if (it == 0) stage_b1(t, 0);
+        for (int tn = t + gridDim.x; tn < num_tiles; tn += gridDim.x) {
+          if (active(tn / m_tiles)) {
+            stage_b1(tn, (it + 1) & 1);
+            break;
+          }
         }
       }
-      mbar_wait(sbar, it & 1);
-
-      // ---- E1: h1 = relu(acc1 + b1) -> sH1 (K-major, 128B swizzle) [+ HBM, mask bits]
+      const float* b1s = fz_b1 + (it & 1) * 256;
+      mbar_wait(&sbar1[it & 1], (it >> 1) & 1);
       mbar_wait(acc1full, it & 1);
+      if (it > 0) mbar_wait(acc2full, (it - 1) & 1);  // the layer-2 MMAs have read sH1
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (threadIdx.x == 64) TC_TRACE_TILE(it, 1);
-      {
-        const uint32_t tacc = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        uint32_t* mrow = (g.m1 && row < g.M)
-                             ? g.m1 + grp * g.m1_gs + static_cast<long long>(row) * g.m1_ld
-                             : nullptr;
-        // chunks in register pairs (va, vb): the next chunk's tcgen05.ld is in flight while the
-        // current one is processed; static register names (no local-memory arrays)
-        auto e1_chunk = [&](float* cur, int c0) {
-          uint32_t bits = 0u;
+      const uint32_t tacc = tmem + (static_cast<uint32_t>(q * 32) << 16);
+      uint32_t* mrow = (g.m1 && row < g.M)
+                           ? g.m1 + grp * g.m1_gs + static_cast<long long>(row) * g.m1_ld
+                           : nullptr;
+      // 16-column sub-chunks in register pairs (va, vb): the next sub-chunk's tcgen05.ld is in
+      // flight while the current one is processed (static register names, 96-register budget)
+      // (mask bits only when a mask is kept: two instantiations of the sub-chunk body)
+      uint32_t bits = 0u;
+      auto e1_body = [&](float* cur, int c0, auto keep_mask) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float z = cur[j] + fz_b1[c0 + j];
-            cur[j] = z > 0.0f ? z : 0.0f;
-            bits |= (z > 0.0f ? 1u : 0u) << j;
-          }
-          uint8_t* rowp = sH1 + (c0 >> 6) * 16384 + r * 128;
-          const int j0 = (c0 & 63) >> 3;
+        for (int j = 0; j < 16; ++j) {
+          const float z = cur[j] + b1s[c0 + j];
+          cur[j] = z > 0.0f ? z : 0.0f;
+          if constexpr (decltype(keep_mask)::value) bits |= (z > 0.0f ? 1u : 0u) << ((c0 & 16) + j);
+        }
+        uint8_t* rowp = sH1 + (c0 >> 6) * 16384 + r * 128;
+        const int j0 = (c0 & 63) >> 3;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint4 w4 = make_uint4(pack_bf16x2(cur[8 * u], cur[8 * u + 1]),
-                                        pack_bf16x2(cur[8 * u + 2], cur[8 * u + 3]),
-                                        pack_bf16x2(cur[8 * u + 4], cur[8 * u + 5]),
-                                        pack_bf16x2(cur[8 * u + 6], cur[8 * u + 7]));
-            *reinterpret_cast<uint4*>(rowp + (((j0 + u) ^ (r & 7)) << 4)) = w4;
+        for (int u = 0; u < 2; ++u) {
+          const uint4 w4 = make_uint4(pack_bf16x2(cur[8 * u], cur[8 * u + 1]),
+                                      pack_bf16x2(cur[8 * u + 2], cur[8 * u + 3]),
+                                      pack_bf16x2(cur[8 * u + 4], cur[8 * u + 5]),
+                                      pack_bf16x2(cur[8 * u + 6], cur[8 * u + 7]));
+          *reinterpret_cast<uint4*>(rowp + (((j0 + u) ^ (r & 7)) << 4)) = w4;
+        }
+        if constexpr (decltype(keep_mask)::value) {
+          if (c0 & 16) {
+            mrow[c0 >> 5] = bits;
+            bits = 0u;
           }
-          if (mrow) mrow[c0 >> 5] = bits;
-        };
-        float va[32], vb[32];
-        const int cb = hf * hc1 * 32;  // a multiple of 64: each pair is one K chunk of h1
-        tmem_ld32(tacc + static_cast<uint32_t>(cb), va);
+        }
+      };
+      auto e1_sub = [&](float* cur, int c0) {
+        if (mrow) e1_body(cur, c0, std::true_type{});
+        else e1_body(cur, c0, std::false_type{});
+      };
+      float va[16], vb[16];
+      const int cb = hf * hc1 * 32;  // a multiple of 64: every 4 sub-chunks are one K chunk
+      const int ns = hc1 * 2;
+      tmem_ld16(tacc + static_cast<uint32_t>(cb), va);
 #pragma unroll 1
-        for (int ci = 0; ci < hc1; ci += 2) {
-          tmem_ld_wait(va);
-          tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 1) * 32), vb);
-          e1_chunk(va, cb + ci * 32);
-          tmem_ld_wait(vb);
-          if (ci + 2 < hc1) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 2) * 32), va);
-          e1_chunk(vb, cb + (ci + 1) * 32);
+      for (int si = 0; si < ns; si += 2) {
+        tmem_ld_wait16(va);
+        tmem_ld16(tacc + static_cast<uint32_t>(cb + (si + 1) * 16), vb);
+        e1_sub(va, cb + si * 16);
+        tmem_ld_wait16(vb);
+        if (si + 2 < ns) tmem_ld16(tacc + static_cast<uint32_t>(cb + (si + 2) * 16), va);
+        e1_sub(vb, cb + (si + 1) * 16);
+        if ((si & 3) == 2) {
           // K chunk kc complete in this warp's rows: visible to the MMA (async proxy), to HBM
-          const int kc = (cb + ci * 32) >> 6;
+          const int kc = (cb + si * 16) >> 6;
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
@@ -1146,116 +1184,157 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
         }
       }
       if (threadIdx.x == 64) TC_TRACE_TILE(it, 2);
-
-      // ---- E2: relu(acc2 + b2) -> output layer (+ h2 to HBM)
+      ++it;
+    }
+    if (lane == 0) tma_store_wait_all();
+  } else {
+    // ---------------- E2: warp w reads TMEM lane quadrant q = w % 4, column half hf of acc2
+    const int ew = warp - 2 - kEpiWarps, q = warp & 3, hf = ew >> 2;
+    constexpr int NA = NO;
+    const int hc2 = (g.H2 + 63) / 64;  // 32-column chunks of h2 per half
+    const int tid2 = threadIdx.x - 64 - kEpiThreads;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int grp = t / m_tiles, m0 = (t % m_tiles) * kBM;
+      if (!active(grp)) continue;
+      const int mem = grp % g.n_members;
+      const int row0 = m0 + q * 32, row = row0 + lane;
+      // ---- stage b2, W_out of this group once every E2 warp is done with the previous tile's
+      e2_bar_sync();
+      if (tid2 == 0) {
+        const uint32_t by2 = g.H2 * 4, byw = g.H2 * nout * 4;
+        mbar_expect_tx(sbar2, by2 + byw);
+        bulk_g2s(fz_b2, g.b2 + grp * g.p_gs, by2, sbar2);
+        bulk_g2s(fz_w, g.ow + grp * g.p_gs, byw, sbar2);
+      }
+      const float* obg = g.ow + grp * g.p_gs + static_cast<long long>(g.H2) * nout;
+      const bool noisy = g.out_epi == EPI_BIAS_TANH_NOISE && g.noise_eps && row < g.M;
+      const float* eg =
+          noisy ? g.noise_eps + grp * g.ne_gs + static_cast<long long>(row) * g.ne_rs : nullptr;
+      float ob[NA], ep[NA];
+      if (!kRt && hf == 0) {  // fixed widths: output bias and noise in flight during E2
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          ob[o] = __ldg(obg + o);
+          ep[o] = noisy ? __ldg(eg + o) : 0.0f;
+        }
+      }
+      mbar_wait(sbar2, it & 1);
       mbar_wait(acc2full, it & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (threadIdx.x == 64) TC_TRACE_TILE(it, 3);
-      // sH1 becomes staging: h1's HBM copies must have been read out by every warp
-      if (lane == 0) tma_store_wait_read<0>();
-      __syncwarp();
-      epi_bar_sync();
-      {
-        const uint32_t tacc = tmem + 256u + (static_cast<uint32_t>(q * 32) << 16);
-        uint32_t* mrow = (g.m2 && row < g.M)
-                             ? g.m2 + grp * g.m2_gs + static_cast<long long>(row) * g.m2_ld
-                             : nullptr;
-        float oacc[NA];
+      if (tid2 == 0) TC_TRACE_TILE(it, 3);
+      const uint32_t tacc = tmem + 256u + (static_cast<uint32_t>(q * 32) << 16);
+      uint32_t* mrow = (g.m2 && row < g.M)
+                           ? g.m2 + grp * g.m2_gs + static_cast<long long>(row) * g.m2_ld
+                           : nullptr;
+      float oacc[NA];
 #pragma unroll
-        for (int o = 0; o < NA; ++o) oacc[o] = 0.0f;
-        auto e2_chunk = [&](float* cur, int c0) {
-          uint32_t bits = 0u;
+      for (int o = 0; o < NA; ++o) oacc[o] = 0.0f;
+      // 16-column sub-chunks, double-buffered like E1; kept h2 rows go to HBM as 2 x 16 B
+      __nv_bfloat16* h2row = (g.H2g && row < g.M)
+                                 ? static_cast<__nv_bfloat16*>(g.H2g) + grp * g.h2_gs +
+                                       static_cast<long long>(row) * g.h2_ld
+                                 : nullptr;
+      uint32_t bits = 0u;
+      auto e2_body = [&](float* cur, int c0, auto keep_mask) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float z = cur[j] + fz_b2[c0 + j];
-            const float h = z > 0.0f ? z : 0.0f;
-            cur[j] = h;
-            bits |= (z > 0.0f ? 1u : 0u) << j;
-            const float* wr = fz_w + (c0 + j) * nout;
+        for (int j = 0; j < 16; ++j) {
+          const float z = cur[j] + fz_b2[c0 + j];
+          const float h = z > 0.0f ? z : 0.0f;
+          cur[j] = h;
+          if constexpr (decltype(keep_mask)::value) bits |= (z > 0.0f ? 1u : 0u) << ((c0 & 16) + j);
+          const float* wr = fz_w + (c0 + j) * nout;
 #pragma unroll
-            for (int o = 0; o < NA; ++o) {
-              if (NO == 16 && o >= nout) break;
-              oacc[o] = oacc[o] + h * wr[o];
-            }
+          for (int o = 0; o < NA; ++o) {
+            if (kRt && o >= nout) break;
+            oacc[o] = oacc[o] + h * wr[o];
           }
-          if (g.H2g) {
-            uint8_t* box = wbuf + (nchunk & 1) * 2048;
-            if (lane == 0 && nchunk >= 2) tma_store_wait_read<1>();
-            __syncwarp();
+        }
+        if (h2row) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint4 w4 = make_uint4(pack_bf16x2(cur[8 * u], cur[8 * u + 1]),
-                                          pack_bf16x2(cur[8 * u + 2], cur[8 * u + 3]),
-                                          pack_bf16x2(cur[8 * u + 4], cur[8 * u + 5]),
-                                          pack_bf16x2(cur[8 * u + 6], cur[8 * u + 7]));
-              *reinterpret_cast<uint4*>(box + sw64(lane, u)) = w4;
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) tma_store_3d(&tmH2, box, c0, row0, grp);
-            ++nchunk;
-            if (mrow) mrow[c0 >> 5] = bits;
+          for (int u = 0; u < 2; ++u)
+            *reinterpret_cast<uint4*>(h2row + c0 + 8 * u) =
+                make_uint4(pack_bf16x2(cur[8 * u], cur[8 * u + 1]),
+                           pack_bf16x2(cur[8 * u + 2], cur[8 * u + 3]),
+                           pack_bf16x2(cur[8 * u + 4], cur[8 * u + 5]),
+                           pack_bf16x2(cur[8 * u + 6], cur[8 * u + 7]));
+        }
+        if constexpr (decltype(keep_mask)::value) {
+          if (c0 & 16) {
+            mrow[c0 >> 5] = bits;
+            bits = 0u;
           }
-        };
-        const int cb = hf * hc2 * 32;
-        const int nc = max(0, min(hc2, (g.H2 - cb + 31) / 32));  // this half's chunks < H2
-        float va[32], vb[32];
-        if (nc > 0) tmem_ld32(tacc + static_cast<uint32_t>(cb), va);
+        }
+      };
+      auto e2_sub = [&](float* cur, int c0) {
+        if (mrow) e2_body(cur, c0, std::true_type{});
+        else e2_body(cur, c0, std::false_type{});
+      };
+      const int cb = hf * hc2 * 32;
+      const int nc = max(0, min(hc2, (g.H2 - cb + 31) / 32));  // this half's chunks < H2
+      const int ns = 2 * nc;                                   // 16-column sub-chunks
+      float va[16], vb[16];
+      if (ns > 0) tmem_ld16(tacc + static_cast<uint32_t>(cb), va);
 #pragma unroll 1
-        for (int ci = 0; ci < nc; ci += 2) {
-          tmem_ld_wait(va);
-          if (ci + 1 < nc) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 1) * 32), vb);
-          e2_chunk(va, cb + ci * 32);
-          if (ci + 1 < nc) {
-            tmem_ld_wait(vb);
-            if (ci + 2 < nc) tmem_ld32(tacc + static_cast<uint32_t>(cb + (ci + 2) * 32), va);
-            e2_chunk(vb, cb + (ci + 1) * 32);
-          }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(acc2empty);
-        if (threadIdx.x == 64) TC_TRACE_TILE(it, 4);
-        // half 1 hands its partial sums to half 0 (double-buffered by tile parity)
-        float* os = osum + (((it & 1) * 4 + q) * 32 + lane) * NA;
-        if (hf == 1) {
+      for (int si = 0; si < ns; si += 2) {
+        tmem_ld_wait16(va);
+        tmem_ld16(tacc + static_cast<uint32_t>(cb + (si + 1) * 16), vb);
+        e2_sub(va, cb + si * 16);
+        tmem_ld_wait16(vb);
+        if (si + 2 < ns) tmem_ld16(tacc + static_cast<uint32_t>(cb + (si + 2) * 16), va);
+        e2_sub(vb, cb + (si + 1) * 16);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(acc2empty);
+      if (tid2 == 0) TC_TRACE_TILE(it, 4);
+      // half 1 hands its partial sums to half 0 (double-buffered by tile parity)
+      float* os = osum + (((it & 1) * 4 + q) * 32 + lane) * NA;
+      if (hf == 1) {
 #pragma unroll
-          for (int o = 0; o < NA; ++o) os[o] = oacc[o];
-        }
-        quad_bar_sync(q);
-        if (hf == 0 && row < g.M) {
-          const long long obase = grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
-          const bool tanh_out = g.out_epi == EPI_BIAS_TANH || g.out_epi == EPI_BIAS_TANH_NOISE;
+        for (int o = 0; o < NA; ++o) os[o] = oacc[o];
+      }
+      quad_bar_sync(q);
+      if (hf == 0 && row < g.M) {
+        if (kRt) {
 #pragma unroll
           for (int o = 0; o < NA; ++o) {
             if (o >= nout) break;
-            const float y = (oacc[o] + os[o]) + ob[o];
-            float rr = y;
-            if (tanh_out) {
-              const float th = epi_tanhf(y);
-              if (g.oC2) g.oC2[grp * g.oc2_gs + static_cast<long long>(row) * g.oc2_rs + o] = th;
-              rr = (g.out_scale != 1.0f) ? th * g.out_scale : th;
-              if (g.out_epi == EPI_BIAS_TANH_NOISE) {
-                float eps;
-                if (g.noise_eps) {
-                  eps = ep[o];
-                } else {
-                  const uint64_t e = static_cast<uint64_t>(row) * nout + o;
-                  eps = epi_normal(g.noise_key[mem], 2 * e) * g.noise_sd[mem];
-                  eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
-                }
-                rr = clampf_ref(rr + eps, -g.bound, g.bound);
-              }
-            }
-            if (g.oc16) static_cast<__nv_bfloat16*>(g.oC)[obase + o] = __float2bfloat16_rn(rr);
-            else static_cast<float*>(g.oC)[obase + o] = rr;
+            ob[o] = __ldg(obg + o);
+            ep[o] = noisy ? __ldg(eg + o) : 0.0f;
           }
+        }
+        const long long obase = grp * g.oc_gs + static_cast<long long>(row) * g.oc_rs;
+        const bool tanh_out = g.out_epi == EPI_BIAS_TANH || g.out_epi == EPI_BIAS_TANH_NOISE;
+#pragma unroll
+        for (int o = 0; o < NA; ++o) {
+          if (o >= nout) break;
+          const float y = (oacc[o] + os[o]) + ob[o];
+          float rr = y;
+          if (tanh_out) {
+            const float th = epi_tanhf(y);
+            if (g.oC2) g.oC2[grp * g.oc2_gs + static_cast<long long>(row) * g.oc2_rs + o] = th;
+            rr = (g.out_scale != 1.0f) ? th * g.out_scale : th;
+            if (g.out_epi == EPI_BIAS_TANH_NOISE) {
+              float eps;
+              if (g.noise_eps) {
+                eps = ep[o];
+              } else {
+                const uint64_t e = static_cast<uint64_t>(row) * nout + o;
+                eps = epi_normal(g.noise_key[mem], 2 * e) * g.noise_sd[mem];
+                eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+              }
+              rr = clampf_ref(rr + eps, -g.bound, g.bound);
+            }
+          }
+          if (g.oc16) static_cast<__nv_bfloat16*>(g.oC)[obase + o] = __float2bfloat16_rn(rr);
+          else static_cast<float*>(g.oC)[obase + o] = rr;
         }
       }
       ++it;
     }
-    if (lane == 0) tma_store_wait_all();
-    if (threadIdx.x == 64) TC_TRACE(62);
+    if (tid2 == 0) TC_TRACE(62);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1506,7 +1585,7 @@ void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn
 bool mlp_fwd2_ok(const Fwd2Args& a) {
   auto al16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
   return a.in >= 1 && a.in <= 64 && a.H1 % 128 == 0 && a.H1 <= 256 && a.H2 % 32 == 0 &&
-         a.H2 >= 32 && a.H2 <= 256 && a.nout >= 1 && a.nout <= 16 && a.x_ld % 8 == 0 &&
+         a.H2 >= 32 && a.H2 <= 256 && a.nout >= 1 && a.nout <= 12 && a.x_ld % 8 == 0 &&
          a.x_gs % 8 == 0 && a.w_gs % 8 == 0 && a.p_gs % 4 == 0 && al16(a.X) && al16(a.W1) &&
          al16(a.W2) && al16(a.b1) && al16(a.b2) && al16(a.ow) &&
          (!a.H1g || (al16(a.H1g) && a.h1_ld % 8 == 0 && a.h1_gs % 8 == 0)) &&
@@ -1528,12 +1607,11 @@ void launch_fwd2_tpl(const Fwd2Args& a, cudaStream_t s) {
                                    a.x_ld, a.x_gs, 64, kBM, SWZ_128);
   const CUtensorMap tw1 = make_tmap(a.W1, 2, a.H1, a.in, a.groups, a.H1, a.w_gs, 64, 64, SWZ_128);
   const CUtensorMap tw2 = make_tmap(a.W2, 2, a.H2, a.H1, a.groups, a.H2, a.w_gs, 64, 64, SWZ_128);
-  CUtensorMap th1{}, th2{};
+  CUtensorMap th1{};
   if (a.H1g) th1 = make_tmap(a.H1g, 2, a.H1, a.M, a.groups, a.h1_ld, a.h1_gs, 64, 32, SWZ_128);
-  if (a.H2g) th2 = make_tmap(a.H2g, 2, a.H2, a.M, a.groups, a.h2_ld, a.h2_gs, 32, 32, SWZ_64);
   const int tiles = a.groups * ((a.M + kBM - 1) / kBM);
-  launch_k(k_mlp_fwd2<NO>, std::min(tiles, num_sms()), 64 + kEpiThreads, smem, s, tx, tw1, tw2,
-           th1, th2, a);
+  launch_k(k_mlp_fwd2<NO>, std::min(tiles, num_sms()), kF2Threads, smem, s, tx, tw1, tw2,
+           th1, a);
 }
 }  // namespace
 
@@ -1549,8 +1627,7 @@ void launch_mlp_fwd2(const Fwd2Args& a0, cudaStream_t s) {
   switch (a.nout) {
     case 1: launch_fwd2_tpl<1>(a, s); return;
     case 6: launch_fwd2_tpl<6>(a, s); return;
-    case 12: launch_fwd2_tpl<12>(a, s); return;
-    default: launch_fwd2_tpl<16>(a, s); return;
+    default: launch_fwd2_tpl<12>(a, s); return;  // any width <= 12
   }
 }
 

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--pop", type=int, default=80)
     ap.add_argument("--out", default=None)
     ap.add_argument("--precision", default="tf32", choices=["tf32", "bf16"])
+    ap.add_argument("--dump", type=int, nargs="*", default=[0, 2], help="launches to dump")
     args = ap.parse_args()
     os.environ.setdefault("PBRL_TC_TRACE", "1")
     import torch
@@ -111,6 +112,37 @@ def main():
         gap = (a - prev) / 1e3 if prev is not None else 0.0
         lines.append(f"| {li} | {(a - t00) / 1e3:.1f} | {(b - t00) / 1e3:.1f} | {gap:.1f} |")
         prev = b
+    # per-CTA spread: entry, first tile start (after the PDL wait), exit -- relative to the
+    # launch's first CTA entry
+    lines += ["", "| # | entry p50/max us | tile0 p50/max us | exit min/p50/max us |",
+              "|---|---|---|---|"]
+    for li, a, b in win:
+        s = stamps[li].astype(np.int64)
+        s = s[s[:, 0] > 0]
+        e0, t0s, ex = (s[:, 0] - a) / 1e3, (s[:, 2] - a) / 1e3, (s[:, 63] - a) / 1e3
+        t0s = t0s[s[:, 2] > 0]
+        q = lambda v, f: float(np.percentile(v, f)) if len(v) else float("nan")
+        lines.append(f"| {li} | {q(e0, 50):.1f} / {e0.max():.1f} | {q(t0s, 50):.1f} / "
+                     f"{q(t0s, 100):.1f} | {ex.min():.1f} / {q(ex, 50):.1f} / {ex.max():.1f} |")
+    # raw per-tile stamps (us from the launch's first entry) of the slowest and the median CTA
+    for li in args.dump:
+        s = stamps[li].astype(np.int64)
+        s = s[s[:, 0] > 0]
+        if not len(s):
+            continue
+        a = s[:, 0].min()
+        order = np.argsort(s[:, 63])
+        lines += ["", f"launch {li}: tile stamps [start, acc1/after waits, E1 done, acc2, E2 done]"]
+        for tag, c in (("slowest", s[order[-1]]), ("median", s[order[len(order) // 2]])):
+            tl = []
+            for it in range(10):
+                b = 2 + 6 * it
+                if c[b] == 0:
+                    break
+                tl.append("[" + ", ".join(f"{(c[b + k] - a) / 1e3:.1f}" if c[b + k] else "-"
+                                          for k in range(5)) + "]")
+            lines.append(f"  {tag}: entry {(c[0] - a) / 1e3:.1f} " + " ".join(tl) +
+                         f" exit {(c[63] - a) / 1e3:.1f}")
     if win:
         busy = sum(b - a for _, a, b in win) / 1e3
         lines.append(f"\nGEMM launches busy {busy:.1f} us of a {(win[-1][2] - t00) / 1e3:.1f} us window")
