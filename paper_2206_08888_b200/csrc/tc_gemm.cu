@@ -223,10 +223,10 @@ __device__ __forceinline__ uint32_t sw128(int r, int j) {
 __device__ __forceinline__ uint32_t sw64(int r, int j) {
   return static_cast<uint32_t>(r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
 }
+// one cvt.rn.bf16x2.f32 (F2FP.BF16.F32.PACK_AB); lo in the low half, round-to-nearest-even
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
-  const uint32_t a = __bfloat16_as_ushort(__float2bfloat16_rn(lo));
-  const uint32_t b = __bfloat16_as_ushort(__float2bfloat16_rn(hi));
-  return a | (b << 16);
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
 }
 
 // Optional phase timeline (TcArgs::trace, diagnostics only): per CTA kTraceSlots globaltimer
@@ -1084,6 +1084,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           mma_commit(&w2empty[s]);
         }
         mma_commit(acc2full);  // also: the layer-2 MMAs have read sH1
+        TC_TRACE_TILE(it, 5);  // every h1 chunk of this tile was waited on and issued
         ++it;
       }
     }
@@ -1228,7 +1229,9 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       uint32_t* mrow = (g.m2 && row < g.M)
                            ? g.m2 + grp * g.m2_gs + static_cast<long long>(row) * g.m2_ld
                            : nullptr;
-      float oacc[NA];
+      // output-layer partial dot products (fused multiply-add: BF16 mode only); a single output
+      // keeps 4 interleaved partial sums so the FMA chain is not one dependent sequence
+      float oacc[NA], o1p[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int o = 0; o < NA; ++o) oacc[o] = 0.0f;
       // 16-column sub-chunks, double-buffered like E1; kept h2 rows go to HBM as 2 x 16 B
@@ -1245,10 +1248,15 @@ __global__ void __launch_bounds__(kF2Threads, 1)
           cur[j] = h;
           if constexpr (decltype(keep_mask)::value) bits |= (z > 0.0f ? 1u : 0u) << ((c0 & 16) + j);
           const float* wr = fz_w + (c0 + j) * nout;
+          if constexpr (NO == 1) {
+            if (j & 3) o1p[(j & 3) - 1] = __fmaf_rn(h, wr[0], o1p[(j & 3) - 1]);
+            else oacc[0] = __fmaf_rn(h, wr[0], oacc[0]);
+          } else {
 #pragma unroll
-          for (int o = 0; o < NA; ++o) {
-            if (kRt && o >= nout) break;
-            oacc[o] = oacc[o] + h * wr[o];
+            for (int o = 0; o < NA; ++o) {
+              if (kRt && o >= nout) break;
+              oacc[o] = __fmaf_rn(h, wr[o], oacc[o]);
+            }
           }
         }
         if (h2row) {
@@ -1285,6 +1293,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
         if (si + 2 < ns) tmem_ld16(tacc + static_cast<uint32_t>(cb + (si + 2) * 16), va);
         e2_sub(vb, cb + (si + 1) * 16);
       }
+      if constexpr (NO == 1) oacc[0] = (oacc[0] + o1p[0]) + (o1p[1] + o1p[2]);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(acc2empty);

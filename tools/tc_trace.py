@@ -132,7 +132,8 @@ def main():
             continue
         a = s[:, 0].min()
         order = np.argsort(s[:, 63])
-        lines += ["", f"launch {li}: tile stamps [start, acc1/after waits, E1 done, acc2, E2 done]"]
+        lines += ["", f"launch {li}: tile stamps [start, acc1/after waits, E1 done, acc2, E2 done, "
+                  "MMA2 issued]"]
         for tag, c in (("slowest", s[order[-1]]), ("median", s[order[len(order) // 2]])):
             tl = []
             for it in range(10):
@@ -140,7 +141,7 @@ def main():
                 if c[b] == 0:
                     break
                 tl.append("[" + ", ".join(f"{(c[b + k] - a) / 1e3:.1f}" if c[b + k] else "-"
-                                          for k in range(5)) + "]")
+                                          for k in range(6)) + "]")
             lines.append(f"  {tag}: entry {(c[0] - a) / 1e3:.1f} " + " ".join(tl) +
                          f" exit {(c[63] - a) / 1e3:.1f}")
     if win:
