@@ -896,28 +896,30 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts
-template <typename AT>
+// (IT: 32-bit element indices whenever the batch allows -- the row / column split is then a
+// 32-bit division instead of a 64-bit one)
+template <typename AT, typename IT>
 __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float* s,
                              const float* a, const float* r, const float* s2, const float* d,
                              AT* in_sa, AT* in_s2a, AT* sa_pi, float* r_out, float* d_out,
                              AT* in_s, int lsp) {
   PDL_ENTRY();
-  const int dsa = ds + da;
-  const long long rows = static_cast<long long>(n) * B;
-  const long long total = rows * dsa;
-  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long row = e / dsa;
-    const int c = static_cast<int>(e % dsa);
-    const long long o = row * lsa + c;
+  const IT dsa = static_cast<IT>(ds + da);
+  const IT rows = static_cast<IT>(n) * static_cast<IT>(B);
+  const IT total = rows * dsa;
+  for (IT e = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<IT>(gridDim.x) * blockDim.x) {
+    const IT row = e / dsa;
+    const int c = static_cast<int>(e - row * dsa);
+    const long long o = static_cast<long long>(row) * lsa + c;
     if (c < ds) {
-      const float sv = s[row * ds + c];
+      const float sv = s[static_cast<long long>(row) * ds + c];
       act_st(in_sa, o, sv);
       act_st(sa_pi, o, sv);
-      act_st(in_s2a, o, s2[row * ds + c]);
-      if (in_s) act_st(in_s, row * lsp + c, sv);
+      act_st(in_s2a, o, s2[static_cast<long long>(row) * ds + c]);
+      if (in_s) act_st(in_s, static_cast<long long>(row) * lsp + c, sv);
     } else {
-      act_st(in_sa, o, a[row * da + (c - ds)]);
+      act_st(in_sa, o, a[static_cast<long long>(row) * da + (c - ds)]);
     }
     if (c == 0) {
       r_out[row] = r[row];
@@ -926,21 +928,34 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float*
   }
 }
 
+template <typename AT>
+static void launch_pack_t(int blocks, bool narrow, cudaStream_t st, int n, int B, int ds, int da,
+                          int lsa, const float* s, const float* a, const float* r, const float* s2,
+                          const float* d, void* in_sa, void* in_s2a, void* sa_pi, float* r_out,
+                          float* d_out, void* in_s, int lsp) {
+  if (narrow)
+    launch_k(k_pack_batch<AT, unsigned>, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d,
+             static_cast<AT*>(in_sa), static_cast<AT*>(in_s2a), static_cast<AT*>(sa_pi), r_out,
+             d_out, static_cast<AT*>(in_s), lsp);
+  else
+    launch_k(k_pack_batch<AT, long long>, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d,
+             static_cast<AT*>(in_sa), static_cast<AT*>(in_s2a), static_cast<AT*>(sa_pi), r_out,
+             d_out, static_cast<AT*>(in_s), lsp);
+}
+
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, void* in_sa,
                        void* in_s2a, void* sa_pi, float* r_out, float* d_out, int act16,
                        cudaStream_t st, void* in_s, int lsp) {
   const long long total = static_cast<long long>(n) * B * (ds + da);
   const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
+  const bool narrow = total + 256LL * blocks < (1LL << 32);
   if (act16)
-    launch_k(k_pack_batch<__nv_bfloat16>, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d,
-             static_cast<__nv_bfloat16*>(in_sa), static_cast<__nv_bfloat16*>(in_s2a),
-             static_cast<__nv_bfloat16*>(sa_pi), r_out, d_out,
-             static_cast<__nv_bfloat16*>(in_s), lsp);
+    launch_pack_t<__nv_bfloat16>(blocks, narrow, st, n, B, ds, da, lsa, s, a, r, s2, d, in_sa,
+                                 in_s2a, sa_pi, r_out, d_out, in_s, lsp);
   else
-    launch_k(k_pack_batch<float>, blocks, 256, 0, st, n, B, ds, da, lsa, s, a, r, s2, d,
-             static_cast<float*>(in_sa), static_cast<float*>(in_s2a), static_cast<float*>(sa_pi),
-             r_out, d_out, static_cast<float*>(in_s), lsp);
+    launch_pack_t<float>(blocks, narrow, st, n, B, ds, da, lsa, s, a, r, s2, d, in_sa, in_s2a,
+                         sa_pi, r_out, d_out, in_s, lsp);
 }
 
 // y = r + gamma*(1-done)*min(Q1', Q2')   (algos.hpp:268-281)
