@@ -443,9 +443,20 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     });
     if (!device_ptrs) CUDA_CHECK(cudaEventRecord(ev_free[i & 1u], stream));
     step(B, d_mask);
-    if (losses_out)  // this step's critic1 / critic2 / policy losses -> host (async)
-      CUDA_CHECK(cudaMemcpyAsync(losses_out + static_cast<size_t>(i) * 3 * n, losses.p,
-                                 3 * n * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    if (losses_out) {
+      // this step's critic1 / critic2 / policy losses -> a device history slot; the history
+      // goes to the host in one copy per kLossHist steps (async, in stream order)
+      const size_t row = static_cast<size_t>(3) * n;
+      loss_hist.alloc(kLossHist * row);
+      CUDA_CHECK(cudaMemcpyAsync(loss_hist.p + (i % kLossHist) * row, losses.p,
+                                 row * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+      if (i % kLossHist == kLossHist - 1 || i + 1 == k) {
+        const uint32_t first = i - i % kLossHist;
+        CUDA_CHECK(cudaMemcpyAsync(losses_out + first * row, loss_hist.p,
+                                   (i - first + 1) * row * sizeof(double),
+                                   cudaMemcpyDeviceToHost, stream));
+      }
+    }
   }
   host_mask = nullptr;
   if (losses_out) sync();

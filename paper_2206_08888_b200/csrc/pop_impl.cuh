@@ -164,6 +164,10 @@ struct Pop {
   DBuf<uint64_t> steps, streams, key_a, key_b;
   DBuf<int> fire;
   DBuf<double> delay_acc, losses;
+  // per-step losses of an update_batches call, kept on the device and read back in blocks of
+  // kLossHist steps (one D2H per block instead of one per step)
+  static constexpr uint32_t kLossHist = 64;
+  DBuf<double> loss_hist;
   DBuf<float> log_alpha, alpha_m, alpha_v;
   DBuf<uint8_t> mask_buf;
 

@@ -162,11 +162,12 @@ def test_launch_count_independent_of_population(pb, ora):
     assert counts[0] == counts[1] == counts[2]
 
 
-@pytest.mark.parametrize("precision", ["ffma32", "bf16"])
-def test_update_k_steps_with_losses_matches_single_steps(pb, ora, precision):
+@pytest.mark.parametrize("precision,K", [("ffma32", 5), ("bf16", 5), ("bf16", 70)])
+def test_update_k_steps_with_losses_matches_single_steps(pb, ora, precision, K):
     """pbrl_update_batches_losses (k host batches, overlapped H2D staging, every step's losses)
-    leaves the same state and reports the same per-step losses as k single-step calls."""
-    n, B, K = 3, 128, 5
+    leaves the same state and reports the same per-step losses as k single-step calls (K = 70:
+    the device-side loss history is read back in blocks of 64 steps)."""
+    n, B = 3, 128
     raw = ora.synthetic_batches(K, n, B, 17, 6, 13)
     hy = pb.Td3Hyper.defaults(n)
     a = pb.make_td3_state(n, 17, 6, [64, 64] if precision == "ffma32" else [256, 256], 1.0, 13,
