@@ -620,14 +620,17 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
       a.dbx[grp * a.dbx_gs + col] = t;
     }
   }
-  if (a.top && a.loss && blockIdx.x == 0 && threadIdx.x == 0) {  // row order, double
+  if (a.top && a.loss && blockIdx.x == 0 && threadIdx.x < 32) {
+    // fast modes only (this kernel never runs in the bit-exact mode): warp tree in double
+    // instead of one thread walking the rows
     double s = 0.0;
-    if (a.top == 3) {
-      for (int b = 0; b < B; ++b) s -= static_cast<double>(Ls[b]);
-    } else {
-      for (int b = 0; b < B; ++b) s += static_cast<double>(Ls[b]) * static_cast<double>(Ls[b]);
+    for (int b = threadIdx.x; b < B; b += 32) {
+      const double l = static_cast<double>(Ls[b]);
+      s += a.top == 3 ? -l : l * l;
     }
-    a.loss[grp] = s / static_cast<double>(B);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (threadIdx.x == 0) a.loss[grp] = s / static_cast<double>(B);
   }
   if (!a.dW) return;
   float* dW = a.dW + grp * a.dw_gs;
