@@ -19,3 +19,9 @@ PBRL_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source 
   > gpurun_out/ncu_full_bf16.log 2>&1
 tail -2 gpurun_out/ncu_full_bf16.log
 ls gpurun_out
+# summarise on the box (the .ncu-rep files would exceed the 64 MiB copy-back limit)
+python profiles/summarize.py r1_final_bf16 gpurun_out/launches_bf16.csv gpurun_out/full_bf16.ncu-rep > /dev/null 2>&1
+python profiles/summarize.py r1_final_tf32 gpurun_out/launches_tf32.csv > /dev/null 2>&1
+mkdir -p gpurun_out/profiles_box
+cp profiles/r1_final_bf16_*.md profiles/r1_final_tf32_*.md profiles/traffic_bf16_D.json gpurun_out/profiles_box/
+rm -f gpurun_out/*.ncu-rep
