@@ -950,13 +950,14 @@ __device__ __forceinline__ void e2_bar_sync() {  // the E2 warps only
   asm volatile("bar.sync 6, %0;" ::"n"(kEpiThreads) : "memory");
 }
 
-// NO = 1, 6: exact output width; NO = 12: any width <= 12 (runtime g.nout)
+// NO = 1, 6, 12: exact output width; NO = 16: any width <= 16 (runtime g.nout)
 template <int NO>
 __global__ void __launch_bounds__(kF2Threads, 1)
     k_mlp_fwd2(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmH1,
                const Fwd2Args g) {
-  constexpr bool kRt = NO == 12;
+  constexpr bool kRt = NO == 16;
+  constexpr bool kEarly = NO <= 6;  // output bias / noise loaded before E2 (register budget)
   constexpr int R = f2_ring<NO>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1214,7 +1215,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       const float* eg =
           noisy ? g.noise_eps + grp * g.ne_gs + static_cast<long long>(row) * g.ne_rs : nullptr;
       float ob[NA], ep[NA];
-      if (!kRt && hf == 0) {  // fixed widths: output bias and noise in flight during E2
+      if (kEarly && hf == 0) {  // narrow outputs: output bias and noise in flight during E2
 #pragma unroll
         for (int o = 0; o < NA; ++o) {
           ob[o] = __ldg(obg + o);
@@ -1306,7 +1307,7 @@ __global__ void __launch_bounds__(kF2Threads, 1)
       }
       quad_bar_sync(q);
       if (hf == 0 && row < g.M) {
-        if (kRt) {
+        if (!kEarly) {
 #pragma unroll
           for (int o = 0; o < NA; ++o) {
             if (o >= nout) break;
@@ -1502,7 +1503,9 @@ int pick_bn(const TcArgs& g, bool b_mn) {
   for (int bn : {64, 128, 256}) {
     const long long tiles = static_cast<long long>(g.groups) * m_tiles * ((N + bn - 1) / bn);
     const double waves = static_cast<double>((tiles + sms - 1) / sms);
-    const double cost = waves * (std::min(bn, ((N + 31) / 32) * 32) + 48);
+    // per-tile cost: its columns plus a fixed ~160-column equivalent (pipeline fill, epilogue
+    // setup; measured: every config-D product is faster at 256 than at 128 with 1.7x the waves)
+    const double cost = waves * (std::min(bn, ((N + 31) / 32) * 32) + 160);
     if (cost < best_cost - 1e-9) {
       best_cost = cost;
       best = bn;
@@ -1594,7 +1597,7 @@ void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn
 bool mlp_fwd2_ok(const Fwd2Args& a) {
   auto al16 = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
   return a.in >= 1 && a.in <= 64 && a.H1 % 128 == 0 && a.H1 <= 256 && a.H2 % 32 == 0 &&
-         a.H2 >= 32 && a.H2 <= 256 && a.nout >= 1 && a.nout <= 12 && a.x_ld % 8 == 0 &&
+         a.H2 >= 32 && a.H2 <= 256 && a.nout >= 1 && a.nout <= 16 && a.x_ld % 8 == 0 &&
          a.x_gs % 8 == 0 && a.w_gs % 8 == 0 && a.p_gs % 4 == 0 && al16(a.X) && al16(a.W1) &&
          al16(a.W2) && al16(a.b1) && al16(a.b2) && al16(a.ow) &&
          (!a.H1g || (al16(a.H1g) && a.h1_ld % 8 == 0 && a.h1_gs % 8 == 0)) &&
@@ -1636,7 +1639,8 @@ void launch_mlp_fwd2(const Fwd2Args& a0, cudaStream_t s) {
   switch (a.nout) {
     case 1: launch_fwd2_tpl<1>(a, s); return;
     case 6: launch_fwd2_tpl<6>(a, s); return;
-    default: launch_fwd2_tpl<12>(a, s); return;  // any width <= 12
+    case 12: launch_fwd2_tpl<12>(a, s); return;
+    default: launch_fwd2_tpl<16>(a, s); return;  // any width <= 16
   }
 }
 
