@@ -458,9 +458,9 @@ bool Pop::mlp_forward2(const NetShape& sh, const float* W, int groups, int B, Ma
     a.H2g = const_cast<float*>(h2.p);
     a.h2_gs = h2.gs;
     a.h2_ld = h2.ld;
-    a.m2 = h2.mask;
-    a.m2_gs = h2.mgs;
-    a.m2_ld = h2.mld;
+    // no mask bits for h2: with two hidden layers the backward reads h2's ReLU' from the values
+    // (output-layer backward) and only h1's bits (the layer-1 dX epilogues)
+    a.m2 = nullptr;
   }
   a.active = active;
   if (noise) {
