@@ -458,9 +458,14 @@ bool Pop::mlp_forward2(const NetShape& sh, const float* W, int groups, int B, Ma
     a.H2g = const_cast<float*>(h2.p);
     a.h2_gs = h2.gs;
     a.h2_ld = h2.ld;
-    // no mask bits for h2: with two hidden layers the backward reads h2's ReLU' from the values
-    // (output-layer backward) and only h1's bits (the layer-1 dX epilogues)
-    a.m2 = nullptr;
+    // h2's mask bits only when the output layer's backward is a tensor-core dX product (the
+    // output-layer backward kernel, mlp_backward's condition, reads ReLU' from the values;
+    // the layer-1 dX epilogues read h1's bits)
+    const bool out_bwd_kernel =
+        sh.dims[3] <= 16 && static_cast<long long>(B) * sh.dims[3] <= 32768;
+    a.m2 = out_bwd_kernel ? nullptr : h2.mask;
+    a.m2_gs = h2.mgs;
+    a.m2_ld = h2.mld;
   }
   a.active = active;
   if (noise) {

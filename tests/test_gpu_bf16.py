@@ -138,3 +138,20 @@ np.savez(sys.argv[1], **{net: st.params(net) for net in TD3_NETS})
         out[flag] = np.load(path)
     for net in TD3_NETS:
         assert np.array_equal(out["0"][net], out["1"][net]), net
+
+
+
+def test_bf16_large_batch_output_layer_is_a_loud_config_error(pb, ora):
+    """Known BF16-mode boundary: with B * n_out > 32768 (policy: 8192 x 6)
+    the output layer's backward would be a K = n_out < 8 dX product, which has no tensor-core
+    shape and no bf16 CUDA-core fallback -- the update raises ConfigError instead of silently
+    computing something else (TF32 / FFMA32 modes run it)."""
+    import numpy as np
+    from helpers import to_batch
+    n, B = 2, 8192
+    st = pb.make_td3_state(n, 17, 6, [128, 64], 1.0, 9, precision="bf16")
+    raw = ora.synthetic_batches(1, n, B, 17, 6, 9)
+    hy = pb.Td3Hyper.defaults(n)
+    hy.policy_delay_ratio = [1.0] * n
+    with pytest.raises(pb.ConfigError):
+        pb.td3_update_step(st, to_batch(pb, raw, 0), hy)
