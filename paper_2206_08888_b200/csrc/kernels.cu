@@ -1090,9 +1090,9 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
     adam_one(a, pv.y, mv.y, vv.y, gv.y);
     adam_one(a, pv.z, mv.z, vv.z, gv.z);
     adam_one(a, pv.w, mv.w, vv.w, gv.w);
-    p4[k] = pv;
-    m4[k] = mv;
-    v4[k] = vv;
+    __stcs(&p4[k], pv);  // streaming: the fp32 optimizer state is touched once per step; the
+    __stcs(&m4[k], mv);  // bf16 operand copies the next step reads stay in L2 instead
+    __stcs(&v4[k], vv);
     if (p16) {  // BF16 mode: the tensor-core copy of the fresh parameters
       __nv_bfloat162* d2 = reinterpret_cast<__nv_bfloat162*>(p16 + base) + 2 * k;
       d2[0] = __floats2bfloat162_rn(pv.x, pv.y);
@@ -1103,7 +1103,7 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
       tv.y = a.ta * pv.y + a.tb * tv.y;
       tv.z = a.ta * pv.z + a.tb * tv.z;
       tv.w = a.ta * pv.w + a.tb * tv.w;
-      t4[k] = tv;
+      __stcs(&t4[k], tv);
       if (t16) {
         __nv_bfloat162* d2 = reinterpret_cast<__nv_bfloat162*>(t16 + base) + 2 * k;
         d2[0] = __floats2bfloat162_rn(tv.x, tv.y);
@@ -1119,15 +1119,16 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
     const size_t k1q = kq + str;
     const size_t k1 = k1q < s0 ? k1q : k1q + sk;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 p0 = p4[k0], m0 = m4[k0], v0 = v4[k0], g0 = g4[k0];
-    const float4 t0 = a.polyak ? t4[k0] : z;
+    const float4 p0 = __ldcs(&p4[k0]), m0 = __ldcs(&m4[k0]), v0 = __ldcs(&v4[k0]),
+                 g0 = __ldcs(&g4[k0]);
+    const float4 t0 = a.polyak ? __ldcs(&t4[k0]) : z;
     float4 p1 = z, m1 = z, v1 = z, g1 = z, t1 = z;
     if (two) {
-      p1 = p4[k1];
-      m1 = m4[k1];
-      v1 = v4[k1];
-      g1 = g4[k1];
-      if (a.polyak) t1 = t4[k1];
+      p1 = __ldcs(&p4[k1]);
+      m1 = __ldcs(&m4[k1]);
+      v1 = __ldcs(&v4[k1]);
+      g1 = __ldcs(&g4[k1]);
+      if (a.polyak) t1 = __ldcs(&t4[k1]);
     }
     update(k0, p0, m0, v0, g0, t0);
     if (two) update(k1, p1, m1, v1, g1, t1);
