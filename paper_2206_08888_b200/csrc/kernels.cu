@@ -916,17 +916,17 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float*
     const int c = static_cast<int>(e - row * dsa);
     const long long o = static_cast<long long>(row) * lsa + c;
     if (c < ds) {
-      const float sv = s[static_cast<long long>(row) * ds + c];
+      const float sv = __ldcs(s + static_cast<long long>(row) * ds + c);  // read once
       act_st(in_sa, o, sv);
       act_st(sa_pi, o, sv);
-      act_st(in_s2a, o, s2[static_cast<long long>(row) * ds + c]);
+      act_st(in_s2a, o, __ldcs(s2 + static_cast<long long>(row) * ds + c));
       if (in_s) act_st(in_s, static_cast<long long>(row) * lsp + c, sv);
     } else {
-      act_st(in_sa, o, a[static_cast<long long>(row) * da + (c - ds)]);
+      act_st(in_sa, o, __ldcs(a + static_cast<long long>(row) * da + (c - ds)));
     }
     if (c == 0) {
-      r_out[row] = r[row];
-      d_out[row] = d[row];
+      r_out[row] = __ldcs(r + row);
+      d_out[row] = __ldcs(d + row);
     }
   }
 }
