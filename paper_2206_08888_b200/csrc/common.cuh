@@ -54,6 +54,14 @@ enum RngUse : uint64_t {
 // This is an independent implementation of that published algorithm; it agrees with the host
 // libm on all 2^32 inputs (checked exhaustively on the CPU, and on the device by
 // tests/test_gpu_numerics.py).
+//
+// Attribution: the expm1f / tanhf / expf / log1pf algorithms and their polynomial constants
+// below follow fdlibm as distributed in glibc (sysdeps/ieee754/flt-32), which carries this
+// notice:
+//   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//   Developed at SunPro, a Sun Microsystems, Inc. business.
+//   Permission to use, copy, modify, and distribute this software is freely granted,
+//   provided that this notice is preserved.
 __device__ __forceinline__ uint32_t fbits(float x) { return __float_as_uint(x); }
 __device__ __forceinline__ float bitsf(uint32_t u) { return __uint_as_float(u); }
 

@@ -2,6 +2,8 @@
 // epilogues, and every elementwise / reduction step of TD3 and SAC.  All kernels are grouped
 // over population members (grid.z or grid.y = member or member x critic), so the number of
 // launches per update step does not depend on the population size (test_bench.cpp:40-53).
+#include <math_constants.h>
+
 #include "pop.cuh"
 
 namespace pbrl {
@@ -855,8 +857,7 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
                                  const uint8_t* mask, int* fire, int64_t* t_pol, int64_t* t_c1,
                                  int64_t* t_c2, uint64_t* steps, const uint64_t* streams,
                                  uint64_t seed, uint64_t* noise_key, double* policy_loss,
-                                 cudaGraphConditionalHandle any_fire,
-                                 cudaGraphConditionalHandle any_fire2, int set_cond) {
+                                 cudaGraphConditionalHandle any_fire, int set_cond) {
   PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   int f = 0;
@@ -881,21 +882,16 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
   // graph mode: the policy half of the step is an IF node on "some member fires"
   // (default 0 at every graph launch; any block with a firing member sets it)
   const int any = __syncthreads_or(f);
-  if (set_cond && any && threadIdx.x == 0) {
-    cudaGraphSetConditional(any_fire, 1u);
-    if (set_cond > 1) cudaGraphSetConditional(any_fire2, 1u);
-  }
+  if (set_cond && any && threadIdx.x == 0) cudaGraphSetConditional(any_fire, 1u);
 }
 
 void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const uint8_t* mask,
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
-                           cudaGraphConditionalHandle any_fire,
-                           cudaGraphConditionalHandle any_fire2, int set_cond, cudaStream_t s) {
+                           cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s) {
   launch_k(k_td3_step_begin, (n + 127) / 128, 128, 0, s, n, delay_acc, ratio, mask, fire, t_pol,
-           t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, any_fire2,
-           set_cond);
+           t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, set_cond);
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts
@@ -1058,8 +1054,7 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
                                               const float* tau_a, const float* tau_b,
                                               const int* polyak_gate,
                                               __nv_bfloat16* __restrict__ p16,
-                                              __nv_bfloat16* __restrict__ t16, size_t skip0,
-                                              size_t skip1) {
+                                              __nv_bfloat16* __restrict__ t16) {
   PDL_ENTRY();
   const int grp = blockIdx.y;
   const int m = grp % n;
@@ -1081,8 +1076,6 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
   float4* v4 = reinterpret_cast<float4*>(vo + base);
   const float4* g4 = reinterpret_cast<const float4*>(g + base);
   float4* t4 = a.polyak ? reinterpret_cast<float4*>(tgt + base) : nullptr;
-  // [skip0, skip1) (float4-aligned) was updated by the dW epilogue of its layer (EPI_ADAM)
-  const size_t s0 = skip0 / 4, sk = (skip1 - skip0) / 4;
   // two float4 slots per thread per trip, both slots' loads issued before either is updated
   // (more bytes in flight per thread for the HBM-bound stream)
   auto update = [&](size_t k, float4 pv, float4 mv, float4 vv, float4 gv, float4 tv) {
@@ -1111,13 +1104,11 @@ __global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
       }
     }
   };
-  const size_t cnt = P4 - sk, str = static_cast<size_t>(gridDim.x) * blockDim.x;
-  for (size_t kq = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; kq < cnt;
-       kq += 2 * str) {
-    const size_t k0 = kq < s0 ? kq : kq + sk;
-    const bool two = kq + str < cnt;
-    const size_t k1q = kq + str;
-    const size_t k1 = k1q < s0 ? k1q : k1q + sk;
+  const size_t str = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t k0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; k0 < P4;
+       k0 += 2 * str) {
+    const size_t k1 = k0 + str;
+    const bool two = k1 < P4;
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 p0 = __ldcs(&p4[k0]), m0 = __ldcs(&m4[k0]), v0 = __ldcs(&v4[k0]),
                  g0 = __ldcs(&g4[k0]);
@@ -1154,14 +1145,13 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
                  const float* g, const int64_t* t, const float* corr1, const float* corr2,
                  const float* lr, const int* active, float* tgt, const float* tau_a,
                  const float* tau_b, const int* polyak_gate, __nv_bfloat16* p16,
-                 __nv_bfloat16* t16, cudaStream_t s, size_t skip0, size_t skip1) {
+                 __nv_bfloat16* t16, cudaStream_t s) {
   const int threads = 256;
-  if (skip0 % 4 || skip1 % 4 || skip1 < skip0 || skip1 > P / 4 * 4) skip0 = skip1 = 0;
-  int bx = static_cast<int>((P / 4 - (skip1 - skip0) / 4 + 2 * threads - 1) / (2 * threads));
+  int bx = static_cast<int>((P / 4 + 2 * threads - 1) / (2 * threads));
   bx = bx < 1 ? 1 : bx;
   dim3 grid(bx, groups);
   launch_k(k_adam, grid, threads, 0, s, n, P, stride, p, m, v, g, t, corr1, corr2, lr, active, tgt,
-           tau_a, tau_b, polyak_gate, p16, t16, skip0, skip1);
+           tau_a, tau_b, polyak_gate, p16, t16);
 }
 
 __global__ void k_to_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
@@ -1695,12 +1685,15 @@ void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const f
 __global__ void k_pbt_plan(int n, const double* fitness, int cut, uint64_t key, uint64_t next,
                            uint64_t* order, uint64_t* replaced, uint64_t* donors) {
   PDL_ENTRY();
+  // stable descending rank = #(better) + #(equal with a lower index).  NaN fitness (a diverged
+  // member) ranks as -inf, so the comparison is a total order and `order` a permutation.
+  auto rank_key = [](double f) { return f != f ? -CUDART_INF : f; };
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double fi = fitness[i];
+    const double fi = rank_key(fitness[i]);
     int pos = 0;
     for (int j = 0; j < n; ++j) {
-      const double fj = fitness[j];
-      pos += (fj > fi) || (j < i && !(fj > fi) && !(fi > fj));
+      const double fj = rank_key(fitness[j]);
+      pos += (fj > fi) || (j < i && fj == fi);
     }
     order[pos] = static_cast<uint64_t>(i);
   }

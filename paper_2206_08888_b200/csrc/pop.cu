@@ -69,10 +69,6 @@ Pop::Pop(const pbrl_pop_desc& d) {
   tc_trace_init();
   use_graphs = std::getenv("PBRL_NO_GRAPH") == nullptr;  // eager replay (ncu kernel profiles)
   fwd2_off = std::getenv("PBRL_NO_FWD2") != nullptr;
-  // Adam inside the dW epilogue (EPI_ADAM) is opt-in: bit-identical, but the 8 epilogue warps of
-  // a persistent 1-CTA/SM GEMM cannot keep enough loads in flight for the HBM-bound optimizer
-  // traffic (measured 145k vs 229k agent-updates/s on B200); PBRL_FUSED_ADAM=1 enables it
-  fused_adam_off = std::getenv("PBRL_FUSED_ADAM") == nullptr;
 
   std::vector<size_t> pd{static_cast<size_t>(ds)};
   pd.insert(pd.end(), hidden.begin(), hidden.end());
@@ -174,12 +170,6 @@ Pop::~Pop() {
     if (side2) cudaStreamDestroy(side2);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
-    if (side3) cudaStreamDestroy(side3);
-    if (side4) cudaStreamDestroy(side4);
-    if (ev_c2) cudaEventDestroy(ev_c2);
-    if (ev_c2done) cudaEventDestroy(ev_c2done);
-    if (ev_pfork) cudaEventDestroy(ev_pfork);
-    if (ev_pjoin) cudaEventDestroy(ev_pjoin);
     if (cstream) cudaStreamDestroy(cstream);
     for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1]})
       if (e) cudaEventDestroy(e);

@@ -111,7 +111,6 @@ enum Epi {
   EPI_BIAS_TANH_NOISE = 4,  // as EPI_BIAS_TANH, then TD3 target smoothing noise on C
   EPI_RELU_MASK = 5,    // C = aux(i,j) > 0 ? acc : 0       (activation_backward, relu)
   EPI_TANH_GRAD = 6,    // g = acc * scale; C = g * (1 - aux^2)   (tanh backward, aux = t)
-  EPI_ADAM = 7,         // dW product: Adam (+ Polyak) on the parameters with g = acc (TcArgs)
 };
 
 struct Operand {
@@ -146,8 +145,7 @@ struct GemmArgs {
 
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t s);
 
-// adam_step_inplace per element (pop_tensor.hpp:345-363): shared by k_adam and the EPI_ADAM
-// epilogue of the tensor-core dW product, so both produce the same bits
+// adam_step_inplace per element (pop_tensor.hpp:345-363)
 struct AdamScalars {
   float b1, b2, c1, c2, step, epsv, ta, tb;
   bool polyak;
@@ -207,8 +205,7 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
-                           cudaGraphConditionalHandle any_fire,
-                           cudaGraphConditionalHandle any_fire2, int set_cond, cudaStream_t s);
+                           cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s);
 // in_sa / in_s2a / sa_pi are activation buffers: fp32, or bf16 when act16
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, void* in_sa,
@@ -227,7 +224,7 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
                  const float* g, const int64_t* t, const float* corr1, const float* corr2,
                  const float* lr, const int* active, float* tgt, const float* tau_a,
                  const float* tau_b, const int* polyak_gate, __nv_bfloat16* p16,
-                 __nv_bfloat16* t16, cudaStream_t s, size_t skip0 = 0, size_t skip1 = 0);
+                 __nv_bfloat16* t16, cudaStream_t s);
 // bf16 copy of an fp32 arena (the BF16 mode's tensor-core weight operands)
 void launch_to_bf16(const float* src, __nv_bfloat16* dst, size_t count, cudaStream_t s);
 void launch_fill(float* p, size_t count, float v, cudaStream_t s);

@@ -119,17 +119,6 @@ struct Mat {
 
 inline int pad4(int x) { return (x + 3) / 4 * 4; }
 
-// Adam of one network arena applied inside the tensor-core dW product of its largest layer
-// (EPI_ADAM); the separate k_adam launch then skips that parameter block.
-struct AdamFuse {
-  float *p = nullptr, *m = nullptr, *v = nullptr, *tgt = nullptr;
-  __nv_bfloat16 *p16 = nullptr, *t16 = nullptr;
-  const int64_t* t = nullptr;
-  const float *lr = nullptr, *ta = nullptr, *tb = nullptr;
-  const int* gate = nullptr;
-  size_t skip0 = 0, skip1 = 0;  // set when a layer was fused: the block k_adam must skip
-};
-
 struct StepGraph {
   int B = 0;
   bool masked = false;
@@ -203,15 +192,8 @@ struct Pop {
   // next tcgen05 launch must not read its weight operand before the PDL wait
   bool last_wrote_weights = true;
 
-  // diagnostics only (PBRL_SKIP_CLASSES=bitmask of ProfClass): launches of those classes are
-  // dropped, so the step time without them shows their marginal cost in the replayed graph
-  static int skip_classes() {
-    static const int m = std::getenv("PBRL_SKIP_CLASSES") ? std::atoi(std::getenv("PBRL_SKIP_CLASSES")) : 0;
-    return m;
-  }
   template <typename F>
   void timed(int cls, double flops, double bytes, int gated, F&& f) {
-    if (skip_classes() & (1 << cls)) return;
     cudaEvent_t a = nullptr;
     prof_begin(&a);
     f();
@@ -267,8 +249,8 @@ struct Pop {
   void gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, Mat G, Mat aux,
                float* DX, long long dx_gs, long long dx_ld, int epi, int col0, int ncols,
                const int* active, float scale);
-  bool gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
-               const int* active, bool bias_done = false, AdamFuse* af = nullptr);
+  void gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
+               const int* active, bool bias_done = false);
   void mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
                    std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                    int last_epi, const int* active = nullptr, float* C2 = nullptr,
@@ -279,14 +261,13 @@ struct Pop {
                     int last_epi, const int* active, float* C2, long long c2_gs, long long c2_ld,
                     bool noise, bool keep_hidden, bool out_act);
   bool fwd2_off = false;  // PBRL_NO_FWD2=1: per-layer launches instead (diagnostics)
-  bool fused_adam_off = true;  // PBRL_FUSED_ADAM=1: Adam in the dW epilogue (see pop.cu)
   bool gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, int B, Mat X, Mat H,
                       bool keep_hidden, float* Y, long long y_gs, long long y_ld, int out_epi,
                       const int* active, float* C2, long long c2_gs, long long c2_ld, bool noise,
                       bool out_act);
   void mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
                     Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
-                    const int* active, const OutBwdArgs* top = nullptr, AdamFuse* af = nullptr);
+                    const int* active, const OutBwdArgs* top = nullptr);
   void critic_dx_to_action(int groups, int B, Mat G, std::vector<DBuf<float>>& hs,
                            std::vector<DBuf<float>>& dhs, float* out, long long out_ld, int epi,
                            Mat aux, float scale, const int* active,
@@ -294,14 +275,11 @@ struct Pop {
   void critic_forward(int B);
   bool gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long long out_ld, int epi,
                          Mat aux, float scale, const int* active);
-  void critic_update(int B, const int* polyak_gate, bool forward_done = false,
-                     bool split_c2 = false);
-  cudaStream_t side4 = nullptr;  // critic 2's Adam branch
-  cudaEvent_t ev_c2 = nullptr, ev_c2done = nullptr;
+  void critic_update(int B, const int* polyak_gate, bool forward_done = false);
   cudaStream_t side2 = nullptr;  // parallel graph branch (critic forward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void td3_step(int B, const uint8_t* d_mask);
-  void td3_policy_half(int B, bool forward_done);
+  void td3_policy_half(int B);
   void td3_policy_forward(int B);
   template <typename F>
   void capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body);
@@ -311,8 +289,6 @@ struct Pop {
   std::vector<double> delay_host;
   const uint8_t* host_mask = nullptr;
   bool host_fires();
-  cudaStream_t side3 = nullptr;
-  cudaEvent_t ev_pfork = nullptr, ev_pjoin = nullptr;
   void sac_step(int B);
   void step(int B, const uint8_t* d_mask);
   void update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,

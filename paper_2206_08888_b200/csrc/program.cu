@@ -197,8 +197,8 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
 }
 
 // dW_l and db_l into the gradient arena rows: dW = X^T G, db = column sums of G
-bool Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
-                  const int* active, bool bias_done, AdamFuse* af) {
+void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
+                  const int* active, bool bias_done) {
   const int in = sh.dims[l], out = sh.dims[l + 1];
   const double flops = 2.0 * B * in * out * groups;
   // algorithmic bytes: X (once per member when shared), G, dW
@@ -222,55 +222,23 @@ bool Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
     a.M = mrows;
     a.N = out;
     a.K = B;
-    // Adam fused into this product: the layer's parameters are updated in place from the fp32
-    // accumulator (identical bits to k_adam on a stored gradient); the gradient is not stored
-    const size_t w0 = sh.woff[l], w1 = sh.woff[l] + static_cast<size_t>(in) * out;
-    const bool fuse_adam = af && mrows == in && w0 % 4 == 0 && w1 % 4 == 0 && !fused_adam_off;
-    if (fuse_adam) {
-      a.epi = EPI_ADAM;
-      a.ad_p = af->p + w0;
-      a.ad_m = af->m + w0;
-      a.ad_v = af->v + w0;
-      a.ad_tgt = af->tgt ? af->tgt + w0 : nullptr;
-      a.ad_p16 = af->p16 ? af->p16 + w0 : nullptr;
-      a.ad_t16 = af->t16 ? af->t16 + w0 : nullptr;
-      a.ad_gs = static_cast<long long>(sh.stride);
-      a.ad_t = af->t;
-      a.ad_c1 = corr1.p;
-      a.ad_c2 = corr2.p;
-      a.ad_lr = af->lr;
-      a.ad_ta = af->ta;
-      a.ad_tb = af->tb;
-      a.ad_gate = af->gate;
-      af->skip0 = w0;
-      af->skip1 = w1;
-    }
     a.groups = groups;
     a.n_members = n;
     a.a_by_member = X.by_member;
-    if (!fuse_adam) a.epi = EPI_STORE;
-    a.C = fuse_adam ? nullptr : Gr + sh.woff[l];
+    a.epi = EPI_STORE;
+    a.C = Gr + sh.woff[l];
     a.c_gs = static_cast<long long>(sh.stride);
     a.c_rs = out;
     a.active = active;
-    const double abytes = fuse_adam ? (static_cast<double>(in) * out * groups *
-                                       (24.0 + (af->p16 ? 2.0 : 0.0)) -
-                                       4.0 * groups * in * out)
-                                    : 0.0;
-    timed(PC_GEMM_DW, flops, bytes + abytes, active != nullptr,
+    timed(PC_GEMM_DW, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bg, true, true, a, stream); });
-    if (fuse_adam && af->tgt) {  // Polyak target traffic (+ its bf16 copy), gated like k_adam's
-      const double tb = static_cast<double>(in) * out * groups * (af->t16 ? 10.0 : 8.0);
-      if (af->gate) prof_add_gated_bytes(tb);
-      else if (prof_on && !prof.empty()) prof.back().bytes += tb;
-    }
     // bias gradient: per-column sums of G in row order (pop_add_bias_backward, :236-250),
     // unless the kernel that produced G already wrote them
     if (!bias_done) timed(PC_ELEM, 0.0, 4.0 * B * out * groups, active != nullptr, [&] {
       launch_colsum(groups, n, B, out, G.p, G.gs, G.ld, Gr + sh.boff[l],
                     static_cast<long long>(sh.stride), active, act16() ? 1 : 0, stream);
     });
-    return fuse_adam;
+    return;
   }
   if (act16()) PBRL_THROW(PBRL_E_CONFIG, "bf16 mode: dW product without a tensor-core shape");
   GemmArgs g;
@@ -292,7 +260,6 @@ bool Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
     if (out <= 16) launch_dw_skinny(g, stream);
     else launch_gemm_simt(g, stream);
   });
-  return false;
 }
 
 // ------------------------------------------------------------------ profiling
@@ -572,8 +539,7 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
 // backward of `sh` from the top cotangent G: dW for every layer, dX for layers > 0
 void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups, int B, Mat G,
                        Mat x0, std::vector<DBuf<float>>& hs, std::vector<DBuf<float>>& dhs,
-                       const int* active, const OutBwdArgs* top,
-                       AdamFuse* af) {
+                       const int* active, const OutBwdArgs* top) {
   const int L = sh.depth;
   bool bias_done = false;  // the bias gradient of layer l was produced with its cotangent
   for (int l = L - 1; l >= 0; --l) {
@@ -634,12 +600,10 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       continue;
     }
     if (l > 0) {
-      // dX before dW: a fused optimiser in the dW epilogue must not race the dX read of W_l
       const Mat dh = hid(dhs, l - 1, B, sh, 0);
       gemm_dx(sh, W, l, groups, B, G, x, const_cast<float*>(dh.p), dh.gs, dh.ld, EPI_RELU_MASK,
               0, sh.dims[l], active, 1.0f);
-      gemm_dw(sh, Gr, l, groups, B, x, G, active, bias_done,
-              (af && l == 1 && sh.depth == 3) ? af : nullptr);
+      gemm_dw(sh, Gr, l, groups, B, x, G, active, bias_done);
       G = dh;
     } else {
       gemm_dw(sh, Gr, l, groups, B, x, G, active, bias_done);
@@ -764,7 +728,7 @@ void Pop::critic_forward(int B) {
   mlp_forward(cri, cri_p.p, 2 * n, B, x0, S.ch, S.q.p, B, 1, EPI_BIAS);
 }
 
-void Pop::critic_update(int B, const int* polyak_gate, bool forward_done, bool split_c2) {
+void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
   const int n2 = 2 * n;
   Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
   if (use_tc() && lsa > ds + da) x0.ones_col = ds + da;  // see Pop::ensure_ones
@@ -786,50 +750,15 @@ void Pop::critic_update(int B, const int* polyak_gate, bool forward_done, bool s
           [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
   }
   const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
-  AdamFuse af;
-  af.p = cri_p.p;
-  af.m = cri_m.p;
-  af.v = cri_v.p;
-  af.tgt = cri_t.p;
-  af.p16 = cri_p16.p;
-  af.t16 = cri_t16.p;
-  af.t = t_cri.p;
-  af.lr = clr;
-  af.ta = h_f5.p;
-  af.tb = h_f6.p;
-  af.gate = polyak_gate;
   mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr,
-               &top, use_tc() ? &af : nullptr);
+               &top);
   // 28 B/param Adam (+2 B/param bf16 operand copy in BF16 mode)
-  const double cP = static_cast<double>(cri.P - (af.skip1 - af.skip0));  // k_adam's share
-  if (split_c2) {
-    // TD3 graph mode: critic 2's Adam runs on a parallel branch (the policy half reads critic 1
-    // only, algos.hpp:318-338), so on fire steps it overlaps the policy-loss chain; joined at
-    // the end of the step
-    const size_t o = static_cast<size_t>(n) * cri.stride;
-    CUDA_CHECK(cudaEventRecord(ev_c2, stream));
-    CUDA_CHECK(cudaStreamWaitEvent(side4, ev_c2, 0));
-    std::swap(stream, side4);
-    timed(PC_ADAM, 0.0, cP * n * (act16() ? 30.0 : 28.0), 0, [&] {
-      launch_adam(n, n, cri.P, cri.stride, cri_p.p + o, cri_m.p + o, cri_v.p + o, cri_g.p + o,
-                  t_cri.p + n, corr1.p, corr2.p, clr, nullptr, cri_t.p + o, h_f5.p, h_f6.p,
-                  polyak_gate, cri_p16.p ? cri_p16.p + o : nullptr,
-                  cri_t16.p ? cri_t16.p + o : nullptr, stream, af.skip0, af.skip1);
-    });
-    std::swap(stream, side4);
-    CUDA_CHECK(cudaEventRecord(ev_c2done, side4));
-    timed(PC_ADAM, 0.0, cP * n * (act16() ? 30.0 : 28.0), 0, [&] {
-      launch_adam(n, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
-                  corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, cri_p16.p,
-                  cri_t16.p, stream, af.skip0, af.skip1);
-    });
-  } else {
-    timed(PC_ADAM, 0.0, cP * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
-      launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
-                  corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, cri_p16.p,
-                  cri_t16.p, stream, af.skip0, af.skip1);
-    });
-  }
+  const double cP = static_cast<double>(cri.P);
+  timed(PC_ADAM, 0.0, cP * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
+    launch_adam(n2, n, cri.P, cri.stride, cri_p.p, cri_m.p, cri_v.p, cri_g.p, t_cri.p, corr1.p,
+                corr2.p, clr, nullptr, cri_t.p, h_f5.p, h_f6.p, polyak_gate, cri_p16.p,
+                cri_t16.p, stream);
+  });
   // fused target Polyak: +8 B/param (read + write target), every member (SAC) or fired (TD3)
   const double pb = act16() ? 10.0 : 8.0;
   if (polyak_gate) prof_add_gated_bytes(pb * cP * n2);
@@ -881,29 +810,24 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   // k_td3_step_begin sets when any member fires (steps where no policy fires replay only the
   // critic half); eager mode runs it with every launch gated per member instead
   const bool fork = capturing && use_tc();
-  // PBRL_PFORK=1: policy forward on a parallel conditional branch (measured neutral on B200)
-  static const bool pfork = std::getenv("PBRL_PFORK") != nullptr;
-  cudaGraphConditionalHandle any_fire = 0, any_fire_fwd = 0;
+  cudaGraphConditionalHandle any_fire = 0;
   if (capturing) {
     cudaStreamCaptureStatus st;
     cudaGraph_t g = nullptr;
     CUDA_CHECK(cudaStreamGetCaptureInfo(stream, &st, nullptr, &g, nullptr, nullptr));
     CUDA_CHECK(cudaGraphConditionalHandleCreate(&any_fire, g, 0, cudaGraphCondAssignDefault));
-    if (fork && pfork)
-      CUDA_CHECK(
-          cudaGraphConditionalHandleCreate(&any_fire_fwd, g, 0, cudaGraphCondAssignDefault));
   }
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p, t_cri.p + n,
                           steps.p, streams.p, seed, key_a.p, losses.p + 2 * n, any_fire,
-                          any_fire_fwd, capturing ? (fork && pfork ? 2 : 1) : 0, stream);
+                          capturing ? 1 : 0, stream);
   });
   // graph mode: the online critics' forward on [s | a] does not depend on the target chain, so
   // it runs on a parallel graph branch (its tiles fill the target chain's partial waves)
   if (fork) {
     if (!side2) CUDA_CHECK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
     if (!ev_fork) {
-      for (cudaEvent_t* e : {&ev_fork, &ev_join, &ev_pfork, &ev_pjoin})
+      for (cudaEvent_t* e : {&ev_fork, &ev_join})
         CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
     CUDA_CHECK(cudaEventRecord(ev_fork, stream));
@@ -928,32 +852,10 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
     timed(PC_ELEM, 0.0, 0.0, 0,
           [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
   if (fork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
-  if (fork && pfork) {
-    // the policy forward pi(s) reads only the batch and the (not yet updated) policy: a second
-    // conditional branch overlaps it with the critic backward and Adam
-    CUDA_CHECK(cudaEventRecord(ev_pfork, stream));
-    CUDA_CHECK(cudaStreamWaitEvent(side2, ev_pfork, 0));
-    std::swap(stream, side2);
-    capture_if(any_fire_fwd, side3, [&] { td3_policy_forward(B); });
-    std::swap(stream, side2);
-    CUDA_CHECK(cudaEventRecord(ev_pjoin, side2));
-  }
   // twin critic update; target Polyak fused for members whose policy fires
-  // PBRL_C2FORK=1: critic 2's Adam on a parallel branch next to the policy half (measured
-  // neutral on B200: a 1-CTA/SM GEMM leaves room for one Adam block per SM)
-  const bool split = fork && std::getenv("PBRL_C2FORK") != nullptr;
-  if (split) {
-    if (!side4) CUDA_CHECK(cudaStreamCreateWithFlags(&side4, cudaStreamNonBlocking));
-    if (!ev_c2) {
-      CUDA_CHECK(cudaEventCreateWithFlags(&ev_c2, cudaEventDisableTiming));
-      CUDA_CHECK(cudaEventCreateWithFlags(&ev_c2done, cudaEventDisableTiming));
-    }
-  }
-  critic_update(B, fire.p, fork, split);
-  if (fork && pfork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_pjoin, 0));
-  if (capturing) capture_if(any_fire, side, [&] { td3_policy_half(B, fork && pfork); });
-  else td3_policy_half(B, false);
-  if (split) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_c2done, 0));  // join critic 2's Adam
+  critic_update(B, fire.p, fork);
+  if (capturing) capture_if(any_fire, side, [&] { td3_policy_half(B); });
+  else td3_policy_half(B);
 }
 
 void Pop::td3_policy_forward(int B) {
@@ -965,10 +867,10 @@ void Pop::td3_policy_forward(int B) {
 
 // td3_policy_loss_grads (:318-338) on the UPDATED critic1, policy Adam and the target Polyak,
 // every launch gated by the fire mask
-void Pop::td3_policy_half(int B, bool forward_done) {
+void Pop::td3_policy_half(int B) {
   const long long nbB = B;
   const Mat s = policy_input(B);
-  if (!forward_done) td3_policy_forward(B);
+  td3_policy_forward(B);
   mlp_forward(cri, cri_p.p, n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 0}, S.qh, S.qpi.p, nbB, 1,
               EPI_BIAS, fire.p);
   OutBwdArgs top;
@@ -984,26 +886,12 @@ void Pop::td3_policy_half(int B, bool forward_done) {
   const int lt = pad4(da);
   critic_dx_to_action(n, B, Mat{S.gq.p, nbB, 1, 0}, S.qh, S.qdh, S.gtop.p, lt, EPI_TANH_GRAD,
                       Mat{S.pt.p, nbB * da, da, 0}, pol.out_scale, fire.p, &top);
-  AdamFuse af;
-  af.p = pol_p.p;
-  af.m = pol_m.p;
-  af.v = pol_v.p;
-  af.tgt = pol_t.p;
-  af.p16 = pol_p16.p;
-  af.t16 = pol_t16.p;
-  af.t = t_pol.p;
-  af.lr = h_f1.p;
-  af.ta = h_f5.p;
-  af.tb = h_f6.p;
-  af.gate = nullptr;  // the policy half only updates fired members (tiles gated by fire)
   mlp_backward(pol, pol_p.p, pol_g.p, n, B, Mat{S.gtop.p, nbB * lt, lt, 0}, s, S.ph, S.pdh,
-               fire.p, nullptr, use_tc() ? &af : nullptr);
-  timed(PC_ADAM, 0.0,
-        static_cast<double>(pol.P - (af.skip1 - af.skip0)) * n * (act16() ? 40.0 : 36.0), 1,
-        [&] {
+               fire.p, nullptr);
+  timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * (act16() ? 40.0 : 36.0), 1, [&] {
     launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
                 corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, pol_p16.p, pol_t16.p,
-                stream, af.skip0, af.skip1);
+                stream);
   });
 }
 

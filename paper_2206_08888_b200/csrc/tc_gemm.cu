@@ -328,10 +328,7 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) {
-    TC_TRACE(1);
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // see PDL_ENTRY (pop.cuh)
-  }
+  if (threadIdx.x == 0) TC_TRACE(1);
 
   auto decode = [&](int t, int& grp, int& m0, int& n0) {
     const int nt = t % n_tiles;
@@ -367,6 +364,10 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
         }
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      // the successor may launch only once this grid's predecessor has completed (as in
+      // PDL_ENTRY): a successor that prefetches weights before its own wait then never overlaps
+      // a weight-writing kernel two launches back
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       int cnt = 0, pit = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int grp, m0, n0;
@@ -579,7 +580,6 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
 
       // one 32-column chunk of this thread's row -> swizzled box -> TMA store
       auto store_box = [&](const float* v, int c0) {
-        if (g.dbg == 1) return;
         uint8_t* box = wbuf + (nbox == 2 ? (nchunk & 1) : 0) * kEpiBufBytes;
         if (lane == 0 && nchunk >= nbox) {  // box reused nbox chunks later
           if (nbox == 2) tma_store_wait_read<1>();
@@ -797,52 +797,7 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
           const int col = n0 + c0 + lane;
           const bool col_ok = lane < CW && col < g.N;
           const bool need_aux = epi == EPI_RELU_MASK || epi == EPI_TANH_GRAD;
-          if (col_ok && epi == EPI_ADAM) {
-            // Adam (+ Polyak, + bf16 copies) on this column of the parameter block; the rows of
-            // a chunk are loaded 8 at a time (independent round trips), lanes = columns
-            AdamScalars as;
-            as.b1 = static_cast<float>(0.9);
-            as.b2 = static_cast<float>(0.999);
-            as.c1 = g.ad_c1[g.ad_t[grp]];
-            as.c2 = g.ad_c2[g.ad_t[grp]];
-            as.step = g.ad_lr[mem];
-            as.epsv = static_cast<float>(1e-8);
-            as.polyak = g.ad_tgt && (!g.ad_gate || g.ad_gate[mem]);
-            as.ta = as.polyak ? g.ad_ta[mem] : 0.0f;
-            as.tb = as.polyak ? g.ad_tb[mem] : 0.0f;
-            const long long gb = static_cast<long long>(grp) * g.ad_gs + col;
-#pragma unroll 1
-            for (int r8 = 0; r8 < 32; r8 += 8) {
-              float pv[8], mv[8], vv[8], tv[8];
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const int rw = row0 + r8 + u;
-                const long long e = gb + static_cast<long long>(rw) * g.c_rs;
-                const bool ok = rw < g.M;
-                pv[u] = ok ? g.ad_p[e] : 0.0f;
-                mv[u] = ok ? g.ad_m[e] : 0.0f;
-                vv[u] = ok ? g.ad_v[e] : 0.0f;
-                tv[u] = (ok && as.polyak) ? g.ad_tgt[e] : 0.0f;
-              }
-#pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const int rr = r8 + u;
-                const int rw = row0 + rr;
-                if (rw >= g.M) break;
-                const long long e = gb + static_cast<long long>(rw) * g.c_rs;
-                adam_one(as, pv[u], mv[u], vv[u], T[rr * 33 + lane]);
-                g.ad_p[e] = pv[u];
-                g.ad_m[e] = mv[u];
-                g.ad_v[e] = vv[u];
-                if (g.ad_p16) g.ad_p16[e] = __float2bfloat16_rn(pv[u]);
-                if (as.polyak) {
-                  const float tn = as.ta * pv[u] + as.tb * tv[u];
-                  g.ad_tgt[e] = tn;
-                  if (g.ad_t16) g.ad_t16[e] = __float2bfloat16_rn(tn);
-                }
-              }
-            }
-          } else if (col_ok) {
+          if (col_ok) {
             const float bv = bias ? bias[col] : 0.0f;
 #pragma unroll 1
             for (int r8 = 0; r8 < 32; r8 += 8) {
@@ -1022,15 +977,13 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) {
-    TC_TRACE(1);
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  }
+  if (threadIdx.x == 0) TC_TRACE(1);
   auto active = [&](int grp) { return !g.active || g.active[grp % g.n_members]; };
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       asm volatile("griddepcontrol.wait;" ::: "memory");
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after the wait (k_tc_gemm)
       int it = 0, cnt = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int grp = t / m_tiles, m0 = (t % m_tiles) * kBM;
@@ -1545,8 +1498,6 @@ void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn
                     const TcArgs& g0, cudaStream_t s) {
   TcArgs g = g0;
   const int bn = pick_bn(g, b_mn);
-  static const int dbg = std::getenv("PBRL_TC_DBG") ? std::atoi(std::getenv("PBRL_TC_DBG")) : 0;
-  g.dbg = dbg;
   if (g_trace && g_trace_n < kTraceLaunches) {
     g.trace = g_trace + static_cast<size_t>(g_trace_n) * kTraceCtas * kTraceSlots;
     g_trace_meta[g_trace_n] = TcTraceMeta{bn, a_mn ? 1 : 0, b_mn ? 1 : 0, g.nout, g.M, g.N, g.K,

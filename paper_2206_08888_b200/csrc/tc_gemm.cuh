@@ -59,23 +59,6 @@ struct TcArgs {
   // EPI_TANH_GRAD (aux = tanh values, scale) or EPI_STORE
   int ow_tr = 0;
   long long ow_ld = 0;
-  // EPI_ADAM (a dW product): instead of storing the gradient, apply adam_step_inplace (+ the
-  // Polyak target update, + the bf16 operand copies) to the parameter block it belongs to:
-  // element (r, c) of group g is parameter ad_*[g * ad_gs + r * c_rs + c]
-  float* ad_p = nullptr;
-  float* ad_m = nullptr;
-  float* ad_v = nullptr;
-  float* ad_tgt = nullptr;
-  __nv_bfloat16* ad_p16 = nullptr;
-  __nv_bfloat16* ad_t16 = nullptr;
-  long long ad_gs = 0;
-  const int64_t* ad_t = nullptr;
-  const float* ad_c1 = nullptr;  // bias-correction tables indexed by t
-  const float* ad_c2 = nullptr;
-  const float* ad_lr = nullptr;  // per member
-  const float* ad_ta = nullptr;
-  const float* ad_tb = nullptr;
-  const int* ad_gate = nullptr;  // Polyak gate per member (nullptr: always)
   // ReLU masks as bits: a storing BIAS_RELU / fused epilogue writes bit (c % 32) of word c / 32
   // of row r = (h[r][c] > 0) to mask_out; EPI_RELU_MASK reads mask_in (when set) instead of aux
   uint32_t* mask_out = nullptr;
@@ -87,9 +70,8 @@ struct TcArgs {
   const float* noise_eps = nullptr;
   long long ne_gs = 0, ne_rs = 0;
   int c_tma = 0, aux_tma = 0;  // set by launch_tc_gemm
-  unsigned long long* trace = nullptr;
-  int dbg = 0;
-  int b_prefetch = 0;  // B (weights) may be read before the PDL wait (predecessor wrote none)  // diagnostics (PBRL_TC_DBG): 1 = skip C stores, 2 = direct per-row global stores  // diagnostics timeline (PBRL_TC_TRACE), see tc_gemm.cu
+  unsigned long long* trace = nullptr;  // diagnostics timeline (PBRL_TC_TRACE), see tc_gemm.cu
+  int b_prefetch = 0;  // B (weights) may be read before the PDL wait (predecessor wrote none)
 };
 
 struct TcTraceMeta {

@@ -24,6 +24,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
+from .errors import NotReadyError
 from .pbrl import (EvolvePlan, PBTState, RngSequence, member_blob_size, export_member,
                    import_member)
 
@@ -112,6 +113,12 @@ class ShardedPBT:
         return rings (local indices); returns the global plan (identical on every rank)."""
         if self.n_total < 4:
             return None
+        # readiness first, on every rank: a shard with an unscored member must not leave the
+        # others blocked in the fitness all_gather -- every rank raises NotReadyError together
+        ready = self.gather_fitness(np.asarray([1.0 if pbt_local.every_member_scored() else 0.0]))
+        if not bool(np.all(ready > 0.0)):
+            raise NotReadyError("pbt_rank: every member needs at least one recorded return "
+                                f"(ranks not ready: {np.flatnonzero(ready <= 0.0).tolist()})")
         fitness = self.gather_fitness(pbt_local.fitness())
         replaced, donors = self.shard.plan(fitness, self.trunc, rng)
         lo = self.shard.offset

@@ -224,9 +224,31 @@ def make_synthetic_batches(count: int, n: int, batch: int, obs_dim: int, act_dim
     return [TransitionBatch(*[t[i] for t in ts]) for i in range(count)]
 
 
-def _batch_struct(b: TransitionBatch, keep: list):
+def _check_batch_shapes(b: TransitionBatch, n: int, rows: int, ds: int, da: int) -> None:
+    """TransitionBatch extents (algos.hpp:14-24): s, s2 [n, rows, ds], a [n, rows, da], r and done
+    [n, rows, 1] (or [n, rows]).  The library copies n*rows*dim elements per field, so a wrong
+    width must fail here (ShapeError, naming both shapes) instead of reading out of bounds."""
+    for name, x, dim in (("s", b.s, ds), ("a", b.a, da), ("r", b.r, 1), ("s2", b.s2, ds),
+                         ("done", b.done, 1)):
+        shp = tuple(int(v) for v in x.shape)
+        ok = len(shp) == 3 and shp == (n, rows, dim)
+        if dim == 1 and len(shp) == 2:
+            ok = shp == (n, rows)
+        if not ok:
+            raise ShapeError(f"TransitionBatch.{name}: shape {list(shp)} != "
+                             f"[{n}, {rows}, {dim}]")
+
+
+def _batch_struct(b: TransitionBatch, keep: list, device: int):
     if b.is_device():
-        arrs = [x.contiguous() for x in (b.s, b.a, b.r, b.s2, b.done)]
+        import torch
+        arrs = []
+        for x in (b.s, b.a, b.r, b.s2, b.done):
+            if x.dtype != torch.float32:
+                raise UsageError(f"device batch tensors must be float32 (got {x.dtype})")
+            if x.device.index != device:
+                raise UsageError(f"device batch on {x.device}, population on cuda:{device}")
+            arrs.append(x.contiguous())
         keep.extend(arrs)
         return _lib.Batch(*[x.data_ptr() for x in arrs]), True
     arrs = [_f32(np.asarray(x)) for x in (b.s, b.a, b.r, b.s2, b.done)]
@@ -349,6 +371,32 @@ class _Population:
         return out
 
     # -- updates
+    def lib_stream(self):
+        """The library's CUDA stream of this population as a torch ExternalStream."""
+        if getattr(self, "_ext_stream", None) is None:
+            import torch
+            sp = C.c_void_p()
+            _lib.call("pbrl_get_stream", self._h, C.byref(sp))
+            self._ext_stream = torch.cuda.ExternalStream(sp.value,
+                                                         device=torch.device("cuda", self.device))
+        return self._ext_stream
+
+    def _device_call_begin(self):
+        """Device batches are written on torch's current stream: the library stream waits for
+        that work before its first kernel reads them."""
+        import torch
+        ext = self.lib_stream()
+        ext.wait_stream(torch.cuda.current_stream(torch.device("cuda", self.device)))
+        return ext
+
+    @staticmethod
+    def _device_call_end(ext, keep):
+        """The library runs asynchronously: tensors it reads (incl. .contiguous() temporaries)
+        must not return to torch's caching allocator before the library stream is done."""
+        for x in keep:
+            if hasattr(x, "record_stream"):
+                x.record_stream(ext)
+
     def _update(self, batches: Sequence[TransitionBatch], mask=None,
                 return_losses: bool = False) -> Optional[np.ndarray]:
         if not batches:
@@ -362,7 +410,8 @@ class _Population:
                                   f"population {self.n}")
             if b.rows() != rows:
                 raise ShapeError("all batches of one call must have the same row count")
-            s, d = _batch_struct(b, keep)
+            _check_batch_shapes(b, self.n, rows, self.obs_dim, self.act_dim)
+            s, d = _batch_struct(b, keep, self.device)
             if dev is None:
                 dev = d
             elif dev != d:
@@ -372,6 +421,8 @@ class _Population:
         m = None
         if mask is not None:
             mk = np.ascontiguousarray(np.asarray(mask, dtype=bool).astype(np.uint8))
+            if mk.shape != (self.n,):
+                raise ShapeError(f"policy_member_mask: {mk.size} entries != population {self.n}")
             keep.append(mk)
             m = _ptr(mk, _lib.u8p)
         if return_losses and not dev:
@@ -380,16 +431,21 @@ class _Population:
             _lib.call("pbrl_update_batches_losses", self._h, arr, len(structs), rows, m,
                       _ptr(out, _lib.f64p))
             return out
-        if return_losses:  # device batches: step by step
-            out = np.empty((len(structs), 3, self.n), np.float64)
-            for i in range(len(structs)):
-                one = (_lib.Batch * 1)(structs[i])
-                _lib.call("pbrl_update_batches_device", self._h, one, 1, rows, m)
-                out[i] = np.stack(self.last_losses())
-            return out
-        fn = "pbrl_update_batches_device" if dev else "pbrl_update_batches"
-        _lib.call(fn, self._h, arr, len(structs), rows, m)
-        return None
+        ext = self._device_call_begin() if dev else None
+        try:
+            if return_losses:  # device batches: step by step
+                out = np.empty((len(structs), 3, self.n), np.float64)
+                for i in range(len(structs)):
+                    one = (_lib.Batch * 1)(structs[i])
+                    _lib.call("pbrl_update_batches_device", self._h, one, 1, rows, m)
+                    out[i] = np.stack(self.last_losses())
+                return out
+            fn = "pbrl_update_batches_device" if dev else "pbrl_update_batches"
+            _lib.call(fn, self._h, arr, len(structs), rows, m)
+            return None
+        finally:
+            if ext is not None:
+                self._device_call_end(ext, keep)
 
     def launch_count(self) -> int:
         c = C.c_uint64()
@@ -710,10 +766,16 @@ class EvolvePlan:
     donors: List[int]
 
 
+def _rank_key(f: float) -> float:
+    """Sort key of a fitness value: NaN (a diverged member) ranks as -inf, i.e. last, so the
+    ranking is a total order (the reference's comparator is undefined for NaN)."""
+    return -math.inf if math.isnan(f) else f
+
+
 def pbt_rank(st: PBTState) -> List[int]:
     """pbt_rank (evolve.hpp:112-122): best first, ties toward the lower index."""
     f = st.fitness()
-    return sorted(range(len(f)), key=lambda i: (-f[i], i))
+    return sorted(range(len(f)), key=lambda i: (-_rank_key(f[i]), i))
 
 
 def pbt_plan(st: PBTState, rng: RngSequence, pop: _Population) -> Optional[EvolvePlan]:
@@ -784,7 +846,7 @@ def plan_from_fitness(fitness: Sequence[float], trunc: float, rng: RngSequence
     n = len(fitness)
     if n < 4:
         return [], []
-    order = sorted(range(n), key=lambda i: (-fitness[i], i))
+    order = sorted(range(n), key=lambda i: (-_rank_key(float(fitness[i])), i))
     cut = int(math.ceil(trunc * n))
     replaced, donors = [], []
     for i in range(cut):

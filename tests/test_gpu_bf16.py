@@ -102,45 +102,6 @@ def test_bf16_fused_forward_hidden_shapes(pb, ora, algo, hidden):
         assert e <= DELTA_TOL, (net, e)
 
 
-def test_bf16_fused_adam_epilogue_is_bit_identical(pb, ora):
-    """EPI_ADAM (Adam + Polyak inside the tensor-core dW product, opt-in via PBRL_FUSED_ADAM=1)
-    must produce exactly the parameters of the separate k_adam pass; run in a subprocess so the
-    environment switch is read at population construction."""
-    import os
-    import subprocess
-    import sys
-    code = r'''
-import sys, numpy as np
-sys.path.insert(0, ".")
-sys.path.insert(0, "tests")
-import paper_2206_08888_b200 as pb
-from oracle.oracle import load_oracle
-from helpers import TD3_NETS, to_batch
-ora = load_oracle()
-n, B = 3, 256
-st = pb.make_td3_state(n, 17, 6, [256, 256], 1.0, 5, precision="bf16")
-raw = ora.synthetic_batches(4, n, B, 17, 6, 5)
-hy = pb.Td3Hyper.defaults(n)
-for k in range(4):
-    pb.td3_update_step(st, to_batch(pb, raw, k), hy)
-np.savez(sys.argv[1], **{net: st.params(net) for net in TD3_NETS})
-'''
-    import tempfile
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = {}
-    for flag in ("0", "1"):
-        env = dict(os.environ)
-        env.pop("PBRL_FUSED_ADAM", None)
-        if flag == "1":
-            env["PBRL_FUSED_ADAM"] = "1"
-        path = os.path.join(tempfile.mkdtemp(), f"p{flag}.npz")
-        subprocess.run([sys.executable, "-c", code, path], check=True, cwd=root, env=env)
-        out[flag] = np.load(path)
-    for net in TD3_NETS:
-        assert np.array_equal(out["0"][net], out["1"][net]), net
-
-
-
 def test_bf16_large_batch_output_layer_is_a_loud_config_error(pb, ora):
     """Known BF16-mode boundary (DESIGN.md section 5): with B * n_out > 32768 (policy: 8192 x 6)
     the output layer's backward would be a K = n_out < 8 dX product, which has no tensor-core
