@@ -191,6 +191,63 @@ int pbrl_member_blob_size(pbrl_pop* pop, uint64_t* floats);
 int pbrl_export_member(pbrl_pop* pop, uint64_t member, float* dev_buf);
 int pbrl_import_member(pbrl_pop* pop, uint64_t member, const float* dev_buf);
 
+/* ---- whole-member state copy: slice_member / set_member for states (algos.hpp:425-464,
+ * :839-886).  Copies member sm of src into member dm of dst: every network, Adam m / v / t,
+ * steps, streams, delay_acc (TD3) or log_alpha + its Adam state (SAC), and the hypers.  With dst
+ * a fresh population of one (make_*_state(1, ...)) it is slice_member(src, sm); with src a
+ * singleton it is set_member(dst, dm, single).  Shapes and algorithm must match (ShapeError). */
+int pbrl_copy_member_state(pbrl_pop* dst, uint64_t dst_member, pbrl_pop* src, uint64_t src_member);
+
+/* ---- sharded population: the PBT exchange across devices.
+ * The reference is single-process; this is pbt_evolve_trainer (evolve.hpp:169-213) for a
+ * population split in contiguous member blocks over `world` ranks (rank r owns global members
+ * [r*n, (r+1)*n), desc.member_offset = r*n, desc.n_global = world*n).  The update step needs no
+ * communication (RNG streams keyed by global id); only PBT exchanges data:
+ *   1. all-gather of [ready, fitness of every local member] (doubles);
+ *   2. every rank computes the identical plan on device (pbrl_pbt_plan);
+ *   3. donor -> replaced copies: same-rank pairs on device, cross-rank pairs as grouped
+ *      point-to-point transfers of the member blob (pbrl_export_member layout);
+ *   4. optimiser / delay reset of local receivers; the hyper re-draw in lock-step on every rank
+ *      (each rank draws the prior sample of every replaced member, applies its own). */
+typedef struct pbrl_comm pbrl_comm;
+
+/* host transport: one point-to-point transfer of a HOST buffer */
+typedef struct {
+  int peer;        /* rank */
+  int is_send;     /* 1: send buf to peer, 0: receive into buf from peer */
+  float* buf;
+  uint64_t floats;
+} pbrl_p2p_op;
+
+/* caller-supplied host transport (e.g. gloo through torch.distributed, MPI); both callbacks
+ * return 0 on success and are collective over the ranks. */
+typedef struct {
+  void* ctx;
+  /* recv = [world][count] doubles, rank-major */
+  int (*allgather_f64)(void* ctx, const double* send, uint64_t count, double* recv);
+  /* all ops of this rank as one group (like ncclGroupStart / ncclGroupEnd) */
+  int (*exchange)(void* ctx, const pbrl_p2p_op* ops, uint32_t n_ops);
+} pbrl_comm_ops;
+
+/* NCCL transport over NVLink / NVSwitch: rank 0 calls pbrl_nccl_unique_id, the caller
+ * distributes the 128 bytes, every rank calls pbrl_comm_create_nccl with its device. */
+int pbrl_nccl_unique_id(void* id, size_t len);
+int pbrl_comm_create_nccl(const void* id, int rank, int world, int device, pbrl_comm** out);
+int pbrl_comm_create_host(const pbrl_comm_ops* ops, int rank, int world, int device,
+                          pbrl_comm** out);
+int pbrl_comm_destroy(pbrl_comm* comm);
+/* pbt_evolve_trainer for one shard.  local_fitness: [n] means of this rank's members' return
+ * rings; local_ready = every local member scored (PBTState::every_member_scored).  If any
+ * rank is not ready, EVERY rank returns PBRL_E_NOT_READY (NotReadyError, evolve.hpp:113-115)
+ * and nothing changes.  replaced/donors: [ceil(trunc * n_global)] global ids (the plan, same on
+ * every rank); *rng_next advances like the single-shard pbrl_pbt_evolve.  The caller clears
+ * the return rings of its replaced members (pbt_apply_returns_reset, evolve.hpp:149-152).
+ * exchange_ms (may be NULL): [3] host wall times of (fitness all-gather, plan, copies+resets). */
+int pbrl_pbt_evolve_sharded(pbrl_pop* pop, pbrl_comm* comm, const double* local_fitness,
+                            int local_ready, double trunc, uint64_t rng_key, uint64_t* rng_next,
+                            uint64_t* replaced, uint64_t* donors, uint32_t* count,
+                            double* exchange_ms);
+
 /* ---- synthetic inputs: make_synthetic_batches (bench.hpp:69-93) generated on the device.
  * out: count device batches; each field is a device pointer to [count][n][b][dim] floats laid out
  * contiguously (out->s holds all count batches).  pop may be NULL (current device). */

@@ -104,6 +104,7 @@ class Oracle(_Lib):
         self.bits = F("ora_bits", u64, u64, u64)
         self.uniform = F("ora_uniform", C.c_double, u64, u64)
         self.normal_pair = F("ora_normal_pair", C.c_double, u64, u64)
+        self.set_emulation = F("ora_set_emulation", None, C.c_int)
         for algo in ("td3", "sac"):
             F(f"ora_{algo}_create", vp, u64, u64, u64, u64p, u32, C.c_double, u64)
             F(f"ora_{algo}_destroy", None, vp)

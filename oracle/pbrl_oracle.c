@@ -8,8 +8,10 @@
 #include "pbrl_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #define ORA_MAXL 8
 enum { ACT_NONE = 0, ACT_RELU = 1, ACT_TANH = 2 };
@@ -126,9 +128,84 @@ static void cache_free(ora_cache* c) {
   memset(c, 0, sizeof(*c));
 }
 
+/* Tensor-core operand emulation (NOT the reference: used only by oracle/derive_tolerances.py to
+ * derive the TF32 / BF16 parity tolerances).  0 = exact fp32 (the reference arithmetic), 1 = TF32
+ * operands (fp32 with the low 13 mantissa bits dropped, as tcgen05 kind::tf32 reads fp32 data),
+ * 2 = BF16 operands (round to nearest even).  Applied to both operands of every hidden-layer
+ * product -- forward, dX and dW -- i.e. exactly the products the library runs on tcgen05; the
+ * output layers, biases, losses, Adam and Polyak stay fp32 as in the library. */
+static int g_emul = 0;
+void ora_set_emulation(int mode) { g_emul = mode; }
+
+static float emu(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  if (g_emul == 1) {
+    u &= 0xffffe000u;
+  } else if (g_emul == 2) {
+    if ((u & 0x7fffffffu) > 0x7f800000u) return x;
+    u = (u + 0x7fffu + ((u >> 16) & 1u)) & 0xffff0000u;
+  } else {
+    return x;
+  }
+  memcpy(&x, &u, 4);
+  return x;
+}
+
+/* rounded copy of count floats (malloc'd), or NULL when emulation is off / not a TC product */
+static float* emu_copy(const float* x, uint64_t count, int tc) {
+  if (!g_emul || !tc) return NULL;
+  float* o = (float*)malloc(sizeof(float) * count);
+  for (uint64_t i = 0; i < count; ++i) o[i] = emu(x[i]);
+  return o;
+}
+
+
+/* Members are independent, so the per-member loops of the MLP forward and
+ * backward run on a few pthreads; each member's arithmetic is unchanged, so the result bits do
+ * not depend on the thread count (ORA_THREADS, default: online CPUs, at most 32). */
+typedef void (*member_fn)(void* ctx, uint64_t m);
+typedef struct {
+  member_fn fn;
+  void* ctx;
+  uint64_t n, stride, first;
+} par_job;
+
+static void* par_worker(void* arg) {
+  par_job* j = (par_job*)arg;
+  for (uint64_t m = j->first; m < j->n; m += j->stride) j->fn(j->ctx, m);
+  return NULL;
+}
+
+static void for_members(uint64_t n, member_fn fn, void* ctx) {
+  static long threads = 0;
+  if (threads == 0) {
+    const char* e = getenv("ORA_THREADS");
+    threads = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+    if (threads < 1) threads = 1;
+    if (threads > 32) threads = 32;
+  }
+  uint64_t t = (uint64_t)threads < n ? (uint64_t)threads : n;
+  if (t <= 1) {
+    for (uint64_t m = 0; m < n; ++m) fn(ctx, m);
+    return;
+  }
+  pthread_t tid[32];
+  par_job job[32];
+  for (uint64_t i = 0; i < t; ++i) {
+    job[i] = (par_job){fn, ctx, n, t, i};
+    pthread_create(&tid[i], NULL, par_worker, &job[i]);
+  }
+  for (uint64_t i = 0; i < t; ++i) pthread_join(tid[i], NULL);
+}
+
 /* pop_matmul (pop_tensor.hpp:139-170) + pop_add_bias (:213-232) for one member */
 static void layer_forward(const float* x, uint64_t rows, uint64_t in, const float* w,
-                          const float* bias, uint64_t out, float* z) {
+                          const float* bias, uint64_t out, float* z, int tc) {
+  float* xe = emu_copy(x, rows * in, tc);
+  float* we = emu_copy(w, in * out, tc);
+  if (xe) x = xe;
+  if (we) w = we;
   for (uint64_t r = 0; r < rows; ++r) {
     const float* xr = x + r * in;
     float* zr = z + r * out;
@@ -141,6 +218,8 @@ static void layer_forward(const float* x, uint64_t rows, uint64_t in, const floa
     }
     for (uint64_t o = 0; o < out; ++o) zr[o] = zr[o] + bias[o];
   }
+  free(xe);
+  free(we);
 }
 
 /* activation (pop_tensor.hpp:254-271) */
@@ -150,6 +229,23 @@ static void act_forward(const float* z, float* y, uint64_t count, int act) {
     else if (act == ACT_TANH) y[i] = tanhf(z[i]);
     else y[i] = z[i];
   }
+}
+
+typedef struct {
+  const ora_net* nt;
+  const float* params;
+  ora_cache* c;
+  uint64_t rows;
+  int l;
+} fwd_ctx;
+
+static void fwd_member(void* p, uint64_t m) {
+  const fwd_ctx* f = (const fwd_ctx*)p;
+  const ora_net* nt = f->nt;
+  const uint64_t in = nt->dims[f->l], out = nt->dims[f->l + 1], rows = f->rows;
+  layer_forward(f->c->in[f->l] + m * rows * in, rows, in, f->params + m * nt->P + nt->woff[f->l],
+                f->params + m * nt->P + nt->boff[f->l], out, f->c->z[f->l] + m * rows * out,
+                f->l + 1 < nt->depth);
 }
 
 /* pop_mlp_forward, net_pop.hpp:109-131 */
@@ -164,10 +260,8 @@ static void mlp_forward(const ora_net* nt, const float* params, uint64_t n, uint
   for (int l = 0; l < nt->depth; ++l) {
     const uint64_t in = nt->dims[l], out = nt->dims[l + 1];
     c->z[l] = (float*)malloc(sizeof(float) * n * rows * out);
-    for (uint64_t m = 0; m < n; ++m) {
-      layer_forward(c->in[l] + m * rows * in, rows, in, params + m * nt->P + nt->woff[l],
-                    params + m * nt->P + nt->boff[l], out, c->z[l] + m * rows * out);
-    }
+    fwd_ctx fc = {nt, params, c, rows, l};
+    for_members(n, fwd_member, &fc);
     float* y = (float*)malloc(sizeof(float) * n * rows * out);
     act_forward(c->z[l], y, n * rows * out, (l + 1 < nt->depth) ? ACT_RELU : nt->out_act);
     if (l + 1 < nt->depth) c->in[l + 1] = y;
@@ -182,63 +276,94 @@ static void mlp_forward(const ora_net* nt, const float* params, uint64_t n, uint
 /* pop_mlp_backward, net_pop.hpp:134-160, composed of activation_backward
  * (pop_tensor.hpp:275-297), pop_add_bias_backward (:236-250) and pop_matmul_backward
  * (:173-210).  grads: [n][P] (overwritten); grad_x: [n][rows][dims[0]] or NULL. */
-static void mlp_backward(const ora_net* nt, const float* params, const ora_cache* c,
-                         const float* grad_y, float* grads, float* grad_x) {
-  const uint64_t rows = c->rows;
-  uint64_t widest = 0;
-  for (int l = 0; l <= nt->depth; ++l) widest = nt->dims[l] > widest ? nt->dims[l] : widest;
+typedef struct {
+  const ora_net* nt;
+  const float* params;
+  const ora_cache* c;
+  const float* grad_y;
+  float* grads;
+  float* grad_x;
+  uint64_t widest;
+} bwd_ctx;
+
+static void bwd_member(void* p, uint64_t m) {
+  const bwd_ctx* f = (const bwd_ctx*)p;
+  const ora_net* nt = f->nt;
+  const float* params = f->params;
+  const ora_cache* c = f->c;
+  const float* grad_y = f->grad_y;
+  float* grads = f->grads;
+  float* grad_x = f->grad_x;
+  const uint64_t rows = c->rows, widest = f->widest;
   float* g = (float*)malloc(sizeof(float) * rows * widest);
   float* gx = (float*)malloc(sizeof(float) * rows * widest);
-  for (uint64_t m = 0; m < c->n; ++m) {
-    const uint64_t dout = nt->dims[nt->depth];
-    memcpy(g, grad_y + m * rows * dout, sizeof(float) * rows * dout);
-    if (nt->out_scale != 1.0f) {
-      for (uint64_t i = 0; i < rows * dout; ++i) g[i] *= nt->out_scale;
-    }
-    for (int l = nt->depth - 1; l >= 0; --l) {
-      const uint64_t in = nt->dims[l], out = nt->dims[l + 1];
-      const int act = (l + 1 < nt->depth) ? ACT_RELU : nt->out_act;
-      const float* z = c->z[l] + m * rows * out;
-      if (act == ACT_RELU) {
-        for (uint64_t i = 0; i < rows * out; ++i) {
-          if (!(z[i] > 0.0f)) g[i] = 0.0f;
-        }
-      } else if (act == ACT_TANH) {
-        for (uint64_t i = 0; i < rows * out; ++i) {
-          const float t = tanhf(z[i]);
-          g[i] *= (1.0f - t * t);
-        }
-      }
-      float* gb = grads + m * nt->P + nt->boff[l];
-      for (uint64_t o = 0; o < out; ++o) gb[o] = 0.0f;
-      for (uint64_t r = 0; r < rows; ++r) {
-        for (uint64_t o = 0; o < out; ++o) gb[o] += g[r * out + o];
-      }
-      const float* w = params + m * nt->P + nt->woff[l];
-      float* gw = grads + m * nt->P + nt->woff[l];
-      const float* x = c->in[l] + m * rows * in;
-      for (uint64_t i = 0; i < in * out; ++i) gw[i] = 0.0f;
-      for (uint64_t r = 0; r < rows; ++r) {
-        const float* gr = g + r * out;
-        const float* xr = x + r * in;
-        for (uint64_t i = 0; i < in; ++i) {
-          const float* wr = w + i * out;
-          float acc = 0.0f;
-          for (uint64_t o = 0; o < out; ++o) acc += gr[o] * wr[o];
-          gx[r * in + i] = acc;
-          const float xi = xr[i];
-          float* gwr = gw + i * out;
-          for (uint64_t o = 0; o < out; ++o) gwr[o] += xi * gr[o];
-        }
-      }
-      float* tmp = g;
-      g = gx;
-      gx = tmp;
-    }
-    if (grad_x) memcpy(grad_x + m * rows * nt->dims[0], g, sizeof(float) * rows * nt->dims[0]);
+  const uint64_t dout = nt->dims[nt->depth];
+  memcpy(g, grad_y + m * rows * dout, sizeof(float) * rows * dout);
+  if (nt->out_scale != 1.0f) {
+    for (uint64_t i = 0; i < rows * dout; ++i) g[i] *= nt->out_scale;
   }
+  for (int l = nt->depth - 1; l >= 0; --l) {
+    const uint64_t in = nt->dims[l], out = nt->dims[l + 1];
+    const int act = (l + 1 < nt->depth) ? ACT_RELU : nt->out_act;
+    const float* z = c->z[l] + m * rows * out;
+    if (act == ACT_RELU) {
+      for (uint64_t i = 0; i < rows * out; ++i) {
+        if (!(z[i] > 0.0f)) g[i] = 0.0f;
+      }
+    } else if (act == ACT_TANH) {
+      for (uint64_t i = 0; i < rows * out; ++i) {
+        const float t = tanhf(z[i]);
+        g[i] *= (1.0f - t * t);
+      }
+    }
+    /* emulation only: the hidden-layer cotangent is a tensor-core operand */
+    const int tc = l + 1 < nt->depth;
+    if (g_emul && tc) {
+      for (uint64_t i = 0; i < rows * out; ++i) g[i] = emu(g[i]);
+    }
+    float* gb = grads + m * nt->P + nt->boff[l];
+    for (uint64_t o = 0; o < out; ++o) gb[o] = 0.0f;
+    for (uint64_t r = 0; r < rows; ++r) {
+      for (uint64_t o = 0; o < out; ++o) gb[o] += g[r * out + o];
+    }
+    const float* w = params + m * nt->P + nt->woff[l];
+    float* gw = grads + m * nt->P + nt->woff[l];
+    const float* x = c->in[l] + m * rows * in;
+    float* we = emu_copy(w, in * out, tc);
+    float* xe = emu_copy(x, rows * in, tc);
+    if (we) w = we;
+    if (xe) x = xe;
+    for (uint64_t i = 0; i < in * out; ++i) gw[i] = 0.0f;
+    for (uint64_t r = 0; r < rows; ++r) {
+      const float* gr = g + r * out;
+      const float* xr = x + r * in;
+      for (uint64_t i = 0; i < in; ++i) {
+        const float* wr = w + i * out;
+        float acc = 0.0f;
+        for (uint64_t o = 0; o < out; ++o) acc += gr[o] * wr[o];
+        gx[r * in + i] = acc;
+        const float xi = xr[i];
+        float* gwr = gw + i * out;
+        for (uint64_t o = 0; o < out; ++o) gwr[o] += xi * gr[o];
+      }
+    }
+    free(we);
+    free(xe);
+    float* tmp = g;
+    g = gx;
+    gx = tmp;
+  }
+  if (grad_x) memcpy(grad_x + m * rows * nt->dims[0], g, sizeof(float) * rows * nt->dims[0]);
   free(g);
   free(gx);
+}
+
+static void mlp_backward(const ora_net* nt, const float* params, const ora_cache* c,
+                         const float* grad_y, float* grads, float* grad_x) {
+  uint64_t widest = 0;
+  for (int l = 0; l <= nt->depth; ++l) widest = nt->dims[l] > widest ? nt->dims[l] : widest;
+  bwd_ctx bc = {nt, params, c, grad_y, grads, grad_x, widest};
+  for_members(c->n, bwd_member, &bc);
 }
 
 /* adam_step_inplace for one member (pop_tensor.hpp:328-366); t is shared by every tensor of the

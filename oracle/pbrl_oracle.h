@@ -25,6 +25,9 @@ extern "C" {
 #endif
 
 /* counter RNG, rng.hpp:13-70 */
+/* derive_tolerances.py only: 0 exact fp32, 1 TF32 operands, 2 BF16 operands */
+void ora_set_emulation(int mode);
+
 uint64_t ora_mix64(uint64_t x);
 uint64_t ora_stream_key(uint64_t seed, uint64_t stream, uint64_t use, uint64_t step);
 uint64_t ora_bits(uint64_t key, uint64_t counter);

@@ -38,6 +38,18 @@ class Batch(C.Structure):
     _fields_ = [("s", vp), ("a", vp), ("r", vp), ("s2", vp), ("done", vp)]
 
 
+class P2POp(C.Structure):
+    _fields_ = [("peer", C.c_int), ("is_send", C.c_int), ("buf", f32p), ("floats", u64)]
+
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, vp, f64p, u64, f64p)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, vp, C.POINTER(P2POp), u32)
+
+
+class CommOps(C.Structure):
+    _fields_ = [("ctx", vp), ("allgather_f64", ALLGATHER_FN), ("exchange", EXCHANGE_FN)]
+
+
 # name -> (restype, argtypes); every function returns an int status
 SIGNATURES = {
     "pbrl_pop_create": [C.POINTER(PopDesc), C.POINTER(vp)],
@@ -89,6 +101,12 @@ SIGNATURES = {
                                    C.c_longlong, C.c_longlong, vp, C.c_longlong, C.c_longlong,
                                    vp, C.c_longlong, C.c_longlong],
     "pbrl_synthetic_batches_device": [vp, u64, u64, u64, u64, u64, u64, C.POINTER(Batch)],
+    "pbrl_copy_member_state": [vp, u64, vp, u64],
+    "pbrl_nccl_unique_id": [vp, C.c_size_t],
+    "pbrl_comm_create_nccl": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)],
+    "pbrl_comm_create_host": [C.POINTER(CommOps), C.c_int, C.c_int, C.c_int, C.POINTER(vp)],
+    "pbrl_comm_destroy": [vp],
+    "pbrl_pbt_evolve_sharded": [vp, vp, f64p, C.c_int, dbl, u64, u64p, u64p, u64p, u32p, f64p],
 }
 
 _lib = None

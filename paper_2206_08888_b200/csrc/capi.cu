@@ -1,11 +1,13 @@
 // extern "C" boundary (include/pbrl_b200.h): error mapping, member access, replay, PBT.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <fstream>
 #include <string>
 #include <unordered_map>
 
+#include "comm.cuh"
 #include "pop_impl.cuh"
 #include "tc_gemm.cuh"
 
@@ -57,26 +59,32 @@ struct Seq {
 
 // Td3Prior / SacPrior::sample_member (evolve.hpp:31-73): the sampled fields, then the untuned
 // fields reset to their defaults (set_member copies the whole one-member hyper).
-void prior_sample(Pop* p, Seq& rng, uint64_t m) {
-  auto& h = p->hyper;
-  if (p->algo == PBRL_ALGO_TD3) {
-    h[0][m] = rng.log_uniform(3e-5, 3e-3);
-    h[1][m] = rng.log_uniform(3e-5, 3e-3);
-    h[2][m] = rng.uniform(0.2, 1.0);
-    h[3][m] = rng.uniform(0.0, 1.0);
-    h[4][m] = rng.uniform(0.0, 1.0);
-    h[6][m] = rng.uniform(0.9, 1.0);
-    h[5][m] = 0.5;
-    h[7][m] = 0.005;
+void prior_draw(int algo, Seq& rng, double* h) {
+  if (algo == PBRL_ALGO_TD3) {
+    h[0] = rng.log_uniform(3e-5, 3e-3);
+    h[1] = rng.log_uniform(3e-5, 3e-3);
+    h[2] = rng.uniform(0.2, 1.0);
+    h[3] = rng.uniform(0.0, 1.0);
+    h[4] = rng.uniform(0.0, 1.0);
+    h[6] = rng.uniform(0.9, 1.0);
+    h[5] = 0.5;
+    h[7] = 0.005;
   } else {
-    h[0][m] = rng.log_uniform(3e-5, 3e-3);
-    h[1][m] = rng.log_uniform(3e-5, 3e-3);
-    h[2][m] = rng.log_uniform(3e-5, 3e-3);
-    h[3][m] = rng.uniform(0.2, 2.0) * -1.0;  // SacPrior::default_target_entropy = -1
-    h[4][m] = rng.uniform(0.1, 10.0);
-    h[5][m] = rng.uniform(0.9, 1.0);
-    h[6][m] = 0.005;
+    h[0] = rng.log_uniform(3e-5, 3e-3);
+    h[1] = rng.log_uniform(3e-5, 3e-3);
+    h[2] = rng.log_uniform(3e-5, 3e-3);
+    h[3] = rng.uniform(0.2, 2.0) * -1.0;  // SacPrior::default_target_entropy = -1
+    h[4] = rng.uniform(0.1, 10.0);
+    h[5] = rng.uniform(0.9, 1.0);
+    h[6] = 0.005;
   }
+}
+
+void prior_sample(Pop* p, Seq& rng, uint64_t m) {
+  double h[8];
+  prior_draw(p->algo, rng, h);
+  const int nf = p->algo == PBRL_ALGO_TD3 ? 8 : 7;
+  for (int f = 0; f < nf; ++f) p->hyper[f][m] = h[f];
 }
 }  // namespace
 
@@ -968,6 +976,199 @@ int pbrl_device_bytes(pbrl_pop* pop, uint64_t* bytes) {
       b += d->count * 4;
     if (p->replay) b += p->replay->ring.count * 4;
     *bytes = b;
+  });
+}
+
+
+// ---------------------------------------------------------------- sharded PBT
+struct pbrl_comm {
+  pbrl::Comm* c;
+};
+
+int pbrl_nccl_unique_id(void* id, size_t len) {
+  return guarded([&] {
+    if (!id) PBRL_THROW(PBRL_E_USAGE, "null id buffer");
+    nccl_unique_id(id, len);
+  });
+}
+
+int pbrl_comm_create_nccl(const void* id, int rank, int world, int device, pbrl_comm** out) {
+  return guarded([&] {
+    if (!id || !out) PBRL_THROW(PBRL_E_USAGE, "null argument");
+    *out = nullptr;
+    Comm* c = make_nccl_comm(id, rank, world, device);
+    *out = new pbrl_comm{c};
+  });
+}
+
+int pbrl_comm_create_host(const pbrl_comm_ops* ops, int rank, int world, int device,
+                          pbrl_comm** out) {
+  return guarded([&] {
+    if (!out) PBRL_THROW(PBRL_E_USAGE, "null argument");
+    *out = nullptr;
+    Comm* c = make_host_comm(ops, rank, world, device);
+    *out = new pbrl_comm{c};
+  });
+}
+
+int pbrl_comm_destroy(pbrl_comm* comm) {
+  return guarded([&] {
+    if (!comm) return;
+    delete comm->c;
+    delete comm;
+  });
+}
+
+int pbrl_pbt_evolve_sharded(pbrl_pop* pop, pbrl_comm* comm, const double* local_fitness,
+                            int local_ready, double trunc, uint64_t rng_key, uint64_t* rng_next,
+                            uint64_t* replaced, uint64_t* donors, uint32_t* count,
+                            double* exchange_ms) {
+  using clk = std::chrono::steady_clock;
+  auto ms = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
+  *count = 0;
+  int rc = guarded([&] {
+    Pop* p = P(pop);
+    if (!comm || !comm->c) PBRL_THROW(PBRL_E_USAGE, "pbt_evolve_sharded: null comm");
+    Comm& c = *comm->c;
+    const uint64_t n = static_cast<uint64_t>(p->n);
+    if (c.device != p->device) PBRL_THROW(PBRL_E_USAGE, "pbt_evolve_sharded: comm on another device");
+    if (p->n_global != n * static_cast<uint64_t>(c.world) ||
+        p->member_offset != n * static_cast<uint64_t>(c.rank))
+      PBRL_THROW(PBRL_E_USAGE, "pbt_evolve_sharded: the population must be split in equal "
+                               "contiguous blocks, rank r owning members [r*n, (r+1)*n)");
+    const auto t0 = clk::now();
+    // 1. readiness + fitness of every member, rank-major
+    std::vector<double> send(n + 1), recv((n + 1) * c.world);
+    send[0] = local_ready ? 1.0 : 0.0;
+    std::memcpy(send.data() + 1, local_fitness, n * 8);
+    c.allgather_f64(send.data(), n + 1, recv.data(), p->stream);
+    std::vector<double> fit(n * c.world);
+    std::string not_ready;
+    for (int r = 0; r < c.world; ++r) {
+      if (recv[r * (n + 1)] == 0.0) not_ready += (not_ready.empty() ? "" : ",") + std::to_string(r);
+      std::memcpy(fit.data() + r * n, recv.data() + r * (n + 1) + 1, n * 8);
+    }
+    if (!not_ready.empty())
+      PBRL_THROW(PBRL_E_NOT_READY, "pbt_rank: every member needs at least one recorded return "
+                                   "(ranks not ready: " + not_ready + ")");
+    const auto t1 = clk::now();
+    // 2. the plan, identical on every rank (pbt_rank + pbt_plan, evolve.hpp:112-145)
+    uint32_t cnt = 0;
+    const int prc = pbrl_pbt_plan(pop, fit.data(), n * c.world, trunc, rng_key, rng_next,
+                                  replaced, donors, &cnt);
+    if (prc != PBRL_OK) PBRL_THROW(prc, g_last_error);
+    const auto t2 = clk::now();
+    if (cnt == 0) {
+      if (exchange_ms) exchange_ms[0] = ms(t0, t1), exchange_ms[1] = ms(t1, t2), exchange_ms[2] = 0;
+      return;
+    }
+    // 3. cross-rank exploit copies: one member blob per pair, grouped point-to-point
+    uint64_t blob = 0;
+    if (pbrl_member_blob_size(pop, &blob) != PBRL_OK) PBRL_THROW(PBRL_E_USAGE, g_last_error);
+    std::vector<P2P> ops;
+    std::vector<uint64_t> recv_member;
+    for (uint32_t i = 0; i < cnt; ++i) {
+      const int od = static_cast<int>(replaced[i] / n), os = static_cast<int>(donors[i] / n);
+      if (od == os || (od != c.rank && os != c.rank)) continue;
+      ops.push_back(P2P{os == c.rank ? od : os, os == c.rank, nullptr, blob});
+      recv_member.push_back(os == c.rank ? ~0ull : replaced[i] - p->member_offset);
+    }
+    if (!ops.empty()) {
+      p->pbt_blob.alloc(ops.size() * blob);
+      for (size_t i = 0; i < ops.size(); ++i) ops[i].dev = p->pbt_blob.p + i * blob;
+      // exports (stream-ordered copies of the donors' rows)
+      for (uint32_t i = 0, k = 0; i < cnt; ++i) {
+        const int od = static_cast<int>(replaced[i] / n), os = static_cast<int>(donors[i] / n);
+        if (od == os || (od != c.rank && os != c.rank)) continue;
+        if (os == c.rank) {
+          const int erc = pbrl_export_member(pop, donors[i] - p->member_offset, ops[k].dev);
+          if (erc != PBRL_OK) PBRL_THROW(erc, g_last_error);
+        }
+        ++k;
+      }
+      c.exchange(ops, p->stream);
+      for (size_t k = 0; k < ops.size(); ++k) {
+        if (ops[k].send) continue;
+        const int irc = pbrl_import_member(pop, recv_member[k], ops[k].dev);
+        if (irc != PBRL_OK) PBRL_THROW(irc, g_last_error);
+      }
+    }
+    // local pairs + optimiser / delay resets of the local receivers
+    const int arc = pbrl_pbt_apply(pop, replaced, donors, cnt);
+    if (arc != PBRL_OK) PBRL_THROW(arc, g_last_error);
+    // 4. hyper re-draw in lock-step: every rank draws for every replaced member
+    Seq rng{rng_key, *rng_next};
+    const uint64_t lo = p->member_offset, hi = lo + n;
+    for (uint32_t i = 0; i < cnt; ++i) {
+      double h[8];
+      prior_draw(p->algo, rng, h);
+      if (replaced[i] >= lo && replaced[i] < hi) {
+        const int nf = p->algo == PBRL_ALGO_TD3 ? 8 : 7;
+        for (int f = 0; f < nf; ++f) p->hyper[f][replaced[i] - lo] = h[f];
+      }
+    }
+    *rng_next = rng.next;
+    p->upload_hyper();
+    p->sync();
+    *count = cnt;
+    if (exchange_ms) exchange_ms[0] = ms(t0, t1), exchange_ms[1] = ms(t1, t2), exchange_ms[2] = ms(t2, clk::now());
+  });
+  return rc;
+}
+
+
+// ---------------------------------------------------------------- member state copy (a22)
+// slice_member / set_member for whole states (algos.hpp:425-464, :839-886): every network, the
+// Adam moments and step counters, steps / streams, delay_acc (TD3) or the temperature and its
+// optimiser (SAC), and the member's hypers.  dst and src may be different populations (a
+// population and one of its singletons) of the same algorithm and shapes.
+int pbrl_copy_member_state(pbrl_pop* dst_pop, uint64_t dm, pbrl_pop* src_pop, uint64_t sm) {
+  return guarded([&] {
+    Pop* s = P(src_pop);
+    Pop* d = P(dst_pop);
+    check_member(s, sm, "copy_member_state (source)");
+    check_member(d, dm, "copy_member_state (destination)");
+    if (s->algo != d->algo || s->ds != d->ds || s->da != d->da || s->hidden != d->hidden ||
+        s->bound != d->bound)
+      PBRL_THROW(PBRL_E_SHAPE, "copy_member_state: populations differ in algorithm or shapes");
+    s->sync();
+    cudaStream_t st = d->stream;
+    auto cp = [&](void* to, const void* from, size_t bytes) {
+      CUDA_CHECK(cudaMemcpyAsync(to, from, bytes, cudaMemcpyDefault, st));
+    };
+    for (int net = 0; net < 6; ++net) {
+      if (net == PBRL_NET_POLICY_TARGET && s->algo != PBRL_ALGO_TD3) continue;
+      cp(d->net_row(net, dm), s->net_row(net, sm), d->net_shape(net).P * 4);
+    }
+    for (auto pr : {std::make_pair(&d->pol_m, &s->pol_m), std::make_pair(&d->pol_v, &s->pol_v)})
+      cp(pr.first->p + dm * d->pol.stride, pr.second->p + sm * s->pol.stride, d->pol.P * 4);
+    for (auto pr : {std::make_pair(&d->cri_m, &s->cri_m), std::make_pair(&d->cri_v, &s->cri_v)})
+      for (int c = 0; c < 2; ++c)
+        cp(pr.first->p + (c * d->n + dm) * d->cri.stride,
+           pr.second->p + (c * s->n + sm) * s->cri.stride, d->cri.P * 4);
+    cp(d->t_pol.p + dm, s->t_pol.p + sm, 8);
+    cp(d->t_cri.p + dm, s->t_cri.p + sm, 8);
+    cp(d->t_cri.p + d->n + dm, s->t_cri.p + s->n + sm, 8);
+    cp(d->steps.p + dm, s->steps.p + sm, 8);
+    cp(d->streams.p + dm, s->streams.p + sm, 8);
+    if (s->algo == PBRL_ALGO_TD3) {
+      cp(d->delay_acc.p + dm, s->delay_acc.p + sm, 8);
+      if (d->delay_host.size() != static_cast<size_t>(d->n)) d->delay_host.assign(d->n, 0.0);
+      d->delay_host[dm] = s->delay_host.size() > sm ? s->delay_host[sm] : 0.0;
+    } else {
+      cp(d->log_alpha.p + dm, s->log_alpha.p + sm, 4);
+      cp(d->alpha_m.p + dm, s->alpha_m.p + sm, 4);
+      cp(d->alpha_v.p + dm, s->alpha_v.p + sm, 4);
+      cp(d->t_alpha.p + dm, s->t_alpha.p + sm, 8);
+    }
+    for (size_t f = 0; f < d->hyper.size(); ++f) d->hyper[f][dm] = s->hyper[f][sm];
+    d->upload_hyper();
+    d->t_bound = std::max(d->t_bound, s->t_bound);
+    d->weights_dirty = true;
+    d->last_wrote_weights = true;
+    d->sync();
   });
 }
 

@@ -205,6 +205,7 @@ struct Pop {
   // PBT scratch
   DBuf<double> pbt_fit;
   DBuf<uint64_t> pbt_order, pbt_rep, pbt_don, pbt_src, pbt_dst;
+  DBuf<float> pbt_blob;  // staging of cross-shard exploit copies (pbrl_pbt_evolve_sharded)
 
   explicit Pop(const pbrl_pop_desc& d);
   ~Pop();

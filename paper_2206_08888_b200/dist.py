@@ -1,5 +1,11 @@
-"""Population sharding across GPUs: the PBT exchange step (evolve.hpp:169-213) over
-torch.distributed (NCCL over NVLink/NVSwitch on the B200 box; gloo in the CPU tests).
+"""Population sharding across GPUs: the PBT exchange step (evolve.hpp:169-213).
+
+Product path: ``Comm`` + ``NativeShardedPBT`` -- the exchange runs inside libpbrl_b200.so
+(``pbrl_pbt_evolve_sharded``) over NCCL (``Comm.nccl``, NVLink / NVSwitch) or over a host
+transport the caller supplies (``Comm.host``: torch.distributed, e.g. gloo, for ranks that share
+one GPU).  ``ShardedPBT`` below is the same protocol written with torch.distributed collectives
+around the per-step C-ABI pieces (plan / apply / member blobs); the CPU tests use it with host
+shards to pin the protocol without a GPU.
 
 Each rank owns the contiguous member block [offset, offset + n_local) of an n_total population,
 with RNG streams keyed by GLOBAL member id, so a shard computes exactly what the unsharded
@@ -24,7 +30,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from . import _lib
-from .errors import NotReadyError
+from .errors import NotReadyError, PbrlError
 from .pbrl import (EvolvePlan, PBTState, RngSequence, member_blob_size, export_member,
                    import_member)
 
@@ -151,3 +157,126 @@ class ShardedPBT:
                 pbt_local.returns[dst - lo].clear()
         pbt_local.steps_since_evolve = 0
         return EvolvePlan(list(replaced), list(donors))
+
+
+# ---------------------------------------------------------------- native exchange (C ABI)
+class Comm:
+    """A pbrl_comm handle: the transport of pbrl_pbt_evolve_sharded."""
+
+    def __init__(self, handle, rank: int, world: int, kind: str, keep=()):
+        self.handle, self.rank, self.world, self.kind = handle, rank, world, kind
+        self._keep = keep  # ctypes callbacks must outlive the handle
+
+    @staticmethod
+    def nccl(device: int, group=None) -> "Comm":
+        """NCCL communicator over the ranks of `group` (torch.distributed distributes the id)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = [None]
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            _lib.call("pbrl_nccl_unique_id", buf, 128)
+            uid[0] = buf.raw
+        dist.broadcast_object_list(uid, src=dist.get_global_rank(group, 0) if group else 0,
+                                   group=group)
+        h = C.c_void_p()
+        idb = C.create_string_buffer(uid[0], 128)
+        _lib.call("pbrl_comm_create_nccl", idb, rank, world, device, C.byref(h))
+        return Comm(h, rank, world, "nccl")
+
+    @staticmethod
+    def host(device: int, group=None) -> "Comm":
+        """Host transport over torch.distributed (any backend with CPU tensors, e.g. gloo):
+        the library stages the member blobs through host memory around these callbacks."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def allgather(_ctx, send, count, recv):
+            try:
+                src = torch.from_numpy(np.ctypeslib.as_array(send, (count,)).copy())
+                out = torch.from_numpy(np.ctypeslib.as_array(recv, (world * count,)))
+                parts = list(out.view(world, count).unbind(0))
+                gathered = [torch.empty_like(src) for _ in range(world)]
+                dist.all_gather(gathered, src, group=group)
+                for dst, g in zip(parts, gathered):
+                    dst.copy_(g)
+                return 0
+            except Exception:  # pragma: no cover - reported as PBRL_E_NCCL
+                return 1
+
+        def exchange(_ctx, ops, n_ops):
+            try:
+                reqs = []
+                for i in range(n_ops):
+                    op = ops[i]
+                    t = torch.from_numpy(np.ctypeslib.as_array(op.buf, (op.floats,)))
+                    peer = dist.get_global_rank(group, op.peer) if group else op.peer
+                    fn = dist.isend if op.is_send else dist.irecv
+                    reqs.append(dist.P2POp(fn, t, peer, group))
+                if reqs:
+                    for r in dist.batch_isend_irecv(reqs):
+                        r.wait()
+                return 0
+            except Exception:  # pragma: no cover
+                return 1
+
+        ag, ex = _lib.ALLGATHER_FN(allgather), _lib.EXCHANGE_FN(exchange)
+        ops = _lib.CommOps(None, ag, ex)
+        h = C.c_void_p()
+        _lib.call("pbrl_comm_create_host", C.byref(ops), rank, world, device, C.byref(h))
+        return Comm(h, rank, world, "host", keep=(ag, ex, ops))
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.lib().pbrl_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NativeShardedPBT:
+    """pbt_evolve_trainer for one shard of a population, exchange inside the library
+    (pbrl_pbt_evolve_sharded): fitness all-gather, identical device plan on every rank,
+    cross-rank member blobs point-to-point, resets + lock-step hyper re-draws on the owner."""
+
+    def __init__(self, pop, hyper, comm: Comm, truncation_fraction: float = 0.3):
+        self.pop, self.hyper, self.comm = pop, hyper, comm
+        self.trunc = truncation_fraction
+        self.last_exchange_ms = None
+
+    def evolve(self, pbt_local: PBTState, rng: RngSequence) -> Optional[EvolvePlan]:
+        pop = self.pop
+        n_total = pop.n * self.comm.world
+        if n_total < 4:
+            return None
+        ready = pbt_local.every_member_scored()
+        fit = np.ascontiguousarray(pbt_local.fitness() if ready else np.zeros(pop.n), np.float64)
+        rep = np.zeros(n_total, np.uint64)
+        don = np.zeros(n_total, np.uint64)
+        nxt = C.c_uint64(rng.next)
+        cnt = C.c_uint32()
+        ms = np.zeros(3, np.float64)
+        pop._sync_hyper(self.hyper)
+        _lib.call("pbrl_pbt_evolve_sharded", pop.handle, self.comm.handle,
+                  fit.ctypes.data_as(_lib.f64p), 1 if ready else 0, self.trunc, rng.stream.key,
+                  C.byref(nxt), rep.ctypes.data_as(_lib.u64p), don.ctypes.data_as(_lib.u64p),
+                  C.byref(cnt), ms.ctypes.data_as(_lib.f64p))
+        rng.next = nxt.value
+        self.last_exchange_ms = dict(fitness_allgather=ms[0], plan=ms[1], copies_and_resets=ms[2])
+        c = cnt.value
+        plan = EvolvePlan([int(x) for x in rep[:c]], [int(x) for x in don[:c]])
+        # the re-drawn hypers live in the library: mirror them into the host object
+        for f in pop.FIELDS:
+            setattr(self.hyper, f, [float(v) for v in pop.get_hyper(f)])
+        pop._hyper_cache = None
+        lo = pop.member_offset
+        for dst in plan.replaced:
+            if lo <= dst < lo + pop.n:
+                pbt_local.returns[dst - lo].clear()
+        pbt_local.steps_since_evolve = 0
+        return plan

@@ -500,6 +500,26 @@ def make_sac_state(n, obs_dim, act_dim, hidden, action_bound, seed, mode="indepe
                     member_offset, n_global, mode)
 
 
+def slice_member(st: _Population, i: int) -> _Population:
+    """slice_member for states (algos.hpp:425-447, :839-865): member i as a population of one on
+    the same device -- every network, Adam moments and counters, steps, stream id, delay_acc
+    (TD3) or the temperature state (SAC), and the member's hypers."""
+    if not 0 <= i < st.n:
+        raise UsageError(f"slice_member: index {i} out of range for {st.n} members")
+    one = type(st)(1, st.obs_dim, st.act_dim, st.hidden, st._action_bound, st.seed, st.precision,
+                   st.device, st.member_offset + i, st.n_global)
+    _lib.call("pbrl_copy_member_state", one.handle, 0, st.handle, i)
+    return one
+
+
+def set_member(st: _Population, i: int, sub: _Population) -> None:
+    """set_member for states (algos.hpp:449-464, :867-886): member 0 of `sub` into member i."""
+    if sub.n != 1:
+        raise UsageError("set_member: the source must be a population of one")
+    _lib.call("pbrl_copy_member_state", st.handle, i, sub.handle, 0)
+    st._hyper_cache = None
+
+
 def td3_update_step(st: Td3State, batch: TransitionBatch, hyper: Td3Hyper, hook=None,
                     policy_member_mask=None) -> None:
     """td3_update_step (algos.hpp:351-422)."""

@@ -3,17 +3,14 @@ gradients and weights after K update steps within a stated fp32-relative toleran
 
 Metric: per-step losses, relative error; parameters compared as
 weight DELTAS (w_K - w_0), relative L2 error ||d_dev - d_ref|| / ||d_ref||, because Adam moves
-every weight by ~lr per step so raw weights hide errors.  Stated tolerances:
-  critic / policy losses        rel err <= 5e-2 per step
-  weight deltas after K steps   rel-L2  <= 0.10 (critics), 0.10 (policy)
-The TF32 operand rounding (2^-11 relative) is ~2^12 x fp32's, and Adam's normalisation turns
-gradient-sign flips of near-zero gradient entries into O(lr) differences; the bounds below are
-~2-4x the values measured on B200 (TD3: losses 2.9e-2, deltas 2.4-4.5e-2) for these configurations.
+every weight by ~lr per step so raw weights hide errors.  Tolerances are derived per case on the
+CPU, not calibrated on the GPU: 3x the error of the oracle run with TF32-rounded tensor-core
+operands against the exact fp32 oracle (oracle/derive_tolerances.py -> tests/golden/tolerances.json).
 """
 import numpy as np
 import pytest
 
-from helpers import TD3_NETS, SAC_NETS, raw_at, rel_delta_err, to_batch
+from helpers import TD3_NETS, check_parity, to_batch
 
 pytestmark = pytest.mark.gpu
 
@@ -24,45 +21,11 @@ def pb(cuda):
     return pb
 
 
-def _compare(pb, ora, algo, n, hidden, B, K, seed=7, ds=17, da=6, precision="tf32"):
-    make = pb.make_td3_state if algo == "td3" else pb.make_sac_state
-    st = make(n, ds, da, hidden, 1.0, seed, precision=precision)
-    ref = (ora.td3 if algo == "td3" else ora.sac)(n, ds, da, hidden, 1.0, seed)
-    hy = pb.Td3Hyper.defaults(n) if algo == "td3" else pb.SacHyper.defaults(n, da)
-    if algo == "td3":
-        hy.policy_delay_ratio = [1.0] * n
-    oh = {f: list(getattr(hy, f)) for f in hy.FIELDS}
-    nets = TD3_NETS if algo == "td3" else SAC_NETS
-    w0 = {net: ref.get_net(net).copy() for net in nets}
-    raw = ora.synthetic_batches(K, n, B, ds, da, seed)
-    lerr = []
-    for k in range(K):
-        upd = pb.td3_update_step if algo == "td3" else pb.sac_update_step
-        upd(st, to_batch(pb, raw, k), hy)
-        dl = np.stack(st.last_losses())
-        rl = ref.step(raw_at(raw, k), oh)
-        lerr.append(np.abs(dl - rl) / np.maximum(np.abs(rl), 1e-3))
-    werr = {net: rel_delta_err(st.params(net), ref.get_net(net), w0[net]) for net in nets}
-    return np.max(lerr, axis=(1, 2)), werr
-
-
-@pytest.mark.parametrize("algo", ["td3", "sac"])
-def test_tf32_matches_oracle_within_tolerance(pb, ora, algo):
-    lerr, werr = _compare(pb, ora, algo, 4, [256, 256], 256, 6)
-    print(f"\n{algo} tf32: max loss rel err per step {np.round(lerr, 6).tolist()}")
-    print(f"{algo} tf32: weight-delta rel-L2 {{{', '.join(f'{k}: {v:.4f}' for k, v in werr.items())}}}")
-    assert lerr.max() <= 5e-2
-    for net, e in werr.items():
-        assert e <= 0.10, (net, e)
-
-
-@pytest.mark.parametrize("algo,ds,da", [("td3", 11, 3), ("sac", 9, 8)])
-def test_tf32_other_action_widths(pb, ora, algo, ds, da):
-    """Fused output widths outside the specialised 1 / 6 / 12 (generic runtime-guarded path)."""
-    lerr, werr = _compare(pb, ora, algo, 3, [256, 256], 128, 4, seed=11, ds=ds, da=da)
-    assert lerr.max() <= 5e-2
-    for net, e in werr.items():
-        assert e <= 0.10, (net, e)
+@pytest.mark.parametrize("case", ["A_td3_pop4", "A_sac_pop4", "W_td3_da3", "W_sac_da8"])
+def test_tf32_matches_oracle_within_derived_tolerance(pb, ora, case):
+    """Config-A shapes and fused output widths outside 1 / 6 / 12 (generic runtime-guarded
+    path); tolerances derived on the CPU (tests/golden/tolerances.json)."""
+    check_parity(pb, ora, case, "tf32")
 
 
 def test_tf32_uses_tensor_cores_and_is_deterministic(pb, ora):
