@@ -389,13 +389,17 @@ class _Population:
         ext.wait_stream(torch.cuda.current_stream(torch.device("cuda", self.device)))
         return ext
 
-    @staticmethod
-    def _device_call_end(ext, keep):
+    def _device_call_end(self, ext, keep):
         """The library runs asynchronously: tensors it reads (incl. .contiguous() temporaries)
-        must not return to torch's caching allocator before the library stream is done."""
-        for x in keep:
-            if hasattr(x, "record_stream"):
-                x.record_stream(ext)
+        must not be reused by torch's caching allocator before the library stream is done.
+        torch's current stream waits for the library stream, so any later reuse of that memory
+        (allocations are ordered on the stream that freed them) comes after the library's reads.
+        (record_stream on the library stream would tie the tensors' frees to a stream that dies
+        with the population.)"""
+        import torch
+        if ext is not None:
+            torch.cuda.current_stream(torch.device("cuda", self.device)).wait_stream(ext)
+        del keep
 
     def _update(self, batches: Sequence[TransitionBatch], mask=None,
                 return_losses: bool = False) -> Optional[np.ndarray]:

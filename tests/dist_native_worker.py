@@ -52,7 +52,7 @@ def main():
     n = a.n_total // a.world
     off = a.rank * n
     make = pb.make_td3_state if a.algo == "td3" else pb.make_sac_state
-    st = make(n, 5, 2, [16, 16], 1.0, 60, precision=a.precision, device=0, member_offset=off,
+    st = make(n, 5, 2, [32, 32], 1.0, 60, precision=a.precision, device=0, member_offset=off,
               n_global=a.n_total)
     hy = pb.Td3Hyper.defaults(n) if a.algo == "td3" else pb.SacHyper.defaults(n, 2)
     gb = pb.make_synthetic_batches(4, a.n_total, 32, 5, 2, 9)

@@ -52,7 +52,7 @@ def _run_ranks(tmp_path, world, extra):
 def _single_process(pb, algo, n_total, precision):
     from dist_native_worker import scenario
     make = pb.make_td3_state if algo == "td3" else pb.make_sac_state
-    st = make(n_total, 5, 2, [16, 16], 1.0, 60, precision=precision)
+    st = make(n_total, 5, 2, [32, 32], 1.0, 60, precision=precision)
     hy = pb.Td3Hyper.defaults(n_total) if algo == "td3" else pb.SacHyper.defaults(n_total, 2)
     batches = pb.make_synthetic_batches(4, n_total, 32, 5, 2, 9)
     pbt = pb.PBTState(n_total)

@@ -22,8 +22,8 @@ def _slice_batch(pb, b, m):
 
 @pytest.mark.parametrize("precision", ["ffma32", "bf16"])
 def test_td3_vectorized_equals_singletons(pb, precision):
-    n, ds, da, b = 3, 4, 2, 8
-    st = pb.make_td3_state(n, ds, da, [8, 8], 1.0, 11, precision=precision)
+    n, ds, da, b = 3, 4, 2, 32
+    st = pb.make_td3_state(n, ds, da, [32, 32], 1.0, 11, precision=precision)
     hy = pb.Td3Hyper.defaults(n)
     hy.policy_delay_ratio = [0.5, 1.0, 0.3]  # distinct delays per member
     hy.critic_lr = [3e-4, 1e-3, 3e-4]
@@ -65,14 +65,16 @@ def test_sac_vectorized_equals_singletons(pb):
 
 def test_set_member_round_trip_moves_the_whole_state(pb):
     """set_member(dst, i, slice_member(src, j)): member i of dst becomes member j of src, incl.
-    its stream id (target noise keyed by it), so the next updates agree bit for bit."""
+    its stream id and step count (the target noise is keyed by them and by the state seed, which
+    is state-level: both states share it), so the next updates agree bit for bit."""
     n, ds, da, b = 4, 5, 2, 16
     src = pb.make_td3_state(n, ds, da, [16, 16], 1.0, 31)
-    dst = pb.make_td3_state(n, ds, da, [16, 16], 1.0, 32)
+    dst = pb.make_td3_state(n, ds, da, [16, 16], 1.0, 31)
     hy = pb.Td3Hyper.defaults(n)
     batches = pb.make_synthetic_batches(6, n, b, ds, da, 33)
     for bt in batches[:3]:
         pb.td3_update_step(src, bt, hy)
+    pb.td3_update_step(dst, pb.make_synthetic_batches(1, n, b, ds, da, 34)[0], hy)
     pb.set_member(dst, 1, pb.slice_member(src, 2))
     for net in TD3_NETS:
         assert bits_equal(dst.flatten_member(net, 1), src.flatten_member(net, 2)), net
