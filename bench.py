@@ -51,9 +51,19 @@ def parse():
     ap.add_argument("--pop", type=int, default=None, help="override the total population")
     ap.add_argument("--precision", default=os.environ.get("PBRL_PRECISION", "bf16"),
                     choices=["ffma32", "bf16", "tf32"])
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every GPU runs the config's population (members keyed by global "
-                         "id, total = pop x N); strong: the config's population split over N")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (default, BASELINE config D: pop 80 sharded over N GPUs): the "
+                         "config's population split over the N ranks; weak: every rank runs the "
+                         "config's population (members keyed by global id, total = pop x N)")
+    ap.add_argument("--memory-budget-gib", type=float, default=None,
+                    help="bench_update's memory budget (bench.hpp:35,141-147): ResourceError when "
+                         "the estimated device footprint exceeds it (default: free HBM)")
+    ap.add_argument("--pbt-interval", type=int, default=1000,
+                    help="updates between PBT exchanges; one exchange (fitness all-gather, device "
+                         "plan, exploit copies, resets) is timed and amortised over it")
+    ap.add_argument("--reps", type=int, default=5,
+                    help="the K timed steps are split into this many equal repetitions for the "
+                         "median / IQR (bench.hpp:184-200)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-json", default=None, help="write the per-class profile here")
@@ -101,7 +111,7 @@ def td3_member_update_work(hidden, batch, f=0.5, ds=OBS, da=ACT):
 
 # ------------------------------------------------------------------ clocks during the timed region
 class Clocks:
-    """Samples SM clock and throttle reasons through NVML every 5 ms while the timed region
+    """Samples SM clock and throttle reasons through NVML every 1 ms while the timed region
     runs (the recipe's nvidia-smi clocks line, at a rate that resolves sub-second regions)."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
@@ -134,7 +144,7 @@ class Clocks:
                 self.rows.append((sm, rs))
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
     def __exit__(self, *a):
         self.stop.set()
@@ -147,7 +157,7 @@ class Clocks:
         sm = sorted(r[0] for r in self.rows)
         reasons = sorted({k for _, rs in self.rows for k, bit in self.REASONS.items() if rs & bit})
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max, "reasons": reasons,
-                "samples": len(self.rows), "source": "nvml 5 ms"}
+                "samples": len(self.rows), "source": "nvml 1 ms"}
 
 
 # ------------------------------------------------------------------ CPU baseline (reference build)
@@ -210,10 +220,41 @@ def config_dict(args, cfg, pop, l2, gpus):
 
 
 # ------------------------------------------------------------------ our arm
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: re-run this script under torch.distributed.run with N
+    ranks (one per GPU, rendezvous on 127.0.0.1); rank 0's JSON line is passed through."""
+    import socket
+    import subprocess
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def estimated_bytes(cfg, n, nb, precision):
+    """bench_estimated_bytes (bench.cpp:37-56) for the device layout: per member the fp32
+    parameters, targets, Adam moments and gradients of every network (+ bf16 operand copies),
+    the nb resident synthetic batches, and the activation scratch of one step."""
+    hid = cfg["hidden"]
+    pd, cd = [OBS] + hid + [ACT], [OBS + ACT + 1] + hid + [1]
+    P = lambda d: sum(d[i] * d[i + 1] + d[i + 1] for i in range(len(d) - 1))
+    PP = P(pd) + (P(pd) if cfg["algo"] == "sac" else 0)
+    per_param = 5 * 4 + (4 if precision == "bf16" else 0)
+    state = n * (PP + 2 * P(cd)) * per_param
+    batches = nb * n * cfg["batch"] * (2 * OBS + ACT + 2) * 4
+    scratch = n * cfg["batch"] * sum(hid) * 4 * 12
+    return state + batches + scratch
+
+
 def main():
     args = parse()
     cfg = dict(CONFIGS[args.config])
     pop = args.pop or cfg["pop"]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -223,10 +264,11 @@ def main():
 
     import torch
     import torch.distributed as dist
-    # PBRL_BENCH_BACKEND=gloo (tests only): run the sharded path with several ranks on however
-    # many GPUs exist (ranks share devices round-robin), collectives on the host
-    backend = os.environ.get("PBRL_BENCH_BACKEND", "nccl")
-    gpu = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    ndev = max(1, torch.cuda.device_count())
+    # one rank per GPU over NCCL; with fewer GPUs than ranks (tests, or PBRL_BENCH_BACKEND=gloo)
+    # the ranks share devices round-robin and the collectives run on the host (gloo)
+    backend = os.environ.get("PBRL_BENCH_BACKEND", "nccl" if world <= ndev else "gloo")
+    gpu = local % ndev
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
     if world > 1:
@@ -236,6 +278,7 @@ def main():
             dist.init_process_group(backend)
     import paper_2206_08888_b200 as pb
     from paper_2206_08888_b200 import _lib
+    from paper_2206_08888_b200.errors import ResourceError
 
     if args.scaling == "weak":  # every rank: the config's population, global member ids
         n = pop
@@ -245,30 +288,37 @@ def main():
             raise SystemExit(f"population {pop} does not split over {world} GPUs")
         n = pop // world
     off = rank * n
+    nb = 50  # bench_update's k = 50 distinct batches (bench.hpp:151), resident in HBM
+    need = estimated_bytes(cfg, n, nb, args.precision)
+    budget = (args.memory_budget_gib * 2 ** 30 if args.memory_budget_gib
+              else torch.cuda.mem_get_info(dev)[0])
+    if need > budget:
+        raise ResourceError(f"bench_update: population of {n} needs an estimated {need} bytes, "
+                            f"over the budget of {int(budget)}")
     make = pb.make_td3_state if cfg["algo"] == "td3" else pb.make_sac_state
     st = make(n, OBS, ACT, cfg["hidden"], 1.0, SEED, precision=args.precision, device=gpu,
               member_offset=off, n_global=pop)
     hy = pb.Td3Hyper.defaults(n) if cfg["algo"] == "td3" else pb.SacHyper.defaults(n, ACT)
     st._sync_hyper(hy)
-    L = _lib.lib()
 
     # synthetic inputs in HBM: 50 distinct global batches (bench_update's k=50), local slice
-    nb = 50
     gb = pb.make_synthetic_batches(nb, pop, cfg["batch"], OBS, ACT, SEED, device=dev)
     batches = [pb.TransitionBatch(*[x[off:off + n].contiguous() for x in
                                     (b.s, b.a, b.r, b.s2, b.done)]) for b in gb]
     del gb
-    structs = [_lib.Batch(*[x.data_ptr() for x in (b.s, b.a, b.r, b.s2, b.done)])
-               for b in batches]
     B = cfg["batch"]
 
-    def run(i):
-        arr = (_lib.Batch * 1)(structs[i % nb])
-        _lib.call("pbrl_update_batches_device", st.handle, arr, 1, B, None)
+    def make_runner(p, bl):
+        structs = [_lib.Batch(*[x.data_ptr() for x in (b.s, b.a, b.r, b.s2, b.done)])
+                   for b in bl]
 
-    sp = C.c_void_p()
-    _lib.call("pbrl_get_stream", st.handle, C.byref(sp))
-    lstream = torch.cuda.ExternalStream(sp.value, device=dev)
+        def run(i):
+            arr = (_lib.Batch * 1)(structs[i % len(structs)])
+            _lib.call("pbrl_update_batches_device", p.handle, arr, 1, B, None)
+        return run
+
+    run = make_runner(st, batches)
+    lstream = st.lib_stream()
 
     state_bytes = st.device_bytes()
     in_bytes = sum(x.numel() * 4 for b in batches for x in (b.s, b.a, b.r, b.s2, b.done))
@@ -290,24 +340,29 @@ def main():
         run(i)
     st.synchronize()
 
-    # ---- timed region: K steps, device time on the library stream, max over ranks
+    # ---- timed region: K steps, device time on the library stream, max over ranks.  The K
+    # steps are recorded as `reps` equal repetitions (bench.hpp:184-200: median / IQR).
     K = args.steps
+    R = max(1, min(args.reps, K))
+    edges = [round(K * j / R) for j in range(R + 1)]
     launches0 = st.launch_count()
     with Clocks(gpu) as clk:
         barrier()
         torch.cuda.synchronize(dev)
         st.synchronize()
-        total_ms = 0.0
+        step_ms = []
         if not flush:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(lstream)
-            for i in range(K):
-                run(args.warmup + i)
-            e1.record(lstream)
-            e1.synchronize()
-            total_ms = e0.elapsed_time(e1)
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(R + 1)]
+            evs[0].record(lstream)
+            for j in range(R):
+                for i in range(edges[j], edges[j + 1]):
+                    run(args.warmup + i)
+                evs[j + 1].record(lstream)
+            evs[-1].synchronize()
+            rep_ms = [evs[j].elapsed_time(evs[j + 1]) for j in range(R)]
+            total_ms = sum(rep_ms)
         else:
-            evs = []
+            pairs = []
             for i in range(K):
                 with torch.cuda.stream(lstream):
                     flush_buf.fill_(float(i))  # evict L2 between steps (outside the events)
@@ -315,15 +370,27 @@ def main():
                 a.record(lstream)
                 run(args.warmup + i)
                 b.record(lstream)
-                evs.append((a, b))
+                pairs.append((a, b))
             st.synchronize()
-            total_ms = sum(a.elapsed_time(b) for a, b in evs)
+            step_ms = [a.elapsed_time(b) for a, b in pairs]
+            rep_ms = [sum(step_ms[edges[j]:edges[j + 1]]) for j in range(R)]
+            total_ms = sum(step_ms)
         st.synchronize()
         torch.cuda.synchronize(dev)
         barrier()
     launches = st.launch_count() - launches0
     total_ms = max_over_ranks(total_ms)
     value = pop * K / (total_ms / 1e3)
+    per_step = sorted(r / max(1, edges[j + 1] - edges[j]) for j, r in enumerate(rep_ms))
+
+    def quantile(v, q):
+        x = q * (len(v) - 1)
+        lo = int(x)
+        hi = min(lo + 1, len(v) - 1)
+        return v[lo] + (v[hi] - v[lo]) * (x - lo)
+    reps = {"n": R, "steps_per_rep": K // R, "median_ms_per_step": quantile(per_step, 0.5),
+            "iqr_ms_per_step": quantile(per_step, 0.75) - quantile(per_step, 0.25),
+            "note": "this rank's repetitions; value / ms_per_step use the max over ranks"}
 
     # ---- event-instrumented pass over the same workload: per-kernel-class roofline
     kp = min(K, 10) if K >= 2 else 1
@@ -359,6 +426,11 @@ def main():
                  "avg_launch_ms": avg_ms, "peak_source": pk["src"],
                  "algorithmic_flops_per_launch": dc["flops"] / max(1, dc["launches"]),
                  "algorithmic_bytes_per_launch": dc["bytes"] / max(1, dc["launches"])})
+    # HBM fraction of every byte-bound class (north_star: gather and Adam against HBM peak)
+    classes_hbm = {k: {"gbs": c["bytes"] / (c["ms"] / 1e3) / 1e9 if c["ms"] > 0 else None,
+                       "frac": (c["bytes"] / (c["ms"] / 1e3) / 1e9) / pk["hbm"]
+                       if c["ms"] > 0 else None}
+                   for k, c in cls.items() if k in ("adam_polyak", "gather_pack", "elementwise")}
     # whole-step roofline: T_roof = max(n F / P_tc, n Bytes / BW_hbm)
     step_roof = None
     if cfg["algo"] == "td3":
@@ -412,12 +484,74 @@ def main():
                "d2h_bytes_per_step": 3 * n * 8, "steps": ke, "steps_per_call": KC,
                "host_wall_value": pop * ke / wall}
 
+    # ---- config B: vectorization overhead, t(pop 10) / t(pop 1) per step (target <= 1.5)
+    vec = None
+    if args.config == "B" and world == 1:
+        one = make(1, OBS, ACT, cfg["hidden"], 1.0, SEED, precision=args.precision, device=gpu)
+        one._sync_hyper(pb.Td3Hyper.defaults(1))
+        b1 = [pb.TransitionBatch(*[x[:1].contiguous() for x in (b.s, b.a, b.r, b.s2, b.done)])
+              for b in batches]
+        run1 = make_runner(one, b1)
+        for i in range(args.warmup):
+            run1(i)
+        one.synchronize()
+        ls1 = one.lib_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ls1)
+        for i in range(K):
+            run1(args.warmup + i)
+        e1.record(ls1)
+        e1.synchronize()
+        t1 = e0.elapsed_time(e1) / K
+        vec = {"t_pop1_ms_per_step": t1, "t_pop10_ms_per_step": total_ms / K,
+               "ratio": (total_ms / K) / t1, "target": 1.5}
+
+    # ---- PBT exchange, timed separately: fitness all-gather over
+    # the ranks, identical device plan, exploit copies (cross-rank member blobs over NCCL,
+    # same-rank on device), optimiser resets and hyper re-draws; amortised over pbt_interval
+    # updates.  Returns are synthetic: record_return from RngStream::of(7, m, kGeneric, event).
+    pbt = None
+    if pop >= 4:
+        from paper_2206_08888_b200.dist import Comm, NativeShardedPBT
+        comm = (Comm.nccl(device=gpu) if (world > 1 and backend == "nccl")
+                else Comm.host(device=gpu) if world > 1 else None)
+        if comm is None:  # single rank: a one-rank host transport (no communication)
+            comm = _solo_comm(gpu)
+        pstate = pb.PBTState(n)
+        rng = pb.RngSequence(SEED, 0, "kDonorChoice")
+        ex = NativeShardedPBT(st, hy, comm)
+        times, parts, plans = [], [], []
+        for ev in range(3):
+            for m in range(n):
+                g = off + m
+                pstate.record_return(m, pb.RngStream.of(SEED, g, "kGeneric", ev).uniform(0))
+            st.synchronize()
+            barrier()
+            t0 = time.perf_counter()
+            plan = ex.evolve(pstate, rng)
+            dt = (time.perf_counter() - t0) * 1e3
+            times.append(max_over_ranks(dt))
+            parts.append(ex.last_exchange_ms)
+            plans.append(plan)
+        per = pop // world if args.scaling == "strong" else n
+        cross = [sum(1 for d, s_ in zip(p.replaced, p.donors) if d // per != s_ // per)
+                 for p in plans]
+        blob = pb.pbrl.member_blob_size(st) * 4
+        med = sorted(times)[1]
+        pbt = {"ms": med, "samples_ms": times, "transport": comm.kind,
+               "breakdown_ms_rank0": parts[1], "replaced": len(plans[1].replaced),
+               "cross_rank_copies": cross[1], "blob_bytes": blob,
+               "interval_updates": args.pbt_interval,
+               "amortised_share_of_step_time": med / (args.pbt_interval * total_ms / K)}
+        comm.close()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(cfg, pop)
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "agent-updates/s", "n_gpus": world,
+        ngpu = min(world, ndev) if backend != "nccl" else world
+        line = {"metric": METRIC, "value": value, "unit": "agent-updates/s", "n_gpus": ngpu,
                 "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K,
                 "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                 "dtype": {"ffma32": "f32", "bf16": "bf16", "tf32": "tf32"}[args.precision],
@@ -426,13 +560,37 @@ def main():
                                       "flushed between steps" if flush else
                                       f"inputs+state {(state_bytes + in_bytes) / 2**20:.0f} MiB "
                                       f"per GPU > L2", world),
-                "roofline": roof, "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "roofline": roof, "step_roofline": step_roof, "class_hbm": classes_hbm,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "reps": reps,
+                "pbt_exchange": pbt, "vectorization_overhead": vec,
+                "ranks": world, "backend": backend if world > 1 else None,
                 "clocks": clk.summary(), "profile": {k: {kk: round(vv, 6) if isinstance(vv, float)
                                                          else vv for kk, vv in v.items()}
                                                      for k, v in cls.items()}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _solo_comm(gpu):
+    """A one-rank host transport: the all-gather is a copy, there is nothing to exchange."""
+    import ctypes as C_
+    import numpy as np
+    from paper_2206_08888_b200 import _lib
+    from paper_2206_08888_b200.dist import Comm
+
+    def allgather(_ctx, send, count, recv):
+        np.ctypeslib.as_array(recv, (count,))[:] = np.ctypeslib.as_array(send, (count,))
+        return 0
+
+    def exchange(_ctx, ops, n_ops):
+        return 0 if n_ops == 0 else 1
+
+    ag, ex = _lib.ALLGATHER_FN(allgather), _lib.EXCHANGE_FN(exchange)
+    ops = _lib.CommOps(None, ag, ex)
+    h = C_.c_void_p()
+    _lib.call("pbrl_comm_create_host", C_.byref(ops), 0, 1, gpu, C_.byref(h))
+    return Comm(h, 0, 1, "host (single rank)", keep=(ag, ex, ops))
 
 
 if __name__ == "__main__":

@@ -630,11 +630,14 @@ bool replay_ready(Pop* p, uint64_t min_size) {
 // as fp32 rows, so it gathers with act16 = 0 (the buffers hold enough bytes for either)
 void gather(Pop* p, int B, uint64_t seed, uint64_t draw_id, int act16) {
   Replay* r = p->replay;
+  cudaEvent_t a = nullptr;
+  p->prof_begin(&a);
   launch_replay_gather(p->n, B, p->ds, p->da, p->lsa, r->rw, r->ring.p, r->cap,
                        r->mode == PBRL_REPLAY_SHARED, r->sizes.p, p->streams.p, seed, draw_id,
                        p->S.in_sa.p, p->S.in_s2a.p, p->S.sa_pi.p, p->S.r.p, p->S.d.p, act16,
                        p->stream, p->S.in_s.p, p->lsp);
   p->count_launch(1);
+  p->prof_end(a, PC_GATHER, 0.0, p->pack_bytes(B), 0);
 }
 }  // namespace
 

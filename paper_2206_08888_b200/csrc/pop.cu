@@ -427,7 +427,7 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
       s2 = S.bs2[sl].p;
       d = S.bd[sl].p;
     }
-    timed(PC_GATHER, 0.0, 0.0, 0, [&] {
+    timed(PC_GATHER, 0.0, pack_bytes(B), 0, [&] {
       launch_pack_batch(n, B, ds, da, lsa, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
                         S.d.p, act16() ? 1 : 0, stream, S.in_s.p, lsp);
     });

@@ -202,6 +202,14 @@ struct Pop {
     last_wrote_weights = cls == PC_ADAM;
   }
 
+  // algorithmic HBM bytes of one batch pack / replay gather: the transition rows read (s, a, r,
+  // s2, done: 2 ds + da + 2 floats) and the operand blocks written (critic input [s|a], target
+  // critic input s2, policy-loss critic input s, policy input s, r, done)
+  double pack_bytes(int B) const {
+    const double rows = static_cast<double>(n) * B;
+    return rows * (4.0 * (2 * ds + da + 2) + aeb() * (2.0 * ds + da + ds + ds) + 8.0);
+  }
+
   // PBT scratch
   DBuf<double> pbt_fit;
   DBuf<uint64_t> pbt_order, pbt_rep, pbt_don, pbt_src, pbt_dst;
