@@ -738,7 +738,7 @@ int pbrl_pbt_apply(pbrl_pop* pop, const uint64_t* replaced, const uint64_t* dono
       p->pbt_dst.alloc(np);
       p->pbt_src.upload(src.data(), np, p->stream);
       p->pbt_dst.upload(dst.data(), np, p->stream);
-      p->last_wrote_weights = true;
+      p->weights_written_outside();
       launch_member_copy(p->pol_p.p, p->pol.stride, p->pol.P, p->pbt_src.p, p->pbt_dst.p, np, p->stream);
       if (p->algo == PBRL_ALGO_TD3)
         launch_member_copy(p->pol_t.p, p->pol.stride, p->pol.P, p->pbt_src.p, p->pbt_dst.p, np, p->stream);
@@ -1170,7 +1170,7 @@ int pbrl_copy_member_state(pbrl_pop* dst_pop, uint64_t dm, pbrl_pop* src_pop, ui
     d->upload_hyper();
     d->t_bound = std::max(d->t_bound, s->t_bound);
     d->weights_dirty = true;
-    d->last_wrote_weights = true;
+    d->weights_written_outside();
     d->sync();
   });
 }

@@ -1045,7 +1045,10 @@ void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, doubl
 
 // Member rows start 256-byte aligned (stride = P rounded up to 64), so each row is processed as
 // float4 vectors (5 x 128-bit loads, 3-4 x 128-bit stores per thread) plus a scalar tail.
-__global__ void __launch_bounds__(256) k_adam(int n, size_t P, size_t stride,
+// __launch_bounds__(256, 4): at most 64 registers, 4 blocks (32 warps) per SM -- the occupancy
+// that keeps enough 128-bit loads in flight for this HBM-bound stream (with 112 registers and 2
+// blocks per SM the optimizer launches ran 40% longer on B200).
+__global__ void __launch_bounds__(256, 4) k_adam(int n, size_t P, size_t stride,
                                               float* __restrict__ p, float* __restrict__ mo,
                                               float* __restrict__ vo, const float* __restrict__ g,
                                               const int64_t* t, const float* corr1,

@@ -189,7 +189,7 @@ void Pop::refresh_shadows() {
   launch_to_bf16(cri_p.p, cri_p16.p, nc, stream);
   launch_to_bf16(cri_t.p, cri_t16.p, nc, stream);
   count_launch(pol_t16.p ? 4 : 3);
-  last_wrote_weights = true;
+  weights_written_outside();
   weights_dirty = false;
 }
 

@@ -1,6 +1,8 @@
 // Population object (host side of the C ABI).
 #pragma once
 
+#include <unordered_map>
+
 #include <atomic>
 #include <string>
 #include <vector>
@@ -190,7 +192,25 @@ struct Pop {
   void prof_add_gated_bytes(double bytes);
   // true when the latest kernel on the stream wrote parameters (Adam, PBT copies, init): the
   // next tcgen05 launch must not read its weight operand before the PDL wait
-  bool last_wrote_weights = true;
+  //
+  // PDL window per capture stream: kernels with PDL_ENTRY wait for their predecessor and then
+  // trigger; the tcgen05 kernels trigger early (before their wait), so their successor can start
+  // while kernels several launches back still run.  A successor may read weights before its
+  // wait (b_prefetch) only if no kernel from the last wait-then-trigger launch on (inclusive)
+  // wrote weights.  A stream's first kernel after a fork has a full dependency (window empty).
+  std::unordered_map<cudaStream_t, bool> wwin;  // true: a weight write may still be in flight
+  bool next_early_trigger = false;
+  bool tc_prefetch_ok() {
+    auto it = wwin.find(stream);
+    const bool ok = it != wwin.end() && !it->second;
+    next_early_trigger = true;
+    return ok;
+  }
+  void weights_written_outside() {  // PBT copies, set_member, init: every window dirty
+    for (auto& kv : wwin) kv.second = true;
+    wwin[stream] = true;
+  }
+  void fork_window(cudaStream_t s) { wwin[s] = false; }
 
   template <typename F>
   void timed(int cls, double flops, double bytes, int gated, F&& f) {
@@ -199,7 +219,10 @@ struct Pop {
     f();
     count_launch(1);
     prof_end(a, cls, flops, bytes, gated);
-    last_wrote_weights = cls == PC_ADAM;
+    const bool writes = cls == PC_ADAM;
+    bool& w = wwin.try_emplace(stream, true).first->second;
+    w = next_early_trigger ? (w || writes) : writes;
+    next_early_trigger = false;
   }
 
   // algorithmic HBM bytes of one batch pack / replay gather: the transition rows read (s, a, r,

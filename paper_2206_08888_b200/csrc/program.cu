@@ -75,7 +75,7 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
       a.mo_gs = ymask->mgs;
       a.mo_ld = ymask->mld;
     }
-    a.b_prefetch = last_wrote_weights ? 0 : 1;
+    a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
     timed(PC_GEMM_FWD, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
     return;
@@ -168,7 +168,7 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
     }
     a.scale = scale;
     a.active = active;
-    a.b_prefetch = last_wrote_weights ? 0 : 1;
+    a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
     timed(PC_GEMM_DX, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, false, a, stream); });
     return;
@@ -530,7 +530,7 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
             static_cast<double>(groups) * in * hdim) +
       4.0 * groups * (hdim + hdim * nout + nout) + oe * groups * B * nout +
       (keep_hidden ? groups * B * (ae * hdim + 4.0 * ((hdim + 31) / 32)) : 0.0);
-  a.b_prefetch = last_wrote_weights ? 0 : 1;
+  a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
   timed(PC_GEMM_FWD, flops, bytes, active != nullptr,
         [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
   return true;
@@ -712,7 +712,7 @@ bool Pop::gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long
   a.aux_by_member = aux.by_member;
   a.scale = scale;
   a.active = active;
-  a.b_prefetch = last_wrote_weights ? 0 : 1;
+  a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
   const double flops = 2.0 * B * groups * (static_cast<double>(Hn) * H + H * da);
   const double bytes = eb * groups * (static_cast<double>(B) * Hn + static_cast<double>(Hn) * H) +
                        4.0 * groups * (B * ((H + 31) / 32) + H * da + 2.0 * B * da);
@@ -789,6 +789,7 @@ void Pop::capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body) 
   CUDA_CHECK(cudaStreamBeginCaptureToGraph(cap, bg, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal));
   std::swap(stream, cap);
+  wwin[stream] = true;  // conservative: the body's first kernels do not prefetch weights
   try {
     body();
   } catch (...) {
@@ -833,6 +834,7 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
     CUDA_CHECK(cudaEventRecord(ev_fork, stream));
     CUDA_CHECK(cudaStreamWaitEvent(side2, ev_fork, 0));
     std::swap(stream, side2);
+    fork_window(stream);  // full dependency on the fork point: nothing in flight
     critic_forward(B);
     std::swap(stream, side2);
     CUDA_CHECK(cudaEventRecord(ev_join, side2));

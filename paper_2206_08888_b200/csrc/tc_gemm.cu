@@ -328,7 +328,14 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) TC_TRACE(1);
+  if (threadIdx.x == 0) {
+    TC_TRACE(1);
+    // early PDL trigger: the successor's launch and prologue overlap this whole grid.  The host
+    // lets a successor prefetch weights before its own wait only if no kernel since the last
+    // wait-then-trigger launch wrote weights (Pop::tc_prefetch_ok), because with early triggers
+    // the successor can start while kernels several launches back are still running.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
 
   auto decode = [&](int t, int& grp, int& m0, int& n0) {
     const int nt = t % n_tiles;
@@ -364,10 +371,6 @@ __global__ void __launch_bounds__(64 + kEpiThreads, 1)
         }
       }
       asm volatile("griddepcontrol.wait;" ::: "memory");
-      // the successor may launch only once this grid's predecessor has completed (as in
-      // PDL_ENTRY): a successor that prefetches weights before its own wait then never overlaps
-      // a weight-writing kernel two launches back
-      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
       int cnt = 0, pit = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         int grp, m0, n0;
@@ -977,13 +980,19 @@ __global__ void __launch_bounds__(kF2Threads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) TC_TRACE(1);
+  if (threadIdx.x == 0) {
+    TC_TRACE(1);
+    // early PDL trigger: the successor's launch and prologue overlap this whole grid.  The host
+    // lets a successor prefetch weights before its own wait only if no kernel since the last
+    // wait-then-trigger launch wrote weights (Pop::tc_prefetch_ok), because with early triggers
+    // the successor can start while kernels several launches back are still running.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   auto active = [&](int grp) { return !g.active || g.active[grp % g.n_members]; };
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer
       asm volatile("griddepcontrol.wait;" ::: "memory");
-      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // after the wait (k_tc_gemm)
       int it = 0, cnt = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const int grp = t / m_tiles, m0 = (t % m_tiles) * kBM;
