@@ -145,6 +145,10 @@ int pbrl_last_losses(pbrl_pop* pop, double* critic1, double* critic2, double* po
 int pbrl_save_checkpoint(pbrl_pop* pop, int net, const char* path);
 int pbrl_load_checkpoint(pbrl_pop* pop, int net, const char* path);
 int pbrl_serialize_state(pbrl_pop* pop, const char* path);
+/* Inverse of pbrl_serialize_state (TD3): full-trainer resume -- networks, Adam m / v / t,
+ * delay_acc, steps -- from that byte layout (the reference writes it, algos.hpp:989-1015, but
+ * ships no loader).  ConfigError on a truncated file or a population / shape mismatch. */
+int pbrl_deserialize_state(pbrl_pop* pop, const char* path);
 
 /* ---- action selection: act (TD3, algos.hpp:895-915) / sac_act (SAC, :918-942) for every
  * member on rows observations each, keyed by the population's member streams: obs [n][rows][ds]

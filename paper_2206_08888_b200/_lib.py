@@ -72,6 +72,7 @@ SIGNATURES = {
     "pbrl_save_checkpoint": [vp, C.c_int, C.c_char_p],
     "pbrl_load_checkpoint": [vp, C.c_int, C.c_char_p],
     "pbrl_serialize_state": [vp, C.c_char_p],
+    "pbrl_deserialize_state": [vp, C.c_char_p],
     "pbrl_replay_save_snapshot": [vp, u64, C.c_char_p],
     "pbrl_replay_load_snapshot": [vp, u64, C.c_char_p],
     "pbrl_update_k": [vp, u32, u64, u64, u64, u64, intp],

@@ -146,35 +146,11 @@ void save_net(Pop* p, int net, std::ostream& os) {
   os.write(reinterpret_cast<const char*>(flat.data()),
            static_cast<std::streamsize>(flat.size() * 4));
 }
-}  // namespace
 
-}  // namespace pbrl
-
-using namespace pbrl;
-
-extern "C" {
-
-int pbrl_save_checkpoint(pbrl_pop* pop, int net, const char* path) {
-  return guarded([&] {
-    Pop* p = P(pop);
-    p->net_row(net, 0);  // validates the network id
-    std::ofstream os(path ? path : "", std::ios::binary);
-    if (!path || !os) PBRL_THROW(PBRL_E_CONFIG, std::string("save_checkpoint: cannot open ") + (path ? path : "(null)"));
-    save_net(p, net, os);
-    if (!os) PBRL_THROW(PBRL_E_RESOURCE, "save_checkpoint: write failed");
-  });
-}
-
-// load_checkpoint (net_pop.hpp:264-296) into an existing population: the file's population
-// size, extents, activation and scale must match this network (ConfigError otherwise, as the
-// reference raises for a bad magic / precision / truncated file)
-int pbrl_load_checkpoint(pbrl_pop* pop, int net, const char* path) {
-  return guarded([&] {
-    Pop* p = P(pop);
-    const NetShape& sh = p->net_shape(net);
-    float* dst0 = p->net_row(net, 0);
-    std::ifstream is(path ? path : "", std::ios::binary);
-    if (!path || !is) PBRL_THROW(PBRL_E_CONFIG, std::string("load_checkpoint: cannot open ") + (path ? path : "(null)"));
+// load_checkpoint (net_pop.hpp:262-304) from a stream: PBRLNET1 header checks, then the rows
+void load_net(Pop* p, int net, std::istream& is) {
+  const NetShape& sh = p->net_shape(net);
+  float* dst0 = p->net_row(net, 0);
     char magic[8];
     is.read(magic, sizeof(magic));
     if (!is || std::memcmp(magic, kNetMagic, sizeof(magic)) != 0)
@@ -202,7 +178,38 @@ int pbrl_load_checkpoint(pbrl_pop* pop, int net, const char* path) {
     if (!is) PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: truncated file");
     CUDA_CHECK(cudaMemcpy2DAsync(dst0, sh.stride * 4, flat.data(), sh.P * 4, sh.P * 4, p->n,
                                  cudaMemcpyHostToDevice, p->stream));
-    p->weights_dirty = true;
+  p->weights_dirty = true;
+  p->weights_written_outside();
+}
+}  // namespace
+
+}  // namespace pbrl
+
+using namespace pbrl;
+
+extern "C" {
+
+int pbrl_save_checkpoint(pbrl_pop* pop, int net, const char* path) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    p->net_row(net, 0);  // validates the network id
+    std::ofstream os(path ? path : "", std::ios::binary);
+    if (!path || !os) PBRL_THROW(PBRL_E_CONFIG, std::string("save_checkpoint: cannot open ") + (path ? path : "(null)"));
+    save_net(p, net, os);
+    if (!os) PBRL_THROW(PBRL_E_RESOURCE, "save_checkpoint: write failed");
+  });
+}
+
+// load_checkpoint (net_pop.hpp:264-296) into an existing population: the file's population
+// size, extents, activation and scale must match this network (ConfigError otherwise, as the
+// reference raises for a bad magic / precision / truncated file)
+int pbrl_load_checkpoint(pbrl_pop* pop, int net, const char* path) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    p->net_row(net, 0);  // validates the network id
+    std::ifstream is(path ? path : "", std::ios::binary);
+    if (!path || !is) PBRL_THROW(PBRL_E_CONFIG, std::string("load_checkpoint: cannot open ") + (path ? path : "(null)"));
+    load_net(p, net, is);
     p->sync();
   });
 }
@@ -255,6 +262,68 @@ int pbrl_serialize_state(pbrl_pop* pop, const char* path) {
     os.write(reinterpret_cast<const char*>(acc.data()), 8 * n);
     os.write(reinterpret_cast<const char*>(steps.data()), 8 * n);
     if (!os) PBRL_THROW(PBRL_E_RESOURCE, "serialize_state: write failed");
+  });
+}
+
+// The inverse of serialize_state (the reference writes it but has no loader): full-trainer
+// resume of a TD3 population from that byte stream -- the six networks, every Adam moment and
+// step counter, delay_acc and steps.  Extents are checked against this population.
+int pbrl_deserialize_state(pbrl_pop* pop, const char* path) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    if (p->algo != PBRL_ALGO_TD3) PBRL_THROW(PBRL_E_USAGE, "deserialize_state: TD3 only (as serialize_state)");
+    std::ifstream is(path ? path : "", std::ios::binary);
+    if (!path || !is) PBRL_THROW(PBRL_E_CONFIG, std::string("deserialize_state: cannot open ") + (path ? path : "(null)"));
+    for (int net = 0; net < 6; ++net) load_net(p, net, is);
+    const int n = p->n;
+    int64_t tmax = 0;
+    auto load_adam = [&](const NetShape& sh, float* m_arena, float* v_arena, int64_t* t_dev) {
+      std::vector<float> m(static_cast<size_t>(n) * sh.P), v(m.size());
+      std::vector<int64_t> t(n), t0(n);
+      bool first = true;
+      auto seg = [&](std::vector<float>& a, size_t off, size_t cnt) {
+        for (int mm = 0; mm < n; ++mm)
+          is.read(reinterpret_cast<char*>(a.data() + static_cast<size_t>(mm) * sh.P + off),
+                  static_cast<std::streamsize>(cnt * 4));
+      };
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int l = 0; l < sh.depth; ++l) {
+          const size_t off = pass == 0 ? sh.woff[l] : sh.boff[l];
+          const size_t cnt = static_cast<size_t>(sh.dims[l + 1]) * (pass == 0 ? sh.dims[l] : 1);
+          seg(m, off, cnt);
+          seg(v, off, cnt);
+          is.read(reinterpret_cast<char*>(first ? t0.data() : t.data()), 8 * n);
+          // MlpAdam steps every tensor of a network together (optim.hpp:23-30)
+          if (!first && t != t0)
+            PBRL_THROW(PBRL_E_CONFIG, "deserialize_state: Adam step counters differ across tensors");
+          first = false;
+        }
+      }
+      if (!is) PBRL_THROW(PBRL_E_CONFIG, "deserialize_state: truncated file");
+      CUDA_CHECK(cudaMemcpy2DAsync(m_arena, sh.stride * 4, m.data(), sh.P * 4, sh.P * 4, n,
+                                   cudaMemcpyHostToDevice, p->stream));
+      CUDA_CHECK(cudaMemcpy2DAsync(v_arena, sh.stride * 4, v.data(), sh.P * 4, sh.P * 4, n,
+                                   cudaMemcpyHostToDevice, p->stream));
+      CUDA_CHECK(cudaMemcpyAsync(t_dev, t0.data(), 8 * n, cudaMemcpyHostToDevice, p->stream));
+      p->sync();
+      for (int64_t x : t0) tmax = std::max(tmax, x);
+    };
+    load_adam(p->pol, p->pol_m.p, p->pol_v.p, p->t_pol.p);
+    load_adam(p->cri, p->cri_m.p, p->cri_v.p, p->t_cri.p);
+    load_adam(p->cri, p->cri_m.p + static_cast<size_t>(n) * p->cri.stride,
+              p->cri_v.p + static_cast<size_t>(n) * p->cri.stride, p->t_cri.p + n);
+    std::vector<double> acc(n);
+    std::vector<uint64_t> steps(n);
+    is.read(reinterpret_cast<char*>(acc.data()), 8 * n);
+    is.read(reinterpret_cast<char*>(steps.data()), 8 * n);
+    if (!is) PBRL_THROW(PBRL_E_CONFIG, "deserialize_state: truncated file");
+    is.peek();
+    if (!is.eof()) PBRL_THROW(PBRL_E_CONFIG, "deserialize_state: trailing bytes (population or shape mismatch)");
+    CUDA_CHECK(cudaMemcpyAsync(p->delay_acc.p, acc.data(), 8 * n, cudaMemcpyHostToDevice, p->stream));
+    CUDA_CHECK(cudaMemcpyAsync(p->steps.p, steps.data(), 8 * n, cudaMemcpyHostToDevice, p->stream));
+    p->delay_host = acc;
+    p->t_bound = std::max<uint64_t>(p->t_bound, static_cast<uint64_t>(tmax));
+    p->sync();
   });
 }
 

@@ -575,6 +575,11 @@ def serialize_state(st, path) -> None:
     _lib.call("pbrl_serialize_state", st._h, str(path).encode())
 
 
+def deserialize_state(st, path) -> None:
+    """Full-trainer resume from a serialize_state file (the inverse the reference lacks)."""
+    _lib.call("pbrl_deserialize_state", st.handle, str(path).encode())
+
+
 # ---------------------------------------------------------------------- action selection
 def _act(st, obs, noise_std, seed, steps, deterministic):
     obs = np.ascontiguousarray(obs, np.float32)

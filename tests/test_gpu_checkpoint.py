@@ -107,3 +107,35 @@ def test_replay_snapshot_matches_reference(pb, ref, tmp_path):
         assert np.array_equal(u, v)
     with pytest.raises(pb.ConfigError):
         pb.DeviceReplay(st2, cap + 1, "per_agent").load_snapshot(tmp_path / "ref0.buf", 0)
+
+
+def test_deserialize_state_resumes_a_reference_run(pb, ref, tmp_path):
+    """Full-trainer resume: the reference's serialize_state file of a run after K steps loads
+    into a fresh device population, and K more steps on both leave bit-identical states."""
+    from oracle.oracle import td3_defaults
+    n, hidden, K, seed = 3, [32, 32], 3, 41
+    r = ref.td3(n, 17, 6, hidden, 1.0, seed)
+    raw = ref.synthetic_batches(2 * K, n, 32, 17, 6, seed)
+    for k in range(K):  # odd K with delay 0.5: delay_acc = 0.5 at the cut
+        r.step(raw_at(raw, k), td3_defaults(n))
+    path = tmp_path / "ref_state.bin"
+    assert ref.lib.ref_td3f_serialize_state(r.h, str(path).encode()) == 0
+    st = pb.make_td3_state(n, 17, 6, hidden, 1.0, seed, precision="ffma32")
+    pb.deserialize_state(st, path)
+    hy = pb.Td3Hyper.defaults(n)
+    for k in range(K, 2 * K):
+        pb.td3_update_step(st, to_batch(pb, raw, k), hy)
+        r.step(raw_at(raw, k), td3_defaults(n))
+    for net in TD3_NETS:
+        assert np.array_equal(st.params(net).view(np.uint32), r.get_net(net).view(np.uint32)), net
+    pb.serialize_state(st, tmp_path / "dev.bin")
+    assert ref.lib.ref_td3f_serialize_state(r.h, str(tmp_path / "ref2.bin").encode()) == 0
+    assert (tmp_path / "dev.bin").read_bytes() == (tmp_path / "ref2.bin").read_bytes()
+
+
+def test_deserialize_state_rejects_other_population(pb, tmp_path):
+    a = pb.make_td3_state(2, 17, 6, [32, 32], 1.0, 1, precision="ffma32")
+    b = pb.make_td3_state(3, 17, 6, [32, 32], 1.0, 1, precision="ffma32")
+    pb.serialize_state(a, tmp_path / "a.bin")
+    with pytest.raises(pb.ConfigError):
+        pb.deserialize_state(b, tmp_path / "a.bin")
