@@ -195,6 +195,26 @@ int pbrl_member_blob_size(pbrl_pop* pop, uint64_t* floats);
 int pbrl_export_member(pbrl_pop* pop, uint64_t member, float* dev_buf);
 int pbrl_import_member(pbrl_pop* pop, uint64_t member, const float* dev_buf);
 
+/* ---- snapshot publication: SnapshotMailbox / ActorSnapshot (pipeline.hpp:31-83) and the
+ * actor refresh of actor_loop (pipeline.hpp:255-285), device-resident.  The learner publishes
+ * its policy population (+ per-member exploration scales) into one of three device slots with a
+ * stream-ordered copy (never waits for actors); an actor thread owns its own population handle
+ * (same shapes, precision and member ids: make it with the learner's descriptor), adopts the
+ * newest version with pbrl_actor_refresh and then acts with pbrl_act on its own handle and
+ * stream, concurrently with the learner's updates.  Readers never see a half-written slot. */
+typedef struct pbrl_mailbox pbrl_mailbox;
+int pbrl_mailbox_create(pbrl_pop* learner, pbrl_mailbox** out);
+int pbrl_mailbox_destroy(pbrl_mailbox* mb);
+/* SnapshotMailbox::publish: *version = the new version (1, 2, ...); explore_std: [n] or NULL */
+int pbrl_mailbox_publish(pbrl_mailbox* mb, pbrl_pop* learner, const double* explore_std,
+                         uint64_t* version);
+int pbrl_mailbox_version(pbrl_mailbox* mb, uint64_t* version);
+/* refresh(): copy the newest snapshot into `actor` if its version changed; *version = the
+ * version the actor now holds (0 = nothing published yet); explore_std: [n] or NULL */
+int pbrl_actor_refresh(pbrl_pop* actor, pbrl_mailbox* mb, uint64_t* version, double* explore_std);
+/* ActorSnapshot::compute_checksum of the newest snapshot (FNV-1a, pipeline.hpp:38-47) */
+int pbrl_mailbox_checksum(pbrl_mailbox* mb, uint64_t* version, uint64_t* checksum);
+
 /* ---- whole-member state copy: slice_member / set_member for states (algos.hpp:425-464,
  * :839-886).  Copies member sm of src into member dm of dst: every network, Adam m / v / t,
  * steps, streams, delay_acc (TD3) or log_alpha + its Adam state (SAC), and the hypers.  With dst

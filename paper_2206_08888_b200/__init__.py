@@ -11,6 +11,7 @@ from .pbrl import (NETS, PBTState, RngSequence, RngStream, SacHyper, SacPrior, S
                    pbt_apply_returns_reset, pbt_evolve_trainer, pbt_plan, pbt_rank,
                    sac_update_step, sample_batch, td3_update_step, update_k_steps, act, sac_act,
                    save_checkpoint, load_checkpoint, serialize_state, deserialize_state,
-                   update_k_from_replay, slice_member, set_member)
+                   update_k_from_replay, slice_member, set_member,
+                   SnapshotMailbox, actor_refresh)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

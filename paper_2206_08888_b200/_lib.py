@@ -103,6 +103,12 @@ SIGNATURES = {
                                    vp, C.c_longlong, C.c_longlong],
     "pbrl_synthetic_batches_device": [vp, u64, u64, u64, u64, u64, u64, C.POINTER(Batch)],
     "pbrl_copy_member_state": [vp, u64, vp, u64],
+    "pbrl_mailbox_create": [vp, C.POINTER(vp)],
+    "pbrl_mailbox_destroy": [vp],
+    "pbrl_mailbox_publish": [vp, vp, f64p, u64p],
+    "pbrl_mailbox_version": [vp, u64p],
+    "pbrl_actor_refresh": [vp, vp, u64p, f64p],
+    "pbrl_mailbox_checksum": [vp, u64p, u64p],
     "pbrl_nccl_unique_id": [vp, C.c_size_t],
     "pbrl_comm_create_nccl": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)],
     "pbrl_comm_create_host": [C.POINTER(CommOps), C.c_int, C.c_int, C.c_int, C.POINTER(vp)],

@@ -35,6 +35,12 @@ int guarded(F&& f) {
   }
 }
 
+}  // namespace
+
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+namespace {
+
 Pop* P(pbrl_pop* h) {
   if (!h) PBRL_THROW(PBRL_E_USAGE, "null population handle");
   Pop* p = reinterpret_cast<Pop*>(h);

@@ -121,6 +121,8 @@ struct Mat {
 
 inline int pad4(int x) { return (x + 3) / 4 * 4; }
 
+void set_last_error(const std::string& m);  // pbrl_last_error() of the calling thread
+
 struct StepGraph {
   int B = 0;
   bool masked = false;
@@ -232,6 +234,10 @@ struct Pop {
     const double rows = static_cast<double>(n) * B;
     return rows * (4.0 * (2 * ds + da + 2) + aeb() * (2.0 * ds + da + ds + ds) + 8.0);
   }
+
+  // actor side of a snapshot mailbox (pbrl_actor_refresh): the version held and its scales
+  uint64_t snap_version = 0;
+  std::vector<double> snap_explore;
 
   // PBT scratch
   DBuf<double> pbt_fit;

@@ -615,6 +615,54 @@ def sac_act(st: "SacState", obs, seed: int, steps, deterministic: bool = False):
 
 # ---------------------------------------------------------------------- replay
 @dataclass
+class SnapshotMailbox:
+    """SnapshotMailbox (pipeline.hpp:53-83), device-resident: the learner publishes its policy
+    population (+ explore_std) into a device slot; actors adopt it with actor_refresh."""
+
+    def __init__(self, learner: _Population):
+        h = C.c_void_p()
+        _lib.call("pbrl_mailbox_create", learner.handle, C.byref(h))
+        self._h, self.n = h, learner.n
+
+    def publish(self, learner: _Population, explore_std=None) -> int:
+        v = C.c_uint64()
+        ex = None if explore_std is None else np.ascontiguousarray(explore_std, np.float64)
+        if ex is not None and ex.size != self.n:
+            raise ShapeError(f"publish: explore_std has {ex.size} entries, population {self.n}")
+        _lib.call("pbrl_mailbox_publish", self._h, learner.handle,
+                  None if ex is None else _ptr(ex, _lib.f64p), C.byref(v))
+        return v.value
+
+    def version(self) -> int:
+        v = C.c_uint64()
+        _lib.call("pbrl_mailbox_version", self._h, C.byref(v))
+        return v.value
+
+    def checksum(self):
+        """(version, ActorSnapshot::compute_checksum) of the newest snapshot."""
+        v, c = C.c_uint64(), C.c_uint64()
+        _lib.call("pbrl_mailbox_checksum", self._h, C.byref(v), C.byref(c))
+        return v.value, c.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.lib().pbrl_mailbox_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
+def actor_refresh(actor: _Population, mailbox: SnapshotMailbox):
+    """actor_loop's refresh() (pipeline.hpp:270-279): adopt the newest snapshot into the
+    actor's own population if its version changed.  Returns (version held, explore_std)."""
+    v = C.c_uint64()
+    ex = np.zeros(actor.n, np.float64)
+    _lib.call("pbrl_actor_refresh", actor.handle, mailbox._h, C.byref(v), _ptr(ex, _lib.f64p))
+    return v.value, ex
+
+
 class Transition:
     """Transition (replay.hpp:17-24)."""
     s: Sequence[float]
