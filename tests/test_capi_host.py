@@ -143,3 +143,24 @@ def test_cpp_facade_compiles():
     r = subprocess.run(["make", "-s", "-B", "-C", str(ROOT / "examples")], capture_output=True,
                        text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_harness_host_logic():
+    """bench.cpp:20-56 host logic: mode names, config validation, median / IQR, the footprint
+    estimate (no device needed)."""
+    from paper_2206_08888_b200 import harness as hz
+    from paper_2206_08888_b200.errors import ConfigError
+    for m in hz.BENCH_MODES:
+        assert hz.parse_bench_mode(m) == m
+    with pytest.raises(ConfigError):
+        hz.parse_bench_mode("gpu")
+    with pytest.raises(ConfigError):
+        hz.BenchConfig(reps=2).validate()
+    r = hz.BenchResult(times_ms=[5.0, 1.0, 4.0, 2.0, 3.0])
+    hz.summarize_bench(r)
+    assert r.median_ms == 3.0 and r.iqr_ms == 4.0 - 2.0
+    cfg = hz.BenchConfig(n=3, k=4, batch=16, obs_dim=5, act_dim=2, hidden=[8, 8])
+    pol = 5 * 8 + 8 + 8 * 8 + 8 + 8 * 2 + 2
+    q = 7 * 8 + 8 + 8 * 8 + 8 + 8 + 1
+    want = 3 * (pol + 2 * q) * 16 + 4 * 3 * 16 * (2 * 5 + 2 + 2) * 4 + 16 * 3 * 16 * 8 * 4
+    assert hz.bench_estimated_bytes(cfg) == want
