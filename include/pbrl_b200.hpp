@@ -82,7 +82,7 @@ enum class Net : int {
   kCritic1Target = PBRL_NET_CRITIC1_TARGET,
   kCritic2Target = PBRL_NET_CRITIC2_TARGET,
 };
-enum class Precision : int { kFfma32 = PBRL_PREC_FFMA32, kTf32 = PBRL_PREC_TF32 };
+enum class Precision : int { kFfma32 = PBRL_PREC_FFMA32, kTf32 = PBRL_PREC_TF32, kBf16 = PBRL_PREC_BF16 };
 
 // ---------------------------------------------------------------- batches (algos.hpp:14-24)
 struct TransitionBatch {

@@ -1,0 +1,32 @@
+"""The threaded run_training on the device (include/pbrl_b200_pipeline.hpp, SURVEY.md §8(f)
+item 2): actor threads acting through device snapshot refreshes, the ingest thread's batched
+device inserts under the ratio guard, device sample + update bursts on the learner thread, PBT.
+Runs examples/run_training_demo (C++) and checks its summary."""
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.mark.parametrize("precision,pbt", [("bf16", 1), ("ffma32", 0)])
+def test_run_training_demo(cuda, precision, pbt):
+    subprocess.run(["make", "-s", "-C", str(ROOT / "examples"), "run_training_demo"], check=True)
+    r = subprocess.run([str(ROOT / "examples" / "run_training_demo"), "4", "2", "400", "20",
+                        str(pbt), precision], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    kv = dict(re.findall(r"(\w+)=([\d.]+)", r.stdout.splitlines()[0]))
+    assert int(kv["update_steps"]) == 400
+    assert int(kv["env_steps"]) >= 4 * 200  # at least the warm-up of every ring
+    assert int(kv["dropped"]) == 0
+    assert int(kv["published"]) >= 400 // 20
+    assert int(kv["device_inserts"]) > 0
+    # the ratio guard holds the run near one update per member env step (slack 5 %)
+    assert 0.7 < float(kv["ratio"]) < 1.3, r.stdout
+    if pbt:
+        assert int(kv["evolve_events"]) >= 1, r.stdout
+    returns = [float(x) for x in r.stdout.splitlines()[1].split()[1:]]
+    assert len(returns) == 4 and all(x > -1e9 for x in returns)
