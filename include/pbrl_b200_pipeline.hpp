@@ -27,6 +27,8 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <deque>
 #include <functional>
 #include <limits>
@@ -649,6 +651,10 @@ inline RunSummary run_training(const RunConfig& cfg) {
         pbt.steps_since_evolve += k_next;
         bool scored = true;
         for (const auto& q : pbt.returns) scored = scored && !q.empty();
+        if (std::getenv("PBRL_PIPELINE_DEBUG"))
+          std::fprintf(stderr, "burst done=%llu since=%llu scored=%d\n",
+                       (unsigned long long)done_updates,
+                       (unsigned long long)pbt.steps_since_evolve, (int)scored);
         if (pbt.steps_since_evolve >= pbt.evolve_interval && scored) {
           std::lock_guard<std::mutex> lk(learner_mu);
           auto plan = pbt_evolve_trainer(pbt, learner, pbt_key, pbt_next);
