@@ -71,6 +71,12 @@ def unpack_hyper(a: np.ndarray, fields) -> dict:
     return {f: a[i].copy() for i, f in enumerate(fields)}
 
 
+class OraDvd(C.Structure):
+    """ora_dvd (pbrl_oracle.h)"""
+    _fields_ = [("probe", C.POINTER(C.c_double)), ("m_states", C.c_uint64),
+                ("length_scale", C.c_double), ("jitter", C.c_double), ("lam", C.c_double)]
+
+
 class _Lib:
     prefix = ""
 
@@ -90,9 +96,60 @@ class _Lib:
     def _declare(self):
         raise NotImplementedError
 
+    # ---- DvD / CEM (evolve.hpp:221-525), same surface on both libraries ---------------------
+    def dvd_lambda(self, step, start, end, horizon):
+        return getattr(self.lib, f"{self.pfx}_dvd_lambda")(step, start, end, horizon)
+
+    def dvd_loss(self, emb, length_scale, jitter, lam):
+        """(loss, logdet, grad [n][dim]); raises FloatingPointError on a singular kernel."""
+        emb = np.ascontiguousarray(emb, np.float64)
+        n, dim = emb.shape
+        loss, logdet = C.c_double(), C.c_double()
+        grad = np.zeros_like(emb)
+        rc = getattr(self.lib, f"{self.pfx}_dvd_loss")(_ptr(emb, f64p), n, dim, length_scale,
+                                                         jitter, lam, C.byref(loss),
+                                                         C.byref(logdet), _ptr(grad, f64p))
+        if rc == -10:
+            raise FloatingPointError("DegeneratePopulationError")
+        if rc < 0:
+            raise ValueError(f"dvd_loss: config error ({rc})")
+        return loss.value, logdet.value, grad
+
+    def median_pairwise_distance(self, emb):
+        emb = np.ascontiguousarray(emb, np.float64)
+        return getattr(self.lib, f"{self.pfx}_median_pairwise_distance")(_ptr(emb, f64p),
+                                                                         *emb.shape)
+
+    def cem_sample(self, mean, var, noise, count, key, next_):
+        """candidates [count][dim] and the advanced RngSequence counter"""
+        mean = np.ascontiguousarray(mean, np.float64)
+        var = np.ascontiguousarray(var, np.float64)
+        out = np.zeros((count, mean.size), np.float64)
+        nx = C.c_uint64(next_)
+        getattr(self.lib, f"{self.pfx}_cem_sample")(_ptr(mean, f64p), _ptr(var, f64p), noise,
+                                                     mean.size, count, key, C.byref(nx),
+                                                     _ptr(out, f64p))
+        return out, nx.value
+
+    def cem_update(self, mean, var, noise, cands, scores, noise_final=1e-3, noise_decay=0.999,
+                   elite_fraction=0.5):
+        """(mean, var, noise) after cem_update; ValueError on ConfigError"""
+        mean = np.array(mean, np.float64)
+        var = np.array(var, np.float64)
+        cands = np.ascontiguousarray(cands, np.float64)
+        scores = np.ascontiguousarray(scores, np.float64)
+        nz = C.c_double(noise)
+        rc = getattr(self.lib, f"{self.pfx}_cem_update")(
+            _ptr(mean, f64p), _ptr(var, f64p), C.byref(nz), noise_final, noise_decay,
+            elite_fraction, mean.size, _ptr(cands, f64p), _ptr(scores, f64p), cands.shape[0])
+        if rc < 0:
+            raise ValueError(f"cem_update: config error ({rc})")
+        return mean, var, nz.value
+
 
 class Oracle(_Lib):
     """The C restatement (oracle/pbrl_oracle.c)."""
+    pfx = "ora"
 
     def __init__(self, path: Path = ORACLE_SO):
         super().__init__(path)
@@ -112,6 +169,18 @@ class Oracle(_Lib):
             F(f"ora_{algo}_get_net", None, vp, C.c_int, u64, f32p)
             F(f"ora_{algo}_set_net", None, vp, C.c_int, u64, f32p)
             F(f"ora_{algo}_get_adam", None, vp, C.c_int, u64, f32p, f32p, i64p)
+        for algo in ("td3", "sac"):
+            F(f"ora_{algo}_create_mode", vp, u64, u64, u64, u64p, u32, C.c_double, u64, C.c_int)
+        F("ora_td3_step_hook", C.c_int, vp, f32p, f32p, f32p, f32p, f32p, u64, f64p, C.c_char_p,
+          f64p, C.POINTER(OraDvd))
+        F("ora_dvd_lambda", C.c_double, u64, C.c_double, C.c_double, u64)
+        F("ora_dvd_loss", C.c_int, f64p, u64, u64, C.c_double, C.c_double, C.c_double, f64p, f64p,
+          f64p)
+        F("ora_median_pairwise_distance", C.c_double, f64p, u64, u64)
+        F("ora_td3_dvd_embed", None, vp, f64p, u64, f32p)
+        F("ora_cem_sample", None, f64p, f64p, C.c_double, u64, u64, u64, u64p, f64p)
+        F("ora_cem_update", C.c_int, f64p, f64p, f64p, C.c_double, C.c_double, C.c_double, u64,
+          f64p, f64p, u64)
         F("ora_td3_get_counters", None, vp, f64p, u64p)
         F("ora_td3_target", None, vp, f32p, f32p, f32p, u64, f64p, f32p)
         F("ora_td3_step", C.c_int, vp, f32p, f32p, f32p, f32p, f32p, u64, f64p, C.c_char_p, f64p)
@@ -132,11 +201,11 @@ class Oracle(_Lib):
         F("ora_sac_pbt_evolve", C.c_int, vp, f64p, u32p, u64, f64p, C.c_double, u64, u64p, u64p,
           u64p)
 
-    def td3(self, n, ds, da, hidden, bound, seed):
-        return _State(self, "ora_td3", n, ds, da, hidden, bound, seed, "td3")
+    def td3(self, n, ds, da, hidden, bound, seed, shared=False):
+        return _State(self, "ora_td3", n, ds, da, hidden, bound, seed, "td3", shared=shared)
 
-    def sac(self, n, ds, da, hidden, bound, seed):
-        return _State(self, "ora_sac", n, ds, da, hidden, bound, seed, "sac")
+    def sac(self, n, ds, da, hidden, bound, seed, shared=False):
+        return _State(self, "ora_sac", n, ds, da, hidden, bound, seed, "sac", shared=shared)
 
     def synthetic_batches(self, count, n, b, ds, da, seed):
         s = np.zeros((count, n, b, ds), np.float32)
@@ -191,6 +260,7 @@ class Oracle(_Lib):
 
 class Ref(_Lib):
     """The unmodified reference (oracle/_ref/libpbrl_ref.so)."""
+    pfx = "ref"
 
     def __init__(self, path: Path = REF_SO):
         super().__init__(path)
@@ -243,14 +313,27 @@ class Ref(_Lib):
         F("ref_bench_update", C.c_int, C.c_int, C.c_int, u64, u64, u64, u64, u64p, u32, u64, f64p,
           f64p, f64p, u64p)
         F("ref_kernel_invocations", u64)
+        for algo in ("td3f", "td3d", "sacf", "sacd"):
+            F(f"ref_{algo}_create_mode", vp, u64, u64, u64, u64p, u32, C.c_double, u64, C.c_int)
+        for algo, fp in (("td3f", f32p), ("td3d", f64p)):
+            F(f"ref_{algo}_step_dvd", C.c_int, vp, fp, fp, fp, fp, fp, u64, f64p, C.c_char_p, f64p,
+              u64, C.c_double, C.c_double, C.c_double, C.c_double, u64, u64)
+            F(f"ref_{algo}_dvd_embed", None, vp, f64p, u64, fp)
+        F("ref_dvd_lambda", C.c_double, u64, C.c_double, C.c_double, u64)
+        F("ref_dvd_loss", C.c_int, f64p, u64, u64, C.c_double, C.c_double, C.c_double, f64p, f64p,
+          f64p)
+        F("ref_median_pairwise_distance", C.c_double, f64p, u64, u64)
+        F("ref_cem_sample", None, f64p, f64p, C.c_double, u64, u64, u64, u64p, f64p)
+        F("ref_cem_update", C.c_int, f64p, f64p, f64p, C.c_double, C.c_double, C.c_double, u64,
+          f64p, f64p, u64)
 
-    def td3(self, n, ds, da, hidden, bound, seed, dtype=np.float32):
+    def td3(self, n, ds, da, hidden, bound, seed, dtype=np.float32, shared=False):
         sfx = "td3f" if dtype == np.float32 else "td3d"
-        return _State(self, f"ref_{sfx}", n, ds, da, hidden, bound, seed, "td3", dtype)
+        return _State(self, f"ref_{sfx}", n, ds, da, hidden, bound, seed, "td3", dtype, shared)
 
-    def sac(self, n, ds, da, hidden, bound, seed, dtype=np.float32):
+    def sac(self, n, ds, da, hidden, bound, seed, dtype=np.float32, shared=False):
         sfx = "sacf" if dtype == np.float32 else "sacd"
-        return _State(self, f"ref_{sfx}", n, ds, da, hidden, bound, seed, "sac", dtype)
+        return _State(self, f"ref_{sfx}", n, ds, da, hidden, bound, seed, "sac", dtype, shared)
 
     def synthetic_batches(self, count, n, b, ds, da, seed):
         s = np.zeros((count, n, b, ds), np.float32)
@@ -322,13 +405,17 @@ def _rings(rings, counts):
 class _State:
     """A TD3 or SAC population state living in one of the CPU libraries."""
 
-    def __init__(self, owner, prefix, n, ds, da, hidden, bound, seed, algo, dtype=np.float32):
+    def __init__(self, owner, prefix, n, ds, da, hidden, bound, seed, algo, dtype=np.float32,
+                 shared=False):
         self.o, self.p, self.algo, self.dtype = owner, prefix, algo, dtype
         self.n, self.ds, self.da = n, ds, da
+        self.shared = bool(shared)
+        self.nc = 1 if shared else n  # critic population (PopMode::kSharedCritic: 1)
         self.fp = f32p if dtype == np.float32 else f64p
         h = np.asarray(hidden, np.uint64)
-        self.h = getattr(owner.lib, f"{prefix}_create")(n, ds, da, _ptr(h, u64p), len(hidden),
-                                                        bound, seed)
+        self.h = getattr(owner.lib, f"{prefix}_create_mode")(n, ds, da, _ptr(h, u64p),
+                                                             len(hidden), bound, seed,
+                                                             1 if shared else 0)
         self.fields = TD3_FIELDS if algo == "td3" else SAC_FIELDS
 
     def __del__(self):
@@ -347,7 +434,8 @@ class _State:
         k = NETS.get(net, net)
         P = self.param_count(k)
         if m is None:
-            return np.stack([self.get_net(k, i) for i in range(self.n)])
+            cnt = self.n if k <= 1 else self.nc
+            return np.stack([self.get_net(k, i) for i in range(cnt)])
         out = np.zeros(P, self.dtype)
         self._f("get_net")(self.h, k, m, _ptr(out, self.fp))
         return out
@@ -382,11 +470,31 @@ class _State:
         s, a, r, s2, d = (np.ascontiguousarray(x, self.dtype) for x in batch)
         return s, a, r, s2, d, s.shape[1]
 
-    def step(self, batch, hyper, policy_mask=None, want_losses=False):
+    def step(self, batch, hyper, policy_mask=None, want_losses=False, dvd=None):
+        """One update step.  dvd (TD3): dict probe [M][ds] (double), length_scale, jitter and
+        the LambdaSchedule lam_start / lam_end / horizon at `step` (dvd_policy_hook)."""
         s, a, r, s2, d, b = self._batch(batch)
         hy = pack_hyper(hyper, self.fields, self.n)
         args = [self.h] + [_ptr(x, self.fp) for x in (s, a, r, s2, d)] + [b, _ptr(hy, f64p)]
         losses = np.zeros((3, self.n), np.float64)
+        if dvd is not None:
+            probe = np.ascontiguousarray(dvd["probe"], np.float64)
+            ms = probe.shape[0]
+            mask = None if policy_mask is None else bytes(np.asarray(policy_mask, np.uint8))
+            if isinstance(self.o, Oracle):
+                lam = self.o.lib.ora_dvd_lambda(dvd.get("step", 0), dvd["lam_start"],
+                                                dvd["lam_end"], dvd["horizon"])
+                cfg = OraDvd(_ptr(probe, f64p), ms, dvd["length_scale"], dvd["jitter"], lam)
+                rc = self.o.lib.ora_td3_step_hook(*args, mask, _ptr(losses, f64p), C.byref(cfg))
+            else:
+                rc = self._f("step_dvd")(*args, mask, _ptr(probe, f64p), ms, dvd["length_scale"],
+                                         dvd["jitter"], dvd["lam_start"], dvd["lam_end"],
+                                         dvd["horizon"], dvd.get("step", 0))
+            if rc == -10:
+                raise FloatingPointError("DegeneratePopulationError")
+            if rc < 0:
+                raise ValueError(f"step failed ({rc})")
+            return losses
         if isinstance(self.o, Oracle):
             if self.algo == "td3":
                 mask = None if policy_mask is None else bytes(np.asarray(policy_mask, np.uint8))
@@ -410,6 +518,13 @@ class _State:
         if rc == -2:
             raise ValueError("config error")
         return losses
+
+    def dvd_embed(self, probe):
+        """dvd_embed (evolve.hpp:314-339): [n][M*da] deterministic actions on the probes"""
+        probe = np.ascontiguousarray(probe, np.float64)
+        out = np.zeros((self.n, probe.shape[0] * self.da), self.dtype)
+        self._f("dvd_embed")(self.h, _ptr(probe, f64p), probe.shape[0], _ptr(out, self.fp))
+        return out
 
     def act(self, obs, seed, steps, noise_std=None, deterministic=False):
         """act / sac_act (algos.hpp:895-942): actions [n][rows][da] for obs [n][rows][ds]."""

@@ -435,6 +435,8 @@ static void mse_grads(const ora_net* nt, const float* params, uint64_t n, uint64
 /* ------------------------------------------------------------------ TD3 (algos.hpp) */
 struct ora_td3 {
   uint64_t n, ds, da;
+  uint64_t nc;  /* critic population: n, or 1 in shared-critic mode (algos.hpp:197) */
+  int shared;   /* PopMode::kSharedCritic */
   ora_net pol, cri;
   float bound;
   uint64_t seed;
@@ -453,11 +455,13 @@ static const ora_net* td3_shape(const ora_td3* st, int net) {
 
 static int td3_opt_index(int net) { return net == 0 ? 0 : (net == 2 ? 1 : 2); }
 
-/* make_td3_state, algos.hpp:181-212 */
-ora_td3* ora_td3_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
-                        uint32_t nh, double bound, uint64_t seed) {
+/* make_td3_state, algos.hpp:181-212; shared != 0 is PopMode::kSharedCritic (critic_n = 1) */
+ora_td3* ora_td3_create_mode(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
+                             uint32_t nh, double bound, uint64_t seed, int shared) {
   ora_td3* st = (ora_td3*)calloc(1, sizeof(ora_td3));
   st->n = n;
+  st->shared = shared ? 1 : 0;
+  st->nc = shared ? 1 : n;
   st->ds = ds;
   st->da = da;
   st->bound = (float)bound;
@@ -470,26 +474,33 @@ ora_td3* ora_td3_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hi
   dims[0] = ds + da;
   dims[nh + 1] = 1;
   net_make(&st->cri, dims, (int)nh + 2, ACT_NONE, 1.0f);
+  const uint64_t nc = st->nc;
   for (int k = 0; k < 6; ++k) {
-    st->net[k] = (float*)calloc(n * td3_shape(st, k)->P, sizeof(float));
+    st->net[k] = (float*)calloc((k <= 1 ? n : nc) * td3_shape(st, k)->P, sizeof(float));
   }
   net_init(&st->pol, st->net[0], n, ora_mix64(seed ^ 0xA1));
-  net_init(&st->cri, st->net[2], n, ora_mix64(seed ^ 0xB2));
-  net_init(&st->cri, st->net[3], n, ora_mix64(seed ^ 0xC3));
+  net_init(&st->cri, st->net[2], nc, ora_mix64(seed ^ 0xB2));
+  net_init(&st->cri, st->net[3], nc, ora_mix64(seed ^ 0xC3));
   memcpy(st->net[1], st->net[0], sizeof(float) * n * st->pol.P);
-  memcpy(st->net[4], st->net[2], sizeof(float) * n * st->cri.P);
-  memcpy(st->net[5], st->net[3], sizeof(float) * n * st->cri.P);
+  memcpy(st->net[4], st->net[2], sizeof(float) * nc * st->cri.P);
+  memcpy(st->net[5], st->net[3], sizeof(float) * nc * st->cri.P);
   for (int k = 0; k < 3; ++k) {
     const uint64_t P = (k == 0) ? st->pol.P : st->cri.P;
-    st->am[k] = (float*)calloc(n * P, sizeof(float));
-    st->av[k] = (float*)calloc(n * P, sizeof(float));
-    st->at[k] = (int64_t*)calloc(n, sizeof(int64_t));
+    const uint64_t cnt = (k == 0) ? n : nc;
+    st->am[k] = (float*)calloc(cnt * P, sizeof(float));
+    st->av[k] = (float*)calloc(cnt * P, sizeof(float));
+    st->at[k] = (int64_t*)calloc(cnt, sizeof(int64_t));
   }
   st->delay_acc = (double*)calloc(n, sizeof(double));
   st->steps = (uint64_t*)calloc(n, sizeof(uint64_t));
   st->streams = (uint64_t*)calloc(n, sizeof(uint64_t));
   for (uint64_t i = 0; i < n; ++i) st->streams[i] = i;
   return st;
+}
+
+ora_td3* ora_td3_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
+                        uint32_t nh, double bound, uint64_t seed) {
+  return ora_td3_create_mode(n, ds, da, hidden, nh, bound, seed, 0);
 }
 
 void ora_td3_destroy(ora_td3* st) {
@@ -571,8 +582,11 @@ void ora_td3_target(const ora_td3* st, const float* s2, const float* r, const fl
   }
   float* sa2 = concat(s2, a2, n, b, ds, da);
   ora_cache c1, c2;
-  mlp_forward(&st->cri, st->net[4], n, b, sa2, &c1);
-  mlp_forward(&st->cri, st->net[5], n, b, sa2, &c2);
+  /* critic_forward (algos.hpp:219-227): a shared critic sees the population folded into its
+   * batch axis -- the same row-major buffer read as nc = 1 member of n*b rows */
+  const uint64_t rc = st->shared ? n * b : b;
+  mlp_forward(&st->cri, st->net[4], st->nc, rc, sa2, &c1);
+  mlp_forward(&st->cri, st->net[5], st->nc, rc, sa2, &c2);
   for (uint64_t m = 0; m < n; ++m) {
     const float g = (float)HY(hyper, TH_GAMMA, n, m);
     for (uint64_t i = 0; i < b; ++i) {
@@ -587,11 +601,206 @@ void ora_td3_target(const ora_td3* st, const float* s2, const float* r, const fl
   cache_free(&c2);
 }
 
-/* td3_update_step, algos.hpp:351-422 (independent mode) */
-int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, const float* s2,
-                 const float* d, uint64_t b, const double* hyper, const char* policy_mask,
-                 double* losses) {
-  const uint64_t n = st->n, ds = st->ds, da = st->da;
+/* ------------------------------------------------------------------ DvD (evolve.hpp:304-525) */
+double ora_dvd_lambda(uint64_t step, double start, double end, uint64_t horizon) {
+  if (horizon == 0 || step >= horizon) return end;
+  const double frac = (double)step / (double)horizon;
+  return start + (end - start) * frac;
+}
+
+/* canonical_order (evolve.hpp:404-418): stable lexicographic sort of the embedding rows */
+static const double* g_canon_e;
+static uint64_t g_canon_dim;
+static int canon_cmp(const void* pa, const void* pb) {
+  const uint64_t a = *(const uint64_t*)pa, b = *(const uint64_t*)pb;
+  const double* ra = g_canon_e + a * g_canon_dim;
+  const double* rb = g_canon_e + b * g_canon_dim;
+  for (uint64_t k = 0; k < g_canon_dim; ++k) {
+    if (ra[k] != rb[k]) return ra[k] < rb[k] ? -1 : 1;
+  }
+  return a < b ? -1 : (a > b ? 1 : 0); /* stable: ties keep index order */
+}
+
+/* cholesky / cholesky_inverse (evolve.hpp:364-400) */
+static int chol(double* a, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) {
+    for (uint64_t j = 0; j <= i; ++j) {
+      double sum = a[i * n + j];
+      for (uint64_t k = 0; k < j; ++k) sum -= a[i * n + k] * a[j * n + k];
+      if (i == j) {
+        if (!(sum > 0.0)) return 0;
+        a[i * n + i] = sqrt(sum);
+      } else {
+        a[i * n + j] = sum / a[j * n + j];
+      }
+    }
+    for (uint64_t j = i + 1; j < n; ++j) a[i * n + j] = 0.0;
+  }
+  return 1;
+}
+
+static void chol_inverse(const double* l, uint64_t n, double* inv) {
+  double* col = (double*)malloc(sizeof(double) * n);
+  for (uint64_t c = 0; c < n; ++c) {
+    for (uint64_t i = 0; i < n; ++i) {
+      double sum = (i == c) ? 1.0 : 0.0;
+      for (uint64_t k = 0; k < i; ++k) sum -= l[i * n + k] * col[k];
+      col[i] = sum / l[i * n + i];
+    }
+    for (uint64_t ii = n; ii-- > 0;) {
+      double sum = col[ii];
+      for (uint64_t k = ii + 1; k < n; ++k) sum -= l[k * n + ii] * col[k];
+      col[ii] = sum / l[ii * n + ii];
+    }
+    for (uint64_t i = 0; i < n; ++i) inv[i * n + c] = col[i];
+  }
+  free(col);
+}
+
+/* dvd_loss, evolve.hpp:425-478 */
+int ora_dvd_loss(const double* emb, uint64_t n, uint64_t dim, double length_scale, double jitter,
+                 double lambda, double* loss, double* logdet_out, double* grad) {
+  if (n < 2) return -2;
+  if (!(length_scale > 0)) return -2;
+  uint64_t* order = (uint64_t*)malloc(sizeof(uint64_t) * n);
+  for (uint64_t i = 0; i < n; ++i) order[i] = i;
+  g_canon_e = emb;
+  g_canon_dim = dim;
+  qsort(order, n, sizeof(uint64_t), canon_cmp);
+  const double inv2l2 = 1.0 / (2.0 * length_scale * length_scale);
+  double* kernel = (double*)malloc(sizeof(double) * n * n);
+  for (uint64_t i = 0; i < n; ++i) {
+    kernel[i * n + i] = 1.0;
+    const double* ri = emb + order[i] * dim;
+    for (uint64_t j = 0; j < i; ++j) {
+      const double* rj = emb + order[j] * dim;
+      double d2 = 0;
+      for (uint64_t k = 0; k < dim; ++k) {
+        const double d = ri[k] - rj[k];
+        d2 += d * d;
+      }
+      const double kij = exp(-d2 * inv2l2);
+      kernel[i * n + j] = kij;
+      kernel[j * n + i] = kij;
+    }
+  }
+  double* m = (double*)malloc(sizeof(double) * n * n);
+  memcpy(m, kernel, sizeof(double) * n * n);
+  for (uint64_t i = 0; i < n; ++i) m[i * n + i] += jitter;
+  if (!chol(m, n)) {
+    free(order);
+    free(kernel);
+    free(m);
+    return -10; /* DegeneratePopulationError */
+  }
+  double logdet = 0;
+  for (uint64_t i = 0; i < n; ++i) logdet += 2.0 * log(m[i * n + i]);
+  double* minv = (double*)malloc(sizeof(double) * n * n);
+  chol_inverse(m, n, minv);
+  if (logdet_out) *logdet_out = logdet;
+  if (loss) *loss = -lambda * logdet;
+  if (grad) {
+    memset(grad, 0, sizeof(double) * n * dim);
+    const double coef = 2.0 * lambda / (length_scale * length_scale);
+    for (uint64_t i = 0; i < n; ++i) {
+      double* gi = grad + order[i] * dim;
+      const double* ri = emb + order[i] * dim;
+      for (uint64_t j = 0; j < n; ++j) {
+        if (j == i) continue;
+        const double* rj = emb + order[j] * dim;
+        const double w = coef * minv[i * n + j] * kernel[i * n + j];
+        for (uint64_t k = 0; k < dim; ++k) gi[k] += w * (ri[k] - rj[k]);
+      }
+    }
+  }
+  free(order);
+  free(kernel);
+  free(m);
+  free(minv);
+  return 0;
+}
+
+static int dbl_cmp(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* median_pairwise_distance, evolve.hpp:481-499 */
+double ora_median_pairwise_distance(const double* emb, uint64_t n, uint64_t dim) {
+  if (n < 2) return 1.0;
+  const uint64_t cnt = n * (n - 1) / 2;
+  double* d = (double*)malloc(sizeof(double) * cnt);
+  uint64_t at = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    for (uint64_t j = i + 1; j < n; ++j) {
+      double d2 = 0;
+      for (uint64_t k = 0; k < dim; ++k) {
+        const double x = emb[i * dim + k] - emb[j * dim + k];
+        d2 += x * x;
+      }
+      d[at++] = sqrt(d2);
+    }
+  }
+  qsort(d, cnt, sizeof(double), dbl_cmp);
+  const double med = d[cnt / 2];
+  free(d);
+  return med > 0 ? med : 1.0;
+}
+
+/* dvd_embed_cached (evolve.hpp:314-332): the probe states (double, cast to T as in
+ * dvd_policy_hook) replicated per member, then the policy forward; out [n][m_states*da] */
+static float* dvd_probe_block(const ora_td3* st, const double* probe, uint64_t ms) {
+  float* x = (float*)malloc(sizeof(float) * st->n * ms * st->ds);
+  for (uint64_t m = 0; m < st->n; ++m) {
+    for (uint64_t i = 0; i < ms * st->ds; ++i) x[m * ms * st->ds + i] = (float)probe[i];
+  }
+  return x;
+}
+
+void ora_td3_dvd_embed(const ora_td3* st, const double* probe, uint64_t m_states, float* out) {
+  float* x = dvd_probe_block(st, probe, m_states);
+  ora_cache c;
+  mlp_forward(&st->pol, st->net[0], st->n, m_states, x, &c);
+  memcpy(out, c.out, sizeof(float) * st->n * m_states * st->da);
+  cache_free(&c);
+  free(x);
+}
+
+/* dvd_policy_hook (evolve.hpp:507-525) applied to the policy gradients g [n][Pp] */
+static int dvd_hook(const ora_td3* st, const ora_dvd* dv, float* g) {
+  if (dv->lambda == 0.0) return 0;
+  const uint64_t n = st->n, ms = dv->m_states, da = st->da, dim = ms * da, Pp = st->pol.P;
+  float* x = dvd_probe_block(st, dv->probe, ms);
+  ora_cache c;
+  mlp_forward(&st->pol, st->net[0], n, ms, x, &c);
+  double* e = (double*)malloc(sizeof(double) * n * dim);
+  double* ge = (double*)malloc(sizeof(double) * n * dim);
+  for (uint64_t i = 0; i < n * dim; ++i) e[i] = (double)c.out[i];
+  const int rc = ora_dvd_loss(e, n, dim, dv->length_scale, dv->jitter, dv->lambda, NULL, NULL, ge);
+  if (rc == 0) {
+    float* gf = (float*)malloc(sizeof(float) * n * dim);
+    for (uint64_t i = 0; i < n * dim; ++i) gf[i] = (float)ge[i];
+    float* dg = (float*)malloc(sizeof(float) * n * Pp);
+    mlp_backward(&st->pol, st->net[0], &c, gf, dg, NULL);
+    for (uint64_t i = 0; i < n * Pp; ++i) g[i] += 1.0f * dg[i]; /* add_scaled, optim.hpp:75-85 */
+    free(gf);
+    free(dg);
+  }
+  free(e);
+  free(ge);
+  free(x);
+  cache_free(&c);
+  return rc;
+}
+
+/* td3_update_step, algos.hpp:351-422: independent or shared-critic mode, optional
+ * policy_member_mask and DvD policy-gradient hook */
+int ora_td3_step_hook(ora_td3* st, const float* s, const float* a, const float* r,
+                      const float* s2, const float* d, uint64_t b, const double* hyper,
+                      const char* policy_mask, double* losses, const ora_dvd* dvd) {
+  const uint64_t n = st->n, ds = st->ds, da = st->da, nc = st->nc;
+  const int shared = st->shared;
+  const uint64_t rc = shared ? n * b : b; /* critic rows per critic member (folded batch) */
   if (td3_validate(hyper, n)) return -2;
   float* y = (float*)malloc(sizeof(float) * n * b);
   ora_td3_target(st, s2, r, d, b, hyper, y);
@@ -599,10 +808,12 @@ int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, co
   float* sa = concat(s, a, n, b, ds, da);
   const uint64_t Pc = st->cri.P, Pp = st->pol.P;
   float* g = (float*)malloc(sizeof(float) * n * (Pc > Pp ? Pc : Pp));
+  if (losses) memset(losses, 0, sizeof(double) * 3 * n);
   for (int c = 0; c < 2; ++c) {
     float* params = st->net[2 + c];
-    mse_grads(&st->cri, params, n, b, sa, y, g, losses ? losses + c * n : NULL);
-    for (uint64_t m = 0; m < n; ++m) {
+    /* shared: critic_lr = {critic_lr[0]} (algos.hpp:366-367), one loss over n*b rows */
+    mse_grads(&st->cri, params, nc, rc, sa, y, g, losses ? losses + c * n : NULL);
+    for (uint64_t m = 0; m < nc; ++m) {
       adam_member(params + m * Pc, g + m * Pc, st->am[1 + c] + m * Pc, st->av[1 + c] + m * Pc,
                   &st->at[1 + c][m], Pc, HY(hyper, TH_CLR, n, m));
     }
@@ -611,22 +822,26 @@ int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, co
   char* fire = (char*)calloc(n, 1);
   int any = 0;
   for (uint64_t m = 0; m < n; ++m) {
-    st->delay_acc[m] += HY(hyper, TH_DELAY, n, m);
-    if (st->delay_acc[m] >= 1.0 - 1e-12) {
-      st->delay_acc[m] -= 1.0;
-      fire[m] = 1;
+    if (shared) {
+      fire[m] = 1; /* one critic update per policy-population update (algos.hpp:382-384) */
+    } else {
+      st->delay_acc[m] += HY(hyper, TH_DELAY, n, m);
+      if (st->delay_acc[m] >= 1.0 - 1e-12) {
+        st->delay_acc[m] -= 1.0;
+        fire[m] = 1;
+      }
     }
     if (policy_mask && !policy_mask[m]) fire[m] = 0;
     any = any || fire[m];
   }
-  if (losses) memset(losses + 2 * n, 0, sizeof(double) * n);
+  int rc_hook = 0;
 
   if (any) {
     /* td3_policy_loss_grads, algos.hpp:318-338 */
     ora_cache cp, cq;
     mlp_forward(&st->pol, st->net[0], n, b, s, &cp);
     float* spa = concat(s, cp.out, n, b, ds, da);
-    mlp_forward(&st->cri, st->net[2], n, b, spa, &cq);
+    mlp_forward(&st->cri, st->net[2], nc, rc, spa, &cq);
     if (losses) {
       for (uint64_t m = 0; m < n; ++m) {
         double acc = 0.0;
@@ -641,17 +856,24 @@ int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, co
     mlp_backward(&st->cri, st->net[2], &cq, gq, g, gsa);
     float* ga = take_cols(gsa, n * b, ds + da, ds, da);
     mlp_backward(&st->pol, st->net[0], &cp, ga, g, NULL);
-    for (uint64_t m = 0; m < n; ++m) {
-      if (!fire[m]) continue;
-      adam_member(st->net[0] + m * Pp, g + m * Pp, st->am[0] + m * Pp, st->av[0] + m * Pp,
-                  &st->at[0][m], Pp, HY(hyper, TH_PLR, n, m));
-    }
-    for (uint64_t m = 0; m < n; ++m) {
-      if (!fire[m]) continue;
-      const double tau = HY(hyper, TH_TAU, n, m);
-      polyak_member(st->net[1] + m * Pp, st->net[0] + m * Pp, Pp, tau);
-      polyak_member(st->net[4] + m * Pc, st->net[2] + m * Pc, Pc, tau);
-      polyak_member(st->net[5] + m * Pc, st->net[3] + m * Pc, Pc, tau);
+    if (dvd) rc_hook = dvd_hook(st, dvd, g);
+    if (rc_hook == 0) {
+      for (uint64_t m = 0; m < n; ++m) {
+        if (!fire[m]) continue;
+        adam_member(st->net[0] + m * Pp, g + m * Pp, st->am[0] + m * Pp, st->av[0] + m * Pp,
+                    &st->at[0][m], Pp, HY(hyper, TH_PLR, n, m));
+      }
+      for (uint64_t m = 0; m < n; ++m) {
+        if (!fire[m]) continue;
+        polyak_member(st->net[1] + m * Pp, st->net[0] + m * Pp, Pp, HY(hyper, TH_TAU, n, m));
+      }
+      /* critic targets: per fired member, or the one shared critic with tau[0] (:407-418) */
+      for (uint64_t m = 0; m < nc; ++m) {
+        if (!shared && !fire[m]) continue;
+        const double tau = HY(hyper, TH_TAU, n, m);
+        polyak_member(st->net[4] + m * Pc, st->net[2] + m * Pc, Pc, tau);
+        polyak_member(st->net[5] + m * Pc, st->net[3] + m * Pc, Pc, tau);
+      }
     }
     free(spa);
     free(gq);
@@ -660,17 +882,80 @@ int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, co
     cache_free(&cp);
     cache_free(&cq);
   }
-  for (uint64_t m = 0; m < n; ++m) st->steps[m] += 1;
+  if (rc_hook == 0) {
+    for (uint64_t m = 0; m < n; ++m) st->steps[m] += 1;
+  }
   free(fire);
   free(g);
   free(sa);
   free(y);
+  return rc_hook;
+}
+
+int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, const float* s2,
+                 const float* d, uint64_t b, const double* hyper, const char* policy_mask,
+                 double* losses) {
+  return ora_td3_step_hook(st, s, a, r, s2, d, b, hyper, policy_mask, losses, NULL);
+}
+
+/* ------------------------------------------------------------------ CEM (evolve.hpp:221-297) */
+void ora_cem_sample(const double* mean, const double* var, double noise, uint64_t dim,
+                    uint64_t count, uint64_t key, uint64_t* next, double* out) {
+  for (uint64_t c = 0; c < count; ++c) {
+    for (uint64_t i = 0; i < dim; ++i) {
+      const uint64_t ctr = *next;
+      *next += 2;
+      out[c * dim + i] = mean[i] + sqrt(var[i] + noise) * ora_normal_pair(key, ctr);
+    }
+  }
+}
+
+static const double* g_cem_scores;
+static int cem_cmp(const void* pa, const void* pb) {
+  const uint64_t a = *(const uint64_t*)pa, b = *(const uint64_t*)pb;
+  if (g_cem_scores[a] > g_cem_scores[b]) return -1;
+  if (g_cem_scores[b] > g_cem_scores[a]) return 1;
+  return a < b ? -1 : (a > b ? 1 : 0); /* stable_sort: ties keep index order */
+}
+
+int ora_cem_update(double* mean, double* var, double* noise, double noise_final,
+                   double noise_decay, double elite_fraction, uint64_t dim, const double* cands,
+                   const double* scores, uint64_t count) {
+  if (count < 2 || count % 2 != 0) return -2;
+  for (uint64_t i = 0; i < count; ++i) {
+    if (!isfinite(scores[i])) return -2;
+  }
+  uint64_t* order = (uint64_t*)malloc(sizeof(uint64_t) * count);
+  for (uint64_t i = 0; i < count; ++i) order[i] = i;
+  g_cem_scores = scores;
+  qsort(order, count, sizeof(uint64_t), cem_cmp);
+  const uint64_t elite = (uint64_t)(elite_fraction * (double)count);
+  for (uint64_t i = 0; i < dim; ++i) mean[i] = 0.0;
+  for (uint64_t e = 0; e < elite; ++e) {
+    const double* c = cands + order[e] * dim;
+    for (uint64_t i = 0; i < dim; ++i) mean[i] += c[i];
+  }
+  for (uint64_t i = 0; i < dim; ++i) mean[i] /= (double)elite;
+  for (uint64_t i = 0; i < dim; ++i) var[i] = 0.0;
+  for (uint64_t e = 0; e < elite; ++e) {
+    const double* c = cands + order[e] * dim;
+    for (uint64_t i = 0; i < dim; ++i) {
+      const double dd = c[i] - mean[i];
+      var[i] += dd * dd;
+    }
+  }
+  for (uint64_t i = 0; i < dim; ++i) var[i] /= (double)elite;
+  const double nn = *noise * noise_decay;
+  *noise = noise_final < nn ? nn : noise_final; /* std::max(noise_final, noise * decay) */
+  free(order);
   return 0;
 }
 
 /* ------------------------------------------------------------------ SAC (algos.hpp:470-837) */
 struct ora_sac {
   uint64_t n, ds, da;
+  uint64_t nc;  /* critic population: n, or 1 in shared-critic mode (algos.hpp:506) */
+  int shared;
   ora_net pol, cri;
   float bound;
   uint64_t seed;
@@ -690,10 +975,13 @@ static const ora_net* sac_shape(const ora_sac* st, int net) {
   return net == 0 ? &st->pol : &st->cri;
 }
 
-ora_sac* ora_sac_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
-                        uint32_t nh, double bound, uint64_t seed) {
+ora_sac* ora_sac_create_mode(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
+                             uint32_t nh, double bound, uint64_t seed, int shared) {
   ora_sac* st = (ora_sac*)calloc(1, sizeof(ora_sac));
   st->n = n;
+  st->shared = shared ? 1 : 0;
+  st->nc = shared ? 1 : n;
+  const uint64_t nc = st->nc;
   st->ds = ds;
   st->da = da;
   st->bound = (float)bound;
@@ -708,18 +996,19 @@ ora_sac* ora_sac_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hi
   net_make(&st->cri, dims, (int)nh + 2, ACT_NONE, 1.0f);
   for (int k = 0; k < 6; ++k) {
     if (k == 1) continue;
-    st->net[k] = (float*)calloc(n * sac_shape(st, k)->P, sizeof(float));
+    st->net[k] = (float*)calloc((k == 0 ? n : nc) * sac_shape(st, k)->P, sizeof(float));
   }
   net_init(&st->pol, st->net[0], n, ora_mix64(seed ^ 0xD4));
-  net_init(&st->cri, st->net[2], n, ora_mix64(seed ^ 0xE5));
-  net_init(&st->cri, st->net[3], n, ora_mix64(seed ^ 0xF6));
-  memcpy(st->net[4], st->net[2], sizeof(float) * n * st->cri.P);
-  memcpy(st->net[5], st->net[3], sizeof(float) * n * st->cri.P);
+  net_init(&st->cri, st->net[2], nc, ora_mix64(seed ^ 0xE5));
+  net_init(&st->cri, st->net[3], nc, ora_mix64(seed ^ 0xF6));
+  memcpy(st->net[4], st->net[2], sizeof(float) * nc * st->cri.P);
+  memcpy(st->net[5], st->net[3], sizeof(float) * nc * st->cri.P);
   for (int k = 0; k < 3; ++k) {
     const uint64_t P = (k == 0) ? st->pol.P : st->cri.P;
-    st->am[k] = (float*)calloc(n * P, sizeof(float));
-    st->av[k] = (float*)calloc(n * P, sizeof(float));
-    st->at[k] = (int64_t*)calloc(n, sizeof(int64_t));
+    const uint64_t cnt = (k == 0) ? n : nc;
+    st->am[k] = (float*)calloc(cnt * P, sizeof(float));
+    st->av[k] = (float*)calloc(cnt * P, sizeof(float));
+    st->at[k] = (int64_t*)calloc(cnt, sizeof(int64_t));
   }
   st->log_alpha = (float*)calloc(n, sizeof(float));
   st->alpha_m = (float*)calloc(n, sizeof(float));
@@ -729,6 +1018,11 @@ ora_sac* ora_sac_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hi
   st->streams = (uint64_t*)calloc(n, sizeof(uint64_t));
   for (uint64_t i = 0; i < n; ++i) st->streams[i] = i;
   return st;
+}
+
+ora_sac* ora_sac_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
+                        uint32_t nh, double bound, uint64_t seed) {
+  return ora_sac_create_mode(n, ds, da, hidden, nh, bound, seed, 0);
 }
 
 void ora_sac_destroy(ora_sac* st) {
@@ -902,8 +1196,9 @@ static void sac_target(const ora_sac* st, const float* s2, const float* r, const
   for (uint64_t k = 0; k < nb * da; ++k) x[k] *= st->bound;
   float* sa2 = concat(s2, x, n, b, ds, da);
   ora_cache c1, c2;
-  mlp_forward(&st->cri, st->net[4], n, b, sa2, &c1);
-  mlp_forward(&st->cri, st->net[5], n, b, sa2, &c2);
+  const uint64_t rc = st->shared ? nb : b; /* critic_forward folding (algos.hpp:219-227) */
+  mlp_forward(&st->cri, st->net[4], st->nc, rc, sa2, &c1);
+  mlp_forward(&st->cri, st->net[5], st->nc, rc, sa2, &c2);
   for (uint64_t m = 0; m < n; ++m) {
     const float g = (float)HY(hyper, SH_GAMMA, n, m);
     const float rs = (float)HY(hyper, SH_RS, n, m);
@@ -938,10 +1233,12 @@ int ora_sac_step(ora_sac* st, const float* s, const float* a, const float* r, co
   sac_target(st, s2, r, d, b, hyper, y);
   float* sa = concat(s, a, n, b, ds, da);
   float* g = (float*)malloc(sizeof(float) * n * (Pc > Pp ? Pc : Pp));
+  const uint64_t nc = st->nc, rc = st->shared ? nb : b;
+  if (losses) memset(losses, 0, sizeof(double) * 3 * n);
   for (int c = 0; c < 2; ++c) {
     float* params = st->net[2 + c];
-    mse_grads(&st->cri, params, n, b, sa, y, g, losses ? losses + c * n : NULL);
-    for (uint64_t m = 0; m < n; ++m) {
+    mse_grads(&st->cri, params, nc, rc, sa, y, g, losses ? losses + c * n : NULL);
+    for (uint64_t m = 0; m < nc; ++m) {
       adam_member(params + m * Pc, g + m * Pc, st->am[1 + c] + m * Pc, st->av[1 + c] + m * Pc,
                   &st->at[1 + c][m], Pc, HY(hyper, SH_CLR, n, m));
     }
@@ -967,8 +1264,8 @@ int ora_sac_step(ora_sac* st, const float* s, const float* a, const float* r, co
   }
   float* spa = concat(s, act, n, b, ds, da);
   ora_cache c1, c2;
-  mlp_forward(&st->cri, st->net[2], n, b, spa, &c1);
-  mlp_forward(&st->cri, st->net[3], n, b, spa, &c2);
+  mlp_forward(&st->cri, st->net[2], nc, rc, spa, &c1);
+  mlp_forward(&st->cri, st->net[3], nc, rc, spa, &c2);
   float* gq1 = (float*)calloc(nb, sizeof(float));
   float* gq2 = (float*)calloc(nb, sizeof(float));
   float* lw = (float*)malloc(sizeof(float) * nb);
@@ -1024,7 +1321,7 @@ int ora_sac_step(ora_sac* st, const float* s, const float* a, const float* r, co
     adam_member(&st->log_alpha[m], &ga1, &st->alpha_m[m], &st->alpha_v[m], &st->alpha_t[m], 1,
                 HY(hyper, SH_ALR, n, m));
   }
-  for (uint64_t m = 0; m < n; ++m) {
+  for (uint64_t m = 0; m < nc; ++m) { /* shared: {tau[0]} on the one critic (:827-834) */
     const double tau = HY(hyper, SH_TAU, n, m);
     polyak_member(st->net[4] + m * Pc, st->net[2] + m * Pc, Pc, tau);
     polyak_member(st->net[5] + m * Pc, st->net[3] + m * Pc, Pc, tau);
@@ -1228,6 +1525,7 @@ int ora_td3_pbt_evolve(ora_td3* st, const double* rings, const uint32_t* counts,
   const uint64_t n = st->n;
   const int cnt = ora_pbt_plan(rings, counts, n, ring_cap, 0.3, rng_key, rng_next, replaced, donors);
   if (cnt <= 0) return cnt;
+  if (st->shared) return -3; /* copy_member on the 1-member critic: UsageError (net_pop.hpp:194) */
   for (int i = 0; i < cnt; ++i) {
     const uint64_t dst = replaced[i], src = donors[i];
     for (int k = 0; k < 6; ++k) {
@@ -1255,6 +1553,7 @@ int ora_sac_pbt_evolve(ora_sac* st, const double* rings, const uint32_t* counts,
   const uint64_t n = st->n;
   const int cnt = ora_pbt_plan(rings, counts, n, ring_cap, 0.3, rng_key, rng_next, replaced, donors);
   if (cnt <= 0) return cnt;
+  if (st->shared) return -3; /* copy_member on the 1-member critic: UsageError (net_pop.hpp:194) */
   for (int i = 0; i < cnt; ++i) {
     const uint64_t dst = replaced[i], src = donors[i];
     for (int k = 0; k < 6; ++k) {

@@ -40,6 +40,10 @@ double ora_normal_pair(uint64_t key, uint64_t counter);
 typedef struct ora_td3 ora_td3;
 ora_td3* ora_td3_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
                         uint32_t nh, double bound, uint64_t seed);
+/* shared != 0: PopMode::kSharedCritic -- critic nets (2..5) and their Adam states have ONE
+ * member; the critic loss averages over the population folded into the batch */
+ora_td3* ora_td3_create_mode(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
+                             uint32_t nh, double bound, uint64_t seed, int shared);
 void ora_td3_destroy(ora_td3* st);
 uint64_t ora_td3_param_count(const ora_td3* st, int net);
 void ora_td3_get_net(const ora_td3* st, int net, uint64_t m, float* out);
@@ -57,6 +61,36 @@ void ora_td3_act(const ora_td3* st, const float* obs, uint64_t rows, const doubl
 int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, const float* s2,
                  const float* d, uint64_t b, const double* hyper, const char* policy_mask,
                  double* losses);
+/* shared-critic losses: losses[0] = critic1 MSE over all n*b rows, losses[n] = critic2 */
+
+/* DvD (evolve.hpp:304-525).  probe: [m_states][obs] doubles (DvDConfig::probe_states, cast to
+ * float as dvd_policy_hook does); lambda = dvd_lambda(step, schedule). */
+typedef struct {
+  const double* probe;
+  uint64_t m_states;
+  double length_scale, jitter, lambda;
+} ora_dvd;
+/* td3_update_step with the dvd_policy_hook (NULL: none).  returns 0, -2, or -10 when the
+ * hook's kernel matrix is singular (DegeneratePopulationError; the critic step has run). */
+int ora_td3_step_hook(ora_td3* st, const float* s, const float* a, const float* r,
+                      const float* s2, const float* d, uint64_t b, const double* hyper,
+                      const char* policy_mask, double* losses, const ora_dvd* dvd);
+double ora_dvd_lambda(uint64_t step, double start, double end, uint64_t horizon);
+/* dvd_loss: emb [n][dim]; grad [n][dim] (optional).  0, -2 (ConfigError), -10 (Degenerate) */
+int ora_dvd_loss(const double* emb, uint64_t n, uint64_t dim, double length_scale, double jitter,
+                 double lambda, double* loss, double* logdet, double* grad);
+double ora_median_pairwise_distance(const double* emb, uint64_t n, uint64_t dim);
+/* dvd_embed: out [n][m_states*da] */
+void ora_td3_dvd_embed(const ora_td3* st, const double* probe, uint64_t m_states, float* out);
+
+/* CEM (evolve.hpp:221-297): cem_sample draws count x dim normals from the RngSequence
+ * (key, *next), candidate-major; cem_update refits mean / var to the elites and decays noise.
+ * returns 0 or -2 (ConfigError: fewer than 2, odd count, non-finite score). */
+void ora_cem_sample(const double* mean, const double* var, double noise, uint64_t dim,
+                    uint64_t count, uint64_t key, uint64_t* next, double* out);
+int ora_cem_update(double* mean, double* var, double* noise, double noise_final,
+                   double noise_decay, double elite_fraction, uint64_t dim, const double* cands,
+                   const double* scores, uint64_t count);
 
 /* SAC population state (algos.hpp:473-521).  nets: 0 policy, 2 critic1, 3 critic2,
  * 4 critic1_target, 5 critic2_target.  Hyper arrays are [7][n]: policy_lr, critic_lr, alpha_lr,
@@ -64,6 +98,8 @@ int ora_td3_step(ora_td3* st, const float* s, const float* a, const float* r, co
 typedef struct ora_sac ora_sac;
 ora_sac* ora_sac_create(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
                         uint32_t nh, double bound, uint64_t seed);
+ora_sac* ora_sac_create_mode(uint64_t n, uint64_t ds, uint64_t da, const uint64_t* hidden,
+                             uint32_t nh, double bound, uint64_t seed, int shared);
 void ora_sac_destroy(ora_sac* st);
 uint64_t ora_sac_param_count(const ora_sac* st, int net);
 void ora_sac_get_net(const ora_sac* st, int net, uint64_t m, float* out);

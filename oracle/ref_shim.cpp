@@ -159,6 +159,9 @@ int guarded(F&& f) {
   } catch (const DataStarvationError& e) {
     g_err = e.what();
     return -6;
+  } catch (const DegeneratePopulationError& e) {
+    g_err = e.what();
+    return -10;
   } catch (const std::exception& e) {
     g_err = e.what();
     return -9;
@@ -187,6 +190,44 @@ float ref_tanhf(float x) { return std::tanh(x); }
                                  std::uint64_t seed) {                                           \
     return new Td3State<T>(                                                                      \
         make_td3_state<T>(n, ds, da, to_dims(hidden, nh), static_cast<T>(bound), seed));         \
+  }                                                                                              \
+  void* ref_td3##SUFFIX##_create_mode(std::uint64_t n, std::uint64_t ds, std::uint64_t da,       \
+                                      const std::uint64_t* hidden, std::uint32_t nh,             \
+                                      double bound, std::uint64_t seed, int shared) {            \
+    return new Td3State<T>(make_td3_state<T>(                                                    \
+        n, ds, da, to_dims(hidden, nh), static_cast<T>(bound), seed,                             \
+        shared ? PopMode::kSharedCritic : PopMode::kIndependent));                               \
+  }                                                                                              \
+  /* td3_update_step with dvd_policy_hook(cfg, step) (evolve.hpp:507-525) */                     \
+  int ref_td3##SUFFIX##_step_dvd(void* h, const T* s, const T* a, const T* r, const T* s2,       \
+                                 const T* d, std::uint64_t b, const double* hyper,               \
+                                 const char* policy_mask, const double* probe,                   \
+                                 std::uint64_t m_states, double length_scale, double jitter,     \
+                                 double lam_start, double lam_end, std::uint64_t horizon,        \
+                                 std::uint64_t step) {                                           \
+    return guarded([&] {                                                                         \
+      auto& st = *static_cast<Td3State<T>*>(h);                                                  \
+      const std::size_t n = st.members();                                                        \
+      auto batch = batch_from(s, a, r, s2, d, n, b, st.obs_dim, st.act_dim);                     \
+      auto hy = td3_hyper_from(hyper, n);                                                        \
+      DvDConfig cfg;                                                                             \
+      cfg.probe_states.assign(probe, probe + m_states * st.obs_dim);                             \
+      cfg.m_states = m_states;                                                                   \
+      cfg.length_scale = length_scale;                                                           \
+      cfg.jitter = jitter;                                                                       \
+      cfg.schedule = LambdaSchedule{lam_start, lam_end, horizon};                                \
+      PolicyGradHook<T> hook = dvd_policy_hook<T>(cfg, step);                                    \
+      std::vector<char> mask;                                                                    \
+      if (policy_mask) mask.assign(policy_mask, policy_mask + n);                                \
+      td3_update_step<T>(st, batch, hy, &hook, policy_mask ? &mask : nullptr);                   \
+    });                                                                                          \
+  }                                                                                              \
+  void ref_td3##SUFFIX##_dvd_embed(void* h, const double* probe, std::uint64_t m_states,         \
+                                   T* out) {                                                     \
+    auto& st = *static_cast<Td3State<T>*>(h);                                                    \
+    std::vector<T> pr(probe, probe + m_states * st.obs_dim);                                     \
+    auto e = dvd_embed(st.policy, pr, m_states);                                                 \
+    std::memcpy(out, e.data.data(), e.data.size() * sizeof(T));                                  \
   }                                                                                              \
   void ref_td3##SUFFIX##_destroy(void* h) { delete static_cast<Td3State<T>*>(h); }               \
   void* ref_td3##SUFFIX##_clone(void* h) {                                                       \
@@ -281,6 +322,13 @@ PBRL_REF_TD3(d, double)
                                  std::uint64_t seed) {                                           \
     return new SacState<T>(                                                                      \
         make_sac_state<T>(n, ds, da, to_dims(hidden, nh), static_cast<T>(bound), seed));         \
+  }                                                                                              \
+  void* ref_sac##SUFFIX##_create_mode(std::uint64_t n, std::uint64_t ds, std::uint64_t da,       \
+                                      const std::uint64_t* hidden, std::uint32_t nh,             \
+                                      double bound, std::uint64_t seed, int shared) {            \
+    return new SacState<T>(make_sac_state<T>(                                                    \
+        n, ds, da, to_dims(hidden, nh), static_cast<T>(bound), seed,                             \
+        shared ? PopMode::kSharedCritic : PopMode::kIndependent));                               \
   }                                                                                              \
   void ref_sac##SUFFIX##_destroy(void* h) { delete static_cast<SacState<T>*>(h); }               \
   std::uint64_t ref_sac##SUFFIX##_param_count(void* h, int net) {                                \
@@ -575,5 +623,62 @@ int ref_bench_update(int mode, int algo, std::uint64_t n, std::uint64_t k, std::
 }
 
 std::uint64_t ref_kernel_invocations() { return kernel_invocations().load(); }
+
+// ---------------------------------------------------------------- DvD / CEM (evolve.hpp:221-525)
+double ref_dvd_lambda(std::uint64_t step, double start, double end, std::uint64_t horizon) {
+  return dvd_lambda(step, LambdaSchedule{start, end, horizon});
+}
+
+int ref_dvd_loss(const double* emb, std::uint64_t n, std::uint64_t dim, double length_scale,
+                 double jitter, double lambda, double* loss, double* logdet, double* grad) {
+  return guarded([&] {
+    PopTensor<double> e = PopTensor<double>::zeros({n, dim});
+    std::memcpy(e.data.data(), emb, n * dim * sizeof(double));
+    DvdLossOut out = dvd_loss(e, length_scale, jitter, lambda);
+    *loss = out.loss;
+    *logdet = out.logdet;
+    std::memcpy(grad, out.grad.data.data(), n * dim * sizeof(double));
+  });
+}
+
+double ref_median_pairwise_distance(const double* emb, std::uint64_t n, std::uint64_t dim) {
+  PopTensor<double> e = PopTensor<double>::zeros({n, dim});
+  std::memcpy(e.data.data(), emb, n * dim * sizeof(double));
+  return median_pairwise_distance(e);
+}
+
+// cem_sample from RngSequence(seed, stream_id, use, step) advanced to *next
+void ref_cem_sample(const double* mean, const double* var, double noise, std::uint64_t dim,
+                    std::uint64_t count, std::uint64_t key, std::uint64_t* next, double* out) {
+  CEMState st;
+  st.mean.assign(mean, mean + dim);
+  st.var.assign(var, var + dim);
+  st.noise = noise;
+  RngSequence rng(RngStream{key});
+  rng.next = *next;
+  auto c = cem_sample(st, count, rng);
+  for (std::size_t i = 0; i < count; ++i) std::memcpy(out + i * dim, c[i].data(), dim * 8);
+  *next = rng.next;
+}
+
+int ref_cem_update(double* mean, double* var, double* noise, double noise_final,
+                   double noise_decay, double elite_fraction, std::uint64_t dim,
+                   const double* cands, const double* scores, std::uint64_t count) {
+  return guarded([&] {
+    CEMState st;
+    st.mean.assign(mean, mean + dim);
+    st.var.assign(var, var + dim);
+    st.noise = *noise;
+    st.noise_final = noise_final;
+    st.noise_decay = noise_decay;
+    st.elite_fraction = elite_fraction;
+    std::vector<std::vector<double>> c(count);
+    for (std::size_t i = 0; i < count; ++i) c[i].assign(cands + i * dim, cands + (i + 1) * dim);
+    cem_update(st, c, std::vector<double>(scores, scores + count));
+    std::memcpy(mean, st.mean.data(), dim * 8);
+    std::memcpy(var, st.var.data(), dim * 8);
+    *noise = st.noise;
+  });
+}
 
 }  // extern "C"
