@@ -38,6 +38,7 @@ extern "C" {
 #define PBRL_E_STARVATION (-6)  /* DataStarvationError */
 #define PBRL_E_CUDA (-7)
 #define PBRL_E_NCCL (-8)
+#define PBRL_E_DEGENERATE (-9)  /* DegeneratePopulationError (DvD kernel matrix singular) */
 
 #define PBRL_ALGO_TD3 0
 #define PBRL_ALGO_SAC 1
@@ -54,6 +55,11 @@ extern "C" {
 #define PBRL_NET_CRITIC2 3
 #define PBRL_NET_CRITIC1_TARGET 4
 #define PBRL_NET_CRITIC2_TARGET 5
+
+/* PopMode (algos.hpp:26): one critic pair per member, or ONE shared critic pair whose batch is
+ * the population folded into rows (CEM-RL / DvD; critic_forward, algos.hpp:219-233) */
+#define PBRL_MODE_INDEPENDENT 0
+#define PBRL_MODE_SHARED_CRITIC 1
 
 #define PBRL_REPLAY_PER_AGENT 0 /* BufferMode::kPerAgent (replay.hpp:175) */
 #define PBRL_REPLAY_SHARED 1    /* BufferMode::kShared */
@@ -74,6 +80,7 @@ typedef struct {
   int device;               /* CUDA ordinal */
   uint64_t member_offset;   /* global id of local member 0 (0 unless sharded) */
   uint64_t n_global;        /* population size across shards (0 = n) */
+  int mode;                 /* PBRL_MODE_* (make_td3_state / make_sac_state `mode`) */
 } pbrl_pop_desc;
 
 /* One population batch (TransitionBatch, algos.hpp:14-24): s [n][B][obs], a [n][B][act],
@@ -251,6 +258,9 @@ typedef struct {
   int (*allgather_f64)(void* ctx, const double* send, uint64_t count, double* recv);
   /* all ops of this rank as one group (like ncclGroupStart / ncclGroupEnd) */
   int (*exchange)(void* ctx, const pbrl_p2p_op* ops, uint32_t n_ops);
+  /* in-place sum over the ranks of buf[count] (shared-critic gradients; may be NULL when no
+   * shared-critic population is attached) */
+  int (*allreduce_f32)(void* ctx, float* buf, uint64_t count);
 } pbrl_comm_ops;
 
 /* NCCL transport over NVLink / NVSwitch: rank 0 calls pbrl_nccl_unique_id, the caller
@@ -271,6 +281,51 @@ int pbrl_pbt_evolve_sharded(pbrl_pop* pop, pbrl_comm* comm, const double* local_
                             int local_ready, double trunc, uint64_t rng_key, uint64_t* rng_next,
                             uint64_t* replaced, uint64_t* donors, uint32_t* count,
                             double* exchange_ms);
+
+/* ---- shared critic across shards: the per-step critic-gradient all-reduce.
+ * A PBRL_MODE_SHARED_CRITIC population sharded over `world` ranks (member_offset / n_global as
+ * above) keeps an identical replica of the one critic pair on every rank; each step sums the
+ * critic gradients of the local folded batches over the ranks (NCCL all-reduce, or the host
+ * transport's allreduce_f32) before the critic Adam, so every replica takes the same step the
+ * unsharded population would (loss scale 2 / (n_global * B), mse_loss_grads algos.hpp:288-314).
+ * comm = NULL detaches.  The steps of an attached population run eagerly (no step graph). */
+int pbrl_attach_comm(pbrl_pop* pop, pbrl_comm* comm);
+
+/* ---- DvD (evolve.hpp:304-525): log-determinant diversity over behavioural embeddings.
+ * pbrl_set_dvd installs dvd_policy_hook(cfg, step) for the following update calls (TD3):
+ * probe [m_states][obs] doubles (DvDConfig::probe_states), lambda = dvd_lambda(step, schedule)
+ * (lambda 0 or probe NULL: no hook).  On a step where some policy updates, the hook's gradient of
+ * -lambda * logdet(K + jitter I) through the policies' embeddings is added to the policy
+ * gradients before the policy Adam (add_scaled, optim.hpp:75-85).  A singular kernel matrix
+ * fails the update with PBRL_E_DEGENERATE before the step runs. */
+int pbrl_set_dvd(pbrl_pop* pop, const double* probe, uint64_t m_states, double length_scale,
+                 double jitter, double lambda);
+/* dvd_embed (:334-339): out [n][m_states * act] deterministic actions on the probe states */
+int pbrl_dvd_embed(pbrl_pop* pop, const double* probe, uint64_t m_states, float* out);
+/* dvd_loss (:425-478) on host data: emb [n][dim]; grad [n][dim] (may be NULL) */
+int pbrl_dvd_loss(const double* emb, uint64_t n, uint64_t dim, double length_scale, double jitter,
+                  double lambda, double* loss, double* logdet, double* grad);
+int pbrl_median_pairwise_distance(const double* emb, uint64_t n, uint64_t dim, double* out);
+int pbrl_dvd_lambda(uint64_t step, double start, double end, uint64_t horizon, double* out);
+
+/* ---- CEM (evolve.hpp:221-297) over the flat policy vectors of a TD3 population, on device.
+ * pbrl_cem_create: cem_init(mean, init_var) with mean [P] doubles, or NULL for
+ * flatten_member(policy, 0) as run_training does (pipeline_run.hpp:159-162).
+ * pbrl_cem_resample: cem_resample (pipeline_run.hpp:148-158) -- cem_sample(cem, n, rng) with
+ * the RngSequence (rng_key, *rng_next), every candidate written into its member's policy, targets
+ * set to the policies, policy Adam state reset; the candidates are kept for the refit.
+ * pbrl_cem_update: cem_update(cem, candidates, scores[n]) -- elites by stable score order.
+ * Single-shard populations only. */
+typedef struct pbrl_cem pbrl_cem;
+int pbrl_cem_create(pbrl_pop* pop, const double* mean, double init_var, pbrl_cem** out);
+int pbrl_cem_destroy(pbrl_cem* cem);
+/* CEMState fields (defaults 1e-2 / 1e-3 / 0.999 / 0.5) */
+int pbrl_cem_set_params(pbrl_cem* cem, double noise, double noise_final, double noise_decay,
+                        double elite_fraction);
+int pbrl_cem_get(pbrl_cem* cem, double* mean, double* var, double* noise);
+int pbrl_cem_resample(pbrl_cem* cem, uint64_t rng_key, uint64_t* rng_next);
+int pbrl_cem_candidates(pbrl_cem* cem, double* out /* [n][P] */);
+int pbrl_cem_update(pbrl_cem* cem, const double* scores, uint64_t count);
 
 /* ---- synthetic inputs: make_synthetic_batches (bench.hpp:69-93) generated on the device.
  * out: count device batches; each field is a device pointer to [count][n][b][dim] floats laid out

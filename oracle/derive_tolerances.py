@@ -76,12 +76,32 @@ CASES = {
     "C_sac_pop32": dict(algo="sac", n=32, hidden=[256, 256], batch=256, K=4, seed=7),
     # config E: 3 x 512, batch 1024, pop 8
     "E_td3_pop8": dict(algo="td3", n=8, hidden=[512, 512, 512], batch=1024, K=2, seed=7),
+    # shared-critic mode: one critic pair on the folded batch
+    "S_td3_shared_pop8": dict(algo="td3", n=8, hidden=[256, 256], batch=256, K=4, seed=7,
+                              shared=True),
+    "S_td3_shared_pop80": dict(algo="td3", n=80, hidden=[256, 256], batch=256, K=3, seed=7,
+                               shared=True),
+    "S_sac_shared_pop8": dict(algo="sac", n=8, hidden=[256, 256], batch=256, K=4, seed=7,
+                              shared=True),
+    # shared critic + the DvD policy-gradient hook (10 probe states, lambda 0.5)
+    "S_td3_dvd_pop8": dict(algo="td3", n=8, hidden=[256, 256], batch=256, K=4, seed=7,
+                           shared=True, dvd=dict(ms=10, length_scale=0.7, lam=0.5, seed=3)),
 }
+
+
+def dvd_cfg(d, ds):
+    """the DvD hook of a parity case: probe states U[-1, 1) from numpy's PCG64(seed)"""
+    if not d:
+        return None
+    probe = np.random.default_rng(d["seed"]).uniform(-1.0, 1.0, (d["ms"], ds))
+    return {"probe": probe, "length_scale": d["length_scale"], "jitter": 1e-6,
+            "lam_start": d["lam"], "lam_end": d["lam"], "horizon": 1, "step": 0}
 
 
 def case_args(c):
     return dict(algo=c["algo"], n=c["n"], hidden=list(c["hidden"]), batch=c["batch"], K=c["K"],
-                seed=c["seed"], ds=c.get("ds", 17), da=c.get("da", 6), ratio=c.get("ratio"))
+                seed=c["seed"], ds=c.get("ds", 17), da=c.get("da", 6), ratio=c.get("ratio"),
+                shared=bool(c.get("shared", False)), dvd=c.get("dvd"))
 
 
 def hyper_for(algo, n, da, ratio):
@@ -91,18 +111,23 @@ def hyper_for(algo, n, da, ratio):
     return hy
 
 
-def run(lib, algo, n, hidden, batch, K, seed, ds, da, ratio, dtype=np.float32, raw=None):
+def run(lib, algo, n, hidden, batch, K, seed, ds, da, ratio, dtype=np.float32, raw=None,
+        shared=False, dvd=None):
     """K steps on `lib` (Oracle or Ref); returns (losses [K][3][n] or [K][3], w0, wK)."""
     nets = TD3_NETS if algo == "td3" else SAC_NETS
     make = lib.td3 if algo == "td3" else lib.sac
-    st = make(n, ds, da, hidden, 1.0, seed) if isinstance(lib, Oracle) else \
-        make(n, ds, da, hidden, 1.0, seed, dtype=dtype)
+    st = make(n, ds, da, hidden, 1.0, seed, shared=shared) if isinstance(lib, Oracle) else \
+        make(n, ds, da, hidden, 1.0, seed, dtype=dtype, shared=shared)
     hy = hyper_for(algo, n, da, ratio)
     w0 = {net: st.get_net(net).astype(np.float64) for net in nets}
     losses = []
     for k in range(K):
         b = tuple(x[k] for x in raw)
-        losses.append(st.step(b, hy) if isinstance(lib, Oracle)
+        if dvd:
+            lk = st.step(b, hy, dvd=dvd_cfg(dvd, ds))
+            losses.append(lk if isinstance(lib, Oracle) else np.zeros(3))
+            continue
+        losses.append(st.step(b, hy) if isinstance(lib, Oracle) or shared
                       else st.step(b, hy, want_losses=True))
     wk = {net: st.get_net(net).astype(np.float64) for net in nets}
     return np.asarray(losses), w0, wk

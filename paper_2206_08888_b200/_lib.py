@@ -31,7 +31,7 @@ class PopDesc(C.Structure):
     _fields_ = [("algo", C.c_int), ("n", u64), ("obs_dim", u64), ("act_dim", u64),
                 ("n_hidden", u32), ("hidden", u64p), ("action_bound", dbl), ("seed", u64),
                 ("precision", C.c_int), ("device", C.c_int), ("member_offset", u64),
-                ("n_global", u64)]
+                ("n_global", u64), ("mode", C.c_int)]
 
 
 class Batch(C.Structure):
@@ -44,14 +44,29 @@ class P2POp(C.Structure):
 
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, vp, f64p, u64, f64p)
 EXCHANGE_FN = C.CFUNCTYPE(C.c_int, vp, C.POINTER(P2POp), u32)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, vp, f32p, u64)
 
 
 class CommOps(C.Structure):
-    _fields_ = [("ctx", vp), ("allgather_f64", ALLGATHER_FN), ("exchange", EXCHANGE_FN)]
+    _fields_ = [("ctx", vp), ("allgather_f64", ALLGATHER_FN), ("exchange", EXCHANGE_FN),
+                ("allreduce_f32", ALLREDUCE_FN)]
 
 
 # name -> (restype, argtypes); every function returns an int status
 SIGNATURES = {
+    "pbrl_attach_comm": [vp, vp],
+    "pbrl_set_dvd": [vp, f64p, u64, dbl, dbl, dbl],
+    "pbrl_dvd_embed": [vp, f64p, u64, f32p],
+    "pbrl_dvd_loss": [f64p, u64, u64, dbl, dbl, dbl, f64p, f64p, f64p],
+    "pbrl_median_pairwise_distance": [f64p, u64, u64, f64p],
+    "pbrl_dvd_lambda": [u64, dbl, dbl, u64, f64p],
+    "pbrl_cem_create": [vp, f64p, dbl, C.POINTER(vp)],
+    "pbrl_cem_destroy": [vp],
+    "pbrl_cem_set_params": [vp, dbl, dbl, dbl, dbl],
+    "pbrl_cem_get": [vp, f64p, f64p, f64p],
+    "pbrl_cem_resample": [vp, u64, C.POINTER(u64)],
+    "pbrl_cem_candidates": [vp, f64p],
+    "pbrl_cem_update": [vp, f64p, u64],
     "pbrl_pop_create": [C.POINTER(PopDesc), C.POINTER(vp)],
     "pbrl_pop_destroy": [vp],
     "pbrl_last_error": [C.c_char_p, C.c_size_t],

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <fstream>
+#include <memory>
 #include <string>
 #include <unordered_map>
 
@@ -50,6 +51,19 @@ Pop* P(pbrl_pop* h) {
 
 void check_member(const Pop* p, uint64_t m, const char* what) {
   if (m >= static_cast<uint64_t>(p->n)) PBRL_THROW(PBRL_E_USAGE, std::string(what) + ": index out of range");
+}
+
+// member index of one network (a shared critic has ONE member, algos.hpp:197)
+void check_net_member(const Pop* p, int net, uint64_t m, const char* what) {
+  if (m >= static_cast<uint64_t>(p->net_members(net)))
+    PBRL_THROW(PBRL_E_USAGE, std::string(what) + ": index out of range");
+}
+
+// per-member splitting / exchange of whole agents (slice_member, PBT copies) has no meaning for
+// a shared critic (algos.hpp:427-429, copy_member's range check net_pop.hpp:193-195)
+void check_independent(const Pop* p, const char* what) {
+  if (p->shared)
+    PBRL_THROW(PBRL_E_USAGE, std::string(what) + ": shared-critic state cannot be split per member");
 }
 
 // RngSequence (rng.hpp:74-95) on the host, used for the PBT hyper re-draws so they match the
@@ -101,9 +115,9 @@ float* Pop::net_row(int net, uint64_t member) {
       if (algo != PBRL_ALGO_TD3) PBRL_THROW(PBRL_E_USAGE, "SAC has no policy target");
       return pol_t.p + member * pol.stride;
     case PBRL_NET_CRITIC1: return cri_p.p + member * cri.stride;
-    case PBRL_NET_CRITIC2: return cri_p.p + (n + member) * cri.stride;
+    case PBRL_NET_CRITIC2: return cri_p.p + (ncrit + member) * cri.stride;
     case PBRL_NET_CRITIC1_TARGET: return cri_t.p + member * cri.stride;
-    case PBRL_NET_CRITIC2_TARGET: return cri_t.p + (n + member) * cri.stride;
+    case PBRL_NET_CRITIC2_TARGET: return cri_t.p + (ncrit + member) * cri.stride;
     default: PBRL_THROW(PBRL_E_USAGE, "unknown network id");
   }
 }
@@ -130,9 +144,10 @@ V get(std::istream& is) {
 // the whole population of one network, member rows in flatten_member order
 std::vector<float> net_rows(Pop* p, int net) {
   const NetShape& sh = p->net_shape(net);
-  std::vector<float> flat(static_cast<size_t>(p->n) * sh.P);
+  const int rows = p->net_members(net);
+  std::vector<float> flat(static_cast<size_t>(rows) * sh.P);
   CUDA_CHECK(cudaMemcpy2DAsync(flat.data(), sh.P * 4, p->net_row(net, 0), sh.stride * 4,
-                               sh.P * 4, p->n, cudaMemcpyDeviceToHost, p->stream));
+                               sh.P * 4, rows, cudaMemcpyDeviceToHost, p->stream));
   p->sync();
   return flat;
 }
@@ -144,7 +159,7 @@ void save_net(Pop* p, int net, std::ostream& os) {
   const std::vector<float> flat = net_rows(p, net);
   os.write(kNetMagic, sizeof(kNetMagic));
   put<uint32_t>(os, 4);
-  put<uint64_t>(os, static_cast<uint64_t>(p->n));
+  put<uint64_t>(os, static_cast<uint64_t>(p->net_members(net)));
   put<uint64_t>(os, static_cast<uint64_t>(sh.depth + 1));
   for (int l = 0; l <= sh.depth; ++l) put<uint64_t>(os, static_cast<uint64_t>(sh.dims[l]));
   put<uint8_t>(os, static_cast<uint8_t>(sh.out_act));
@@ -166,9 +181,10 @@ void load_net(Pop* p, int net, std::istream& is) {
       PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: file stores " + std::to_string(prec * 8) +
                                     "-bit values but 32-bit was requested");
     const uint64_t fn = get<uint64_t>(is), nd = get<uint64_t>(is);
-    if (fn != static_cast<uint64_t>(p->n))
+    const int rows = p->net_members(net);
+    if (fn != static_cast<uint64_t>(rows))
       PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: population size " + std::to_string(fn) +
-                                    " != " + std::to_string(p->n));
+                                    " != " + std::to_string(rows));
     if (nd != static_cast<uint64_t>(sh.depth + 1))
       PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: network depth mismatch");
     for (int l = 0; l <= sh.depth; ++l)
@@ -179,10 +195,10 @@ void load_net(Pop* p, int net, std::istream& is) {
     if (act != static_cast<uint8_t>(sh.out_act) ||
         static_cast<float>(scale) != sh.out_scale)
       PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: output activation / scale mismatch");
-    std::vector<float> flat(static_cast<size_t>(p->n) * sh.P);
+    std::vector<float> flat(static_cast<size_t>(rows) * sh.P);
     is.read(reinterpret_cast<char*>(flat.data()), static_cast<std::streamsize>(flat.size() * 4));
     if (!is) PBRL_THROW(PBRL_E_CONFIG, "load_checkpoint: truncated file");
-    CUDA_CHECK(cudaMemcpy2DAsync(dst0, sh.stride * 4, flat.data(), sh.P * 4, sh.P * 4, p->n,
+    CUDA_CHECK(cudaMemcpy2DAsync(dst0, sh.stride * 4, flat.data(), sh.P * 4, sh.P * 4, rows,
                                  cudaMemcpyHostToDevice, p->stream));
   p->weights_dirty = true;
   p->weights_written_outside();
@@ -231,8 +247,10 @@ int pbrl_serialize_state(pbrl_pop* pop, const char* path) {
     if (!path || !os) PBRL_THROW(PBRL_E_CONFIG, std::string("serialize_state: cannot open ") + (path ? path : "(null)"));
     for (int net = 0; net < 6; ++net) save_net(p, net, os);
     const int n = p->n;
-    auto dump_adam = [&](const NetShape& sh, const float* m_arena, const float* v_arena,
-                         const int64_t* t_dev) {
+    // rows: the network's members (a shared critic has one)
+    auto dump_adam = [&](const NetShape& sh, int rows, const float* m_arena,
+                         const float* v_arena, const int64_t* t_dev) {
+      const int n = rows;
       std::vector<float> m(static_cast<size_t>(n) * sh.P), v(m.size());
       std::vector<int64_t> t(n);
       CUDA_CHECK(cudaMemcpy2DAsync(m.data(), sh.P * 4, m_arena, sh.stride * 4, sh.P * 4, n,
@@ -256,10 +274,11 @@ int pbrl_serialize_state(pbrl_pop* pop, const char* path) {
         }
       }
     };
-    dump_adam(p->pol, p->pol_m.p, p->pol_v.p, p->t_pol.p);
-    dump_adam(p->cri, p->cri_m.p, p->cri_v.p, p->t_cri.p);
-    dump_adam(p->cri, p->cri_m.p + static_cast<size_t>(n) * p->cri.stride,
-              p->cri_v.p + static_cast<size_t>(n) * p->cri.stride, p->t_cri.p + n);
+    const int nc = p->ncrit;
+    dump_adam(p->pol, n, p->pol_m.p, p->pol_v.p, p->t_pol.p);
+    dump_adam(p->cri, nc, p->cri_m.p, p->cri_v.p, p->t_cri.p);
+    dump_adam(p->cri, nc, p->cri_m.p + static_cast<size_t>(nc) * p->cri.stride,
+              p->cri_v.p + static_cast<size_t>(nc) * p->cri.stride, p->t_cri.p + nc);
     std::vector<double> acc(n);
     std::vector<uint64_t> steps(n);
     CUDA_CHECK(cudaMemcpyAsync(acc.data(), p->delay_acc.p, 8 * n, cudaMemcpyDeviceToHost, p->stream));
@@ -283,7 +302,9 @@ int pbrl_deserialize_state(pbrl_pop* pop, const char* path) {
     for (int net = 0; net < 6; ++net) load_net(p, net, is);
     const int n = p->n;
     int64_t tmax = 0;
-    auto load_adam = [&](const NetShape& sh, float* m_arena, float* v_arena, int64_t* t_dev) {
+    auto load_adam = [&](const NetShape& sh, int rows, float* m_arena, float* v_arena,
+                         int64_t* t_dev) {
+      const int n = rows;
       std::vector<float> m(static_cast<size_t>(n) * sh.P), v(m.size());
       std::vector<int64_t> t(n), t0(n);
       bool first = true;
@@ -314,10 +335,11 @@ int pbrl_deserialize_state(pbrl_pop* pop, const char* path) {
       p->sync();
       for (int64_t x : t0) tmax = std::max(tmax, x);
     };
-    load_adam(p->pol, p->pol_m.p, p->pol_v.p, p->t_pol.p);
-    load_adam(p->cri, p->cri_m.p, p->cri_v.p, p->t_cri.p);
-    load_adam(p->cri, p->cri_m.p + static_cast<size_t>(n) * p->cri.stride,
-              p->cri_v.p + static_cast<size_t>(n) * p->cri.stride, p->t_cri.p + n);
+    const int nc = p->ncrit;
+    load_adam(p->pol, n, p->pol_m.p, p->pol_v.p, p->t_pol.p);
+    load_adam(p->cri, nc, p->cri_m.p, p->cri_v.p, p->t_cri.p);
+    load_adam(p->cri, nc, p->cri_m.p + static_cast<size_t>(nc) * p->cri.stride,
+              p->cri_v.p + static_cast<size_t>(nc) * p->cri.stride, p->t_cri.p + nc);
     std::vector<double> acc(n);
     std::vector<uint64_t> steps(n);
     is.read(reinterpret_cast<char*>(acc.data()), 8 * n);
@@ -400,7 +422,7 @@ int pbrl_param_count(pbrl_pop* pop, int net, uint64_t* count) {
 int pbrl_get_member(pbrl_pop* pop, int net, uint64_t member, float* flat) {
   return guarded([&] {
     Pop* p = P(pop);
-    check_member(p, member, "flatten_member");
+    check_net_member(p, net, member, "flatten_member");
     const float* src = p->net_row(net, member);
     CUDA_CHECK(cudaMemcpyAsync(flat, src, p->net_shape(net).P * 4, cudaMemcpyDeviceToHost,
                                p->stream));
@@ -411,7 +433,7 @@ int pbrl_get_member(pbrl_pop* pop, int net, uint64_t member, float* flat) {
 int pbrl_set_member(pbrl_pop* pop, int net, uint64_t member, const float* flat) {
   return guarded([&] {
     Pop* p = P(pop);
-    check_member(p, member, "unflatten_member");
+    check_net_member(p, net, member, "unflatten_member");
     float* dst = p->net_row(net, member);
     CUDA_CHECK(cudaMemcpyAsync(dst, flat, p->net_shape(net).P * 4, cudaMemcpyHostToDevice,
                                p->stream));
@@ -423,8 +445,8 @@ int pbrl_set_member(pbrl_pop* pop, int net, uint64_t member, const float* flat) 
 int pbrl_copy_member(pbrl_pop* pop, int net, uint64_t src, uint64_t dst) {
   return guarded([&] {
     Pop* p = P(pop);
-    if (src >= static_cast<uint64_t>(p->n) || dst >= static_cast<uint64_t>(p->n))
-      PBRL_THROW(PBRL_E_USAGE, "copy_member: index out of range");
+    const uint64_t rows = static_cast<uint64_t>(p->net_members(net));
+    if (src >= rows || dst >= rows) PBRL_THROW(PBRL_E_USAGE, "copy_member: index out of range");
     if (src == dst) return;
     CUDA_CHECK(cudaMemcpyAsync(p->net_row(net, dst), p->net_row(net, src),
                                p->net_shape(net).P * 4, cudaMemcpyDeviceToDevice, p->stream));
@@ -436,7 +458,7 @@ int pbrl_copy_member(pbrl_pop* pop, int net, uint64_t src, uint64_t dst) {
 int pbrl_get_adam(pbrl_pop* pop, int net, uint64_t member, float* m, float* v, int64_t* t) {
   return guarded([&] {
     Pop* p = P(pop);
-    check_member(p, member, "get_adam");
+    check_net_member(p, net == PBRL_NET_POLICY ? net : PBRL_NET_CRITIC1, member, "get_adam");
     const float *pm, *pv;
     const int64_t* pt;
     size_t P_;
@@ -446,7 +468,7 @@ int pbrl_get_adam(pbrl_pop* pop, int net, uint64_t member, float* m, float* v, i
       pt = p->t_pol.p + member;
       P_ = p->pol.P;
     } else if (net == PBRL_NET_CRITIC1 || net == PBRL_NET_CRITIC2) {
-      const uint64_t row = (net == PBRL_NET_CRITIC1 ? 0 : p->n) + member;
+      const uint64_t row = (net == PBRL_NET_CRITIC1 ? 0 : p->ncrit) + member;
       pm = p->cri_m.p + row * p->cri.stride;
       pv = p->cri_v.p + row * p->cri.stride;
       pt = p->t_cri.p + row;
@@ -514,10 +536,13 @@ int pbrl_last_losses(pbrl_pop* pop, double* c1, double* c2, double* pl) {
   return guarded([&] {
     Pop* p = P(pop);
     const size_t n = p->n;
-    if (c1) CUDA_CHECK(cudaMemcpyAsync(c1, p->losses.p, 8 * n, cudaMemcpyDeviceToHost, p->stream));
-    if (c2) CUDA_CHECK(cudaMemcpyAsync(c2, p->losses.p + n, 8 * n, cudaMemcpyDeviceToHost, p->stream));
-    if (pl) CUDA_CHECK(cudaMemcpyAsync(pl, p->losses.p + 2 * n, 8 * n, cudaMemcpyDeviceToHost, p->stream));
+    std::vector<double> h(3 * n);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), p->losses.p, 8 * 3 * n, cudaMemcpyDeviceToHost, p->stream));
     p->sync();
+    p->shared_losses_layout(h.data());
+    if (c1) std::memcpy(c1, h.data(), 8 * n);
+    if (c2) std::memcpy(c2, h.data() + n, 8 * n);
+    if (pl) std::memcpy(pl, h.data() + 2 * n, 8 * n);
   });
 }
 
@@ -794,6 +819,7 @@ int pbrl_pbt_apply(pbrl_pop* pop, const uint64_t* replaced, const uint64_t* dono
                    uint32_t count) {
   return guarded([&] {
     Pop* p = P(pop);
+    if (count > 0) check_independent(p, "pbt exploit copy");
     const uint64_t lo = p->member_offset, hi = lo + p->n;
     std::vector<uint64_t> src, dst, reset;
     for (uint32_t i = 0; i < count; ++i) {
@@ -898,6 +924,7 @@ int pbrl_export_member(pbrl_pop* pop, uint64_t member, float* buf) {
   return guarded([&] {
     Pop* p = P(pop);
     check_member(p, member, "export_member");
+    check_independent(p, "export_member");
     size_t at = 0;
     for (int net = 0; net < 6; ++net) {
       if (net == PBRL_NET_POLICY_TARGET && p->algo != PBRL_ALGO_TD3) continue;
@@ -916,6 +943,7 @@ int pbrl_import_member(pbrl_pop* pop, uint64_t member, const float* buf) {
   return guarded([&] {
     Pop* p = P(pop);
     check_member(p, member, "import_member");
+    check_independent(p, "import_member");
     size_t at = 0;
     for (int net = 0; net < 6; ++net) {
       if (net == PBRL_NET_POLICY_TARGET && p->algo != PBRL_ALGO_TD3) continue;
@@ -1109,6 +1137,7 @@ int pbrl_pbt_evolve_sharded(pbrl_pop* pop, pbrl_comm* comm, const double* local_
   int rc = guarded([&] {
     Pop* p = P(pop);
     if (!comm || !comm->c) PBRL_THROW(PBRL_E_USAGE, "pbt_evolve_sharded: null comm");
+    check_independent(p, "pbt_evolve_sharded");
     Comm& c = *comm->c;
     const uint64_t n = static_cast<uint64_t>(p->n);
     if (c.device != p->device) PBRL_THROW(PBRL_E_USAGE, "pbt_evolve_sharded: comm on another device");
@@ -1206,6 +1235,8 @@ int pbrl_copy_member_state(pbrl_pop* dst_pop, uint64_t dm, pbrl_pop* src_pop, ui
   return guarded([&] {
     Pop* s = P(src_pop);
     Pop* d = P(dst_pop);
+    check_independent(s, "slice_member");
+    check_independent(d, "set_member");
     check_member(s, sm, "copy_member_state (source)");
     check_member(d, dm, "copy_member_state (destination)");
     if (s->algo != d->algo || s->ds != d->ds || s->da != d->da || s->hidden != d->hidden ||
@@ -1250,4 +1281,140 @@ int pbrl_copy_member_state(pbrl_pop* dst_pop, uint64_t dm, pbrl_pop* src_pop, ui
   });
 }
 
+// ---------------------------------------------------------------- shared critic over shards
+int pbrl_attach_comm(pbrl_pop* pop, pbrl_comm* comm) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    if (!comm) {
+      p->comm_reduce = nullptr;
+      p->use_graphs = p->graphs_allowed;
+      p->invalidate_graphs();
+      return;
+    }
+    if (!comm->c) PBRL_THROW(PBRL_E_USAGE, "attach_comm: null comm");
+    if (!p->shared)
+      PBRL_THROW(PBRL_E_USAGE, "attach_comm: only a shared-critic population exchanges data per step");
+    Comm* c = comm->c;
+    if (p->n_global != static_cast<uint64_t>(p->n) * c->world ||
+        p->member_offset != static_cast<uint64_t>(p->n) * c->rank)
+      PBRL_THROW(PBRL_E_CONFIG, "attach_comm: shard layout != (rank * n, world * n)");
+    p->comm_reduce = [c](float* buf, size_t count, cudaStream_t s) { c->allreduce_f32(buf, count, s); };
+    p->use_graphs = false;  // the host transport cannot sit inside a graph
+    p->invalidate_graphs();
+  });
+}
+
+// ---------------------------------------------------------------- DvD (evolve.hpp:304-525)
+int pbrl_set_dvd(pbrl_pop* pop, const double* probe, uint64_t m_states, double length_scale,
+                 double jitter, double lambda) {
+  return guarded([&] { P(pop)->set_dvd(probe, m_states, length_scale, jitter, lambda); });
+}
+
+int pbrl_dvd_embed(pbrl_pop* pop, const double* probe, uint64_t m_states, float* out) {
+  return guarded([&] {
+    Pop* p = P(pop);
+    if (p->algo != PBRL_ALGO_TD3) PBRL_THROW(PBRL_E_USAGE, "dvd_embed: TD3 policies only");
+    if (!probe || !out || m_states < 1) PBRL_THROW(PBRL_E_SHAPE, "dvd_embed: probe matrix size != M * observation_dim");
+    // dvd_embed_cached (:314-332): probes (double -> T) replicated per member, then the policy
+    // forward == deterministic act
+    const size_t per = static_cast<size_t>(m_states) * p->ds;
+    std::vector<float> obs(per * p->n);
+    for (int m = 0; m < p->n; ++m)
+      for (size_t i = 0; i < per; ++i) obs[m * per + i] = static_cast<float>(probe[i]);
+    std::vector<uint64_t> steps(p->n, 0);
+    p->act(obs.data(), m_states, nullptr, 0, steps.data(), 1, out);
+  });
+}
+
+int pbrl_dvd_loss(const double* emb, uint64_t n, uint64_t dim, double length_scale, double jitter,
+                  double lambda, double* loss, double* logdet, double* grad) {
+  return guarded([&] {
+    if (!emb && n > 0) PBRL_THROW(PBRL_E_USAGE, "dvd_loss: null embeddings");
+    dvd_loss_host(emb, n, dim, length_scale, jitter, lambda, loss, logdet, grad);
+  });
+}
+
+int pbrl_median_pairwise_distance(const double* emb, uint64_t n, uint64_t dim, double* out) {
+  return guarded([&] { *out = median_pairwise_distance_host(emb, n, dim); });
+}
+
+int pbrl_dvd_lambda(uint64_t step, double start, double end, uint64_t horizon, double* out) {
+  return guarded([&] {
+    if (horizon == 0 || step >= horizon) {
+      *out = end;
+    } else {
+      const double frac = static_cast<double>(step) / static_cast<double>(horizon);
+      *out = start + (end - start) * frac;
+    }
+  });
+}
+
+// ---------------------------------------------------------------- CEM (evolve.hpp:221-297)
+struct pbrl_cem {
+  std::unique_ptr<Cem> c;
+};
+
+int pbrl_cem_create(pbrl_pop* pop, const double* mean, double init_var, pbrl_cem** out) {
+  return guarded([&] {
+    if (!out) PBRL_THROW(PBRL_E_USAGE, "null output handle");
+    auto h = std::make_unique<pbrl_cem>();
+    h->c = std::make_unique<Cem>(P(pop), mean, init_var);
+    *out = h.release();
+  });
+}
+
+int pbrl_cem_destroy(pbrl_cem* cem) {
+  delete cem;
+  return PBRL_OK;
+}
+
+static Cem& C_(pbrl_cem* h) {
+  if (!h || !h->c) PBRL_THROW(PBRL_E_USAGE, "null CEM handle");
+  CUDA_CHECK(cudaSetDevice(h->c->pop->device));
+  return *h->c;
+}
+
+int pbrl_cem_set_params(pbrl_cem* cem, double noise, double noise_final, double noise_decay,
+                        double elite_fraction) {
+  return guarded([&] {
+    Cem& c = C_(cem);
+    c.noise = noise;
+    c.noise_final = noise_final;
+    c.noise_decay = noise_decay;
+    c.elite_fraction = elite_fraction;
+  });
+}
+
+int pbrl_cem_get(pbrl_cem* cem, double* mean, double* var, double* noise) {
+  return guarded([&] {
+    Cem& c = C_(cem);
+    cudaStream_t s = c.pop->stream;
+    if (mean) CUDA_CHECK(cudaMemcpyAsync(mean, c.mean.p, c.dim * 8, cudaMemcpyDeviceToHost, s));
+    if (var) CUDA_CHECK(cudaMemcpyAsync(var, c.var.p, c.dim * 8, cudaMemcpyDeviceToHost, s));
+    c.pop->sync();
+    if (noise) *noise = c.noise;
+  });
+}
+
+int pbrl_cem_resample(pbrl_cem* cem, uint64_t rng_key, uint64_t* rng_next) {
+  return guarded([&] {
+    if (!rng_next) PBRL_THROW(PBRL_E_USAGE, "null rng counter");
+    C_(cem).resample(rng_key, rng_next);
+  });
+}
+
+int pbrl_cem_candidates(pbrl_cem* cem, double* out) {
+  return guarded([&] {
+    Cem& c = C_(cem);
+    CUDA_CHECK(cudaMemcpyAsync(out, c.cand.p, c.cand.count * 8, cudaMemcpyDeviceToHost,
+                               c.pop->stream));
+    c.pop->sync();
+  });
+}
+
+int pbrl_cem_update(pbrl_cem* cem, const double* scores, uint64_t count) {
+  return guarded([&] { C_(cem).update(scores, count); });
+}
+
 }  // extern "C"
+

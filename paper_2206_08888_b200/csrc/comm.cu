@@ -23,6 +23,8 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
@@ -44,6 +46,7 @@ const NcclApi& nccl() {
     sym(a.CommInitRank, "ncclCommInitRank");
     sym(a.CommDestroy, "ncclCommDestroy");
     sym(a.AllGather, "ncclAllGather");
+    sym(a.AllReduce, "ncclAllReduce");
     sym(a.Send, "ncclSend");
     sym(a.Recv, "ncclRecv");
     sym(a.GroupStart, "ncclGroupStart");
@@ -92,6 +95,11 @@ struct NcclComm final : Comm {
     CUDA_CHECK(cudaStreamSynchronize(s));
   }
 
+  void allreduce_f32(float* dev, uint64_t count, cudaStream_t s) override {
+    if (!nccl().AllReduce) PBRL_THROW(PBRL_E_NCCL, "ncclAllReduce not found");
+    NCCL_CHECK(nccl().AllReduce(dev, dev, count, ncclFloat32, ncclSum, comm, s));
+  }
+
   void exchange(const std::vector<P2P>& ops, cudaStream_t s) override {
     if (ops.empty()) return;
     NCCL_CHECK(nccl().GroupStart());
@@ -113,6 +121,17 @@ struct HostComm final : Comm {
   void allgather_f64(const double* send, uint64_t count, double* recv, cudaStream_t) override {
     if (ops.allgather_f64(ops.ctx, send, count, recv) != 0)
       PBRL_THROW(PBRL_E_NCCL, "pbrl_comm_ops.allgather_f64 failed");
+  }
+
+  void allreduce_f32(float* dev, uint64_t count, cudaStream_t s) override {
+    if (!ops.allreduce_f32) PBRL_THROW(PBRL_E_USAGE, "pbrl_comm_ops.allreduce_f32 not provided");
+    std::vector<float> h(count);
+    CUDA_CHECK(cudaMemcpyAsync(h.data(), dev, count * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    if (ops.allreduce_f32(ops.ctx, h.data(), count) != 0)
+      PBRL_THROW(PBRL_E_NCCL, "pbrl_comm_ops.allreduce_f32 failed");
+    CUDA_CHECK(cudaMemcpyAsync(dev, h.data(), count * 4, cudaMemcpyHostToDevice, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
   }
 
   // device blobs are staged through host memory around the caller's exchange callback

@@ -28,6 +28,9 @@ struct Comm {
   virtual void allgather_f64(const double* send, uint64_t count, double* recv, cudaStream_t s) = 0;
   // grouped point-to-point of device buffers, stream-ordered on s; returns when complete
   virtual void exchange(const std::vector<P2P>& ops, cudaStream_t s) = 0;
+  // in-place sum over the ranks of a device float buffer, stream-ordered on s (the shared
+  // critic's per-step gradient all-reduce)
+  virtual void allreduce_f32(float* dev, uint64_t count, cudaStream_t s) = 0;
   virtual const char* kind() const = 0;
 };
 

@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
           yv = a.y[mb + b];
         }
         const float dl = qv - yv;
-        Gs[b] = (2.0f / static_cast<float>(B)) * dl;
+        Gs[b] = (2.0f / static_cast<float>(a.norm_rows ? a.norm_rows : B)) * dl;
         Ls[b] = dl;
       }
     }
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
     } else {
       for (int b = 0; b < B; ++b) acc += static_cast<double>(Ls[b]) * static_cast<double>(Ls[b]);
     }
-    a.loss[grp] = acc / static_cast<double>(B);
+    a.loss[grp] = acc / static_cast<double>(a.top != 3 && a.norm_rows ? a.norm_rows : B);
   }
   if (!a.dW) return;
   float* dW = a.dW + grp * a.dw_gs;
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
           yv = a.y[mb + b];
         }
         const float dl = qv - yv;
-        Gs[b] = (2.0f / static_cast<float>(B)) * dl;
+        Gs[b] = (2.0f / static_cast<float>(a.norm_rows ? a.norm_rows : B)) * dl;
         Ls[b] = dl;
       }
     }
@@ -632,7 +632,8 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (threadIdx.x == 0) a.loss[grp] = s / static_cast<double>(B);
+    if (threadIdx.x == 0)
+      a.loss[grp] = s / static_cast<double>(a.top != 3 && a.norm_rows ? a.norm_rows : B);
   }
   if (!a.dW) return;
   float* dW = a.dW + grp * a.dw_gs;
@@ -857,21 +858,28 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
                                  const uint8_t* mask, int* fire, int64_t* t_pol, int64_t* t_c1,
                                  int64_t* t_c2, uint64_t* steps, const uint64_t* streams,
                                  uint64_t seed, uint64_t* noise_key, double* policy_loss,
-                                 cudaGraphConditionalHandle any_fire, int set_cond) {
+                                 cudaGraphConditionalHandle any_fire, int set_cond, int shared,
+                                 int ncrit) {
   PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   int f = 0;
   if (m < n) {
-    double acc = delay_acc[m] + ratio[m];
-    if (acc >= 1.0 - 1e-12) {
-      acc -= 1.0;
-      f = 1;
+    if (shared) {
+      f = 1;  // shared critic: every policy updates every step (algos.hpp:382-384)
+    } else {
+      double acc = delay_acc[m] + ratio[m];
+      if (acc >= 1.0 - 1e-12) {
+        acc -= 1.0;
+        f = 1;
+      }
+      delay_acc[m] = acc;
     }
-    delay_acc[m] = acc;
     if (mask && !mask[m]) f = 0;
     fire[m] = f;
-    t_c1[m] += 1;
-    t_c2[m] += 1;
+    if (m < ncrit) {
+      t_c1[m] += 1;
+      t_c2[m] += 1;
+    }
     if (f) t_pol[m] += 1;
     // members that do not fire report a zero policy loss (k_td3_policy_loss writes the rest);
     // written here because the policy half may be skipped altogether
@@ -883,15 +891,25 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
   // (default 0 at every graph launch; any block with a firing member sets it)
   const int any = __syncthreads_or(f);
   if (set_cond && any && threadIdx.x == 0) cudaGraphSetConditional(any_fire, 1u);
+  if (shared && blockIdx.x == 0) {
+    // fire[n]: some member fires -> the shared critic's target Polyak (cmask {1}, :407-418);
+    // block 0 scans the whole mask so no cross-block ordering is needed
+    int a = 0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) a |= (!mask || mask[j]) ? 1 : 0;
+    a = __syncthreads_or(a);
+    if (threadIdx.x == 0) fire[n] = a;
+  }
 }
 
 void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const uint8_t* mask,
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
-                           cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s) {
+                           cudaGraphConditionalHandle any_fire, int set_cond, int shared,
+                           int ncrit, cudaStream_t s) {
   launch_k(k_td3_step_begin, (n + 127) / 128, 128, 0, s, n, delay_acc, ratio, mask, fire, t_pol,
-           t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, set_cond);
+           t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, set_cond, shared,
+           ncrit);
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts
@@ -978,12 +996,14 @@ void launch_td_target(int n, int B, const float* r, const float* d, const float*
 // double products) and summed by one thread in row order (the reference's double rounding).
 constexpr int kLossChunk = 1024;
 
-__global__ void k_mse(int n, int B, const float* q, const float* y, float* dq, double* loss) {
+__global__ void k_mse(int n, int B, const float* q, const float* y, float* dq, double* loss,
+                      int norm_rows) {
   PDL_ENTRY();
   __shared__ double sq[kLossChunk];
   const int grp = blockIdx.x;
   const int m = grp % n;
-  const float scale = 2.0f / static_cast<float>(B);
+  const int nr = norm_rows ? norm_rows : B;  // shared critic: rows of the folded population
+  const float scale = 2.0f / static_cast<float>(nr);
   const float* qg = q + static_cast<long long>(grp) * B;
   const float* yg = y + static_cast<long long>(m) * B;
   double acc = 0.0;
@@ -1000,12 +1020,12 @@ __global__ void k_mse(int n, int B, const float* q, const float* y, float* dq, d
       for (int i = 0; i < nb; ++i) acc += sq[i];
     __syncthreads();
   }
-  if (threadIdx.x == 0) loss[grp] = acc / static_cast<double>(B);
+  if (threadIdx.x == 0) loss[grp] = acc / static_cast<double>(nr);
 }
 
 void launch_mse(int groups, int n, int B, const float* q, const float* y, float* dq, double* loss,
-                cudaStream_t s) {
-  launch_k(k_mse, groups, 256, 0, s, n, B, q, y, dq, loss);
+                cudaStream_t s, int norm_rows) {
+  launch_k(k_mse, groups, 256, 0, s, n, B, q, y, dq, loss, norm_rows);
 }
 
 // td3_policy_loss_grads (algos.hpp:318-338): loss = -sum q / B; cotangent -1/B everywhere

@@ -58,6 +58,10 @@ Pop::Pop(const pbrl_pop_desc& d) {
   da = static_cast<int>(d.act_dim);
   member_offset = d.member_offset;
   n_global = d.n_global ? d.n_global : d.n;
+  if (d.mode != PBRL_MODE_INDEPENDENT && d.mode != PBRL_MODE_SHARED_CRITIC)
+    PBRL_THROW(PBRL_E_CONFIG, "unknown population mode");
+  shared = d.mode == PBRL_MODE_SHARED_CRITIC;
+  ncrit = shared ? 1 : n;
   bound = static_cast<float>(d.action_bound);
   seed = d.seed;
   for (uint32_t i = 0; i < d.n_hidden; ++i) {
@@ -67,7 +71,7 @@ Pop::Pop(const pbrl_pop_desc& d) {
   CUDA_CHECK(cudaSetDevice(device));
   CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   tc_trace_init();
-  use_graphs = std::getenv("PBRL_NO_GRAPH") == nullptr;  // eager replay (ncu kernel profiles)
+  use_graphs = graphs_allowed = std::getenv("PBRL_NO_GRAPH") == nullptr;  // eager (ncu profiles)
   fwd2_off = std::getenv("PBRL_NO_FWD2") != nullptr;
 
   std::vector<size_t> pd{static_cast<size_t>(ds)};
@@ -80,7 +84,7 @@ Pop::Pop(const pbrl_pop_desc& d) {
   cri.make(qd, ACT_NONE, 1.0f);
 
   const size_t np = static_cast<size_t>(n) * pol.stride;
-  const size_t nc = 2 * static_cast<size_t>(n) * cri.stride;
+  const size_t nc = 2 * static_cast<size_t>(ncrit) * cri.stride;
   pol_p.alloc(np);
   pol_m.alloc(np);
   pol_v.alloc(np);
@@ -92,10 +96,10 @@ Pop::Pop(const pbrl_pop_desc& d) {
   cri_v.alloc(nc);
   cri_g.alloc(nc);
   t_pol.alloc(n);
-  t_cri.alloc(2 * n);
+  t_cri.alloc(2 * ncrit);
   steps.alloc(n);
   streams.alloc(n);
-  fire.alloc(n);
+  fire.alloc(n + 1);  // fire[n]: "some member fires" (shared critic's target Polyak gate)
   delay_acc.alloc(n);
   key_a.alloc(n);
   key_b.alloc(n);
@@ -126,8 +130,10 @@ Pop::Pop(const pbrl_pop_desc& d) {
   const uint64_t s_c1 = mix64(seed ^ (algo == PBRL_ALGO_TD3 ? 0xB2 : 0xE5));
   const uint64_t s_c2 = mix64(seed ^ (algo == PBRL_ALGO_TD3 ? 0xC3 : 0xF6));
   launch_init_net(pol, pol_p.p, n, member_offset, s_pol, stream);
-  launch_init_net(cri, cri_p.p, n, member_offset, s_c1, stream);
-  launch_init_net(cri, cri_p.p + static_cast<size_t>(n) * cri.stride, n, member_offset, s_c2,
+  // the shared critic is critic member 0 on every shard (init_pop_mlp(1, ...), algos.hpp:199)
+  const uint64_t c_off = shared ? 0 : member_offset;
+  launch_init_net(cri, cri_p.p, ncrit, c_off, s_c1, stream);
+  launch_init_net(cri, cri_p.p + static_cast<size_t>(ncrit) * cri.stride, ncrit, c_off, s_c2,
                   stream);
   count_launch(3 * pol.depth);
   if (algo == PBRL_ALGO_TD3)
@@ -160,6 +166,11 @@ Pop::Pop(const pbrl_pop_desc& d) {
   sync();
 }
 
+CriticFold::CriticFold(Pop& pop, int b) : p(pop), n0(pop.n), B(pop.crows(b)) {
+  if (p.shared) p.n = 1;
+}
+CriticFold::~CriticFold() { p.n = n0; }
+
 Pop::~Pop() {
   invalidate_graphs();
   for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
@@ -183,7 +194,7 @@ void Pop::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
 void Pop::refresh_shadows() {
   if (!act16()) return;
   const size_t np = static_cast<size_t>(n) * pol.stride;
-  const size_t nc = 2 * static_cast<size_t>(n) * cri.stride;
+  const size_t nc = 2 * static_cast<size_t>(ncrit) * cri.stride;
   launch_to_bf16(pol_p.p, pol_p16.p, np, stream);
   if (pol_t16.p) launch_to_bf16(pol_t.p, pol_t16.p, np, stream);
   launch_to_bf16(cri_p.p, cri_p16.p, nc, stream);
@@ -449,7 +460,10 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     }
   }
   host_mask = nullptr;
-  if (losses_out) sync();
+  if (losses_out) {
+    sync();
+    for (uint32_t i = 0; i < k; ++i) shared_losses_layout(losses_out + static_cast<size_t>(i) * 3 * n);
+  }
   CUDA_CHECK(cudaGetLastError());
 }
 

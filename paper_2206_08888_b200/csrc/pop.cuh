@@ -190,6 +190,7 @@ struct OutBwdArgs {
   double* loss = nullptr;
   const int* active = nullptr;
   int exact = 1;  // 1: reference summation order (FFMA32); 0: warp-parallel tree (TF32)
+  int norm_rows = 0;  // top 1/2: rows of the MSE mean (0 = B; shared critic: n_global * B)
 };
 void launch_out_backward(const OutBwdArgs& a, cudaStream_t s);
 
@@ -205,7 +206,8 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            int* fire, int64_t* t_pol, int64_t* t_c1, int64_t* t_c2,
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
-                           cudaGraphConditionalHandle any_fire, int set_cond, cudaStream_t s);
+                           cudaGraphConditionalHandle any_fire, int set_cond, int shared,
+                           int ncrit, cudaStream_t s);
 // in_sa / in_s2a / sa_pi are activation buffers: fp32, or bf16 when act16
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, void* in_sa,
@@ -213,8 +215,9 @@ void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, co
                        cudaStream_t st, void* in_s = nullptr, int lsp = 0);
 void launch_td_target(int n, int B, const float* r, const float* d, const float* q2n,
                       const float* gamma, float* y, cudaStream_t s);
+// norm_rows: rows of the MSE mean (0 = B; the folded population when the critic is shared)
 void launch_mse(int groups, int n, int B, const float* q, const float* y, float* dq, double* loss,
-                cudaStream_t s);
+                cudaStream_t s, int norm_rows = 0);
 void launch_td3_policy_loss(int n, int B, const float* q, const int* fire, double* loss,
                             float* gq, cudaStream_t s);
 // Adam (pop_tensor.hpp:328-366) over a [groups][stride] arena, first P floats per group, with

@@ -1,6 +1,7 @@
 // Population object (host side of the C ABI).
 #pragma once
 
+#include <functional>
 #include <unordered_map>
 
 #include <atomic>
@@ -126,15 +127,50 @@ void set_last_error(const std::string& m);  // pbrl_last_error() of the calling 
 struct StepGraph {
   int B = 0;
   bool masked = false;
+  bool dvd = false;  // the DvD gradient add sits in the policy half
   cudaGraphExec_t exec = nullptr;
   size_t nodes = 0;       // kernel nodes outside conditional bodies
   size_t cond_nodes = 0;  // kernel nodes inside the policy-half conditional bodies
+};
+
+struct Pop;
+// Critic operations of a shared-critic population see it as ONE member whose batch has n*B
+// rows (a pure reinterpretation of the [n][B][...] activation blocks); inside the scope the
+// population's member count reads 1, so group -> member maps and per-member hyper indices
+// (critic_lr[0], tau[0]) follow the reference's shared-mode vectors (algos.hpp:366, :407).
+struct CriticFold {
+  Pop& p;
+  int n0, B;
+  CriticFold(Pop& pop, int b);
+  ~CriticFold();
 };
 
 struct Pop {
   int algo = PBRL_ALGO_TD3, precision = PBRL_PREC_FFMA32, device = 0;
   int n = 0, ds = 0, da = 0;
   uint64_t member_offset = 0, n_global = 0;
+  // PopMode::kSharedCritic (algos.hpp:197): ONE critic pair serves every policy; its batch is
+  // the population folded into rows (critic_forward, algos.hpp:219-233).  ncrit = critic
+  // members (n, or 1); critic2 rows start at ncrit in the critic arenas.
+  bool shared = false;
+  int ncrit = 0;
+  int net_members(int net) const {
+    return (net == PBRL_NET_POLICY || net == PBRL_NET_POLICY_TARGET) ? n : ncrit;
+  }
+  int crows(int B) const { return shared ? n * B : B; }  // rows of one critic group
+  // host copy of the [3][n] losses: a folded critic step writes critic2's loss at index 1;
+  // report it at n (critic1 / critic2 / policy rows as in independent mode)
+  void shared_losses_layout(double* h) const {
+    if (shared && n > 1) {
+      h[n] = h[1];
+      h[1] = 0.0;
+    }
+  }
+  // dq / loss scale rows of the critic MSE (mse_loss_grads): the folded batch of the whole
+  // population, across shards when the critic is shared over ranks
+  double mse_rows(int B) const {
+    return shared ? static_cast<double>(n_global) * B : static_cast<double>(B);
+  }
   float bound = 1.0f;
   uint64_t seed = 0;
   std::vector<size_t> hidden;
@@ -314,6 +350,26 @@ struct Pop {
   bool gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long long out_ld, int epi,
                          Mat aux, float scale, const int* active);
   void critic_update(int B, const int* polyak_gate, bool forward_done = false);
+  bool td_target_fused(int B) const;
+  // DvD policy-gradient hook (dvd_policy_hook, evolve.hpp:507-525) for the following update
+  // calls: probe block, embeddings, tanh values, cotangents, the hook's gradient arena
+  struct Dvd {
+    bool on = false;
+    int ms = 0, ldx = 0;
+    double ls = 1.0, jitter = 1e-6, lambda = 0.0;
+    std::vector<double> probe;
+    DBuf<float> obs, x, emb, t, gemb, gz, grad;
+    std::vector<DBuf<float>> h, dh;
+  } dvd;
+  void set_dvd(const double* probe, uint64_t m_states, double length_scale, double jitter,
+               double lambda);
+  void dvd_forward();
+  void dvd_prepass();
+  // shared critic over shards: in-place sum of the critic gradient arena across ranks before
+  // the critic Adam (set by pbrl_attach_comm; the step then runs eagerly)
+  std::function<void(float*, size_t, cudaStream_t)> comm_reduce;
+  DBuf<float> flag_f;  // the "some member fires" flag as a float for that all-reduce
+  bool graphs_allowed = true;  // PBRL_NO_GRAPH unset
   cudaStream_t side2 = nullptr;  // parallel graph branch (critic forward)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void td3_step(int B, const uint8_t* d_mask);
@@ -341,5 +397,26 @@ struct Pop {
   float* net_row(int net, uint64_t member);
   const NetShape& net_shape(int net) const;
 };
+
+// CEM search distribution over flat policy vectors (CEMState, evolve.hpp:221-297), resident on
+// the population's device; the last sampled candidates are kept (double) for the refit
+struct Cem {
+  Pop* pop;
+  size_t dim = 0;
+  DBuf<double> mean, var, cand;
+  DBuf<uint64_t> order_d;
+  double noise = 1e-2, noise_init = 1e-2, noise_final = 1e-3, noise_decay = 0.999;
+  double elite_fraction = 0.5;
+  bool sampled = false;
+  Cem(Pop* p, const double* mean0, double init_var);
+  void resample(uint64_t key, uint64_t* next);
+  void update(const double* scores, uint64_t count);
+};
+
+int dvd_loss_host(const double* emb, uint64_t n, uint64_t dim, double length_scale, double jitter,
+                  double lambda, double* loss, double* logdet, double* grad);
+double median_pairwise_distance_host(const double* emb, uint64_t n, uint64_t dim);
+void launch_add_into(float* acc, const float* other, size_t count, cudaStream_t s);
+void launch_flag_convert(int* flag, float* flag_f, int to_float, cudaStream_t s);
 
 }  // namespace pbrl

@@ -723,21 +723,29 @@ bool Pop::gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long
 
 // Twin critics as one grouped problem of 2n groups: forward on [s|a], MSE cotangent,
 // backward, fused Adam + target Polyak (algos.hpp:369-377, :401-418).
-void Pop::critic_forward(int B) {
+void Pop::critic_forward(int B0) {
+  CriticFold f(*this, B0);  // shared critic: 2 groups of n*B rows
+  const int B = f.B;
   const Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
   mlp_forward(cri, cri_p.p, 2 * n, B, x0, S.ch, S.q.p, B, 1, EPI_BIAS);
 }
 
-void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
+void Pop::critic_update(int B0, const int* polyak_gate, bool forward_done) {
+  CriticFold f(*this, B0);
+  const int B = f.B;
+  // shared critic: its target Polyak runs when some member fires (cmask {1}, :407-418)
+  if (shared && polyak_gate) polyak_gate = fire.p + f.n0;
+  const int nrows = shared ? static_cast<int>(mse_rows(B0)) : 0;
   const int n2 = 2 * n;
   Mat x0{S.in_sa.p, static_cast<long long>(B) * lsa, lsa, 1};
   if (use_tc() && lsa > ds + da) x0.ones_col = ds + da;  // see Pop::ensure_ones
   if (!forward_done) critic_forward(B);
   // tensor-core modes: the TD target (TD3) and mse_loss_grads run inside the output-layer
-  // backward; FFMA32 keeps the separate kernels (the reference's operation order)
+  // backward; FFMA32 keeps the separate kernels (the reference's operation order).  A shared
+  // critic takes y from k_td_target (its gamma is per policy member, not per critic group).
   OutBwdArgs top;
   if (use_tc() && cri.dims[cri.depth] == 1 && B <= 32768) {
-    top.top = algo == PBRL_ALGO_TD3 ? 1 : 2;
+    top.top = algo == PBRL_ALGO_TD3 && !shared ? 1 : 2;
     top.q = S.q.p;
     top.r = S.r.p;
     top.d = S.d.p;
@@ -745,13 +753,28 @@ void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
     top.gamma = h_f4.p;
     top.y = S.y.p;
     top.loss = losses.p;
+    top.norm_rows = nrows;
   } else {
     timed(PC_ELEM, 0.0, 0.0, 0,
-          [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream); });
+          [&] { launch_mse(n2, n, B, S.q.p, S.y.p, S.dq.p, losses.p, stream, nrows); });
   }
   const float* clr = algo == PBRL_ALGO_TD3 ? h_f0.p : h_f1.p;
   mlp_backward(cri, cri_p.p, cri_g.p, n2, B, Mat{S.dq.p, B, 1, 0}, x0, S.ch, S.dh, nullptr,
                &top);
+  if (shared && comm_reduce) {
+    // one critic replica per shard: the gradient of the whole folded population is the sum of
+    // the shards' (each scaled by 2 / (n_global B)); the target-Polyak gate is "some member of
+    // any shard fires"
+    comm_reduce(cri_g.p, cri_g.count, stream);
+    if (polyak_gate) {
+      flag_f.alloc(1);
+      int* fl = const_cast<int*>(polyak_gate);
+      launch_flag_convert(fl, flag_f.p, 1, stream);
+      comm_reduce(flag_f.p, 1, stream);
+      launch_flag_convert(fl, flag_f.p, 0, stream);
+      count_launch(2);
+    }
+  }
   // 28 B/param Adam (+2 B/param bf16 operand copy in BF16 mode)
   const double cP = static_cast<double>(cri.P);
   timed(PC_ADAM, 0.0, cP * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
@@ -763,6 +786,11 @@ void Pop::critic_update(int B, const int* polyak_gate, bool forward_done) {
   const double pb = act16() ? 10.0 : 8.0;
   if (polyak_gate) prof_add_gated_bytes(pb * cP * n2);
   else if (prof_on && !prof.empty()) prof.back().bytes += pb * cP * n2;
+}
+
+// the tensor-core modes compute the TD target inside the critic's output-layer backward
+bool Pop::td_target_fused(int B) const {
+  return use_tc() && cri.dims[cri.depth] == 1 && crows(B) <= 32768 && !shared;
 }
 
 // ------------------------------------------------------------------ TD3 step (algos.hpp:351-422)
@@ -819,9 +847,9 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
     CUDA_CHECK(cudaGraphConditionalHandleCreate(&any_fire, g, 0, cudaGraphCondAssignDefault));
   }
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
-    launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p, t_cri.p + n,
-                          steps.p, streams.p, seed, key_a.p, losses.p + 2 * n, any_fire,
-                          capturing ? 1 : 0, stream);
+    launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p,
+                          t_cri.p + ncrit, steps.p, streams.p, seed, key_a.p, losses.p + 2 * n,
+                          any_fire, capturing ? 1 : 0, shared ? 1 : 0, ncrit, stream);
   });
   // graph mode: the online critics' forward on [s | a] does not depend on the target chain, so
   // it runs on a parallel graph branch (its tiles fill the target chain's partial waves)
@@ -848,9 +876,13 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   const Mat s2{S.in_s2a.p, nbB * lsa, lsa, 0};
   mlp_forward(pol, pol_t.p, n, B, s2, S.tp_h, aoff(S.in_s2a.p, ds), nbB * lsa, lsa,
               EPI_BIAS_TANH_NOISE, nullptr, nullptr, 0, 0, true, false, true);
-  mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
-              nbB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
-  if (!(use_tc() && cri.dims[cri.depth] == 1 && B <= 32768))  // else fused (critic_update)
+  {
+    CriticFold f(*this, B);
+    const long long cB = f.B;
+    mlp_forward(cri, cri_t.p, 2 * n, f.B, Mat{S.in_s2a.p, cB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
+                cB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
+  }
+  if (!td_target_fused(B))  // else fused (critic_update)
     timed(PC_ELEM, 0.0, 0.0, 0,
           [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
   if (fork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
@@ -873,10 +905,15 @@ void Pop::td3_policy_half(int B) {
   const long long nbB = B;
   const Mat s = policy_input(B);
   td3_policy_forward(B);
-  mlp_forward(cri, cri_p.p, n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 0}, S.qh, S.qpi.p, nbB, 1,
-              EPI_BIAS, fire.p);
+  // critic1 on [s | pi(s)]; a shared critic runs every member's rows (folded, ungated)
+  {
+    CriticFold f(*this, B);
+    const long long cB = f.B;
+    mlp_forward(cri, cri_p.p, n, f.B, Mat{S.sa_pi.p, cB * lsa, lsa, 0}, S.qh, S.qpi.p, cB, 1,
+                EPI_BIAS, shared ? nullptr : fire.p);
+  }
   OutBwdArgs top;
-  if (use_tc() && cri.dims[cri.depth] == 1 && B <= 32768) {  // fused: critic output-layer dX
+  if (td_target_fused(B)) {  // fused: critic output-layer dX (the policy loss's -1/B)
     top.top = 3;
     top.q = S.qpi.p;
     top.loss = losses.p + 2 * n;
@@ -886,10 +923,19 @@ void Pop::td3_policy_half(int B) {
     });
   }
   const int lt = pad4(da);
-  critic_dx_to_action(n, B, Mat{S.gq.p, nbB, 1, 0}, S.qh, S.qdh, S.gtop.p, lt, EPI_TANH_GRAD,
-                      Mat{S.pt.p, nbB * da, da, 0}, pol.out_scale, fire.p, &top);
+  {
+    CriticFold f(*this, B);
+    const long long cB = f.B;
+    critic_dx_to_action(n, f.B, Mat{S.gq.p, cB, 1, 0}, S.qh, S.qdh, S.gtop.p, lt, EPI_TANH_GRAD,
+                        Mat{S.pt.p, cB * da, da, 0}, pol.out_scale, shared ? nullptr : fire.p,
+                        &top);
+  }
   mlp_backward(pol, pol_p.p, pol_g.p, n, B, Mat{S.gtop.p, nbB * lt, lt, 0}, s, S.ph, S.pdh,
                fire.p, nullptr);
+  if (dvd.on) {  // the DvD hook's gradient (computed by dvd_prepass before the step)
+    const size_t cnt = static_cast<size_t>(n) * pol.stride;
+    timed(PC_ELEM, 0.0, 12.0 * cnt, 0, [&] { launch_add_into(pol_g.p, dvd.grad.p, cnt, stream); });
+  }
   timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * (act16() ? 40.0 : 36.0), 1, [&] {
     launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
                 corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, pol_p16.p, pol_t16.p,
@@ -913,8 +959,12 @@ void Pop::sac_step(int B) {
     launch_sac_head(n, B, ds, da, lsa, S.head.p, key_b.p, bound, S.in_s2a.p, nullptr, nullptr,
                     nullptr, nullptr, nullptr, S.logp2.p, act16() ? 1 : 0, stream);
   });
-  mlp_forward(cri, cri_t.p, 2 * n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
-              nbB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
+  {
+    CriticFold f(*this, B);
+    const long long cB = f.B;
+    mlp_forward(cri, cri_t.p, 2 * n, f.B, Mat{S.in_s2a.p, cB * lsa, lsa, 1}, S.tq_h, S.tq_out.p,
+                cB, 1, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
+  }
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_y(n, B, S.r.p, S.d.p, S.tq_out.p, S.logp2.p, log_alpha.p, h_f4.p, h_f3.p, S.y.p,
                  stream);
@@ -927,14 +977,22 @@ void Pop::sac_step(int B) {
     launch_sac_head(n, B, ds, da, lsa, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p,
                     S.ls.p, S.clamped.p, S.eps.p, S.logp.p, act16() ? 1 : 0, stream);
   });
-  mlp_forward(cri, cri_p.p, 2 * n, B, Mat{S.sa_pi.p, nbB * lsa, lsa, 1}, S.qh, S.qpi.p, nbB, 1,
-              EPI_BIAS);
+  {
+    CriticFold f(*this, B);
+    const long long cB = f.B;
+    mlp_forward(cri, cri_p.p, 2 * n, f.B, Mat{S.sa_pi.p, cB * lsa, lsa, 1}, S.qh, S.qpi.p, cB, 1,
+                EPI_BIAS);
+  }
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_policy_top(n, B, S.qpi.p, S.logp.p, log_alpha.p, losses.p + 2 * n, S.gq.p, S.lw.p,
                           stream);
   });
-  critic_dx_to_action(2 * n, B, Mat{S.gq.p, nbB, 1, 0}, S.qh, S.qdh, S.ga.p, da, EPI_STORE,
-                      Mat{}, 1.0f, nullptr);
+  {
+    CriticFold f(*this, B);
+    const long long cB = f.B;
+    critic_dx_to_action(2 * n, f.B, Mat{S.gq.p, cB, 1, 0}, S.qh, S.qdh, S.ga.p, da, EPI_STORE,
+                        Mat{}, 1.0f, nullptr);
+  }
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_sac_head_grad(n, B, da, S.ga.p, S.lw.p, S.x.p, S.th.p, S.ls.p, S.clamped.p, S.eps.p,
                          bound, S.gtop.p, stream);
@@ -1020,13 +1078,15 @@ bool Pop::host_fires() {
   if (delay_host.size() != static_cast<size_t>(n)) delay_host.assign(n, 0.0);
   bool any = false;
   for (int m = 0; m < n; ++m) {
-    double acc = delay_host[m] + hyper[2][m];
-    bool f = false;
-    if (acc >= 1.0 - 1e-12) {
-      acc -= 1.0;
-      f = true;
+    bool f = shared;  // shared critic: every policy updates every step
+    if (!shared) {
+      double acc = delay_host[m] + hyper[2][m];
+      if (acc >= 1.0 - 1e-12) {
+        acc -= 1.0;
+        f = true;
+      }
+      delay_host[m] = acc;
     }
-    delay_host[m] = acc;
     if (host_mask && !host_mask[m]) f = false;
     any = any || f;
   }
@@ -1043,17 +1103,20 @@ void Pop::invalidate_graphs() {
 void Pop::step(int B, const uint8_t* d_mask) {
   ensure_corr(t_bound + 4);
   const bool fires = algo == PBRL_ALGO_TD3 ? host_fires() : true;  // advances the mirror
+  // the DvD hook runs only when some policy updates (td3_update_step, algos.hpp:394-396)
+  if (dvd.on && fires) dvd_prepass();
   if (act16() && weights_dirty) refresh_shadows();
   if (prof_on || !use_graphs) {
     run_program(B, d_mask);
   } else {
     StepGraph* sg = nullptr;
     for (auto& g : graphs)
-      if (g.B == B && g.masked == (d_mask != nullptr)) sg = &g;
+      if (g.B == B && g.masked == (d_mask != nullptr) && g.dvd == dvd.on) sg = &g;
     if (!sg) {
       StepGraph g;
       g.B = B;
       g.masked = d_mask != nullptr;
+      g.dvd = dvd.on;
       cudaGraph_t graph;
       capturing = true;
       cond_body_nodes = 0;

@@ -221,11 +221,20 @@ class Comm:
             except Exception:  # pragma: no cover
                 return 1
 
+        def allreduce(_ctx, buf, count):
+            try:
+                t = torch.from_numpy(np.ctypeslib.as_array(buf, (count,)))
+                dist.all_reduce(t, group=group)  # in place, sum
+                return 0
+            except Exception:  # pragma: no cover
+                return 1
+
         ag, ex = _lib.ALLGATHER_FN(allgather), _lib.EXCHANGE_FN(exchange)
-        ops = _lib.CommOps(None, ag, ex)
+        ar = _lib.ALLREDUCE_FN(allreduce)
+        ops = _lib.CommOps(None, ag, ex, ar)
         h = C.c_void_p()
         _lib.call("pbrl_comm_create_host", C.byref(ops), rank, world, device, C.byref(h))
-        return Comm(h, rank, world, "host", keep=(ag, ex, ops))
+        return Comm(h, rank, world, "host", keep=(ag, ex, ar, ops))
 
     def close(self) -> None:
         if self.handle:

@@ -29,6 +29,10 @@ class DataStarvationError(PbrlError, RuntimeError):
     """A sampler ran dry inside update_k_steps (errors.hpp:39, algos.hpp:958-962)."""
 
 
+class DegeneratePopulationError(PbrlError, RuntimeError):
+    """DvD kernel matrix not positive definite even with jitter (errors.hpp:45)."""
+
+
 class CudaError(PbrlError, RuntimeError):
     """A CUDA runtime call failed."""
 
@@ -38,7 +42,7 @@ class NcclError(PbrlError, RuntimeError):
 
 
 _CODES = {-1: ShapeError, -2: ConfigError, -3: UsageError, -4: NotReadyError, -5: ResourceError,
-          -6: DataStarvationError, -7: CudaError, -8: NcclError}
+          -6: DataStarvationError, -7: CudaError, -8: NcclError, -9: DegeneratePopulationError}
 
 
 def raise_for(code: int, message: str) -> None:

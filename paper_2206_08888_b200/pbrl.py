@@ -27,6 +27,8 @@ from . import _lib
 from .errors import (ConfigError, DataStarvationError, NotReadyError, ShapeError, UsageError)
 
 PRECISIONS = {"ffma32": 0, "bf16": 1, "tf32": 2}
+MODES = {"independent": 0, "kIndependent": 0, "shared_critic": 1, "kSharedCritic": 1,
+         "shared": 1}
 NETS = {"policy": 0, "policy_target": 1, "critic1": 2, "critic2": 3, "critic1_target": 4,
         "critic2_target": 5}
 TD3_FIELDS = ("critic_lr", "policy_lr", "policy_delay_ratio", "explore_std", "target_std",
@@ -263,8 +265,12 @@ class _Population:
 
     def __init__(self, n, obs_dim, act_dim, hidden, action_bound, seed, precision="ffma32",
                  device=0, member_offset=0, n_global=None, mode="independent"):
-        if mode not in ("independent", "kIndependent"):
-            raise ConfigError("shared-critic mode is outside the B200 path (SURVEY.md §8(f))")
+        if mode not in MODES:
+            raise ConfigError(f"unknown population mode {mode!r}")
+        # PopMode (algos.hpp:26): a shared-critic population has ONE critic pair whose batch is
+        # the population folded into rows (CEM-RL / DvD)
+        self.mode = "shared_critic" if MODES[mode] else "independent"
+        self.shared = bool(MODES[mode])
         if precision not in PRECISIONS:
             raise ConfigError(f"unknown precision {precision!r}")
         self.n, self.obs_dim, self.act_dim = int(n), int(obs_dim), int(act_dim)
@@ -279,7 +285,7 @@ class _Population:
         desc = _lib.PopDesc(self.algo, self.n, self.obs_dim, self.act_dim, len(self.hidden),
                             C.cast(hid, _lib.u64p), self._action_bound, self.seed,
                             PRECISIONS[precision], self.device, self.member_offset,
-                            self.n_global)
+                            self.n_global, MODES[mode])
         h = C.c_void_p()
         _lib.call("pbrl_pop_create", C.byref(desc), C.byref(h))
         self._h = h
@@ -324,8 +330,13 @@ class _Population:
     def copy_member(self, net, src: int, dst: int) -> None:
         _lib.call("pbrl_copy_member", self._h, NETS.get(net, net), src, dst)
 
+    def net_members(self, net) -> int:
+        """members of one network: n, or 1 for the critics of a shared-critic population"""
+        k = NETS.get(net, net)
+        return self.n if (k <= 1 or not self.shared) else 1
+
     def params(self, net) -> np.ndarray:
-        return np.stack([self.flatten_member(net, i) for i in range(self.n)])
+        return np.stack([self.flatten_member(net, i) for i in range(self.net_members(net))])
 
     def adam(self, net, i: int):
         P = self.param_count(net)
@@ -451,6 +462,12 @@ class _Population:
             if ext is not None:
                 self._device_call_end(ext, keep)
 
+    def attach_comm(self, comm) -> None:
+        """Shared-critic population sharded over ranks: sum the critic gradients over `comm`
+        (dist.Comm) every step before the critic Adam (pbrl_attach_comm); None detaches."""
+        _lib.call("pbrl_attach_comm", self._h, None if comm is None else comm.handle)
+        self._comm = comm
+
     def launch_count(self) -> int:
         c = C.c_uint64()
         _lib.call("pbrl_launch_count", self._h, C.byref(c))
@@ -526,11 +543,29 @@ def set_member(st: _Population, i: int, sub: _Population) -> None:
 
 def td3_update_step(st: Td3State, batch: TransitionBatch, hyper: Td3Hyper, hook=None,
                     policy_member_mask=None) -> None:
-    """td3_update_step (algos.hpp:351-422)."""
-    if hook is not None:
-        raise ConfigError("policy-gradient hooks (DvD) are outside the B200 path")
+    """td3_update_step (algos.hpp:351-422).  hook: a DvdHook from dvd_policy_hook (the only
+    PolicyGradHook the reference builds, evolve.hpp:507-525), applied on the device."""
     st._sync_hyper(hyper)
-    st._update([batch], policy_member_mask)
+    with _hooked(st, hook):
+        st._update([batch], policy_member_mask)
+
+
+class _hooked:
+    """Installs a DvD hook on the population for the duration of one update call."""
+
+    def __init__(self, st, hook):
+        self.st, self.hook = st, hook
+
+    def __enter__(self):
+        if self.hook is not None:
+            if not isinstance(self.hook, DvdHook):
+                raise ConfigError("td3_update_step: hook must come from dvd_policy_hook")
+            self.hook._install(self.st)
+
+    def __exit__(self, *exc):
+        if self.hook is not None:
+            _lib.call("pbrl_set_dvd", self.st.handle, None, 0, 1.0, 0.0, 0.0)
+        return False
 
 
 def sac_update_step(st: SacState, batch: TransitionBatch, hyper: SacHyper) -> None:
@@ -540,7 +575,7 @@ def sac_update_step(st: SacState, batch: TransitionBatch, hyper: SacHyper) -> No
 
 
 def update_k_steps(st, sampler: Callable[[], Optional[TransitionBatch]], k: int, hyper,
-                   return_losses: bool = False) -> Optional[np.ndarray]:
+                   hook=None, return_losses: bool = False) -> Optional[np.ndarray]:
     """update_k_steps (algos.hpp:953-983): k chained steps, no export in between; the device
     runs them back to back.  An exhausted sampler raises DataStarvationError.  return_losses:
     the k steps' critic1 / critic2 / policy losses as a [k, 3, n] array (with host batches the
@@ -554,7 +589,188 @@ def update_k_steps(st, sampler: Callable[[], Optional[TransitionBatch]], k: int,
             raise DataStarvationError(f"update_k_steps: sampler exhausted after {i} of {k} steps")
         batches.append(b)
     st._sync_hyper(hyper)
-    return st._update(batches, return_losses=return_losses)
+    with _hooked(st, hook):
+        return st._update(batches, return_losses=return_losses)
+
+
+# ---------------------------------------------------------------------- DvD (evolve.hpp:304-525)
+@dataclass
+class LambdaSchedule:
+    """Linear ramp from start to end over horizon steps, clamped afterwards (evolve.hpp:304-309)."""
+    start: float = 0.0
+    end: float = 0.5
+    horizon: int = 1
+
+
+def dvd_lambda(step: int, s: LambdaSchedule) -> float:
+    """dvd_lambda (evolve.hpp:311-315)."""
+    out = C.c_double()
+    _lib.call("pbrl_dvd_lambda", int(step), float(s.start), float(s.end), int(s.horizon),
+              C.byref(out))
+    return out.value
+
+
+@dataclass
+class DvDConfig:
+    """DvDConfig (evolve.hpp:480-497): probe states (row-major M x ds), kernel and schedule."""
+    probe_states: Sequence[float] = field(default_factory=list)
+    m_states: int = 0
+    length_scale: float = 1.0
+    jitter: float = 1e-6
+    schedule: LambdaSchedule = field(default_factory=LambdaSchedule)
+
+    def validate(self, population: int) -> None:
+        if self.m_states < population:
+            raise ConfigError("DvDConfig: need at least as many probe states as members")
+        if not self.length_scale > 0:
+            raise ConfigError("DvDConfig: length scale must be positive")
+        if self.jitter < 0:
+            raise ConfigError("DvDConfig: jitter must be >= 0")
+
+
+class DvdHook:
+    """dvd_policy_hook(cfg, step) (evolve.hpp:507-525): the diversity gradient of
+    -lambda * logdet(K + jitter I) over the policies' probe-state embeddings, added to the policy
+    gradients inside the device update step."""
+
+    def __init__(self, cfg: DvDConfig, lam: float):
+        self.cfg, self.lam = cfg, float(lam)
+
+    def _install(self, st) -> None:
+        probe = np.ascontiguousarray(np.asarray(self.cfg.probe_states, np.float64).ravel())
+        if probe.size != self.cfg.m_states * st.obs_dim:
+            raise ShapeError("dvd_embed: probe matrix size != M * observation_dim")
+        _lib.call("pbrl_set_dvd", st.handle, _ptr(probe, _lib.f64p), self.cfg.m_states,
+                  float(self.cfg.length_scale), float(self.cfg.jitter), self.lam)
+
+
+def dvd_policy_hook(cfg: DvDConfig, step: int) -> DvdHook:
+    return DvdHook(cfg, dvd_lambda(step, cfg.schedule))
+
+
+def dvd_embed(policies: "Td3State", probe_states, m_states: int) -> np.ndarray:
+    """dvd_embed (evolve.hpp:334-339): [n, m_states * da] deterministic actions on the probes."""
+    probe = np.ascontiguousarray(np.asarray(probe_states, np.float64).ravel())
+    if probe.size != m_states * policies.obs_dim:
+        raise ShapeError("dvd_embed: probe matrix size != M * observation_dim")
+    out = np.empty((policies.n, m_states * policies.act_dim), np.float32)
+    _lib.call("pbrl_dvd_embed", policies.handle, _ptr(probe, _lib.f64p), m_states,
+              _ptr(out, _lib.f32p))
+    return out
+
+
+@dataclass
+class DvdLossOut:
+    loss: float
+    logdet: float
+    grad: np.ndarray  # [n, E]
+
+
+def dvd_loss(embeddings, length_scale: float, jitter: float, lam: float) -> DvdLossOut:
+    """dvd_loss (evolve.hpp:425-478) on host embeddings (double)."""
+    e = np.ascontiguousarray(embeddings, np.float64)
+    if e.ndim != 2 or e.shape[0] < 2:
+        raise ConfigError("dvd_loss: need at least two embedding rows")
+    loss, logdet = C.c_double(), C.c_double()
+    grad = np.zeros_like(e)
+    _lib.call("pbrl_dvd_loss", _ptr(e, _lib.f64p), e.shape[0], e.shape[1], float(length_scale),
+              float(jitter), float(lam), C.byref(loss), C.byref(logdet), _ptr(grad, _lib.f64p))
+    return DvdLossOut(loss.value, logdet.value, grad)
+
+
+def median_pairwise_distance(embeddings) -> float:
+    """median_pairwise_distance (evolve.hpp:481-499)."""
+    e = np.ascontiguousarray(embeddings, np.float64)
+    out = C.c_double()
+    _lib.call("pbrl_median_pairwise_distance", _ptr(e, _lib.f64p), e.shape[0],
+              int(np.prod(e.shape[1:])) if e.ndim > 1 else 1, C.byref(out))
+    return out.value
+
+
+# ---------------------------------------------------------------------- CEM (evolve.hpp:221-297)
+class CEMState:
+    """CEMState (evolve.hpp:224-233) over the flat policy vectors of a TD3 population, resident
+    on its device: mean / var (double [P]), the noise schedule and the last candidates."""
+
+    def __init__(self, policies: "Td3State", mean=None, init_var: float = 0.0):
+        self.pop = policies
+        m = None if mean is None else np.ascontiguousarray(mean, np.float64)
+        if m is not None and m.size != policies.param_count("policy"):
+            raise ShapeError("cem_init: mean length != policy parameter count")
+        h = C.c_void_p()
+        _lib.call("pbrl_cem_create", policies.handle,
+                  None if m is None else _ptr(m, _lib.f64p), float(init_var), C.byref(h))
+        self._h = h
+        self._keep = m
+        self.noise_init, self.noise_final, self.noise_decay = 1e-2, 1e-3, 0.999
+        self.elite_fraction = 0.5
+        self._noise = 1e-2
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _lib.lib().pbrl_cem_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def _push(self):
+        _lib.call("pbrl_cem_set_params", self._h, self._noise, self.noise_final,
+                  self.noise_decay, self.elite_fraction)
+
+    @property
+    def noise(self) -> float:
+        return self._noise
+
+    @noise.setter
+    def noise(self, v: float) -> None:
+        self._noise = float(v)
+
+    def _get(self):
+        P = self.pop.param_count("policy")
+        mean, var = np.empty(P, np.float64), np.empty(P, np.float64)
+        nz = C.c_double()
+        _lib.call("pbrl_cem_get", self._h, _ptr(mean, _lib.f64p), _ptr(var, _lib.f64p),
+                  C.byref(nz))
+        return mean, var, nz.value
+
+    @property
+    def mean(self) -> np.ndarray:
+        return self._get()[0]
+
+    @property
+    def var(self) -> np.ndarray:
+        return self._get()[1]
+
+    def candidates(self) -> np.ndarray:
+        out = np.empty((self.pop.n, self.pop.param_count("policy")), np.float64)
+        _lib.call("pbrl_cem_candidates", self._h, _ptr(out, _lib.f64p))
+        return out
+
+
+def cem_init(policies: "Td3State", mean=None, init_var: float = 0.0) -> CEMState:
+    """cem_init (evolve.hpp:235-241); mean None = flatten_member(policy, 0) (pipeline_run.hpp:159)."""
+    return CEMState(policies, mean, init_var)
+
+
+def cem_resample(cem: CEMState, rng: RngSequence) -> np.ndarray:
+    """cem_resample (pipeline_run.hpp:148-158): cem_sample(cem, n, rng) on the device, each
+    candidate written into its member's policy, targets = policies, policy Adam reset.  Returns
+    the candidates [n, P] (double)."""
+    cem._push()
+    nx = C.c_uint64(rng.next)
+    _lib.call("pbrl_cem_resample", cem._h, rng.stream.key, C.byref(nx))
+    rng.next = nx.value
+    return cem.candidates()
+
+
+def cem_update(cem: CEMState, scores) -> None:
+    """cem_update (evolve.hpp:255-297) against the candidates of the last cem_resample."""
+    sc = np.ascontiguousarray(scores, np.float64)
+    cem._push()
+    _lib.call("pbrl_cem_update", cem._h, _ptr(sc, _lib.f64p), sc.size)
+    cem._noise = max(cem.noise_final, cem._noise * cem.noise_decay)
 
 
 # ---------------------------------------------------------------------- checkpoints

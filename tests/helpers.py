@@ -54,10 +54,12 @@ def parity_case(pb, ora, name, precision, device=0):
     c = tolerances()["cases"][name]
     algo, n, hidden, B, K, seed = c["algo"], c["n"], c["hidden"], c["batch"], c["K"], c["seed"]
     ds, da, ratio = c["ds"], c["da"], c["ratio"]
+    shared = bool(c.get("shared", False))
     make = pb.make_td3_state if algo == "td3" else pb.make_sac_state
-    st = make(n, ds, da, hidden, 1.0, seed, precision=precision, device=device)
+    st = make(n, ds, da, hidden, 1.0, seed, precision=precision, device=device,
+              mode="shared_critic" if shared else "independent")
     ora.set_emulation(0)
-    ref = (ora.td3 if algo == "td3" else ora.sac)(n, ds, da, hidden, 1.0, seed)
+    ref = (ora.td3 if algo == "td3" else ora.sac)(n, ds, da, hidden, 1.0, seed, shared=shared)
     hy = pb.Td3Hyper.defaults(n) if algo == "td3" else pb.SacHyper.defaults(n, da)
     if algo == "td3" and ratio is not None:
         hy.policy_delay_ratio = [ratio] * n
@@ -66,11 +68,24 @@ def parity_case(pb, ora, name, precision, device=0):
     w0 = {net: ref.get_net(net).astype(np.float64) for net in nets}
     raw = ora.synthetic_batches(K, n, B, ds, da, seed)
     upd = pb.td3_update_step if algo == "td3" else pb.sac_update_step
+    dcfg, hook = None, None
+    if c.get("dvd"):
+        d = c["dvd"]
+        probe = np.random.default_rng(d["seed"]).uniform(-1.0, 1.0, (d["ms"], ds))
+        dcfg = {"probe": probe, "length_scale": d["length_scale"], "jitter": 1e-6,
+                "lam_start": d["lam"], "lam_end": d["lam"], "horizon": 1, "step": 0}
+        cfg = pb.DvDConfig(probe.ravel(), d["ms"], d["length_scale"], 1e-6,
+                           pb.LambdaSchedule(d["lam"], d["lam"], 1))
+        hook = pb.dvd_policy_hook(cfg, 0)
     lerr = []
     for k in range(K):
-        upd(st, to_batch(pb, raw, k), hy)
+        if hook is not None:
+            upd(st, to_batch(pb, raw, k), hy, hook=hook)
+        else:
+            upd(st, to_batch(pb, raw, k), hy)
         dl = np.stack(st.last_losses()).astype(np.float64)
-        rl = ref.step(raw_at(raw, k), oh)
+        rl = ref.step(raw_at(raw, k), oh) if dcfg is None else ref.step(raw_at(raw, k), oh,
+                                                                         dvd=dcfg)
         lerr.append(float(np.max(np.abs(dl - rl) / np.maximum(np.abs(rl), 1e-3))))
     werr = {net: rel_delta_err(st.params(net), ref.get_net(net), w0[net]) for net in nets}
     return np.asarray(lerr), werr
