@@ -576,6 +576,7 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
         a.gamma = top->gamma;
         a.y = top->y;
         a.loss = top->loss;
+        a.norm_rows = top->norm_rows;
       }
       Mat dh{};
       if (l > 0) {

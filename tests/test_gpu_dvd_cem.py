@@ -119,7 +119,7 @@ def test_cem_resample_and_update(pb, ora):
     assert rng.next == nxt == 2 * n * P
     # device double log / cos may differ from glibc in the last bit: the candidates agree to a
     # few double ulp and the float policies bit for bit (but for a rare rounding-boundary case)
-    assert np.max(np.abs(cand - want) / np.maximum(np.abs(want), 1e-300)) < 1e-14
+    assert np.max(np.abs(cand - want)) < 1e-14
     pol = st.params("policy")
     assert np.mean(pol == want.astype(np.float32)) > 1 - 1e-5
     assert bits_equal(pol, cand.astype(np.float32))
@@ -140,4 +140,4 @@ def test_cem_resample_and_update(pb, ora):
     # the next generation samples around the refit mean
     cand2 = pb.cem_resample(cem, rng)
     want2, _ = ora.cem_sample(m2, v2, nz, n, rng.stream.key, 2 * n * P)
-    assert np.max(np.abs(cand2 - want2) / np.maximum(np.abs(want2), 1e-300)) < 1e-14
+    assert np.max(np.abs(cand2 - want2)) < 1e-14

@@ -44,8 +44,8 @@ def test_td3_shared_bitexact(pb, ora, n, hidden, B, K):
     hy.tau = list(np.linspace(0.005, 0.05, n))
     oh = {f: list(getattr(hy, f)) for f in pb.Td3Hyper.FIELDS}
     raw = ora.synthetic_batches(K, n, B, ds, da, 29)
-    p2 = st.flatten_member("policy", 2)
     for k in range(K):
+        p2 = st.flatten_member("policy", 2)
         mask = [1, 1] + [0] * (n - 2) if k == 1 else None
         if k == 2:
             mask = [0] * n  # nobody fires: no policy update, no critic-target Polyak
