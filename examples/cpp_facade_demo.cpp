@@ -8,7 +8,7 @@
 int main() {
   namespace pb = pbrl::b200;
   const std::size_t n = 4, ds = 17, da = 6, B = 64;
-  auto st = pb::make_td3_state(n, ds, da, {256, 256}, 1.0, 7, pb::Precision::kTf32);
+  auto st = pb::make_td3_state(n, ds, da, {256, 256}, 1.0, 7, pb::PopMode::kIndependent, pb::Precision::kTf32);
   auto hy = pb::Td3Hyper::defaults(n);
   std::mt19937 gen(1);
   std::uniform_real_distribution<float> u(-1.f, 1.f);

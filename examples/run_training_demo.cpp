@@ -3,7 +3,9 @@
 // replay rings with batched inserts under the ratio guard, and the learner thread running
 // device sample + K-update bursts (the reference's run_training, pipeline_run.hpp:77-468).
 //
-//   run_training_demo [pop] [workers] [total_updates] [K] [pbt 0|1] [bf16|tf32|ffma32]
+//   run_training_demo [pop] [workers] [total_updates] [K] [none|pbt|cem|dvd (0|1 = none|pbt)]
+//                     [bf16|tf32|ffma32]
+// cem / dvd run the shared-critic TD3 population on one shared replay ring (pipeline.hpp:229-238).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -18,7 +20,17 @@ int main(int argc, char** argv) {
   cfg.actor_workers = argc > 2 ? std::strtoul(argv[2], nullptr, 10) : 2;
   cfg.total_updates = argc > 3 ? std::strtoul(argv[3], nullptr, 10) : 400;
   cfg.updates_per_burst = argc > 4 ? std::strtoul(argv[4], nullptr, 10) : 20;
-  cfg.strategy = (argc > 5 && std::atoi(argv[5])) ? Strategy::kPbt : Strategy::kNone;
+  const char* strat = argc > 5 ? argv[5] : "none";
+  cfg.strategy = (!std::strcmp(strat, "1") || !std::strcmp(strat, "pbt")) ? Strategy::kPbt
+                 : !std::strcmp(strat, "cem")                            ? Strategy::kCem
+                 : !std::strcmp(strat, "dvd")                            ? Strategy::kDvd
+                                                                         : Strategy::kNone;
+  if (cfg.strategy == Strategy::kCem || cfg.strategy == Strategy::kDvd) {
+    cfg.mode = PopMode::kSharedCritic;
+    cfg.buffer_mode = BufferMode::kShared;
+    cfg.cem_generation_updates = 100;
+    cfg.dvd.schedule = LambdaSchedule{0.0, 0.5, 200};
+  }
   const char* prec = argc > 6 ? argv[6] : "bf16";
   cfg.precision = !std::strcmp(prec, "tf32")     ? Precision::kTf32
                   : !std::strcmp(prec, "ffma32") ? Precision::kFfma32

@@ -139,6 +139,11 @@ int pbrl_update_batches_losses(pbrl_pop* pop, const pbrl_batch* batches, uint32_
  * holds fewer than max(min_size, 1) transitions (sample_batch's nullopt). */
 int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t sample_seed, uint64_t first_draw_id,
                   uint64_t batch_rows, uint64_t min_size, int* ready);
+/* the same with td3_update_step's policy_member_mask on every step ([n] bytes; TD3) -- the
+ * CEM-RL learner trains only the first half of the population (pipeline_run.hpp:322-326) */
+int pbrl_update_k_masked(pbrl_pop* pop, uint32_t k, uint64_t sample_seed, uint64_t first_draw_id,
+                         uint64_t batch_rows, uint64_t min_size, const uint8_t* policy_mask,
+                         int* ready);
 /* Per-member losses of the LAST step: critic1 / critic2 MSE (mse_loss_grads, algos.hpp:288-314)
  * and the policy loss (td3_policy_loss_grads :318-338 / sac_policy_loss_grads :643-735);
  * each [n] (TD3 policy entries are 0 for members that did not fire). */

@@ -15,6 +15,7 @@
 // TransitionBatch (algos.hpp:14-24), row-major [N][B][dim].
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <deque>
 #include <functional>
@@ -53,6 +54,10 @@ class DataStarvationError : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
 };
+class DegeneratePopulationError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
 class DeviceError : public std::runtime_error {
  public:
   using std::runtime_error::runtime_error;
@@ -70,6 +75,7 @@ inline void check(int rc) {
     case PBRL_E_NOT_READY: throw NotReadyError(m);
     case PBRL_E_RESOURCE: throw ResourceError(m);
     case PBRL_E_STARVATION: throw DataStarvationError(m);
+    case PBRL_E_DEGENERATE: throw DegeneratePopulationError(m);
     default: throw DeviceError(m);
   }
 }
@@ -83,6 +89,10 @@ enum class Net : int {
   kCritic2Target = PBRL_NET_CRITIC2_TARGET,
 };
 enum class Precision : int { kFfma32 = PBRL_PREC_FFMA32, kTf32 = PBRL_PREC_TF32, kBf16 = PBRL_PREC_BF16 };
+enum class PopMode : int {  // algos.hpp:26
+  kIndependent = PBRL_MODE_INDEPENDENT,
+  kSharedCritic = PBRL_MODE_SHARED_CRITIC,
+};
 
 // ---------------------------------------------------------------- batches (algos.hpp:14-24)
 struct TransitionBatch {
@@ -143,7 +153,8 @@ class Population {
   Population(int algo, std::size_t n, std::size_t obs_dim, std::size_t act_dim,
              const std::vector<std::size_t>& hidden, double action_bound, std::uint64_t seed,
              Precision precision = Precision::kFfma32, int device = 0,
-             std::uint64_t member_offset = 0, std::uint64_t n_global = 0)
+             std::uint64_t member_offset = 0, std::uint64_t n_global = 0,
+             PopMode mode = PopMode::kIndependent)
       : n_(n), ds_(obs_dim), da_(act_dim) {
     std::vector<std::uint64_t> h(hidden.begin(), hidden.end());
     pbrl_pop_desc d{};
@@ -159,6 +170,7 @@ class Population {
     d.device = device;
     d.member_offset = member_offset;
     d.n_global = n_global;
+    d.mode = static_cast<int>(mode);
     check(pbrl_pop_create(&d, &h_));
   }
   ~Population() {
@@ -201,7 +213,7 @@ class Population {
     }
   }
   friend void td3_update_step(class Td3State&, const TransitionBatch&, const Td3Hyper&,
-                              const std::vector<char>*);
+                              const struct PolicyGradHook*, const std::vector<char>*);
   friend void sac_update_step(class SacState&, const TransitionBatch&, const SacHyper&);
   template <typename S, typename H>
   friend void update_k_steps(S&, const std::function<std::optional<TransitionBatch>()>&,
@@ -228,26 +240,145 @@ class SacState : public Population {  // algos.hpp:473-521
 
 inline Td3State make_td3_state(std::size_t n, std::size_t obs_dim, std::size_t act_dim,
                                const std::vector<std::size_t>& hidden, double action_bound,
-                               std::uint64_t seed, Precision precision = Precision::kFfma32,
-                               int device = 0) {
+                               std::uint64_t seed, PopMode mode = PopMode::kIndependent,
+                               Precision precision = Precision::kFfma32, int device = 0) {
   return Td3State(PBRL_ALGO_TD3, n, obs_dim, act_dim, hidden, action_bound, seed, precision,
-                  device);
+                  device, 0, 0, mode);
 }
 
 inline SacState make_sac_state(std::size_t n, std::size_t obs_dim, std::size_t act_dim,
                                const std::vector<std::size_t>& hidden, double action_bound,
-                               std::uint64_t seed, Precision precision = Precision::kFfma32,
-                               int device = 0) {
+                               std::uint64_t seed, PopMode mode = PopMode::kIndependent,
+                               Precision precision = Precision::kFfma32, int device = 0) {
   return SacState(PBRL_ALGO_SAC, n, obs_dim, act_dim, hidden, action_bound, seed, precision,
-                  device);
+                  device, 0, 0, mode);
+}
+
+// ---------------------------------------------------------------- DvD (evolve.hpp:304-525)
+struct LambdaSchedule {
+  double start = 0.0;
+  double end = 0.5;
+  std::uint64_t horizon = 1;
+};
+
+inline double dvd_lambda(std::uint64_t step, const LambdaSchedule& s) {
+  double out = 0;
+  check(pbrl_dvd_lambda(step, s.start, s.end, s.horizon, &out));
+  return out;
+}
+
+struct DvDConfig {
+  std::vector<double> probe_states;  // row-major M x ds
+  std::size_t m_states = 0;
+  double length_scale = 1.0;
+  double jitter = 1e-6;
+  LambdaSchedule schedule;
+  void validate(std::size_t population) const {
+    if (m_states < population)
+      throw ConfigError("DvDConfig: need at least as many probe states as members");
+    if (!(length_scale > 0)) throw ConfigError("DvDConfig: length scale must be positive");
+    if (jitter < 0) throw ConfigError("DvDConfig: jitter must be >= 0");
+  }
+};
+
+// dvd_policy_hook(cfg, step): applied on the device inside the update calls it is passed to
+struct PolicyGradHook {
+  DvDConfig cfg;
+  double lambda = 0.0;
+};
+inline PolicyGradHook dvd_policy_hook(const DvDConfig& cfg, std::uint64_t step) {
+  return PolicyGradHook{cfg, dvd_lambda(step, cfg.schedule)};
+}
+
+struct DvdLossOut {
+  double loss = 0, logdet = 0;
+  std::vector<double> grad;  // [N][E]
+};
+inline DvdLossOut dvd_loss(const std::vector<double>& emb, std::size_t n, double length_scale,
+                           double jitter, double lambda) {
+  if (n == 0 || emb.size() % n != 0) throw ShapeError("dvd_loss: embeddings not [N, E]");
+  DvdLossOut o;
+  o.grad.assign(emb.size(), 0.0);
+  check(pbrl_dvd_loss(emb.data(), n, emb.size() / n, length_scale, jitter, lambda, &o.loss,
+                      &o.logdet, o.grad.data()));
+  return o;
+}
+inline double median_pairwise_distance(const std::vector<double>& emb, std::size_t n) {
+  double out = 1.0;
+  check(pbrl_median_pairwise_distance(emb.data(), n, n ? emb.size() / n : 0, &out));
+  return out;
+}
+inline std::vector<float> dvd_embed(Population& policies, const std::vector<double>& probe,
+                                    std::size_t m_states) {
+  std::vector<float> out(policies.members() * m_states * policies.act_dim());
+  check(pbrl_dvd_embed(policies.handle(), probe.data(), m_states, out.data()));
+  return out;
+}
+
+namespace detail {
+struct HookScope {  // installs the hook for one update call
+  pbrl_pop* h;
+  bool on;
+  HookScope(pbrl_pop* pop, const PolicyGradHook* hook, std::size_t obs_dim) : h(pop), on(hook) {
+    if (!hook) return;
+    if (hook->cfg.probe_states.size() != hook->cfg.m_states * obs_dim)
+      throw ShapeError("dvd_embed: probe matrix size != M * observation_dim");
+    check(pbrl_set_dvd(h, hook->cfg.probe_states.data(), hook->cfg.m_states,
+                       hook->cfg.length_scale, hook->cfg.jitter, hook->lambda));
+  }
+  ~HookScope() {
+    if (on) pbrl_set_dvd(h, nullptr, 0, 1.0, 0.0, 0.0);
+  }
+};
+}  // namespace detail
+
+// ---------------------------------------------------------------- CEM (evolve.hpp:221-297)
+// The search distribution lives on the population's device; cem_resample draws the candidates
+// straight into the policies (pipeline_run.hpp:148-158).
+class CEMState {
+ public:
+  CEMState(Population& policies, const std::vector<double>* mean, double init_var)
+      : pop_(&policies) {
+    check(pbrl_cem_create(policies.handle(), mean ? mean->data() : nullptr, init_var, &h_));
+  }
+  ~CEMState() {
+    if (h_) pbrl_cem_destroy(h_);
+  }
+  CEMState(const CEMState&) = delete;
+  CEMState& operator=(const CEMState&) = delete;
+  double noise = 1e-2, noise_init = 1e-2, noise_final = 1e-3, noise_decay = 0.999;
+  double elite_fraction = 0.5;
+  pbrl_cem* handle() const { return h_; }
+  Population& population() const { return *pop_; }
+  void push() const { check(pbrl_cem_set_params(h_, noise, noise_final, noise_decay, elite_fraction)); }
+
+ private:
+  Population* pop_;
+  pbrl_cem* h_ = nullptr;
+};
+
+// cem_resample: RngSequence (key, *next) as the reference's RngSequence(seed, 2, kCemDraw, gen)
+inline void cem_resample(CEMState& st, std::uint64_t rng_key, std::uint64_t* rng_next) {
+  st.push();
+  check(pbrl_cem_resample(st.handle(), rng_key, rng_next));
+}
+inline void cem_resample_into(CEMState& st, std::uint64_t rng_key, std::uint64_t* rng_next) {
+  cem_resample(st, rng_key, rng_next);
+}
+inline void cem_update(CEMState& st, const std::vector<double>& scores) {
+  st.push();
+  check(pbrl_cem_update(st.handle(), scores.data(), scores.size()));
+  st.noise = std::max(st.noise_final, st.noise * st.noise_decay);
 }
 
 // td3_update_step (algos.hpp:351-422); policy_member_mask as in the reference
 inline void td3_update_step(Td3State& st, const TransitionBatch& batch, const Td3Hyper& hyper,
+                            const PolicyGradHook* hook = nullptr,
                             const std::vector<char>* policy_member_mask = nullptr) {
   if (batch.members() != st.members())
     throw ConfigError("td3_update_step: batch population != state population");
   st.sync_hyper(hyper);
+  detail::HookScope hs(st.handle(), hook, st.obs_dim());
   const pbrl_batch b = batch.view();
   std::vector<std::uint8_t> mask;
   if (policy_member_mask) mask.assign(policy_member_mask->begin(), policy_member_mask->end());

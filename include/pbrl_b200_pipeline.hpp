@@ -302,10 +302,11 @@ class PointMassEnv final : public Env {
 
 // ---------------------------------------------------------------- configuration / summary
 enum class Algo { kTd3, kSac };
-enum class Strategy { kNone, kPbt };
+enum class Strategy { kNone, kPbt, kCem, kDvd };
 
-struct RunConfig {  // pipeline.hpp:180-244 (the independent-mode fields)
+struct RunConfig {  // pipeline.hpp:176-244
   Algo algo = Algo::kTd3;
+  PopMode mode = PopMode::kIndependent;
   Strategy strategy = Strategy::kNone;
   std::size_t population = 1;
   std::size_t updates_per_burst = 50;  // K
@@ -328,6 +329,11 @@ struct RunConfig {  // pipeline.hpp:180-244 (the independent-mode fields)
   bool bootstrap_timeouts = true;
   std::chrono::milliseconds starvation_timeout{30000};
   std::uint64_t pbt_interval = 2000;
+  std::size_t cem_generation_updates = 500;  // update steps per generation
+  double cem_init_var = 0.0;
+  DvDConfig dvd;
+  bool dvd_auto_probe = true;  // probe states from environment resets
+  std::size_t dvd_probe_count = 16;
   std::size_t insert_block = 256;  // transitions per batched device insert
   Precision precision = Precision::kBf16;
   int device = 0;
@@ -341,6 +347,16 @@ struct RunConfig {  // pipeline.hpp:180-244 (the independent-mode fields)
     if (!(env_steps_per_member_per_update > 0))
       throw ConfigError("RunConfig: env_steps_per_member_per_update must be positive");
     if (!make_env) throw ConfigError("RunConfig: make_env is required");
+    if (strategy == Strategy::kCem || strategy == Strategy::kDvd) {
+      if (mode != PopMode::kSharedCritic)
+        throw ConfigError("RunConfig: CEM and DvD strategies require shared-critic mode");
+      if (buffer_mode != BufferMode::kShared)
+        throw ConfigError("RunConfig: CEM and DvD strategies require a shared buffer");
+      if (strategy == Strategy::kCem && population % 2 != 0)
+        throw ConfigError("RunConfig: CEM needs an even population");
+      if (algo != Algo::kTd3)  // pipeline_run.hpp:81-83
+        throw ConfigError("RunConfig: CEM and DvD strategies are TD3-only");
+    }
     if (strategy == Strategy::kPbt && buffer_mode != BufferMode::kPerAgent)
       throw ConfigError("RunConfig: PBT tunes hyperparameters, so buffers must not be mixed");
   }
@@ -443,7 +459,8 @@ inline void actor_loop(const RunConfig& cfg, const std::vector<std::size_t>& mem
 
 }  // namespace detail
 
-// run_training (pipeline_run.hpp:77-468) for independent-mode TD3 / SAC, optionally with PBT.
+// run_training (pipeline_run.hpp:77-468): TD3 / SAC, independent or shared critic, with PBT,
+// CEM (pipeline_run.hpp:143-162, :388-409) or DvD (:164-181, :343-347).
 inline RunSummary run_training(const RunConfig& cfg) {
   cfg.validate();
   const std::size_t n = cfg.population;
@@ -457,7 +474,8 @@ inline RunSummary run_training(const RunConfig& cfg) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   };
   const int algo = cfg.algo == Algo::kTd3 ? PBRL_ALGO_TD3 : PBRL_ALGO_SAC;
-  Population learner(algo, n, ds, da, cfg.hidden, bound, cfg.seed, cfg.precision, cfg.device);
+  Population learner(algo, n, ds, da, cfg.hidden, bound, cfg.seed, cfg.precision, cfg.device, 0,
+                     0, cfg.mode);
   std::mutex learner_mu;  // the C ABI's one-caller-per-handle contract
 
   // hypers (pipeline_run.hpp:94-125)
@@ -516,6 +534,53 @@ inline RunSummary run_training(const RunConfig& cfg) {
       return x ^ (x >> 31);
     };
     pbt_key = mix(mix(mix(mix(cfg.seed) ^ 0) ^ 8) ^ 0);
+  }
+  auto mix64 = [](std::uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+  };
+  auto stream_key = [&](std::uint64_t seed, std::uint64_t stream, std::uint64_t use,
+                        std::uint64_t step) {
+    return mix64(mix64(mix64(mix64(seed) ^ stream) ^ use) ^ step);
+  };
+
+  // CEM (pipeline_run.hpp:143-162): the distribution around flatten_member(policy, 0), every
+  // generation drawn into the policies from RngSequence(seed, 2, kCemDraw, generation)
+  std::unique_ptr<CEMState> cem;
+  std::vector<std::vector<double>> cem_gen_returns(n);
+  std::size_t cem_gen_done = 0;
+  std::uint64_t cem_generation = 0;
+  std::vector<std::uint8_t> cem_train_mask;
+  auto cem_resample = [&] {
+    std::uint64_t next = 0;
+    cem_resample_into(*cem, stream_key(cfg.seed, 2, 10, cem_generation++), &next);
+    for (auto& r : cem_gen_returns) r.clear();
+  };
+  if (cfg.strategy == Strategy::kCem) cem = std::make_unique<CEMState>(learner, nullptr, cfg.cem_init_var);
+
+  // DvD (pipeline_run.hpp:164-181): probe states from environment resets, the length scale the
+  // median pairwise distance of the initial embeddings (frozen for the run)
+  DvDConfig dvd = cfg.dvd;
+  if (cfg.strategy == Strategy::kDvd) {
+    if (cfg.dvd_auto_probe) {
+      dvd.m_states = std::max(cfg.dvd_probe_count, n);
+      dvd.probe_states.clear();
+      auto env = cfg.make_env();
+      for (std::size_t i = 0; i < dvd.m_states; ++i) {
+        const std::vector<double> obs = env->reset(mix64(cfg.seed ^ 0x9E0B0E5ull) + i);
+        dvd.probe_states.insert(dvd.probe_states.end(), obs.begin(), obs.end());
+      }
+    }
+    const std::vector<float> emb = dvd_embed(learner, dvd.probe_states, dvd.m_states);
+    dvd.length_scale = median_pairwise_distance(std::vector<double>(emb.begin(), emb.end()), n);
+    dvd.validate(n);
+  }
+  if (cfg.strategy == Strategy::kCem) {  // :322-327
+    cem_train_mask.assign(n, 0);
+    for (std::size_t m = 0; m < n / 2; ++m) cem_train_mask[m] = 1;
+    cem_resample();
   }
   {
     std::lock_guard<std::mutex> lk(learner_mu);
@@ -606,8 +671,12 @@ inline RunSummary run_training(const RunConfig& cfg) {
   std::string abort_reason;
   auto handle_reports = [&] {
     for (const EpisodeReport& r : reports.drain()) {
-      if (r.deterministic_eval) summary.eval_episodes += 1;
-      else pbt.record_return(r.member, r.ep_return);
+      if (r.deterministic_eval) {
+        summary.eval_episodes += 1;
+      } else {
+        pbt.record_return(r.member, r.ep_return);
+        if (cfg.strategy == Strategy::kCem) cem_gen_returns[r.member].push_back(r.ep_return);
+      }
     }
   };
   try {
@@ -620,8 +689,17 @@ inline RunSummary run_training(const RunConfig& cfg) {
           int ok = 0;
           {
             std::lock_guard<std::mutex> lk(learner_mu);
-            check(pbrl_update_k(learner.handle(), static_cast<std::uint32_t>(k_next), cfg.seed,
-                                draw_id, cfg.batch_size, cfg.warmup_per_buffer, &ok));
+            // DvD: dvd_policy_hook(dvd, done_updates) for this burst (:343-347)
+            std::optional<detail::HookScope> hook;
+            PolicyGradHook hk;
+            if (cfg.strategy == Strategy::kDvd) {
+              hk = dvd_policy_hook(dvd, done_updates);
+              hook.emplace(learner.handle(), &hk, ds);
+            }
+            check(pbrl_update_k_masked(learner.handle(), static_cast<std::uint32_t>(k_next),
+                                       cfg.seed, draw_id, cfg.batch_size, cfg.warmup_per_buffer,
+                                       cem_train_mask.empty() ? nullptr : cem_train_mask.data(),
+                                       &ok));
           }
           if (ok) {
             ready = true;
@@ -662,6 +740,28 @@ inline RunSummary run_training(const RunConfig& cfg) {
             summary.evolve_events += 1;
             mailbox.publish(learner, explore_vec());
             published += 1;
+          }
+        }
+      }
+      if (cfg.strategy == Strategy::kCem) {  // :388-409
+        cem_gen_done += k_next;
+        if (cem_gen_done >= cfg.cem_generation_updates) {
+          bool all_scored = true;
+          for (const auto& r : cem_gen_returns) all_scored = all_scored && !r.empty();
+          if (all_scored) {  // otherwise the generation extends by another burst
+            std::vector<double> scores(n);
+            for (std::size_t m = 0; m < n; ++m) {
+              double acc = 0;
+              for (double v : cem_gen_returns[m]) acc += v;
+              scores[m] = acc / static_cast<double>(cem_gen_returns[m].size());
+            }
+            std::lock_guard<std::mutex> lk(learner_mu);
+            cem_update(*cem, scores);
+            cem_resample();
+            mailbox.publish(learner, explore_vec());
+            published += 1;
+            summary.evolve_events += 1;
+            cem_gen_done = 0;
           }
         }
       }

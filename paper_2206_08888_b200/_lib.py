@@ -55,6 +55,7 @@ class CommOps(C.Structure):
 # name -> (restype, argtypes); every function returns an int status
 SIGNATURES = {
     "pbrl_attach_comm": [vp, vp],
+    "pbrl_update_k_masked": [vp, u32, u64, u64, u64, u64, u8p, intp],
     "pbrl_set_dvd": [vp, f64p, u64, dbl, dbl, dbl],
     "pbrl_dvd_embed": [vp, f64p, u64, f32p],
     "pbrl_dvd_loss": [f64p, u64, u64, dbl, dbl, dbl, f64p, f64p, f64p],

@@ -769,25 +769,40 @@ int pbrl_sample_batch(pbrl_pop* pop, uint64_t seed, uint64_t draw_id, uint64_t r
   });
 }
 
-int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t seed, uint64_t first_draw_id,
-                  uint64_t rows, uint64_t min_size, int* ready) {
+int pbrl_update_k_masked(pbrl_pop* pop, uint32_t k, uint64_t seed, uint64_t first_draw_id,
+                         uint64_t rows, uint64_t min_size, const uint8_t* policy_mask, int* ready) {
   return guarded([&] {
     Pop* p = P(pop);
     *ready = 0;
     if (k < 1) PBRL_THROW(PBRL_E_CONFIG, "update_k_steps: k must be >= 1");
+    if (policy_mask && p->algo != PBRL_ALGO_TD3)
+      PBRL_THROW(PBRL_E_USAGE, "policy_member_mask is a TD3 option");
     if (!replay_ready(p, min_size)) return;
     p->validate_hyper();
     const int B = static_cast<int>(rows);
     p->ensure_scratch(B);
     p->ensure_ones();
     p->ensure_corr(p->t_bound + k + 4);
+    const uint8_t* d_mask = nullptr;
+    p->host_mask = policy_mask;
+    if (policy_mask) {
+      p->mask_buf.alloc(p->n);
+      p->mask_buf.upload(policy_mask, p->n, p->stream);
+      d_mask = p->mask_buf.p;
+    }
     for (uint32_t i = 0; i < k; ++i) {
       gather(p, B, seed, first_draw_id + i, p->act16() ? 1 : 0);
-      p->step(B, nullptr);
+      p->step(B, d_mask);
     }
+    p->host_mask = nullptr;
     CUDA_CHECK(cudaGetLastError());
     *ready = 1;
   });
+}
+
+int pbrl_update_k(pbrl_pop* pop, uint32_t k, uint64_t seed, uint64_t first_draw_id,
+                  uint64_t rows, uint64_t min_size, int* ready) {
+  return pbrl_update_k_masked(pop, k, seed, first_draw_id, rows, min_size, nullptr, ready);
 }
 
 // ---------------------------------------------------------------- PBT

@@ -460,6 +460,7 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     }
   }
   host_mask = nullptr;
+  host_mask = nullptr;  // the caller's buffer is only valid during the call
   if (losses_out) {
     sync();
     for (uint32_t i = 0; i < k; ++i) shared_losses_layout(losses_out + static_cast<size_t>(i) * 3 * n);
