@@ -179,6 +179,11 @@ Pop::~Pop() {
     cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
+    for (int i = 0; i < 2; ++i) {
+      if (side3[i]) cudaStreamDestroy(side3[i]);
+      if (ev_f3[i]) cudaEventDestroy(ev_f3[i]);
+      if (ev_j3[i]) cudaEventDestroy(ev_j3[i]);
+    }
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (cstream) cudaStreamDestroy(cstream);

@@ -324,7 +324,26 @@ struct Pop {
                float* DX, long long dx_gs, long long dx_ld, int epi, int col0, int ncols,
                const int* active, float scale);
   void gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
-               const int* active, bool bias_done = false);
+               const int* active, bool bias_done = false, int max_ctas = 0);
+  // graph mode, tensor-core modes: the last two weight-gradient products of a 2-hidden-layer
+  // backward on two graph branches with split persistent grids (PBRL_NO_DWFORK=1 disables)
+  static constexpr int kDwSideCtas = 40;
+  // [0]: the step graph, [1]: conditional bodies (a stream that joined one capture stays in it
+  // until that capture ends, so each capture graph forks onto its own stream)
+  cudaStream_t side3[2] = {nullptr, nullptr};
+  cudaEvent_t ev_f3[2] = {nullptr, nullptr}, ev_j3[2] = {nullptr, nullptr};
+  bool in_cond_body = false;  // capturing a conditional body (its own capture graph)
+  int cta_cap = 0;  // > 0: persistent tcgen05 launches use at most this many CTAs
+  // SMs of the online-critic forward branch while the target chain runs beside it (0: no split;
+  // PBRL_FWD_SPLIT overrides)
+  int fwd_split() const {
+    static const int v = std::getenv("PBRL_FWD_SPLIT") ? std::atoi(std::getenv("PBRL_FWD_SPLIT")) : 64;
+    return v;
+  }
+  bool dw_fork_ok() const {
+    static const bool off = std::getenv("PBRL_NO_DWFORK") != nullptr;
+    return capturing && use_tc() && !off;
+  }
   void mlp_forward(const NetShape& sh, const float* W, int groups, int B, Mat x,
                    std::vector<DBuf<float>>& hs, float* out, long long out_gs, long long out_ld,
                    int last_epi, const int* active = nullptr, float* C2 = nullptr,

@@ -76,6 +76,8 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
       a.mo_ld = ymask->mld;
     }
     a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
+  a.max_ctas = cta_cap;
+    a.max_ctas = cta_cap;
     timed(PC_GEMM_FWD, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
     return;
@@ -169,6 +171,8 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
     a.scale = scale;
     a.active = active;
     a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
+  a.max_ctas = cta_cap;
+    a.max_ctas = cta_cap;
     timed(PC_GEMM_DX, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, false, a, stream); });
     return;
@@ -198,7 +202,7 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
 
 // dW_l and db_l into the gradient arena rows: dW = X^T G, db = column sums of G
 void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X, Mat G,
-                  const int* active, bool bias_done) {
+                  const int* active, bool bias_done, int max_ctas) {
   const int in = sh.dims[l], out = sh.dims[l + 1];
   const double flops = 2.0 * B * in * out * groups;
   // algorithmic bytes: X (once per member when shared), G, dW
@@ -230,6 +234,7 @@ void Pop::gemm_dw(const NetShape& sh, float* Gr, int l, int groups, int B, Mat X
     a.c_gs = static_cast<long long>(sh.stride);
     a.c_rs = out;
     a.active = active;
+    a.max_ctas = max_ctas ? max_ctas : cta_cap;
     timed(PC_GEMM_DW, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bg, true, true, a, stream); });
     // bias gradient: per-column sums of G in row order (pop_add_bias_backward, :236-250),
@@ -455,6 +460,7 @@ bool Pop::mlp_forward2(const NetShape& sh, const float* W, int groups, int B, Ma
       4.0 * groups * (H1 + H2 + H2 * no + no) + (out_act ? 2.0 : 4.0) * groups * B * no +
       (keep_hidden ? groups * B * (2.0 * (H1 + H2) + 4.0 * ((H1 + 31) / 32 + (H2 + 31) / 32))
                    : 0.0);
+  a.max_ctas = cta_cap;
   timed(PC_GEMM_FWD, flops, bytes, active != nullptr, [&] { launch_mlp_fwd2(a, stream); });
   return true;
 }
@@ -531,6 +537,7 @@ bool Pop::gemm_fwd_fused(const NetShape& sh, const float* W, int l, int groups, 
       4.0 * groups * (hdim + hdim * nout + nout) + oe * groups * B * nout +
       (keep_hidden ? groups * B * (ae * hdim + 4.0 * ((hdim + 31) / 32)) : 0.0);
   a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
+  a.max_ctas = cta_cap;
   timed(PC_GEMM_FWD, flops, bytes, active != nullptr,
         [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
   return true;
@@ -599,6 +606,34 @@ void Pop::mlp_backward(const NetShape& sh, const float* W, float* Gr, int groups
       G = dh;
       bias_done = a.dbx != nullptr;
       continue;
+    }
+    if (l == 1 && L == 3 && dw_fork_ok()) {
+      // graph mode: after the dX product, the two weight-gradient products are independent --
+      // dW1 (h1^T dh2) keeps most of the SMs on the main branch while dW0 (x0^T dh1, a few small
+      // tiles) runs on a parallel branch on the rest (capped persistent grids co-reside, so
+      // dW0 leaves the critical path instead of trailing dW1)
+      const Mat dh = hid(dhs, 0, B, sh, 0);
+      gemm_dx(sh, W, 1, groups, B, G, x, const_cast<float*>(dh.p), dh.gs, dh.ld, EPI_RELU_MASK,
+              0, sh.dims[1], active, 1.0f);
+      const int fi = in_cond_body ? 1 : 0;
+      cudaStream_t& sd = side3[fi];
+      if (!sd) CUDA_CHECK(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking));
+      if (!ev_f3[fi]) {
+        for (cudaEvent_t* e : {&ev_f3[fi], &ev_j3[fi]})
+          CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      }
+      static const int side_ctas = std::getenv("PBRL_DW_SIDE") ? std::atoi(std::getenv("PBRL_DW_SIDE"))
+                                                               : kDwSideCtas;
+      CUDA_CHECK(cudaEventRecord(ev_f3[fi], stream));
+      CUDA_CHECK(cudaStreamWaitEvent(sd, ev_f3[fi], 0));
+      std::swap(stream, sd);
+      fork_window(stream);
+      gemm_dw(sh, Gr, 0, groups, B, x0, dh, active, false, side_ctas);
+      std::swap(stream, sd);
+      CUDA_CHECK(cudaEventRecord(ev_j3[fi], sd));
+      gemm_dw(sh, Gr, 1, groups, B, x, G, active, bias_done, num_sms_host() - side_ctas);
+      CUDA_CHECK(cudaStreamWaitEvent(stream, ev_j3[fi], 0));
+      return;
     }
     if (l > 0) {
       const Mat dh = hid(dhs, l - 1, B, sh, 0);
@@ -714,6 +749,7 @@ bool Pop::gemm_dx_to_action(int groups, int B, Mat G, Mat mask, float* out, long
   a.scale = scale;
   a.active = active;
   a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
+  a.max_ctas = cta_cap;
   const double flops = 2.0 * B * groups * (static_cast<double>(Hn) * H + H * da);
   const double bytes = eb * groups * (static_cast<double>(B) * Hn + static_cast<double>(Hn) * H) +
                        4.0 * groups * (B * ((H + 31) / 32) + H * da + 2.0 * B * da);
@@ -819,13 +855,16 @@ void Pop::capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body) 
                                            cudaStreamCaptureModeThreadLocal));
   std::swap(stream, cap);
   wwin[stream] = true;  // conservative: the body's first kernels do not prefetch weights
+  in_cond_body = true;
   try {
     body();
   } catch (...) {
+    in_cond_body = false;
     std::swap(stream, cap);
     cudaStreamEndCapture(cap, &bg);
     throw;
   }
+  in_cond_body = false;
   std::swap(stream, cap);
   CUDA_CHECK(cudaStreamEndCapture(cap, &bg));
   size_t nb = 0;
@@ -864,9 +903,12 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
     CUDA_CHECK(cudaStreamWaitEvent(side2, ev_fork, 0));
     std::swap(stream, side2);
     fork_window(stream);  // full dependency on the fork point: nothing in flight
+    // the two branches run side by side on disjoint SM sets (capped persistent grids)
+    cta_cap = fwd_split();
     critic_forward(B);
     std::swap(stream, side2);
     CUDA_CHECK(cudaEventRecord(ev_join, side2));
+    cta_cap = fwd_split() ? num_sms_host() - fwd_split() : 0;
   }
   // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
   if (use_tc()) {
@@ -886,6 +928,7 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   if (!td_target_fused(B))  // else fused (critic_update)
     timed(PC_ELEM, 0.0, 0.0, 0,
           [&] { launch_td_target(n, B, S.r.p, S.d.p, S.tq_out.p, h_f4.p, S.y.p, stream); });
+  cta_cap = 0;
   if (fork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
   // twin critic update; target Polyak fused for members whose policy fires
   critic_update(B, fire.p, fork);

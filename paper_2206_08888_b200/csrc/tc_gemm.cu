@@ -1379,7 +1379,8 @@ void launch_tpl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
   g.stages = std::max(1, std::min(nk, smax));
   const int tiles = g.groups * ((g.M + kBM - 1) / kBM) * ((g.N + BN - 1) / BN);
   if (g.nout > 0 && (g.N > BN || g.nout > 16)) PBRL_THROW(PBRL_E_USAGE, "tc_gemm: bad fused output");
-  launch_k(k_tc_gemm<BN, A_MN, B_MN, NO, EB>, std::min(tiles, num_sms()), 64 + kEpiThreads,
+  const int ctas = std::min(tiles, g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms());
+  launch_k(k_tc_gemm<BN, A_MN, B_MN, NO, EB>, ctas, 64 + kEpiThreads,
            smem_bytes<BN, NO>(g.stages), s, a, b, c, x, g);
 }
 
@@ -1416,6 +1417,8 @@ void launch_bn(int bn, const CUtensorMap& a, const CUtensorMap& b, const CUtenso
   PBRL_THROW(PBRL_E_USAGE, "tc_gemm: unsupported tile width");
 }
 }  // namespace
+
+int num_sms_host() { return num_sms(); }
 
 // 3-D tensor map over [groups][rows][cols] elements of eb bytes (fp32 or bf16); swizzle: 128B
 // for K-major operand tiles (and 32 x 32 fp32 epilogue boxes), 128B_ATOM_32B for MN-major fp32
@@ -1459,7 +1462,7 @@ int pick_bn(const TcArgs& g, bool b_mn) {
   static const int pin = std::getenv("PBRL_TC_BN") ? std::atoi(std::getenv("PBRL_TC_BN")) : 0;
   if (pin == 64 || pin == 128 || pin == 256) return pin;
   const int m_tiles = (g.M + kBM - 1) / kBM;
-  const int sms = num_sms();
+  const int sms = g.max_ctas > 0 ? std::min(g.max_ctas, num_sms()) : num_sms();
   int best = 256;
   double best_cost = 1e30;
   for (int bn : {64, 128, 256}) {
@@ -1582,8 +1585,8 @@ void launch_fwd2_tpl(const Fwd2Args& a, cudaStream_t s) {
   CUtensorMap th1{};
   if (a.H1g) th1 = make_tmap(a.H1g, 2, a.H1, a.M, a.groups, a.h1_ld, a.h1_gs, 64, 32, SWZ_128);
   const int tiles = a.groups * ((a.M + kBM - 1) / kBM);
-  launch_k(k_mlp_fwd2<NO>, std::min(tiles, num_sms()), kF2Threads, smem, s, tx, tw1, tw2,
-           th1, a);
+  const int ctas = std::min(tiles, a.max_ctas > 0 ? std::min(a.max_ctas, num_sms()) : num_sms());
+  launch_k(k_mlp_fwd2<NO>, ctas, kF2Threads, smem, s, tx, tw1, tw2, th1, a);
 }
 }  // namespace
 

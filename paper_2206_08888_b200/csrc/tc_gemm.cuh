@@ -72,6 +72,7 @@ struct TcArgs {
   int c_tma = 0, aux_tma = 0;  // set by launch_tc_gemm
   unsigned long long* trace = nullptr;  // diagnostics timeline (PBRL_TC_TRACE), see tc_gemm.cu
   int b_prefetch = 0;  // B (weights) may be read before the PDL wait (predecessor wrote none)
+  int max_ctas = 0;    // > 0: cap the persistent grid (a concurrent launch takes the other SMs)
 };
 
 struct TcTraceMeta {
@@ -100,6 +101,7 @@ void launch_tc_gemm(const TcOperand& A, const TcOperand& B, bool a_mn, bool b_mn
 // multiple of 64 and <= 256, H2 a multiple of 32 and <= 256, nout <= 16.
 struct Fwd2Args {
   int M = 0, in = 0, H1 = 0, H2 = 0, groups = 0, n_members = 1;
+  int max_ctas = 0;  // > 0: cap the persistent grid (a concurrent branch takes the other SMs)
   const void* X = nullptr;  // bf16 [groups or members][M][x_ld]
   long long x_ld = 0, x_gs = 0;
   int x_by_member = 0;
@@ -136,5 +138,7 @@ struct Fwd2Args {
 };
 bool mlp_fwd2_ok(const Fwd2Args& a);
 void launch_mlp_fwd2(const Fwd2Args& a, cudaStream_t s);
+
+int num_sms_host();  // multiprocessors of the current device
 
 }  // namespace pbrl
