@@ -335,10 +335,13 @@ struct Pop {
   bool in_cond_body = false;  // capturing a conditional body (its own capture graph)
   int cta_cap = 0;  // > 0: persistent tcgen05 launches use at most this many CTAs
   // SMs of the online-critic forward branch while the target chain runs beside it (0: no split;
-  // PBRL_FWD_SPLIT overrides)
-  int fwd_split() const {
+  // PBRL_FWD_SPLIT overrides).  Only for the fused two-hidden-layer forward with a few waves of
+  // tiles (config D: 320): with thousands of tiles (config E) every launch fills the machine and
+  // the split only halves each branch's throughput (measured: config E pop 64, 28.9k -> 25.5k).
+  int fwd_split(int B) const {
     static const int v = std::getenv("PBRL_FWD_SPLIT") ? std::atoi(std::getenv("PBRL_FWD_SPLIT")) : 64;
-    return v;
+    const long long tiles = 2LL * (shared ? 1 : n) * ((crows(B) + 127) / 128);
+    return cri.depth == 3 && tiles <= 3LL * 148 ? v : 0;
   }
   bool dw_fork_ok() const {
     static const bool off = std::getenv("PBRL_NO_DWFORK") != nullptr;

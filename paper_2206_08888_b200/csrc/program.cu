@@ -904,11 +904,11 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
     std::swap(stream, side2);
     fork_window(stream);  // full dependency on the fork point: nothing in flight
     // the two branches run side by side on disjoint SM sets (capped persistent grids)
-    cta_cap = fwd_split();
+    cta_cap = fwd_split(B);
     critic_forward(B);
     std::swap(stream, side2);
     CUDA_CHECK(cudaEventRecord(ev_join, side2));
-    cta_cap = fwd_split() ? num_sms_host() - fwd_split() : 0;
+    cta_cap = fwd_split(B) ? num_sms_host() - fwd_split(B) : 0;
   }
   // td3_critic_target (algos.hpp:241-282): pi'(s2) + clipped noise, twin target critics, y
   if (use_tc()) {
