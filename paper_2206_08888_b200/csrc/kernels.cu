@@ -562,10 +562,22 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
       }
     }
   } else {
+    // the block's copy of the cotangent: 8 independent loads in flight per thread before any
+    // shared store (one global latency instead of one per element)
     const float* G = a.G + grp * a.g_gs;
-    for (int e = threadIdx.x; e < B * nout; e += blockDim.x) {
-      const int b = e / nout, o = e - b * nout;
-      Gs[e] = G[static_cast<long long>(b) * a.g_ld + o];
+    constexpr int PF = 8;
+    const int tot = B * nout;
+    for (int e0 = threadIdx.x; e0 < tot; e0 += PF * blockDim.x) {
+      float t[PF];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int e = e0 + u * blockDim.x;
+        const int b = e / nout, o = e - b * nout;
+        t[u] = e < tot ? G[static_cast<long long>(b) * a.g_ld + o] : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < PF; ++u)
+        if (e0 + u * blockDim.x < tot) Gs[e0 + u * blockDim.x] = t[u];
     }
   }
   float w[CW][NA], acc[CW][NA], csum[CW];
