@@ -130,11 +130,56 @@ def act_case(ref: Ref):
     np.savez_compressed(OUT / "act.npz", **out)
 
 
+def f4_case(ref: Ref):
+    """shared-critic TD3 with member masks and the DvD hook, shared-critic SAC, dvd_loss,
+    median_pairwise_distance and CEM sample / update"""
+    n, ds, da, hidden, B, K = 4, 5, 2, [8, 8], 6, 4
+    out = dict(n=n, ds=ds, da=da, hidden=np.asarray(hidden), B=B, K=K)
+    raw = ref.synthetic_batches(K, n, B, ds, da, 34)
+    probe = np.random.default_rng(5).uniform(-1, 1, (n + 2, ds))
+    out["probe"] = probe
+    st = ref.td3(n, ds, da, hidden, 1.0, 33, shared=True)
+    hy = td3_defaults(n)
+    for k in range(K):
+        dvd = {"probe": probe, "length_scale": 0.7, "jitter": 1e-6, "lam_start": 0.1,
+               "lam_end": 0.7, "horizon": 4, "step": k}
+        mask = [1, 1, 0, 0] if k == 1 else None
+        if k == 3:
+            st.step(tuple(x[k] for x in raw), hy, policy_mask=mask)
+        else:
+            st.step(tuple(x[k] for x in raw), hy, policy_mask=mask, dvd=dvd)
+    for k in TD3_NETS:
+        out[f"td3_{k}"] = st.get_net(k)
+    ss = ref.sac(n, ds, da, hidden, 1.0, 41, shared=True)
+    for k in range(K):
+        ss.step(tuple(x[k] for x in raw), sac_defaults(n, da))
+    for k in SAC_NETS:
+        out[f"sac_{k}"] = ss.get_net(k)
+    rng = np.random.default_rng(9)
+    e = rng.normal(size=(7, 12))
+    out["dvd_emb"] = e
+    loss, logdet, grad = ref.dvd_loss(e, 0.9, 1e-8, 1.3)
+    out["dvd_loss"], out["dvd_logdet"], out["dvd_grad"] = loss, logdet, grad
+    out["median"] = ref.median_pairwise_distance(e)
+    mean, var = rng.normal(size=37), rng.uniform(0, 0.1, 37)
+    key = ref.stream_key(7, 2, 10, 0)
+    cand, nxt = ref.cem_sample(mean, var, 1e-2, 6, key, 4)
+    scores = rng.normal(size=6)
+    m2, v2, nz = ref.cem_update(mean, var, 1e-2, cand, scores)
+    out.update(cem_mean=mean, cem_var=var, cem_key=np.uint64(key), cem_cand=cand,
+               cem_next=np.uint64(nxt), cem_scores=scores, cem_mean2=m2, cem_var2=v2,
+               cem_noise2=nz)
+    np.savez_compressed(OUT / "f4.npz", **out)
+
+
 def main():
     ref = Ref()
     OUT.mkdir(parents=True, exist_ok=True)
     if sys.argv[1:] == ["act"]:
         act_case(ref)
+        return
+    if sys.argv[1:] == ["f4"]:
+        f4_case(ref)
         return
     td3_case(ref, "td3_small", 3, 4, 2, [8, 8], 8, 20, 11, 12,
              hyper=dict(policy_delay_ratio=[0.5, 1.0, 0.3], critic_lr=[3e-4, 1e-3, 3e-4]))
@@ -145,6 +190,7 @@ def main():
     pbt_case(ref)
     tanh_case(ref)
     act_case(ref)
+    f4_case(ref)
     print("golden fixtures written to", OUT)
 
 

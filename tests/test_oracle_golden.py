@@ -111,3 +111,38 @@ def test_act_golden(ora):
         for det in (0, 1):
             got = st.act(g["obs"], int(g["seed"]), g["steps"], g["noise"], bool(det))
             assert bits_equal(got, g[f"{algo}_det{det}"]), (algo, det)
+
+
+def test_f4_golden(ora):
+    """shared-critic TD3 (+ member mask, DvD hook) / SAC, dvd_loss, median, CEM: the oracle
+    against the reference's outputs (oracle/make_golden.py f4)"""
+    g = _load("f4")
+    n, ds, da, B, K = (int(g[k]) for k in ("n", "ds", "da", "B", "K"))
+    hidden = [int(h) for h in g["hidden"]]
+    raw = ora.synthetic_batches(K, n, B, ds, da, 34)
+    from oracle.oracle import sac_defaults, td3_defaults
+    st = ora.td3(n, ds, da, hidden, 1.0, 33, shared=True)
+    for k in range(K):
+        dvd = {"probe": g["probe"], "length_scale": 0.7, "jitter": 1e-6, "lam_start": 0.1,
+               "lam_end": 0.7, "horizon": 4, "step": k}
+        mask = [1, 1, 0, 0] if k == 1 else None
+        if k == 3:
+            st.step(raw_at(raw, k), td3_defaults(n), policy_mask=mask)
+        else:
+            st.step(raw_at(raw, k), td3_defaults(n), policy_mask=mask, dvd=dvd)
+    for k in TD3_NETS:
+        assert bits_equal(st.get_net(k), g[f"td3_{k}"]), k
+    ss = ora.sac(n, ds, da, hidden, 1.0, 41, shared=True)
+    for k in range(K):
+        ss.step(raw_at(raw, k), sac_defaults(n, da))
+    for k in SAC_NETS:
+        assert bits_equal(ss.get_net(k), g[f"sac_{k}"]), k
+    loss, logdet, grad = ora.dvd_loss(g["dvd_emb"], 0.9, 1e-8, 1.3)
+    assert loss == g["dvd_loss"] and logdet == g["dvd_logdet"]
+    assert np.array_equal(grad, g["dvd_grad"])
+    assert ora.median_pairwise_distance(g["dvd_emb"]) == g["median"]
+    cand, nxt = ora.cem_sample(g["cem_mean"], g["cem_var"], 1e-2, 6, int(g["cem_key"]), 4)
+    assert nxt == int(g["cem_next"]) and np.array_equal(cand, g["cem_cand"])
+    m2, v2, nz = ora.cem_update(g["cem_mean"], g["cem_var"], 1e-2, g["cem_cand"], g["cem_scores"])
+    assert np.array_equal(m2, g["cem_mean2"]) and np.array_equal(v2, g["cem_var2"])
+    assert nz == g["cem_noise2"]
