@@ -305,9 +305,9 @@ int pbrl_attach_comm(pbrl_pop* pop, pbrl_comm* comm);
  * fails the update with PBRL_E_DEGENERATE before the step runs. */
 int pbrl_set_dvd(pbrl_pop* pop, const double* probe, uint64_t m_states, double length_scale,
                  double jitter, double lambda);
-/* dvd_embed (:334-339): out [n][m_states * act] deterministic actions on the probe states */
+/* dvd_embed (:337-340): out [n][m_states * act] deterministic actions on the probe states */
 int pbrl_dvd_embed(pbrl_pop* pop, const double* probe, uint64_t m_states, float* out);
-/* dvd_loss (:425-478) on host data: emb [n][dim]; grad [n][dim] (may be NULL) */
+/* dvd_loss (:411-465) on host data: emb [n][dim]; grad [n][dim] (may be NULL) */
 int pbrl_dvd_loss(const double* emb, uint64_t n, uint64_t dim, double length_scale, double jitter,
                   double lambda, double* loss, double* logdet, double* grad);
 int pbrl_median_pairwise_distance(const double* emb, uint64_t n, uint64_t dim, double* out);

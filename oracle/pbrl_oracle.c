@@ -608,7 +608,7 @@ double ora_dvd_lambda(uint64_t step, double start, double end, uint64_t horizon)
   return start + (end - start) * frac;
 }
 
-/* canonical_order (evolve.hpp:404-418): stable lexicographic sort of the embedding rows */
+/* canonical_order (evolve.hpp:391-405): stable lexicographic sort of the embedding rows */
 static const double* g_canon_e;
 static uint64_t g_canon_dim;
 static int canon_cmp(const void* pa, const void* pb) {
@@ -657,7 +657,7 @@ static void chol_inverse(const double* l, uint64_t n, double* inv) {
   free(col);
 }
 
-/* dvd_loss, evolve.hpp:425-478 */
+/* dvd_loss, evolve.hpp:411-465 */
 int ora_dvd_loss(const double* emb, uint64_t n, uint64_t dim, double length_scale, double jitter,
                  double lambda, double* loss, double* logdet_out, double* grad) {
   if (n < 2) return -2;
@@ -725,7 +725,7 @@ static int dbl_cmp(const void* a, const void* b) {
   return x < y ? -1 : (x > y ? 1 : 0);
 }
 
-/* median_pairwise_distance, evolve.hpp:481-499 */
+/* median_pairwise_distance, evolve.hpp:469-486 */
 double ora_median_pairwise_distance(const double* emb, uint64_t n, uint64_t dim) {
   if (n < 2) return 1.0;
   const uint64_t cnt = n * (n - 1) / 2;
@@ -747,7 +747,7 @@ double ora_median_pairwise_distance(const double* emb, uint64_t n, uint64_t dim)
   return med > 0 ? med : 1.0;
 }
 
-/* dvd_embed_cached (evolve.hpp:314-332): the probe states (double, cast to T as in
+/* dvd_embed_cached (evolve.hpp:319-335): the probe states (double, cast to T as in
  * dvd_policy_hook) replicated per member, then the policy forward; out [n][m_states*da] */
 static float* dvd_probe_block(const ora_td3* st, const double* probe, uint64_t ms) {
   float* x = (float*)malloc(sizeof(float) * st->n * ms * st->ds);

@@ -1330,7 +1330,7 @@ int pbrl_dvd_embed(pbrl_pop* pop, const double* probe, uint64_t m_states, float*
     Pop* p = P(pop);
     if (p->algo != PBRL_ALGO_TD3) PBRL_THROW(PBRL_E_USAGE, "dvd_embed: TD3 policies only");
     if (!probe || !out || m_states < 1) PBRL_THROW(PBRL_E_SHAPE, "dvd_embed: probe matrix size != M * observation_dim");
-    // dvd_embed_cached (:314-332): probes (double -> T) replicated per member, then the policy
+    // dvd_embed_cached (:319-335): probes (double -> T) replicated per member, then the policy
     // forward == deterministic act
     const size_t per = static_cast<size_t>(m_states) * p->ds;
     std::vector<float> obs(per * p->n);

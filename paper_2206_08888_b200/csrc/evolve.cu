@@ -25,12 +25,12 @@
 namespace pbrl {
 
 // ------------------------------------------------------------------ DvD host math
-// dvd_loss (evolve.hpp:425-478), bit-for-bit the reference's double arithmetic
+// dvd_loss (evolve.hpp:411-465), bit-for-bit the reference's double arithmetic
 int dvd_loss_host(const double* emb, uint64_t n, uint64_t dim, double length_scale, double jitter,
                   double lambda, double* loss, double* logdet_out, double* grad) {
   if (n < 2) PBRL_THROW(PBRL_E_CONFIG, "dvd_loss: need at least two embedding rows");
   if (!(length_scale > 0)) PBRL_THROW(PBRL_E_CONFIG, "dvd_loss: length scale must be positive");
-  // canonical_order (:404-418): stable lexicographic sort of the rows
+  // canonical_order (:391-405): stable lexicographic sort of the rows
   std::vector<uint64_t> order(n);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
@@ -59,7 +59,7 @@ int dvd_loss_host(const double* emb, uint64_t n, uint64_t dim, double length_sca
   }
   std::vector<double> m = kernel;
   for (uint64_t i = 0; i < n; ++i) m[i * n + i] += jitter;
-  // cholesky (:364-381)
+  // cholesky (:352-367)
   for (uint64_t i = 0; i < n; ++i) {
     for (uint64_t j = 0; j <= i; ++j) {
       double sum = m[i * n + j];
@@ -78,7 +78,7 @@ int dvd_loss_host(const double* emb, uint64_t n, uint64_t dim, double length_sca
   }
   double logdet = 0;
   for (uint64_t i = 0; i < n; ++i) logdet += 2.0 * std::log(m[i * n + i]);
-  // cholesky_inverse (:384-400)
+  // cholesky_inverse (:370-388)
   std::vector<double> minv(n * n), col(n);
   for (uint64_t c = 0; c < n; ++c) {
     for (uint64_t i = 0; i < n; ++i) {
@@ -112,7 +112,7 @@ int dvd_loss_host(const double* emb, uint64_t n, uint64_t dim, double length_sca
   return 0;
 }
 
-// median_pairwise_distance (evolve.hpp:481-499)
+// median_pairwise_distance (evolve.hpp:469-486)
 double median_pairwise_distance_host(const double* emb, uint64_t n, uint64_t dim) {
   std::vector<double> d;
   for (uint64_t i = 0; i < n; ++i)
@@ -218,7 +218,7 @@ void Pop::set_dvd(const double* probe, uint64_t m_states, double length_scale, d
     dvd.obs.alloc(rows * ds);
   }
   dvd.grad.alloc(static_cast<size_t>(n) * pol.stride);
-  // the probe block, replicated per member and cast to float (dvd_embed_cached, :314-332)
+  // the probe block, replicated per member and cast to float (dvd_embed_cached, :319-335)
   std::vector<float> xs(static_cast<size_t>(rows) * ds);
   for (int m = 0; m < n; ++m)
     for (size_t i = 0; i < static_cast<size_t>(ms) * ds; ++i)

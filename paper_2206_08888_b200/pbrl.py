@@ -603,7 +603,7 @@ class LambdaSchedule:
 
 
 def dvd_lambda(step: int, s: LambdaSchedule) -> float:
-    """dvd_lambda (evolve.hpp:311-315)."""
+    """dvd_lambda (evolve.hpp:310-314)."""
     out = C.c_double()
     _lib.call("pbrl_dvd_lambda", int(step), float(s.start), float(s.end), int(s.horizon),
               C.byref(out))
@@ -612,7 +612,7 @@ def dvd_lambda(step: int, s: LambdaSchedule) -> float:
 
 @dataclass
 class DvDConfig:
-    """DvDConfig (evolve.hpp:480-497): probe states (row-major M x ds), kernel and schedule."""
+    """DvDConfig (evolve.hpp:489-503): probe states (row-major M x ds), kernel and schedule."""
     probe_states: Sequence[float] = field(default_factory=list)
     m_states: int = 0
     length_scale: float = 1.0
@@ -649,7 +649,7 @@ def dvd_policy_hook(cfg: DvDConfig, step: int) -> DvdHook:
 
 
 def dvd_embed(policies: "Td3State", probe_states, m_states: int) -> np.ndarray:
-    """dvd_embed (evolve.hpp:334-339): [n, m_states * da] deterministic actions on the probes."""
+    """dvd_embed (evolve.hpp:337-340): [n, m_states * da] deterministic actions on the probes."""
     probe = np.ascontiguousarray(np.asarray(probe_states, np.float64).ravel())
     if probe.size != m_states * policies.obs_dim:
         raise ShapeError("dvd_embed: probe matrix size != M * observation_dim")
@@ -667,7 +667,7 @@ class DvdLossOut:
 
 
 def dvd_loss(embeddings, length_scale: float, jitter: float, lam: float) -> DvdLossOut:
-    """dvd_loss (evolve.hpp:425-478) on host embeddings (double)."""
+    """dvd_loss (evolve.hpp:411-465) on host embeddings (double)."""
     e = np.ascontiguousarray(embeddings, np.float64)
     if e.ndim != 2 or e.shape[0] < 2:
         raise ConfigError("dvd_loss: need at least two embedding rows")
@@ -679,7 +679,7 @@ def dvd_loss(embeddings, length_scale: float, jitter: float, lam: float) -> DvdL
 
 
 def median_pairwise_distance(embeddings) -> float:
-    """median_pairwise_distance (evolve.hpp:481-499)."""
+    """median_pairwise_distance (evolve.hpp:469-486)."""
     e = np.ascontiguousarray(embeddings, np.float64)
     out = C.c_double()
     _lib.call("pbrl_median_pairwise_distance", _ptr(e, _lib.f64p), e.shape[0],
@@ -750,7 +750,7 @@ class CEMState:
 
 
 def cem_init(policies: "Td3State", mean=None, init_var: float = 0.0) -> CEMState:
-    """cem_init (evolve.hpp:235-241); mean None = flatten_member(policy, 0) (pipeline_run.hpp:159)."""
+    """cem_init (evolve.hpp:231-237); mean None = flatten_member(policy, 0) (pipeline_run.hpp:159)."""
     return CEMState(policies, mean, init_var)
 
 
