@@ -75,6 +75,46 @@ int main() {
   Env::Step s{};
   for (int i = 0; i < 5; ++i) s = e.step({0.5, -0.5});
   EXPECT(s.done && s.reward <= 0);
+
+  // RunConfig::validate for the shared-critic strategies (pipeline.hpp:229-238,
+  // pipeline_run.hpp:81-83): CEM / DvD need shared-critic mode, one shared buffer, TD3, and CEM
+  // an even population; PBT needs per-agent buffers
+  auto rejects = [](const RunConfig& rc) {
+    try {
+      rc.validate();
+    } catch (const ConfigError&) {
+      return true;
+    }
+    return false;
+  };
+  RunConfig rc;
+  rc.population = 4;
+  rc.strategy = Strategy::kCem;
+  EXPECT(rejects(rc));  // independent mode
+  rc.mode = PopMode::kSharedCritic;
+  EXPECT(rejects(rc));  // per-agent buffers
+  rc.buffer_mode = BufferMode::kShared;
+  EXPECT(!rejects(rc));
+  rc.population = 5;
+  EXPECT(rejects(rc));  // odd CEM population
+  rc.strategy = Strategy::kDvd;
+  EXPECT(!rejects(rc));
+  rc.algo = Algo::kSac;
+  EXPECT(rejects(rc));  // TD3-only strategies
+  rc = RunConfig{};
+  rc.strategy = Strategy::kPbt;
+  rc.buffer_mode = BufferMode::kShared;
+  EXPECT(rejects(rc));
+  // DvD schedule and configuration checks (evolve.hpp:304-314, :489-503)
+  DvDConfig dv;
+  dv.m_states = 2;
+  bool dthrew = false;
+  try {
+    dv.validate(3);
+  } catch (const ConfigError&) {
+    dthrew = true;
+  }
+  EXPECT(dthrew);
   std::printf("pipeline host: OK\n");
   return 0;
 }
