@@ -451,16 +451,17 @@ def main():
 
     # ---- e2e through the C ABI: pinned host batches, every step's H2D copy and the D2H of every
     # step's losses inside the timed region.  update_k_steps semantics (algos.hpp:953-983): each
-    # call runs KC host batches (the copy of batch i+1 overlaps step i) and returns the KC steps'
-    # critic1 / critic2 / policy losses.
+    # call runs KC = 50 host batches -- the reference bench's K --
+    # with the copy of batch i+1 overlapping step i, and returns the KC steps' critic1 / critic2 /
+    # policy losses.
     e2e = None
     if not args.no_e2e:
         hb = [[x.cpu().pin_memory() for x in (b.s, b.a, b.r, b.s2, b.done)] for b in batches[:10]]
         hstructs = [_lib.Batch(*[x.data_ptr() for x in h]) for h in hb]
-        KC = 10
+        KC = 50
         loss = torch.empty(KC * 3 * n, dtype=torch.float64).pin_memory()
         lptr = C.cast(loss.data_ptr(), _lib.f64p)
-        calls = max(1, min(K, 50) // KC)
+        calls = max(1, min(K, 100) // KC)
 
         def run_host(c):
             arr = (_lib.Batch * KC)(*[hstructs[(c * KC + j) % len(hstructs)] for j in range(KC)])
