@@ -62,6 +62,7 @@ Pop::Pop(const pbrl_pop_desc& d) {
     PBRL_THROW(PBRL_E_CONFIG, "unknown population mode");
   shared = d.mode == PBRL_MODE_SHARED_CRITIC;
   ncrit = shared ? 1 : n;
+  n_local = n;
   bound = static_cast<float>(d.action_bound);
   seed = d.seed;
   for (uint32_t i = 0; i < d.n_hidden; ++i) {
@@ -170,6 +171,10 @@ CriticFold::CriticFold(Pop& pop, int b) : p(pop), n0(pop.n), B(pop.crows(b)) {
   if (p.shared) p.n = 1;
 }
 CriticFold::~CriticFold() { p.n = n0; }
+CriticUnfold::CriticUnfold(Pop& pop) : p(pop), n1(pop.n) {
+  if (p.shared) p.n = p.n_local;
+}
+CriticUnfold::~CriticUnfold() { p.n = n1; }
 
 Pop::~Pop() {
   invalidate_graphs();
@@ -179,6 +184,9 @@ Pop::~Pop() {
     cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
+    if (side6) cudaStreamDestroy(side6);
+    if (ev_f6) cudaEventDestroy(ev_f6);
+    if (ev_j6) cudaEventDestroy(ev_j6);
     for (int i = 0; i < 2; ++i) {
       if (side3[i]) cudaStreamDestroy(side3[i]);
       if (ev_f3[i]) cudaEventDestroy(ev_f3[i]);

@@ -144,6 +144,14 @@ struct CriticFold {
   CriticFold(Pop& pop, int b);
   ~CriticFold();
 };
+// the population's own member count back inside a CriticFold scope (policy work between critic
+// launches)
+struct CriticUnfold {
+  Pop& p;
+  int n1;
+  explicit CriticUnfold(Pop& pop);
+  ~CriticUnfold();
+};
 
 struct Pop {
   int algo = PBRL_ALGO_TD3, precision = PBRL_PREC_FFMA32, device = 0;
@@ -154,6 +162,7 @@ struct Pop {
   // members (n, or 1); critic2 rows start at ncrit in the critic arenas.
   bool shared = false;
   int ncrit = 0;
+  int n_local = 0;  // the population's member count (n reads 1 inside a CriticFold)
   int net_members(int net) const {
     return (net == PBRL_NET_POLICY || net == PBRL_NET_POLICY_TARGET) ? n : ncrit;
   }
@@ -334,6 +343,16 @@ struct Pop {
   cudaEvent_t ev_f3[2] = {nullptr, nullptr}, ev_j3[2] = {nullptr, nullptr};
   bool in_cond_body = false;  // capturing a conditional body (its own capture graph)
   int cta_cap = 0;  // > 0: persistent tcgen05 launches use at most this many CTAs
+  // TD3 graph mode: the policy forward on a branch beside the critic Adam (PBRL_POL_FORK = its
+  // SMs, 0 disables)
+  std::function<void()> pre_adam;
+  bool pol_fwd_done = false;
+  cudaStream_t side6 = nullptr;
+  cudaEvent_t ev_f6 = nullptr, ev_j6 = nullptr;
+  int pol_fork_ctas() const {
+    static const int v = std::getenv("PBRL_POL_FORK") ? std::atoi(std::getenv("PBRL_POL_FORK")) : 40;
+    return v;
+  }
   // SMs of the online-critic forward branch while the target chain runs beside it (0: no split;
   // PBRL_FWD_SPLIT overrides).  Only for the fused two-hidden-layer forward with a few waves of
   // tiles (config D: 320): with thousands of tiles (config E) every launch fills the machine and

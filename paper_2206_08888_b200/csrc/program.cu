@@ -812,6 +812,10 @@ void Pop::critic_update(int B0, const int* polyak_gate, bool forward_done) {
       count_launch(2);
     }
   }
+  if (pre_adam) {  // TD3 graph mode: the policy forward forks off beside the critic Adam
+    CriticUnfold u(*this);
+    pre_adam();
+  }
   // 28 B/param Adam (+2 B/param bf16 operand copy in BF16 mode)
   const double cP = static_cast<double>(cri.P);
   timed(PC_ADAM, 0.0, cP * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
@@ -931,7 +935,34 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   cta_cap = 0;
   if (fork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
   // twin critic update; target Polyak fused for members whose policy fires
+  // graph mode, fused forward: the policy forward of the policy half depends only on the
+  // policies (unchanged until the policy Adam), so it runs on a branch beside the critic Adam on
+  // a few SMs (gated per member by the fire mask: near-empty when no policy fires); the branch
+  // rejoins before the policy half
+  bool pol_fwd_forked = false;
+  if (fork && pol_fork_ctas() > 0) {
+    pre_adam = [&] {
+      if (!side6) CUDA_CHECK(cudaStreamCreateWithFlags(&side6, cudaStreamNonBlocking));
+      if (!ev_f6) {
+        for (cudaEvent_t* e : {&ev_f6, &ev_j6})
+          CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      }
+      CUDA_CHECK(cudaEventRecord(ev_f6, stream));
+      CUDA_CHECK(cudaStreamWaitEvent(side6, ev_f6, 0));
+      std::swap(stream, side6);
+      fork_window(stream);
+      cta_cap = pol_fork_ctas();
+      td3_policy_forward(B);
+      cta_cap = 0;
+      std::swap(stream, side6);
+      CUDA_CHECK(cudaEventRecord(ev_j6, side6));
+      pol_fwd_forked = true;
+    };
+  }
   critic_update(B, fire.p, fork);
+  pre_adam = nullptr;
+  if (pol_fwd_forked) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_j6, 0));
+  pol_fwd_done = pol_fwd_forked;
   if (capturing) capture_if(any_fire, side, [&] { td3_policy_half(B); });
   else td3_policy_half(B);
 }
@@ -948,7 +979,8 @@ void Pop::td3_policy_forward(int B) {
 void Pop::td3_policy_half(int B) {
   const long long nbB = B;
   const Mat s = policy_input(B);
-  td3_policy_forward(B);
+  if (!pol_fwd_done) td3_policy_forward(B);
+  pol_fwd_done = false;
   // critic1 on [s | pi(s)]; a shared critic runs every member's rows (folded, ungated)
   {
     CriticFold f(*this, B);
