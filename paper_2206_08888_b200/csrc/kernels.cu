@@ -1189,6 +1189,18 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
            tau_a, tau_b, polyak_gate, p16, t16);
 }
 
+__global__ void k_copy_f64(double* dst, const double* src, size_t count) {
+  PDL_ENTRY();
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+void launch_copy_f64(double* dst, const double* src, size_t count, cudaStream_t s) {
+  launch_k(k_copy_f64, static_cast<int>(std::min<size_t>((count + 255) / 256, 64)), 256, 0, s, dst,
+           src, count);
+}
+
 __global__ void k_to_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                           size_t count) {
   PDL_ENTRY();

@@ -462,8 +462,10 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
       // goes to the host in one copy per kLossHist steps (async, in stream order)
       const size_t row = static_cast<size_t>(3) * n;
       loss_hist.alloc(kLossHist * row);
-      CUDA_CHECK(cudaMemcpyAsync(loss_hist.p + (i % kLossHist) * row, losses.p,
-                                 row * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+      // a kernel rather than a copy node, so the programmatic-dependent-launch chain from this
+      // step's graph into the next step's pack is not broken
+      launch_copy_f64(loss_hist.p + (i % kLossHist) * row, losses.p, row, stream);
+      count_launch(1);
       if (i % kLossHist == kLossHist - 1 || i + 1 == k) {
         const uint32_t first = i - i % kLossHist;
         CUDA_CHECK(cudaMemcpyAsync(losses_out + first * row, loss_hist.p,

@@ -231,6 +231,7 @@ void launch_adam(int groups, int n, size_t P, size_t stride, float* p, float* m,
 // bf16 copy of an fp32 arena (the BF16 mode's tensor-core weight operands)
 void launch_to_bf16(const float* src, __nv_bfloat16* dst, size_t count, cudaStream_t s);
 void launch_fill(float* p, size_t count, float v, cudaStream_t s);
+void launch_copy_f64(double* dst, const double* src, size_t count, cudaStream_t s);
 // column `col` of a [rows][ld] activation block := v (fp32, or bf16 when act16)
 void launch_fill_col(void* p, long long rows, int ld, int col, float v, int act16, cudaStream_t s);
 // bias gradient of a layer: dst[g][o] = sum_b G[g][b][o] in row order (groups gated by active)
