@@ -66,6 +66,10 @@ def parse():
                          "median / IQR (bench.hpp:184-200)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--replay", action="store_true",
+                    help="replay-inclusive variant (SURVEY.md §8(d)): per-agent HBM rings "
+                         "pre-filled with 100,000 synthetic transitions per member, every step "
+                         "samples its batch on the device (draw_id = step, min_size 1000)")
     ap.add_argument("--profile-json", default=None, help="write the per-class profile here")
     return ap.parse_args()
 
@@ -216,7 +220,9 @@ def config_dict(args, cfg, pop, l2, gpus):
             "algo": cfg["algo"], "population": pop, "population_per_gpu": per,
             "hidden": cfg["hidden"], "batch": cfg["batch"], "obs_dim": OBS, "act_dim": ACT,
             "parallelism": f"population shards x{gpus} ({args.scaling} scaling, no per-step "
-                           f"collective)", "precision": args.precision, "l2": l2}
+                           f"collective)", "precision": args.precision, "l2": l2,
+            "inputs": "device replay rings (sampled per step)" if getattr(args, "replay", False)
+                      else "50 synthetic batches resident in HBM"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -318,6 +324,31 @@ def main():
         return run
 
     run = make_runner(st, batches)
+    replay_note = None
+    if args.replay:
+        # replay-inclusive: the device rings of run_training's learner (sample_batch +
+        # update_k_steps fused, pbrl_update_k), filled with U[-1, 1) transitions, done ~ 0.02
+        import numpy as np
+        cap, chunk = 100_000, 5_000
+        rb = pb.DeviceReplay(st, cap, "per_agent")
+        rng = np.random.default_rng(SEED + rank)
+        for c0 in range(0, cap, chunk):
+            rows = n * chunk
+            s_ = rng.uniform(-1, 1, (rows, OBS)).astype(np.float32)
+            a_ = rng.uniform(-1, 1, (rows, ACT)).astype(np.float32)
+            r_ = rng.uniform(-1, 1, rows).astype(np.float32)
+            s2_ = rng.uniform(-1, 1, (rows, OBS)).astype(np.float32)
+            d_ = (rng.uniform(0, 1, rows) < 0.02).astype(np.float32)
+            rb.insert(s_, a_, r_, s2_, d_, np.repeat(np.arange(n, dtype=np.uint32), chunk))
+        ready = C.c_int()
+
+        def run(i):
+            _lib.call("pbrl_update_k", st.handle, 1, SEED, i, B, 1000, C.byref(ready))
+            if not ready.value:
+                raise RuntimeError("replay rings not ready")
+        replay_note = (f"per-agent HBM rings, {cap} transitions per member, min_size 1000, "
+                       "draw_id = step (pbrl_update_k: device sample_batch + update)")
+        args.no_e2e = True
     lstream = st.lib_stream()
 
     state_bytes = st.device_bytes()
@@ -556,7 +587,9 @@ def main():
                 "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K,
                 "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
                 "dtype": {"ffma32": "f32", "bf16": "bf16", "tf32": "tf32"}[args.precision],
-                "data": "synthetic (make_synthetic_batches semantics, seed 7, 50 batches in HBM)",
+                "data": ("synthetic (make_synthetic_batches semantics, seed 7, 50 batches in HBM)"
+                         if not replay_note else "synthetic transitions in device replay rings: "
+                         + replay_note),
                 "config": config_dict(args, cfg, pop,
                                       "flushed between steps" if flush else
                                       f"inputs+state {(state_bytes + in_bytes) / 2**20:.0f} MiB "

@@ -1669,39 +1669,65 @@ void launch_replay_scatter(const float* rows, const uint64_t* dst_row, uint64_t 
 }
 
 // sample_batch (replay.hpp:181-204): slot = bits(key, b) % size with key =
-// RngStream::of(seed, streams[m], kSample, draw_id); one warp gathers one row (coalesced 4 B
-// lanes over the row) straight into the critic-input layouts.
+// RngStream::of(seed, streams[m], kSample, draw_id), rows gathered into the critic-input layouts.
+// Warp w gathers rows [8w, 8w + 8): lanes 0-7 each derive one row's slot (stream key, counter
+// hash, modulo), the slots are broadcast, and the 8 rows' words are loaded together (up to 11
+// independent loads per lane in flight, one memory round trip for 8 random rows) before they are
+// routed into the critic-input layouts.
+constexpr int kGatherRows = 8;
+
 template <typename AT>
-__global__ void k_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const float* ring,
-                                uint64_t cap, int shared, const uint64_t* sizes,
-                                const uint64_t* streams, uint64_t seed, uint64_t draw_id,
-                                AT* in_sa, AT* in_s2a, AT* sa_pi, float* r_out, float* d_out,
-                                AT* in_s, int lsp) {
+__global__ void __launch_bounds__(256) k_replay_gather(
+    int n, int B, int ds, int da, int lsa, int rw, const float* ring, uint64_t cap, int shared,
+    const uint64_t* sizes, const uint64_t* streams, uint64_t seed, uint64_t draw_id, AT* in_sa,
+    AT* in_s2a, AT* sa_pi, float* r_out, float* d_out, AT* in_s, int lsp) {
   PDL_ENTRY();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= n * B) return;
-  const int m = warp / B, b = warp % B;
-  const int buf = shared ? 0 : m;
-  const uint64_t key = stream_key(seed, streams[m], kSample, draw_id);
-  const uint64_t slot = rng_bits(key, static_cast<uint64_t>(b)) % sizes[buf];
-  const float* row = ring + (static_cast<uint64_t>(buf) * cap + slot) * rw;
+  const int rows = n * B;
+  const int g0 = warp * kGatherRows;
+  if (g0 >= rows) return;
+  const int width = 2 * ds + da + 2;  // s | a | s2 | r | done
+  uint64_t base = 0;
+  if (lane < kGatherRows && g0 + lane < rows) {
+    const int g = g0 + lane, m = g / B, b = g - m * B;
+    const int buf = shared ? 0 : m;
+    const uint64_t key = stream_key(seed, streams[m], kSample, draw_id);
+    const uint64_t slot = rng_bits(key, static_cast<uint64_t>(b)) % sizes[buf];
+    base = (static_cast<uint64_t>(buf) * cap + slot) * rw;
+  }
+  constexpr int kMaxPer = 16;  // words per lane: 8 rows x width <= 32 x 16 (width <= 64)
+  const int total = kGatherRows * width;
+  float v[kMaxPer];
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int e = lane + 32 * u;
+    const int r = e / width;
+    const uint64_t rb = __shfl_sync(0xffffffffu, base, r < kGatherRows ? r : 0);
+    v[u] = (e < total && g0 + r < rows) ? __ldcs(ring + rb + (e - r * width)) : 0.0f;
+  }
   const int dsa = ds + da;
-  const long long o = static_cast<long long>(warp) * lsa;
-  for (int c = lane; c < 2 * ds + da + 2; c += 32) {
-    const float v = row[c];
+#pragma unroll
+  for (int u = 0; u < kMaxPer; ++u) {
+    const int e = lane + 32 * u;
+    if (e >= total) break;
+    const int r = e / width, c = e - r * width;
+    const int g = g0 + r;
+    if (g >= rows) continue;
+    const long long o = static_cast<long long>(g) * lsa;
+    const float x = v[u];
     if (c < ds) {
-      act_st(in_sa, o + c, v);
-      if (sa_pi) act_st(sa_pi, o + c, v);
-      if (in_s) act_st(in_s, static_cast<long long>(warp) * lsp + c, v);
+      act_st(in_sa, o + c, x);
+      if (sa_pi) act_st(sa_pi, o + c, x);
+      if (in_s) act_st(in_s, static_cast<long long>(g) * lsp + c, x);
     } else if (c < dsa) {
-      act_st(in_sa, o + c, v);
+      act_st(in_sa, o + c, x);
     } else if (c < dsa + ds) {
-      act_st(in_s2a, o + (c - dsa), v);
+      act_st(in_s2a, o + (c - dsa), x);
     } else if (c == dsa + ds) {
-      r_out[warp] = v;
+      r_out[g] = x;
     } else {
-      d_out[warp] = v;
+      d_out[g] = x;
     }
   }
 }
@@ -1711,7 +1737,9 @@ void launch_replay_gather(int n, int B, int ds, int da, int lsa, int rw, const f
                           const uint64_t* streams, uint64_t seed, uint64_t draw_id,
                           void* in_sa, void* in_s2a, void* sa_pi, float* r_out, float* d_out,
                           int act16, cudaStream_t s, void* in_s, int lsp) {
-  const long long warps = static_cast<long long>(n) * B;
+  if (2 * ds + da + 2 > 64)
+    PBRL_THROW(PBRL_E_CONFIG, "replay gather: transitions wider than 64 words");
+  const long long warps = (static_cast<long long>(n) * B + kGatherRows - 1) / kGatherRows;
   const int blocks = static_cast<int>((warps * 32 + 255) / 256);
   if (act16)
     launch_k(k_replay_gather<__nv_bfloat16>, blocks, 256, 0, s, n, B, ds, da, lsa, rw, ring, cap,
