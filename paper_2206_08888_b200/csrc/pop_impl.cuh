@@ -354,13 +354,14 @@ struct Pop {
     return v;
   }
   // SMs of the online-critic forward branch while the target chain runs beside it (0: no split;
-  // PBRL_FWD_SPLIT overrides).  Only for the fused two-hidden-layer forward with a few waves of
-  // tiles (config D: 320): with thousands of tiles (config E) every launch fills the machine and
-  // the split only halves each branch's throughput (measured: config E pop 64, 28.9k -> 25.5k).
+  // PBRL_FWD_SPLIT overrides).  Only for the fused two-hidden-layer forward with a partial second
+  // wave of tiles (config D: 320 on 148 SMs): under one wave (config C: 128) each branch would
+  // just get fewer SMs than tiles (measured 112k -> 110k), and with thousands of tiles (config E)
+  // every launch fills the machine anyway (28.9k -> 25.5k).
   int fwd_split(int B) const {
     static const int v = std::getenv("PBRL_FWD_SPLIT") ? std::atoi(std::getenv("PBRL_FWD_SPLIT")) : 64;
     const long long tiles = 2LL * (shared ? 1 : n) * ((crows(B) + 127) / 128);
-    return cri.depth == 3 && tiles <= 3LL * 148 ? v : 0;
+    return cri.depth == 3 && tiles > 148 && tiles <= 3LL * 148 ? v : 0;
   }
   bool dw_fork_ok() const {
     static const bool off = std::getenv("PBRL_NO_DWFORK") != nullptr;

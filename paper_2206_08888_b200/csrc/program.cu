@@ -1028,6 +1028,26 @@ void Pop::sac_step(int B) {
     launch_sac_step_begin(n, t_pol.p, t_cri.p, t_cri.p + n, t_alpha.p, steps.p, streams.p, seed,
                           key_a.p, key_b.p, stream);
   });
+  // graph mode: the online critics' forward on [s | a] beside the target chain (split SMs), as in
+  // td3_step
+  const bool fork = capturing && use_tc();
+  const int split = fork ? fwd_split(B) : 0;
+  if (fork) {
+    if (!side2) CUDA_CHECK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+    if (!ev_fork) {
+      for (cudaEvent_t* e : {&ev_fork, &ev_join})
+        CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    CUDA_CHECK(cudaEventRecord(ev_fork, stream));
+    CUDA_CHECK(cudaStreamWaitEvent(side2, ev_fork, 0));
+    std::swap(stream, side2);
+    fork_window(stream);
+    cta_cap = split;
+    critic_forward(B);
+    std::swap(stream, side2);
+    CUDA_CHECK(cudaEventRecord(ev_join, side2));
+    cta_cap = split ? num_sms_host() - split : 0;
+  }
   // sac_critic_target (algos.hpp:739-776): current policy on s2, eps' draws, twin targets
   mlp_forward(pol, pol_p.p, n, B, Mat{S.in_s2a.p, nbB * lsa, lsa, 0}, S.tp_h, S.head.p, nbB * hd,
               hd, EPI_BIAS, nullptr, nullptr, 0, 0, false, false);
@@ -1045,14 +1065,42 @@ void Pop::sac_step(int B) {
     launch_sac_y(n, B, S.r.p, S.d.p, S.tq_out.p, S.logp2.p, log_alpha.p, h_f4.p, h_f3.p, S.y.p,
                  stream);
   });
-  critic_update(B, nullptr);  // critic targets tracked every step (:827-834)
-  // sac_policy_loss_grads (:643-735) through both UPDATED critics
+  cta_cap = 0;
+  if (fork) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_join, 0));
+  // sac_policy_loss_grads (:643-735): the policy forward + head on s depend only on the policy
+  // (updated after this), so in graph mode they run on a branch beside the critic Adam
   const Mat s = policy_input(B);
-  mlp_forward(pol, pol_p.p, n, B, s, S.ph, S.head.p, nbB * hd, hd, EPI_BIAS);
-  timed(PC_ELEM, 0.0, 0.0, 0, [&] {
-    launch_sac_head(n, B, ds, da, lsa, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p,
-                    S.ls.p, S.clamped.p, S.eps.p, S.logp.p, act16() ? 1 : 0, stream);
-  });
+  auto policy_head = [&] {
+    mlp_forward(pol, pol_p.p, n, B, s, S.ph, S.head.p, nbB * hd, hd, EPI_BIAS);
+    timed(PC_ELEM, 0.0, 0.0, 0, [&] {
+      launch_sac_head(n, B, ds, da, lsa, S.head.p, key_a.p, bound, S.sa_pi.p, S.x.p, S.th.p,
+                      S.ls.p, S.clamped.p, S.eps.p, S.logp.p, act16() ? 1 : 0, stream);
+    });
+  };
+  bool pol_forked = false;
+  if (fork && pol_fork_ctas() > 0) {
+    pre_adam = [&] {
+      if (!side6) CUDA_CHECK(cudaStreamCreateWithFlags(&side6, cudaStreamNonBlocking));
+      if (!ev_f6) {
+        for (cudaEvent_t* e : {&ev_f6, &ev_j6})
+          CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      }
+      CUDA_CHECK(cudaEventRecord(ev_f6, stream));
+      CUDA_CHECK(cudaStreamWaitEvent(side6, ev_f6, 0));
+      std::swap(stream, side6);
+      fork_window(stream);
+      cta_cap = pol_fork_ctas();
+      policy_head();
+      cta_cap = 0;
+      std::swap(stream, side6);
+      CUDA_CHECK(cudaEventRecord(ev_j6, side6));
+      pol_forked = true;
+    };
+  }
+  critic_update(B, nullptr, fork);  // critic targets tracked every step (:827-834)
+  pre_adam = nullptr;
+  if (pol_forked) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_j6, 0));
+  else policy_head();
   {
     CriticFold f(*this, B);
     const long long cB = f.B;
