@@ -425,6 +425,7 @@ struct Pop {
   std::vector<double> delay_host;
   const uint8_t* host_mask = nullptr;
   bool host_fires();
+  bool eager_fires = true;  // this step's host-mirror fire decision (eager replay)
   void sac_step(int B);
   void step(int B, const uint8_t* d_mask);
   void update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,

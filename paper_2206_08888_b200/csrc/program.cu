@@ -964,7 +964,7 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   if (pol_fwd_forked) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_j6, 0));
   pol_fwd_done = pol_fwd_forked;
   if (capturing) capture_if(any_fire, side, [&] { td3_policy_half(B); });
-  else td3_policy_half(B);
+  else if (eager_fires) td3_policy_half(B);  // eager: skipped like the IF node when none fires
 }
 
 void Pop::td3_policy_forward(int B) {
@@ -1227,6 +1227,7 @@ void Pop::invalidate_graphs() {
 void Pop::step(int B, const uint8_t* d_mask) {
   ensure_corr(t_bound + 4);
   const bool fires = algo == PBRL_ALGO_TD3 ? host_fires() : true;  // advances the mirror
+  eager_fires = fires;
   // the DvD hook runs only when some policy updates (td3_update_step, algos.hpp:394-396)
   if (dvd.on && fires) dvd_prepass();
   if (act16() && weights_dirty) refresh_shadows();
