@@ -15,6 +15,7 @@ for P in 1 8 64 256; do
   timeout 300 python bench.py --config E --pop $P --no-cpu-baseline --steps 20 --warmup 3 > gpurun_out/${TAG}_bench_E_$P.json 2>&1
 done
 timeout 300 python bench.py --gpus 2 --no-cpu-baseline > gpurun_out/${TAG}_bench_D_2ranks.json 2>&1
+timeout 600 python bench.py --replay --no-cpu-baseline > gpurun_out/${TAG}_bench_D_replay.json 2>&1
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${TAG}_bench_ref.json 2>&1
 for P in bf16 tf32; do
   PBRL_NO_GRAPH=1 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
