@@ -349,9 +349,12 @@ struct Pop {
   bool pol_fwd_done = false;
   cudaStream_t side6 = nullptr;
   cudaEvent_t ev_f6 = nullptr, ev_j6 = nullptr;
-  int pol_fork_ctas() const {
+  int pol_fork_ctas(int B) const {
     static const int v = std::getenv("PBRL_POL_FORK") ? std::atoi(std::getenv("PBRL_POL_FORK")) : 40;
-    return v;
+    // only a fused (2-hidden-layer) policy forward of a few tiles fits beside the Adam; a deep /
+    // wide one (config E: thousands of tiles) on 40 SMs would outlast it
+    const long long tiles = static_cast<long long>(n_local) * ((B + 127) / 128);
+    return pol.depth == 3 && tiles <= 2LL * 148 ? v : 0;
   }
   // SMs of the online-critic forward branch while the target chain runs beside it (0: no split;
   // PBRL_FWD_SPLIT overrides).  Only for the fused two-hidden-layer forward with a partial second

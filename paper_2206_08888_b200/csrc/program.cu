@@ -940,7 +940,7 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   // a few SMs (gated per member by the fire mask: near-empty when no policy fires); the branch
   // rejoins before the policy half
   bool pol_fwd_forked = false;
-  if (fork && pol_fork_ctas() > 0) {
+  if (fork && pol_fork_ctas(B) > 0) {
     pre_adam = [&] {
       if (!side6) CUDA_CHECK(cudaStreamCreateWithFlags(&side6, cudaStreamNonBlocking));
       if (!ev_f6) {
@@ -951,7 +951,7 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
       CUDA_CHECK(cudaStreamWaitEvent(side6, ev_f6, 0));
       std::swap(stream, side6);
       fork_window(stream);
-      cta_cap = pol_fork_ctas();
+      cta_cap = pol_fork_ctas(B);
       td3_policy_forward(B);
       cta_cap = 0;
       std::swap(stream, side6);
@@ -1078,7 +1078,7 @@ void Pop::sac_step(int B) {
     });
   };
   bool pol_forked = false;
-  if (fork && pol_fork_ctas() > 0) {
+  if (fork && pol_fork_ctas(B) > 0) {
     pre_adam = [&] {
       if (!side6) CUDA_CHECK(cudaStreamCreateWithFlags(&side6, cudaStreamNonBlocking));
       if (!ev_f6) {
@@ -1089,7 +1089,7 @@ void Pop::sac_step(int B) {
       CUDA_CHECK(cudaStreamWaitEvent(side6, ev_f6, 0));
       std::swap(stream, side6);
       fork_window(stream);
-      cta_cap = pol_fork_ctas();
+      cta_cap = pol_fork_ctas(B);
       policy_head();
       cta_cap = 0;
       std::swap(stream, side6);
