@@ -128,6 +128,7 @@ struct StepGraph {
   int B = 0;
   bool masked = false;
   bool dvd = false;  // the DvD gradient add sits in the policy half
+  bool fire = false;  // TD3: the policy half captured unconditionally (host mirror: some fire)
   cudaGraphExec_t exec = nullptr;
   size_t nodes = 0;       // kernel nodes outside conditional bodies
   size_t cond_nodes = 0;  // kernel nodes inside the policy-half conditional bodies
@@ -429,6 +430,13 @@ struct Pop {
   const uint8_t* host_mask = nullptr;
   bool host_fires();
   bool eager_fires = true;  // this step's host-mirror fire decision (eager replay)
+  // capturing the fire-step graph: the policy half is captured inline (kernels gated per member
+  // by the device fire mask) instead of inside the conditional IF node
+  bool cap_fire = false;
+  bool fire_graphs() const {
+    static const bool off = std::getenv("PBRL_NO_FIRE_GRAPH") != nullptr;
+    return !off;
+  }
   void sac_step(int B);
   void step(int B, const uint8_t* d_mask);
   void update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,

@@ -883,8 +883,11 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   // k_td3_step_begin sets when any member fires (steps where no policy fires replay only the
   // critic half); eager mode runs it with every launch gated per member instead
   const bool fork = capturing && use_tc();
+  // the fire-step graph (cap_fire) has no conditional node: the host mirror predicted that some
+  // policy fires, and every policy-half launch is gated per member by the device fire mask
+  const bool cond = capturing && !cap_fire;
   cudaGraphConditionalHandle any_fire = 0;
-  if (capturing) {
+  if (cond) {
     cudaStreamCaptureStatus st;
     cudaGraph_t g = nullptr;
     CUDA_CHECK(cudaStreamGetCaptureInfo(stream, &st, nullptr, &g, nullptr, nullptr));
@@ -893,7 +896,7 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p,
                           t_cri.p + ncrit, steps.p, streams.p, seed, key_a.p, losses.p + 2 * n,
-                          any_fire, capturing ? 1 : 0, shared ? 1 : 0, ncrit, stream);
+                          any_fire, cond ? 1 : 0, shared ? 1 : 0, ncrit, stream);
   });
   // graph mode: the online critics' forward on [s | a] does not depend on the target chain, so
   // it runs on a parallel graph branch (its tiles fill the target chain's partial waves)
@@ -940,7 +943,9 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   // a few SMs (gated per member by the fire mask: near-empty when no policy fires); the branch
   // rejoins before the policy half
   bool pol_fwd_forked = false;
-  if (fork && pol_fork_ctas(B) > 0) {
+  static const bool fire_fork = std::getenv("PBRL_FIRE_POL_FORK") == nullptr ||
+                                std::atoi(std::getenv("PBRL_FIRE_POL_FORK")) != 0;
+  if (fork && pol_fork_ctas(B) > 0 && (cap_fire ? fire_fork : !fire_graphs())) {
     pre_adam = [&] {
       if (!side6) CUDA_CHECK(cudaStreamCreateWithFlags(&side6, cudaStreamNonBlocking));
       if (!ev_f6) {
@@ -963,8 +968,8 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   pre_adam = nullptr;
   if (pol_fwd_forked) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_j6, 0));
   pol_fwd_done = pol_fwd_forked;
-  if (capturing) capture_if(any_fire, side, [&] { td3_policy_half(B); });
-  else if (eager_fires) td3_policy_half(B);  // eager: skipped like the IF node when none fires
+  if (cond) capture_if(any_fire, side, [&] { td3_policy_half(B); });
+  else if (capturing || eager_fires) td3_policy_half(B);  // eager: skipped when none fires
 }
 
 void Pop::td3_policy_forward(int B) {
@@ -1228,6 +1233,11 @@ void Pop::step(int B, const uint8_t* d_mask) {
   ensure_corr(t_bound + 4);
   const bool fires = algo == PBRL_ALGO_TD3 ? host_fires() : true;  // advances the mirror
   eager_fires = fires;
+  // TD3 graph mode: two step graphs, picked by the host mirror's fire decision -- the fire-step
+  // graph runs the policy half inline (no conditional-node boundary on its critical path), the
+  // other keeps it in the IF node (the device decides: a step the mirror did not predict still
+  // updates its policies)
+  const bool fg = algo == PBRL_ALGO_TD3 && fires && fire_graphs();
   // the DvD hook runs only when some policy updates (td3_update_step, algos.hpp:394-396)
   if (dvd.on && fires) dvd_prepass();
   if (act16() && weights_dirty) refresh_shadows();
@@ -1236,14 +1246,17 @@ void Pop::step(int B, const uint8_t* d_mask) {
   } else {
     StepGraph* sg = nullptr;
     for (auto& g : graphs)
-      if (g.B == B && g.masked == (d_mask != nullptr) && g.dvd == dvd.on) sg = &g;
+      if (g.B == B && g.masked == (d_mask != nullptr) && g.dvd == dvd.on && g.fire == fg)
+        sg = &g;
     if (!sg) {
       StepGraph g;
       g.B = B;
       g.masked = d_mask != nullptr;
       g.dvd = dvd.on;
+      g.fire = fg;
       cudaGraph_t graph;
       capturing = true;
+      cap_fire = fg;
       cond_body_nodes = 0;
       cond_nodes = 0;
       CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
@@ -1252,10 +1265,12 @@ void Pop::step(int B, const uint8_t* d_mask) {
       } catch (...) {
         cudaStreamEndCapture(stream, &graph);
         capturing = false;
+        cap_fire = false;
         throw;
       }
       CUDA_CHECK(cudaStreamEndCapture(stream, &graph));
       capturing = false;
+      cap_fire = false;
       size_t nodes = 0;
       CUDA_CHECK(cudaGraphGetNodes(graph, nullptr, &nodes));
       // kernel nodes: the conditional nodes stand for their bodies (the policy half)

@@ -1,0 +1,46 @@
+"""Graph-mode kernel timeline of config D steps through CUPTI (torch.profiler / kineto records
+the kernels of graph launches one by one): writes gpurun_out/timeline_<tag>.json with
+(name, stream, start_us, dur_us) per kernel.  args: tag [ratio] [precision]"""
+import json
+import sys
+import torch
+sys.path.insert(0, ".")
+import paper_2206_08888_b200 as pb
+from paper_2206_08888_b200 import _lib
+
+tag = sys.argv[1] if len(sys.argv) > 1 else "d"
+ratio = float(sys.argv[2]) if len(sys.argv) > 2 else 0.5
+prec = sys.argv[3] if len(sys.argv) > 3 else "bf16"
+n, B = 80, 256
+st = pb.make_td3_state(n, 17, 6, [256, 256], 1.0, 7, precision=prec, device=0)
+hy = pb.Td3Hyper.defaults(n)
+hy.policy_delay_ratio = [ratio] * n
+st._sync_hyper(hy)
+gb = pb.make_synthetic_batches(8, n, B, 17, 6, 7, device=torch.device("cuda", 0))
+structs = [_lib.Batch(*[x.data_ptr() for x in (b.s, b.a, b.r, b.s2, b.done)]) for b in gb]
+
+
+def run(i):
+    arr = (_lib.Batch * 1)(structs[i % len(structs)])
+    _lib.call("pbrl_update_batches_device", st.handle, arr, 1, B, None)
+
+
+for i in range(30):
+    run(i)
+st.synchronize()
+from torch.profiler import profile, ProfilerActivity
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for i in range(12):
+        run(i)
+    st.synchronize()
+prof.export_chrome_trace(f"gpurun_out/trace_{tag}.json")
+ev = json.load(open(f"gpurun_out/trace_{tag}.json"))["traceEvents"]
+ks = [dict(name=e["name"], stream=e.get("args", {}).get("stream", e.get("tid")),
+           start=float(e["ts"]), dur=float(e.get("dur", 0)))
+      for e in ev if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")]
+ks.sort(key=lambda k: k["start"])
+t0 = ks[0]["start"] if ks else 0.0
+for k in ks:
+    k["start"] -= t0
+json.dump(ks, open(f"gpurun_out/timeline_{tag}.json", "w"), indent=0)
+print(len(ks), "kernels")
