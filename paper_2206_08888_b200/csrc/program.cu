@@ -857,15 +857,21 @@ void Pop::capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body) 
   cudaGraph_t bg = cp.conditional.phGraph_out[0];
   CUDA_CHECK(cudaStreamBeginCaptureToGraph(cap, bg, nullptr, nullptr, 0,
                                            cudaStreamCaptureModeThreadLocal));
+  const cudaStream_t outer = stream, inner = cap;
   std::swap(stream, cap);
   wwin[stream] = true;  // conservative: the body's first kernels do not prefetch weights
   in_cond_body = true;
   try {
     body();
   } catch (...) {
+    // a throw may leave a fork unjoined or the member stream swapped with a branch: restore
+    // the streams, end the body capture and clear its error before rethrowing
     in_cond_body = false;
-    std::swap(stream, cap);
-    cudaStreamEndCapture(cap, &bg);
+    stream = outer;
+    cap = inner;
+    cudaGraph_t part = nullptr;
+    cudaStreamEndCapture(cap, &part);
+    (void)cudaGetLastError();
     throw;
   }
   in_cond_body = false;
@@ -1260,12 +1266,22 @@ void Pop::step(int B, const uint8_t* d_mask) {
       cond_body_nodes = 0;
       cond_nodes = 0;
       CUDA_CHECK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      const cudaStream_t s0 = stream;
       try {
         run_program(B, d_mask);
       } catch (...) {
-        cudaStreamEndCapture(stream, &graph);
+        // restore the member stream (a throw inside a fork leaves it swapped with a branch),
+        // end the capture (an unjoined branch makes that fail) and clear the error, so the
+        // next call does not report it
+        stream = s0;
+        graph = nullptr;
+        if (cudaStreamEndCapture(stream, &graph) == cudaSuccess && graph) cudaGraphDestroy(graph);
+        (void)cudaGetLastError();
         capturing = false;
         cap_fire = false;
+        in_cond_body = false;
+        cta_cap = 0;
+        pre_adam = nullptr;
         throw;
       }
       CUDA_CHECK(cudaStreamEndCapture(stream, &graph));
