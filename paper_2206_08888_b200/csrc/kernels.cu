@@ -927,6 +927,7 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts
 // (IT: 32-bit element indices whenever the batch allows -- the row / column split is then a
 // 32-bit division instead of a 64-bit one)
+constexpr int kPackU = 2;
 template <typename AT, typename IT>
 __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float* s,
                              const float* a, const float* r, const float* s2, const float* d,
@@ -936,23 +937,47 @@ __global__ void k_pack_batch(int n, int B, int ds, int da, int lsa, const float*
   const IT dsa = static_cast<IT>(ds + da);
   const IT rows = static_cast<IT>(n) * static_cast<IT>(B);
   const IT total = rows * dsa;
-  for (IT e = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<IT>(gridDim.x) * blockDim.x) {
-    const IT row = e / dsa;
-    const int c = static_cast<int>(e - row * dsa);
-    const long long o = static_cast<long long>(row) * lsa + c;
-    if (c < ds) {
-      const float sv = __ldcs(s + static_cast<long long>(row) * ds + c);  // read once
-      act_st(in_sa, o, sv);
-      act_st(sa_pi, o, sv);
-      act_st(in_s2a, o, __ldcs(s2 + static_cast<long long>(row) * ds + c));
-      if (in_s) act_st(in_s, static_cast<long long>(row) * lsp + c, sv);
-    } else {
-      act_st(in_sa, o, __ldcs(a + static_cast<long long>(row) * da + (c - ds)));
+  // kPackU elements per thread, kPackU * gridDim.x * blockDim.x apart: every load of a thread is
+  // issued before its stores (the grid covers the batch in one resident wave)
+  const IT span = static_cast<IT>(gridDim.x) * blockDim.x;
+  for (IT e0 = blockIdx.x * static_cast<IT>(blockDim.x) + threadIdx.x; e0 < total;
+       e0 += kPackU * span) {
+    float v[kPackU], v2[kPackU], rv[kPackU], dv[kPackU];
+    IT row[kPackU];
+    int col[kPackU];
+#pragma unroll
+    for (int u = 0; u < kPackU; ++u) {
+      const IT e = e0 + u * span;
+      row[u] = e / dsa;
+      col[u] = static_cast<int>(e - row[u] * dsa);
+      if (e >= total) continue;
+      const int c = col[u];
+      if (c < ds) {
+        v[u] = __ldcs(s + static_cast<long long>(row[u]) * ds + c);
+        v2[u] = __ldcs(s2 + static_cast<long long>(row[u]) * ds + c);
+      } else {
+        v[u] = __ldcs(a + static_cast<long long>(row[u]) * da + (c - ds));
+      }
+      if (c == 0) {
+        rv[u] = __ldcs(r + row[u]);
+        dv[u] = __ldcs(d + row[u]);
+      }
     }
-    if (c == 0) {
-      r_out[row] = __ldcs(r + row);
-      d_out[row] = __ldcs(d + row);
+#pragma unroll
+    for (int u = 0; u < kPackU; ++u) {
+      if (e0 + u * span >= total) continue;
+      const int c = col[u];
+      const long long o = static_cast<long long>(row[u]) * lsa + c;
+      act_st(in_sa, o, v[u]);
+      if (c < ds) {
+        act_st(sa_pi, o, v[u]);
+        act_st(in_s2a, o, v2[u]);
+        if (in_s) act_st(in_s, static_cast<long long>(row[u]) * lsp + c, v[u]);
+      }
+      if (c == 0) {
+        r_out[row[u]] = rv[u];
+        d_out[row[u]] = dv[u];
+      }
     }
   }
 }
@@ -977,8 +1002,9 @@ void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, co
                        void* in_s2a, void* sa_pi, float* r_out, float* d_out, int act16,
                        cudaStream_t st, void* in_s, int lsp) {
   const long long total = static_cast<long long>(n) * B * (ds + da);
-  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 148 * 16));
-  const bool narrow = total + 256LL * blocks < (1LL << 32);
+  const int blocks =
+      static_cast<int>(std::min<long long>((total + 256 * kPackU - 1) / (256 * kPackU), 148 * 8));
+  const bool narrow = total + 256LL * kPackU * blocks < (1LL << 32);
   if (act16)
     launch_pack_t<__nv_bfloat16>(blocks, narrow, st, n, B, ds, da, lsa, s, a, r, s2, d, in_sa,
                                  in_s2a, sa_pi, r_out, d_out, in_s, lsp);
