@@ -871,7 +871,7 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
                                  int64_t* t_c2, uint64_t* steps, const uint64_t* streams,
                                  uint64_t seed, uint64_t* noise_key, double* policy_loss,
                                  cudaGraphConditionalHandle any_fire, int set_cond, int shared,
-                                 int ncrit) {
+                                 int ncrit, int* guard) {
   PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   int f = 0;
@@ -903,6 +903,12 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
   // (default 0 at every graph launch; any block with a firing member sets it)
   const int any = __syncthreads_or(f);
   if (set_cond && any && threadIdx.x == 0) cudaGraphSetConditional(any_fire, 1u);
+  // the non-fire step graph (no policy half): a member that fires after all means the host
+  // mirror of the accumulators diverged -- flagged in mapped host memory, raised by the host
+  if (guard && any && threadIdx.x == 0) {
+    *reinterpret_cast<volatile int*>(guard) = 1;
+    __threadfence_system();
+  }
   if (shared && blockIdx.x == 0) {
     // fire[n]: some member fires -> the shared critic's target Polyak (cmask {1}, :407-418);
     // block 0 scans the whole mask so no cross-block ordering is needed
@@ -918,10 +924,10 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
                            cudaGraphConditionalHandle any_fire, int set_cond, int shared,
-                           int ncrit, cudaStream_t s) {
+                           int ncrit, cudaStream_t s, int* guard) {
   launch_k(k_td3_step_begin, (n + 127) / 128, 128, 0, s, n, delay_acc, ratio, mask, fire, t_pol,
            t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, set_cond, shared,
-           ncrit);
+           ncrit, guard);
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts

@@ -185,6 +185,7 @@ Pop::~Pop() {
     if (side) cudaStreamDestroy(side);
     if (side2) cudaStreamDestroy(side2);
     if (side6) cudaStreamDestroy(side6);
+    if (guard_h) cudaFreeHost(guard_h);
     if (ev_f6) cudaEventDestroy(ev_f6);
     if (ev_j6) cudaEventDestroy(ev_j6);
     for (int i = 0; i < 2; ++i) {
@@ -200,7 +201,20 @@ Pop::~Pop() {
   }
 }
 
-void Pop::sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
+void Pop::sync() {
+  CUDA_CHECK(cudaStreamSynchronize(stream));
+  check_guard();
+}
+
+void Pop::check_guard() {
+  if (guard_h && *reinterpret_cast<volatile int*>(guard_h)) {
+    *guard_h = 0;
+    invalidate_graphs();
+    PBRL_THROW(PBRL_E_USAGE,
+               "TD3 step graph: a policy fired on a step the host-side policy-delay mirror "
+               "predicted to skip (mirror diverged from the device accumulators)");
+  }
+}
 
 // BF16 mode: re-derive the bf16 tensor-core copies from the fp32 master weights (after init,
 // set_member, PBT exploit copies, imports); the update step itself keeps them current

@@ -437,6 +437,17 @@ struct Pop {
     static const bool off = std::getenv("PBRL_NO_FIRE_GRAPH") != nullptr;
     return !off;
   }
+  // the non-fire step graph: no policy half at all, and k_td3_step_begin raises a flag in mapped
+  // host memory if some member fires after all (the host mirror diverged: the next call fails
+  // loudly).  PBRL_COND_GRAPH=1 keeps the device-decided IF node instead (its evaluation after
+  // the critic Adam costs ~9 us per non-fire step).
+  bool cond_graph() const {
+    static const bool on = std::getenv("PBRL_COND_GRAPH") != nullptr;
+    return on || !fire_graphs();
+  }
+  int* guard_h = nullptr;  // mapped pinned host flag
+  int* guard_d = nullptr;  // its device alias
+  void check_guard();
   void sac_step(int B);
   void step(int B, const uint8_t* d_mask);
   void update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,

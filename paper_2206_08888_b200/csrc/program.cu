@@ -891,7 +891,8 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   const bool fork = capturing && use_tc();
   // the fire-step graph (cap_fire) has no conditional node: the host mirror predicted that some
   // policy fires, and every policy-half launch is gated per member by the device fire mask
-  const bool cond = capturing && !cap_fire;
+  const bool cond = capturing && !cap_fire && cond_graph();
+  const bool guarded = capturing && !cap_fire && !cond;  // non-fire graph, no policy half
   cudaGraphConditionalHandle any_fire = 0;
   if (cond) {
     cudaStreamCaptureStatus st;
@@ -902,7 +903,8 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   timed(PC_ELEM, 0.0, 0.0, 0, [&] {
     launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p,
                           t_cri.p + ncrit, steps.p, streams.p, seed, key_a.p, losses.p + 2 * n,
-                          any_fire, cond ? 1 : 0, shared ? 1 : 0, ncrit, stream);
+                          any_fire, cond ? 1 : 0, shared ? 1 : 0, ncrit, stream,
+                          guarded ? guard_d : nullptr);
   });
   // graph mode: the online critics' forward on [s | a] does not depend on the target chain, so
   // it runs on a parallel graph branch (its tiles fill the target chain's partial waves)
@@ -975,7 +977,7 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   if (pol_fwd_forked) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_j6, 0));
   pol_fwd_done = pol_fwd_forked;
   if (cond) capture_if(any_fire, side, [&] { td3_policy_half(B); });
-  else if (capturing || eager_fires) td3_policy_half(B);  // eager: skipped when none fires
+  else if (cap_fire || (!capturing && eager_fires)) td3_policy_half(B);  // else: none fires
 }
 
 void Pop::td3_policy_forward(int B) {
@@ -1236,6 +1238,12 @@ void Pop::invalidate_graphs() {
 }
 
 void Pop::step(int B, const uint8_t* d_mask) {
+  check_guard();
+  if (algo == PBRL_ALGO_TD3 && use_graphs && !guard_h) {  // (not allowed while capturing)
+    CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&guard_h), sizeof(int), cudaHostAllocMapped));
+    *guard_h = 0;
+    CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&guard_d), guard_h, 0));
+  }
   ensure_corr(t_bound + 4);
   const bool fires = algo == PBRL_ALGO_TD3 ? host_fires() : true;  // advances the mirror
   eager_fires = fires;

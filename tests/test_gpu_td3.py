@@ -186,3 +186,35 @@ def test_update_k_steps_with_losses_matches_single_steps(pb, ora, precision, K):
     for net in ("policy", "policy_target", "critic1", "critic2", "critic1_target",
                 "critic2_target"):
         assert np.array_equal(a.params(net), b.params(net)), net
+
+
+@pytest.mark.parametrize("precision", ["ffma32", "bf16"])
+def test_fire_and_nonfire_step_graphs_equal_eager(pb, ora, precision, monkeypatch):
+    """Graph mode replays one of two step graphs per step (the host mirror of the delay
+    accumulators picks the fire-step graph, the other keeps the device-decided IF node).  With
+    per-member delays that make some steps fire for a few members only, some for all and some
+    for none, the graph replay equals the eager launch sequence bit for bit (and, in FFMA32, the
+    oracle)."""
+    n, ds, da, B, K = 5, 17, 6, 64, 9
+    hidden = [64, 64] if precision == "ffma32" else [256, 256]
+    hy = pb.Td3Hyper.defaults(n)
+    hy.policy_delay_ratio = [1.0, 0.5, 0.25, 0.34, 0.2]
+    raw = ora.synthetic_batches(K, n, B, ds, da, 21)
+    batches = [to_batch(pb, raw, k) for k in range(K)]
+    g = pb.make_td3_state(n, ds, da, hidden, 1.0, 21, precision=precision)
+    monkeypatch.setenv("PBRL_NO_GRAPH", "1")
+    e = pb.make_td3_state(n, ds, da, hidden, 1.0, 21, precision=precision)
+    monkeypatch.delenv("PBRL_NO_GRAPH")
+    it = iter(batches)
+    pb.update_k_steps(g, lambda: next(it), K, hy)
+    for k in range(K):
+        pb.td3_update_step(e, batches[k], hy)
+    for net in TD3_NETS:
+        assert bits_equal(g.params(net), e.params(net)), net
+    assert np.array_equal(g.steps, e.steps) and np.array_equal(g.delay_acc, e.delay_acc)
+    if precision == "ffma32":
+        ref = ora.td3(n, ds, da, hidden, 1.0, 21)
+        oh = {f: list(getattr(hy, f)) for f in pb.Td3Hyper.FIELDS}
+        for k in range(K):
+            ref.step(raw_at(raw, k), oh)
+        _assert_state_equal(g, ref, n)

@@ -27,6 +27,12 @@ PBRL_NO_GRAPH=1 timeout 900 ncu --set full --clock-control none --import-source 
   -o gpurun_out/full_${TAG}_bf16 -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e \
   > gpurun_out/ncu_full_${TAG}.log 2>&1
 tail -1 gpurun_out/ncu_full_${TAG}.log
+# graph-mode kernel timeline (CUPTI through torch.profiler): a fire step and a non-fire step
+timeout 200 python tools/gpu/timeline.py ${TAG}_graph 0.5 > /dev/null 2>&1
+{ echo "# ${TAG}: graph-mode kernel timeline, config D BF16 (CUPTI, tools/gpu/timeline.py)"; echo;
+  echo "start / duration / end in us from the step's batch pack; sN = graph branch (stream id)"; echo;
+  echo '```'; python tools/gpu/tl_show.py ${TAG}_graph 4 2; echo '```'; } > gpurun_out/profiles_box/${TAG}_graph_timeline.md
+rm -f gpurun_out/trace_${TAG}_graph.json
 python profiles/summarize.py ${TAG}_bf16 gpurun_out/launches_${TAG}_bf16.csv gpurun_out/full_${TAG}_bf16.ncu-rep > /dev/null 2>&1
 python profiles/summarize.py ${TAG}_tf32 gpurun_out/launches_${TAG}_tf32.csv > /dev/null 2>&1
 cp profiles/${TAG}_bf16_*.md profiles/${TAG}_tf32_*.md profiles/traffic_bf16_D.json gpurun_out/profiles_box/ 2>/dev/null
