@@ -521,8 +521,27 @@ template <> struct VecN<__nv_bfloat16, 2> {
   }
 };
 
+// Resident blocks per SM asked of ptxas and row loads in flight per thread, per output width
+// (compile-time PBRL_OBV_{MINB,U}{1,N}).  Measured on B200 (config D BF16, alternating runs):
+// single-output (critic) layers 4 blocks / 4 loads (64 registers) against the unconstrained
+// 103-register build with 8 loads (2 blocks/SM: 640 blocks in 2.2 waves), 314k -> 322k
+// agent-updates/s; 5 blocks (48 registers) 315k.  The 6-output (policy) layer: 3 blocks / 8 loads
+// (80 registers) 323k, 4 / 4 322k, 5 / 2 316k.
+#ifndef PBRL_OBV_MINB1
+#define PBRL_OBV_MINB1 4
+#endif
+#ifndef PBRL_OBV_U1
+#define PBRL_OBV_U1 4
+#endif
+#ifndef PBRL_OBV_MINBN
+#define PBRL_OBV_MINBN 3
+#endif
+#ifndef PBRL_OBV_UN
+#define PBRL_OBV_UN 8
+#endif
 template <int NO, typename AT, int CW>
-__global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdArgs a) {
+__global__ void __launch_bounds__(kOvQuads* kOvSlices, NO == 1 ? PBRL_OBV_MINB1 : PBRL_OBV_MINBN)
+    k_out_backward_v(OutBwdArgs a) {
   PDL_ENTRY();
   extern __shared__ float sm[];
   constexpr int NA = NO, CB = CW * kOvQuads;  // columns per block
@@ -595,7 +614,7 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices) k_out_backward_v(OutBwdAr
   const int b0 = sl * rows, b1 = min(B, b0 + rows);
   AT* dX = a.dX ? static_cast<AT*>(a.dX) + grp * a.dx_gs : nullptr;
   if (live) {
-    constexpr int U = 8;
+    constexpr int U = NO == 1 ? PBRL_OBV_U1 : PBRL_OBV_UN;
     for (int b = b0; b < b1; b += U) {
       float xv[U][CW];
 #pragma unroll

@@ -196,6 +196,10 @@ Pop::~Pop() {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (cstream) cudaStreamDestroy(cstream);
+    if (pstream) cudaStreamDestroy(pstream);
+    if (side_sf) cudaStreamDestroy(side_sf);
+    for (cudaEvent_t e : {ev_stage_free, ev_packed, ev_sf_fork, ev_sf_join})
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {ev_copied[0], ev_copied[1], ev_free[0], ev_free[1]})
       if (e) cudaEventDestroy(e);
   }
@@ -452,13 +456,24 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     slot_used[sl] = true;
   };
   if (!device_ptrs) stage(0);
+  const bool ovl = pack_overlap_ok();
+  if (ovl && !pstream) {
+    CUDA_CHECK(cudaStreamCreateWithFlags(&pstream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev_packed, cudaEventDisableTiming));
+  }
+  last_step_stage_ev = false;  // across calls the member stream may carry other work
   for (uint32_t i = 0; i < k; ++i) {
     const pbrl_batch& b = batches[i];
     const float *s = b.s, *a = b.a, *r = b.r, *s2 = b.s2, *d = b.done;
+    // the pack of batch i overlaps the last Adam of step i-1 (after its ev_stage_free) when
+    // step i-1 was a graph that records it; otherwise it runs in member-stream order
+    const bool side = ovl && last_step_stage_ev;
+    cudaStream_t ps = side ? pstream : stream;
+    if (side) CUDA_CHECK(cudaStreamWaitEvent(ps, ev_stage_free, 0));
     if (!device_ptrs) {
       if (i + 1 < k) stage(i + 1);  // overlaps this step
       const int sl = static_cast<int>(i & 1u);
-      CUDA_CHECK(cudaStreamWaitEvent(stream, ev_copied[sl], 0));
+      CUDA_CHECK(cudaStreamWaitEvent(ps, ev_copied[sl], 0));
       s = S.bs[sl].p;
       a = S.ba[sl].p;
       r = S.br[sl].p;
@@ -467,9 +482,13 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     }
     timed(PC_GATHER, 0.0, pack_bytes(B), 0, [&] {
       launch_pack_batch(n, B, ds, da, lsa, s, a, r, s2, d, S.in_sa.p, S.in_s2a.p, S.sa_pi.p, S.r.p,
-                        S.d.p, act16() ? 1 : 0, stream, S.in_s.p, lsp);
+                        S.d.p, act16() ? 1 : 0, ps, S.in_s.p, lsp);
     });
-    if (!device_ptrs) CUDA_CHECK(cudaEventRecord(ev_free[i & 1u], stream));
+    if (!device_ptrs) CUDA_CHECK(cudaEventRecord(ev_free[i & 1u], ps));
+    if (side) {
+      CUDA_CHECK(cudaEventRecord(ev_packed, ps));
+      CUDA_CHECK(cudaStreamWaitEvent(stream, ev_packed, 0));
+    }
     step(B, d_mask);
     if (losses_out) {
       // this step's critic1 / critic2 / policy losses -> a device history slot; the history

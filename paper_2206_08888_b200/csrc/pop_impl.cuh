@@ -132,6 +132,7 @@ struct StepGraph {
   cudaGraphExec_t exec = nullptr;
   size_t nodes = 0;       // kernel nodes outside conditional bodies
   size_t cond_nodes = 0;  // kernel nodes inside the policy-half conditional bodies
+  bool stage_ev = false;  // records ev_stage_free once the step has read its packed batch
 };
 
 struct Pop;
@@ -457,6 +458,20 @@ struct Pop {
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   bool slot_used[2] = {false, false};
+  // TD3 step graphs record ev_stage_free (an external event-record node on a branch) right
+  // before the step's last Adam, the point after which nothing in the step reads the packed
+  // batch (in_sa / in_s2a / in_s / sa_pi's state part / r / d); inside one update_batches call
+  // the next batch's pack then runs on pstream beside that Adam instead of after the graph
+  cudaStream_t pstream = nullptr, side_sf = nullptr;
+  cudaEvent_t ev_stage_free = nullptr, ev_packed = nullptr, ev_sf_fork = nullptr,
+              ev_sf_join = nullptr;
+  int stage_mark = 0;  // capture: 1 = mark before the critic Adam, 2 = before the policy Adam
+  bool stage_joined = true;  // the marker branch has been joined back
+  bool stage_ev_captured = false;  // the graph being captured records ev_stage_free
+  bool last_step_stage_ev = false;  // the last step() launched a graph recording ev_stage_free
+  bool pack_overlap_ok() const;
+  void mark_stage_free();
+  void join_stage_free();
 
   // helpers for member-level access
   float* net_row(int net, uint64_t member);

@@ -816,6 +816,7 @@ void Pop::critic_update(int B0, const int* polyak_gate, bool forward_done) {
     CriticUnfold u(*this);
     pre_adam();
   }
+  if (stage_mark == 1) mark_stage_free();
   // 28 B/param Adam (+2 B/param bf16 operand copy in BF16 mode)
   const double cP = static_cast<double>(cri.P);
   timed(PC_ADAM, 0.0, cP * n2 * (act16() ? 30.0 : 28.0), 0, [&] {
@@ -972,12 +973,50 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
       pol_fwd_forked = true;
     };
   }
+  // the non-fire graph reads its packed batch last in the critic backward, the fire-step graph
+  // in the policy backward
+  const bool mark = capturing && pack_overlap_ok() && (guarded || cap_fire);
+  if (mark && guarded) stage_mark = 1;
   critic_update(B, fire.p, fork);
   pre_adam = nullptr;
   if (pol_fwd_forked) CUDA_CHECK(cudaStreamWaitEvent(stream, ev_j6, 0));
   pol_fwd_done = pol_fwd_forked;
+  if (mark && cap_fire) stage_mark = 2;
   if (cond) capture_if(any_fire, side, [&] { td3_policy_half(B); });
   else if (cap_fire || (!capturing && eager_fires)) td3_policy_half(B);  // else: none fires
+  stage_mark = 0;
+  join_stage_free();
+}
+
+// TD3 independent-mode step graphs only: the shared critic, DvD (its pre-pass) and the
+// conditional-node graph keep the pack on the member stream
+bool Pop::pack_overlap_ok() const {
+  static const bool off = std::getenv("PBRL_NO_PACK_OVERLAP") != nullptr;
+  return !off && algo == PBRL_ALGO_TD3 && !shared && !dvd.on && use_graphs && !prof_on &&
+         fire_graphs() && !cond_graph();
+}
+
+// capture: an external event-record node for ev_stage_free on a branch forked at the current
+// point of the member stream (the next kernel keeps its programmatic edge to its predecessor)
+void Pop::mark_stage_free() {
+  if (!side_sf) CUDA_CHECK(cudaStreamCreateWithFlags(&side_sf, cudaStreamNonBlocking));
+  if (!ev_stage_free) {
+    for (cudaEvent_t* e : {&ev_stage_free, &ev_sf_fork, &ev_sf_join})
+      CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  CUDA_CHECK(cudaEventRecord(ev_sf_fork, stream));
+  CUDA_CHECK(cudaStreamWaitEvent(side_sf, ev_sf_fork, 0));
+  CUDA_CHECK(cudaEventRecordWithFlags(ev_stage_free, side_sf, cudaEventRecordExternal));
+  CUDA_CHECK(cudaEventRecord(ev_sf_join, side_sf));
+  stage_joined = false;
+  stage_ev_captured = true;
+  stage_mark = 0;
+}
+
+void Pop::join_stage_free() {
+  if (stage_joined) return;
+  CUDA_CHECK(cudaStreamWaitEvent(stream, ev_sf_join, 0));
+  stage_joined = true;
 }
 
 void Pop::td3_policy_forward(int B) {
@@ -1025,6 +1064,7 @@ void Pop::td3_policy_half(int B) {
     const size_t cnt = static_cast<size_t>(n) * pol.stride;
     timed(PC_ELEM, 0.0, 12.0 * cnt, 0, [&] { launch_add_into(pol_g.p, dvd.grad.p, cnt, stream); });
   }
+  if (stage_mark == 2) mark_stage_free();
   timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * (act16() ? 40.0 : 36.0), 1, [&] {
     launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
                 corr2.p, h_f1.p, fire.p, pol_t.p, h_f5.p, h_f6.p, nullptr, pol_p16.p, pol_t16.p,
@@ -1239,6 +1279,7 @@ void Pop::invalidate_graphs() {
 
 void Pop::step(int B, const uint8_t* d_mask) {
   check_guard();
+  last_step_stage_ev = false;
   if (algo == PBRL_ALGO_TD3 && use_graphs && !guard_h) {  // (not allowed while capturing)
     CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&guard_h), sizeof(int), cudaHostAllocMapped));
     *guard_h = 0;
@@ -1287,6 +1328,9 @@ void Pop::step(int B, const uint8_t* d_mask) {
         (void)cudaGetLastError();
         capturing = false;
         cap_fire = false;
+        stage_mark = 0;
+        stage_joined = true;
+        stage_ev_captured = false;
         in_cond_body = false;
         cta_cap = 0;
         pre_adam = nullptr;
@@ -1295,6 +1339,8 @@ void Pop::step(int B, const uint8_t* d_mask) {
       CUDA_CHECK(cudaStreamEndCapture(stream, &graph));
       capturing = false;
       cap_fire = false;
+      g.stage_ev = ev_stage_free && stage_ev_captured;
+      stage_ev_captured = false;
       size_t nodes = 0;
       CUDA_CHECK(cudaGraphGetNodes(graph, nullptr, &nodes));
       // kernel nodes: the conditional nodes stand for their bodies (the policy half)
@@ -1307,6 +1353,7 @@ void Pop::step(int B, const uint8_t* d_mask) {
     }
     CUDA_CHECK(cudaGraphLaunch(sg->exec, stream));
     count_launch(sg->nodes + (fires ? sg->cond_nodes : 0));
+    last_step_stage_ev = sg->stage_ev;
   }
   t_bound += 1;
   prof_step_done();

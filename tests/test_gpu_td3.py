@@ -188,6 +188,30 @@ def test_update_k_steps_with_losses_matches_single_steps(pb, ora, precision, K):
         assert np.array_equal(a.params(net), b.params(net)), net
 
 
+@pytest.mark.parametrize("precision,n", [("bf16", 80), ("ffma32", 6)])
+def test_pack_overlap_device_batches_equal_single_steps(pb, ora, precision, n):
+    """Inside one update call the pack of batch i+1 runs on its own stream beside step i's last
+    Adam (after the step graph's ev_stage_free record node).  K device batches in one call at the
+    config-D shape (80 members, B = 256, both step graphs, policy delays mixed so some steps fire
+    for a few members only, some for none) leave the same state, bit for bit, as K single-step calls, whose packs
+    run in member-stream order."""
+    import torch
+    B, K = 256, 12
+    hidden = [256, 256] if precision == "bf16" else [64, 64]
+    hy = pb.Td3Hyper.defaults(n)
+    hy.policy_delay_ratio = [[0.5, 0.25, 0.34, 0.2, 0.5][m % 5] for m in range(n)]
+    gb = pb.make_synthetic_batches(K, n, B, 17, 6, 31, device=torch.device("cuda", 0))
+    a = pb.make_td3_state(n, 17, 6, hidden, 1.0, 31, precision=precision)
+    b = pb.make_td3_state(n, 17, 6, hidden, 1.0, 31, precision=precision)
+    it = iter(gb)
+    pb.update_k_steps(a, lambda: next(it), K, hy)
+    for k in range(K):
+        pb.td3_update_step(b, gb[k], hy)
+    for net in TD3_NETS:
+        assert bits_equal(a.params(net), b.params(net)), net
+    assert np.array_equal(a.steps, b.steps) and np.array_equal(a.delay_acc, b.delay_acc)
+
+
 @pytest.mark.parametrize("precision", ["ffma32", "bf16"])
 def test_fire_and_nonfire_step_graphs_equal_eager(pb, ora, precision, monkeypatch):
     """Graph mode replays one of two step graphs per step (the host mirror of the delay
