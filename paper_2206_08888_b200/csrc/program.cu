@@ -988,12 +988,12 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
   join_stage_free();
 }
 
-// TD3 independent-mode step graphs only: the shared critic, DvD (its pre-pass) and the
-// conditional-node graph keep the pack on the member stream
+// independent-mode step graphs only (TD3: the two step graphs, not the conditional-node one):
+// the shared critic and DvD (its pre-pass) keep the pack on the member stream
 bool Pop::pack_overlap_ok() const {
   static const bool off = std::getenv("PBRL_NO_PACK_OVERLAP") != nullptr;
-  return !off && algo == PBRL_ALGO_TD3 && !shared && !dvd.on && use_graphs && !prof_on &&
-         fire_graphs() && !cond_graph();
+  if (off || shared || dvd.on || !use_graphs || prof_on) return false;
+  return algo == PBRL_ALGO_SAC || (fire_graphs() && !cond_graph());
 }
 
 // capture: an external event-record node for ev_stage_free on a branch forked at the current
@@ -1176,6 +1176,8 @@ void Pop::sac_step(int B) {
   });
   mlp_backward(pol, pol_p.p, pol_g.p, n, B, Mat{S.gtop.p, nbB * hd, hd, 0}, s, S.ph, S.pdh,
                nullptr);
+  // the policy backward is the step's last reader of its packed batch
+  if (capturing && pack_overlap_ok()) mark_stage_free();
   timed(PC_ADAM, 0.0, static_cast<double>(pol.P) * n * 28.0, 0, [&] {
     launch_adam(n, n, pol.P, pol.stride, pol_p.p, pol_m.p, pol_v.p, pol_g.p, t_pol.p, corr1.p,
                 corr2.p, h_f0.p, nullptr, nullptr, nullptr, nullptr, nullptr, pol_p16.p, nullptr,
@@ -1185,6 +1187,7 @@ void Pop::sac_step(int B) {
     launch_sac_alpha(n, B, S.logp.p, log_alpha.p, h_d0.p, log_alpha.p, alpha_m.p, alpha_v.p,
                      t_alpha.p, corr1.p, corr2.p, h_f2.p, stream);
   });
+  join_stage_free();
 }
 
 // ------------------------------------------------------------------ action selection

@@ -212,6 +212,26 @@ def test_pack_overlap_device_batches_equal_single_steps(pb, ora, precision, n):
     assert np.array_equal(a.steps, b.steps) and np.array_equal(a.delay_acc, b.delay_acc)
 
 
+@pytest.mark.parametrize("precision", ["bf16", "ffma32"])
+def test_pack_overlap_sac_device_batches_equal_single_steps(pb, ora, precision):
+    """The same for the SAC step graph (config C shape: 32 members, B = 256), whose policy
+    backward is the last reader of the packed batch."""
+    import torch
+    from helpers import SAC_NETS
+    n, B, K = 32, 256, 8
+    hidden = [256, 256] if precision == "bf16" else [64, 64]
+    hy = pb.SacHyper.defaults(n, 6)
+    gb = pb.make_synthetic_batches(K, n, B, 17, 6, 37, device=torch.device("cuda", 0))
+    a = pb.make_sac_state(n, 17, 6, hidden, 1.0, 37, precision=precision)
+    b = pb.make_sac_state(n, 17, 6, hidden, 1.0, 37, precision=precision)
+    it = iter(gb)
+    pb.update_k_steps(a, lambda: next(it), K, hy)
+    for k in range(K):
+        pb.sac_update_step(b, gb[k], hy)
+    for net in SAC_NETS:
+        assert bits_equal(a.params(net), b.params(net)), net
+
+
 @pytest.mark.parametrize("precision", ["ffma32", "bf16"])
 def test_fire_and_nonfire_step_graphs_equal_eager(pb, ora, precision, monkeypatch):
     """Graph mode replays one of two step graphs per step (the host mirror of the delay
