@@ -485,7 +485,8 @@ def main():
     classes_hbm = {k: {"gbs": c["bytes"] / (c["ms"] / 1e3) / 1e9 if c["ms"] > 0 else None,
                        "frac": (c["bytes"] / (c["ms"] / 1e3) / 1e9) / pk["hbm"]
                        if c["ms"] > 0 else None}
-                   for k, c in cls.items() if k in ("adam_polyak", "gather_pack", "elementwise")}
+                   for k, c in cls.items()
+                   if k in ("adam_polyak", "gather_pack", "elementwise") and c["bytes"] > 0}
     # whole-step roofline: T_roof = max(n F / P_tc, n Bytes / BW_hbm)
     work = td3_member_update_work if cfg["algo"] == "td3" else sac_member_update_work
     fl, by = work(cfg["hidden"], cfg["batch"])

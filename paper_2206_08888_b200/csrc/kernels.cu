@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(kObCols* kObSlices) k_out_backward(OutBwdArgs 
 // per block (enough blocks and loads in flight to cover HBM latency); slices combined in slice
 // order (deterministic).  Requires H % 4 == 0 and 4-element
 // aligned rows (launch_out_backward checks and otherwise uses k_out_backward).
-constexpr int kOvQuads = 16, kOvSlices = 16;  // 64 columns x 16 row slices per block
+constexpr int kOvQuads = 16;  // CW x 16 columns per block; row slices: ov_slices<NO>()
 
 template <typename AT, int CW> struct VecN;
 template <> struct VecN<float, 4> {
@@ -539,8 +539,15 @@ template <> struct VecN<__nv_bfloat16, 2> {
 #ifndef PBRL_OBV_UN
 #define PBRL_OBV_UN 8
 #endif
+#ifndef PBRL_OBV_SL1
+#define PBRL_OBV_SL1 16
+#endif
+#ifndef PBRL_OBV_SLN
+#define PBRL_OBV_SLN 16
+#endif
+template <int NO> __host__ __device__ constexpr int ov_slices() { return NO == 1 ? PBRL_OBV_SL1 : PBRL_OBV_SLN; }
 template <int NO, typename AT, int CW>
-__global__ void __launch_bounds__(kOvQuads* kOvSlices, NO == 1 ? PBRL_OBV_MINB1 : PBRL_OBV_MINBN)
+__global__ void __launch_bounds__(kOvQuads* ov_slices<NO>(), NO == 1 ? PBRL_OBV_MINB1 : PBRL_OBV_MINBN)
     k_out_backward_v(OutBwdArgs a) {
   PDL_ENTRY();
   extern __shared__ float sm[];
@@ -548,8 +555,8 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices, NO == 1 ? PBRL_OBV_MINB1 
   const int nout = NO < 16 ? NO : a.nout, B = a.B;
   float* Gs = sm;                                // [B][nout]
   float* Ls = Gs + B * nout;                     // [B]
-  float* Ps = Ls + B;                            // [kOvSlices][CB][nout]
-  float* Cs = Ps + kOvSlices * CB * nout;        // [kOvSlices][CB]
+  float* Ps = Ls + B;                            // [ov_slices<NO>()][CB][nout]
+  float* Cs = Ps + ov_slices<NO>() * CB * nout;        // [ov_slices<NO>()][CB]
   const int grp = blockIdx.y;
   const int mem = grp % a.n_members;
   if (a.active && !a.active[mem]) return;
@@ -610,7 +617,7 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices, NO == 1 ? PBRL_OBV_MINB1 
     }
   }
   __syncthreads();
-  const int rows = (B + kOvSlices - 1) / kOvSlices;
+  const int rows = (B + ov_slices<NO>() - 1) / ov_slices<NO>();
   const int b0 = sl * rows, b1 = min(B, b0 + rows);
   AT* dX = a.dX ? static_cast<AT*>(a.dX) + grp * a.dx_gs : nullptr;
   if (live) {
@@ -649,7 +656,7 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices, NO == 1 ? PBRL_OBV_MINB1 
       const int col = blockIdx.x * CB + cc;
       if (col >= a.H) continue;
       float t = Cs[cc];
-      for (int q = 1; q < kOvSlices; ++q) t += Cs[q * CB + cc];
+      for (int q = 1; q < ov_slices<NO>(); ++q) t += Cs[q * CB + cc];
       a.dbx[grp * a.dbx_gs + col] = t;
     }
   }
@@ -679,7 +686,7 @@ __global__ void __launch_bounds__(kOvQuads* kOvSlices, NO == 1 ? PBRL_OBV_MINB1 
     const int col = blockIdx.x * CB + cc;
     if (col >= a.H) continue;
     float t = Ps[cc * nout + o];
-    for (int q = 1; q < kOvSlices; ++q) t += Ps[(q * CB + cc) * nout + o];
+    for (int q = 1; q < ov_slices<NO>(); ++q) t += Ps[(q * CB + cc) * nout + o];
     dW[static_cast<long long>(col) * nout + o] = t;
   }
   if (blockIdx.x == 0) {  // db of the output layer: warp tree
@@ -709,7 +716,7 @@ static bool launch_ob_v(const OutBwdArgs& a, cudaStream_t s) {
       return false;
     constexpr int CB = CW * kOvQuads;
     const size_t smem = (static_cast<size_t>(a.B) * (a.nout + 1) +
-                         static_cast<size_t>(kOvSlices) * CB * (a.nout + 1)) * 4;
+                         static_cast<size_t>(ov_slices<NO>()) * CB * (a.nout + 1)) * 4;
     if (smem > 200 * 1024) return false;
     static bool attr = false;
     if (!attr) {
@@ -718,7 +725,7 @@ static bool launch_ob_v(const OutBwdArgs& a, cudaStream_t s) {
       attr = true;
     }
     dim3 grid((a.H + CB - 1) / CB, a.groups);
-    launch_k(k_out_backward_v<NO, AT, CW>, grid, kOvQuads * kOvSlices, smem, s, a);
+    launch_k(k_out_backward_v<NO, AT, CW>, grid, kOvQuads * ov_slices<NO>(), smem, s, a);
     return true;
   }
 }
