@@ -526,7 +526,9 @@ template <> struct VecN<__nv_bfloat16, 2> {
 // single-output (critic) layers 4 blocks / 4 loads (64 registers) against the unconstrained
 // 103-register build with 8 loads (2 blocks/SM: 640 blocks in 2.2 waves), 314k -> 322k
 // agent-updates/s; 5 blocks (48 registers) 315k.  The 6-output (policy) layer: 3 blocks / 8 loads
-// (80 registers) 323k, 4 / 4 322k, 5 / 2 316k.
+// (80 registers) 323k, 4 / 4 322k, 5 / 2 316k; then 8 row slices (128-thread blocks, 4 per SM,
+// 94 registers, 8 loads: the 640 blocks resident in one wave) 329.2k -> 330.4k (the critic at 8
+// slices: 321k).
 #ifndef PBRL_OBV_MINB1
 #define PBRL_OBV_MINB1 4
 #endif
@@ -534,7 +536,7 @@ template <> struct VecN<__nv_bfloat16, 2> {
 #define PBRL_OBV_U1 4
 #endif
 #ifndef PBRL_OBV_MINBN
-#define PBRL_OBV_MINBN 3
+#define PBRL_OBV_MINBN 4
 #endif
 #ifndef PBRL_OBV_UN
 #define PBRL_OBV_UN 8
@@ -543,9 +545,11 @@ template <> struct VecN<__nv_bfloat16, 2> {
 #define PBRL_OBV_SL1 16
 #endif
 #ifndef PBRL_OBV_SLN
-#define PBRL_OBV_SLN 16
+#define PBRL_OBV_SLN 8
 #endif
-template <int NO> __host__ __device__ constexpr int ov_slices() { return NO == 1 ? PBRL_OBV_SL1 : PBRL_OBV_SLN; }
+template <int NO> __host__ __device__ constexpr int ov_slices() {
+  return NO == 1 ? PBRL_OBV_SL1 : PBRL_OBV_SLN;
+}
 template <int NO, typename AT, int CW>
 __global__ void __launch_bounds__(kOvQuads* ov_slices<NO>(), NO == 1 ? PBRL_OBV_MINB1 : PBRL_OBV_MINBN)
     k_out_backward_v(OutBwdArgs a) {
