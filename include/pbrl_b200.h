@@ -125,7 +125,10 @@ int pbrl_get_alpha(pbrl_pop* pop, float* log_alpha, float* m, float* v, int64_t*
  * policy_mask (TD3 only, may be NULL): [n] bytes, policy_member_mask of td3_update_step. */
 int pbrl_update_batches(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k, uint64_t batch_rows,
                         const uint8_t* policy_mask);
-/* Same with device-resident batches (pointers valid on the population's device). */
+/* Same with device-resident batches (pointers valid on the population's device).  Inside one
+ * call (k > 1) the pack of batch i+1 runs beside step i's last Adam on a library stream, so k
+ * batches per call are faster than k calls; the batches must stay valid until the call's work
+ * has completed on the population's stream. */
 int pbrl_update_batches_device(pbrl_pop* pop, const pbrl_batch* batches, uint32_t k,
                                uint64_t batch_rows, const uint8_t* policy_mask);
 /* update_k_steps over k HOST batches with every step's losses returned: losses[i][0..2][n] =
