@@ -901,10 +901,22 @@ __global__ void k_td3_step_begin(int n, double* delay_acc, const double* ratio,
                                  int64_t* t_c2, uint64_t* steps, const uint64_t* streams,
                                  uint64_t seed, uint64_t* noise_key, double* policy_loss,
                                  cudaGraphConditionalHandle any_fire, int set_cond, int shared,
-                                 int ncrit, int* guard) {
+                                 int ncrit, int* guard, double* hist, const uint64_t* hist_base,
+                                 int hist_slots) {
   PDL_ENTRY();
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   int f = 0;
+  if (m < n && hist) {
+    // loss history of an update call (pbrl_update_batches_losses): the previous step's
+    // critic1 / critic2 / policy losses of this member into its history slot, before this step
+    // overwrites them (steps[m] - hist_base[m] = steps of the call already begun)
+    const uint64_t s = steps[m] - hist_base[m];
+    if (s >= 1) {
+      const double* losses = policy_loss - 2 * n;  // [critic1 | critic2 | policy][n]
+      double* row = hist + static_cast<size_t>((s - 1) % hist_slots) * 3 * n;
+      for (int q = 0; q < 3; ++q) row[q * n + m] = losses[q * n + m];
+    }
+  }
   if (m < n) {
     if (shared) {
       f = 1;  // shared critic: every policy updates every step (algos.hpp:382-384)
@@ -954,10 +966,11 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
                            cudaGraphConditionalHandle any_fire, int set_cond, int shared,
-                           int ncrit, cudaStream_t s, int* guard) {
+                           int ncrit, cudaStream_t s, int* guard, double* hist,
+                           const uint64_t* hist_base, int hist_slots) {
   launch_k(k_td3_step_begin, (n + 127) / 128, 128, 0, s, n, delay_acc, ratio, mask, fire, t_pol,
            t_c1, t_c2, steps, streams, seed, noise_key, policy_loss, any_fire, set_cond, shared,
-           ncrit, guard);
+           ncrit, guard, hist, hist_base, hist_slots);
 }
 
 // concat_features (pop_tensor.hpp:432-456) of the batch into the critic-input layouts

@@ -433,6 +433,28 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
     const pbrl_batch& b = batches[i];
     if (!b.s || !b.a || !b.r || !b.s2 || !b.done) PBRL_THROW(PBRL_E_USAGE, "null batch pointer");
   }
+  // every step's losses: a device history of kLossHist slots, read back one block at a time
+  const size_t row = static_cast<size_t>(3) * n;
+  if (losses_out) loss_hist.alloc(kLossHist * row);
+  auto hist_d2h = [&](uint32_t j, bool last) {  // once step j's losses are in the history
+    if (j % kLossHist != kLossHist - 1 && !last) return;
+    const uint32_t first = j - j % kLossHist;
+    CUDA_CHECK(cudaMemcpyAsync(losses_out + first * row, loss_hist.p,
+                               (j - first + 1) * row * sizeof(double), cudaMemcpyDeviceToHost,
+                               stream));
+  };
+  // TD3: k_td3_step_begin of step i+1 files step i's losses (keyed by steps[] - hist_base[]),
+  // so no copy launch sits between the step graphs
+  struct HistScope {
+    bool& on;
+    ~HistScope() { on = false; }
+  } hist_scope{hist_on};
+  hist_on = losses_out && algo == PBRL_ALGO_TD3;
+  if (hist_on) {
+    hist_base.alloc(n);
+    CUDA_CHECK(cudaMemcpyAsync(hist_base.p, steps.p, n * sizeof(uint64_t),
+                               cudaMemcpyDeviceToDevice, stream));
+  }
   if (!device_ptrs && !cstream) {
     CUDA_CHECK(cudaStreamCreateWithFlags(&cstream, cudaStreamNonBlocking));
     for (int sl = 0; sl < 2; ++sl) {
@@ -490,22 +512,21 @@ void Pop::update_batches(const pbrl_batch* batches, uint32_t k, uint64_t rows,
       CUDA_CHECK(cudaStreamWaitEvent(stream, ev_packed, 0));
     }
     step(B, d_mask);
-    if (losses_out) {
+    if (losses_out && !hist_on) {
       // this step's critic1 / critic2 / policy losses -> a device history slot; the history
-      // goes to the host in one copy per kLossHist steps (async, in stream order)
-      const size_t row = static_cast<size_t>(3) * n;
-      loss_hist.alloc(kLossHist * row);
-      // a kernel rather than a copy node, so the programmatic-dependent-launch chain from this
-      // step's graph into the next step's pack is not broken
+      // goes to the host in one copy per kLossHist steps (async, in stream order).  A kernel
+      // rather than a copy node, so the programmatic-dependent-launch chain is not broken.
       launch_copy_f64(loss_hist.p + (i % kLossHist) * row, losses.p, row, stream);
       count_launch(1);
-      if (i % kLossHist == kLossHist - 1 || i + 1 == k) {
-        const uint32_t first = i - i % kLossHist;
-        CUDA_CHECK(cudaMemcpyAsync(losses_out + first * row, loss_hist.p,
-                                   (i - first + 1) * row * sizeof(double),
-                                   cudaMemcpyDeviceToHost, stream));
-      }
+      hist_d2h(i, i + 1 == k);
+    } else if (hist_on && i >= 1) {
+      hist_d2h(i - 1, false);  // step i's begin has filed step i-1's losses
     }
+  }
+  if (hist_on) {  // the last step's losses (no next begin files them)
+    launch_copy_f64(loss_hist.p + ((k - 1) % kLossHist) * row, losses.p, row, stream);
+    count_launch(1);
+    hist_d2h(k - 1, true);
   }
   host_mask = nullptr;
   host_mask = nullptr;  // the caller's buffer is only valid during the call

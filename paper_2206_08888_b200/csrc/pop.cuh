@@ -207,7 +207,8 @@ void launch_td3_step_begin(int n, double* delay_acc, const double* ratio, const 
                            uint64_t* steps, const uint64_t* streams, uint64_t seed,
                            uint64_t* noise_key, double* policy_loss,
                            cudaGraphConditionalHandle any_fire, int set_cond, int shared,
-                           int ncrit, cudaStream_t s, int* guard = nullptr);
+                           int ncrit, cudaStream_t s, int* guard = nullptr, double* hist = nullptr,
+                           const uint64_t* hist_base = nullptr, int hist_slots = 0);
 // in_sa / in_s2a / sa_pi are activation buffers: fp32, or bf16 when act16
 void launch_pack_batch(int n, int B, int ds, int da, int lsa, const float* s, const float* a,
                        const float* r, const float* s2, const float* d, void* in_sa,

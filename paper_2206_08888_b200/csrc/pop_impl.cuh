@@ -133,6 +133,7 @@ struct StepGraph {
   size_t nodes = 0;       // kernel nodes outside conditional bodies
   size_t cond_nodes = 0;  // kernel nodes inside the policy-half conditional bodies
   bool stage_ev = false;  // records ev_stage_free once the step has read its packed batch
+  bool hist = false;      // k_td3_step_begin writes the loss history
 };
 
 struct Pop;
@@ -208,6 +209,10 @@ struct Pop {
   // kLossHist steps (one D2H per block instead of one per step)
   static constexpr uint32_t kLossHist = 64;
   DBuf<double> loss_hist;
+  // TD3: k_td3_step_begin of step i+1 copies step i's losses into the history (no copy launch
+  // between the step graphs); hist_base = steps[] at the start of the call
+  bool hist_on = false;
+  DBuf<uint64_t> hist_base;
   DBuf<float> log_alpha, alpha_m, alpha_v;
   DBuf<uint8_t> mask_buf;
 

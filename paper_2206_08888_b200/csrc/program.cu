@@ -905,7 +905,8 @@ void Pop::td3_step(int B, const uint8_t* d_mask) {
     launch_td3_step_begin(n, delay_acc.p, h_d0.p, d_mask, fire.p, t_pol.p, t_cri.p,
                           t_cri.p + ncrit, steps.p, streams.p, seed, key_a.p, losses.p + 2 * n,
                           any_fire, cond ? 1 : 0, shared ? 1 : 0, ncrit, stream,
-                          guarded ? guard_d : nullptr);
+                          guarded ? guard_d : nullptr, hist_on ? loss_hist.p : nullptr,
+                          hist_base.p, static_cast<int>(kLossHist));
   });
   // graph mode: the online critics' forward on [s | a] does not depend on the target chain, so
   // it runs on a parallel graph branch (its tiles fill the target chain's partial waves)
@@ -1304,7 +1305,8 @@ void Pop::step(int B, const uint8_t* d_mask) {
   } else {
     StepGraph* sg = nullptr;
     for (auto& g : graphs)
-      if (g.B == B && g.masked == (d_mask != nullptr) && g.dvd == dvd.on && g.fire == fg)
+      if (g.B == B && g.masked == (d_mask != nullptr) && g.dvd == dvd.on && g.fire == fg &&
+          g.hist == hist_on)
         sg = &g;
     if (!sg) {
       StepGraph g;
@@ -1312,6 +1314,7 @@ void Pop::step(int B, const uint8_t* d_mask) {
       g.masked = d_mask != nullptr;
       g.dvd = dvd.on;
       g.fire = fg;
+      g.hist = hist_on;
       cudaGraph_t graph;
       capturing = true;
       cap_fire = fg;
