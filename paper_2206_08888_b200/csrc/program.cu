@@ -838,6 +838,8 @@ bool Pop::td_target_fused(int B) const {
 // ------------------------------------------------------------------ TD3 step (algos.hpp:351-422)
 // Graph capture: append an IF node on `h` at the current capture point of `stream` and capture
 // body() into its body graph (on cap, a stream of its own).
+static size_t kernel_nodes(cudaGraph_t g);
+
 template <typename F>
 void Pop::capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body) {
   cudaStreamCaptureStatus st;
@@ -878,10 +880,24 @@ void Pop::capture_if(cudaGraphConditionalHandle h, cudaStream_t& cap, F&& body) 
   in_cond_body = false;
   std::swap(stream, cap);
   CUDA_CHECK(cudaStreamEndCapture(cap, &bg));
-  size_t nb = 0;
-  CUDA_CHECK(cudaGraphGetNodes(bg, nullptr, &nb));
-  cond_body_nodes += nb;
+  cond_body_nodes += kernel_nodes(bg);
   ++cond_nodes;
+}
+
+// kernel nodes of a captured graph (event-record nodes and the conditional nodes themselves are
+// not kernel launches)
+static size_t kernel_nodes(cudaGraph_t g) {
+  size_t nb = 0;
+  CUDA_CHECK(cudaGraphGetNodes(g, nullptr, &nb));
+  std::vector<cudaGraphNode_t> nodes(nb);
+  if (nb) CUDA_CHECK(cudaGraphGetNodes(g, nodes.data(), &nb));
+  size_t k = 0;
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    CUDA_CHECK(cudaGraphNodeGetType(nd, &t));
+    k += t == cudaGraphNodeTypeKernel ? 1 : 0;
+  }
+  return k;
 }
 
 void Pop::td3_step(int B, const uint8_t* d_mask) {
@@ -1347,10 +1363,8 @@ void Pop::step(int B, const uint8_t* d_mask) {
       cap_fire = false;
       g.stage_ev = ev_stage_free && stage_ev_captured;
       stage_ev_captured = false;
-      size_t nodes = 0;
-      CUDA_CHECK(cudaGraphGetNodes(graph, nullptr, &nodes));
-      // kernel nodes: the conditional nodes stand for their bodies (the policy half)
-      g.nodes = nodes - cond_nodes;
+      // kernel nodes; the conditional nodes stand for their bodies (the policy half)
+      g.nodes = kernel_nodes(graph);
       g.cond_nodes = cond_body_nodes;
       CUDA_CHECK(cudaGraphInstantiate(&g.exec, graph, 0));
       CUDA_CHECK(cudaGraphDestroy(graph));

@@ -212,6 +212,30 @@ def test_pack_overlap_device_batches_equal_single_steps(pb, ora, precision, n):
     assert np.array_equal(a.steps, b.steps) and np.array_equal(a.delay_acc, b.delay_acc)
 
 
+def test_graph_launch_count_equals_eager(pb, monkeypatch):
+    """The launch counter (bench.py's gpu_launches) counts the kernels a replayed step graph
+    runs -- not its event-record or conditional nodes -- so K graph-mode steps (fire and
+    non-fire graphs, packs beside the previous Adam) count what K eager steps launch."""
+    import torch
+    n, B, K = 8, 256, 6
+    hy = pb.Td3Hyper.defaults(n)
+    hy.policy_delay_ratio = [0.5] * n
+    gb = pb.make_synthetic_batches(K + 2, n, B, 17, 6, 41, device=torch.device("cuda", 0))
+    g = pb.make_td3_state(n, 17, 6, [256, 256], 1.0, 41, precision="bf16")
+    monkeypatch.setenv("PBRL_NO_GRAPH", "1")
+    e = pb.make_td3_state(n, 17, 6, [256, 256], 1.0, 41, precision="bf16")
+    monkeypatch.delenv("PBRL_NO_GRAPH")
+    counts = []
+    for st in (g, e):
+        for k in range(2):  # warm-up: the graphs are captured here
+            pb.td3_update_step(st, gb[k], hy)
+        before = st.launch_count()
+        it = iter(gb[2:])
+        pb.update_k_steps(st, lambda: next(it), K, hy)
+        counts.append(st.launch_count() - before)
+    assert counts[0] == counts[1], counts
+
+
 @pytest.mark.parametrize("precision", ["bf16", "ffma32"])
 def test_pack_overlap_sac_device_batches_equal_single_steps(pb, ora, precision):
     """The same for the SAC step graph (config C shape: 32 members, B = 256), whose policy
