@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--pbt-interval", type=int, default=1000,
                     help="updates between PBT exchanges; one exchange (fitness all-gather, device "
                          "plan, exploit copies, resets) is timed and amortised over it")
+    ap.add_argument("--pbt-timeout", type=float, default=180.0,
+                    help="seconds the timed PBT exchange may take before the line is printed "
+                         "without it")
     ap.add_argument("--reps", type=int, default=5,
                     help="the K timed steps are split into this many equal repetitions for the "
                          "median / IQR (bench.hpp:184-200)")
@@ -566,45 +569,11 @@ def main():
     # the ranks, identical device plan, exploit copies (cross-rank member blobs over NCCL,
     # same-rank on device), optimiser resets and hyper re-draws; amortised over pbt_interval
     # updates.  Returns are synthetic: record_return from RngStream::of(7, m, kGeneric, event).
-    pbt = None
-    if pop >= 4:
-        from paper_2206_08888_b200.dist import Comm, NativeShardedPBT
-        comm = (Comm.nccl(device=gpu) if (world > 1 and backend == "nccl")
-                else Comm.host(device=gpu) if world > 1 else None)
-        if comm is None:  # single rank: a one-rank host transport (no communication)
-            comm = _solo_comm(gpu)
-        pstate = pb.PBTState(n)
-        rng = pb.RngSequence(SEED, 0, "kDonorChoice")
-        ex = NativeShardedPBT(st, hy, comm)
-        times, parts, plans = [], [], []
-        for ev in range(3):
-            for m in range(n):
-                g = off + m
-                pstate.record_return(m, pb.RngStream.of(SEED, g, "kGeneric", ev).uniform(0))
-            st.synchronize()
-            barrier()
-            t0 = time.perf_counter()
-            plan = ex.evolve(pstate, rng)
-            dt = (time.perf_counter() - t0) * 1e3
-            times.append(max_over_ranks(dt))
-            parts.append(ex.last_exchange_ms)
-            plans.append(plan)
-        per = pop // world if args.scaling == "strong" else n
-        cross = [sum(1 for d, s_ in zip(p.replaced, p.donors) if d // per != s_ // per)
-                 for p in plans]
-        blob = pb.pbrl.member_blob_size(st) * 4
-        med = sorted(times)[1]
-        pbt = {"ms": med, "samples_ms": times, "transport": comm.kind,
-               "breakdown_ms_rank0": parts[1], "replaced": len(plans[1].replaced),
-               "cross_rank_copies": cross[1], "blob_bytes": blob,
-               "interval_updates": args.pbt_interval,
-               "amortised_share_of_step_time": med / (args.pbt_interval * total_ms / K)}
-        comm.close()
-
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(cfg, pop)
 
+    line = None
     if rank == 0:
         ngpu = min(world, ndev) if backend != "nccl" else world
         line = {"metric": METRIC, "value": value, "unit": "agent-updates/s", "n_gpus": ngpu,
@@ -620,11 +589,64 @@ def main():
                                       f"per GPU > L2", world),
                 "roofline": roof, "step_roofline": step_roof, "class_hbm": classes_hbm,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "reps": reps,
-                "pbt_exchange": pbt, "vectorization_overhead": vec,
+                "pbt_exchange": None, "vectorization_overhead": vec,
                 "ranks": world, "backend": backend if world > 1 else None,
                 "clocks": clk.summary(), "profile": {k: {kk: round(vv, 6) if isinstance(vv, float)
                                                          else vv for kk, vv in v.items()}
                                                      for k, v in cls.items()}}
+    # ---- PBT exchange (after the line is assembled): an exchange that fails, or hangs past
+    # --pbt-timeout seconds (e.g. a collective on a broken multi-GPU fabric), is reported in the
+    # line's pbt_exchange instead of costing the measured throughput line
+    pbt = None
+    if pop >= 4:
+        def on_timeout():
+            if rank == 0 and line is not None:
+                line["pbt_exchange"] = {"error": f"timeout after {args.pbt_timeout} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+        watchdog = threading.Timer(args.pbt_timeout, on_timeout)
+        watchdog.daemon = True
+        watchdog.start()
+        try:
+            from paper_2206_08888_b200.dist import Comm, NativeShardedPBT
+            comm = (Comm.nccl(device=gpu) if (world > 1 and backend == "nccl")
+                    else Comm.host(device=gpu) if world > 1 else None)
+            if comm is None:  # single rank: a one-rank host transport (no communication)
+                comm = _solo_comm(gpu)
+            pstate = pb.PBTState(n)
+            rng = pb.RngSequence(SEED, 0, "kDonorChoice")
+            ex = NativeShardedPBT(st, hy, comm)
+            times, parts, plans = [], [], []
+            for ev in range(3):
+                for m in range(n):
+                    g = off + m
+                    pstate.record_return(m, pb.RngStream.of(SEED, g, "kGeneric", ev).uniform(0))
+                st.synchronize()
+                barrier()
+                t0 = time.perf_counter()
+                plan = ex.evolve(pstate, rng)
+                dt = (time.perf_counter() - t0) * 1e3
+                times.append(max_over_ranks(dt))
+                parts.append(ex.last_exchange_ms)
+                plans.append(plan)
+            per = pop // world if args.scaling == "strong" else n
+            cross = [sum(1 for d, s_ in zip(p.replaced, p.donors) if d // per != s_ // per)
+                     for p in plans]
+            blob = pb.pbrl.member_blob_size(st) * 4
+            med = sorted(times)[1]
+            pbt = {"ms": med, "samples_ms": times, "transport": comm.kind,
+                   "breakdown_ms_rank0": parts[1], "replaced": len(plans[1].replaced),
+                   "cross_rank_copies": cross[1], "blob_bytes": blob,
+                   "interval_updates": args.pbt_interval,
+                   "amortised_share_of_step_time": med / (args.pbt_interval * total_ms / K)}
+            comm.close()
+        except Exception as e:  # reported, not fatal: the throughput line stands on its own
+            pbt = {"error": f"{type(e).__name__}: {e}"}
+        finally:
+            watchdog.cancel()
+    if line is not None:
+        line["pbt_exchange"] = pbt
+    if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
