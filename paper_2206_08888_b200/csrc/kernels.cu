@@ -41,9 +41,13 @@ __device__ __forceinline__ float simt_epilogue(const GemmArgs& g, float v, int g
       if (g.epi == EPI_BIAS_TANH_NOISE) {
         // algos.hpp:252-262: eps = clamp((T)normal * sd, +-clip); a = clamp(a + eps, +-bound)
         const uint64_t e = static_cast<uint64_t>(gi) * g.N + gj;
-        float eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) *
-                    g.noise_sd[mem];
-        eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+        float eps;
+        if (g.noise_eps) {  // the identical draw, precomputed (tensor-core modes)
+          eps = g.noise_eps[mem * g.ne_gs + static_cast<long long>(e)];
+        } else {
+          eps = static_cast<float>(rng_normal_pair(g.noise_key[mem], 2 * e)) * g.noise_sd[mem];
+          eps = clampf_ref(eps, -g.noise_clip[mem], g.noise_clip[mem]);
+        }
         v = clampf_ref(v + eps, -g.bound, g.bound);
       }
       break;
@@ -797,50 +801,76 @@ __global__ void __launch_bounds__(256) k_fwd_rowdot(const GemmArgs g) {
   const float* bias = g.bias.p ? g.bias.p + (g.bias.by_member ? mem : grp) * g.bias.gs : nullptr;
   const float* aux = g.aux.p ? g.aux.p + (g.aux.by_member ? mem : grp) * g.aux.gs : nullptr;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
-  for (int row = blockIdx.x * (blockDim.x >> 5) + warp; row < g.M; row += nwarps) {
-    const AT* xr = A + static_cast<long long>(row) * g.A.rs;
-    float acc[NMAX];
+  // two rows per warp trip (both rows' loads in flight, each W slice read from shared memory
+  // once for both); fast modes only, so the dot runs on FMA
+  auto load8 = [&](const AT* xr, int k0, float* x) {
+    if (sizeof(AT) == 2) {
+      const uint4 u = *reinterpret_cast<const uint4*>(xr + k0);
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-    for (int o = 0; o < NMAX; ++o) acc[o] = 0.0f;
-    for (int k0 = lane * 8; k0 < g.K; k0 += 256) {
-      float x[8];
-      if (sizeof(AT) == 2) {
-        const uint4 u = *reinterpret_cast<const uint4*>(xr + k0);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = __bfloat1622float2(h[j]);
-          x[2 * j] = f.x;
-          x[2 * j + 1] = f.y;
-        }
-      } else {
-        const float4 u0 = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xr) + k0);
-        const float4 u1 =
-            *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xr) + k0 + 4);
-        x[0] = u0.x; x[1] = u0.y; x[2] = u0.z; x[3] = u0.w;
-        x[4] = u1.x; x[5] = u1.y; x[6] = u1.z; x[7] = u1.w;
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        x[2 * j] = f.x;
+        x[2 * j + 1] = f.y;
       }
+    } else {
+      const float4 u0 = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xr) + k0);
+      const float4 u1 =
+          *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(xr) + k0 + 4);
+      x[0] = u0.x; x[1] = u0.y; x[2] = u0.z; x[3] = u0.w;
+      x[4] = u1.x; x[5] = u1.y; x[6] = u1.z; x[7] = u1.w;
+    }
+  };
+  for (int r0 = 2 * (blockIdx.x * (blockDim.x >> 5) + warp); r0 < g.M; r0 += 2 * nwarps) {
+    const bool two = r0 + 1 < g.M;
+    const AT* xa = A + static_cast<long long>(r0) * g.A.rs;
+    const AT* xb = two ? xa + g.A.rs : xa;
+    float acc[2][NMAX];
+#pragma unroll
+    for (int o = 0; o < NMAX; ++o) acc[0][o] = acc[1][o] = 0.0f;
+    for (int k0 = lane * 8; k0 < g.K; k0 += 256) {
+      float x[2][8];
+      load8(xa, k0, x[0]);
+      load8(xb, k0, x[1]);
 #pragma unroll
       for (int o = 0; o < NMAX; ++o) {
         if (NMAX > 1 && o >= g.N) break;
         const float4 w0 = *reinterpret_cast<const float4*>(Ws + o * g.K + k0);
         const float4 w1 = *reinterpret_cast<const float4*>(Ws + o * g.K + k0 + 4);
-        acc[o] = acc[o] + x[0] * w0.x + x[1] * w0.y + x[2] * w0.z + x[3] * w0.w + x[4] * w1.x +
-                 x[5] * w1.y + x[6] * w1.z + x[7] * w1.w;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          float t = acc[r][o];
+          t = __fmaf_rn(x[r][0], w0.x, t);
+          t = __fmaf_rn(x[r][1], w0.y, t);
+          t = __fmaf_rn(x[r][2], w0.z, t);
+          t = __fmaf_rn(x[r][3], w0.w, t);
+          t = __fmaf_rn(x[r][4], w1.x, t);
+          t = __fmaf_rn(x[r][5], w1.y, t);
+          t = __fmaf_rn(x[r][6], w1.z, t);
+          acc[r][o] = __fmaf_rn(x[r][7], w1.w, t);
+        }
       }
     }
 #pragma unroll
-    for (int o = 0; o < NMAX; ++o)
+    for (int o = 0; o < NMAX; ++o) {
+      if (NMAX > 1 && o >= g.N) break;
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], off);
-    if (lane < g.N) {
+      for (int off = 16; off > 0; off >>= 1) {
+        acc[0][o] += __shfl_xor_sync(0xffffffffu, acc[0][o], off);
+        acc[1][o] += __shfl_xor_sync(0xffffffffu, acc[1][o], off);
+      }
+    }
+    // lanes 0..N-1 finish row r0, lanes 16..16+N-1 row r0 + 1 (N <= 16)
+    const int r = lane >> 4, o_l = lane & 15;
+    if (o_l < g.N && (r == 0 || two)) {
       float v = 0.0f;
 #pragma unroll
       for (int o = 0; o < NMAX; ++o)
-        if (o == lane) v = acc[o];
-      v = simt_epilogue(g, v, row, lane, grp, mem, bias, aux);
-      if (g.c16) act_st(reinterpret_cast<__nv_bfloat16*>(g.C), cbase + row * g.c_rs + lane, v);
-      else g.C[cbase + row * g.c_rs + lane] = v;
+        if (o == o_l) v = acc[r][o];
+      const int row = r0 + r;
+      v = simt_epilogue(g, v, row, o_l, grp, mem, bias, aux);
+      if (g.c16) act_st(reinterpret_cast<__nv_bfloat16*>(g.C), cbase + row * g.c_rs + o_l, v);
+      else g.C[cbase + row * g.c_rs + o_l] = v;
     }
   }
 }

@@ -140,6 +140,9 @@ struct GemmArgs {
   const uint64_t* noise_key = nullptr;
   const float* noise_sd = nullptr;
   const float* noise_clip = nullptr;
+  // tensor-core modes: the same draws precomputed by k_td3_target_noise, [member][M][N]
+  const float* noise_eps = nullptr;
+  long long ne_gs = 0;
   float bound = 1.0f;
 };
 

@@ -76,7 +76,6 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
       a.mo_ld = ymask->mld;
     }
     a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
-  a.max_ctas = cta_cap;
     a.max_ctas = cta_cap;
     timed(PC_GEMM_FWD, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, true, a, stream); });
@@ -111,6 +110,10 @@ void Pop::gemm_fwd(const NetShape& sh, const float* W, int l, int groups, int B,
     g.noise_sd = h_f2.p;
     g.noise_clip = h_f3.p;
     g.bound = bound;
+    if (use_tc() && algo == PBRL_ALGO_TD3 && out == da) {  // precomputed by launch_td3_target_noise
+      g.noise_eps = S.tnoise.p;
+      g.ne_gs = static_cast<long long>(B) * da;
+    }
   }
   timed(PC_GEMM_FWD, flops, bytes, active != nullptr, [&] {
     if (out <= 16) launch_fwd_skinny(g, stream);
@@ -171,7 +174,6 @@ void Pop::gemm_dx(const NetShape& sh, const float* W, int l, int groups, int B, 
     a.scale = scale;
     a.active = active;
     a.b_prefetch = tc_prefetch_ok() ? 1 : 0;
-  a.max_ctas = cta_cap;
     a.max_ctas = cta_cap;
     timed(PC_GEMM_DX, flops, bytes, active != nullptr,
           [&] { launch_tc_gemm(A, Bw, false, false, a, stream); });
