@@ -555,7 +555,8 @@ template <int NO> __host__ __device__ constexpr int ov_slices() {
   return NO == 1 ? PBRL_OBV_SL1 : PBRL_OBV_SLN;
 }
 template <int NO, typename AT, int CW>
-__global__ void __launch_bounds__(kOvQuads* ov_slices<NO>(), NO == 1 ? PBRL_OBV_MINB1 : PBRL_OBV_MINBN)
+__global__ void __launch_bounds__(kOvQuads* ov_slices<NO>(),
+                                  NO == 1 ? PBRL_OBV_MINB1 : PBRL_OBV_MINBN)
     k_out_backward_v(OutBwdArgs a) {
   PDL_ENTRY();
   extern __shared__ float sm[];

@@ -193,8 +193,8 @@ def test_pack_overlap_device_batches_equal_single_steps(pb, ora, precision, n):
     """Inside one update call the pack of batch i+1 runs on its own stream beside step i's last
     Adam (after the step graph's ev_stage_free record node).  K device batches in one call at the
     config-D shape (80 members, B = 256, both step graphs, policy delays mixed so some steps fire
-    for a few members only, some for none) leave the same state, bit for bit, as K single-step calls, whose packs
-    run in member-stream order."""
+    for a few members only, some for none) leave the same state, bit for bit, as K single-step
+    calls, whose packs run in member-stream order."""
     import torch
     B, K = 256, 12
     hidden = [256, 256] if precision == "bf16" else [64, 64]
