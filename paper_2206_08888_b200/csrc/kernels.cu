@@ -9,9 +9,10 @@
 namespace pbrl {
 
 int carveout_pref() {
-  // measured on B200 (TD3 pop 80, BF16): driver default 233.9k, 100% 227.5k, 0% 222.7k,
-  // 25-60% ~237k agent-updates/s
-  static const int c = std::getenv("PBRL_CARVEOUT") ? std::atoi(std::getenv("PBRL_CARVEOUT")) : 50;
+  // measured on B200 (TD3 pop 80, BF16): round 1 driver default 233.9k, 100% 227.5k, 0% 222.7k,
+  // 25-60% ~237k agent-updates/s; end of round 2: 0% 315.9k, 10% 328.2k, 18-25% 333.4k,
+  // 33% 332.0k, 50% 330.0k, 75% 321.7k, driver default 312.2k
+  static const int c = std::getenv("PBRL_CARVEOUT") ? std::atoi(std::getenv("PBRL_CARVEOUT")) : 25;
   return c;
 }
 
